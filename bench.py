@@ -1,0 +1,360 @@
+"""Benchmark of the B200 rank-structured Cholesky hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 1]
+
+Default workload: BASELINE config[1] -- 512 independent supernodes (256x256 SPD
+diagonal, 2048x256 rank-48+noise off-diagonal): POTRF + TRSM + Gaussian sketch
+(r=58, q=1) + pivoted-QR compression, i.e. the reference composition
+dense_cholesky -> tri_solve -> low_rank_approx per block.  A step is one pass over
+the whole batch.  value = aggregate factor GFLOP/s (algorithmic FLOPs of SURVEY
+§8(d) / device time), inputs resident in HBM; e2e = the same through the host
+API (H2D of inputs, host PCG64 sketches, D2H of the factor).
+
+Multi-GPU: one process per GPU (torchrun), each rank factors its own batch of
+512 supernodes (the config shards by independent supernodes; no collective on the
+data path) -> scaling "weak"; time = max over ranks of the device-timed region.
+"""
+
+import argparse
+import concurrent.futures as cf
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factor+PCG time to rel-res 1e-6 (s); factor GFLOP/s as % of FP64 TC peak"
+FP64_DATASHEET_TFLOPS = 40.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--nb", type=int, default=512)
+    p.add_argument("--cpu-sample", type=int, default=48, help="blocks in the CPU baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peak_tflops(torch):
+    """Measured FP64 ceiling on this GPU: cuBLAS DGEMM (torch float64 matmul), best of 5."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    c = a @ b
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b, out=c)
+        e.record()
+        e.synchronize()
+        best = max(best, 2.0 * n**3 / (s.elapsed_time(e) * 1e-3) / 1e12)
+    del a, b, c
+    return best
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+# ---------------------------------------------------------------------------
+# config[1]
+
+
+def cfg1_inputs(nb):
+    from paper_1507_05593_b200.problems import batched_supernodes
+
+    return batched_supernodes(nb=nb)
+
+
+def cpu_cfg1(D, B, sample, threads):
+    """Oracle port of the reference composition on `sample` blocks, `threads` host
+    threads (one BLAS thread each).  Returns (GFLOP/s, seconds, flops)."""
+    try:
+        import threadpoolctl
+
+        limiter = threadpoolctl.threadpool_limits(limits=1)
+    except Exception:
+        limiter = None
+    from oracle import kernels as ok
+    from paper_1507_05593_b200.batched import model_flops
+
+    def one(i):
+        ok.cfg1_block(D[i], B[i], 58, 1, ok.block_seed(0, 0, i))
+
+    t0 = time.perf_counter()
+    if threads > 1:
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(sample)))
+    else:
+        for i in range(sample):
+            one(i)
+    dt = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    fl = model_flops(sample, 256, 2048, 58, 1)
+    return fl / dt / 1e9, dt, fl
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    nb = min(args.nb, args.cpu_sample)
+    D, B = cfg1_inputs(nb)
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_cfg1(D, B, nb, threads)
+    t_all = 0.0
+    for _ in range(args.steps):
+        g, dt, _ = cpu_cfg1(D, B, nb, threads)
+        vals.append(g)
+        t_all += dt
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator of BASELINE config[1])",
+        "config": {"workload": "config[1] batched supernode factor+compress", "blocks_per_step": nb,
+                   "n": 256, "m": 2048, "sketch_rank": 58, "power_iters": 1},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"{nb} of 512 config[1] blocks per step, oracle/kernels.cfg1_block "
+                                   f"(scipy LAPACK, 1 BLAS thread per worker)"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200_cfg1(args, rank, world, torch, dist):
+    from paper_1507_05593_b200 import _lib
+    from paper_1507_05593_b200 import engine as E
+    from paper_1507_05593_b200.batched import BatchedSupernodes, make_sketches, model_flops
+
+    lib = _lib.load()
+    nb, n, m, r, q = args.nb, 256, 2048, 58, 1
+    D, B = cfg1_inputs(nb)
+    bs = BatchedSupernodes(nb, n, m, r, q=q, chunk=32)
+    D0 = torch.from_numpy(D).cuda()
+    B0 = torch.from_numpy(B).cuda()
+    Om = make_sketches(nb, m, r, master=0, threads=os.cpu_count() or 1)
+    bs.Om.copy_(torch.from_numpy(Om))
+
+    def step():
+        bs.D.copy_(D0)
+        bs.B.copy_(B0)
+        bs.run()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    bs.check_info()
+    ranks = bs.rank.cpu().numpy()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        lib.rsc_launch_counter(1)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+        launches = int(lib.rsc_launch_counter(1))
+        barrier()
+    t = ev0.elapsed_time(ev1) * 1e-3
+    if dist is not None:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    flops = model_flops(nb, n, m, r, q)
+    value = world * flops * args.steps / t / 1e9
+
+    # roofline of the dominant kernel (the DMMA GEMM of the sketch products), timed
+    # live on the launching stream with CUDA events
+    LO, G, H, Omd = bs.B, bs.G, bs.H, bs.Om
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    reps = 3
+    evs[0].record()
+    for _ in range(reps):
+        E.gemm_strided_batched(LO, Omd, G, transA=True)
+        E.gemm_strided_batched(LO, G, H)
+    evs[1].record()
+    torch.cuda.synchronize()
+    gemm_t = evs[0].elapsed_time(evs[1]) * 1e-3 / (2 * reps)
+    gemm_flops = 2.0 * nb * m * n * r
+    peak = fp64_peak_tflops(torch)
+
+    # end to end through the host API
+    e2e = None
+    if rank == 0 or True:
+        st = bs.pinned_staging()
+        Dh, Bh = D, B
+        bs.factor_compress_host(Dh, Bh, pinned=st)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            bs.factor_compress_host(Dh, Bh, pinned=st)
+        te = (time.perf_counter() - t0) / args.steps
+        if dist is not None:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * flops / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": bs.h2d_bytes(),
+               "d2h_bytes_per_step": bs.d2h_bytes(), "seconds_per_step": te}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sample = min(args.cpu_sample, nb)
+        threads = os.cpu_count() or 1
+        g, dt, _ = cpu_cfg1(D, B, sample, threads)
+        cpu = {"value": g, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+               "sample": f"{sample} of {nb} config[1] blocks ({dt:.1f} s wall), oracle/kernels.cfg1_block, "
+                         f"1 BLAS thread per worker"}
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator of BASELINE config[1]; reference PCG64 sketches)",
+        "config": {"workload": "config[1] batched supernode factor+compress", "blocks_per_gpu": nb, "n": 256,
+                   "m": 2048, "true_rank": 48, "sketch_rank": r, "power_iters": q,
+                   "factor_seconds_per_step": t / args.steps,
+                   "fp64_tc_frac_of_step": value / world / 1e3 / peak,
+                   "kept_ranks": sorted(set(int(x) for x in ranks)),
+                   "l2": "inputs larger than L2 (2.4 GB/step); step re-copies D,B from a pristine device copy "
+                         "(in-place kernels)"},
+        "roofline": {"bound": "tensor", "achieved": gemm_flops / gemm_t / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": gemm_flops / gemm_t / 1e12 / peak, "traffic": None,
+                     "kernel": "gemm_grouped_kernel (sketch products L_O^T Omega, L_O G)",
+                     "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64 "
+                                    f"entry); datasheet {FP64_DATASHEET_TFLOPS} TF"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if args.config == 1:
+            run_b200_cfg1(args, rank, world, torch, dist)
+        else:
+            from paper_1507_05593_b200.benchsparse import run_sparse
+
+            run_sparse(args, rank, world, torch, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,151 @@
+/*
+ * rsc_b200.h -- C ABI of librsc_b200.so, the B200 (sm_100a) numeric engine of the
+ * rank-structured supernodal Cholesky preconditioner (Chadwick & Bindel,
+ * arXiv 1507.05593).
+ *
+ * Conventions (all entry points):
+ *   - every matrix is FP64, ROW-MAJOR, addressed as X[i*ld + j];
+ *   - pointers named *_dev are device pointers, everything else lives on the host;
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered and
+ *     asynchronous, the library keeps no global state and allocates nothing
+ *     persistent (caller-owned workspaces only);
+ *   - return value: 0 ok, <0 bad argument (index of the offending argument, negated),
+ *     >0 CUDA error code from the launch.  Numerical failures (a non-positive
+ *     Cholesky pivot) are reported through per-matrix device `info` words with the
+ *     LAPACK convention (1-based failing column, 0 = success), which the host turns
+ *     into IndefiniteError(info-1) exactly like rschol.kernels.dense_cholesky
+ *     (reference pkg/src/rschol/kernels.py:34-38).
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/rschol/).
+ */
+#ifndef RSC_B200_H
+#define RSC_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One GEMM problem (possibly a strided batch) of a grouped launch:
+ *   C[b] (+)= alpha * op(A[b]) @ op(B[b]) + beta * C[b]      for b < batch
+ * op(A) is M x K (A stored M x K, or K x M when transA), op(B) is K x N.
+ * Optional index maps (device int32 arrays, NULL = identity):
+ *   b_rows : row k of op(B) is read from B row b_rows[k]        (transB == 0 only)
+ *   c_rows : row m of the result goes to C row c_rows[m]
+ *   c_cols : column n of the result goes to C column c_cols[n]
+ * atomic != 0: C += alpha*op(A)op(B) with FP64 atomics (beta ignored) so that
+ * several problems of one launch may scatter into the same target block. */
+typedef struct {
+    const double *A;
+    const double *B;
+    double *C;
+    long long strideA, strideB, strideC;
+    const int *b_rows;
+    const int *c_rows;
+    const int *c_cols;
+    int M, N, K;
+    int lda, ldb, ldc;
+    int batch;
+    int atomic;
+    double alpha, beta;
+} rsc_gemm_problem;
+
+/* Grouped FP64 tensor-core (DMMA) GEMM.  Replaces every numpy `@` on the
+ * factorization path: factor.py:383-398 (_assemble_schur), factor.py:444-455 and
+ * 471-483 (off_diagonal_multiply[_trans]), diagblocks.py:220-262 (windowed source
+ * products), blocks.py:35-39 (LowRankBlock.matmat/rmatmat), kernels.py:107-112. */
+int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *problems,
+                     int count, void *stream);
+
+/* Batched in-place lower Cholesky of `count` matrices (sizes may differ).
+ * A[i] (n[i] x n[i], ld lda[i]) : lower triangle read, overwritten by L with the
+ * strict upper triangle zeroed (dpotrf lower + clean).  Dinv[i] (n[i] x 64, ld 64)
+ * receives the inverses of L's 64x64 diagonal blocks, used by rsc_trsm_batched.
+ * info_dev[i] = 0 or the 1-based column of the first non-positive pivot.
+ * Replaces kernels.py:22-39 dense_cholesky (called at factor.py:614,
+ * diagblocks.py:300, interior.py:140). */
+int rsc_potrf_batched(int count, double *const *A, const int *n, const int *lda,
+                      double *const *Dinv, int *info_dev, void *stream);
+
+/* Batched triangular solve with lower factors produced by rsc_potrf_batched.
+ *   side = 0 (left):  B (n x cols)  <- L^{-1} B       (trans = 0)
+ *                                   <- L^{-T} B       (trans = 1)
+ *   side = 1 (right): B (rows x n)  <- B L^{-T}       (trans = 1 only)
+ * `m[i]` is the number of right-hand-side columns (left) or rows (right).
+ * Replaces kernels.py:42-64 tri_solve (factor.py:414,633; interior.py:60,74,141;
+ * diagblocks.py:178). */
+int rsc_trsm_batched(int side, int trans, int count, const double *const *L,
+                     const int *n, const int *ldl, const double *const *Dinv,
+                     double *const *B, const int *m, const int *ldb, void *stream);
+
+/* Inverses of the 64x64 diagonal blocks of caller-supplied lower triangles
+ * (Dinv[i]: n[i] x 64, ld 64), so rsc_trsm_batched can solve with them. */
+int rsc_trtri_diag_batched(int count, const double *const *L, const int *n,
+                           const int *ldl, double *const *Dinv, void *stream);
+
+/* Batched column-pivoted Householder QR with the reference rank cutoff.
+ * G[i] (m[i] x k[i], ld ldg[i]) is destroyed.  rank_dev[i] receives
+ * #{ |R_jj| > max(m,k) * eps * |R_00| } (eps = 2^-52), and Q[i] (m[i] x k[i],
+ * ld ldq[i]) receives the first rank_dev[i] columns of the orthonormal factor
+ * (remaining columns unspecified).  Pivot selection, Householder vectors and the
+ * partial-norm downdating follow LAPACK dgeqp3/dlaqp2 + dorg2r, which is what
+ * scipy.linalg.qr(pivoting=True) runs.  work_dev: caller workspace of at least
+ * rsc_qrcp_workspace_bytes(count, m, k) bytes.
+ * Replaces kernels.py:67-82 orthonormalize. */
+long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k);
+int rsc_qrcp_batched(int count, double *const *G, const int *m, const int *k,
+                     const int *ldg, double *const *Q, const int *ldq, int *rank_dev,
+                     void *work_dev, void *stream);
+
+/* Batched symmetric scatter of CSR blocks into dense row-major blocks:
+ *   D[i][r, c] = values[p]  for the CSR block i (rows r < nrows[i]).
+ * Used to materialize A(C_j, C_j), A(R_j, C_j) (factor.py:378-379,
+ * diagblocks.py:294).  D must be zeroed by the caller. */
+int rsc_csr_to_dense_batched(int count, const int *const *rowptr,
+                             const int *const *colidx, const double *const *values,
+                             const int *nrows, double *const *D, const int *ldd,
+                             void *stream);
+
+/* Y (nrows x r) = alpha * S @ X + beta * Y for a CSR block S (nrows x ncols)
+ * and dense row-major X (ncols x r).  Replaces the scipy sparse block products
+ * factor.py:444 and 471 (A(R_j,C_j) @ G1, A(R_j,C_j)^T @ G), interior.py:92-95. */
+int rsc_spmm_csr(int nrows, int r, const int *rowptr_dev, const int *colidx_dev,
+                 const double *values_dev, const double *X_dev, int ldx,
+                 double alpha, double beta, double *Y_dev, int ldy, void *stream);
+
+/* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */
+int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,
+                 const double *values_dev, const double *x_dev, double *y_dev,
+                 void *stream);
+
+/* Gather / scatter of rows: dst[i, :] = src[idx[i], :]  (gather)
+ *                           dst[idx[i], :] += alpha*src[i, :]  (scatter_add) */
+int rsc_gather_rows(int nrows, int ncols, const int *idx_dev, const double *src_dev,
+                    int lds, double *dst_dev, int ldd, void *stream);
+int rsc_scatter_add_rows(int nrows, int ncols, const int *idx_dev, double alpha,
+                         const double *src_dev, int lds, double *dst_dev, int ldd,
+                         void *stream);
+
+/* PCG vector kernels (pcg.py:104-128).  dot: out_dev[0] = x.y (deterministic
+ * two-pass tree reduction).  axpy: y += alpha_dev[0]*scale * x.  xpby:
+ * p = z + (num/den) * p with num/den read from device scalars. */
+int rsc_dot(int n, const double *x_dev, const double *y_dev, double *out_dev,
+            double *work_dev, void *stream);
+int rsc_pcg_update_xr(int n, const double *rz_dev, const double *pap_dev,
+                      double *x_dev, double *r_dev, const double *p_dev,
+                      const double *ap_dev, void *stream);
+int rsc_pcg_update_p(int n, const double *rznew_dev, const double *rz_dev,
+                     const double *z_dev, double *p_dev, void *stream);
+
+/* Number of kernels this process launched through the library (reset != 0
+ * returns the count and zeroes it).  Diagnostic only. */
+long long rsc_launch_counter(int reset);
+
+/* Library self-description, for load checks. */
+const char *rsc_version(void);
+int rsc_device_arch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSC_B200_H */

@@ -1,0 +1,116 @@
+"""ctypes binding of librsc_b200.so (the C ABI declared in include/rsc_b200.h).
+
+The product path has no CPU fallback: importing a compute entry point without the
+built library, or calling it without a CUDA device, raises immediately.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsc_b200.so")
+
+# numpy mirror of rsc_gemm_problem (include/rsc_b200.h); 120 bytes, naturally aligned
+GEMM_DTYPE = np.dtype(
+    [
+        ("A", "u8"), ("B", "u8"), ("C", "u8"),
+        ("sA", "i8"), ("sB", "i8"), ("sC", "i8"),
+        ("b_rows", "u8"), ("c_rows", "u8"), ("c_cols", "u8"),
+        ("M", "i4"), ("N", "i4"), ("K", "i4"),
+        ("lda", "i4"), ("ldb", "i4"), ("ldc", "i4"),
+        ("batch", "i4"), ("atomic", "i4"),
+        ("alpha", "f8"), ("beta", "f8"),
+    ]
+)
+assert GEMM_DTYPE.itemsize == 120
+
+# every symbol include/rsc_b200.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "rsc_gemm_grouped",
+    "rsc_potrf_batched",
+    "rsc_trsm_batched",
+    "rsc_trtri_diag_batched",
+    "rsc_qrcp_workspace_bytes",
+    "rsc_qrcp_batched",
+    "rsc_csr_to_dense_batched",
+    "rsc_spmm_csr",
+    "rsc_spmv_csr",
+    "rsc_gather_rows",
+    "rsc_scatter_add_rows",
+    "rsc_dot",
+    "rsc_pcg_update_xr",
+    "rsc_pcg_update_p",
+    "rsc_launch_counter",
+    "rsc_version",
+    "rsc_device_arch",
+)
+
+_lib = None
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+D = ctypes.c_double
+LL = ctypes.c_longlong
+
+_SIGS = {
+    "rsc_gemm_grouped": (I, [I, I, P, I, P]),
+    "rsc_potrf_batched": (I, [I, P, P, P, P, P, P]),
+    "rsc_trsm_batched": (I, [I, I, I, P, P, P, P, P, P, P, P]),
+    "rsc_trtri_diag_batched": (I, [I, P, P, P, P, P]),
+    "rsc_qrcp_workspace_bytes": (LL, [I, P, P]),
+    "rsc_qrcp_batched": (I, [I, P, P, P, P, P, P, P, P, P]),
+    "rsc_csr_to_dense_batched": (I, [I, P, P, P, P, P, P, P]),
+    "rsc_spmm_csr": (I, [I, I, P, P, P, P, I, D, D, P, I, P]),
+    "rsc_spmv_csr": (I, [I, P, P, P, P, P, P]),
+    "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
+    "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),
+    "rsc_dot": (I, [I, P, P, P, P, P]),
+    "rsc_pcg_update_xr": (I, [I, P, P, P, P, P, P, P]),
+    "rsc_pcg_update_p": (I, [I, P, P, P, P, P]),
+    "rsc_launch_counter": (LL, [I]),
+    "rsc_version": (ctypes.c_char_p, []),
+    "rsc_device_arch": (I, []),
+}
+
+
+class NativeLibraryMissing(RuntimeError):
+    """librsc_b200.so is not built (run __graft_entry__.build())."""
+
+
+def load():
+    """Load (once) and return the native library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} not found; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed with status {rc}")
+
+
+def ptr_array(ptrs):
+    """Host array of device pointers (uint64) for the batched entry points."""
+    return np.ascontiguousarray(np.asarray(ptrs, dtype=np.uint64))
+
+
+def int_array(vals):
+    return np.ascontiguousarray(np.asarray(vals, dtype=np.int32))
+
+
+def addr(a):
+    """ctypes address of a host numpy array (or None)."""
+    return None if a is None else a.ctypes.data

@@ -1,0 +1,156 @@
+"""Level-batched supernode factor + compression (the config[1] kernel pipeline).
+
+For a batch of independent supernodes (diagonal block D_i, off-diagonal block B_i)
+this runs, entirely on the device and batched across supernodes:
+
+    L_D = chol(D)                       rsc_potrf_batched      (factor.py:614)
+    L_O = B L_D^{-T}                    rsc_trsm_batched        (factor.py:414,633)
+    G   = L_O^T Omega                   grouped DMMA GEMM       (kernels.py:107)
+    q x { H = L_O G ; G = L_O^T H }     grouped DMMA GEMM       (kernels.py:108-110)
+    U   = orth(G)  (pivoted QR+cutoff)  rsc_qrcp_batched        (kernels.py:111)
+    V   = L_O U                         grouped DMMA GEMM       (kernels.py:112)
+
+which is the reference composition dense_cholesky -> tri_solve -> low_rank_approx
+for every block.  Omega_i are the reference's own PCG64 sketches
+(seed `_block_seed(seed, 0, i)`), generated on host threads and uploaded unchanged.
+
+To keep each block's 2048x256 L_O resident in the 126 MB L2 across the five
+stages, the batch is processed in chunks (`chunk` supernodes at a time).
+"""
+
+import concurrent.futures as cf
+import math
+
+import numpy as np
+import torch
+
+from . import engine as E
+from .errors import IndefiniteError
+
+FLOPS_NOTE = "POTRF n^3/3 + TRSM m n^2 + (2+2q) GEMMs 2 m n r + QRCP 4 n r^2"
+
+
+def block_seed(master, *tags):
+    """Seed of one sketch: SeedSequence((master,)+tags) -> first uint64 word
+    (reference factor.py:324-326)."""
+    ss = np.random.SeedSequence((int(master),) + tuple(int(t) for t in tags))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+def sketch(m, r, seed):
+    return np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r))
+
+
+def make_sketches(nb, m, r, master=0, threads=8, out=None):
+    """Host PCG64 sketches for blocks 0..nb-1 (numpy releases the GIL while filling,
+    so a thread pool scales across blocks)."""
+    if out is None:
+        out = np.empty((nb, m, r))
+    seeds = [block_seed(master, 0, i) for i in range(nb)]
+
+    def fill(i):
+        out[i] = sketch(m, r, seeds[i])
+
+    if threads <= 1:
+        for i in range(nb):
+            fill(i)
+    else:
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(fill, range(nb)))
+    return out
+
+
+def model_flops(nb, n, m, r, q):
+    """Algorithmic FLOPs of the reference composition (SURVEY §8(d) work model)."""
+    per = n**3 / 3 + m * n * n + (2 + 2 * q) * 2.0 * m * n * r + 4.0 * n * r * r
+    return nb * per
+
+
+class BatchedSupernodes:
+    """Device workspace for a batch of `nb` supernodes of shape (n, m) with sketch width r."""
+
+    def __init__(self, nb, n, m, r, q=1, chunk=32):
+        self.nb, self.n, self.m, self.r, self.q = nb, n, m, r, q
+        self.chunk = max(1, min(chunk, nb))
+        self.D = E.empty(nb, n, n)
+        self.B = E.empty(nb, m, n)
+        self.Om = E.empty(nb, m, r)
+        self.Dinv = E.empty(nb, n, 64)
+        self.G = E.empty(nb, n, r)
+        self.H = E.empty(nb, m, r)
+        self.U = E.empty(nb, n, r)
+        self.V = E.empty(nb, m, r)
+        self.info = E.zeros(nb, dtype=E.I32)
+        self.rank = E.zeros(nb, dtype=E.I32)
+        self._qr_work = None
+
+    def run(self):
+        """Factor + compress every block (inputs already in self.D / self.B / self.Om)."""
+        n, m, r, q = self.n, self.m, self.r, self.q
+        for c0 in range(0, self.nb, self.chunk):
+            c1 = min(self.nb, c0 + self.chunk)
+            cnt = c1 - c0
+            idx = range(c0, c1)
+            Dp = [self.D[i].data_ptr() for i in idx]
+            Ip = [self.Dinv[i].data_ptr() for i in idx]
+            E.potrf_batched(Dp, [n] * cnt, [n] * cnt, Ip, self.info[c0:c1])
+            Bp = [self.B[i].data_ptr() for i in idx]
+            E.trsm_batched("right", 1, Dp, [n] * cnt, [n] * cnt, Ip, Bp, [m] * cnt, [n] * cnt)
+            LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
+            E.gemm_strided_batched(LO, Om, G, transA=True)
+            for _ in range(q):
+                E.gemm_strided_batched(LO, G, H)
+                E.gemm_strided_batched(LO, H, G, transA=True)
+            self._qr_work = E.qrcp_batched([self.G[i].data_ptr() for i in idx], [n] * cnt, [r] * cnt,
+                                           [r] * cnt, [self.U[i].data_ptr() for i in idx], [r] * cnt,
+                                           self.rank[c0:c1])
+            E.gemm_strided_batched(LO, self.U[c0:c1], self.V[c0:c1])
+
+    def check_info(self):
+        info = self.info.cpu().numpy()
+        bad = np.nonzero(info)[0]
+        if bad.size:
+            raise IndefiniteError(int(info[bad[0]]) - 1, f"block {int(bad[0])}: pivot {int(info[bad[0]]) - 1}")
+
+    def factor_compress_host(self, D, B, master=0, threads=8, pinned=None):
+        """Public host-buffer entry point: H2D of D/B (pinned staging), host PCG64
+        sketches generated on `threads` threads while the copies fly, the batched
+        pipeline, then D2H of (L_D, V, U, ranks).  Returns host arrays."""
+        if pinned is None:
+            pinned = self.pinned_staging()
+        st = pinned
+        np.copyto(st["D"].numpy(), D)
+        np.copyto(st["B"].numpy(), B)
+        self.D.copy_(st["D"], non_blocking=True)
+        self.B.copy_(st["B"], non_blocking=True)
+        make_sketches(self.nb, self.m, self.r, master=master, threads=threads, out=st["Om"].numpy())
+        self.Om.copy_(st["Om"], non_blocking=True)
+        self.run()
+        st["LD"].copy_(self.D, non_blocking=True)
+        st["V"].copy_(self.V, non_blocking=True)
+        st["U"].copy_(self.U, non_blocking=True)
+        st["rank"].copy_(self.rank, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self.check_info()
+        return st["LD"].numpy(), st["V"].numpy(), st["U"].numpy(), st["rank"].numpy()
+
+    def pinned_staging(self):
+        nb, n, m, r = self.nb, self.n, self.m, self.r
+
+        def pin(*shape, dtype=torch.float64):
+            return torch.empty(*shape, dtype=dtype, pin_memory=True)
+
+        return {"D": pin(nb, n, n), "B": pin(nb, m, n), "Om": pin(nb, m, r), "LD": pin(nb, n, n),
+                "V": pin(nb, m, r), "U": pin(nb, n, r), "rank": pin(nb, dtype=torch.int32)}
+
+    def h2d_bytes(self):
+        return 8 * self.nb * (self.n * self.n + self.m * self.n + self.m * self.r)
+
+    def d2h_bytes(self):
+        return 8 * self.nb * (self.n * self.n + self.m * self.r + self.n * self.r) + 4 * self.nb
+
+    def results(self, i):
+        """Host copies (L_D, L_O, V, U) of block i, ranks applied."""
+        k = int(self.rank[i].item())
+        return (self.D[i].cpu().numpy(), self.B[i].cpu().numpy(), self.V[i, :, :k].cpu().numpy(),
+                self.U[i, :, :k].cpu().numpy())

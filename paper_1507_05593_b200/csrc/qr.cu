@@ -1,0 +1,274 @@
+// Batched column-pivoted Householder QR (LAPACK dgeqp3/dlaqp2 semantics) with the
+// reference rank cutoff and explicit Q (dorg2r) for the kept columns.
+//
+// Reference: kernels.py:67-82 orthonormalize ->
+//   Q, R, _ = scipy.linalg.qr(G, mode="economic", pivoting=True)
+//   rank = #{ |R_ii| > max(m,k) * eps * |R_00| };  return Q[:, :rank]
+// The kept count is decided by |R_ii| sitting as close as 1% to the cutoff, so the
+// pivot rule (first index of the largest partial norm), the Householder convention
+// (dlarfg: beta = -sign(alpha) * ||x||) and the partial-norm downdating with the
+// sqrt(eps) recomputation threshold (dlaqp2) are reproduced, in FP64 throughout.
+// Q[:, :rank] only depends on the first `rank` reflectors (H_i e_j = e_j for i > j),
+// so dorg2r is run on those only.
+//
+// One CTA per matrix.  The sketch is transposed into a column-major tile so every
+// Householder step is warp-per-column with coalesced, conflict-free access; the tile
+// lives in shared memory when it fits (cfg1: 256 x 58) and otherwise in a global
+// (L2-resident) workspace.
+#include <vector>
+#include "common.cuh"
+
+namespace {
+
+constexpr int QR_THREADS = 512;
+constexpr int QR_MAXK = 1024;
+constexpr int MAXB = 160;
+constexpr double EPS = 2.220446049250313e-16;        // np.finfo(float64).eps
+constexpr double TOL3Z = 1.0536712127723509e-08;     // sqrt(dlamch('E')) = sqrt(2^-53)
+
+struct QrArgs {
+    int count;
+    double *G[MAXB];
+    double *Q[MAXB];
+    long long woff[MAXB];
+    int m[MAXB], k[MAXB], ldg[MAXB], ldq[MAXB];
+    int base;
+};
+
+__device__ __forceinline__ double col_norm2(const double *c, int r0, int m, int lane) {
+    double s = 0.0;
+    for (int r = r0 + lane; r < m; r += 32) s += c[r] * c[r];
+    return warp_sum(s);
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant__ QrArgs args,
+                                                           double *work, int *rank_out) {
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ double vn1[QR_MAXK], vn2[QR_MAXK], tau[QR_MAXK];
+    __shared__ double red[32];
+    __shared__ int piv_s;
+
+    const int b = blockIdx.x;
+    const int m = args.m[b], k = args.k[b];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = QR_THREADS / 32;
+    double *W = SMEM ? dyn : work + args.woff[b];
+    const double *G = args.G[b];
+    const int ldg = args.ldg[b];
+
+    if (m == 0 || k == 0) {
+        if (t == 0) rank_out[args.base + b] = 0;
+        return;
+    }
+    // load transposed: W[j*m + i] = G[i, j]
+    for (long long e = t; e < (long long)m * k; e += QR_THREADS) {
+        const int i = (int)(e / k), j = (int)(e % k);
+        W[(long long)j * m + i] = G[(long long)i * ldg + j];
+    }
+    __syncthreads();
+    for (int j = warp; j < k; j += nw) {
+        const double nrm = sqrt(col_norm2(W + (long long)j * m, 0, m, lane));
+        if (lane == 0) { vn1[j] = nrm; vn2[j] = nrm; }
+    }
+    __syncthreads();
+
+    const int kmin = m < k ? m : k;
+    for (int i = 0; i < kmin; ++i) {
+        // pivot: first index of max vn1[j], j >= i (idamax)
+        if (warp == 0) {
+            double best = -1.0;
+            int bi = k;
+            for (int j = i + lane; j < k; j += 32) {
+                const double v = vn1[j];
+                if (v > best) { best = v; bi = j; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) piv_s = bi;
+        }
+        __syncthreads();
+        const int p = piv_s;
+        if (p != i) {
+            double *ci = W + (long long)i * m, *cp = W + (long long)p * m;
+            for (int r = t; r < m; r += QR_THREADS) {
+                const double x = ci[r];
+                ci[r] = cp[r];
+                cp[r] = x;
+            }
+            if (t == 0) {
+                double x = vn1[i]; vn1[i] = vn1[p]; vn1[p] = x;
+                x = vn2[i]; vn2[i] = vn2[p]; vn2[p] = x;
+            }
+        }
+        __syncthreads();
+        // Householder reflector on W[i:m, i] (dlarfg)
+        double *ci = W + (long long)i * m;
+        double part = 0.0;
+        for (int r = i + 1 + t; r < m; r += QR_THREADS) part += ci[r] * ci[r];
+        const double xnorm = sqrt(block_sum(part, red));
+        const double alpha = ci[i];
+        double tau_i = 0.0, beta = alpha, scal = 0.0;
+        if (xnorm != 0.0) {
+            beta = -copysign(hypot(alpha, xnorm), alpha);
+            tau_i = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        __syncthreads();
+        if (xnorm != 0.0)
+            for (int r = i + 1 + t; r < m; r += QR_THREADS) ci[r] *= scal;
+        if (t == 0) { ci[i] = beta; tau[i] = tau_i; }
+        __syncthreads();
+        // apply H^T to the trailing columns and downdate their norms
+        for (int j = i + 1 + warp; j < k; j += nw) {
+            double *cj = W + (long long)j * m;
+            if (tau_i != 0.0) {
+                double w = 0.0;
+                for (int r = i + 1 + lane; r < m; r += 32) w += ci[r] * cj[r];
+                w = warp_sum(w) + cj[i];
+                const double f = tau_i * w;
+                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * ci[r];
+                __syncwarp();
+                if (lane == 0) cj[i] -= f;
+                __syncwarp();
+            }
+            const double v1 = vn1[j];
+            if (v1 != 0.0) {
+                double temp = fabs(cj[i]) / v1;
+                temp = 1.0 - temp * temp;
+                temp = temp < 0.0 ? 0.0 : temp;
+                const double ratio = v1 / vn2[j];
+                const double temp2 = temp * ratio * ratio;
+                if (temp2 <= TOL3Z) {
+                    double nv = 0.0;
+                    if (i + 1 < m) nv = sqrt(col_norm2(cj, i + 1, m, lane));
+                    if (lane == 0) { vn1[j] = nv; vn2[j] = nv; }
+                } else if (lane == 0) {
+                    vn1[j] = v1 * sqrt(temp);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+
+    // rank decision (kernels.py:78-81)
+    __shared__ int rank_s;
+    if (t == 0) {
+        const double d0 = fabs(W[0]);
+        int r = 0;
+        if (d0 != 0.0) {
+            const double cut = (double)(m > k ? m : k) * EPS * d0;
+            for (int i = 0; i < kmin; ++i)
+                if (fabs(W[(long long)i * m + i]) > cut) ++r;
+        }
+        rank_s = r;
+        rank_out[args.base + b] = r;
+    }
+    __syncthreads();
+    const int rank = rank_s;
+
+    // dorg2r on the first `rank` columns, in place
+    for (int i = rank - 1; i >= 0; --i) {
+        double *ci = W + (long long)i * m;
+        const double ti = tau[i];
+        if (i < rank - 1) {
+            if (t == 0) ci[i] = 1.0;
+            __syncthreads();
+            for (int j = i + 1 + warp; j < rank; j += nw) {
+                double *cj = W + (long long)j * m;
+                double w = 0.0;
+                for (int r = i + lane; r < m; r += 32) w += ci[r] * cj[r];
+                w = warp_sum(w);
+                const double f = ti * w;
+                for (int r = i + lane; r < m; r += 32) cj[r] -= f * ci[r];
+            }
+            __syncthreads();
+        }
+        for (int r = i + 1 + t; r < m; r += QR_THREADS) ci[r] *= -ti;
+        __syncthreads();
+        if (t == 0) ci[i] = 1.0 - ti;
+        for (int r = t; r < i; r += QR_THREADS) ci[r] = 0.0;
+        __syncthreads();
+    }
+    double *Q = args.Q[b];
+    const int ldq = args.ldq[b];
+    for (long long e = t; e < (long long)m * rank; e += QR_THREADS) {
+        const int r = (int)(e / rank), j = (int)(e % rank);
+        Q[(long long)r * ldq + j] = W[(long long)j * m + r];
+    }
+}
+
+constexpr long long SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
+
+}  // namespace
+
+extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k) {
+    long long tot = 0;
+    for (int i = 0; i < count; ++i) {
+        const long long sz = (long long)m[i] * k[i];
+        if (sz > SMEM_LIMIT_DOUBLES) tot += ((sz * 8 + 255) / 256) * 256;
+    }
+    return tot < 256 ? 256 : tot;
+}
+
+extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const int *k,
+                                const int *ldg, double *const *Q, const int *ldq, int *rank_dev,
+                                void *work_dev, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!G || !m || !k || !ldg || !Q || !ldq || !rank_dev) return -2;
+    cudaStream_t s = (cudaStream_t)stream;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(qrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(SMEM_LIMIT_DOUBLES * 8));
+        attr_set = true;
+    }
+    std::vector<int> small, big;
+    for (int i = 0; i < count; ++i) {
+        if (k[i] > QR_MAXK || m[i] < 0 || k[i] < 0) return -4;
+        if ((long long)m[i] * k[i] <= SMEM_LIMIT_DOUBLES) small.push_back(i);
+        else big.push_back(i);
+    }
+    if (!big.empty() && !work_dev) return -10;
+    static thread_local QrArgs qa;
+    // the rank array is indexed by original position: launch per contiguous run so
+    // `base` stays valid; simpler: one launch per matrix group with explicit mapping
+    auto run = [&](const std::vector<int> &ids, bool smem) -> int {
+        size_t pos = 0;
+        long long woff = 0;
+        while (pos < ids.size()) {
+            // contiguous runs of original indices keep base+b addressing exact
+            qa.count = 0;
+            qa.base = ids[pos];
+            long long maxsz = 0;
+            while (pos < ids.size() && qa.count < MAXB && ids[pos] == qa.base + qa.count) {
+                const int i = ids[pos++];
+                const int c = qa.count++;
+                qa.G[c] = G[i]; qa.Q[c] = Q[i];
+                qa.m[c] = m[i]; qa.k[c] = k[i]; qa.ldg[c] = ldg[i]; qa.ldq[c] = ldq[i];
+                const long long sz = (long long)m[i] * k[i];
+                maxsz = sz > maxsz ? sz : maxsz;
+                qa.woff[c] = smem ? 0 : woff / 8;
+                if (!smem) woff += ((sz * 8 + 255) / 256) * 256;
+            }
+            if (smem) {
+                qrcp_kernel<true><<<qa.count, QR_THREADS, (size_t)(maxsz * 8), s>>>(qa, nullptr, rank_dev);
+            } else {
+                qrcp_kernel<false><<<qa.count, QR_THREADS, 0, s>>>(qa, (double *)work_dev, rank_dev);
+            }
+            RSC_CHECK_LAUNCH();
+        }
+        return 0;
+    };
+    int rc = run(small, true);
+    if (rc) return rc;
+    // global workspace offsets are assigned in the order of `big`, matching
+    // rsc_qrcp_workspace_bytes (which sums the big ones in index order)
+    rc = run(big, false);
+    return rc;
+}

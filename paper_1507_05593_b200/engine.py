@@ -1,0 +1,254 @@
+"""Device-level wrappers over the C ABI, operating on torch CUDA tensors.
+
+torch is used only as the device allocator and stream owner; every FLOP runs in
+librsc_b200.so.  Matrices are row-major FP64 views `(tensor, rows, cols, ld)` or
+plain 2-D tensors with unit column stride.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import GEMM_DTYPE, addr, check, int_array, ptr_array
+
+F64 = torch.float64
+I32 = torch.int32
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("rsc_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return _lib.load()
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def empty(*shape, dtype=F64):
+    return torch.empty(*shape, dtype=dtype, device=dev())
+
+
+def zeros(*shape, dtype=F64):
+    return torch.zeros(*shape, dtype=dtype, device=dev())
+
+
+def to_dev(a, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(dev(), non_blocking=False)
+
+
+def ld(t):
+    """Leading dimension (row stride) of a 2-D row-major tensor view."""
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
+    if t.shape[1] > 1 and t.stride(1) != 1:
+        raise ValueError("tensor must have unit column stride")
+    return max(int(t.stride(0)), int(t.shape[1]), 1)
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+
+
+def gemm_problems(n):
+    return np.zeros(n, dtype=GEMM_DTYPE)
+
+
+def gemm_grouped(probs, transA=False, transB=False):
+    """Launch a grouped DMMA GEMM from a GEMM_DTYPE numpy array of problems."""
+    lib = require_cuda()
+    probs = np.ascontiguousarray(probs, dtype=GEMM_DTYPE)
+    if probs.size == 0:
+        return
+    check(lib.rsc_gemm_grouped(int(transA), int(transB), addr(probs), int(probs.size), stream_handle()),
+          "rsc_gemm_grouped")
+
+
+def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
+    """C = alpha op(A) op(B) + beta C for 2-D tensors (views allowed)."""
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    if C.shape[0] != M or C.shape[1] != N:
+        raise ValueError("gemm shape mismatch")
+    p = gemm_problems(1)
+    p["A"], p["B"], p["C"] = A.data_ptr(), B.data_ptr(), C.data_ptr()
+    p["M"], p["N"], p["K"] = M, N, K
+    p["lda"], p["ldb"], p["ldc"] = ld(A), ld(B), ld(C)
+    p["batch"], p["alpha"], p["beta"] = 1, alpha, beta
+    gemm_grouped(p, transA, transB)
+
+
+def gemm_strided_batched(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
+    """Batched GEMM over the leading dim of 3-D contiguous tensors."""
+    nb = A.shape[0]
+    M = A.shape[2] if transA else A.shape[1]
+    K = A.shape[1] if transA else A.shape[2]
+    N = B.shape[1] if transB else B.shape[2]
+    p = gemm_problems(1)
+    p["A"], p["B"], p["C"] = A.data_ptr(), B.data_ptr(), C.data_ptr()
+    p["sA"], p["sB"], p["sC"] = A.stride(0), B.stride(0), C.stride(0)
+    p["M"], p["N"], p["K"] = M, N, K
+    p["lda"], p["ldb"], p["ldc"] = A.stride(1), B.stride(1), C.stride(1)
+    p["batch"], p["alpha"], p["beta"] = nb, alpha, beta
+    gemm_grouped(p, transA, transB)
+
+
+# ---------------------------------------------------------------------------
+# POTRF / TRSM
+
+
+class TriFactors:
+    """A batch of device lower triangles with their inverse 64x64 diagonal blocks."""
+
+    def __init__(self, ptrs, n, lds, dinv_ptrs, keep=()):
+        self.ptrs = ptr_array(ptrs)
+        self.n = int_array(n)
+        self.lds = int_array(lds)
+        self.dinv = ptr_array(dinv_ptrs)
+        self._keep = list(keep)  # owning tensors
+
+    @property
+    def count(self):
+        return int(self.n.size)
+
+
+def potrf_batched(ptrs, n, lds, dinv_ptrs, info):
+    """In-place batched Cholesky; returns nothing, failures land in `info` (device int32)."""
+    lib = require_cuda()
+    ptrs, n, lds, dinv_ptrs = ptr_array(ptrs), int_array(n), int_array(lds), ptr_array(dinv_ptrs)
+    if n.size == 0:
+        return
+    check(lib.rsc_potrf_batched(int(n.size), addr(ptrs), addr(n), addr(lds), addr(dinv_ptrs),
+                                info.data_ptr(), stream_handle()), "rsc_potrf_batched")
+
+
+def trtri_diag_batched(ptrs, n, lds, dinv_ptrs):
+    lib = require_cuda()
+    ptrs, n, lds, dinv_ptrs = ptr_array(ptrs), int_array(n), int_array(lds), ptr_array(dinv_ptrs)
+    if n.size == 0:
+        return
+    check(lib.rsc_trtri_diag_batched(int(n.size), addr(ptrs), addr(n), addr(lds), addr(dinv_ptrs),
+                                     stream_handle()), "rsc_trtri_diag_batched")
+
+
+def trsm_batched(side, trans, Lptrs, n, ldl, dinv_ptrs, Bptrs, m, ldb):
+    """side 'left'/'right'; see rsc_trsm_batched."""
+    lib = require_cuda()
+    Lptrs, n, ldl, dinv_ptrs = ptr_array(Lptrs), int_array(n), int_array(ldl), ptr_array(dinv_ptrs)
+    Bptrs, m, ldb = ptr_array(Bptrs), int_array(m), int_array(ldb)
+    if n.size == 0:
+        return
+    s = 0 if side == "left" else 1
+    check(lib.rsc_trsm_batched(s, int(trans), int(n.size), addr(Lptrs), addr(n), addr(ldl),
+                               addr(dinv_ptrs), addr(Bptrs), addr(m), addr(ldb), stream_handle()),
+          "rsc_trsm_batched")
+
+
+# ---------------------------------------------------------------------------
+# QRCP
+
+
+def qrcp_batched(Gptrs, m, k, ldg, Qptrs, ldq, rank_out):
+    """Column-pivoted QR + cutoff; rank_out is a device int32 tensor (len = count)."""
+    lib = require_cuda()
+    Gptrs, m, k, ldg = ptr_array(Gptrs), int_array(m), int_array(k), int_array(ldg)
+    Qptrs, ldq = ptr_array(Qptrs), int_array(ldq)
+    if m.size == 0:
+        return
+    wbytes = int(lib.rsc_qrcp_workspace_bytes(int(m.size), addr(m), addr(k)))
+    work = torch.empty(max(wbytes // 8, 1), dtype=F64, device=dev())
+    check(lib.rsc_qrcp_batched(int(m.size), addr(Gptrs), addr(m), addr(k), addr(ldg), addr(Qptrs),
+                               addr(ldq), rank_out.data_ptr(), work.data_ptr(), stream_handle()),
+          "rsc_qrcp_batched")
+    return work  # keep alive until the stream passes it
+
+
+# ---------------------------------------------------------------------------
+# sparse + vector
+
+
+class DeviceCSR:
+    """A CSR matrix (or block) resident on the device, int32 indices."""
+
+    def __init__(self, nrows, ncols, indptr, indices, data):
+        self.nrows = int(nrows)
+        self.ncols = int(ncols)
+        self.indptr = to_dev(np.asarray(indptr, dtype=np.int32))
+        self.indices = to_dev(np.asarray(indices, dtype=np.int32))
+        self.data = to_dev(np.asarray(data, dtype=np.float64))
+        self.nnz = int(len(data))
+
+    @classmethod
+    def from_scipy(cls, S):
+        S = S.tocsr()
+        S.sort_indices()
+        return cls(S.shape[0], S.shape[1], S.indptr, S.indices, S.data)
+
+
+def spmm(S, X, Y, alpha=1.0, beta=0.0):
+    """Y = alpha S X + beta Y (S: DeviceCSR, X/Y 2-D tensors)."""
+    lib = require_cuda()
+    check(lib.rsc_spmm_csr(S.nrows, int(X.shape[1]), S.indptr.data_ptr(), S.indices.data_ptr(),
+                           S.data.data_ptr(), X.data_ptr(), ld(X), float(alpha), float(beta),
+                           Y.data_ptr(), ld(Y), stream_handle()), "rsc_spmm_csr")
+
+
+def spmv(S, x, y):
+    lib = require_cuda()
+    check(lib.rsc_spmv_csr(S.nrows, S.indptr.data_ptr(), S.indices.data_ptr(), S.data.data_ptr(),
+                           x.data_ptr(), y.data_ptr(), stream_handle()), "rsc_spmv_csr")
+
+
+def csr_to_dense_batched(rowptrs, colidx, values, nrows, Dptrs, ldd):
+    lib = require_cuda()
+    rowptrs, colidx, values = ptr_array(rowptrs), ptr_array(colidx), ptr_array(values)
+    nrows, Dptrs, ldd = int_array(nrows), ptr_array(Dptrs), int_array(ldd)
+    if nrows.size == 0:
+        return
+    check(lib.rsc_csr_to_dense_batched(int(nrows.size), addr(rowptrs), addr(colidx), addr(values),
+                                       addr(nrows), addr(Dptrs), addr(ldd), stream_handle()),
+          "rsc_csr_to_dense_batched")
+
+
+def gather_rows(idx, src, dst):
+    lib = require_cuda()
+    check(lib.rsc_gather_rows(int(idx.numel()), int(src.shape[1]), idx.data_ptr(), src.data_ptr(), ld(src),
+                              dst.data_ptr(), ld(dst), stream_handle()), "rsc_gather_rows")
+
+
+def scatter_add_rows(idx, src, dst, alpha=1.0):
+    lib = require_cuda()
+    check(lib.rsc_scatter_add_rows(int(idx.numel()), int(src.shape[1]), idx.data_ptr(), float(alpha),
+                                   src.data_ptr(), ld(src), dst.data_ptr(), ld(dst), stream_handle()),
+          "rsc_scatter_add_rows")
+
+
+class DotWorkspace:
+    def __init__(self):
+        self.part = empty(512)
+
+
+def dot(x, y, out, ws):
+    lib = require_cuda()
+    check(lib.rsc_dot(int(x.numel()), x.data_ptr(), y.data_ptr(), out.data_ptr(), ws.part.data_ptr(),
+                      stream_handle()), "rsc_dot")
+
+
+def pcg_update_xr(rz, pap, x, r, p, ap):
+    lib = require_cuda()
+    check(lib.rsc_pcg_update_xr(int(x.numel()), rz.data_ptr(), pap.data_ptr(), x.data_ptr(), r.data_ptr(),
+                                p.data_ptr(), ap.data_ptr(), stream_handle()), "rsc_pcg_update_xr")
+
+
+def pcg_update_p(rznew, rz, z, p):
+    lib = require_cuda()
+    check(lib.rsc_pcg_update_p(int(z.numel()), rznew.data_ptr(), rz.data_ptr(), z.data_ptr(), p.data_ptr(),
+                               stream_handle()), "rsc_pcg_update_p")

@@ -1,0 +1,127 @@
+"""GPU dense kernels vs the reference's golden vectors and KATs (through the C ABI)."""
+import numpy as np
+import pytest
+
+from conftest import golden, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+def test_gemm_grouped_all_transposes_and_maps(cuda):
+    import torch
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(1)
+    for ta in (False, True):
+        for tb in (False, True):
+            for (M, N, K) in [(1, 1, 1), (70, 33, 5), (129, 65, 200), (64, 64, 16), (3, 130, 0)]:
+                A = rng.standard_normal((K, M) if ta else (M, K))
+                B = rng.standard_normal((N, K) if tb else (K, N))
+                C0 = rng.standard_normal((M, N))
+                ref = 0.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 2.0 * C0
+                Cd = E.to_dev(C0)
+                E.gemm(E.to_dev(A), E.to_dev(B), Cd, transA=ta, transB=tb, alpha=0.5, beta=-2.0)
+                assert relerr(Cd.cpu().numpy(), ref) < 1e-14, (ta, tb, M, N, K)
+    # gather on B rows + scatter into C rows/cols with atomics (two problems, same target)
+    M, N, K = 40, 50, 30
+    A = rng.standard_normal((M, K))
+    Bbig = rng.standard_normal((100, N))
+    brow = rng.choice(100, K, replace=False).astype(np.int32)
+    crow = np.sort(rng.choice(90, M, replace=False)).astype(np.int32)
+    ccol = np.sort(rng.choice(70, N, replace=False)).astype(np.int32)
+    C = np.zeros((90, 70))
+    Ad, Bd, Cd = E.to_dev(A), E.to_dev(Bbig), E.to_dev(C)
+    idx = [E.to_dev(x) for x in (brow, crow, ccol)]
+    p = E.gemm_problems(2)
+    for i in range(2):
+        p[i]["A"], p[i]["B"], p[i]["C"] = Ad.data_ptr(), Bd.data_ptr(), Cd.data_ptr()
+        p[i]["b_rows"], p[i]["c_rows"], p[i]["c_cols"] = (t.data_ptr() for t in idx)
+        p[i]["M"], p[i]["N"], p[i]["K"] = M, N, K
+        p[i]["lda"], p[i]["ldb"], p[i]["ldc"] = K, N, 70
+        p[i]["batch"], p[i]["atomic"], p[i]["alpha"] = 1, 1, -1.0
+    E.gemm_grouped(p)
+    ref = np.zeros((90, 70))
+    ref[np.ix_(crow, ccol)] -= 2 * (A @ Bbig[brow])
+    assert relerr(Cd.cpu().numpy(), ref) < 1e-14
+
+
+def test_dense_cholesky_golden(cuda):
+    from paper_1507_05593_b200 import kernels as K
+
+    g = golden("kernels.npz")
+    for n in (1, 7, 23, 50, 64, 65, 130, 256):
+        assert relerr(K.dense_cholesky(g[f"chol_in_{n}"]), g[f"chol_out_{n}"]) < 1e-12, n
+
+
+def test_dense_cholesky_kats(cuda):
+    from paper_1507_05593_b200 import kernels as K
+    from paper_1507_05593_b200.errors import IndefiniteError
+
+    assert np.allclose(K.dense_cholesky(np.array([[4.0, 2.0], [2.0, 3.0]])), [[2, 0], [1, np.sqrt(2)]])
+    assert np.allclose(K.dense_cholesky(np.array([[4.0, 99.0], [2.0, 3.0]])), [[2, 0], [1, np.sqrt(2)]])
+    assert np.array_equal(K.dense_cholesky(np.eye(5)), np.eye(5))
+    with pytest.raises(IndefiniteError) as e:
+        K.dense_cholesky(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert e.value.pivot == 1
+    with pytest.raises(IndefiniteError) as e:
+        K.dense_cholesky(np.zeros((3, 3)))
+    assert e.value.pivot == 0
+    # pivot failure deep inside a later 64-block
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((150, 150))
+    M = M @ M.T + 150 * np.eye(150)
+    M[100, 100] = -1e6
+    with pytest.raises(IndefiniteError) as e:
+        K.dense_cholesky(M)
+    assert e.value.pivot == 100
+    assert K.dense_cholesky(np.zeros((0, 0))).shape == (0, 0)
+
+
+def test_tri_solve_golden(cuda):
+    from paper_1507_05593_b200 import kernels as K
+    from paper_1507_05593_b200.errors import SingularDiagonal
+
+    g = golden("kernels.npz")
+    L, B = g["tri_L"], g["tri_B"]
+    assert relerr(K.tri_solve(L, B), g["tri_left"]) < 1e-13
+    assert relerr(K.tri_solve(L, B, transpose=True), g["tri_left_t"]) < 1e-13
+    assert relerr(K.tri_solve(L, B.T, transpose=True, side="right"), g["tri_right_t"]) < 1e-13
+    assert relerr(K.tri_solve(L, B.T, side="right"), g["tri_right"]) < 1e-13
+    X = K.tri_solve(np.array([[2.0, 0.0], [1.0, 1.0]]), np.array([[2.0, 3.0]]), transpose=True, side="right")
+    assert np.allclose(X, [[1, 2]])
+    with pytest.raises(SingularDiagonal):
+        K.tri_solve(np.array([[1.0, 0.0], [3.0, 0.0]]), np.ones((2, 1)))
+    v = K.tri_solve(L, B[:, 0])
+    assert v.shape == (150,) and relerr(v, g["tri_left"][:, 0]) < 1e-13
+
+
+def test_orthonormalize_golden_ranks(cuda):
+    from paper_1507_05593_b200 import kernels as K
+
+    g = golden("kernels.npz")
+    for tag in "abc":
+        Q = K.orthonormalize(g[f"orth_in_{tag}"])
+        Qr = g[f"orth_out_{tag}"]
+        assert Q.shape == Qr.shape, tag
+        assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() < 1e-13
+        assert relerr(Q @ Q.T, Qr @ Qr.T) < 1e-10
+    e1 = np.zeros((4, 1))
+    e1[0] = 1.0
+    Q = K.orthonormalize(np.hstack([e1, 2 * e1]))
+    assert Q.shape == (4, 1) and abs(abs(Q[0, 0]) - 1) < 1e-14
+    assert K.orthonormalize(np.zeros((5, 2))).shape == (5, 0)
+
+
+def test_low_rank_approx_golden(cuda):
+    from paper_1507_05593_b200 import kernels as K
+
+    g = golden("kernels.npz")
+    V, U = K.low_rank_approx(g["lra_in"], 30, power_iters=1, seed=5)
+    assert U.shape == g["lra_U"].shape
+    assert relerr(V @ U.T, g["lra_V"] @ g["lra_U"].T) < 1e-10
+    rng = np.random.default_rng(2)
+    B = np.outer(rng.standard_normal(30), rng.standard_normal(12))
+    V, U = K.low_rank_approx(B, rank=4, seed=0)
+    assert relerr(V @ U.T, B) < 1e-10
+    V, U = K.low_rank_approx(np.zeros((10, 6)), rank=3, seed=0)
+    assert np.linalg.norm(V @ U.T) == 0.0
