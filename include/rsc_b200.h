@@ -137,6 +137,16 @@ int rsc_pcg_update_xr(int n, const double *rz_dev, const double *pap_dev,
 int rsc_pcg_update_p(int n, const double *rznew_dev, const double *rz_dev,
                      const double *z_dev, double *p_dev, void *stream);
 
+/* ---- host-only symbolic analysis (no device work; symbolic.py:44-151) ----
+ * Inputs: the permuted matrix in lower CSC (col_ptr[n+1], row_idx[nnz], int64).
+ * etree: parent[j] (-1 for roots).  postorder: children ascending, roots ascending.
+ * colcounts: nonzeros per column of the Cholesky factor, diagonal included. */
+int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_idx,
+                  long long *parent);
+int rsc_sym_postorder(long long n, const long long *parent, long long *post);
+int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *row_idx,
+                      const long long *parent, const long long *post, long long *counts);
+
 /* Number of kernels this process launched through the library (reset != 0
  * returns the count and zeroes it).  Diagnostic only. */
 long long rsc_launch_counter(int reset);

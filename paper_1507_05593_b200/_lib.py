@@ -42,6 +42,9 @@ EXPORTED = (
     "rsc_dot",
     "rsc_pcg_update_xr",
     "rsc_pcg_update_p",
+    "rsc_sym_etree",
+    "rsc_sym_postorder",
+    "rsc_sym_colcounts",
     "rsc_launch_counter",
     "rsc_version",
     "rsc_device_arch",
@@ -69,6 +72,9 @@ _SIGS = {
     "rsc_dot": (I, [I, P, P, P, P, P]),
     "rsc_pcg_update_xr": (I, [I, P, P, P, P, P, P, P]),
     "rsc_pcg_update_p": (I, [I, P, P, P, P, P]),
+    "rsc_sym_etree": (I, [LL, P, P, P]),
+    "rsc_sym_postorder": (I, [LL, P, P]),
+    "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
     "rsc_launch_counter": (LL, [I]),
     "rsc_version": (ctypes.c_char_p, []),
     "rsc_device_arch": (I, []),

@@ -48,6 +48,8 @@ def ld(t):
     """Leading dimension (row stride) of a 2-D row-major tensor view."""
     if t.dim() != 2:
         raise ValueError("expected a 2-D tensor")
+    if t.numel() == 0:
+        return max(int(t.shape[1]), 1)
     if t.shape[1] > 1 and t.stride(1) != 1:
         raise ValueError("tensor must have unit column stride")
     return max(int(t.stride(0)), int(t.shape[1]), 1)

@@ -78,6 +78,91 @@ def sec_cfg1(nb=4):
     np.savez_compressed(os.path.join(OUT, "cfg1.npz"), **out)
 
 
+INF = float("inf")
+# name -> (generator, args, strip zeros, knob overrides, keep dense_lower)
+FACTOR_CASES = {
+    "l2d16_exact": ("laplacian_2d", (16,), False, dict(tau_o=INF), True),
+    "l3d8_small": ("laplacian_3d", (8,), False, dict(tau_o=16, tau_d=32, oversample=4), True),
+    "l3d12": ("laplacian_3d", (12,), False, dict(tau_d=64), True),
+    "l3d16": ("laplacian_3d", (16,), False, dict(tau_d=64), False),
+    "el5": ("elasticity_3d", (5,), True, dict(tau_o=16, tau_d=32, oversample=4), True),
+    "el7": ("elasticity_3d", (7,), True, dict(tau_d=64), False),
+    "cfg0": ("laplacian_2d", (128,), False, dict(), False),
+    "l3d24": ("laplacian_3d", (24,), False, dict(), False),
+    "l3d16_noint": ("laplacian_3d", (16,), False, dict(tau_d=64, interior_blocks=False), False),
+}
+
+
+def _strip(A):
+    keep = A.values != 0.0
+    cols = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.col_ptr))
+    return rs.SparseSpdMatrix.from_coo(A.n, A.row_idx[keep], cols[keep], A.values[keep])
+
+
+def _units_code(units):
+    """(kind, first, last) per unit: kind 0 interior [members j0..j1], 1 node j."""
+    out = []
+    for kind, obj in units:
+        if kind == "interior":
+            ids = [m.j for m in obj.members]
+            out.append((0, ids[0], ids[-1]))
+        else:
+            out.append((1, obj.j, obj.j))
+    return np.array(out, dtype=np.int64).reshape(-1, 3)
+
+
+def sec_factor():
+    """Symbolic plan + numeric results of the reference on small instances."""
+    for name, (gen, args, strip, over, keep_dense) in FACTOR_CASES.items():
+        A, coords = getattr(rprob, gen)(*args)
+        if strip:
+            A = _strip(A)
+        cfg = rs.SolverConfig(**dict(KNOBS, **over))
+        F = rs.factorize(A, cfg, coords=coords)
+        part = F.partition
+        rows = part.rows
+        out = {
+            "perm": F.perm.forward,
+            "starts": part.starts,
+            "is_sep": part.is_separator,
+            "rows_ptr": np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.int64),
+            "rows_idx": np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64),
+            "units": _units_code(F.units),
+            "stored_scalars": np.array([F.stored_scalars()]),
+            "restarts": np.array([F.stats.restarts]),
+            "counts": np.array([F.stats.compressed_offdiag, F.stats.compressed_diag, F.stats.dense_fallback]),
+        }
+        # diagonal-tree leaf sizes per tree node and kept ranks of compressed blocks
+        ranks = []
+        for kind, obj in F.units:
+            if kind != "node":
+                continue
+            if isinstance(obj.offdiag, rs.LowRankBlock):
+                ranks.append((obj.j, -1, obj.offdiag.rank))
+            if isinstance(obj.diag, rs.DiagBlockTree):
+                for s in obj.diag.inorder_ids():
+                    b = obj.diag.blocks[s]
+                    if isinstance(b, rs.LowRankBlock):
+                        ranks.append((obj.j, s, b.rank))
+                out[f"leaves_{obj.j}"] = np.array(
+                    [obj.diag.nodes[s].hi - obj.diag.nodes[s].lo for s in obj.diag.leaf_ids()])
+        out["ranks"] = np.array(ranks, dtype=np.int64).reshape(-1, 3)
+        r = np.random.default_rng(1).standard_normal(A.n)
+        out["apply_r"] = F.apply(r)
+        b = np.random.default_rng(0).standard_normal(A.n)
+        x, rep = rs.pcg_solve(A, b, preconditioner=F, tol=1e-6)
+        out["pcg_x"] = x
+        out["pcg_iters"] = np.array([rep.iterations])
+        out["pcg_hist"] = np.array(rep.relative_residual_history)
+        if keep_dense:
+            L = F.dense_lower()
+            Bm = rs.permute_symmetric(A, F.perm).dense()
+            out["L_dense"] = L
+            out["resid"] = np.array([np.linalg.norm(L @ L.T - Bm) / np.linalg.norm(A.dense())])
+        np.savez_compressed(os.path.join(OUT, f"factor_{name}.npz"), **out)
+        print(" ", name, A.n, "iters", rep.iterations, "ranks", len(ranks))
+
+
 if __name__ == "__main__":
     sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
     secs = sys.argv[1:] or ["kernels", "cfg1"]
