@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--config", type=int, default=1)
     p.add_argument("--nb", type=int, default=512)
+    p.add_argument("--chunk", type=int, default=None, help="supernodes per grouped launch (default: all)")
     p.add_argument("--cpu-sample", type=int, default=48, help="blocks in the CPU baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -211,7 +212,7 @@ def run_b200_cfg1(args, rank, world, torch, dist):
     lib = _lib.load()
     nb, n, m, r, q = args.nb, 256, 2048, 58, 1
     D, B = cfg1_inputs(nb)
-    bs = BatchedSupernodes(nb, n, m, r, q=q, chunk=32)
+    bs = BatchedSupernodes(nb, n, m, r, q=q, chunk=args.chunk)
     D0 = torch.from_numpy(D).cuda()
     B0 = torch.from_numpy(B).cuda()
     Om = make_sketches(nb, m, r, master=0, threads=os.cpu_count() or 1)
@@ -259,7 +260,7 @@ def run_b200_cfg1(args, rank, world, torch, dist):
     reps = 3
     evs[0].record()
     for _ in range(reps):
-        E.gemm_strided_batched(LO, Omd, G, transA=True)
+        E.gemm_strided_batched(LO, Omd, G, transA=True, splitk=bs.splitk)
         E.gemm_strided_batched(LO, G, H)
     evs[1].record()
     torch.cuda.synchronize()

@@ -14,8 +14,9 @@ which is the reference composition dense_cholesky -> tri_solve -> low_rank_appro
 for every block.  Omega_i are the reference's own PCG64 sketches
 (seed `_block_seed(seed, 0, i)`), generated on host threads and uploaded unchanged.
 
-To keep each block's 2048x256 L_O resident in the 126 MB L2 across the five
-stages, the batch is processed in chunks (`chunk` supernodes at a time).
+The whole batch goes through each stage in one grouped launch (the products
+stream L_O from HBM at ~8 flop/byte, above the FP64 ridge); `chunk` can cut the
+batch to trade launch width for L2 residency.
 """
 
 import concurrent.futures as cf
@@ -69,9 +70,11 @@ def model_flops(nb, n, m, r, q):
 class BatchedSupernodes:
     """Device workspace for a batch of `nb` supernodes of shape (n, m) with sketch width r."""
 
-    def __init__(self, nb, n, m, r, q=1, chunk=32):
+    def __init__(self, nb, n, m, r, q=1, chunk=None, splitk=None):
         self.nb, self.n, self.m, self.r, self.q = nb, n, m, r, q
-        self.chunk = max(1, min(chunk, nb))
+        self.chunk = nb if chunk is None else max(1, min(chunk, nb))
+        # split the tall K = m of L_O^T X so a launch has >= ~4 CTAs per SM
+        self.splitk = splitk if splitk is not None else max(1, min(m // 256, 16))
         self.D = E.empty(nb, n, n)
         self.B = E.empty(nb, m, n)
         self.Om = E.empty(nb, m, r)
@@ -97,10 +100,10 @@ class BatchedSupernodes:
             Bp = [self.B[i].data_ptr() for i in idx]
             E.trsm_batched("right", 1, Dp, [n] * cnt, [n] * cnt, Ip, Bp, [m] * cnt, [n] * cnt)
             LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
-            E.gemm_strided_batched(LO, Om, G, transA=True)
+            E.gemm_strided_batched(LO, Om, G, transA=True, splitk=self.splitk)
             for _ in range(q):
                 E.gemm_strided_batched(LO, G, H)
-                E.gemm_strided_batched(LO, H, G, transA=True)
+                E.gemm_strided_batched(LO, H, G, transA=True, splitk=self.splitk)
             self._qr_work = E.qrcp_batched([self.G[i].data_ptr() for i in idx], [n] * cnt, [r] * cnt,
                                            [r] * cnt, [self.U[i].data_ptr() for i in idx], [r] * cnt,
                                            self.rank[c0:c1])

@@ -28,11 +28,50 @@ struct DiagArgs {
     int base;  // index of A[0] within the caller's info array
 };
 
+// 64x64 diagonal block in shared memory, 256 threads: thread t owns row
+// i = t >> 2 and the columns j == (t & 3) mod 4.  L lives in the lower triangle;
+// its inverse is kept transposed in the strict upper part plus the pad column:
+// inv[i][c] (i >= c) lives at s[c][i + 1].
+// Right-looking Cholesky, then column-parallel forward substitution L X = I.
+// Returns the 0-based failing pivot or -1.
+__device__ int factor_invert_64(double (*s)[NB + 1], int nb, bool factor) {
+    const int t = threadIdx.x, i = t >> 2, cg = t & 3;
+    if (factor) {
+        for (int k = 0; k < nb; ++k) {
+            const double piv = s[k][k];
+            if (!(piv > 0.0)) return k;  // uniform: every thread read the same value
+            const double d = sqrt(piv);
+            __syncthreads();
+            if (i > k && i < nb && cg == 0) s[i][k] /= d;
+            if (t == 0) s[k][k] = d;
+            __syncthreads();
+            if (i > k && i < nb) {
+                const double lik = s[i][k];
+                for (int j = k + 1 + ((cg - (k + 1)) & 3); j <= i; j += 4) s[i][j] -= lik * s[j][k];
+            }
+            __syncthreads();
+        }
+    }
+    // X = L^{-1}: row k of X is final once the updates from rows < k are in
+    for (int c = cg; c <= i && i < nb; c += 4) s[c][i + 1] = (c == i) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        const double dk = s[k][k];
+        if (i == k)
+            for (int c = cg; c <= k; c += 4) s[c][k + 1] /= dk;
+        __syncthreads();
+        if (i > k && i < nb) {
+            const double lik = s[i][k];
+            for (int c = cg; c <= k; c += 4) s[c][i + 1] -= lik * s[c][k + 1];
+        }
+        __syncthreads();
+    }
+    return -1;
+}
+
 // One CTA per matrix: factor the diagonal block of panel `step` and invert it.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(const __grid_constant__ DiagArgs args,
                                                           int *info) {
-    // L in the lower triangle; its inverse is kept transposed in the strict upper
-    // part plus the pad column: inv[i][c] (i >= c) lives at s[c][i + 1].
     __shared__ double s[NB][NB + 1];
     const int b = blockIdx.x;
     const int n = args.n[b];
@@ -44,43 +83,17 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(const __grid_constant__
     const int lda = args.lda[b];
     const int t = threadIdx.x;
     for (int e = t; e < NB * NB; e += blockDim.x) {
-        const int i = e / NB, j = e % NB;
-        double v = 0.0;
-        if (i < nb && j <= i) v = A[(long long)(j0 + i) * lda + j0 + j];
-        s[i][j] = v;
+        const int i = e >> 6, j = e & 63;
+        s[i][j] = (i < nb && j <= i) ? A[(long long)(j0 + i) * lda + j0 + j] : 0.0;
     }
     __syncthreads();
-    for (int k = 0; k < nb; ++k) {
-        const double piv = s[k][k];
-        if (!(piv > 0.0)) {  // uniform across the CTA
-            if (t == 0) info[args.base + b] = j0 + k + 1;
-            return;
-        }
-        const double d = sqrt(piv);
-        __syncthreads();  // everyone has read s[k][k]
-        if (t == 0) s[k][k] = d;
-        for (int i = k + 1 + t; i < nb; i += blockDim.x) s[i][k] /= d;
-        __syncthreads();
-        // trailing update of the lower triangle
-        const int m = nb - k - 1;
-        for (int e = t; e < m * m; e += blockDim.x) {
-            const int i = k + 1 + e / m, j = k + 1 + e % m;
-            if (j <= i) s[i][j] -= s[i][k] * s[j][k];
-        }
-        __syncthreads();
+    const int bad = factor_invert_64(s, nb, true);
+    if (bad >= 0) {
+        if (t == 0) info[args.base + b] = j0 + bad + 1;
+        return;
     }
-    // inverse of the lower triangle: column c of X solves L x = e_c (rows >= c)
-    for (int c = t; c < nb; c += blockDim.x) {
-        for (int i = c; i < nb; ++i) {
-            double acc = (i == c) ? 1.0 : 0.0;
-            for (int k = c; k < i; ++k) acc -= s[i][k] * s[c][k + 1];
-            s[c][i + 1] = acc / s[i][i];
-        }
-    }
-    __syncthreads();
-    // write back L (lower, upper part of the block row zeroed) and Dinv
     for (int e = t; e < nb * NB; e += blockDim.x) {
-        const int i = e / NB, j = e % NB;
+        const int i = e >> 6, j = e & 63;
         if (j < nb) A[(long long)(j0 + i) * lda + j0 + j] = (j <= i) ? s[i][j] : 0.0;
         args.Dinv[b][(long long)(j0 + i) * NB + j] = (j < nb && j <= i) ? s[j][i + 1] : 0.0;
     }
@@ -106,20 +119,13 @@ __global__ void __launch_bounds__(256) trtri_diag_kernel(const __grid_constant__
     const int lda = args.lda[b];
     const int t = threadIdx.x;
     for (int e = t; e < NB * NB; e += blockDim.x) {
-        const int i = e / NB, j = e % NB;
+        const int i = e >> 6, j = e & 63;
         s[i][j] = (i < nb && j <= i) ? A[(long long)(j0 + i) * lda + j0 + j] : 0.0;
     }
     __syncthreads();
-    for (int c = t; c < nb; c += blockDim.x) {
-        for (int i = c; i < nb; ++i) {
-            double acc = (i == c) ? 1.0 : 0.0;
-            for (int k = c; k < i; ++k) acc -= s[i][k] * s[c][k + 1];
-            s[c][i + 1] = acc / s[i][i];
-        }
-    }
-    __syncthreads();
+    factor_invert_64(s, nb, false);
     for (int e = t; e < nb * NB; e += blockDim.x) {
-        const int i = e / NB, j = e % NB;
+        const int i = e >> 6, j = e & 63;
         args.Dinv[b][(long long)(j0 + i) * NB + j] = (j < nb && j <= i) ? s[j][i + 1] : 0.0;
     }
 }

@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     const int m = args.m[b], k = args.k[b];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = QR_THREADS / 32;
     double *W = SMEM ? dyn : work + args.woff[b];
+    const int ldw = m | 1;  // odd column stride: conflict-free transposed load
     const double *G = args.G[b];
     const int ldg = args.ldg[b];
 
@@ -63,11 +64,11 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     // load transposed: W[j*m + i] = G[i, j]
     for (long long e = t; e < (long long)m * k; e += QR_THREADS) {
         const int i = (int)(e / k), j = (int)(e % k);
-        W[(long long)j * m + i] = G[(long long)i * ldg + j];
+        W[(long long)j * ldw + i] = G[(long long)i * ldg + j];
     }
     __syncthreads();
     for (int j = warp; j < k; j += nw) {
-        const double nrm = sqrt(col_norm2(W + (long long)j * m, 0, m, lane));
+        const double nrm = sqrt(col_norm2(W + (long long)j * ldw, 0, m, lane));
         if (lane == 0) { vn1[j] = nrm; vn2[j] = nrm; }
     }
     __syncthreads();
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         __syncthreads();
         const int p = piv_s;
         if (p != i) {
-            double *ci = W + (long long)i * m, *cp = W + (long long)p * m;
+            double *ci = W + (long long)i * ldw, *cp = W + (long long)p * ldw;
             for (int r = t; r < m; r += QR_THREADS) {
                 const double x = ci[r];
                 ci[r] = cp[r];
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         }
         __syncthreads();
         // Householder reflector on W[i:m, i] (dlarfg)
-        double *ci = W + (long long)i * m;
+        double *ci = W + (long long)i * ldw;
         double part = 0.0;
         for (int r = i + 1 + t; r < m; r += QR_THREADS) part += ci[r] * ci[r];
         const double xnorm = sqrt(block_sum(part, red));
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         __syncthreads();
         // apply H^T to the trailing columns and downdate their norms
         for (int j = i + 1 + warp; j < k; j += nw) {
-            double *cj = W + (long long)j * m;
+            double *cj = W + (long long)j * ldw;
             if (tau_i != 0.0) {
                 double w = 0.0;
                 for (int r = i + 1 + lane; r < m; r += 32) w += ci[r] * cj[r];
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         if (d0 != 0.0) {
             const double cut = (double)(m > k ? m : k) * EPS * d0;
             for (int i = 0; i < kmin; ++i)
-                if (fabs(W[(long long)i * m + i]) > cut) ++r;
+                if (fabs(W[(long long)i * ldw + i]) > cut) ++r;
         }
         rank_s = r;
         rank_out[args.base + b] = r;
@@ -173,13 +174,13 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
 
     // dorg2r on the first `rank` columns, in place
     for (int i = rank - 1; i >= 0; --i) {
-        double *ci = W + (long long)i * m;
+        double *ci = W + (long long)i * ldw;
         const double ti = tau[i];
         if (i < rank - 1) {
             if (t == 0) ci[i] = 1.0;
             __syncthreads();
             for (int j = i + 1 + warp; j < rank; j += nw) {
-                double *cj = W + (long long)j * m;
+                double *cj = W + (long long)j * ldw;
                 double w = 0.0;
                 for (int r = i + lane; r < m; r += 32) w += ci[r] * cj[r];
                 w = warp_sum(w);
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     const int ldq = args.ldq[b];
     for (long long e = t; e < (long long)m * rank; e += QR_THREADS) {
         const int r = (int)(e / rank), j = (int)(e % rank);
-        Q[(long long)r * ldq + j] = W[(long long)j * m + r];
+        Q[(long long)r * ldq + j] = W[(long long)j * ldw + r];
     }
 }
 
@@ -209,7 +210,7 @@ constexpr long long SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
 extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k) {
     long long tot = 0;
     for (int i = 0; i < count; ++i) {
-        const long long sz = (long long)m[i] * k[i];
+        const long long sz = (long long)(m[i] | 1) * k[i];
         if (sz > SMEM_LIMIT_DOUBLES) tot += ((sz * 8 + 255) / 256) * 256;
     }
     return tot < 256 ? 256 : tot;
@@ -231,7 +232,7 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     std::vector<int> small, big;
     for (int i = 0; i < count; ++i) {
         if (k[i] > QR_MAXK || m[i] < 0 || k[i] < 0) return -4;
-        if ((long long)m[i] * k[i] <= SMEM_LIMIT_DOUBLES) small.push_back(i);
+        if ((long long)(m[i] | 1) * k[i] <= SMEM_LIMIT_DOUBLES) small.push_back(i);
         else big.push_back(i);
     }
     if (!big.empty() && !work_dev) return -10;
@@ -251,7 +252,7 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                 const int c = qa.count++;
                 qa.G[c] = G[i]; qa.Q[c] = Q[i];
                 qa.m[c] = m[i]; qa.k[c] = k[i]; qa.ldg[c] = ldg[i]; qa.ldq[c] = ldq[i];
-                const long long sz = (long long)m[i] * k[i];
+                const long long sz = (long long)(m[i] | 1) * k[i];
                 maxsz = sz > maxsz ? sz : maxsz;
                 qa.woff[c] = smem ? 0 : woff / 8;
                 if (!smem) woff += ((sz * 8 + 255) / 256) * 256;

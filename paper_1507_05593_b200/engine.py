@@ -88,18 +88,42 @@ def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
     gemm_grouped(p, transA, transB)
 
 
-def gemm_strided_batched(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
-    """Batched GEMM over the leading dim of 3-D contiguous tensors."""
+def gemm_strided_batched(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0, splitk=1):
+    """Batched GEMM over the leading dim of 3-D contiguous tensors.
+
+    splitk > 1 cuts K into `splitk` slabs accumulated with FP64 atomics (C is
+    zeroed first when beta == 0) -- for the tall-K sketch products L_O^T X whose
+    output tile count alone cannot fill 148 SMs."""
     nb = A.shape[0]
     M = A.shape[2] if transA else A.shape[1]
     K = A.shape[1] if transA else A.shape[2]
     N = B.shape[1] if transB else B.shape[2]
-    p = gemm_problems(1)
-    p["A"], p["B"], p["C"] = A.data_ptr(), B.data_ptr(), C.data_ptr()
+    splitk = max(1, min(int(splitk), K // 16 if K >= 32 else 1))
+    if splitk > 1:
+        if beta == 0.0:
+            C.zero_()
+        elif beta != 1.0:
+            C.mul_(beta)
+    kc = -(-K // splitk)
+    kc = -(-kc // 16) * 16
+    starts = list(range(0, K, kc))
+    p = gemm_problems(len(starts))
+    for i, k0 in enumerate(starts):
+        a_off = (k0 * A.stride(1)) if transA else k0
+        b_off = k0 if transB else (k0 * B.stride(1))
+        p[i]["A"] = A.data_ptr() + 8 * a_off
+        p[i]["B"] = B.data_ptr() + 8 * b_off
+        p[i]["C"] = C.data_ptr()
+        p[i]["K"] = min(kc, K - k0)
     p["sA"], p["sB"], p["sC"] = A.stride(0), B.stride(0), C.stride(0)
-    p["M"], p["N"], p["K"] = M, N, K
+    p["M"], p["N"] = M, N
     p["lda"], p["ldb"], p["ldc"] = A.stride(1), B.stride(1), C.stride(1)
-    p["batch"], p["alpha"], p["beta"] = nb, alpha, beta
+    p["batch"], p["alpha"] = nb, alpha
+    if len(starts) > 1:
+        p["atomic"] = 1
+        p["beta"] = 1.0
+    else:
+        p["beta"] = beta
     gemm_grouped(p, transA, transB)
 
 
