@@ -20,7 +20,7 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
 constexpr int PADK = BK + 4;   // [m][k] / [n][k] row stride (doubles)
-constexpr int PADM = BM + 8;   // [k][m] / [k][n] row stride (doubles)
+constexpr int PADM = BM + 4;   // [k][m] / [k][n] row stride: 2*PADM = 8 mod 32 banks
 constexpr int A_SZ = (BM * PADK > BK * PADM) ? BM * PADK : BK * PADM;
 constexpr int B_SZ = A_SZ;
 constexpr int MAXP = 192;

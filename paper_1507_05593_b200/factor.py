@@ -1,0 +1,850 @@
+"""GPU numeric rank-structured factorization (drop-in for rschol.factorize).
+
+Host Python walks the unit plan (factor.py:556-639 order) and issues grouped
+sm_100a kernels through the C ABI; all numeric data stays in HBM:
+
+  interior blocks    all factored up front in ONE batched POTRF + ONE batched TRSM
+                     (they depend on nothing), coupling rows materialized as
+                     Y_B = A(off_rows, C_B) L_B^{-T}  (interior.py:29-156)
+  Schur assembly     gather -> DMMA -> scatter-subtract, one grouped launch over all
+                     sources of the target (factor.py:372-399, diagblocks.py:220-238)
+  implicit products  two grouped launches per product: T_s = X_s^T G[map] for all
+                     sources, then W[map] -= Y_s T_s with FP64 atomics
+                     (factor.py:427-483, diagblocks.py:241-346)
+  compression        host PCG64 sketch -> products -> pivoted QR (rank cutoff) ->
+                     projection V = L_O U  (factor.py:486-505, diagblocks.py:349-370)
+  diagonal trees     leaf Schur + POTRF, internal blocks compressed or dense
+                     (diagblocks.py:276-346), Alg. 4 tree solves on device
+  restart            IndefiniteError restarts the pass with alpha_d *= growth when a
+                     diagonal tree was started before the failing pivot
+                     (factor.py:702-718)
+"""
+
+import math
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine as E
+from ._lib import GEMM_DTYPE
+from .errors import DimensionMismatch, IndefiniteError, TooManyRestarts
+from .plan import NumericPlan
+from .sparse import as_spd
+from .symbolic import analyze, block_rank
+
+__all__ = ["SolverConfig", "FactorStats", "RankStructuredFactor", "block_rank", "factorize"]
+
+DENSE_FALLBACK_FRACTION = 0.75
+
+
+@dataclass
+class SolverConfig:
+    """Tuning knobs (factor.py:65-111), same names, defaults and validation."""
+
+    tau_o: float = 400
+    tau_d: int = 256
+    alpha_o: float = 1.0
+    alpha_d: float = 0.5
+    oversample: int = 8
+    power_iters: int = 1
+    seed: int = 0
+    interior_blocks: bool = True
+    max_restarts: int = 10
+    alpha_d_growth: float = 1.25
+
+    def __post_init__(self):
+        if self.tau_o < 1 or self.tau_d < 1:
+            raise ValueError("tau_o and tau_d must be positive")
+        if self.alpha_o <= 0 or self.alpha_d <= 0 or self.oversample <= 0:
+            raise ValueError("alpha_o, alpha_d and oversample must be positive")
+        if self.power_iters < 0 or self.max_restarts < 0:
+            raise ValueError("power_iters and max_restarts must be nonnegative")
+        if self.alpha_d_growth <= 1.0:
+            raise ValueError("alpha_d_growth must exceed 1")
+
+    def to_dict(self):
+        d = dict(self.__dict__)
+        if not math.isfinite(self.tau_o):
+            d["tau_o"] = "inf"
+        return d
+
+
+@dataclass
+class FactorStats:
+    n: int = 0
+    nnz_lower: int = 0
+    supernodes: int = 0
+    separator_supernodes: int = 0
+    interior_block_count: int = 0
+    compressed_offdiag: int = 0
+    compressed_diag: int = 0
+    dense_fallback: int = 0
+    stored_scalars: int = 0
+    restarts: int = 0
+    alpha_d_final: float = 0.0
+    alpha_d_history: list = field(default_factory=list)
+    phase_times: dict = field(default_factory=dict)
+    seed: int = 0
+    gpu_launches: int = 0
+    model_gflop: float = 0.0
+
+    @property
+    def compressed_blocks(self):
+        return self.compressed_offdiag + self.compressed_diag
+
+    def to_dict(self):
+        return {
+            "n": self.n, "nnz": self.nnz_lower, "supernodes": self.supernodes,
+            "separator_supernodes": self.separator_supernodes, "interior_blocks": self.interior_block_count,
+            "compressed_blocks": self.compressed_blocks, "compressed_offdiag": self.compressed_offdiag,
+            "compressed_diag": self.compressed_diag, "dense_fallback": self.dense_fallback,
+            "stored_scalars": self.stored_scalars, "restarts": self.restarts,
+            "alpha_D_final": self.alpha_d_final, "alpha_D_history": self.alpha_d_history,
+            "phase_times": self.phase_times, "seed": self.seed,
+        }
+
+
+def _block_seed(master, *tags):
+    """factor.py:324-326."""
+    ss = np.random.SeedSequence((int(master),) + tuple(int(t) for t in tags))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+def _gaussian(m, n, seed):
+    """Reference PCG64 stream (kernels.py:85-92), generated on the host."""
+    return np.random.Generator(np.random.PCG64(seed)).standard_normal((m, n))
+
+
+# ---------------------------------------------------------------------------
+# device factor blocks
+
+
+class DenseTri:
+    """Dense lower triangle + inverse 64x64 diagonal blocks."""
+
+    __slots__ = ("L", "Dinv", "n")
+
+    def __init__(self, L, Dinv):
+        self.L, self.Dinv, self.n = L, Dinv, L.shape[0]
+
+    def solve(self, X, transpose=False):
+        """X <- L^{-1} X (or L^{-T} X) in place; X is an n x r row-major view."""
+        if self.n == 0 or X.shape[1] == 0:
+            return
+        E.trsm_batched("left", 1 if transpose else 0, [self.L.data_ptr()], [self.n], [E.ld(self.L)],
+                       [self.Dinv.data_ptr()], [X.data_ptr()], [X.shape[1]], [E.ld(X)])
+
+
+class DevLR:
+    """Low-rank block V U^T (U orthonormal), with E = V (U^T U) kept for the
+    eff_rows role of blocks.py:103-113."""
+
+    __slots__ = ("V", "U", "E", "k")
+
+    def __init__(self, V, U, Eff):
+        self.V, self.U, self.E, self.k = V, U, Eff, U.shape[1]
+
+
+class DeviceTree:
+    """Numeric content of a hierarchical diagonal (DenseTri leaves, dense or
+    DevLR couplings) and its Alg. 4 solve (diagblocks.py:176-213)."""
+
+    def __init__(self, shape):
+        self.shape = shape
+        self.blocks = {}
+
+    def solve(self, X, transpose=False, s=None):
+        nd = self.shape.root if s is None else self.shape.nodes[s]
+        self._solve(nd, X, transpose)
+
+    def _solve(self, nd, X, transpose):
+        if nd.is_leaf:
+            self.blocks[nd.s].solve(X, transpose)
+            return
+        k = nd.split - nd.lo
+        X1, X2 = X[:k], X[k:]
+        b = self.blocks[nd.s]
+        if transpose:
+            self._solve(nd.right, X2, True)
+            _couple_sub(b, X2, X1, transpose=True)
+            self._solve(nd.left, X1, True)
+        else:
+            self._solve(nd.left, X1, False)
+            _couple_sub(b, X1, X2, transpose=False)
+            self._solve(nd.right, X2, False)
+
+
+def _gemm1(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
+    if C.shape[0] == 0 or C.shape[1] == 0:
+        return
+    E.gemm(A, B, C, transA=transA, transB=transB, alpha=alpha, beta=beta)
+
+
+def _couple_sub(b, X, Y, transpose):
+    """Y -= block @ X (or block^T @ X) for a dense or low-rank coupling block."""
+    r = X.shape[1]
+    if isinstance(b, DevLR):
+        if b.k == 0:
+            return
+        t = E.empty(b.k, r)
+        if transpose:  # U (V^T X)
+            _gemm1(b.V, X, t, transA=True)
+            _gemm1(b.U, t, Y, alpha=-1.0, beta=1.0)
+        else:  # V (U^T X)
+            _gemm1(b.U, X, t, transA=True)
+            _gemm1(b.V, t, Y, alpha=-1.0, beta=1.0)
+    else:
+        _gemm1(b, X, Y, transA=transpose, alpha=-1.0, beta=1.0)
+
+
+def _raw_eff(obj):
+    """(raw, eff) panels of a dense or low-rank block (blocks.py:103-119)."""
+    if isinstance(obj, DevLR):
+        return obj.V, obj.E
+    return obj, obj
+
+
+class Grouped:
+    """Accumulates problems of one grouped GEMM launch (vectorized descriptor build)."""
+
+    def __init__(self, transA, transB):
+        self.tA, self.tB = transA, transB
+        self.rows = []
+
+    def add(self, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, b_rows=0, c_rows=0, c_cols=0, atomic=0):
+        if M > 0 and N > 0:
+            self.rows.append((A, B, C, 0, 0, 0, b_rows, c_rows, c_cols, M, N, K, max(lda, 1), max(ldb, 1),
+                              max(ldc, 1), 1, atomic, alpha, beta))
+
+    def launch(self):
+        if self.rows:
+            E.gemm_grouped(np.array(self.rows, dtype=GEMM_DTYPE), self.tA, self.tB)
+            self.rows = []
+
+
+# ---------------------------------------------------------------------------
+# unit records
+
+
+class InteriorUnit:
+    """Exact subdomain factor L_B (dense triangle) + materialized coupling Y_B."""
+
+    kind = "interior"
+
+    def __init__(self, u, members, c0, c1, off_rows, tri, Y, stored):
+        self.u, self.members, self.c0, self.c1 = u, members, c0, c1
+        self.rows = off_rows
+        self.off_rows = off_rows
+        self.diag = tri
+        self.off = Y
+        self._stored = stored
+
+    @property
+    def ncols(self):
+        return self.c1 - self.c0
+
+
+class NodeUnit:
+    kind = "node"
+
+    def __init__(self, u, j, c0, c1, rows):
+        self.u, self.j, self.c0, self.c1, self.rows = u, j, c0, c1, rows
+        self.diag = None
+        self.off = None
+
+    @property
+    def ncols(self):
+        return self.c1 - self.c0
+
+
+# ---------------------------------------------------------------------------
+# the numeric pass
+
+
+class _Indefinite(Exception):
+    def __init__(self, unit, pivot):
+        self.unit, self.pivot = unit, pivot
+
+
+class NumericPass:
+    """One left-to-right sweep on the device (factor.py:538-639)."""
+
+    def __init__(self, plan, cfg, alpha_d):
+        self.np = plan
+        self.sym = plan.sym
+        self.cfg = cfg
+        self.alpha_d = alpha_d
+        self.counters = {"diag_trees": 0, "compressed_off": 0, "compressed_diag": 0, "dense_fallback": 0}
+        self.units = []
+        self.src_panel = {}  # source id -> (raw tensor, eff tensor)
+        self.ranks = {}
+        self.flops = 0.0
+
+    # -- helpers -----------------------------------------------------------
+    def _info_check(self, info, unit):
+        v = info.cpu().numpy()
+        bad = np.nonzero(v)[0]
+        if bad.size:
+            raise _Indefinite(unit, int(v[bad[0]]) - 1)
+
+    def _potrf(self, M, unit):
+        n = M.shape[0]
+        Dinv = E.empty(max(n, 1), 64)
+        info = E.zeros(1, dtype=E.I32)
+        if n:
+            E.potrf_batched([M.data_ptr()], [n], [E.ld(M)], [Dinv.data_ptr()], info)
+            self._info_check(info, unit)
+        self.flops += n**3 / 3.0
+        return DenseTri(M, Dinv)
+
+    def _dense_from_csr(self, blk, nrows, ncols):
+        D = E.zeros(nrows, ncols)
+        if blk is not None and blk.nnz and nrows and ncols:
+            E.csr_to_dense_batched([blk.indptr_ptr], [blk.indices_ptr], [blk.data_ptr], [blk.nrows],
+                                   [D.data_ptr()], [E.ld(D)])
+        return D
+
+    def _spmm(self, blk, X, Y, alpha=1.0, beta=0.0):
+        if blk is None or blk.nrows == 0 or X.shape[1] == 0:
+            if beta == 0.0:
+                Y.zero_()
+            return
+        lib = E.require_cuda()
+        E.check(lib.rsc_spmm_csr(blk.nrows, int(X.shape[1]), blk.indptr_ptr, blk.indices_ptr, blk.data_ptr,
+                                    X.data_ptr(), E.ld(X), float(alpha), float(beta), Y.data_ptr(), E.ld(Y),
+                                    E.stream_handle()), "rsc_spmm_csr")
+        self.flops += 2.0 * blk.nnz * X.shape[1]
+
+    def _orth(self, G):
+        """Pivoted QR + reference cutoff -> U (m x kept) (kernels.py:67-82)."""
+        m, k = G.shape
+        if m == 0 or k == 0:
+            return E.empty(m, 0)
+        Q = E.empty(m, k)
+        rank = E.zeros(1, dtype=E.I32)
+        work = E.qrcp_batched([G.data_ptr()], [m], [k], [E.ld(G)], [Q.data_ptr()], [E.ld(Q)], rank)
+        kept = int(rank.item())
+        del work
+        self.flops += 4.0 * m * k * k
+        return Q[:, :kept].contiguous()
+
+    def _lowrank(self, V, U):
+        k = U.shape[1]
+        utu = E.empty(k, k)
+        _gemm1(U, U, utu, transA=True)
+        Eff = E.empty(V.shape[0], k)
+        _gemm1(V, utu, Eff)
+        return DevLR(V, U, Eff)
+
+    def _idx(self, off):
+        return self.np.idx.ptr(off)
+
+    # -- interior blocks -----------------------------------------------------
+    def factor_interiors(self):
+        """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
+        Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM."""
+        ints = self.np.interior
+        if not ints:
+            return {}
+        Ls, Ds, Ys = [], [], []
+        for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
+            nb = c1 - c0
+            Ls.append(self._dense_from_csr(A_BB, nb, nb))
+            Ds.append(E.empty(max(nb, 1), 64))
+            Ys.append(self._dense_from_csr(A_off, off_rows.size, nb))
+        info = E.zeros(len(ints), dtype=E.I32)
+        E.potrf_batched([L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
+                        [D.data_ptr() for D in Ds], info)
+        E.trsm_batched("right", 1, [L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
+                       [D.data_ptr() for D in Ds], [Y.data_ptr() for Y in Ys], [Y.shape[0] for Y in Ys],
+                       [E.ld(Y) for Y in Ys])
+        iv = info.cpu().numpy()
+        out = {}
+        self.first_interior_failure = None
+        for i, (u, ids, c0, c1, off_rows, A_off, A_BB) in enumerate(ints):
+            if iv[i] and self.first_interior_failure is None:
+                self.first_interior_failure = (u, int(iv[i]) - 1)
+            nb = c1 - c0
+            stored = (A_off.nnz if A_off is not None else 0)
+            part = self.sym.partition
+            for j in ids:
+                j0, j1 = part.cols(j)
+                ncj = j1 - j0
+                nib = int(np.searchsorted(part.rows[j], c1))
+                stored += ncj * (ncj + 1) // 2 + ncj * nib
+            out[u] = InteriorUnit(u, ids, c0, c1, off_rows, DenseTri(Ls[i], Ds[i]), Ys[i], stored)
+            self.flops += nb**3 / 3.0 + off_rows.size * nb * nb
+        return out
+
+    # -- Schur assembly of a non-tree node (factor.py:372-399) -----------------
+    def assemble(self, node, pairs, want_off, want_diag=True):
+        j = node.j
+        nc = node.ncols
+        A_CC, A_RC, _ = self.np.node_blocks[j]
+        R = node.rows
+        want_off = want_off and R.size > 0
+        UD = self._dense_from_csr(A_CC, nc, nc) if want_diag else None
+        UO = self._dense_from_csr(A_RC, R.size, nc) if want_off else None
+        g = Grouped(False, True)
+        for pr in pairs:
+            raw, eff = self.src_panel[pr.s]
+            w = raw.shape[1]
+            if w == 0 or pr.n_rd == 0:
+                continue
+            ld = E.ld(raw)
+            cpos = self._idx(pr.cpos_off)
+            Q = raw.data_ptr() + 8 * pr.lo * ld
+            if want_diag:
+                g.add(eff.data_ptr() + 8 * pr.lo * ld, ld, Q, ld, UD.data_ptr(), nc, pr.n_rd, pr.n_rd, w,
+                      -1.0, 1.0, c_rows=cpos, c_cols=cpos, atomic=1)
+                self.flops += 2.0 * pr.n_rd * pr.n_rd * w
+            if want_off and pr.n_ro > 0:
+                g.add(eff.data_ptr() + 8 * pr.hi * ld, ld, Q, ld, UO.data_ptr(), nc, pr.n_ro, pr.n_rd, w,
+                      -1.0, 1.0, c_rows=self._idx(pr.rpos_off), c_cols=cpos, atomic=1)
+                self.flops += 2.0 * pr.n_ro * pr.n_rd * w
+        g.launch()
+        return UD, UO
+
+    # -- diagonal solve of node j (dense or tree) ------------------------------
+    @staticmethod
+    def diag_solve(node, X, transpose, s=None):
+        if isinstance(node.diag, DeviceTree):
+            node.diag.solve(X, transpose, s)
+        else:
+            node.diag.solve(X, transpose)
+
+    # -- implicit off-diagonal products (factor.py:427-483) --------------------
+    def off_mul(self, node, pairs, G):
+        """W = L_O G without forming L_O (G: nc x r)."""
+        R = node.rows
+        r = G.shape[1]
+        W = E.empty(R.size, r)
+        if R.size == 0 or r == 0:
+            return W.zero_()
+        G1 = G.clone()
+        self.diag_solve(node, G1, transpose=True)
+        self.flops += node.ncols**2 * r
+        _, A_RC, _ = self.np.node_blocks[node.j]
+        self._spmm(A_RC, G1, W)
+        self._source_products(pairs, G1, W, r, trans=False)
+        return W
+
+    def off_mul_t(self, node, pairs, G):
+        """W = L_O^T G (G: |R| x r), diagonal solve last."""
+        r = G.shape[1]
+        nc = node.ncols
+        W = E.empty(nc, r)
+        if r == 0:
+            return W
+        _, _, A_CR = self.np.node_blocks[node.j]
+        self._spmm(A_CR, G, W)
+        self._source_products(pairs, G, W, r, trans=True)
+        self.diag_solve(node, W, transpose=False)
+        self.flops += nc * nc * r
+        return W
+
+    def _source_products(self, pairs, G, W, r, trans):
+        use = [p for p in pairs if p.n_rd > 0 and p.n_ro > 0 and self.src_panel[p.s][0].shape[1] > 0]
+        if not use:
+            return
+        widths = [self.src_panel[p.s][0].shape[1] for p in use]
+        offs = np.concatenate([[0], np.cumsum(np.asarray(widths) * r)])
+        T = E.empty(int(offs[-1]))
+        g1, g2 = Grouped(True, False), Grouped(False, False)
+        for p, w, o in zip(use, widths, offs[:-1]):
+            raw, eff = self.src_panel[p.s]
+            ld = E.ld(raw)
+            tp = T.data_ptr() + 8 * int(o)
+            cpos, rpos = self._idx(p.cpos_off), self._idx(p.rpos_off)
+            if not trans:
+                # T = V[lo:hi]^T G1[cpos] ; W[rpos] -= E[hi:] T
+                g1.add(raw.data_ptr() + 8 * p.lo * ld, ld, G.data_ptr(), r, tp, r, w, r, p.n_rd, 1.0, 0.0,
+                       b_rows=cpos)
+                g2.add(eff.data_ptr() + 8 * p.hi * ld, ld, tp, r, W.data_ptr(), r, p.n_ro, r, w, -1.0, 1.0,
+                       c_rows=rpos, atomic=1)
+            else:
+                # T = E[hi:]^T G[rpos] ; W[cpos] -= V[lo:hi] T
+                g1.add(eff.data_ptr() + 8 * p.hi * ld, ld, G.data_ptr(), r, tp, r, w, r, p.n_ro, 1.0, 0.0,
+                       b_rows=rpos)
+                g2.add(raw.data_ptr() + 8 * p.lo * ld, ld, tp, r, W.data_ptr(), r, p.n_rd, r, w, -1.0, 1.0,
+                       c_rows=cpos, atomic=1)
+            self.flops += 2.0 * (p.n_rd + p.n_ro) * w * r
+        g1.launch()
+        g2.launch()
+
+    def approx_off(self, node, pairs, rank):
+        """Alg. 3 (factor.py:486-505)."""
+        R = node.rows
+        rank = min(rank, R.size, node.ncols)
+        G = E.to_dev(_gaussian(R.size, rank, _block_seed(self.cfg.seed, 0, node.j)))
+        G = self.off_mul_t(node, pairs, G)
+        for _ in range(self.cfg.power_iters):
+            G = self.off_mul_t(node, pairs, self.off_mul(node, pairs, G))
+        U = self._orth(G)
+        V = self.off_mul(node, pairs, U)
+        return self._lowrank(V, U)
+
+    # -- diagonal trees (diagblocks.py) ----------------------------------------
+    def _path_terms(self, tree, s, rspan, cspan):
+        out = []
+        for p in tree.shape.path_above(s):
+            base = tree.shape.nodes[p].split
+            raw, eff = _raw_eff(tree.blocks[p])
+            out.append((raw, eff, rspan[0] - base, rspan[1] - base, cspan[0] - base, cspan[1] - base))
+        return out
+
+    def factor_leaf(self, node, s):
+        tree = node.diag
+        j = node.j
+        maps, blk, _ = self.np.tree_maps[(j, s)]
+        lf = tree.shape.nodes[s]
+        k = lf.hi - lf.lo
+        U = self._dense_from_csr(blk, k, k)
+        g = Grouped(False, True)
+        for m in maps:
+            raw, eff = self.src_panel[m.s]
+            w = raw.shape[1]
+            if w == 0:
+                continue
+            ld = E.ld(raw)
+            g.add(eff.data_ptr() + 8 * m.rlo * ld, ld, raw.data_ptr() + 8 * m.clo * ld, ld, U.data_ptr(), k,
+                  m.rhi - m.rlo, m.chi - m.clo, w, -1.0, 1.0, c_rows=self._idx(m.ridx_off),
+                  c_cols=self._idx(m.cidx_off), atomic=1)
+            self.flops += 2.0 * (m.rhi - m.rlo) * (m.chi - m.clo) * w
+        for raw, eff, a, b, c, d in self._path_terms(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi)):
+            w = raw.shape[1]
+            if w == 0:
+                continue
+            ld = E.ld(raw)
+            g.add(eff.data_ptr() + 8 * a * ld, ld, raw.data_ptr() + 8 * c * ld, ld, U.data_ptr(), k, b - a,
+                  d - c, w, -1.0, 1.0, atomic=1)
+            self.flops += 2.0 * (b - a) * (d - c) * w
+        g.launch()
+        return self._potrf(U, node.u)
+
+    def diag_mul(self, node, s, G, transpose):
+        """Alg. 5: product of internal tree block s with G (diagblocks.py:303-346)."""
+        tree = node.diag
+        shape = tree.shape
+        blk_nd = shape.nodes[s]
+        (r0, r1), (c0, c1) = shape.span(s)
+        maps, blk, blkT = self.np.tree_maps[(node.j, s)]
+        r = G.shape[1]
+        g1, g2 = Grouped(True, False), Grouped(False, False)
+        terms = []
+        if not transpose:
+            G1 = G.clone()
+            tree.solve(G1, transpose=True, s=blk_nd.left.s)
+            self.flops += (c1 - c0) ** 2 * r
+            W = E.empty(r1 - r0, r)
+            self._spmm(blk, G1, W)
+            src = G1
+        else:
+            W = E.empty(c1 - c0, r)
+            self._spmm(blkT, G, W)
+            src = G
+        for m in maps:
+            raw, eff = self.src_panel[m.s]
+            w = raw.shape[1]
+            if w:
+                terms.append((raw, eff, w, m.clo, m.chi, m.rlo, m.rhi, self._idx(m.cidx_off), self._idx(m.ridx_off)))
+        for raw, eff, a, b, c, d in self._path_terms(tree, s, (r0, r1), (c0, c1)):
+            w = raw.shape[1]
+            if w:
+                terms.append((raw, eff, w, c, d, a, b, 0, 0))
+        if terms:
+            widths = np.array([t[2] for t in terms])
+            offs = np.concatenate([[0], np.cumsum(widths * r)])
+            T = E.empty(int(offs[-1]))
+            for (raw, eff, w, clo, chi, rlo, rhi, cidx, ridx), o in zip(terms, offs[:-1]):
+                ld = E.ld(raw)
+                tp = T.data_ptr() + 8 * int(o)
+                if not transpose:
+                    g1.add(raw.data_ptr() + 8 * clo * ld, ld, src.data_ptr(), r, tp, r, w, r, chi - clo, 1.0, 0.0,
+                           b_rows=cidx)
+                    g2.add(eff.data_ptr() + 8 * rlo * ld, ld, tp, r, W.data_ptr(), r, rhi - rlo, r, w, -1.0, 1.0,
+                           c_rows=ridx, atomic=1)
+                else:
+                    g1.add(eff.data_ptr() + 8 * rlo * ld, ld, src.data_ptr(), r, tp, r, w, r, rhi - rlo, 1.0, 0.0,
+                           b_rows=ridx)
+                    g2.add(raw.data_ptr() + 8 * clo * ld, ld, tp, r, W.data_ptr(), r, chi - clo, r, w, -1.0, 1.0,
+                           c_rows=cidx, atomic=1)
+                self.flops += 2.0 * ((chi - clo) + (rhi - rlo)) * w * r
+            g1.launch()
+            g2.launch()
+        if transpose:
+            tree.solve(W, transpose=False, s=blk_nd.left.s)
+            self.flops += (c1 - c0) ** 2 * r
+        return W
+
+    def approx_diag(self, node, s, rank):
+        (r0, r1), (c0, c1) = node.diag.shape.span(s)
+        rank = min(rank, r1 - r0, c1 - c0)
+        G = E.to_dev(_gaussian(r1 - r0, rank, _block_seed(self.cfg.seed, 1, node.j, s)))
+        G = self.diag_mul(node, s, G, True)
+        for _ in range(self.cfg.power_iters):
+            G = self.diag_mul(node, s, self.diag_mul(node, s, G, False), True)
+        U = self._orth(G)
+        V = self.diag_mul(node, s, U, False)
+        return self._lowrank(V, U)
+
+    def factor_tree(self, node):
+        from .diagtree import TreeShape  # noqa: F401
+
+        shape = self.np.tree_shapes[node.j]
+        tree = DeviceTree(shape)
+        node.diag = tree
+        for s in shape.order:
+            tn = shape.nodes[s]
+            if tn.is_leaf:
+                tree.blocks[s] = self.factor_leaf(node, s)
+                continue
+            nrows, ncols = tn.hi - tn.split, tn.split - tn.lo
+            r = block_rank(nrows, ncols, self.alpha_d, self.cfg.oversample)
+            if r >= DENSE_FALLBACK_FRACTION * min(nrows, ncols):
+                eye = E.zeros(ncols, ncols)
+                eye.fill_diagonal_(1.0)
+                tree.blocks[s] = self.diag_mul(node, s, eye, False)
+                self.counters["dense_fallback"] += 1
+            else:
+                tree.blocks[s] = self.approx_diag(node, s, r)
+                self.ranks[("diag", node.j, s)] = tree.blocks[s].k
+                self.counters["compressed_diag"] += 1
+
+    # -- the sweep -------------------------------------------------------------
+    def run(self):
+        part = self.sym.partition
+        cfg = self.cfg
+        interiors = self.factor_interiors()
+        fail = self.first_interior_failure
+        for u, (kind, payload) in enumerate(self.sym.units):
+            if fail is not None and u >= fail[0]:
+                raise _Indefinite(*fail)
+            if kind == "interior":
+                iu = interiors[u]
+                self.units.append(iu)
+                sid = self.np.unit_source.get(u)
+                if sid is not None:
+                    self.src_panel[sid] = (iu.off, iu.off)
+                continue
+            j = payload
+            c0, c1 = part.cols(j)
+            nc = c1 - c0
+            R = part.rows[j]
+            pairs = self.np.targets[j]
+            compress = bool(part.is_separator[j])
+            node = NodeUnit(u, j, c0, c1, R)
+            tree_diag = compress and j in self.sym.sep_splits
+            r_off = block_rank(R.size, nc, cfg.alpha_o, cfg.oversample)
+            compress_off = bool(compress and R.size and r_off < DENSE_FALLBACK_FRACTION * min(R.size, nc))
+            UO = None
+            if tree_diag:
+                self.counters["diag_trees"] += 1
+                self.factor_tree(node)
+            else:
+                UD, UO = self.assemble(node, pairs, want_off=not compress_off)
+                node.diag = self._potrf(UD, u)
+            if R.size == 0:
+                node.off = None
+            elif compress_off:
+                node.off = self.approx_off(node, pairs, r_off)
+                self.ranks[("off", j)] = node.off.k
+                self.counters["compressed_off"] += 1
+            else:
+                if compress:
+                    self.counters["dense_fallback"] += 1
+                if tree_diag:
+                    _, UO = self.assemble(node, pairs, want_off=True, want_diag=False)
+                    X = UO.t().contiguous()
+                    node.diag.solve(X, transpose=False)
+                    node.off = X.t().contiguous()
+                else:
+                    E.trsm_batched("right", 1, [node.diag.L.data_ptr()], [nc], [E.ld(node.diag.L)],
+                                   [node.diag.Dinv.data_ptr()], [UO.data_ptr()], [UO.shape[0]], [E.ld(UO)])
+                    node.off = UO
+                self.flops += R.size * nc * nc
+            self.units.append(node)
+            sid = self.np.unit_source.get(u)
+            if sid is not None:
+                raw, eff = _raw_eff(node.off)
+                self.src_panel[sid] = (raw, eff)
+
+
+# ---------------------------------------------------------------------------
+# factor container
+
+
+class RankStructuredFactor:
+    """Approximate Cholesky factor resident on the B200, applied as an SPD
+    preconditioner (factor.py:155-310)."""
+
+    def __init__(self, n, sym, plan, config):
+        self.n = n
+        self.sym = sym
+        self.plan = plan
+        self.perm = sym.perm
+        self.partition = sym.partition
+        self.config = config
+        self.units = []
+        self.ranks = {}
+        self.stats = FactorStats(n=n, seed=config.seed)
+        self._apply = None
+
+    # -- application -----------------------------------------------------------
+    def apply(self, r):
+        """z = P^T (L L^T)^{-1} P r (host vector in, host vector out)."""
+        r = np.asarray(r, dtype=np.float64)
+        if r.shape != (self.n,):
+            raise DimensionMismatch(f"expected vector of length {self.n}")
+        y = E.to_dev(r)
+        z = self.apply_device(y)
+        return z.cpu().numpy()
+
+    __call__ = apply
+
+    def apply_device(self, r_dev, out=None):
+        from .apply import DeviceApply
+
+        if self._apply is None:
+            self._apply = DeviceApply(self)
+        return self._apply(r_dev, out)
+
+    # -- inspection ------------------------------------------------------------
+    def stored_scalars(self):
+        total = 0
+        for un in self.units:
+            if un.kind == "interior":
+                total += un._stored
+                continue
+            nc = un.ncols
+            if isinstance(un.diag, DeviceTree):
+                for s, nd in un.diag.shape.nodes.items():
+                    b = un.diag.blocks[s]
+                    if nd.is_leaf:
+                        k = nd.hi - nd.lo
+                        total += k * (k + 1) // 2
+                    elif isinstance(b, DevLR):
+                        total += b.V.numel() + b.U.numel()
+                    else:
+                        total += b.numel()
+            else:
+                total += nc * (nc + 1) // 2
+            if isinstance(un.off, DevLR):
+                total += un.off.V.numel() + un.off.U.numel()
+            elif un.off is not None:
+                total += un.off.numel()
+        return total
+
+    def _diag_dense(self, un):
+        if isinstance(un.diag, DeviceTree):
+            shape = un.diag.shape
+            Ld = np.zeros((un.ncols, un.ncols))
+            for s, nd in shape.nodes.items():
+                (r0, r1), (c0, c1) = shape.span(s)
+                b = un.diag.blocks[s]
+                if nd.is_leaf:
+                    Ld[r0:r1, c0:c1] = np.tril(b.L.cpu().numpy())
+                elif isinstance(b, DevLR):
+                    Ld[r0:r1, c0:c1] = b.V.cpu().numpy() @ b.U.cpu().numpy().T
+                else:
+                    Ld[r0:r1, c0:c1] = b.cpu().numpy()
+            return Ld
+        return np.tril(un.diag.L.cpu().numpy())
+
+    def _off_dense(self, un):
+        if isinstance(un.off, DevLR):
+            return un.off.V.cpu().numpy() @ un.off.U.cpu().numpy().T
+        return un.off.cpu().numpy()
+
+    def dense_lower(self):
+        """Explicit lower-triangular factor (small problems, testing)."""
+        L = np.zeros((self.n, self.n))
+        for un in self.units:
+            L[un.c0:un.c1, un.c0:un.c1] = self._diag_dense(un)
+            if un.rows.size and un.off is not None:
+                L[un.rows, un.c0:un.c1] = self._off_dense(un)
+        return L
+
+    def to_scipy_lower(self):
+        import scipy.sparse as sp
+
+        rows, cols, vals = [], [], []
+        for un in self.units:
+            cr = np.arange(un.c0, un.c1)
+            for blk, rr in ((self._diag_dense(un), cr),
+                            (self._off_dense(un) if (un.rows.size and un.off is not None) else None, un.rows)):
+                if blk is None:
+                    continue
+                a, b = np.nonzero(blk)
+                rows.append(rr[a])
+                cols.append(cr[b])
+                vals.append(blk[a, b])
+        if not rows:
+            return sp.csc_matrix((self.n, self.n))
+        return sp.csc_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                             shape=(self.n, self.n))
+
+
+def factorize(A, config=None, coords=None):
+    """Order, analyze and factor A on the B200 (factor.py:642-740).
+
+    Same contract as rschol.factorize: ordering/symbolic on the host, the numeric
+    sweep on the device, restart with alpha_d *= alpha_d_growth on an indefinite
+    pivot once a diagonal tree is in play, TooManyRestarts after max_restarts.
+    """
+    E.require_cuda()
+    A = as_spd(A)
+    config = config if config is not None else SolverConfig()
+    t0 = time.perf_counter()
+    sym = analyze(A, config.tau_o, config.tau_d, config.interior_blocks, coords=coords)
+    t_plan0 = time.perf_counter()
+    plan = NumericPlan(sym, config.interior_blocks)
+    t2 = time.perf_counter()
+    from . import _lib
+
+    lib = _lib.load()
+    launches0 = int(lib.rsc_launch_counter(0))
+    alpha_d = config.alpha_d
+    history = [alpha_d]
+    restarts = 0
+    while True:
+        ps = NumericPass(plan, config, alpha_d)
+        try:
+            ps.run()
+            torch.cuda.current_stream().synchronize()
+            break
+        except _Indefinite as e:
+            if ps.counters["diag_trees"] == 0:
+                raise IndefiniteError(e.pivot) from None
+            restarts += 1
+            if restarts > config.max_restarts:
+                raise TooManyRestarts(
+                    f"still indefinite after {config.max_restarts} restarts (alpha_d reached {alpha_d:g})"
+                ) from None
+            alpha_d *= config.alpha_d_growth
+            history.append(alpha_d)
+    t3 = time.perf_counter()
+    F = RankStructuredFactor(A.n, sym, plan, config)
+    F.units = ps.units
+    F.ranks = ps.ranks
+    part = sym.partition
+    st = F.stats
+    st.n, st.nnz_lower = A.n, A.nnz_lower
+    st.supernodes = part.count
+    st.separator_supernodes = int(part.is_separator.sum())
+    st.interior_block_count = len(plan.interior)
+    st.compressed_offdiag = ps.counters["compressed_off"]
+    st.compressed_diag = ps.counters["compressed_diag"]
+    st.dense_fallback = ps.counters["dense_fallback"]
+    st.stored_scalars = F.stored_scalars()
+    st.restarts = restarts
+    st.alpha_d_final = alpha_d
+    st.alpha_d_history = history
+    st.gpu_launches = int(lib.rsc_launch_counter(0)) - launches0
+    st.model_gflop = ps.flops / 1e9
+    st.phase_times = {"ordering": sym.t_ordering, "symbolic": sym.t_symbolic + (t2 - t_plan0),
+                      "numeric": t3 - t2, "total": t3 - t0}
+    return F

@@ -1,0 +1,240 @@
+"""Plan compiler: flattens the symbolic plan into the static index data the GPU
+numeric phase consumes, uploaded once.
+
+Everything the reference recomputes on every call is a function of the symbolic
+structure alone, so it is computed here once (SURVEY §7 "Plan"):
+
+  * the update sources of every compressed supernode j, in reference order
+    (the bucket walk of factor.py:545-554,572 visits exactly the sources whose row
+    set meets C_j, sorted by their first column);
+  * per (source, target) pair the descendant map of symbolic.py:309-356:
+    lo/hi = searchsorted(rows_s, (c0, c1)), cpos = rows_s[lo:hi] - c0 and
+    rpos = searchsorted(R_j, rows_s[hi:])  (factor.py:389-398, 450-455, 477-482);
+  * the A blocks A(C_j, C_j), A(R_j, C_j), A(C_j, R_j) as device CSR blocks
+    (factor.py:378-379, 444, 471);
+  * interior blocks' off_rows (interior.py:152-154) -- these are structural.
+
+Interior blocks are materialized: Y_B = A(off_rows, C_B) L_B^{-T} is formed once,
+which turns every interior source into a dense panel (exactly the operator
+L(rows, C_B) of interior.py:77-95; rows outside off_rows are exact zeros).
+"""
+
+import numpy as np
+import torch
+
+from . import engine as E
+
+
+class Source:
+    """One update source: an interior block (rows = off_rows) or a compressed
+    supernode (rows = R_j).  `order` is its first column (factor.py:565,639)."""
+
+    __slots__ = ("sid", "kind", "unit", "rows", "order", "c0", "c1")
+
+    def __init__(self, sid, kind, unit, rows, c0, c1):
+        self.sid, self.kind, self.unit = sid, kind, unit
+        self.rows = rows
+        self.order = c0
+        self.c0, self.c1 = c0, c1
+
+
+class Pair:
+    """Descendant map of source s into target supernode j."""
+
+    __slots__ = ("s", "lo", "hi", "n_rd", "n_ro", "cpos_off", "rpos_off")
+
+    def __init__(self, s, lo, hi, cpos_off, rpos_off, nrows):
+        self.s = s
+        self.lo, self.hi = lo, hi
+        self.n_rd = hi - lo
+        self.n_ro = nrows - hi
+        self.cpos_off, self.rpos_off = cpos_off, rpos_off
+
+
+class IndexPool:
+    """Host accumulator of int32 index arrays, uploaded as one device buffer."""
+
+    def __init__(self):
+        self.chunks = []
+        self.size = 0
+
+    def add(self, arr):
+        arr = np.asarray(arr, dtype=np.int32)
+        off = self.size
+        if arr.size:
+            self.chunks.append(arr)
+            self.size += arr.size
+        return off
+
+    def upload(self):
+        host = np.concatenate(self.chunks) if self.chunks else np.zeros(1, np.int32)
+        self.host = host
+        self.dev = E.to_dev(host)
+        return self.dev
+
+    def ptr(self, off):
+        return self.dev.data_ptr() + 4 * int(off)
+
+
+class CsrPool:
+    """Many small CSR blocks in three device buffers (rowptr int32 per block,
+    colidx int32, values f64)."""
+
+    def __init__(self):
+        self.rp, self.ci, self.v = [], [], []
+        self.nrp = self.nnz = 0
+
+    def add(self, S):
+        S = S.tocsr()
+        S.sort_indices()
+        rp_off, nz_off = self.nrp, self.nnz
+        self.rp.append(S.indptr.astype(np.int32))
+        self.ci.append(S.indices.astype(np.int32))
+        self.v.append(S.data.astype(np.float64))
+        self.nrp += S.shape[0] + 1
+        self.nnz += S.nnz
+        return CsrBlock(self, S.shape[0], S.shape[1], rp_off, nz_off, S.nnz)
+
+    def upload(self):
+        self.rp_dev = E.to_dev(np.concatenate(self.rp) if self.rp else np.zeros(1, np.int32))
+        self.ci_dev = E.to_dev(np.concatenate(self.ci) if self.ci else np.zeros(1, np.int32))
+        self.v_dev = E.to_dev(np.concatenate(self.v) if self.v else np.zeros(1))
+
+
+class CsrBlock:
+    """View of one block of a CsrPool (rowptr entries are block-local offsets)."""
+
+    def __init__(self, pool, nrows, ncols, rp_off, nz_off, nnz):
+        self.pool, self.nrows, self.ncols = pool, nrows, ncols
+        self.rp_off, self.nz_off, self.nnz = rp_off, nz_off, nnz
+
+    @property
+    def indptr_ptr(self):
+        return self.pool.rp_dev.data_ptr() + 4 * self.rp_off
+
+    @property
+    def indices_ptr(self):
+        return self.pool.ci_dev.data_ptr() + 4 * self.nz_off
+
+    @property
+    def data_ptr(self):
+        return self.pool.v_dev.data_ptr() + 8 * self.nz_off
+
+
+class TreeBlockMaps:
+    """Window maps of one source into one diagonal-tree block (diagblocks.py:230-262):
+    rows of the source inside the row window [r0,r1) and column window [c0,c1)."""
+
+    __slots__ = ("s", "clo", "chi", "rlo", "rhi", "cidx_off", "ridx_off")
+
+
+class NumericPlan:
+    """Static device-side plan for the numeric phase of one symbolic plan."""
+
+    def __init__(self, sym, interior_enabled):
+        self.sym = sym
+        part = sym.partition
+        B = sym.B
+        full = B.to_csr_full()
+        self.full = full
+        self.idx = IndexPool()
+        self.csr = CsrPool()
+        self.sources = []
+        self.unit_source = {}      # unit index -> source id
+        self.targets = {}          # node j -> [Pair] (reference order)
+        self.node_blocks = {}      # node j -> (A_CC, A_RC, A_CR)
+        self.rows_off = {}         # node j / ("int", u) -> index offset of its row set
+        self.interior = []         # (unit index, members, c0, c1, off_rows, A_off csr, A_BB csr)
+        supernode_of = lambda cols: np.searchsorted(part.starts, cols, side="right") - 1
+
+        touched = {}  # j -> list of source ids
+        for u, (kind, payload) in enumerate(sym.units):
+            if kind == "interior":
+                ids = payload
+                c0, c1 = int(part.starts[ids[0]]), int(part.starts[ids[-1] + 1])
+                tails = []
+                for j in ids:
+                    rj = part.rows[j]
+                    nib = int(np.searchsorted(rj, c1))
+                    if rj.size > nib:
+                        tails.append(rj[nib:])
+                off_rows = np.unique(np.concatenate(tails)) if tails else np.empty(0, np.int64)
+                A_BB = self.csr.add(full[c0:c1, c0:c1])
+                A_off = self.csr.add(full[off_rows, c0:c1]) if off_rows.size else None
+                roff = self.idx.add(off_rows)
+                self.rows_off[("int", u)] = roff
+                self.interior.append((u, ids, c0, c1, off_rows, A_off, A_BB))
+                if off_rows.size:
+                    sid = len(self.sources)
+                    self.sources.append(Source(sid, "interior", u, off_rows, c0, c1))
+                    self.unit_source[u] = sid
+                continue
+            j = payload
+            c0, c1 = part.cols(j)
+            R = part.rows[j]
+            self.targets[j] = []
+            A_CC = self.csr.add(full[c0:c1, c0:c1])
+            A_RC = self.csr.add(full[R, c0:c1]) if R.size else None
+            A_CR = self.csr.add(full[R, c0:c1].T.tocsr()) if R.size else None
+            self.node_blocks[j] = (A_CC, A_RC, A_CR)
+            self.rows_off[j] = self.idx.add(R)
+            if R.size:
+                sid = len(self.sources)
+                self.sources.append(Source(sid, "node", u, R, c0, c1))
+                self.unit_source[u] = sid
+        # every supernode a source's rows fall into is a target of that source
+        for src in self.sources:
+            for j in np.unique(supernode_of(src.rows)):
+                touched.setdefault(int(j), []).append(src.sid)
+        self._build_targets(part, touched)
+        self.tree_maps = {}
+        self._build_tree_maps(part)
+        self.idx.upload()
+        self.csr.upload()
+
+    def _build_targets(self, part, touched):
+        for j in list(self.targets):
+            c0, c1 = part.cols(j)
+            R = part.rows[j]
+            pairs = []
+            for sid in touched.get(j, []):
+                src = self.sources[sid]
+                rows = src.rows
+                lo, hi = np.searchsorted(rows, (c0, c1))
+                if lo == hi:
+                    continue
+                cpos = rows[lo:hi] - c0
+                rpos = np.searchsorted(R, rows[hi:])
+                pairs.append(Pair(sid, int(lo), int(hi), self.idx.add(cpos), self.idx.add(rpos), rows.size))
+            pairs.sort(key=lambda p: self.sources[p.s].order)
+            self.targets[j] = pairs
+
+    def _build_tree_maps(self, part):
+        """Window maps for every (tree node j, block s, source) with both windows
+        non-empty (diagblocks.py:231-234, 252-255), plus the A windows."""
+        from .diagtree import TreeShape
+
+        self.tree_shapes = {}
+        for j, split in self.sym.sep_splits.items():
+            c0, c1 = part.cols(j)
+            shape = TreeShape(c1 - c0, c0, split)
+            self.tree_shapes[j] = shape
+            for s in shape.order:
+                (r0, r1), (cc0, cc1) = shape.span(s)
+                gr0, gr1, gc0, gc1 = c0 + r0, c0 + r1, c0 + cc0, c0 + cc1
+                maps = []
+                for pr in self.targets[j]:
+                    rows = self.sources[pr.s].rows
+                    clo, chi = np.searchsorted(rows, (gc0, gc1))
+                    rlo, rhi = np.searchsorted(rows, (gr0, gr1))
+                    if clo == chi or rlo == rhi:
+                        continue
+                    m = TreeBlockMaps()
+                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(clo), int(chi), int(rlo), int(rhi)
+                    m.cidx_off = self.idx.add(rows[clo:chi] - gc0)
+                    m.ridx_off = self.idx.add(rows[rlo:rhi] - gr0)
+                    maps.append(m)
+                win = self.full[gr0:gr1, gc0:gc1]
+                blk = self.csr.add(win)
+                blkT = self.csr.add(win.T.tocsr()) if (gr0, gr1) != (gc0, gc1) else None
+                self.tree_maps[(j, s)] = (maps, blk, blkT)
