@@ -347,6 +347,7 @@ class NumericPass:
         """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
         Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM."""
         ints = self.np.interior
+        self.first_interior_failure = None
         if not ints:
             return {}
         Ls, Ds, Ys = [], [], []
