@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--config", type=int, default=1)
     p.add_argument("--nb", type=int, default=512)
     p.add_argument("--chunk", type=int, default=None, help="supernodes per grouped launch (default: all)")
+    p.add_argument("--grid", type=int, default=None, help="grid size override for sparse configs")
     p.add_argument("--cpu-sample", type=int, default=48, help="blocks in the CPU baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()

@@ -1,0 +1,158 @@
+"""bench.py --config 0|2|3|4: factor + PCG to rel-res 1e-6 on a sparse config.
+
+value   = device-timed numeric factorization + PCG (symbolic plan prepared, A and b
+          resident in HBM) in seconds -- the BASELINE metric "factor+PCG time".
+e2e     = the public API end to end: factorize(A, config, coords) (host ordering +
+          symbolic + plan upload + numeric) and pcg_solve(A, b) with host b in and
+          host x out.
+cpu_baseline = the oracle (the reference algorithm restated on scipy/LAPACK) on a
+          bounded sample -- the same generator at a smaller grid -- with the time
+          extrapolated to the full config by the ratio of modeled work.
+"""
+
+import json
+import os
+import time
+
+import numpy as np
+
+KNOBS = dict(tau_o=32, oversample=10, alpha_o=1.0, alpha_d=0.5, tau_d=256, power_iters=1, seed=0,
+             interior_blocks=True, max_restarts=10)
+METRIC = "factor+PCG time to rel-res 1e-6 (s); factor GFLOP/s as % of FP64 TC peak"
+GRID = {0: 128, 2: 64, 3: 96, 4: 65}
+SAMPLE_GRID = {0: 128, 2: 32, 3: 32, 4: 21}
+NAMES = {0: "config[0] 2D Laplacian 128^2", 2: "config[2] 3D Laplacian 64^3",
+         3: "config[3] 3D lognormal FV diffusion 96^3", 4: "config[4] 3D elasticity 64^3 elements (zeros stripped)"}
+
+
+def _problem(cfg, grid):
+    from paper_1507_05593_b200.problems import diffusion_fv_3d, elasticity_3d, laplacian_2d, laplacian_3d
+
+    if cfg == 0:
+        return laplacian_2d(grid)
+    if cfg == 2:
+        return laplacian_3d(grid)
+    if cfg == 3:
+        return diffusion_fv_3d(grid)
+    return elasticity_3d(grid, strip_zeros=True)
+
+
+def cpu_sample(cfg, grid):
+    """Oracle factor+PCG on the sample grid; returns (seconds, n, iterations)."""
+    try:
+        import threadpoolctl
+
+        threadpoolctl.threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:
+        pass
+    from oracle import numeric as on
+
+    A, coords = _problem(cfg, grid)
+    b = np.random.default_rng(0).standard_normal(A.n)
+    t0 = time.perf_counter()
+    F = on.factorize(A, on.Config(**KNOBS), coords=coords)
+    x, rep = on.pcg(A, b, F, tol=1e-6)
+    return time.perf_counter() - t0, A.n, rep.iterations
+
+
+def run_sparse(args, rank, world, torch, dist):
+    from paper_1507_05593_b200 import _lib
+    from paper_1507_05593_b200 import engine as E
+    from paper_1507_05593_b200.factor import SolverConfig, factorize, prepare
+    from paper_1507_05593_b200.pcg import pcg_solve, pcg_solve_device
+
+    import bench as B
+
+    cfg = args.config
+    lib = _lib.load()
+    A, coords = _problem(cfg, args.grid or GRID[cfg])
+    n = A.n
+    b = np.random.default_rng(0).standard_normal(n)
+    conf = SolverConfig(**KNOBS)
+    t_prep0 = time.perf_counter()
+    prep = prepare(A, conf, coords)
+    t_prep = time.perf_counter() - t_prep0
+    bd = E.to_dev(b)
+    A.device_csr()
+
+    def step():
+        F = factorize(A, prepared=prep)
+        x, rep = pcg_solve_device(A, bd, preconditioner=F, tol=1e-6)
+        return F, rep
+
+    for _ in range(max(args.warmup, 1)):
+        F, rep = step()
+    torch.cuda.synchronize()
+    with B.ClockSampler(torch.cuda.current_device()) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        lib.rsc_launch_counter(1)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tf = []
+        ev0.record()
+        for _ in range(args.steps):
+            F, rep = step()
+            tf.append(F.stats.phase_times["numeric"])
+        ev1.record()
+        torch.cuda.synchronize()
+        launches = int(lib.rsc_launch_counter(1))
+        if dist is not None:
+            dist.barrier()
+    t = ev0.elapsed_time(ev1) * 1e-3 / args.steps
+    if dist is not None:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    work = F.stats.model_gflop
+    # dominant kernel: the grouped DMMA GEMM, timed per launch with CUDA events
+    E.PROFILE = E.KernelProfile()
+    step()
+    prof = E.PROFILE.summary()
+    E.PROFILE = None
+    peak = B.fp64_peak_tflops(torch)
+    # end to end through the public API (host A, coords, b in; host x out)
+    t0 = time.perf_counter()
+    for _ in range(max(1, min(args.steps, 2))):
+        F2 = factorize(A, conf, coords=coords)
+        x, rep2 = pcg_solve(A, b, preconditioner=F2, tol=1e-6)
+    te = (time.perf_counter() - t0) / max(1, min(args.steps, 2))
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sg = SAMPLE_GRID[cfg]
+        ts, ns, its = cpu_sample(cfg, sg)
+        # modeled-work ratio from the GPU work counter on both sizes
+        if sg != (args.grid or GRID[cfg]):
+            As, cs = _problem(cfg, sg)
+            Fs = factorize(As, conf, coords=cs)
+            ratio = work / max(Fs.stats.model_gflop, 1e-12)
+        else:
+            ratio = 1.0
+        cpu = {"value": ts * ratio, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle factor+PCG on grid {sg} (n={ns}, {its} PCG its) took {ts:.1f} s; scaled by the "
+                         f"modeled-work ratio {ratio:.1f} to the full config"}
+    line = {
+        "metric": METRIC, "value": t, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 1), "ms_per_step": 1e3 * t, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator; reference PCG64 sketches)",
+        "config": {"workload": NAMES[cfg], "n": n, "nnz_lower": A.nnz_lower, "knobs": KNOBS, "tol": 1e-6,
+                   "pcg_iterations": rep.iterations, "final_relres": rep.relative_residual,
+                   "numeric_factor_s": float(np.median(tf)), "symbolic_prepare_s": t_prep,
+                   "modeled_gflop": work, "factor_gflops": work / float(np.median(tf)),
+                   "restarts": F.stats.restarts, "compressed_offdiag": F.stats.compressed_offdiag,
+                   "compressed_diag": F.stats.compressed_diag, "stored_scalars": F.stats.stored_scalars},
+        "roofline": {"bound": "tensor", "achieved": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12,
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12 / peak, "traffic": None,
+                     "kernel": "gemm_grouped_kernel (all grouped GEMM launches of one factor+PCG)",
+                     "kernel_seconds": prof["seconds"], "kernel_share_of_step": prof["seconds"] / t,
+                     "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(8 * (A.nnz_lower * 2 + n)),
+                "d2h_bytes_per_step": int(8 * n)},
+        "gpu_launches": launches // args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)

@@ -63,14 +63,39 @@ def gemm_problems(n):
     return np.zeros(n, dtype=GEMM_DTYPE)
 
 
+class KernelProfile:
+    """Optional CUDA-event timing of every grouped-GEMM launch (bench.py roofline):
+    records (start, end, flops) with flops = sum of 2 M N K * batch of the launch."""
+
+    def __init__(self):
+        self.records = []
+
+    def summary(self):
+        torch.cuda.synchronize()
+        t = sum(s.elapsed_time(e) for s, e, _ in self.records) * 1e-3
+        f = sum(fl for _, _, fl in self.records)
+        return {"launch_groups": len(self.records), "seconds": t, "flops": f}
+
+
+PROFILE = None
+
+
 def gemm_grouped(probs, transA=False, transB=False):
     """Launch a grouped DMMA GEMM from a GEMM_DTYPE numpy array of problems."""
     lib = require_cuda()
     probs = np.ascontiguousarray(probs, dtype=GEMM_DTYPE)
     if probs.size == 0:
         return
+    prof = PROFILE
+    if prof is not None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
     check(lib.rsc_gemm_grouped(int(transA), int(transB), addr(probs), int(probs.size), stream_handle()),
           "rsc_gemm_grouped")
+    if prof is not None:
+        e.record()
+        fl = float(np.sum(2.0 * probs["M"].astype(np.float64) * probs["N"] * probs["K"] * probs["batch"]))
+        prof.records.append((s, e, fl))
 
 
 def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):

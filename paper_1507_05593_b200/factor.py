@@ -789,21 +789,36 @@ class RankStructuredFactor:
                              shape=(self.n, self.n))
 
 
-def factorize(A, config=None, coords=None):
+def prepare(A, config=None, coords=None):
+    """Host half of factorize: ordering + symbolic + device plan upload.  The
+    result can be reused by factorize(..., prepared=...) for repeated numeric
+    factorizations of matrices with the same pattern (quasi-static load steps)."""
+    E.require_cuda()
+    A = as_spd(A)
+    config = config if config is not None else SolverConfig()
+    t0 = time.perf_counter()
+    sym = analyze(A, config.tau_o, config.tau_d, config.interior_blocks, coords=coords)
+    t1 = time.perf_counter()
+    plan = NumericPlan(sym, config.interior_blocks)
+    t2 = time.perf_counter()
+    return (sym, plan, config, t0, t1, t2)
+
+
+def factorize(A, config=None, coords=None, prepared=None):
     """Order, analyze and factor A on the B200 (factor.py:642-740).
 
     Same contract as rschol.factorize: ordering/symbolic on the host, the numeric
     sweep on the device, restart with alpha_d *= alpha_d_growth on an indefinite
     pivot once a diagonal tree is in play, TooManyRestarts after max_restarts.
     """
-    E.require_cuda()
     A = as_spd(A)
-    config = config if config is not None else SolverConfig()
-    t0 = time.perf_counter()
-    sym = analyze(A, config.tau_o, config.tau_d, config.interior_blocks, coords=coords)
-    t_plan0 = time.perf_counter()
-    plan = NumericPlan(sym, config.interior_blocks)
-    t2 = time.perf_counter()
+    if prepared is None:
+        prepared = prepare(A, config, coords)
+        sym, plan, config, t0, t_plan0, t2 = prepared
+    else:
+        sym, plan, config, _, _, _ = prepared
+        t0 = t_plan0 = t2 = time.perf_counter()
+        sym.t_ordering = sym.t_symbolic = 0.0
     from . import _lib
 
     lib = _lib.load()
