@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
             }
-            if (lane == 0) piv_s = bi;
+            if (lane == 0) piv_s = (bi < k) ? bi : i;  // NaN norms (failed upstream pivot): no swap
         }
         __syncthreads();
         const int p = piv_s;

@@ -37,6 +37,65 @@ def zeros(*shape, dtype=F64):
     return torch.zeros(*shape, dtype=dtype, device=dev())
 
 
+class Arena:
+    """Bump allocator over large FP64 device chunks.
+
+    The numeric pass creates tens of thousands of small blocks; carving them out of
+    a few big allocations keeps cudaMalloc (and its implicit device syncs) off the
+    critical path.  Single-stream use only: memory handed out again after
+    reset() is reused by kernels that are stream-ordered after the earlier ones.
+    """
+
+    ALIGN = 32  # doubles (256 B)
+
+    def __init__(self, chunk_elems=1 << 25):
+        self.chunk = int(chunk_elems)
+        self.chunks = []
+        self.i = 0
+        self.off = 0
+
+    def empty(self, *shape):
+        n = 1
+        for s in shape:
+            n *= int(s)
+        need = max(-(-n // self.ALIGN) * self.ALIGN, self.ALIGN)
+        while True:
+            if self.i < len(self.chunks):
+                buf = self.chunks[self.i]
+                if self.off + need <= buf.numel():
+                    t = buf[self.off:self.off + n].view(*shape) if n else buf[:0].view(*shape)
+                    self.off += need
+                    return t
+                self.i += 1
+                self.off = 0
+                continue
+            self.chunks.append(torch.empty(max(self.chunk, need), dtype=F64, device=dev()))
+
+    def zeros(self, *shape):
+        t = self.empty(*shape)
+        if t.numel():
+            t.zero_()
+        return t
+
+    def reset(self):
+        self.i = 0
+        self.off = 0
+
+    @property
+    def reserved_bytes(self):
+        return 8 * sum(c.numel() for c in self.chunks)
+
+
+SCRATCH = None
+
+
+def scratch(*shape):
+    """Transient FP64 buffer: from the active scratch arena, else torch's allocator."""
+    if SCRATCH is not None:
+        return SCRATCH.empty(*shape)
+    return empty(*shape)
+
+
 def to_dev(a, dtype=None):
     t = torch.as_tensor(np.ascontiguousarray(a))
     if dtype is not None:
@@ -207,15 +266,17 @@ def trsm_batched(side, trans, Lptrs, n, ldl, dinv_ptrs, Bptrs, m, ldb):
 # QRCP
 
 
-def qrcp_batched(Gptrs, m, k, ldg, Qptrs, ldq, rank_out):
-    """Column-pivoted QR + cutoff; rank_out is a device int32 tensor (len = count)."""
+def qrcp_batched(Gptrs, m, k, ldg, Qptrs, ldq, rank_out, alloc=None):
+    """Column-pivoted QR + cutoff; rank_out is a device int32 tensor (len = count).
+    `alloc(n)` provides the FP64 workspace (default: torch allocator)."""
     lib = require_cuda()
     Gptrs, m, k, ldg = ptr_array(Gptrs), int_array(m), int_array(k), int_array(ldg)
     Qptrs, ldq = ptr_array(Qptrs), int_array(ldq)
     if m.size == 0:
         return
     wbytes = int(lib.rsc_qrcp_workspace_bytes(int(m.size), addr(m), addr(k)))
-    work = torch.empty(max(wbytes // 8, 1), dtype=F64, device=dev())
+    nw = max(wbytes // 8, 1)
+    work = alloc(nw) if alloc is not None else torch.empty(nw, dtype=F64, device=dev())
     check(lib.rsc_qrcp_batched(int(m.size), addr(Gptrs), addr(m), addr(k), addr(ldg), addr(Qptrs),
                                addr(ldq), rank_out.data_ptr(), work.data_ptr(), stream_handle()),
           "rsc_qrcp_batched")

@@ -189,7 +189,7 @@ def _couple_sub(b, X, Y, transpose):
     if isinstance(b, DevLR):
         if b.k == 0:
             return
-        t = E.empty(b.k, r)
+        t = E.scratch(b.k, r)
         if transpose:  # U (V^T X)
             _gemm1(b.V, X, t, transA=True)
             _gemm1(b.U, t, Y, alpha=-1.0, beta=1.0)
@@ -265,8 +265,8 @@ class NodeUnit:
 
 
 class _Indefinite(Exception):
-    def __init__(self, unit, pivot):
-        self.unit, self.pivot = unit, pivot
+    def __init__(self, unit, pivot, trees=0):
+        self.unit, self.pivot, self.trees = unit, pivot, trees
 
 
 class NumericPass:
@@ -282,26 +282,45 @@ class NumericPass:
         self.src_panel = {}  # source id -> (raw tensor, eff tensor)
         self.ranks = {}
         self.flops = 0.0
+        self.P = E.Arena()            # factor blocks (persist with the factor)
+        self.S = E.Arena(1 << 24)     # per-unit transients, reset at every unit
+        nints = 4 * (len(self.sym.units) + sum(len(t.nodes) for t in plan.tree_shapes.values())) + 64
+        self.ibuf = E.zeros(nints, dtype=E.I32)  # POTRF info words + QR ranks
+        self.ipos = 0
+        self.pending = []             # (info offset, count, unit, diag trees started so far)
+        self.sketches = plan.sketches_for(cfg, alpha_d)
 
     # -- helpers -----------------------------------------------------------
-    def _info_check(self, info, unit):
-        v = info.cpu().numpy()
-        bad = np.nonzero(v)[0]
-        if bad.size:
-            raise _Indefinite(unit, int(v[bad[0]]) - 1)
+    def _ints(self, n):
+        t = self.ibuf[self.ipos:self.ipos + n]
+        self.ipos += n
+        return t
+
+    def check_pivots(self):
+        """Deferred POTRF info check: raise for the earliest failing unit in sweep
+        order, with the diagonal-tree count as of that unit (factor.py:705-710)."""
+        if not self.pending:
+            return
+        info = self.ibuf[: self.ipos].cpu().numpy()
+        for off, cnt, unit, trees in self.pending:
+            v = info[off:off + cnt]
+            bad = np.nonzero(v)[0]
+            if bad.size:
+                raise _Indefinite(unit, int(v[bad[0]]) - 1, trees)
+        self.pending = []
 
     def _potrf(self, M, unit):
         n = M.shape[0]
-        Dinv = E.empty(max(n, 1), 64)
-        info = E.zeros(1, dtype=E.I32)
+        Dinv = self.P.empty(max(n, 1), 64)
         if n:
+            info = self._ints(1)
             E.potrf_batched([M.data_ptr()], [n], [E.ld(M)], [Dinv.data_ptr()], info)
-            self._info_check(info, unit)
+            self.pending.append((self.ipos - 1, 1, unit, self.counters["diag_trees"]))
         self.flops += n**3 / 3.0
         return DenseTri(M, Dinv)
 
     def _dense_from_csr(self, blk, nrows, ncols):
-        D = E.zeros(nrows, ncols)
+        D = self.P.zeros(nrows, ncols)
         if blk is not None and blk.nnz and nrows and ncols:
             E.csr_to_dense_batched([blk.indptr_ptr], [blk.indices_ptr], [blk.data_ptr], [blk.nrows],
                                    [D.data_ptr()], [E.ld(D)])
@@ -322,20 +341,23 @@ class NumericPass:
         """Pivoted QR + reference cutoff -> U (m x kept) (kernels.py:67-82)."""
         m, k = G.shape
         if m == 0 or k == 0:
-            return E.empty(m, 0)
-        Q = E.empty(m, k)
-        rank = E.zeros(1, dtype=E.I32)
-        work = E.qrcp_batched([G.data_ptr()], [m], [k], [E.ld(G)], [Q.data_ptr()], [E.ld(Q)], rank)
-        kept = int(rank.item())
-        del work
+            return self.P.empty(m, 0)
+        Q = self.S.empty(m, k)
+        rank = self._ints(1)
+        E.qrcp_batched([G.data_ptr()], [m], [k], [E.ld(G)], [Q.data_ptr()], [E.ld(Q)], rank, alloc=self.S.empty)
+        kept = int(rank.item())  # the only data-dependent size: one readback per compression
+        self.check_pivots()
         self.flops += 4.0 * m * k * k
-        return Q[:, :kept].contiguous()
+        U = self.P.empty(m, kept)
+        if kept:
+            U.copy_(Q[:, :kept])
+        return U
 
     def _lowrank(self, V, U):
         k = U.shape[1]
-        utu = E.empty(k, k)
+        utu = self.S.empty(k, k)
         _gemm1(U, U, utu, transA=True)
-        Eff = E.empty(V.shape[0], k)
+        Eff = self.P.empty(V.shape[0], k)
         _gemm1(V, utu, Eff)
         return DevLR(V, U, Eff)
 
@@ -354,9 +376,9 @@ class NumericPass:
         for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
             nb = c1 - c0
             Ls.append(self._dense_from_csr(A_BB, nb, nb))
-            Ds.append(E.empty(max(nb, 1), 64))
+            Ds.append(self.P.empty(max(nb, 1), 64))
             Ys.append(self._dense_from_csr(A_off, off_rows.size, nb))
-        info = E.zeros(len(ints), dtype=E.I32)
+        info = self._ints(len(ints))
         E.potrf_batched([L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
                         [D.data_ptr() for D in Ds], info)
         E.trsm_batched("right", 1, [L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
@@ -367,7 +389,7 @@ class NumericPass:
         self.first_interior_failure = None
         for i, (u, ids, c0, c1, off_rows, A_off, A_BB) in enumerate(ints):
             if iv[i] and self.first_interior_failure is None:
-                self.first_interior_failure = (u, int(iv[i]) - 1)
+                self.first_interior_failure = (u, int(iv[i]) - 1, self._trees_before(u))
             nb = c1 - c0
             stored = (A_off.nnz if A_off is not None else 0)
             part = self.sym.partition
@@ -418,14 +440,15 @@ class NumericPass:
             node.diag.solve(X, transpose)
 
     # -- implicit off-diagonal products (factor.py:427-483) --------------------
-    def off_mul(self, node, pairs, G):
+    def off_mul(self, node, pairs, G, final=False):
         """W = L_O G without forming L_O (G: nc x r)."""
         R = node.rows
         r = G.shape[1]
-        W = E.empty(R.size, r)
+        W = (self.P if final else self.S).empty(R.size, r)
         if R.size == 0 or r == 0:
-            return W.zero_()
-        G1 = G.clone()
+            return W.zero_() if W.numel() else W
+        G1 = self.S.empty(*G.shape)
+        G1.copy_(G)
         self.diag_solve(node, G1, transpose=True)
         self.flops += node.ncols**2 * r
         _, A_RC, _ = self.np.node_blocks[node.j]
@@ -437,7 +460,7 @@ class NumericPass:
         """W = L_O^T G (G: |R| x r), diagonal solve last."""
         r = G.shape[1]
         nc = node.ncols
-        W = E.empty(nc, r)
+        W = self.S.empty(nc, r)
         if r == 0:
             return W
         _, _, A_CR = self.np.node_blocks[node.j]
@@ -453,7 +476,7 @@ class NumericPass:
             return
         widths = [self.src_panel[p.s][0].shape[1] for p in use]
         offs = np.concatenate([[0], np.cumsum(np.asarray(widths) * r)])
-        T = E.empty(int(offs[-1]))
+        T = self.S.empty(int(offs[-1]))
         g1, g2 = Grouped(True, False), Grouped(False, False)
         for p, w, o in zip(use, widths, offs[:-1]):
             raw, eff = self.src_panel[p.s]
@@ -480,12 +503,12 @@ class NumericPass:
         """Alg. 3 (factor.py:486-505)."""
         R = node.rows
         rank = min(rank, R.size, node.ncols)
-        G = E.to_dev(_gaussian(R.size, rank, _block_seed(self.cfg.seed, 0, node.j)))
+        G = self.sketches.device(("off", node.j), R.size, rank, self.S)
         G = self.off_mul_t(node, pairs, G)
         for _ in range(self.cfg.power_iters):
             G = self.off_mul_t(node, pairs, self.off_mul(node, pairs, G))
         U = self._orth(G)
-        V = self.off_mul(node, pairs, U)
+        V = self.off_mul(node, pairs, U, final=True)
         return self._lowrank(V, U)
 
     # -- diagonal trees (diagblocks.py) ----------------------------------------
@@ -526,7 +549,7 @@ class NumericPass:
         g.launch()
         return self._potrf(U, node.u)
 
-    def diag_mul(self, node, s, G, transpose):
+    def diag_mul(self, node, s, G, transpose, final=False):
         """Alg. 5: product of internal tree block s with G (diagblocks.py:303-346)."""
         tree = node.diag
         shape = tree.shape
@@ -536,15 +559,17 @@ class NumericPass:
         r = G.shape[1]
         g1, g2 = Grouped(True, False), Grouped(False, False)
         terms = []
+        mem = self.P if final else self.S
         if not transpose:
-            G1 = G.clone()
+            G1 = self.S.empty(*G.shape)
+            G1.copy_(G)
             tree.solve(G1, transpose=True, s=blk_nd.left.s)
             self.flops += (c1 - c0) ** 2 * r
-            W = E.empty(r1 - r0, r)
+            W = mem.empty(r1 - r0, r)
             self._spmm(blk, G1, W)
             src = G1
         else:
-            W = E.empty(c1 - c0, r)
+            W = mem.empty(c1 - c0, r)
             self._spmm(blkT, G, W)
             src = G
         for m in maps:
@@ -559,7 +584,7 @@ class NumericPass:
         if terms:
             widths = np.array([t[2] for t in terms])
             offs = np.concatenate([[0], np.cumsum(widths * r)])
-            T = E.empty(int(offs[-1]))
+            T = self.S.empty(int(offs[-1]))
             for (raw, eff, w, clo, chi, rlo, rhi, cidx, ridx), o in zip(terms, offs[:-1]):
                 ld = E.ld(raw)
                 tp = T.data_ptr() + 8 * int(o)
@@ -584,12 +609,12 @@ class NumericPass:
     def approx_diag(self, node, s, rank):
         (r0, r1), (c0, c1) = node.diag.shape.span(s)
         rank = min(rank, r1 - r0, c1 - c0)
-        G = E.to_dev(_gaussian(r1 - r0, rank, _block_seed(self.cfg.seed, 1, node.j, s)))
+        G = self.sketches.device(("diag", node.j, s), r1 - r0, rank, self.S)
         G = self.diag_mul(node, s, G, True)
         for _ in range(self.cfg.power_iters):
             G = self.diag_mul(node, s, self.diag_mul(node, s, G, False), True)
         U = self._orth(G)
-        V = self.diag_mul(node, s, U, False)
+        V = self.diag_mul(node, s, U, False, final=True)
         return self._lowrank(V, U)
 
     def factor_tree(self, node):
@@ -599,6 +624,7 @@ class NumericPass:
         tree = DeviceTree(shape)
         node.diag = tree
         for s in shape.order:
+            self.S.reset()  # block outputs are persistent; transients of the last block are dead
             tn = shape.nodes[s]
             if tn.is_leaf:
                 tree.blocks[s] = self.factor_leaf(node, s)
@@ -606,9 +632,9 @@ class NumericPass:
             nrows, ncols = tn.hi - tn.split, tn.split - tn.lo
             r = block_rank(nrows, ncols, self.alpha_d, self.cfg.oversample)
             if r >= DENSE_FALLBACK_FRACTION * min(nrows, ncols):
-                eye = E.zeros(ncols, ncols)
+                eye = self.S.zeros(ncols, ncols)
                 eye.fill_diagonal_(1.0)
-                tree.blocks[s] = self.diag_mul(node, s, eye, False)
+                tree.blocks[s] = self.diag_mul(node, s, eye, False, final=True)
                 self.counters["dense_fallback"] += 1
             else:
                 tree.blocks[s] = self.approx_diag(node, s, r)
@@ -616,13 +642,28 @@ class NumericPass:
                 self.counters["compressed_diag"] += 1
 
     # -- the sweep -------------------------------------------------------------
+    def _trees_before(self, u):
+        """Diagonal trees started before unit u (the restart test of factor.py:709)."""
+        return int(np.searchsorted(self.np.tree_units, u, side="left"))
+
     def run(self):
+        prev = E.SCRATCH
+        E.SCRATCH = self.S
+        try:
+            self._run()
+            self.check_pivots()
+        finally:
+            E.SCRATCH = prev
+
+    def _run(self):
         part = self.sym.partition
         cfg = self.cfg
         interiors = self.factor_interiors()
         fail = self.first_interior_failure
         for u, (kind, payload) in enumerate(self.sym.units):
+            self.S.reset()
             if fail is not None and u >= fail[0]:
+                self.check_pivots()
                 raise _Indefinite(*fail)
             if kind == "interior":
                 iu = interiors[u]
@@ -659,9 +700,11 @@ class NumericPass:
                     self.counters["dense_fallback"] += 1
                 if tree_diag:
                     _, UO = self.assemble(node, pairs, want_off=True, want_diag=False)
-                    X = UO.t().contiguous()
+                    X = self.S.empty(nc, R.size)
+                    X.copy_(UO.t())
                     node.diag.solve(X, transpose=False)
-                    node.off = X.t().contiguous()
+                    node.off = self.P.empty(R.size, nc)
+                    node.off.copy_(X.t())
                 else:
                     E.trsm_batched("right", 1, [node.diag.L.data_ptr()], [nc], [E.ld(node.diag.L)],
                                    [node.diag.Dinv.data_ptr()], [UO.data_ptr()], [UO.shape[0]], [E.ld(UO)])
@@ -833,7 +876,9 @@ def factorize(A, config=None, coords=None, prepared=None):
             torch.cuda.current_stream().synchronize()
             break
         except _Indefinite as e:
-            if ps.counters["diag_trees"] == 0:
+            ps.sketches.drain()  # host threads may still write the shared pinned buffer
+            torch.cuda.current_stream().synchronize()
+            if e.trees == 0:
                 raise IndefiniteError(e.pivot) from None
             restarts += 1
             if restarts > config.max_restarts:

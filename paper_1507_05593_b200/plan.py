@@ -191,6 +191,95 @@ class NumericPlan:
         self._build_tree_maps(part)
         self.idx.upload()
         self.csr.upload()
+        # unit indices of the nodes that get a diagonal tree (restart rule)
+        self.tree_units = np.array(
+            [u for u, (k, j) in enumerate(sym.units)
+             if k == "node" and part.is_separator[j] and j in sym.sep_splits], dtype=np.int64)
+        self._sketch_cache = {}
+
+    def sketch_specs(self, cfg, alpha_d):
+        """(key, m, r, seed) of every Gaussian sketch one numeric pass draws, in sweep
+        order: off-diagonal blocks (seed tag (0, j), factor.py:620-625) and compressed
+        diagonal-tree blocks (seed tag (1, j, s), factor.py:605-610)."""
+        from .symbolic import block_rank
+
+        part = self.sym.partition
+        specs = []
+        for kind, j in self.sym.units:
+            if kind != "node" or not part.is_separator[j]:
+                continue
+            c0, c1 = part.cols(j)
+            nc = c1 - c0
+            R = part.rows[j]
+            if j in self.sym.sep_splits:
+                shape = self.tree_shapes[j]
+                for s in shape.order:
+                    nd = shape.nodes[s]
+                    if nd.is_leaf:
+                        continue
+                    nr, ncl = nd.hi - nd.split, nd.split - nd.lo
+                    r = block_rank(nr, ncl, alpha_d, cfg.oversample)
+                    if r < 0.75 * min(nr, ncl):
+                        specs.append((("diag", j, s), nr, min(r, nr, ncl), _seed(cfg.seed, 1, j, s)))
+            r_off = block_rank(R.size, nc, cfg.alpha_o, cfg.oversample)
+            if R.size and r_off < 0.75 * min(R.size, nc):
+                specs.append((("off", j), R.size, min(r_off, R.size, nc), _seed(cfg.seed, 0, j)))
+        return specs
+
+    def sketches_for(self, cfg, alpha_d):
+        return SketchSet(self.sketch_specs(cfg, alpha_d))
+
+
+def _seed(master, *tags):
+    """factor.py:324-326."""
+    ss = np.random.SeedSequence((int(master),) + tuple(int(t) for t in tags))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+class SketchSet:
+    """Host PCG64 sketches of one pass, generated on a thread pool in sweep order
+    into one pinned buffer while the GPU works (numpy releases the GIL while
+    filling), and copied to the device asynchronously right before use.  The
+    values are the reference's own stream (kernels.py:85-92), unchanged."""
+
+    _pool = None
+    _pinned = None
+
+    def __init__(self, specs):
+        import concurrent.futures as cf
+        import os
+
+        self.index = {}
+        off = 0
+        for key, m, r, seed in specs:
+            self.index[key] = (off, m, r, seed)
+            off += m * r
+        total = max(off, 1)
+        if SketchSet._pinned is None or SketchSet._pinned.numel() < total:
+            SketchSet._pinned = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        host = SketchSet._pinned.numpy()
+        if SketchSet._pool is None:
+            SketchSet._pool = cf.ThreadPoolExecutor(max(1, min(8, (os.cpu_count() or 2) - 1)))
+
+        def fill(off, m, r, seed):
+            out = host[off:off + m * r].reshape(m, r)
+            np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r), out=out)
+
+        self.futures = {key: SketchSet._pool.submit(fill, *v) for key, v in self.index.items()}
+        self.host = SketchSet._pinned
+
+    def drain(self):
+        for f in self.futures.values():
+            f.result()
+
+    def device(self, key, m, r, arena):
+        off, m0, r0, _ = self.index[key]
+        assert (m0, r0) == (m, r), (key, m0, r0, m, r)
+        self.futures[key].result()
+        G = arena.empty(m, r)
+        if m * r:
+            G.view(-1).copy_(self.host[off:off + m * r], non_blocking=True)
+        return G
 
     def _build_targets(self, part, touched):
         for j in list(self.targets):
