@@ -230,6 +230,54 @@ class NumericPlan:
         return SketchSet(self.sketch_specs(cfg, alpha_d))
 
 
+    def _build_targets(self, part, touched):
+        for j in list(self.targets):
+            c0, c1 = part.cols(j)
+            R = part.rows[j]
+            pairs = []
+            for sid in touched.get(j, []):
+                src = self.sources[sid]
+                rows = src.rows
+                lo, hi = np.searchsorted(rows, (c0, c1))
+                if lo == hi:
+                    continue
+                cpos = rows[lo:hi] - c0
+                rpos = np.searchsorted(R, rows[hi:])
+                pairs.append(Pair(sid, int(lo), int(hi), self.idx.add(cpos), self.idx.add(rpos), rows.size))
+            pairs.sort(key=lambda p: self.sources[p.s].order)
+            self.targets[j] = pairs
+
+    def _build_tree_maps(self, part):
+        """Window maps for every (tree node j, block s, source) with both windows
+        non-empty (diagblocks.py:231-234, 252-255), plus the A windows."""
+        from .diagtree import TreeShape
+
+        self.tree_shapes = {}
+        for j, split in self.sym.sep_splits.items():
+            c0, c1 = part.cols(j)
+            shape = TreeShape(c1 - c0, c0, split)
+            self.tree_shapes[j] = shape
+            for s in shape.order:
+                (r0, r1), (cc0, cc1) = shape.span(s)
+                gr0, gr1, gc0, gc1 = c0 + r0, c0 + r1, c0 + cc0, c0 + cc1
+                maps = []
+                for pr in self.targets[j]:
+                    rows = self.sources[pr.s].rows
+                    clo, chi = np.searchsorted(rows, (gc0, gc1))
+                    rlo, rhi = np.searchsorted(rows, (gr0, gr1))
+                    if clo == chi or rlo == rhi:
+                        continue
+                    m = TreeBlockMaps()
+                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(clo), int(chi), int(rlo), int(rhi)
+                    m.cidx_off = self.idx.add(rows[clo:chi] - gc0)
+                    m.ridx_off = self.idx.add(rows[rlo:rhi] - gr0)
+                    maps.append(m)
+                win = self.full[gr0:gr1, gc0:gc1]
+                blk = self.csr.add(win)
+                blkT = self.csr.add(win.T.tocsr()) if (gr0, gr1) != (gc0, gc1) else None
+                self.tree_maps[(j, s)] = (maps, blk, blkT)
+
+
 def _seed(master, *tags):
     """factor.py:324-326."""
     ss = np.random.SeedSequence((int(master),) + tuple(int(t) for t in tags))
@@ -280,50 +328,3 @@ class SketchSet:
         if m * r:
             G.view(-1).copy_(self.host[off:off + m * r], non_blocking=True)
         return G
-
-    def _build_targets(self, part, touched):
-        for j in list(self.targets):
-            c0, c1 = part.cols(j)
-            R = part.rows[j]
-            pairs = []
-            for sid in touched.get(j, []):
-                src = self.sources[sid]
-                rows = src.rows
-                lo, hi = np.searchsorted(rows, (c0, c1))
-                if lo == hi:
-                    continue
-                cpos = rows[lo:hi] - c0
-                rpos = np.searchsorted(R, rows[hi:])
-                pairs.append(Pair(sid, int(lo), int(hi), self.idx.add(cpos), self.idx.add(rpos), rows.size))
-            pairs.sort(key=lambda p: self.sources[p.s].order)
-            self.targets[j] = pairs
-
-    def _build_tree_maps(self, part):
-        """Window maps for every (tree node j, block s, source) with both windows
-        non-empty (diagblocks.py:231-234, 252-255), plus the A windows."""
-        from .diagtree import TreeShape
-
-        self.tree_shapes = {}
-        for j, split in self.sym.sep_splits.items():
-            c0, c1 = part.cols(j)
-            shape = TreeShape(c1 - c0, c0, split)
-            self.tree_shapes[j] = shape
-            for s in shape.order:
-                (r0, r1), (cc0, cc1) = shape.span(s)
-                gr0, gr1, gc0, gc1 = c0 + r0, c0 + r1, c0 + cc0, c0 + cc1
-                maps = []
-                for pr in self.targets[j]:
-                    rows = self.sources[pr.s].rows
-                    clo, chi = np.searchsorted(rows, (gc0, gc1))
-                    rlo, rhi = np.searchsorted(rows, (gr0, gr1))
-                    if clo == chi or rlo == rhi:
-                        continue
-                    m = TreeBlockMaps()
-                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(clo), int(chi), int(rlo), int(rhi)
-                    m.cidx_off = self.idx.add(rows[clo:chi] - gc0)
-                    m.ridx_off = self.idx.add(rows[rlo:rhi] - gr0)
-                    maps.append(m)
-                win = self.full[gr0:gr1, gc0:gc1]
-                blk = self.csr.add(win)
-                blkT = self.csr.add(win.T.tocsr()) if (gr0, gr1) != (gc0, gc1) else None
-                self.tree_maps[(j, s)] = (maps, blk, blkT)
