@@ -113,6 +113,13 @@ int rsc_spmm_csr(int nrows, int r, const int *rowptr_dev, const int *colidx_dev,
                  const double *values_dev, const double *X_dev, int ldx,
                  double alpha, double beta, double *Y_dev, int ldy, void *stream);
 
+/* Grouped form of rsc_spmm_csr over `count` CSR blocks (host arrays of device
+ * pointers / sizes); one launch for all A-block products of a level. */
+int rsc_spmm_csr_batched(int count, const int *const *rowptr, const int *const *colidx,
+                         const double *const *values, const int *nrows, const int *r,
+                         const double *const *X, const int *ldx, double alpha, double beta,
+                         double *const *Y, const int *ldy, void *stream);
+
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */
 int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,
                  const double *values_dev, const double *x_dev, double *y_dev,

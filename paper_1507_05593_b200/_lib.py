@@ -36,6 +36,7 @@ EXPORTED = (
     "rsc_qrcp_batched",
     "rsc_csr_to_dense_batched",
     "rsc_spmm_csr",
+    "rsc_spmm_csr_batched",
     "rsc_spmv_csr",
     "rsc_gather_rows",
     "rsc_scatter_add_rows",
@@ -66,6 +67,7 @@ _SIGS = {
     "rsc_qrcp_batched": (I, [I, P, P, P, P, P, P, P, P, P]),
     "rsc_csr_to_dense_batched": (I, [I, P, P, P, P, P, P, P]),
     "rsc_spmm_csr": (I, [I, I, P, P, P, P, I, D, D, P, I, P]),
+    "rsc_spmm_csr_batched": (I, [I, P, P, P, P, P, P, P, D, D, P, P, P]),
     "rsc_spmv_csr": (I, [I, P, P, P, P, P, P]),
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),

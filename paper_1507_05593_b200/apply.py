@@ -1,92 +1,178 @@
 """Preconditioner application z = P^T (L L^T)^{-1} P r on the device
 (reference factor.py:175-218).
 
-Forward sweep over the units in factorization order: diagonal solve of the unit's
-columns, then the coupling update y[R] -= L_O w (dense panel, materialized interior
-coupling Y_B, or V (U^T w)); backward sweep mirrored.  With Y_B materialized the
-interior branch (two in-block solves + sparse coupling, factor.py:189-194,206-210)
-is the same operator as the dense branch, so every unit runs the same kernels.
+Forward sweep: per unit, a diagonal solve of its columns, then the coupling update
+y[R] -= L_O w (dense panel, materialized interior coupling Y_B, or V (U^T w));
+backward sweep mirrored.  With Y_B materialized the interior branch (two in-block
+solves + sparse coupling, factor.py:189-194,206-210) is the same operator as the
+dense branch, so every unit runs the same kernels.
+
+Level scheduling: a unit depends only on the units whose rows reach into its
+columns (its update sources), so units are grouped by height in that DAG and each
+level runs as a handful of grouped launches -- batched TRSV over all dense
+diagonals of the level, one grouped GEMV-scatter (FP64 atomics) for all dense
+couplings, two for all low-rank couplings, and the diagonal trees of the level
+advanced in lock-step waves (Alg. 4 flattened).  All problem descriptors are
+static after factorization and are built once; the whole apply is then replayed
+from a CUDA graph.
 """
 
 import numpy as np
+import torch
 
 from . import engine as E
 from ._lib import GEMM_DTYPE
-from .factor import DeviceTree, DevLR
+from .factor import DenseTri, DeviceTree, DevLR
+
+
+def _rows(probs):
+    return np.array(probs, dtype=GEMM_DTYPE) if probs else None
+
+
+def _p(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, b_rows=0, c_rows=0, atomic=0):
+    return (A, B, C, 0, 0, 0, b_rows, c_rows, 0, M, N, K, max(lda, 1), max(ldb, 1), max(ldc, 1), 1, atomic,
+            alpha, beta)
+
+
+class _Trsv:
+    """Batched triangular solves on vector slices (one rsc_trsm_batched call)."""
+
+    def __init__(self, tris, ptrs, trans):
+        self.trans = trans
+        self.L = [t.L.data_ptr() for t in tris]
+        self.n = [t.n for t in tris]
+        self.ld = [E.ld(t.L) for t in tris]
+        self.D = [t.Dinv.data_ptr() for t in tris]
+        self.B = list(ptrs)
+
+    def run(self):
+        if self.L:
+            E.trsm_batched("left", self.trans, self.L, self.n, self.ld, self.D, self.B, [1] * len(self.L),
+                           [1] * len(self.L))
 
 
 class DeviceApply:
     def __init__(self, F):
         self.F = F
         self.n = F.n
+        plan = F.plan
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
-        plan = F.plan
-        self.rows_ptr = []
-        for un in F.units:
-            key = ("int", un.u) if un.kind == "interior" else un.j
-            self.rows_ptr.append(plan.idx.ptr(plan.rows_off[key]))
+        self.y = E.empty(self.n, 1)
+        self.zbuf = E.empty(self.n)
+        units = F.units
+        # level of every unit = 1 + max level of its update sources
+        uidx = {un.u: i for i, un in enumerate(units)}
+        level = [0] * len(units)
+        for i, un in enumerate(units):
+            if un.kind == "node":
+                lv = 0
+                for p in plan.targets[un.j]:
+                    su = uidx[plan.sources[p.s].unit]
+                    lv = max(lv, level[su] + 1)
+                level[i] = lv
+        self.levels = []
+        nlev = max(level) + 1 if units else 0
+        yp = self.y.data_ptr()
+        self.scratch = []
+        for lv in range(nlev):
+            idx = [i for i in range(len(units)) if level[i] == lv]
+            self.levels.append(self._build_level([units[i] for i in idx], plan, yp))
+        self.graph = None
+        self.r_in = E.empty(self.n)
 
-    @staticmethod
-    def _prob(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, b_rows=0, c_rows=0):
-        p = np.zeros(1, dtype=GEMM_DTYPE)
-        p["A"], p["B"], p["C"] = A, B, C
-        p["lda"], p["ldb"], p["ldc"] = max(lda, 1), max(ldb, 1), max(ldc, 1)
-        p["M"], p["N"], p["K"] = M, N, K
-        p["alpha"], p["beta"], p["batch"] = alpha, beta, 1
-        p["b_rows"], p["c_rows"] = b_rows, c_rows
-        return p
+    def _rows_ptr(self, plan, un):
+        key = ("int", un.u) if un.kind == "interior" else un.j
+        return plan.idx.ptr(plan.rows_off[key])
 
-    def __call__(self, r_dev, out=None):
-        n = self.n
-        r = r_dev.reshape(n, 1)
-        y = E.empty(n, 1)
-        E.gather_rows(self.inv, r, y)
-        yp = y.data_ptr()
-        units = self.F.units
-        # forward
-        for un, rp in zip(units, self.rows_ptr):
-            w = y[un.c0:un.c1]
-            self._diag_solve(un, w, False)
-            m = un.rows.size
-            if m == 0 or un.off is None:
+    def _build_level(self, us, plan, yp):
+        L = {}
+        dense = [u for u in us if isinstance(u.diag, DenseTri)]
+        trees = [u for u in us if isinstance(u.diag, DeviceTree)]
+        L["fwd_diag"] = _Trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0)
+        L["bwd_diag"] = _Trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1)
+        L["trees"] = trees
+        # coupling products
+        fd, fl1, fl2, bd, bl1, bl2 = [], [], [], [], [], []
+        lr = [u for u in us if isinstance(u.off, DevLR) and u.rows.size and u.off.k]
+        tsz = sum(u.off.k for u in lr)
+        t = E.empty(max(tsz, 1))
+        self.scratch.append(t)
+        toff = 0
+        for u in us:
+            m = u.rows.size
+            if m == 0 or u.off is None:
                 continue
-            if isinstance(un.off, DevLR):
-                k = un.off.k
+            rp = self._rows_ptr(plan, u)
+            w = yp + 8 * u.c0
+            if isinstance(u.off, DevLR):
+                k = u.off.k
                 if k == 0:
                     continue
-                t = E.empty(k, 1)
-                E.gemm_grouped(self._prob(un.off.U.data_ptr(), E.ld(un.off.U), w.data_ptr(), 1, t.data_ptr(), 1,
-                                          k, 1, un.ncols, 1.0, 0.0), True, False)
-                E.gemm_grouped(self._prob(un.off.V.data_ptr(), E.ld(un.off.V), t.data_ptr(), 1, yp, 1, m, 1, k,
-                                          -1.0, 1.0, c_rows=rp))
+                tp = t.data_ptr() + 8 * toff
+                toff += k
+                V, U = u.off.V, u.off.U
+                fl1.append(_p(U.data_ptr(), E.ld(U), w, 1, tp, 1, k, 1, u.ncols, 1.0, 0.0))
+                fl2.append(_p(V.data_ptr(), E.ld(V), tp, 1, yp, 1, m, 1, k, -1.0, 1.0, c_rows=rp, atomic=1))
+                bl1.append(_p(V.data_ptr(), E.ld(V), yp, 1, tp, 1, k, 1, m, 1.0, 0.0, b_rows=rp))
+                bl2.append(_p(U.data_ptr(), E.ld(U), tp, 1, w, 1, u.ncols, 1, k, -1.0, 1.0))
             else:
-                E.gemm_grouped(self._prob(un.off.data_ptr(), E.ld(un.off), w.data_ptr(), 1, yp, 1, m, 1,
-                                          un.ncols, -1.0, 1.0, c_rows=rp))
-        # backward
-        for un, rp in zip(reversed(units), reversed(self.rows_ptr)):
-            w = y[un.c0:un.c1]
-            m = un.rows.size
-            if m and un.off is not None:
-                if isinstance(un.off, DevLR):
-                    k = un.off.k
-                    if k:
-                        t = E.empty(k, 1)
-                        E.gemm_grouped(self._prob(un.off.V.data_ptr(), E.ld(un.off.V), yp, 1, t.data_ptr(), 1, k, 1,
-                                                  m, 1.0, 0.0, b_rows=rp), True, False)
-                        E.gemm_grouped(self._prob(un.off.U.data_ptr(), E.ld(un.off.U), t.data_ptr(), 1, w.data_ptr(),
-                                                  1, un.ncols, 1, k, -1.0, 1.0))
-                else:
-                    E.gemm_grouped(self._prob(un.off.data_ptr(), E.ld(un.off), yp, 1, w.data_ptr(), 1, un.ncols, 1,
-                                              m, -1.0, 1.0, b_rows=rp), True, False)
-            self._diag_solve(un, w, True)
-        z = out if out is not None else E.empty(n)
-        E.gather_rows(self.fwd, y, z.reshape(n, 1))
-        return z
+                O = u.off
+                fd.append(_p(O.data_ptr(), E.ld(O), w, 1, yp, 1, m, 1, u.ncols, -1.0, 1.0, c_rows=rp, atomic=1))
+                bd.append(_p(O.data_ptr(), E.ld(O), yp, 1, w, 1, u.ncols, 1, m, -1.0, 1.0, b_rows=rp))
+        L["fd"], L["fl1"], L["fl2"] = _rows(fd), _rows(fl1), _rows(fl2)
+        L["bd"], L["bl1"], L["bl2"] = _rows(bd), _rows(bl1), _rows(bl2)
+        return L
 
     @staticmethod
-    def _diag_solve(un, w, transpose):
-        if isinstance(un.diag, DeviceTree):
-            un.diag.solve(w, transpose)
+    def _g(probs, ta=False):
+        if probs is not None:
+            E.gemm_grouped(probs, ta, False)
+
+    def _sweep(self):
+        y = self.y
+        for L in self.levels:
+            L["fwd_diag"].run()
+            for u in L["trees"]:
+                u.diag.solve(y[u.c0:u.c1], False)
+            self._g(L["fd"])
+            self._g(L["fl1"], True)
+            self._g(L["fl2"])
+        for L in reversed(self.levels):
+            self._g(L["bd"], True)
+            self._g(L["bl1"], True)
+            self._g(L["bl2"])
+            for u in L["trees"]:
+                u.diag.solve(y[u.c0:u.c1], True)
+            L["bwd_diag"].run()
+
+    def _body(self):
+        n = self.n
+        E.gather_rows(self.inv, self.r_in.reshape(n, 1), self.y)
+        self._sweep()
+        E.gather_rows(self.fwd, self.y, self.zbuf.reshape(n, 1))
+
+    def __call__(self, r_dev, out=None):
+        self.r_in.copy_(r_dev.reshape(-1))
+        if self.graph is None:
+            self._body()  # eager first run (warms the caching allocator)
+            try:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s):
+                        self._body()
+                torch.cuda.current_stream().wait_stream(s)
+                self.graph = g
+            except Exception:
+                self.graph = False
+            # recompute in the normal stream (the eager result above is valid too)
+            self._body()
+        elif self.graph is False:
+            self._body()
         else:
-            un.diag.solve(w, transpose)
+            self.graph.replay()
+        z = out if out is not None else E.empty(self.n)
+        z.copy_(self.zbuf)
+        return z

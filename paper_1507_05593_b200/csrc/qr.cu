@@ -207,11 +207,18 @@ constexpr long long SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
 
 }  // namespace
 
+// multi-CTA path for sketches that do not fit one SM (qr_coop.cu)
+long long rsc_qrcp_coop_doubles(int m, int k);
+int rsc_qrcp_coop(const double *G, int m, int k, int ldg, double *Q, int ldq, int *rank_dev, double *work,
+                  cudaStream_t s);
+
+static inline long long coop_bytes(int m, int k) { return ((rsc_qrcp_coop_doubles(m, k) * 8 + 255) / 256) * 256; }
+
 extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k) {
     long long tot = 0;
     for (int i = 0; i < count; ++i) {
         const long long sz = (long long)(m[i] | 1) * k[i];
-        if (sz > SMEM_LIMIT_DOUBLES) tot += ((sz * 8 + 255) / 256) * 256;
+        if (sz > SMEM_LIMIT_DOUBLES) tot += coop_bytes(m[i], k[i]);
     }
     return tot < 256 ? 256 : tot;
 }
@@ -268,8 +275,14 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     };
     int rc = run(small, true);
     if (rc) return rc;
-    // global workspace offsets are assigned in the order of `big`, matching
-    // rsc_qrcp_workspace_bytes (which sums the big ones in index order)
-    rc = run(big, false);
-    return rc;
+    // large sketches: one cooperative multi-CTA QR each, workspace slices in the
+    // order rsc_qrcp_workspace_bytes sums them
+    long long off = 0;
+    for (int i : big) {
+        rc = rsc_qrcp_coop(G[i], m[i], k[i], ldg[i], Q[i], ldq[i], rank_dev + i,
+                           (double *)((char *)work_dev + off), s);
+        if (rc) return rc;
+        off += coop_bytes(m[i], k[i]);
+    }
+    return 0;
 }

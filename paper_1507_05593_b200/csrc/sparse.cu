@@ -33,6 +33,39 @@ __global__ void csr_to_dense_kernel(const __grid_constant__ CsrDenseArgs a) {
     }
 }
 
+struct SpmmArgs {
+    int count;
+    const int *rowptr[MAXB];
+    const int *colidx[MAXB];
+    const double *values[MAXB];
+    const double *X[MAXB];
+    double *Y[MAXB];
+    int nrows[MAXB], r[MAXB], ldx[MAXB], ldy[MAXB];
+    double alpha, beta;
+};
+
+// grouped SpMM: blockIdx.y = problem, warps stride over its rows
+__global__ void spmm_csr_batched_kernel(const __grid_constant__ SpmmArgs a) {
+    const int b = blockIdx.y;
+    const int nr = a.nrows[b], r = a.r[b];
+    const int *rp = a.rowptr[b];
+    const int *ci = a.colidx[b];
+    const double *v = a.values[b];
+    const double *X = a.X[b];
+    double *Y = a.Y[b];
+    const int ldx = a.ldx[b], ldy = a.ldy[b];
+    const int wpb = blockDim.x / 32;
+    for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < nr; row += gridDim.x * wpb) {
+        const int p0 = rp[row], p1 = rp[row + 1];
+        for (int c = threadIdx.x & 31; c < r; c += 32) {
+            double acc = 0.0;
+            for (int p = p0; p < p1; ++p) acc += v[p] * X[(long long)ci[p] * ldx + c];
+            double *y = Y + (long long)row * ldy + c;
+            *y = (a.beta == 0.0) ? a.alpha * acc : a.alpha * acc + a.beta * (*y);
+        }
+    }
+}
+
 // one warp per output row; lanes stride over the dense columns
 __global__ void spmm_csr_kernel(int nrows, int r, const int *__restrict__ rp,
                                 const int *__restrict__ ci, const double *__restrict__ v,
@@ -166,6 +199,33 @@ extern "C" int rsc_csr_to_dense_batched(int count, const int *const *rowptr, con
         }
         dim3 grid((maxr + 7) / 8 < 64 ? (maxr + 7) / 8 : 64, cnt);
         csr_to_dense_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+        RSC_CHECK_LAUNCH();
+    }
+    return 0;
+}
+
+extern "C" int rsc_spmm_csr_batched(int count, const int *const *rowptr, const int *const *colidx,
+                                    const double *const *values, const int *nrows, const int *r,
+                                    const double *const *X, const int *ldx, double alpha, double beta,
+                                    double *const *Y, const int *ldy, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!rowptr || !colidx || !values || !nrows || !r || !X || !ldx || !Y || !ldy) return -2;
+    static thread_local SpmmArgs a;
+    for (int c0 = 0; c0 < count; c0 += MAXB) {
+        const int cnt = count - c0 < MAXB ? count - c0 : MAXB;
+        a.count = cnt;
+        a.alpha = alpha;
+        a.beta = beta;
+        int maxr = 1;
+        for (int i = 0; i < cnt; ++i) {
+            a.rowptr[i] = rowptr[c0 + i]; a.colidx[i] = colidx[c0 + i]; a.values[i] = values[c0 + i];
+            a.X[i] = X[c0 + i]; a.Y[i] = Y[c0 + i];
+            a.nrows[i] = nrows[c0 + i]; a.r[i] = r[c0 + i]; a.ldx[i] = ldx[c0 + i]; a.ldy[i] = ldy[c0 + i];
+            maxr = nrows[c0 + i] > maxr ? nrows[c0 + i] : maxr;
+        }
+        dim3 grid((maxr + 7) / 8 < 128 ? (maxr + 7) / 8 : 128, cnt);
+        spmm_csr_batched_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
         RSC_CHECK_LAUNCH();
     }
     return 0;

@@ -125,3 +125,22 @@ def test_low_rank_approx_golden(cuda):
     assert relerr(V @ U.T, B) < 1e-10
     V, U = K.low_rank_approx(np.zeros((10, 6)), rank=3, seed=0)
     assert np.linalg.norm(V @ U.T) == 0.0
+
+
+@pytest.mark.parametrize("m,k,true_rank", [(1000, 300, None), (2100, 130, 90), (300, 700, 150)])
+def test_orthonormalize_multi_cta_path(cuda, m, k, true_rank):
+    """Sketches beyond one SM's shared memory go through the cooperative QR."""
+    from oracle import kernels as ok
+    from paper_1507_05593_b200 import kernels as K
+
+    rng = np.random.default_rng(m + k)
+    if true_rank is None:
+        G = rng.standard_normal((m, k))
+    else:
+        G = rng.standard_normal((m, true_rank)) @ rng.standard_normal((true_rank, k)) + 1e-15 * rng.standard_normal(
+            (m, k))
+    Q = K.orthonormalize(G)
+    Qo = ok.orth(G)
+    assert Q.shape == Qo.shape
+    assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() < 1e-12
+    assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
