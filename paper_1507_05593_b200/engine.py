@@ -77,6 +77,18 @@ class Arena:
             t.zero_()
         return t
 
+    def zeros_many(self, shapes):
+        """Several zeroed 2-D blocks carved from one allocation (one memset)."""
+        sizes = [max(-(-(int(a) * int(b)) // self.ALIGN) * self.ALIGN, self.ALIGN) for a, b in shapes]
+        flat = self.empty(sum(sizes))
+        if flat.numel():
+            flat.zero_()
+        out, o = [], 0
+        for (a, b), sz in zip(shapes, sizes):
+            out.append(flat[o:o + int(a) * int(b)].view(int(a), int(b)))
+            o += sz
+        return out
+
     def reset(self):
         self.i = 0
         self.off = 0

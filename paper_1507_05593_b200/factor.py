@@ -365,6 +365,13 @@ class NumericPass:
         return self.np.idx.ptr(off)
 
     # -- interior blocks -----------------------------------------------------
+    def _interior_mats(self, ints):
+        Ls, Ys = [], []
+        for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
+            Ls.append(self._dense_from_csr(A_BB, c1 - c0, c1 - c0))
+            Ys.append(self._dense_from_csr(A_off, off_rows.size, c1 - c0))
+        return Ls, Ys
+
     def factor_interiors(self):
         """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
         Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM."""
@@ -372,12 +379,8 @@ class NumericPass:
         self.first_interior_failure = None
         if not ints:
             return {}
-        Ls, Ds, Ys = [], [], []
-        for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
-            nb = c1 - c0
-            Ls.append(self._dense_from_csr(A_BB, nb, nb))
-            Ds.append(self.P.empty(max(nb, 1), 64))
-            Ys.append(self._dense_from_csr(A_off, off_rows.size, nb))
+        Ls, Ys = self._interior_mats(ints)
+        Ds = [self.P.empty(max(c1 - c0, 1), 64) for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints]
         info = self._ints(len(ints))
         E.potrf_batched([L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
                         [D.data_ptr() for D in Ds], info)
@@ -644,7 +647,8 @@ class NumericPass:
     # -- the sweep -------------------------------------------------------------
     def _trees_before(self, u):
         """Diagonal trees started before unit u (the restart test of factor.py:709)."""
-        return int(np.searchsorted(self.np.tree_units, u, side="left"))
+        # the tree counter is bumped before a tree node's own leaf POTRFs (factor.py:587-588)
+        return int(np.searchsorted(self.np.tree_units, u, side="right"))
 
     def run(self):
         prev = E.SCRATCH
@@ -863,6 +867,7 @@ def factorize(A, config=None, coords=None, prepared=None):
         t0 = t_plan0 = t2 = time.perf_counter()
         sym.t_ordering = sym.t_symbolic = 0.0
     from . import _lib
+    from .numeric import LevelPass
 
     lib = _lib.load()
     launches0 = int(lib.rsc_launch_counter(0))
@@ -870,7 +875,7 @@ def factorize(A, config=None, coords=None, prepared=None):
     history = [alpha_d]
     restarts = 0
     while True:
-        ps = NumericPass(plan, config, alpha_d)
+        ps = LevelPass(plan, config, alpha_d)
         try:
             ps.run()
             torch.cuda.current_stream().synchronize()

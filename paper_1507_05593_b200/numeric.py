@@ -1,0 +1,658 @@
+"""Level-batched numeric sweep (the production driver of factorize).
+
+The reference sweeps its units one at a time (factor.py:556-639).  A compressed
+separator only reads its update sources -- interior blocks and separators lower in
+the nested-dissection tree -- so all separators of one ND level are independent
+and their work is issued together: every step below is ONE grouped launch (or one
+batched call) over all nodes of the level, and the only host<->device
+synchronisations are one rank readback per batched QR.  Results are identical to
+the unit-by-unit order because each node's arithmetic is unchanged; only its
+interleaving with independent nodes differs.
+
+Per level:
+  dense diagonals   A-block scatter + Schur update of all (node, source) pairs,
+                    batched POTRF, batched TRSM for dense off-diagonals
+  diagonal trees    advanced in lock-step over in-order block positions; leaves
+                    by batched window assembly + POTRF, internal blocks by batched
+                    implicit products (Alg. 5) whose Alg. 4 sub-solves run as
+                    lock-step waves across trees
+  compression       sketch products of all compressed off-diagonals of the level
+                    (Alg. 2 and its transpose), one batched pivoted QR, V = L_O U
+
+Pivot failures are collected and resolved at the end of the pass in sweep order
+(the earliest failing unit decides restart vs. re-raise, factor.py:705-710).
+"""
+
+import numpy as np
+
+from . import engine as E
+from .factor import (
+    DENSE_FALLBACK_FRACTION,
+    DenseTri,
+    DeviceTree,
+    DevLR,
+    Grouped,
+    InteriorUnit,
+    NodeUnit,
+    NumericPass,
+    _Indefinite,
+    _raw_eff,
+)
+from .symbolic import block_rank
+
+
+# ---------------------------------------------------------------------------
+# lock-step batched Alg. 4
+
+
+def tree_ops(tree, s, X, transpose):
+    """Flatten the block substitution of subtree s of `tree` acting on X."""
+    ops = []
+    nd0 = tree.shape.root if s is None else tree.shape.nodes[s]
+
+    def rec(nd, Xv):
+        if nd.is_leaf:
+            ops.append(("leaf", tree.blocks[nd.s], Xv, transpose))
+            return
+        k = nd.split - nd.lo
+        X1, X2 = Xv[:k], Xv[k:]
+        b = tree.blocks[nd.s]
+        if transpose:
+            rec(nd.right, X2)
+            ops.append(("couple", b, X2, X1, True))
+            rec(nd.left, X1)
+        else:
+            rec(nd.left, X1)
+            ops.append(("couple", b, X1, X2, False))
+            rec(nd.right, X2)
+
+    rec(nd0, X)
+    return ops
+
+
+def run_waves(seqs, scratch):
+    """Execute op sequences in lock-step: wave w runs op w of every sequence."""
+    seqs = [s for s in seqs if s]
+    if not seqs:
+        return
+    for w in range(max(len(s) for s in seqs)):
+        leaves = {0: [], 1: []}
+        dense = {False: Grouped(False, False), True: Grouped(True, False)}
+        lr1 = {False: Grouped(True, False), True: Grouped(True, False)}
+        lr2 = Grouped(False, False)
+        for seq in seqs:
+            if w >= len(seq):
+                continue
+            op = seq[w]
+            if op[0] == "leaf":
+                _, tri, Xv, tr = op
+                if tri.n and Xv.shape[1]:
+                    leaves[int(tr)].append((tri, Xv))
+                continue
+            _, b, Xs, Yd, tr = op
+            r = Xs.shape[1]
+            if r == 0:
+                continue
+            if isinstance(b, DevLR):
+                if b.k == 0:
+                    continue
+                t = scratch(b.k, r)
+                # t = U^T X (forward) or V^T X (transposed); then Y -= V t or U t
+                P1 = b.V if tr else b.U
+                P2 = b.U if tr else b.V
+                lr1[tr].add(P1.data_ptr(), E.ld(P1), Xs.data_ptr(), E.ld(Xs), t.data_ptr(), r, b.k, r,
+                            Xs.shape[0], 1.0, 0.0)
+                lr2.add(P2.data_ptr(), E.ld(P2), t.data_ptr(), r, Yd.data_ptr(), E.ld(Yd), Yd.shape[0], r, b.k,
+                        -1.0, 1.0)
+            else:
+                M, K = (b.shape[1], b.shape[0]) if tr else (b.shape[0], b.shape[1])
+                dense[tr].add(b.data_ptr(), E.ld(b), Xs.data_ptr(), E.ld(Xs), Yd.data_ptr(), E.ld(Yd), M, r, K,
+                              -1.0, 1.0)
+        for tr, lst in leaves.items():
+            if lst:
+                E.trsm_batched("left", tr, [t.L.data_ptr() for t, _ in lst], [t.n for t, _ in lst],
+                               [E.ld(t.L) for t, _ in lst], [t.Dinv.data_ptr() for t, _ in lst],
+                               [X.data_ptr() for _, X in lst], [X.shape[1] for _, X in lst],
+                               [E.ld(X) for _, X in lst])
+        dense[False].launch()
+        dense[True].launch()
+        lr1[False].launch()
+        lr1[True].launch()
+        lr2.launch()
+
+
+def diag_solve_many(items, scratch):
+    """items: (node, X, transpose[, subtree s]) -> X <- D^{-1} X / D^{-T} X in place."""
+    dense = {0: [], 1: []}
+    seqs = []
+    for it in items:
+        node, X, tr = it[0], it[1], it[2]
+        s = it[3] if len(it) > 3 else None
+        if X.shape[1] == 0 or X.shape[0] == 0:
+            continue
+        if isinstance(node.diag, DeviceTree):
+            seqs.append(tree_ops(node.diag, s, X, tr))
+        else:
+            dense[int(tr)].append((node.diag, X))
+    for tr, lst in dense.items():
+        if lst:
+            E.trsm_batched("left", tr, [t.L.data_ptr() for t, _ in lst], [t.n for t, _ in lst],
+                           [E.ld(t.L) for t, _ in lst], [t.Dinv.data_ptr() for t, _ in lst],
+                           [X.data_ptr() for _, X in lst], [X.shape[1] for _, X in lst], [E.ld(X) for _, X in lst])
+    run_waves(seqs, scratch)
+
+
+# ---------------------------------------------------------------------------
+
+
+class LevelPass(NumericPass):
+    """Level-batched version of NumericPass (same results, far fewer launches)."""
+
+    # -- batched primitives ----------------------------------------------------
+    def _interior_mats(self, ints):
+        blocks = []
+        for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
+            blocks.append((A_BB, c1 - c0, c1 - c0))
+            blocks.append((A_off, off_rows.size, c1 - c0))
+        D = self._dense_many(blocks)
+        return D[0::2], D[1::2]
+
+    def _dense_many(self, blocks):
+        """[(csr block or None, nrows, ncols)] -> persistent dense tensors (one launch)."""
+        outs, rp, ci, va, nr, dp, ld = [], [], [], [], [], [], []
+        mats = self.P.zeros_many([(m, n) for _, m, n in blocks])
+        for (blk, m, n), D in zip(blocks, mats):
+            outs.append(D)
+            if blk is not None and blk.nnz and m and n:
+                rp.append(blk.indptr_ptr)
+                ci.append(blk.indices_ptr)
+                va.append(blk.data_ptr)
+                nr.append(blk.nrows)
+                dp.append(D.data_ptr())
+                ld.append(E.ld(D))
+        if nr:
+            E.csr_to_dense_batched(rp, ci, va, nr, dp, ld)
+        return outs
+
+    def _potrf_many(self, mats_units):
+        mats_units = [(M, u) for M, u in mats_units]
+        tris = []
+        live = []
+        for M, u in mats_units:
+            n = M.shape[0]
+            tris.append(DenseTri(M, self.P.empty(max(n, 1), 64)))
+            if n:
+                live.append((M, u, tris[-1]))
+            self.flops += n**3 / 3.0
+        if live:
+            info = self._ints(len(live))
+            E.potrf_batched([M.data_ptr() for M, _, _ in live], [M.shape[0] for M, _, _ in live],
+                            [E.ld(M) for M, _, _ in live], [t.Dinv.data_ptr() for _, _, t in live], info)
+            base = self.ipos - len(live)
+            for i, (_, u, _) in enumerate(live):
+                self.pending.append((base + i, 1, u, self._trees_before(u)))
+        return tris
+
+    def _spmm_many(self, items, alpha=1.0, beta=0.0):
+        """items: (csr block or None, X, Y) -> Y = alpha S X + beta Y."""
+        rp, ci, va, nr, rr, xp, lx, yp, ly = [], [], [], [], [], [], [], [], []
+        for blk, X, Y in items:
+            if Y.numel() == 0:
+                continue
+            if blk is None or blk.nrows == 0 or X.shape[1] == 0:
+                if beta == 0.0:
+                    Y.zero_()
+                continue
+            rp.append(blk.indptr_ptr)
+            ci.append(blk.indices_ptr)
+            va.append(blk.data_ptr)
+            nr.append(blk.nrows)
+            rr.append(int(X.shape[1]))
+            xp.append(X.data_ptr())
+            lx.append(E.ld(X))
+            yp.append(Y.data_ptr())
+            ly.append(E.ld(Y))
+            self.flops += 2.0 * blk.nnz * X.shape[1]
+        if nr:
+            lib = E.require_cuda()
+            from ._lib import int_array, ptr_array
+
+            a = [ptr_array(rp), ptr_array(ci), ptr_array(va), int_array(nr), int_array(rr), ptr_array(xp),
+                 int_array(lx), ptr_array(yp), int_array(ly)]
+            E.check(lib.rsc_spmm_csr_batched(len(nr), a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data,
+                                             a[3].ctypes.data, a[4].ctypes.data, a[5].ctypes.data,
+                                             a[6].ctypes.data, float(alpha), float(beta), a[7].ctypes.data,
+                                             a[8].ctypes.data, E.stream_handle()), "rsc_spmm_csr_batched")
+
+    def _orth_many(self, Gs):
+        """One batched pivoted QR over all sketches, one readback of all ranks."""
+        Us = [None] * len(Gs)
+        live = [(i, G) for i, G in enumerate(Gs) if G.shape[0] and G.shape[1]]
+        for i, G in enumerate(Gs):
+            if not (G.shape[0] and G.shape[1]):
+                Us[i] = self.P.empty(G.shape[0], 0)
+        if not live:
+            return Us
+        Qs = [self.S.empty(*G.shape) for _, G in live]
+        rank = self._ints(len(live))
+        E.qrcp_batched([G.data_ptr() for _, G in live], [G.shape[0] for _, G in live],
+                       [G.shape[1] for _, G in live], [E.ld(G) for _, G in live], [Q.data_ptr() for Q in Qs],
+                       [E.ld(Q) for Q in Qs], rank, alloc=self.S.empty)
+        kept = rank.cpu().numpy()  # the only data-dependent sizes of the level
+        for (i, G), Q, k in zip(live, Qs, kept):
+            m = G.shape[0]
+            U = self.P.empty(m, int(k))
+            if k:
+                U.copy_(Q[:, :int(k)])
+            Us[i] = U
+            self.flops += 4.0 * m * G.shape[1] ** 2
+        return Us
+
+    def _lowrank_many(self, VUs):
+        out = []
+        g1, g2 = Grouped(True, False), Grouped(False, False)
+        for V, U in VUs:
+            k = U.shape[1]
+            utu = self.S.empty(max(k, 1), max(k, 1))
+            Eff = self.P.empty(V.shape[0], k)
+            if k:
+                g1.add(U.data_ptr(), E.ld(U), U.data_ptr(), E.ld(U), utu.data_ptr(), k, k, k, U.shape[0], 1.0, 0.0)
+                g2.add(V.data_ptr(), E.ld(V), utu.data_ptr(), k, Eff.data_ptr(), E.ld(Eff), V.shape[0], k, k,
+                       1.0, 0.0)
+            out.append(DevLR(V, U, Eff))
+        g1.launch()
+        g2.launch()
+        return out
+
+    # -- dense-diagonal nodes ---------------------------------------------------
+    def assemble_many(self, items):
+        """items: (node, want_diag, want_off) -> [(UD or None, UO or None)] with all
+        Schur updates of all nodes in one grouped launch (factor.py:372-399)."""
+        blocks, layout = [], []
+        for node, wd, wo in items:
+            A_CC, A_RC, _ = self.np.node_blocks[node.j]
+            nc, R = node.ncols, node.rows
+            wo = wo and R.size > 0
+            layout.append((len(blocks) if wd else None, len(blocks) + (1 if wd else 0) if wo else None))
+            if wd:
+                blocks.append((A_CC, nc, nc))
+            if wo:
+                blocks.append((A_RC, R.size, nc))
+        dense = self._dense_many(blocks)
+        out = []
+        g = Grouped(False, True)
+        for (node, wd, wo), (iD, iO) in zip(items, layout):
+            UD = dense[iD] if iD is not None else None
+            UO = dense[iO] if iO is not None else None
+            out.append((UD, UO))
+            nc = node.ncols
+            for pr in self.np.targets[node.j]:
+                raw, eff = self.src_panel[pr.s]
+                w = raw.shape[1]
+                if w == 0 or pr.n_rd == 0:
+                    continue
+                ld = E.ld(raw)
+                cpos = self._idx(pr.cpos_off)
+                Q = raw.data_ptr() + 8 * pr.lo * ld
+                if UD is not None:
+                    g.add(eff.data_ptr() + 8 * pr.lo * ld, ld, Q, ld, UD.data_ptr(), nc, pr.n_rd, pr.n_rd, w,
+                          -1.0, 1.0, c_rows=cpos, c_cols=cpos, atomic=1)
+                    self.flops += 2.0 * pr.n_rd * pr.n_rd * w
+                if UO is not None and pr.n_ro > 0:
+                    g.add(eff.data_ptr() + 8 * pr.hi * ld, ld, Q, ld, UO.data_ptr(), nc, pr.n_ro, pr.n_rd, w,
+                          -1.0, 1.0, c_rows=self._idx(pr.rpos_off), c_cols=cpos, atomic=1)
+                    self.flops += 2.0 * pr.n_ro * pr.n_rd * w
+        g.launch()
+        return out
+
+    # -- implicit products, batched over nodes -----------------------------------
+    def off_mul_many(self, nodes, Gs, final=False):
+        Ws, G1s, sol = [], [], []
+        for node, G in zip(nodes, Gs):
+            R = node.rows
+            r = G.shape[1]
+            W = (self.P if final else self.S).empty(R.size, r)
+            Ws.append(W)
+            G1 = self.S.empty(*G.shape)
+            if G.numel():
+                G1.copy_(G)
+            G1s.append(G1)
+            sol.append((node, G1, True))
+            self.flops += node.ncols**2 * r
+        diag_solve_many(sol, self.S.empty)
+        self._spmm_many([(self.np.node_blocks[n.j][1], G1, W) for n, G1, W in zip(nodes, G1s, Ws)])
+        self._products_many(nodes, G1s, Ws, trans=False)
+        return Ws
+
+    def off_mul_t_many(self, nodes, Gs):
+        Ws = [self.S.empty(n.ncols, G.shape[1]) for n, G in zip(nodes, Gs)]
+        self._spmm_many([(self.np.node_blocks[n.j][2], G, W) for n, G, W in zip(nodes, Gs, Ws)])
+        self._products_many(nodes, Gs, Ws, trans=True)
+        diag_solve_many([(n, W, False) for n, W in zip(nodes, Ws)], self.S.empty)
+        for n, W in zip(nodes, Ws):
+            self.flops += n.ncols**2 * W.shape[1]
+        return Ws
+
+    def _products_many(self, nodes, Gs, Ws, trans):
+        g1, g2 = Grouped(True, False), Grouped(False, False)
+        for node, G, W in zip(nodes, Gs, Ws):
+            r = G.shape[1]
+            if r == 0 or W.numel() == 0:
+                continue
+            use = [p for p in self.np.targets[node.j]
+                   if p.n_rd > 0 and p.n_ro > 0 and self.src_panel[p.s][0].shape[1] > 0]
+            if not use:
+                continue
+            T = self.S.empty(sum(self.src_panel[p.s][0].shape[1] for p in use) * r)
+            o = 0
+            for p in use:
+                raw, eff = self.src_panel[p.s]
+                w = raw.shape[1]
+                ld = E.ld(raw)
+                tp = T.data_ptr() + 8 * o
+                o += w * r
+                cpos, rpos = self._idx(p.cpos_off), self._idx(p.rpos_off)
+                if not trans:
+                    g1.add(raw.data_ptr() + 8 * p.lo * ld, ld, G.data_ptr(), E.ld(G), tp, r, w, r, p.n_rd, 1.0, 0.0,
+                           b_rows=cpos)
+                    g2.add(eff.data_ptr() + 8 * p.hi * ld, ld, tp, r, W.data_ptr(), E.ld(W), p.n_ro, r, w, -1.0, 1.0,
+                           c_rows=rpos, atomic=1)
+                else:
+                    g1.add(eff.data_ptr() + 8 * p.hi * ld, ld, G.data_ptr(), E.ld(G), tp, r, w, r, p.n_ro, 1.0, 0.0,
+                           b_rows=rpos)
+                    g2.add(raw.data_ptr() + 8 * p.lo * ld, ld, tp, r, W.data_ptr(), E.ld(W), p.n_rd, r, w, -1.0, 1.0,
+                           c_rows=cpos, atomic=1)
+                self.flops += 2.0 * (p.n_rd + p.n_ro) * w * r
+        g1.launch()
+        g2.launch()
+
+    def approx_off_many(self, nodes, ranks):
+        """Alg. 3 for every compressed off-diagonal of the level (factor.py:486-505)."""
+        if not nodes:
+            return []
+        Gs = []
+        for node, rk in zip(nodes, ranks):
+            R = node.rows
+            rk = min(rk, R.size, node.ncols)
+            Gs.append(self.sketches.device(("off", node.j), R.size, rk, self.S))
+        Gs = self.off_mul_t_many(nodes, Gs)
+        for _ in range(self.cfg.power_iters):
+            Gs = self.off_mul_t_many(nodes, self.off_mul_many(nodes, Gs))
+        Us = self._orth_many(Gs)
+        Vs = self.off_mul_many(nodes, Us, final=True)
+        return self._lowrank_many(list(zip(Vs, Us)))
+
+    # -- diagonal trees, batched over trees ---------------------------------------
+    def leaves_many(self, items):
+        """items: (node, s) leaf blocks -> DenseTri (Alg. 6, diagblocks.py:276-300)."""
+        blocks = []
+        for node, s in items:
+            _, blk, _ = self.np.tree_maps[(node.j, s)]
+            lf = node.diag.shape.nodes[s]
+            k = lf.hi - lf.lo
+            blocks.append((blk, k, k))
+        Us = self._dense_many(blocks)
+        g = Grouped(False, True)
+        for (node, s), U in zip(items, Us):
+            tree = node.diag
+            maps, _, _ = self.np.tree_maps[(node.j, s)]
+            lf = tree.shape.nodes[s]
+            k = lf.hi - lf.lo
+            for m in maps:
+                raw, eff = self.src_panel[m.s]
+                w = raw.shape[1]
+                if w == 0:
+                    continue
+                ld = E.ld(raw)
+                g.add(eff.data_ptr() + 8 * m.rlo * ld, ld, raw.data_ptr() + 8 * m.clo * ld, ld, U.data_ptr(), k,
+                      m.rhi - m.rlo, m.chi - m.clo, w, -1.0, 1.0, c_rows=self._idx(m.ridx_off),
+                      c_cols=self._idx(m.cidx_off), atomic=1)
+                self.flops += 2.0 * (m.rhi - m.rlo) * (m.chi - m.clo) * w
+            for raw, eff, a, b, c, d in self._path_terms(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi)):
+                w = raw.shape[1]
+                if w == 0:
+                    continue
+                ld = E.ld(raw)
+                g.add(eff.data_ptr() + 8 * a * ld, ld, raw.data_ptr() + 8 * c * ld, ld, U.data_ptr(), k, b - a,
+                      d - c, w, -1.0, 1.0, atomic=1)
+                self.flops += 2.0 * (b - a) * (d - c) * w
+        g.launch()
+        return self._potrf_many([(U, node.u) for (node, s), U in zip(items, Us)])
+
+    def diag_mul_many(self, items, Gs, transpose, final=False):
+        """Alg. 5 for several (node, s) internal blocks at once (diagblocks.py:303-346)."""
+        mem = self.P if final else self.S
+        Ws, srcs, sol, spm = [], [], [], []
+        for (node, s), G in zip(items, Gs):
+            shape = node.diag.shape
+            (r0, r1), (c0, c1) = shape.span(s)
+            _, blk, blkT = self.np.tree_maps[(node.j, s)]
+            r = G.shape[1]
+            if not transpose:
+                G1 = self.S.empty(*G.shape)
+                if G.numel():
+                    G1.copy_(G)
+                sol.append((node, G1, True, shape.nodes[s].left.s))
+                self.flops += (c1 - c0) ** 2 * r
+                W = mem.empty(r1 - r0, r)
+                spm.append((blk, G1, W))
+                srcs.append(G1)
+            else:
+                W = mem.empty(c1 - c0, r)
+                spm.append((blkT, G, W))
+                srcs.append(G)
+            Ws.append(W)
+        if sol:
+            diag_solve_many(sol, self.S.empty)
+        self._spmm_many(spm)
+        g1, g2 = Grouped(True, False), Grouped(False, False)
+        for (node, s), src, W in zip(items, srcs, Ws):
+            tree = node.diag
+            (r0, r1), (c0, c1) = tree.shape.span(s)
+            maps, _, _ = self.np.tree_maps[(node.j, s)]
+            r = src.shape[1]
+            terms = []
+            for m in maps:
+                raw, eff = self.src_panel[m.s]
+                w = raw.shape[1]
+                if w:
+                    terms.append((raw, eff, w, m.clo, m.chi, m.rlo, m.rhi, self._idx(m.cidx_off),
+                                  self._idx(m.ridx_off)))
+            for raw, eff, a, b, c, d in self._path_terms(tree, s, (r0, r1), (c0, c1)):
+                w = raw.shape[1]
+                if w:
+                    terms.append((raw, eff, w, c, d, a, b, 0, 0))
+            if not terms or r == 0:
+                continue
+            T = self.S.empty(sum(t[2] for t in terms) * r)
+            o = 0
+            for raw, eff, w, clo, chi, rlo, rhi, cidx, ridx in terms:
+                ld = E.ld(raw)
+                tp = T.data_ptr() + 8 * o
+                o += w * r
+                if not transpose:
+                    g1.add(raw.data_ptr() + 8 * clo * ld, ld, src.data_ptr(), E.ld(src), tp, r, w, r, chi - clo, 1.0,
+                           0.0, b_rows=cidx)
+                    g2.add(eff.data_ptr() + 8 * rlo * ld, ld, tp, r, W.data_ptr(), E.ld(W), rhi - rlo, r, w, -1.0,
+                           1.0, c_rows=ridx, atomic=1)
+                else:
+                    g1.add(eff.data_ptr() + 8 * rlo * ld, ld, src.data_ptr(), E.ld(src), tp, r, w, r, rhi - rlo, 1.0,
+                           0.0, b_rows=ridx)
+                    g2.add(raw.data_ptr() + 8 * clo * ld, ld, tp, r, W.data_ptr(), E.ld(W), chi - clo, r, w, -1.0,
+                           1.0, c_rows=cidx, atomic=1)
+                self.flops += 2.0 * ((chi - clo) + (rhi - rlo)) * w * r
+        g1.launch()
+        g2.launch()
+        if transpose:
+            sol2 = []
+            for (node, s), W in zip(items, Ws):
+                (r0, r1), (c0, c1) = node.diag.shape.span(s)
+                sol2.append((node, W, False, node.diag.shape.nodes[s].left.s))
+                self.flops += (c1 - c0) ** 2 * W.shape[1]
+            diag_solve_many(sol2, self.S.empty)
+        return Ws
+
+    def approx_diag_many(self, items, ranks):
+        Gs = []
+        for (node, s), rk in zip(items, ranks):
+            (r0, r1), (c0, c1) = node.diag.shape.span(s)
+            rk = min(rk, r1 - r0, c1 - c0)
+            Gs.append(self.sketches.device(("diag", node.j, s), r1 - r0, rk, self.S))
+        Gs = self.diag_mul_many(items, Gs, True)
+        for _ in range(self.cfg.power_iters):
+            Gs = self.diag_mul_many(items, self.diag_mul_many(items, Gs, False), True)
+        Us = self._orth_many(Gs)
+        Vs = self.diag_mul_many(items, Us, False, final=True)
+        return self._lowrank_many(list(zip(Vs, Us)))
+
+    def trees_many(self, nodes):
+        """Build every diagonal tree of the level, advancing all trees one in-order
+        block position at a time (block s only needs blocks < s of its own tree)."""
+        for node in nodes:
+            node.diag = DeviceTree(self.np.tree_shapes[node.j])
+            self.counters["diag_trees"] += 1
+        maxlen = max((len(n.diag.shape.order) for n in nodes), default=0)
+        for p in range(maxlen):
+            self.S.reset()
+            leaves, comp, comp_r, dense = [], [], [], []
+            for node in nodes:
+                order = node.diag.shape.order
+                if p >= len(order):
+                    continue
+                s = order[p]
+                tn = node.diag.shape.nodes[s]
+                if tn.is_leaf:
+                    leaves.append((node, s))
+                    continue
+                nrows, ncols = tn.hi - tn.split, tn.split - tn.lo
+                r = block_rank(nrows, ncols, self.alpha_d, self.cfg.oversample)
+                if r >= DENSE_FALLBACK_FRACTION * min(nrows, ncols):
+                    dense.append((node, s))
+                else:
+                    comp.append((node, s))
+                    comp_r.append(r)
+            if leaves:
+                for (node, s), tri in zip(leaves, self.leaves_many(leaves)):
+                    node.diag.blocks[s] = tri
+            if dense:
+                eyes = []
+                for node, s in dense:
+                    tn = node.diag.shape.nodes[s]
+                    ncols = tn.split - tn.lo
+                    eye = self.S.zeros(ncols, ncols)
+                    eye.fill_diagonal_(1.0)
+                    eyes.append(eye)
+                for (node, s), W in zip(dense, self.diag_mul_many(dense, eyes, False, final=True)):
+                    node.diag.blocks[s] = W
+                    self.counters["dense_fallback"] += 1
+            if comp:
+                for (node, s), lr in zip(comp, self.approx_diag_many(comp, comp_r)):
+                    node.diag.blocks[s] = lr
+                    self.ranks[("diag", node.j, s)] = lr.k
+                    self.counters["compressed_diag"] += 1
+
+    # -- the sweep ------------------------------------------------------------------
+    def _run(self):
+        part = self.sym.partition
+        cfg = self.cfg
+        interiors = self.factor_interiors()
+        fail = self.first_interior_failure
+        if fail is not None:
+            self.pending.append((-1, 0, fail[0], fail[2], fail[1]))
+        by_unit = {}
+        for u, iu in interiors.items():
+            by_unit[u] = iu
+            sid = self.np.unit_source.get(u)
+            if sid is not None:
+                self.src_panel[sid] = (iu.off, iu.off)
+        for level in self.np.node_levels:
+            self.S.reset()
+            nodes, trees, dense, off_dense, off_tree, comp, comp_r = [], [], [], [], [], [], []
+            for u in level:
+                j = self.sym.units[u][1]
+                c0, c1 = part.cols(j)
+                nc = c1 - c0
+                R = part.rows[j]
+                node = NodeUnit(u, j, c0, c1, R)
+                nodes.append(node)
+                by_unit[u] = node
+                compress = bool(part.is_separator[j])
+                tree_diag = compress and j in self.sym.sep_splits
+                r_off = block_rank(R.size, nc, cfg.alpha_o, cfg.oversample)
+                compress_off = bool(compress and R.size and r_off < DENSE_FALLBACK_FRACTION * min(R.size, nc))
+                node._compress, node._compress_off = compress, compress_off
+                (trees if tree_diag else dense).append(node)
+                if R.size and compress_off:
+                    comp.append(node)
+                    comp_r.append(r_off)
+                elif R.size:
+                    (off_tree if tree_diag else off_dense).append(node)
+            # dense diagonals (+ their dense off-diagonal blocks)
+            if dense:
+                asm = self.assemble_many([(n, True, not n._compress_off) for n in dense])
+                tris = self._potrf_many([(UD, n.u) for n, (UD, UO) in zip(dense, asm)])
+                for n, tri, (UD, UO) in zip(dense, tris, asm):
+                    n.diag = tri
+                    n._UO = UO
+            # hierarchical diagonals
+            if trees:
+                self.trees_many(trees)
+            self.S.reset()
+            # dense off-diagonals
+            if off_dense:
+                lst = [n for n in off_dense]
+                E.trsm_batched("right", 1, [n.diag.L.data_ptr() for n in lst], [n.ncols for n in lst],
+                               [E.ld(n.diag.L) for n in lst], [n.diag.Dinv.data_ptr() for n in lst],
+                               [n._UO.data_ptr() for n in lst], [n._UO.shape[0] for n in lst],
+                               [E.ld(n._UO) for n in lst])
+                for n in lst:
+                    n.off = n._UO
+                    self.flops += n.rows.size * n.ncols**2
+            if off_tree:
+                asm = self.assemble_many([(n, False, True) for n in off_tree])
+                Xs = []
+                for n, (_, UO) in zip(off_tree, asm):
+                    X = self.S.empty(n.ncols, n.rows.size)
+                    X.copy_(UO.t())
+                    Xs.append(X)
+                diag_solve_many([(n, X, False) for n, X in zip(off_tree, Xs)], self.S.empty)
+                for n, X in zip(off_tree, Xs):
+                    n.off = self.P.empty(n.rows.size, n.ncols)
+                    n.off.copy_(X.t())
+            for n in off_dense + off_tree:
+                if n._compress:
+                    self.counters["dense_fallback"] += 1
+            # compressed off-diagonals
+            if comp:
+                for n, lr in zip(comp, self.approx_off_many(comp, comp_r)):
+                    n.off = lr
+                    self.ranks[("off", n.j)] = lr.k
+                    self.counters["compressed_off"] += 1
+            for n in nodes:
+                n._UO = None
+                sid = self.np.unit_source.get(n.u)
+                if sid is not None:
+                    self.src_panel[sid] = _raw_eff(n.off)
+        self.units = [by_unit[u] for u in range(len(self.sym.units))]
+
+    def check_pivots(self):
+        """Resolve every recorded pivot failure: the earliest unit in sweep order wins."""
+        if not self.pending:
+            return
+        info = self.ibuf[: self.ipos].cpu().numpy()
+        worst = None
+        for rec in self.pending:
+            off, cnt, unit, trees = rec[:4]
+            if off < 0:
+                cand = (unit, rec[4], trees)
+            else:
+                v = info[off:off + cnt]
+                bad = np.nonzero(v)[0]
+                if not bad.size:
+                    continue
+                cand = (unit, int(v[bad[0]]) - 1, trees)
+            if worst is None or cand[0] < worst[0]:
+                worst = cand
+        self.pending = []
+        if worst is not None:
+            raise _Indefinite(*worst)

@@ -195,7 +195,23 @@ class NumericPlan:
         self.tree_units = np.array(
             [u for u, (k, j) in enumerate(sym.units)
              if k == "node" and part.is_separator[j] and j in sym.sep_splits], dtype=np.int64)
-        self._sketch_cache = {}
+        # node units grouped by height in the source DAG: a node only reads sources of
+        # strictly lower height (interior blocks count as height -1), so each level
+        # is a set of independent nodes
+        height = {}
+        for u, (k, j) in enumerate(sym.units):
+            if k != "node":
+                continue
+            h = 0
+            for p in self.targets[j]:
+                su = self.sources[p.s].unit
+                if su in height:
+                    h = max(h, height[su] + 1)
+            height[u] = h
+        nlev = max(height.values()) + 1 if height else 0
+        self.node_levels = [[] for _ in range(nlev)]
+        for u in sorted(height):
+            self.node_levels[height[u]].append(u)
 
     def sketch_specs(self, cfg, alpha_d):
         """(key, m, r, seed) of every Gaussian sketch one numeric pass draws, in sweep
@@ -205,8 +221,9 @@ class NumericPlan:
 
         part = self.sym.partition
         specs = []
-        for kind, j in self.sym.units:
-            if kind != "node" or not part.is_separator[j]:
+        for u in [u for lev in self.node_levels for u in lev]:  # level-batched use order
+            j = self.sym.units[u][1]
+            if not part.is_separator[j]:
                 continue
             c0, c1 = part.cols(j)
             nc = c1 - c0
