@@ -148,6 +148,10 @@ def diag_solve_many(items, scratch):
 class LevelPass(NumericPass):
     """Level-batched version of NumericPass (same results, far fewer launches)."""
 
+    # fault injection for the restart tests (SURVEY §8(c)(5)): callable(pass, leaf
+    # items) -> True to make the first leaf of that batch indefinite
+    fault_hook = None
+
     # -- batched primitives ----------------------------------------------------
     def _interior_mats(self, ints):
         blocks = []
@@ -417,6 +421,8 @@ class LevelPass(NumericPass):
                       d - c, w, -1.0, 1.0, atomic=1)
                 self.flops += 2.0 * (b - a) * (d - c) * w
         g.launch()
+        if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
+            Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
         return self._potrf_many([(U, node.u) for (node, s), U in zip(items, Us)])
 
     def diag_mul_many(self, items, Gs, transpose, final=False):

@@ -68,3 +68,40 @@ def test_apply_is_symmetric_and_linear(cuda):
     Fu, Fv = F.apply(u), F.apply(v)
     assert abs(Fu @ v - u @ Fv) <= 1e-10 * abs(Fu @ v)
     assert relerr(F.apply(2.0 * u - 3.0 * v), 2.0 * Fu - 3.0 * Fv) < 1e-11
+
+
+def test_restart_alpha_trace_and_reraise(cuda):
+    """Restart protocol (factor.py:702-718): a failing leaf POTRF restarts the whole
+    pass with alpha_d *= 1.25; without a diagonal tree the error propagates."""
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.errors import IndefiniteError, TooManyRestarts
+    from paper_1507_05593_b200.factor import SolverConfig
+    from paper_1507_05593_b200.numeric import LevelPass
+    from paper_1507_05593_b200.problems import laplacian_3d
+
+    A, coords = laplacian_3d(12)
+    calls = {"passes": set()}
+
+    def fail_first_two(ps, items):
+        calls["passes"].add(id(ps))
+        return ps.alpha_d < 0.7  # passes at alpha_d 0.5 and 0.625 fail
+    LevelPass.fault_hook = fail_first_two
+    try:
+        F = factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64), coords=coords)
+        assert F.stats.restarts == 2
+        assert F.stats.alpha_d_history == [0.5, 0.625, 0.78125]
+        with pytest.raises(TooManyRestarts):
+            factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64, max_restarts=1), coords=coords)
+        LevelPass.fault_hook = lambda ps, items: True
+        with pytest.raises(TooManyRestarts):
+            factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64, max_restarts=3), coords=coords)
+    finally:
+        LevelPass.fault_hook = None
+    # no diagonal tree in play: an indefinite matrix re-raises IndefiniteError
+    from paper_1507_05593_b200.sparse import SparseSpdMatrix
+
+    M = A.dense()
+    M[5, 5] = 0.5  # diagonally dominant loss -> indefinite (Laplacian row sum > 0 broken)
+    M[5, 6] = M[6, 5] = -4.0
+    with pytest.raises(IndefiniteError):
+        factorize(SparseSpdMatrix.from_dense(M), SolverConfig(tau_o=float("inf")), coords=coords)
