@@ -26,6 +26,7 @@ Pivot failures are collected and resolved at the end of the pass in sweep order
 import numpy as np
 
 from . import engine as E
+from ._lib import GEMM_DTYPE
 from .factor import (
     DENSE_FALLBACK_FRACTION,
     DenseTri,
@@ -151,6 +152,33 @@ class LevelPass(NumericPass):
     # fault injection for the restart tests: callable(pass, leaf
     # items) -> True to make the first leaf of that batch indefinite
     fault_hook = None
+
+    def __init__(self, plan, cfg, alpha_d):
+        super().__init__(plan, cfg, alpha_d)
+        ns = len(plan.sources)
+        self.s_raw = np.zeros(ns, dtype=np.uint64)   # device address of the raw panel
+        self.s_eff = np.zeros(ns, dtype=np.uint64)   # ... of the eff panel (V U^T U or = raw)
+        self.s_ld = np.ones(ns, dtype=np.int64)
+        self.s_w = np.zeros(ns, dtype=np.int64)      # panel width (0 = contributes nothing)
+        self.idx_base = np.uint64(plan.idx.dev.data_ptr())
+
+    def _set_source(self, sid, raw, eff):
+        self.src_panel[sid] = (raw, eff)
+        self.s_raw[sid] = raw.data_ptr()
+        self.s_eff[sid] = eff.data_ptr()
+        self.s_ld[sid] = E.ld(raw)
+        self.s_w[sid] = raw.shape[1]
+
+    def _pairs(self, j, need_rd=True, need_ro=False):
+        """Flat descriptor arrays of target j's source pairs (widths > 0)."""
+        t = self.np.tarr[j]
+        s = t["s"]
+        keep = self.s_w[s] > 0
+        if need_rd:
+            keep &= t["nrd"] > 0
+        if need_ro:
+            keep &= t["nro"] > 0
+        return {k: v[keep] for k, v in t.items()}
 
     # -- batched primitives ----------------------------------------------------
     def _interior_mats(self, ints):
@@ -284,29 +312,40 @@ class LevelPass(NumericPass):
                 blocks.append((A_RC, R.size, nc))
         dense = self._dense_many(blocks)
         out = []
-        g = Grouped(False, True)
+        probs = []
         for (node, wd, wo), (iD, iO) in zip(items, layout):
             UD = dense[iD] if iD is not None else None
             UO = dense[iO] if iO is not None else None
             out.append((UD, UO))
             nc = node.ncols
-            for pr in self.np.targets[node.j]:
-                raw, eff = self.src_panel[pr.s]
-                w = raw.shape[1]
-                if w == 0 or pr.n_rd == 0:
+            t = self._pairs(node.j, need_rd=True)
+            if t["s"].size == 0:
+                continue
+            s = t["s"]
+            w, ld = self.s_w[s], self.s_ld[s]
+            cpos = self.idx_base + (4 * t["cpos"]).astype(np.uint64)
+            Qp = self.s_raw[s] + (8 * t["lo"] * ld).astype(np.uint64)
+            for tgt, rows_sel in ((UD, None), (UO, "ro")):
+                if tgt is None:
                     continue
-                ld = E.ld(raw)
-                cpos = self._idx(pr.cpos_off)
-                Q = raw.data_ptr() + 8 * pr.lo * ld
-                if UD is not None:
-                    g.add(eff.data_ptr() + 8 * pr.lo * ld, ld, Q, ld, UD.data_ptr(), nc, pr.n_rd, pr.n_rd, w,
-                          -1.0, 1.0, c_rows=cpos, c_cols=cpos, atomic=1)
-                    self.flops += 2.0 * pr.n_rd * pr.n_rd * w
-                if UO is not None and pr.n_ro > 0:
-                    g.add(eff.data_ptr() + 8 * pr.hi * ld, ld, Q, ld, UO.data_ptr(), nc, pr.n_ro, pr.n_rd, w,
-                          -1.0, 1.0, c_rows=self._idx(pr.rpos_off), c_cols=cpos, atomic=1)
-                    self.flops += 2.0 * pr.n_ro * pr.n_rd * w
-        g.launch()
+                sel = np.ones(s.size, dtype=bool) if rows_sel is None else t["nro"] > 0
+                if not sel.any():
+                    continue
+                p = np.zeros(int(sel.sum()), dtype=GEMM_DTYPE)
+                row0 = t["lo"] if rows_sel is None else t["hi"]
+                p["A"] = self.s_eff[s][sel] + (8 * row0[sel] * ld[sel]).astype(np.uint64)
+                p["lda"], p["ldb"] = ld[sel], ld[sel]
+                p["B"], p["C"], p["ldc"] = Qp[sel], tgt.data_ptr(), nc
+                p["M"] = t["nrd"][sel] if rows_sel is None else t["nro"][sel]
+                p["N"], p["K"] = t["nrd"][sel], w[sel]
+                p["c_rows"] = cpos[sel] if rows_sel is None else (
+                    self.idx_base + (4 * t["rpos"][sel]).astype(np.uint64))
+                p["c_cols"] = cpos[sel]
+                p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
+                probs.append(p)
+                self.flops += float(np.sum(2.0 * p["M"] * p["N"] * p["K"]))
+        if probs:
+            E.gemm_grouped(np.concatenate(probs), False, True)
         return out
 
     # -- implicit products, batched over nodes -----------------------------------
@@ -338,37 +377,50 @@ class LevelPass(NumericPass):
         return Ws
 
     def _products_many(self, nodes, Gs, Ws, trans):
-        g1, g2 = Grouped(True, False), Grouped(False, False)
+        """Source terms of Alg. 2 (trans=False: W[rpos] -= E[hi:] (V[lo:hi]^T G[cpos]))
+        or its mirror for all nodes: two grouped launches, descriptors built with
+        numpy over every (node, source) pair at once."""
+        parts = []
         for node, G, W in zip(nodes, Gs, Ws):
             r = G.shape[1]
             if r == 0 or W.numel() == 0:
                 continue
-            use = [p for p in self.np.targets[node.j]
-                   if p.n_rd > 0 and p.n_ro > 0 and self.src_panel[p.s][0].shape[1] > 0]
-            if not use:
+            t = self._pairs(node.j, need_rd=True, need_ro=True)
+            if t["s"].size == 0:
                 continue
-            T = self.S.empty(sum(self.src_panel[p.s][0].shape[1] for p in use) * r)
-            o = 0
-            for p in use:
-                raw, eff = self.src_panel[p.s]
-                w = raw.shape[1]
-                ld = E.ld(raw)
-                tp = T.data_ptr() + 8 * o
-                o += w * r
-                cpos, rpos = self._idx(p.cpos_off), self._idx(p.rpos_off)
-                if not trans:
-                    g1.add(raw.data_ptr() + 8 * p.lo * ld, ld, G.data_ptr(), E.ld(G), tp, r, w, r, p.n_rd, 1.0, 0.0,
-                           b_rows=cpos)
-                    g2.add(eff.data_ptr() + 8 * p.hi * ld, ld, tp, r, W.data_ptr(), E.ld(W), p.n_ro, r, w, -1.0, 1.0,
-                           c_rows=rpos, atomic=1)
-                else:
-                    g1.add(eff.data_ptr() + 8 * p.hi * ld, ld, G.data_ptr(), E.ld(G), tp, r, w, r, p.n_ro, 1.0, 0.0,
-                           b_rows=rpos)
-                    g2.add(raw.data_ptr() + 8 * p.lo * ld, ld, tp, r, W.data_ptr(), E.ld(W), p.n_rd, r, w, -1.0, 1.0,
-                           c_rows=cpos, atomic=1)
-                self.flops += 2.0 * (p.n_rd + p.n_ro) * w * r
-        g1.launch()
-        g2.launch()
+            parts.append((t, r, G.data_ptr(), E.ld(G), W.data_ptr(), E.ld(W)))
+        if not parts:
+            return
+        cat = lambda key: np.concatenate([p[0][key] for p in parts])
+        s, lo, hi, nrd, nro = cat("s"), cat("lo"), cat("hi"), cat("nrd"), cat("nro")
+        cpos = self.idx_base + (4 * cat("cpos")).astype(np.uint64)
+        rpos = self.idx_base + (4 * cat("rpos")).astype(np.uint64)
+        cnt = [p[0]["s"].size for p in parts]
+        rep = lambda i: np.repeat(np.array([p[i] for p in parts]), cnt)
+        r, gp, ldg, wp, ldw = rep(1), rep(2).astype(np.uint64), rep(3), rep(4).astype(np.uint64), rep(5)
+        w, ld = self.s_w[s], self.s_ld[s]
+        tsz = w * r
+        toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
+        T = self.S.empty(int(tsz.sum()))
+        tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
+        raw_lo = self.s_raw[s] + (8 * lo * ld).astype(np.uint64)
+        eff_hi = self.s_eff[s] + (8 * hi * ld).astype(np.uint64)
+        n = s.size
+        p1 = np.zeros(n, dtype=GEMM_DTYPE)
+        p2 = np.zeros(n, dtype=GEMM_DTYPE)
+        p1["B"], p1["ldb"], p1["C"], p1["ldc"], p1["M"], p1["N"] = gp, ldg, tp, r, w, r
+        p1["lda"], p1["batch"], p1["alpha"] = ld, 1, 1.0
+        p2["B"], p2["ldb"], p2["C"], p2["ldc"], p2["N"], p2["K"] = tp, r, wp, ldw, r, w
+        p2["lda"], p2["batch"], p2["alpha"], p2["beta"], p2["atomic"] = ld, 1, -1.0, 1.0, 1
+        if not trans:  # T = V[lo:hi]^T G1[cpos] ; W[rpos] -= E[hi:] T
+            p1["A"], p1["K"], p1["b_rows"] = raw_lo, nrd, cpos
+            p2["A"], p2["M"], p2["c_rows"] = eff_hi, nro, rpos
+        else:  # T = E[hi:]^T G[rpos] ; W[cpos] -= V[lo:hi] T
+            p1["A"], p1["K"], p1["b_rows"] = eff_hi, nro, rpos
+            p2["A"], p2["M"], p2["c_rows"] = raw_lo, nrd, cpos
+        E.gemm_grouped(p1, True, False)
+        E.gemm_grouped(p2, False, False)
+        self.flops += float(np.sum(2.0 * (nrd + nro) * w * r))
 
     def approx_off_many(self, nodes, ranks):
         """Alg. 3 for every compressed off-diagonal of the level (factor.py:486-505)."""
@@ -570,7 +622,7 @@ class LevelPass(NumericPass):
             by_unit[u] = iu
             sid = self.np.unit_source.get(u)
             if sid is not None:
-                self.src_panel[sid] = (iu.off, iu.off)
+                self._set_source(sid, iu.off, iu.off)
         for level in self.np.node_levels:
             self.S.reset()
             nodes, trees, dense, off_dense, off_tree, comp, comp_r = [], [], [], [], [], [], []
@@ -638,7 +690,7 @@ class LevelPass(NumericPass):
                 n._UO = None
                 sid = self.np.unit_source.get(n.u)
                 if sid is not None:
-                    self.src_panel[sid] = _raw_eff(n.off)
+                    self._set_source(sid, *_raw_eff(n.off))
         self.units = [by_unit[u] for u in range(len(self.sym.units))]
 
     def check_pivots(self):

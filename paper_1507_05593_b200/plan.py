@@ -263,6 +263,18 @@ class NumericPlan:
                 pairs.append(Pair(sid, int(lo), int(hi), self.idx.add(cpos), self.idx.add(rpos), rows.size))
             pairs.sort(key=lambda p: self.sources[p.s].order)
             self.targets[j] = pairs
+        # the same maps as flat arrays per target (vectorized descriptor builds)
+        self.tarr = {}
+        for j, pairs in self.targets.items():
+            self.tarr[j] = {
+                "s": np.array([p.s for p in pairs], dtype=np.int64),
+                "lo": np.array([p.lo for p in pairs], dtype=np.int64),
+                "hi": np.array([p.hi for p in pairs], dtype=np.int64),
+                "nrd": np.array([p.n_rd for p in pairs], dtype=np.int64),
+                "nro": np.array([p.n_ro for p in pairs], dtype=np.int64),
+                "cpos": np.array([p.cpos_off for p in pairs], dtype=np.int64),
+                "rpos": np.array([p.rpos_off for p in pairs], dtype=np.int64),
+            }
 
     def _build_tree_maps(self, part):
         """Window maps for every (tree node j, block s, source) with both windows
