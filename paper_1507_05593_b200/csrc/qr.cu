@@ -209,13 +209,14 @@ constexpr long long SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
 
 // multi-CTA path for sketches that do not fit one SM (qr_coop.cu)
 long long rsc_qrcp_coop_doubles(int m, int k);
-int rsc_qrcp_coop(const double *G, int m, int k, int ldg, double *Q, int ldq, int *rank_dev, double *work,
-                  cudaStream_t s);
+int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const int *k, const int *ldg,
+                   double *const *Q, const int *ldq, int *rank_dev, char *work, const long long *work_off,
+                   unsigned *bar, cudaStream_t s);
 
 static inline long long coop_bytes(int m, int k) { return ((rsc_qrcp_coop_doubles(m, k) * 8 + 255) / 256) * 256; }
 
 extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k) {
-    long long tot = 0;
+    long long tot = ((4LL * count + 255) / 256) * 256;  // group-barrier counters
     for (int i = 0; i < count; ++i) {
         const long long sz = (long long)(m[i] | 1) * k[i];
         if (sz > SMEM_LIMIT_DOUBLES) tot += coop_bytes(m[i], k[i]);
@@ -275,14 +276,15 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     };
     int rc = run(small, true);
     if (rc) return rc;
-    // large sketches: one cooperative multi-CTA QR each, workspace slices in the
-    // order rsc_qrcp_workspace_bytes sums them
-    long long off = 0;
+    // large sketches: all of them concurrently in cooperative multi-CTA groups;
+    // workspace = barrier counters, then per-matrix slices in index order
+    if (big.empty()) return 0;
+    std::vector<long long> off(count, 0);
+    long long o = ((4LL * count + 255) / 256) * 256;
     for (int i : big) {
-        rc = rsc_qrcp_coop(G[i], m[i], k[i], ldg[i], Q[i], ldq[i], rank_dev + i,
-                           (double *)((char *)work_dev + off), s);
-        if (rc) return rc;
-        off += coop_bytes(m[i], k[i]);
+        off[i] = o;
+        o += coop_bytes(m[i], k[i]);
     }
-    return 0;
+    return rsc_qrcp_multi((int)big.size(), big.data(), G, m, k, ldg, Q, ldq, rank_dev, (char *)work_dev,
+                          off.data(), (unsigned *)work_dev, s);
 }

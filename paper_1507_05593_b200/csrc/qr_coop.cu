@@ -1,58 +1,107 @@
-// Multi-CTA column-pivoted Householder QR for sketches too large for one SM
-// (e.g. 2048 x 508 off-diagonal sketches of the top separators).
+// Multi-matrix cooperative column-pivoted Householder QR.
 //
 // Same arithmetic contract as qrcp_kernel (LAPACK dlaqp2 pivoting, dlarfg
 // reflectors, partial-norm downdating with the sqrt(eps) recomputation test,
-// dorg2r for the kept columns; reference kernels.py:67-82), distributed by
-// COLUMN OWNERSHIP: CTA b owns physical columns [b*cpc, (b+1)*cpc) and keeps them in
-// shared memory for the whole factorization.  Pivoting never moves data: every CTA
-// keeps the same position->column permutation and applies LAPACK's swap sequence
-// to it redundantly, so the "first position of the largest partial norm" rule is
-// reproduced exactly.  Per step: the owner of the pivot column forms the
-// reflector and publishes it (v, tau) -> grid sync -> every CTA updates its own
-// columns and downdates their norms -> grid sync.
+// dorg2r for the kept columns; reference kernels.py:67-82), for sketches that do
+// not fit one SM and for running many such QRs at once.
 //
-// Q is formed afterwards by an ordinary kernel: column j of Q is
-// H_0 ... H_j e_j applied right-to-left (dorg2r order), one warp per column.
-#include <cooperative_groups.h>
+// Every matrix of a launch gets a GROUP of CTAs; CTA b of a group owns physical
+// columns [b*cpc, (b+1)*cpc) and keeps them in shared memory for the whole
+// factorization.  Pivoting never moves data: every CTA keeps the same
+// position->column permutation and applies LAPACK's swap sequence to it
+// redundantly, so "first position of the largest partial norm" is reproduced
+// exactly.  Per column: the owner of the pivot column forms and publishes the
+// reflector -> group barrier -> every CTA updates its own columns and downdates
+// their norms -> group barrier.  Group barriers are release/acquire counters
+// (one per matrix), so the QRs of a whole ND level run concurrently; the launch is
+// cooperative, which guarantees every CTA of every group is co-resident.
+//
+// Q is formed afterwards (qr_form_q_kernel): column j of Q is H_0 ... H_j e_j
+// applied right-to-left (dorg2r order), one warp per column.
+#include <algorithm>
+#include <vector>
 #include "common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace {
 
 constexpr int CT = 256;  // threads per CTA (8 warps)
+constexpr int MAXM = 96;
 constexpr double EPS = 2.220446049250313e-16;
 constexpr double TOL3Z = 1.0536712127723509e-08;
+constexpr size_t SMEM_BUDGET = 200 * 1024;
 
-struct CoopArgs {
+struct MatDesc {
     const double *G;
-    int ldg, m, k, ldw, cpc;
-    double *W;      // global column-major spill (ldw x k): reflectors for the Q kernel
-    double *vn1, *vn2, *tau, *diagR, *vbuf;
-    int *perm;      // final position -> physical column
+    double *Q;
+    double *W;  // per-matrix workspace: cols (ldw*k) | vn1 | vn2 | tau | diagR | vbuf(m) | perm(k ints)
+    int *rank;
+    int m, k, ldg, ldq, ldw, cpc, nblk, blk0;
 };
 
+struct MArgs {
+    int count;
+    unsigned *bar;  // one zeroed counter per matrix
+    MatDesc d[MAXM];
+};
+
+struct Ws {
+    double *cols, *vn1, *vn2, *tau, *diagR, *vbuf;
+    int *perm;
+};
+
+__device__ __forceinline__ Ws carve(const MatDesc &d) {
+    Ws w;
+    w.cols = d.W;
+    w.vn1 = d.W + (long long)d.ldw * d.k;
+    w.vn2 = w.vn1 + d.k;
+    w.tau = w.vn2 + d.k;
+    w.diagR = w.tau + d.k;
+    w.vbuf = w.diagR + d.k;
+    w.perm = reinterpret_cast<int *>(w.vbuf + d.m);
+    return w;
+}
+
+__device__ __forceinline__ void group_barrier(unsigned *ctr, int nblk, unsigned &epoch) {
+    __syncthreads();
+    if (nblk > 1) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ctr, 1u);
+            const unsigned target = (epoch + 1) * (unsigned)nblk;
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+            } while (v < target);
+        }
+        __syncthreads();
+    }
+    ++epoch;
+}
+
 template <bool SMEM>
-__global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
-    cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs a) {
     extern __shared__ __align__(16) double sm[];
-    const int m = a.m, k = a.k, ldw = a.ldw, cpc = a.cpc;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = CT / 32;
-    const int c0 = blockIdx.x * cpc, c1 = min(k, c0 + cpc);
-    double *cols = SMEM ? sm : a.W + (long long)c0 * ldw;            // owned columns
-    double *v = SMEM ? sm + (long long)cpc * ldw : nullptr;            // reflector copy
-    int *pos2phys = reinterpret_cast<int *>(SMEM ? v + m : sm);
-    int *posof = pos2phys + k;
     __shared__ double red[32];
     __shared__ int piv_s;
-    __shared__ double vsm_fallback[1];
-    (void)vsm_fallback;
+    // locate this CTA's matrix
+    int g = 0;
+    while (g + 1 < a.count && (int)blockIdx.x >= a.d[g + 1].blk0) ++g;
+    const MatDesc &d = a.d[g];
+    const Ws w = carve(d);
+    unsigned *bar = a.bar + g;
+    const int m = d.m, k = d.k, ldw = d.ldw, cpc = d.cpc, nblk = d.nblk;
+    const int lb = blockIdx.x - d.blk0;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = CT / 32;
+    const int c0 = lb * cpc, c1 = min(k, c0 + cpc);
+    double *cols = SMEM ? sm : w.cols + (long long)c0 * ldw;
+    double *v = SMEM ? sm + (long long)cpc * ldw : nullptr;
+    int *pos2phys = reinterpret_cast<int *>(SMEM ? v + m : sm);
+    int *posof = pos2phys + k;
+    unsigned epoch = 0;
 
-    // load owned columns (transposed from row-major G) and their norms
     for (long long e = t; e < (long long)m * (c1 - c0); e += CT) {
         const int r = (int)(e / (c1 - c0)), j = (int)(e % (c1 - c0));
-        cols[(long long)j * ldw + r] = a.G[(long long)r * a.ldg + c0 + j];
+        cols[(long long)j * ldw + r] = d.G[(long long)r * d.ldg + c0 + j];
     }
     for (int j = t; j < k; j += CT) { pos2phys[j] = j; posof[j] = j; }
     __syncthreads();
@@ -61,9 +110,9 @@ __global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
         double s = 0.0;
         for (int r = lane; r < m; r += 32) s += cj[r] * cj[r];
         s = sqrt(warp_sum(s));
-        if (lane == 0) { a.vn1[c0 + j] = s; a.vn2[c0 + j] = s; }
+        if (lane == 0) { w.vn1[c0 + j] = s; w.vn2[c0 + j] = s; }
     }
-    grid.sync();
+    group_barrier(bar, nblk, epoch);
 
     const int kmin = m < k ? m : k;
     for (int i = 0; i < kmin; ++i) {
@@ -72,7 +121,7 @@ __global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
             double best = -1.0;
             int bp = k;
             for (int j = i + lane; j < k; j += 32) {
-                const double vv = __ldcg(a.vn1 + pos2phys[j]);
+                const double vv = __ldcg(w.vn1 + pos2phys[j]);
                 if (vv > best) { best = vv; bp = j; }
             }
 #pragma unroll
@@ -82,7 +131,7 @@ __global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
                 if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
             }
             if (lane == 0) {
-                if (bp >= k) bp = i;  // NaN norms: keep the order
+                if (bp >= k) bp = i;  // NaN norms (failed upstream pivot): keep the order
                 const int ci = pos2phys[i], cp = pos2phys[bp];
                 pos2phys[i] = cp; pos2phys[bp] = ci;
                 posof[cp] = i; posof[ci] = bp;
@@ -91,7 +140,7 @@ __global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
         }
         __syncthreads();
         const int pc = piv_s;
-        // 2. the owner of the pivot column forms and publishes the reflector
+        // 2. the owner of the pivot column forms and publishes the reflector (dlarfg)
         if (pc >= c0 && pc < c1) {
             double *ci = cols + (long long)(pc - c0) * ldw;
             double part = 0.0;
@@ -108,77 +157,93 @@ __global__ void __launch_bounds__(CT) qrcp_coop_kernel(const CoopArgs a) {
             for (int r = i + 1 + t; r < m; r += CT) {
                 const double x = (xnorm != 0.0) ? ci[r] * scal : ci[r];
                 ci[r] = x;
-                a.vbuf[r] = x;
+                if (nblk > 1) w.vbuf[r] = x;
             }
             if (t == 0) {
                 ci[i] = beta;
-                a.vbuf[i] = 1.0;
-                a.tau[i] = tau;
-                a.diagR[i] = beta;
+                w.tau[i] = tau;
+                w.diagR[i] = beta;
             }
-            __threadfence();
         }
-        grid.sync();
-        // 3. every CTA applies H_i^T to its unchosen columns and downdates their norms
-        const double tau = __ldcg(a.tau + i);
+        group_barrier(bar, nblk, epoch);
+        // 3. apply H_i^T to the unchosen owned columns, downdate their norms
+        const double tau = __ldcg(w.tau + i);
         const double *vsrc;
-        if (SMEM) {
-            for (int r = i + t; r < m; r += CT) v[r] = __ldcg(a.vbuf + r);
+        if (nblk == 1) {
+            vsrc = cols + (long long)(pc - c0) * ldw;  // the reflector lives in this CTA
+        } else if (SMEM) {
+            for (int r = i + 1 + t; r < m; r += CT) v[r] = __ldcg(w.vbuf + r);
             __syncthreads();
             vsrc = v;
         } else {
-            vsrc = a.vbuf;
+            vsrc = w.vbuf;
         }
         for (int j = warp; j < c1 - c0; j += nw) {
             const int phys = c0 + j;
             if (posof[phys] <= i) continue;
             double *cj = cols + (long long)j * ldw;
             if (tau != 0.0) {
-                double w = 0.0;
-                for (int r = i + 1 + lane; r < m; r += 32) w += (SMEM ? vsrc[r] : __ldcg(vsrc + r)) * cj[r];
-                w = warp_sum(w) + cj[i];
-                const double f = tau * w;
-                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * (SMEM ? vsrc[r] : __ldcg(vsrc + r));
+                double s = 0.0;
+                for (int r = i + 1 + lane; r < m; r += 32) s += ((SMEM || nblk == 1) ? vsrc[r] : __ldcg(vsrc + r)) * cj[r];
+                s = warp_sum(s) + cj[i];
+                const double f = tau * s;
+                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * ((SMEM || nblk == 1) ? vsrc[r] : __ldcg(vsrc + r));
                 __syncwarp();
                 if (lane == 0) cj[i] -= f;
                 __syncwarp();
             }
-            const double v1 = a.vn1[phys];
+            const double v1 = w.vn1[phys];
             if (v1 != 0.0) {
                 double temp = fabs(cj[i]) / v1;
                 temp = 1.0 - temp * temp;
                 temp = temp < 0.0 ? 0.0 : temp;
-                const double ratio = v1 / a.vn2[phys];
+                const double ratio = v1 / w.vn2[phys];
                 const double temp2 = temp * ratio * ratio;
                 if (temp2 <= TOL3Z) {
                     double s = 0.0;
                     for (int r = i + 1 + lane; r < m; r += 32) s += cj[r] * cj[r];
                     s = (i + 1 < m) ? sqrt(warp_sum(s)) : 0.0;
-                    if (lane == 0) { a.vn1[phys] = s; a.vn2[phys] = s; }
+                    if (lane == 0) { w.vn1[phys] = s; w.vn2[phys] = s; }
                 } else if (lane == 0) {
-                    a.vn1[phys] = v1 * sqrt(temp);
+                    w.vn1[phys] = v1 * sqrt(temp);
                 }
             }
             __syncwarp();
         }
-        __threadfence();
-        grid.sync();
+        group_barrier(bar, nblk, epoch);
     }
     // spill the owned columns (reflectors) for the Q kernel; publish the permutation
     if (SMEM)
-        for (long long e = t; e < (long long)ldw * (c1 - c0); e += CT) a.W[(long long)c0 * ldw + e] = cols[e];
-    if (blockIdx.x == 0)
-        for (int j = t; j < k; j += CT) a.perm[j] = pos2phys[j];
+        for (long long e = t; e < (long long)ldw * (c1 - c0); e += CT) w.cols[(long long)c0 * ldw + e] = cols[e];
+    if (lb == 0)
+        for (int j = t; j < k; j += CT) w.perm[j] = pos2phys[j];
 }
 
-// Q[:, j] = H_0 ... H_j e_j for j < rank; one warp per output column, the column
-// lives in shared memory.  Also writes the kept rank (every CTA computes it).
-__global__ void __launch_bounds__(CT) qr_form_q_kernel(const double *__restrict__ W, int ldw, int m, int k,
-                                                        const int *__restrict__ perm,
-                                                        const double *__restrict__ tau,
-                                                        const double *__restrict__ diagR, double *Q, int ldq,
-                                                        int *rank_out, int warps_per_cta) {
+struct QDesc {
+    double *W;
+    double *Q;
+    int *rank;
+    int m, k, ldw, ldq, blk0, nblk, wpc;
+};
+
+struct QArgs {
+    int count;
+    QDesc d[MAXM];
+};
+
+// Q[:, j] = H_0 ... H_j e_j for j < rank; one warp per output column (in smem);
+// also publishes the kept rank (kernels.py:78-81)
+__global__ void __launch_bounds__(CT) mq_form_q_kernel(const __grid_constant__ QArgs a) {
     extern __shared__ __align__(16) double qcol[];
+    int g = 0;
+    while (g + 1 < a.count && (int)blockIdx.x >= a.d[g + 1].blk0) ++g;
+    const QDesc &d = a.d[g];
+    const int m = d.m, k = d.k, ldw = d.ldw;
+    const double *W = d.W;
+    const double *vn1 = W + (long long)ldw * k;
+    const double *tau = vn1 + 2 * k;
+    const double *diagR = tau + k;
+    const int *perm = reinterpret_cast<const int *>(diagR + k + m);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ int rank_s;
     if (threadIdx.x == 0) {
@@ -191,12 +256,12 @@ __global__ void __launch_bounds__(CT) qr_form_q_kernel(const double *__restrict_
                 if (fabs(diagR[i]) > cut) ++r;
         }
         rank_s = r;
-        if (blockIdx.x == 0) *rank_out = r;
+        if (blockIdx.x == d.blk0) *d.rank = r;
     }
     __syncthreads();
     const int rank = rank_s;
-    if (warp >= warps_per_cta) return;
-    const int j = blockIdx.x * warps_per_cta + warp;
+    if (warp >= d.wpc) return;
+    const int j = (blockIdx.x - d.blk0) * d.wpc + warp;
     if (j >= rank) return;
     double *q = qcol + (long long)warp * m;
     for (int r = lane; r < m; r += 32) q[r] = (r == j) ? 1.0 : 0.0;
@@ -204,80 +269,138 @@ __global__ void __launch_bounds__(CT) qr_form_q_kernel(const double *__restrict_
     for (int i = j; i >= 0; --i) {
         const double *vi = W + (long long)perm[i] * ldw;  // v_i[i] = 1 implicitly
         const double ti = tau[i];
-        double w = 0.0;
-        for (int r = i + 1 + lane; r < m; r += 32) w += vi[r] * q[r];
-        w = warp_sum(w) + q[i];
-        const double f = ti * w;
+        double s = 0.0;
+        for (int r = i + 1 + lane; r < m; r += 32) s += vi[r] * q[r];
+        s = warp_sum(s) + q[i];
+        const double f = ti * s;
         __syncwarp();
         for (int r = i + 1 + lane; r < m; r += 32) q[r] -= f * vi[r];
         if (lane == 0) q[i] -= f;
         __syncwarp();
     }
-    for (int r = lane; r < m; r += 32) Q[(long long)r * ldq + j] = q[r];
+    for (int r = lane; r < m; r += 32) d.Q[(long long)r * d.ldq + j] = q[r];
+}
+
+inline size_t smem_for(int m, int k, int cpc) {
+    const size_t ldw = (size_t)(m | 1);
+    return (size_t)cpc * ldw * 8 + (size_t)m * 8 + sizeof(int) * 2 * (size_t)k;
 }
 
 }  // namespace
 
-// workspace doubles of one cooperative QR
+// workspace doubles of one matrix
 long long rsc_qrcp_coop_doubles(int m, int k) {
     const long long ldw = m | 1;
     return ldw * k + 4LL * k + m + k + 64;
 }
 
-int rsc_qrcp_coop(const double *G, int m, int k, int ldg, double *Q, int ldq, int *rank_dev, double *work,
-                  cudaStream_t s) {
+// Factor `n` matrices (indices into the arrays) concurrently.  work_off[i] is the
+// byte offset of matrix i's workspace in `work`; bar has >= n zeroable counters.
+int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const int *k, const int *ldg,
+                   double *const *Q, const int *ldq, int *rank_dev, char *work, const long long *work_off,
+                   unsigned *bar, cudaStream_t s) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    CoopArgs a;
-    a.G = G; a.ldg = ldg; a.m = m; a.k = k; a.ldw = m | 1;
-    a.W = work;
-    a.vn1 = work + (long long)a.ldw * k;
-    a.vn2 = a.vn1 + k;
-    a.tau = a.vn2 + k;
-    a.diagR = a.tau + k;
-    a.vbuf = a.diagR + k;
-    a.perm = reinterpret_cast<int *>(a.vbuf + m);
-    int cpc = (k + nsm - 1) / nsm;
-    const size_t idx_bytes = sizeof(int) * 2 * (size_t)k;
-    size_t smem = (size_t)cpc * a.ldw * 8 + (size_t)m * 8 + idx_bytes;
-    const bool use_smem = smem <= 200 * 1024;
-    void *fn;
-    if (use_smem) {
-        fn = (void *)qrcp_coop_kernel<true>;
-    } else {
-        smem = idx_bytes;
-        fn = (void *)qrcp_coop_kernel<false>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(mqrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
+        cudaFuncSetAttribute(mqrcp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        cudaFuncSetAttribute(mq_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET);
+        attr = true;
     }
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, CT, smem);
-    if (per_sm < 1) return 77;
-    // enough CTAs to own every column, never more than can be co-resident
-    int nblk = (k + cpc - 1) / cpc;
-    while (nblk > nsm * per_sm) {
-        ++cpc;
-        nblk = (k + cpc - 1) / cpc;
+    // per-matrix plan: fewest CTAs whose owned columns fit shared memory
+    struct P { int i, cpc, nblk; bool smem; size_t sm; };
+    std::vector<P> plans;
+    for (int t = 0; t < n; ++t) {
+        const int i = ids[t];
+        if (m[i] <= 0 || k[i] <= 0) continue;
+        const size_t fixed = (size_t)m[i] * 8 + sizeof(int) * 2 * (size_t)k[i];
+        const size_t per_col = (size_t)(m[i] | 1) * 8;
+        int cpc = fixed < SMEM_BUDGET ? (int)((SMEM_BUDGET - fixed) / per_col) : 0;
+        if (cpc >= 1) {
+            cpc = std::min(cpc, k[i]);
+            const int nblk = (k[i] + cpc - 1) / cpc;
+            if (nblk <= nsm) {
+                plans.push_back({i, cpc, nblk, true, smem_for(m[i], k[i], cpc)});
+                continue;
+            }
+        }
+        cpc = (k[i] + nsm - 1) / nsm;  // global-memory columns, one group over all SMs
+        plans.push_back({i, cpc, (k[i] + cpc - 1) / cpc, false, sizeof(int) * 2 * (size_t)k[i]});
     }
-    if (use_smem) {
-        smem = (size_t)cpc * a.ldw * 8 + (size_t)m * 8 + idx_bytes;
-        if (smem > 200 * 1024) return 78;
+    cudaMemsetAsync(bar, 0, sizeof(unsigned) * (size_t)std::max(n, 1), s);
+    static thread_local MArgs ma;
+    static thread_local QArgs qa;
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool smem = pass == 0;
+        size_t pos = 0;
+        std::vector<P> sel;
+        for (auto &p : plans)
+            if (p.smem == smem) sel.push_back(p);
+        while (pos < sel.size()) {
+            // pack groups while they fit co-resident
+            size_t sm = 0;
+            int blocks = 0, cnt = 0;
+            size_t start = pos;
+            while (pos < sel.size() && cnt < MAXM) {
+                const size_t sm2 = std::max(sm, sel[pos].sm);
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, CT, sm2);
+                if (per_sm < 1) return 77;
+                if (cnt > 0 && blocks + sel[pos].nblk > nsm * per_sm) break;
+                sm = sm2;
+                blocks += sel[pos].nblk;
+                ++cnt;
+                ++pos;
+            }
+            ma.count = cnt;
+            ma.bar = bar;
+            int b0 = 0;
+            for (int c = 0; c < cnt; ++c) {
+                const P &p = sel[start + c];
+                const int i = p.i;
+                MatDesc &d = ma.d[c];
+                d.G = G[i]; d.Q = Q[i];
+                d.W = reinterpret_cast<double *>(work + work_off[i]);
+                d.rank = rank_dev + i;
+                d.m = m[i]; d.k = k[i]; d.ldg = ldg[i]; d.ldq = ldq[i]; d.ldw = m[i] | 1;
+                d.cpc = p.cpc; d.nblk = p.nblk; d.blk0 = b0;
+                b0 += p.nblk;
+            }
+            // distinct barrier counter per matrix of this launch
+            ma.bar = bar + start + (smem ? 0 : 0);
+            void *args[] = {&ma};
+            cudaError_t e = cudaLaunchCooperativeKernel(
+                smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, dim3(b0), dim3(CT), args, sm, s);
+            rsc_count_launch();
+            if (e != cudaSuccess) return (int)e;
+            // Q formation for the same matrices
+            qa.count = cnt;
+            int q0 = 0;
+            size_t qsm = 0;
+            for (int c = 0; c < cnt; ++c) {
+                const MatDesc &d = ma.d[c];
+                int wpc = (int)(SMEM_BUDGET / ((size_t)d.m * 8));
+                wpc = wpc < 1 ? 1 : (wpc > CT / 32 ? CT / 32 : wpc);
+                if ((size_t)d.m * 8 > SMEM_BUDGET) return 79;
+                QDesc &q = qa.d[c];
+                q.W = d.W; q.Q = d.Q; q.rank = d.rank;
+                q.m = d.m; q.k = d.k; q.ldw = d.ldw; q.ldq = d.ldq;
+                q.wpc = wpc; q.blk0 = q0;
+                const int kmin = d.m < d.k ? d.m : d.k;
+                q.nblk = std::max(1, (kmin + wpc - 1) / wpc);
+                q0 += q.nblk;
+                qsm = std::max(qsm, (size_t)wpc * d.m * 8);
+            }
+            mq_form_q_kernel<<<q0, CT, qsm, s>>>(qa);
+            RSC_CHECK_LAUNCH();
+        }
+        // second pass uses fresh counters beyond the first pass's
+        if (pass == 0) {
+            bar += sel.size();
+        }
     }
-    a.cpc = cpc;
-    void *args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(nblk), dim3(CT), args, smem, s);
-    rsc_count_launch();
-    if (e != cudaSuccess) return (int)e;
-    // Q formation
-    int wpc = (int)((200 * 1024) / ((size_t)m * 8));
-    wpc = wpc < 1 ? 1 : (wpc > CT / 32 ? CT / 32 : wpc);
-    if ((size_t)m * 8 > 200 * 1024) return 79;
-    const size_t qsmem = (size_t)wpc * m * 8;
-    cudaFuncSetAttribute(qr_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem);
-    const int kmin = m < k ? m : k;
-    const int qblocks = (kmin + wpc - 1) / wpc;
-    qr_form_q_kernel<<<qblocks > 0 ? qblocks : 1, CT, qsmem, s>>>(a.W, a.ldw, m, k, a.perm, a.tau, a.diagR, Q, ldq,
-                                                                  rank_dev, wpc);
-    RSC_CHECK_LAUNCH();
     return 0;
 }

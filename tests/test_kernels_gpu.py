@@ -144,3 +144,30 @@ def test_orthonormalize_multi_cta_path(cuda, m, k, true_rank):
     assert Q.shape == Qo.shape
     assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() < 1e-12
     assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
+
+
+def test_qrcp_batched_mixed_sizes_concurrent(cuda):
+    """One batched call mixing one-CTA sketches and multi-CTA groups (run concurrently)."""
+    import torch
+    from oracle import kernels as ok
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(9)
+    shapes = [(256, 58), (300, 120), (2048, 40), (700, 333), (64, 16), (1500, 210), (260, 101)]
+    Gs = []
+    for i, (m, k) in enumerate(shapes):
+        r = min(m, k) if i % 2 == 0 else max(2, min(m, k) // 2)
+        Gs.append(rng.standard_normal((m, r)) @ rng.standard_normal((r, k)))
+    Gd = [E.to_dev(G) for G in Gs]
+    Qd = [E.empty(*G.shape) for G in Gs]
+    rank = E.zeros(len(Gs), dtype=E.I32)
+    work = E.qrcp_batched([g.data_ptr() for g in Gd], [s[0] for s in shapes], [s[1] for s in shapes],
+                          [s[1] for s in shapes], [q.data_ptr() for q in Qd], [s[1] for s in shapes], rank)
+    torch.cuda.synchronize()
+    ranks = rank.cpu().numpy()
+    for i, G in enumerate(Gs):
+        Qo = ok.orth(G)
+        assert ranks[i] == Qo.shape[1], (i, ranks[i], Qo.shape)
+        Q = Qd[i][:, :ranks[i]].cpu().numpy()
+        assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
+    del work
