@@ -131,10 +131,12 @@ class DeviceApply:
 
     def _sweep(self):
         y = self.y
+        from .numeric import run_waves, tree_ops
+
         for L in self.levels:
             L["fwd_diag"].run()
-            for u in L["trees"]:
-                u.diag.solve(y[u.c0:u.c1], False)
+            if L["trees"]:  # Alg. 4 of every tree of the level in lock-step waves
+                run_waves([tree_ops(u.diag, None, y[u.c0:u.c1], False) for u in L["trees"]], E.scratch)
             self._g(L["fd"])
             self._g(L["fl1"], True)
             self._g(L["fl2"])
@@ -142,8 +144,8 @@ class DeviceApply:
             self._g(L["bd"], True)
             self._g(L["bl1"], True)
             self._g(L["bl2"])
-            for u in L["trees"]:
-                u.diag.solve(y[u.c0:u.c1], True)
+            if L["trees"]:
+                run_waves([tree_ops(u.diag, None, y[u.c0:u.c1], True) for u in L["trees"]], E.scratch)
             L["bwd_diag"].run()
 
     def _body(self):
@@ -152,10 +154,14 @@ class DeviceApply:
         self._sweep()
         E.gather_rows(self.fwd, self.y, self.zbuf.reshape(n, 1))
 
+    # eager applies before the sweep is captured into a CUDA graph (capture costs
+    # about two eager applies; PCG with 1-3 iterations never amortises it)
+    GRAPH_AFTER = 3
+
     def __call__(self, r_dev, out=None):
         self.r_in.copy_(r_dev.reshape(-1))
-        if self.graph is None:
-            self._body()  # eager first run (warms the caching allocator)
+        self.calls = getattr(self, "calls", 0) + 1
+        if self.graph is None and self.calls > self.GRAPH_AFTER:
             try:
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())
@@ -167,12 +173,10 @@ class DeviceApply:
                 self.graph = g
             except Exception:
                 self.graph = False
-            # recompute in the normal stream (the eager result above is valid too)
-            self._body()
-        elif self.graph is False:
-            self._body()
-        else:
+        if self.graph:
             self.graph.replay()
+        else:
+            self._body()
         z = out if out is not None else E.empty(self.n)
         z.copy_(self.zbuf)
         return z

@@ -37,6 +37,19 @@ def zeros(*shape, dtype=F64):
     return torch.zeros(*shape, dtype=dtype, device=dev())
 
 
+_CHUNK_POOL = []  # device chunks of dead arenas, reused before any new cudaMalloc
+
+
+def _take_chunk(n):
+    best = None
+    for i, c in enumerate(_CHUNK_POOL):
+        if c.numel() >= n and (best is None or c.numel() < _CHUNK_POOL[best].numel()):
+            best = i
+    if best is not None:
+        return _CHUNK_POOL.pop(best)
+    return torch.empty(n, dtype=F64, device=dev())
+
+
 class Arena:
     """Bump allocator over large FP64 device chunks.
 
@@ -69,7 +82,15 @@ class Arena:
                 self.i += 1
                 self.off = 0
                 continue
-            self.chunks.append(torch.empty(max(self.chunk, need), dtype=F64, device=dev()))
+            self.chunks.append(_take_chunk(max(self.chunk, need)))
+
+    def __del__(self):
+        try:
+            for c in self.chunks:
+                _CHUNK_POOL.append(c)
+            self.chunks = []
+        except Exception:
+            pass
 
     def zeros(self, *shape):
         t = self.empty(*shape)

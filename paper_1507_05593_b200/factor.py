@@ -895,6 +895,7 @@ def factorize(A, config=None, coords=None, prepared=None):
     t3 = time.perf_counter()
     F = RankStructuredFactor(A.n, sym, plan, config)
     F.units = ps.units
+    F._mem = ps.P  # the factor owns its arena: chunks return to the pool only when F dies
     F.ranks = ps.ranks
     part = sym.partition
     st = F.stats

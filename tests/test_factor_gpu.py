@@ -105,3 +105,21 @@ def test_restart_alpha_trace_and_reraise(cuda):
     M[5, 6] = M[6, 5] = -4.0
     with pytest.raises(IndefiniteError):
         factorize(SparseSpdMatrix.from_dense(M), SolverConfig(tau_o=float("inf")), coords=coords)
+
+
+def test_apply_graph_replay_matches_eager(cuda):
+    """After a few eager applies the sweep is replayed from a CUDA graph."""
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.factor import SolverConfig
+    from paper_1507_05593_b200.problems import laplacian_3d
+
+    A, coords = laplacian_3d(14)
+    F = factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64), coords=coords)
+    rng = np.random.default_rng(6)
+    vs = [rng.standard_normal(A.n) for _ in range(3)]
+    eager = [F.apply(v) for v in vs]
+    for _ in range(2):
+        again = [F.apply(v) for v in vs]
+        for a, b in zip(eager, again):
+            assert relerr(b, a) < 1e-12
+    assert F._apply.graph not in (None, False)
