@@ -77,6 +77,7 @@ def run_waves(seqs, scratch):
     if not seqs:
         return
     for w in range(max(len(s) for s in seqs)):
+        keep = []  # temporaries must outlive the launches below (torch may recycle freed blocks)
         leaves = {0: [], 1: []}
         dense = {False: Grouped(False, False), True: Grouped(True, False)}
         lr1 = {False: Grouped(True, False), True: Grouped(True, False)}
@@ -98,6 +99,7 @@ def run_waves(seqs, scratch):
                 if b.k == 0:
                     continue
                 t = scratch(b.k, r)
+                keep.append(t)
                 # t = U^T X (forward) or V^T X (transposed); then Y -= V t or U t
                 P1 = b.V if tr else b.U
                 P2 = b.U if tr else b.V

@@ -12,6 +12,8 @@ CASES = {
     "cfg0": ("laplacian_2d", (128,), False, dict(), False),
     "l3d24": ("laplacian_3d", (24,), False, dict(), False),
     "l3d16_noint": ("laplacian_3d", (16,), False, dict(tau_d=64, interior_blocks=False), False),
+    "l3d20_td32": ("laplacian_3d", (20,), False, dict(tau_o=16, tau_d=32, oversample=4), False),
+    "el9_td48": ("elasticity_3d", (9,), True, dict(tau_o=24, tau_d=48, oversample=6), False),
 }
 
 
