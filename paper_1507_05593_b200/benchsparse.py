@@ -42,7 +42,9 @@ def cpu_sample(cfg, grid):
     try:
         import threadpoolctl
 
-        threadpoolctl.threadpool_limits(limits=os.cpu_count() or 1)
+        # one BLAS thread: the reference's default (cli.py:23-32,48) and, for its many
+        # small LAPACK calls, faster than a threaded BLAS
+        threadpoolctl.threadpool_limits(limits=1)
     except Exception:
         pass
     from oracle import numeric as on
@@ -130,7 +132,7 @@ def run_sparse(args, rank, world, torch, dist):
             ratio = work / max(Fs.stats.model_gflop, 1e-12)
         else:
             ratio = 1.0
-        cpu = {"value": ts * ratio, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": ts * ratio, "unit": "s", "cores": 1, "kind": "port",
                "sample": f"oracle factor+PCG on grid {sg} (n={ns}, {its} PCG its) took {ts:.1f} s; scaled by the "
                          f"modeled-work ratio {ratio:.1f} to the full config"}
     line = {
