@@ -24,6 +24,8 @@ constexpr int PADM = BM + 4;   // [k][m] / [k][n] row stride: 2*PADM = 8 mod 32 
 constexpr int A_SZ = (BM * PADK > BK * PADM) ? BM * PADK : BK * PADM;
 constexpr int B_SZ = A_SZ;
 constexpr int MAXP = 192;
+constexpr int STAGES = 3;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_SZ + B_SZ) * sizeof(double);
 
 struct GemmArgs {
     int count;
@@ -82,8 +84,9 @@ __device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const doub
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant__ GemmArgs args) {
-    __shared__ __align__(16) double sA[2][A_SZ];
-    __shared__ __align__(16) double sB[2][B_SZ];
+    extern __shared__ __align__(16) double gsm[];
+    double(*sA)[A_SZ] = reinterpret_cast<double(*)[A_SZ]>(gsm);
+    double(*sB)[B_SZ] = reinterpret_cast<double(*)[B_SZ]>(gsm + STAGES * A_SZ);
 
     // locate problem: last p with tile_begin[p] <= blockIdx.x
     const long long tile = blockIdx.x;
@@ -115,19 +118,20 @@ __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant_
 
     const int nk = (P.K + BK - 1) / BK;
     if (nk > 0) {
-        load_tiles<TA, TB>(P, A, B, m0, n0, 0, sA[0], sB[0]);
-        cp_async_commit();
+        // STAGES-deep cp.async pipeline, one CTA barrier per k-tile
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) load_tiles<TA, TB>(P, A, B, m0, n0, s * BK, sA[s], sB[s]);
+            cp_async_commit();
+        }
         for (int kt = 0; kt < nk; ++kt) {
-            if (kt + 1 < nk) {
-                load_tiles<TA, TB>(P, A, B, m0, n0, (kt + 1) * BK, sA[(kt + 1) & 1], sB[(kt + 1) & 1]);
-                cp_async_commit();
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncthreads();
-            const double *a_s = sA[kt & 1];
-            const double *b_s = sB[kt & 1];
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();  // tile kt landed; everyone is done with tile kt-1's stage
+            const int pf = kt + STAGES - 1;
+            if (pf < nk) load_tiles<TA, TB>(P, A, B, m0, n0, pf * BK, sA[pf % STAGES], sB[pf % STAGES]);
+            cp_async_commit();
+            const double *a_s = sA[kt % STAGES];
+            const double *b_s = sB[kt % STAGES];
 #pragma unroll
             for (int kk = 0; kk < BK; kk += 4) {
                 double af[4], bf[4];
@@ -146,7 +150,6 @@ __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant_
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
-            __syncthreads();
         }
     }
 
@@ -181,7 +184,12 @@ __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant_
 template <bool TA, bool TB>
 int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
     if (tiles <= 0) return 0;
-    gemm_grouped_kernel<TA, TB><<<(unsigned)tiles, NT, 0, s>>>(args);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_grouped_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        attr = true;
+    }
+    gemm_grouped_kernel<TA, TB><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
     RSC_CHECK_LAUNCH();
     return 0;
 }

@@ -35,34 +35,35 @@ struct DiagArgs {
 // Right-looking Cholesky, then column-parallel forward substitution L X = I.
 // Returns the 0-based failing pivot or -1.
 __device__ int factor_invert_64(double (*s)[NB + 1], int nb, bool factor) {
-    const int t = threadIdx.x, i = t >> 2, cg = t & 3;
+    // warp w owns rows i == w (mod 8), lanes run along the row (conflict-free rows)
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (factor) {
         for (int k = 0; k < nb; ++k) {
             const double piv = s[k][k];
             if (!(piv > 0.0)) return k;  // uniform: every thread read the same value
-            const double d = sqrt(piv);
+            const double d = sqrt(piv), rd = 1.0 / d;  // dpotf2 scales by 1/ajj
             __syncthreads();
-            if (i > k && i < nb && cg == 0) s[i][k] /= d;
+            for (int i = k + 1 + t; i < nb; i += blockDim.x) s[i][k] *= rd;
             if (t == 0) s[k][k] = d;
             __syncthreads();
-            if (i > k && i < nb) {
+            for (int i = k + 1 + w; i < nb; i += 8) {
                 const double lik = s[i][k];
-                for (int j = k + 1 + ((cg - (k + 1)) & 3); j <= i; j += 4) s[i][j] -= lik * s[j][k];
+                for (int j = k + 1 + lane; j <= i; j += 32) s[i][j] -= lik * s[j][k];
             }
             __syncthreads();
         }
     }
-    // X = L^{-1}: row k of X is final once the updates from rows < k are in
-    for (int c = cg; c <= i && i < nb; c += 4) s[c][i + 1] = (c == i) ? 1.0 : 0.0;
+    // X = L^{-1} (X[i][c] at s[c][i+1]); row k of X is final once rows < k are in
+    for (int i = w; i < nb; i += 8)
+        for (int c = lane; c <= i; c += 32) s[c][i + 1] = (c == i) ? 1.0 : 0.0;
     __syncthreads();
     for (int k = 0; k < nb; ++k) {
-        const double dk = s[k][k];
-        if (i == k)
-            for (int c = cg; c <= k; c += 4) s[c][k + 1] /= dk;
+        const double rk = 1.0 / s[k][k];
+        for (int c = t; c <= k; c += blockDim.x) s[c][k + 1] *= rk;
         __syncthreads();
-        if (i > k && i < nb) {
+        for (int i = k + 1 + w; i < nb; i += 8) {
             const double lik = s[i][k];
-            for (int c = cg; c <= k; c += 4) s[c][i + 1] -= lik * s[c][k + 1];
+            for (int c = lane; c <= k; c += 32) s[c][i + 1] -= lik * s[c][k + 1];
         }
         __syncthreads();
     }
