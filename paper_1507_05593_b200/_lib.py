@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librsc_b200.so")
+LIB_PATH = os.environ.get("RSC_B200_LIB", os.path.join(_HERE, "librsc_b200.so"))  # override: experiments only
 
 # numpy mirror of rsc_gemm_problem (include/rsc_b200.h); 120 bytes, naturally aligned
 GEMM_DTYPE = np.dtype(

@@ -24,7 +24,10 @@ constexpr int PADM = BM + 4;   // [k][m] / [k][n] row stride: 2*PADM = 8 mod 32 
 constexpr int A_SZ = (BM * PADK > BK * PADM) ? BM * PADK : BK * PADM;
 constexpr int B_SZ = A_SZ;
 constexpr int MAXP = 192;
-constexpr int STAGES = 3;
+#ifndef RSC_GEMM_STAGES
+#define RSC_GEMM_STAGES 2
+#endif
+constexpr int STAGES = RSC_GEMM_STAGES;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_SZ + B_SZ) * sizeof(double);
 
 struct GemmArgs {
