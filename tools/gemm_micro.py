@@ -12,7 +12,7 @@ LO = torch.randn(nb, 2048, 256, dtype=torch.float64, device="cuda")
 Om = torch.randn(nb, 2048, 58, dtype=torch.float64, device="cuda")
 G = torch.empty(nb, 256, 58, dtype=torch.float64, device="cuda")
 H = torch.empty(nb, 2048, 58, dtype=torch.float64, device="cuda")
-X = torch.randn(nb, 2048, 64, dtype=torch.float64, device="cuda")
+X = torch.randn(nb, 2048, 192, dtype=torch.float64, device="cuda")
 Lt = torch.randn(nb, 64, 192, dtype=torch.float64, device="cuda")
 Y = torch.randn(nb, 2048, 64, dtype=torch.float64, device="cuda")
 
@@ -33,7 +33,7 @@ def t(fn, flops, reps=5):
 lib = os.environ.get("RSC_B200_LIB", "default")
 r1 = t(lambda: E.gemm_strided_batched(LO, Om, G, transA=True, splitk=8), 2.0 * nb * 2048 * 256 * 58)
 r2 = t(lambda: E.gemm_strided_batched(LO, G, H), 2.0 * nb * 2048 * 256 * 58)
-r3 = t(lambda: E.gemm_strided_batched(X, Lt, Y, transB=False, alpha=-1.0, beta=1.0), 2.0 * nb * 2048 * 64 * 192)
+r3 = t(lambda: E.gemm_strided_batched(X, Lt, Y, transB=True, alpha=-1.0, beta=1.0), 2.0 * nb * 2048 * 64 * 192)
 big = torch.randn(4096, 4096, dtype=torch.float64, device="cuda")
 C = torch.empty(4096, 4096, dtype=torch.float64, device="cuda")
 r4 = t(lambda: E.gemm(big, big, C), 2.0 * 4096**3, reps=3)
