@@ -120,6 +120,19 @@ int rsc_spmm_csr_batched(int count, const int *const *rowptr, const int *const *
                          const double *const *X, const int *ldx, double alpha, double beta,
                          double *const *Y, const int *ldy, void *stream);
 
+/* Preconditioner-apply kernels (factor.py:187-218), HBM streaming:
+ * rsc_trsv_batched: x[i] <- L_i^{-1} x[i] (trans=0) or L_i^{-T} x[i] (trans=1) for
+ *   lower triangles from rsc_potrf_batched (their Dinv blocks); x[i] contiguous.
+ * rsc_gemv_batched: trans=0: y[yidx[r]] += alpha * sum_c M[r,c] x[c]
+ *                   trans=1: y[yidx[c]] += alpha * sum_r M[r,c] x[xidx[r]]
+ *   (index arrays optional, NULL = identity; FP64 atomics on y). */
+int rsc_trsv_batched(int count, const double *const *L, const int *n, const int *ldl,
+                     const double *const *Dinv, double *const *x, int trans, void *stream);
+int rsc_gemv_batched(int count, const double *const *M, const int *rows, const int *cols,
+                     const int *ldm, const double *const *x, const int *const *xidx,
+                     double *const *y, const int *const *yidx, int trans, double alpha,
+                     void *stream);
+
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */
 int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,
                  const double *values_dev, const double *x_dev, double *y_dev,

@@ -38,6 +38,8 @@ EXPORTED = (
     "rsc_spmm_csr",
     "rsc_spmm_csr_batched",
     "rsc_spmv_csr",
+    "rsc_trsv_batched",
+    "rsc_gemv_batched",
     "rsc_gather_rows",
     "rsc_scatter_add_rows",
     "rsc_dot",
@@ -69,6 +71,8 @@ _SIGS = {
     "rsc_spmm_csr": (I, [I, I, P, P, P, P, I, D, D, P, I, P]),
     "rsc_spmm_csr_batched": (I, [I, P, P, P, P, P, P, P, D, D, P, P, P]),
     "rsc_spmv_csr": (I, [I, P, P, P, P, P, P]),
+    "rsc_trsv_batched": (I, [I, P, P, P, P, P, I, P]),
+    "rsc_gemv_batched": (I, [I, P, P, P, P, P, P, P, P, I, D, P]),
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),
     "rsc_dot": (I, [I, P, P, P, P, P]),

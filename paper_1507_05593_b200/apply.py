@@ -8,47 +8,77 @@ solves + sparse coupling, factor.py:189-194,206-210) is the same operator as the
 dense branch, so every unit runs the same kernels.
 
 Level scheduling: a unit depends only on the units whose rows reach into its
-columns (its update sources), so units are grouped by height in that DAG and each
-level runs as a handful of grouped launches -- batched TRSV over all dense
-diagonals of the level, one grouped GEMV-scatter (FP64 atomics) for all dense
-couplings, two for all low-rank couplings, and the diagonal trees of the level
-advanced in lock-step waves (Alg. 4 flattened).  All problem descriptors are
-static after factorization and are built once; the whole apply is then replayed
-from a CUDA graph.
+columns (its update sources), so units are grouped by height in that DAG.  Each
+level is a handful of launches of the HBM-streaming kernels of csrc/apply.cu:
+one batched TRSV over all dense diagonals of the level, one batched gather/scatter
+GEMV for all dense couplings, two for all low-rank couplings, and the diagonal
+trees of the level advanced in lock-step waves (Alg. 4 flattened).  All launch
+descriptors are static after factorization and built once; after a few eager
+applies the whole sweep is replayed from a CUDA graph.
 """
 
 import numpy as np
 import torch
 
+from . import _lib
 from . import engine as E
-from ._lib import GEMM_DTYPE
+from ._lib import int_array, ptr_array
 from .factor import DenseTri, DeviceTree, DevLR
 
 
-def _rows(probs):
-    return np.array(probs, dtype=GEMM_DTYPE) if probs else None
+class _Launch:
+    """One pre-built batched launch (host descriptor arrays kept alive)."""
+
+    def __init__(self, fn, arrays, scalars):
+        self.fn = fn
+        self.arrays = arrays
+        self.args = [a.ctypes.data if isinstance(a, np.ndarray) else a for a in arrays] + scalars
+
+    def __call__(self, stream):
+        _lib.check(self.fn(*self.args, stream), "apply launch")
 
 
-def _p(A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, b_rows=0, c_rows=0, atomic=0):
-    return (A, B, C, 0, 0, 0, b_rows, c_rows, 0, M, N, K, max(lda, 1), max(ldb, 1), max(ldc, 1), 1, atomic,
-            alpha, beta)
+def _trsv(tris, xptrs, trans):
+    if not tris:
+        return None
+    lib = _lib.load()
+    arrs = [int(len(tris)), ptr_array([t.L.data_ptr() for t in tris]), int_array([t.n for t in tris]),
+            int_array([E.ld(t.L) for t in tris]), ptr_array([t.Dinv.data_ptr() for t in tris]), ptr_array(xptrs)]
+    return _Launch(lib.rsc_trsv_batched, arrs, [int(trans)])
 
 
-class _Trsv:
-    """Batched triangular solves on vector slices (one rsc_trsm_batched call)."""
+def _gemv(items, trans, alpha):
+    """items: (M ptr, rows, cols, ldm, x ptr, xidx ptr|0, y ptr, yidx ptr|0)."""
+    if not items:
+        return None
+    lib = _lib.load()
+    cols = list(zip(*items))
+    arrs = [int(len(items)), ptr_array(cols[0]), int_array(cols[1]), int_array(cols[2]), int_array(cols[3]),
+            ptr_array(cols[4]), ptr_array(cols[5]), ptr_array(cols[6]), ptr_array(cols[7])]
+    return _Launch(lib.rsc_gemv_batched, arrs, [int(trans), float(alpha)])
 
-    def __init__(self, tris, ptrs, trans):
-        self.trans = trans
-        self.L = [t.L.data_ptr() for t in tris]
-        self.n = [t.n for t in tris]
-        self.ld = [E.ld(t.L) for t in tris]
-        self.D = [t.Dinv.data_ptr() for t in tris]
-        self.B = list(ptrs)
+
+class _Prog:
+    """Ordered list of launches and zero-fills (a static program)."""
+
+    def __init__(self):
+        self.steps = []
+
+    def launch(self, l):
+        if l is not None:
+            self.steps.append(l)
+
+    def zero(self, t):
+        if t is not None and t.numel():
+            self.steps.append(("zero", t))
 
     def run(self):
-        if self.L:
-            E.trsm_batched("left", self.trans, self.L, self.n, self.ld, self.D, self.B, [1] * len(self.L),
-                           [1] * len(self.L))
+        s = E.stream_handle()
+        for st in self.steps:
+            if isinstance(st, tuple):
+                st[1].zero_()
+            else:
+                st(s)
 
 
 class DeviceApply:
@@ -60,8 +90,9 @@ class DeviceApply:
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
         self.y = E.empty(self.n, 1)
         self.zbuf = E.empty(self.n)
+        self.r_in = E.empty(self.n)
+        self.keep = []
         units = F.units
-        # level of every unit = 1 + max level of its update sources
         uidx = {un.u: i for i, un in enumerate(units)}
         level = [0] * len(units)
         for i, un in enumerate(units):
@@ -71,87 +102,134 @@ class DeviceApply:
                     su = uidx[plan.sources[p.s].unit]
                     lv = max(lv, level[su] + 1)
                 level[i] = lv
-        self.levels = []
         nlev = max(level) + 1 if units else 0
-        yp = self.y.data_ptr()
-        self.scratch = []
-        for lv in range(nlev):
-            idx = [i for i in range(len(units)) if level[i] == lv]
-            self.levels.append(self._build_level([units[i] for i in idx], plan, yp))
+        groups = [[units[i] for i in range(len(units)) if level[i] == lv] for lv in range(nlev)]
+        self.prog = _Prog()
+        for us in groups:
+            self._forward_level(us, plan)
+        for us in reversed(groups):
+            self._backward_level(us, plan)
         self.graph = None
-        self.r_in = E.empty(self.n)
+        self.calls = 0
 
+    # -- program construction ------------------------------------------------------
     def _rows_ptr(self, plan, un):
         key = ("int", un.u) if un.kind == "interior" else un.j
         return plan.idx.ptr(plan.rows_off[key])
 
-    def _build_level(self, us, plan, yp):
-        L = {}
+    def _tbuf(self, sizes):
+        """One zero-initialised buffer carved into per-problem t vectors."""
+        tot = sum(sizes)
+        if tot == 0:
+            return None, []
+        t = E.empty(tot)
+        self.keep.append(t)
+        offs = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+        return t, [t.data_ptr() + 8 * int(o) for o in offs]
+
+    def _tree_waves(self, trees, trans):
+        """Alg. 4 of every tree in `trees` on its slice of y, in lock-step waves."""
+        from .numeric import tree_ops
+
+        yp = self.y.data_ptr()
+        seqs = [tree_ops(u.diag, None, self.y[u.c0:u.c1], trans) for u in trees]
+        seqs = [s for s in seqs if s]
+        if not seqs:
+            return
+        for w in range(max(len(s) for s in seqs)):
+            leaves, dense, lr = [], [], []
+            for s in seqs:
+                if w >= len(s):
+                    continue
+                op = s[w]
+                if op[0] == "leaf":
+                    if op[1].n:
+                        leaves.append((op[1], op[2].data_ptr()))
+                    continue
+                _, b, Xs, Yd, tr = op
+                if isinstance(b, DevLR):
+                    if b.k:
+                        lr.append((b, Xs, Yd, tr))
+                else:
+                    dense.append((b, Xs, Yd, tr))
+            self.prog.launch(_trsv([t for t, _ in leaves], [p for _, p in leaves], trans))
+            # dense coupling: Y -= B X (forward) or Y -= B^T X (transposed)
+            self.prog.launch(_gemv([(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), Xs.data_ptr(), 0, Yd.data_ptr(), 0)
+                                    for b, Xs, Yd, tr in dense], trans, -1.0))
+            if lr:
+                t, tp = self._tbuf([b.k for b, _, _, _ in lr])
+                self.prog.zero(t)
+                # t = U^T X (forward) or V^T X (transposed)
+                first = [((b.V if tr else b.U), Xs, p) for (b, Xs, Yd, tr), p in zip(lr, tp)]
+                self.prog.launch(_gemv([(P.data_ptr(), P.shape[0], P.shape[1], E.ld(P), Xs.data_ptr(), 0, p, 0)
+                                        for P, Xs, p in first], 1, 1.0))
+                # Y -= V t (forward) or U t (transposed)
+                second = [((b.U if tr else b.V), Yd, p) for (b, Xs, Yd, tr), p in zip(lr, tp)]
+                self.prog.launch(_gemv([(P.data_ptr(), P.shape[0], P.shape[1], E.ld(P), p, 0, Yd.data_ptr(), 0)
+                                        for P, Yd, p in second], 0, -1.0))
+        del yp
+
+    def _forward_level(self, us, plan):
+        yp = self.y.data_ptr()
         dense = [u for u in us if isinstance(u.diag, DenseTri)]
         trees = [u for u in us if isinstance(u.diag, DeviceTree)]
-        L["fwd_diag"] = _Trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0)
-        L["bwd_diag"] = _Trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1)
-        L["trees"] = trees
-        # coupling products
-        fd, fl1, fl2, bd, bl1, bl2 = [], [], [], [], [], []
-        lr = [u for u in us if isinstance(u.off, DevLR) and u.rows.size and u.off.k]
-        tsz = sum(u.off.k for u in lr)
-        t = E.empty(max(tsz, 1))
-        self.scratch.append(t)
-        toff = 0
+        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0))
+        if trees:
+            self._tree_waves(trees, False)
+        dn, lr = [], []
         for u in us:
-            m = u.rows.size
-            if m == 0 or u.off is None:
+            if not u.rows.size or u.off is None:
                 continue
-            rp = self._rows_ptr(plan, u)
-            w = yp + 8 * u.c0
             if isinstance(u.off, DevLR):
-                k = u.off.k
-                if k == 0:
-                    continue
-                tp = t.data_ptr() + 8 * toff
-                toff += k
-                V, U = u.off.V, u.off.U
-                fl1.append(_p(U.data_ptr(), E.ld(U), w, 1, tp, 1, k, 1, u.ncols, 1.0, 0.0))
-                fl2.append(_p(V.data_ptr(), E.ld(V), tp, 1, yp, 1, m, 1, k, -1.0, 1.0, c_rows=rp, atomic=1))
-                bl1.append(_p(V.data_ptr(), E.ld(V), yp, 1, tp, 1, k, 1, m, 1.0, 0.0, b_rows=rp))
-                bl2.append(_p(U.data_ptr(), E.ld(U), tp, 1, w, 1, u.ncols, 1, k, -1.0, 1.0))
+                if u.off.k:
+                    lr.append(u)
             else:
-                O = u.off
-                fd.append(_p(O.data_ptr(), E.ld(O), w, 1, yp, 1, m, 1, u.ncols, -1.0, 1.0, c_rows=rp, atomic=1))
-                bd.append(_p(O.data_ptr(), E.ld(O), yp, 1, w, 1, u.ncols, 1, m, -1.0, 1.0, b_rows=rp))
-        L["fd"], L["fl1"], L["fl2"] = _rows(fd), _rows(fl1), _rows(fl2)
-        L["bd"], L["bl1"], L["bl2"] = _rows(bd), _rows(bl1), _rows(bl2)
-        return L
+                dn.append(u)
+        # y[R] -= L_O w
+        self.prog.launch(_gemv([(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), yp + 8 * u.c0, 0, yp,
+                                 self._rows_ptr(plan, u)) for u in dn], 0, -1.0))
+        if lr:
+            t, tp = self._tbuf([u.off.k for u in lr])
+            self.prog.zero(t)
+            # t = U^T w ; y[R] -= V t
+            self.prog.launch(_gemv([(u.off.U.data_ptr(), u.ncols, u.off.k, E.ld(u.off.U), yp + 8 * u.c0, 0, p, 0)
+                                    for u, p in zip(lr, tp)], 1, 1.0))
+            self.prog.launch(_gemv([(u.off.V.data_ptr(), u.rows.size, u.off.k, E.ld(u.off.V), p, 0, yp,
+                                     self._rows_ptr(plan, u)) for u, p in zip(lr, tp)], 0, -1.0))
 
-    @staticmethod
-    def _g(probs, ta=False):
-        if probs is not None:
-            E.gemm_grouped(probs, ta, False)
+    def _backward_level(self, us, plan):
+        yp = self.y.data_ptr()
+        dn, lr = [], []
+        for u in us:
+            if not u.rows.size or u.off is None:
+                continue
+            if isinstance(u.off, DevLR):
+                if u.off.k:
+                    lr.append(u)
+            else:
+                dn.append(u)
+        # w -= L_O^T y[R]
+        self.prog.launch(_gemv([(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), yp, self._rows_ptr(plan, u),
+                                 yp + 8 * u.c0, 0) for u in dn], 1, -1.0))
+        if lr:
+            t, tp = self._tbuf([u.off.k for u in lr])
+            self.prog.zero(t)
+            # t = V^T y[R] ; w -= U t
+            self.prog.launch(_gemv([(u.off.V.data_ptr(), u.rows.size, u.off.k, E.ld(u.off.V), yp,
+                                     self._rows_ptr(plan, u), p, 0) for u, p in zip(lr, tp)], 1, 1.0))
+            self.prog.launch(_gemv([(u.off.U.data_ptr(), u.ncols, u.off.k, E.ld(u.off.U), p, 0, yp + 8 * u.c0, 0)
+                                    for u, p in zip(lr, tp)], 0, -1.0))
+        trees = [u for u in us if isinstance(u.diag, DeviceTree)]
+        if trees:
+            self._tree_waves(trees, True)
+        dense = [u for u in us if isinstance(u.diag, DenseTri)]
+        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1))
 
-    def _sweep(self):
-        y = self.y
-        from .numeric import run_waves, tree_ops
-
-        for L in self.levels:
-            L["fwd_diag"].run()
-            if L["trees"]:  # Alg. 4 of every tree of the level in lock-step waves
-                run_waves([tree_ops(u.diag, None, y[u.c0:u.c1], False) for u in L["trees"]], E.scratch)
-            self._g(L["fd"])
-            self._g(L["fl1"], True)
-            self._g(L["fl2"])
-        for L in reversed(self.levels):
-            self._g(L["bd"], True)
-            self._g(L["bl1"], True)
-            self._g(L["bl2"])
-            if L["trees"]:
-                run_waves([tree_ops(u.diag, None, y[u.c0:u.c1], True) for u in L["trees"]], E.scratch)
-            L["bwd_diag"].run()
-
+    # -- execution ---------------------------------------------------------------
     def _body(self):
         n = self.n
         E.gather_rows(self.inv, self.r_in.reshape(n, 1), self.y)
-        self._sweep()
+        self.prog.run()
         E.gather_rows(self.fwd, self.y, self.zbuf.reshape(n, 1))
 
     # eager applies before the sweep is captured into a CUDA graph (capture costs
@@ -160,7 +238,7 @@ class DeviceApply:
 
     def __call__(self, r_dev, out=None):
         self.r_in.copy_(r_dev.reshape(-1))
-        self.calls = getattr(self, "calls", 0) + 1
+        self.calls += 1
         if self.graph is None and self.calls > self.GRAPH_AFTER:
             try:
                 s = torch.cuda.Stream()
