@@ -123,14 +123,17 @@ int rsc_spmm_csr_batched(int count, const int *const *rowptr, const int *const *
 /* Preconditioner-apply kernels (factor.py:187-218), HBM streaming:
  * rsc_trsv_batched: x[i] <- L_i^{-1} x[i] (trans=0) or L_i^{-T} x[i] (trans=1) for
  *   lower triangles from rsc_potrf_batched (their Dinv blocks); x[i] contiguous.
- * rsc_gemv_batched: trans=0: y[yidx[r]] += alpha * sum_c M[r,c] x[c]
- *                   trans=1: y[yidx[c]] += alpha * sum_r M[r,c] x[xidx[r]]
+ * rsc_gemv_batched (mode bit 0 = transpose, bit 1 = M lower triangular, bit 2 =
+ *   assign instead of accumulate (transpose 0 only), bit 3 = M upper triangular
+ *   (transpose 0 only)):
+ *                   mode&1==0: y[yidx[r]] += alpha * sum_c M[r,c] x[xidx[c]]
+ *                   mode&1==1: y[yidx[c]] += alpha * sum_r M[r,c] x[xidx[r]]
  *   (index arrays optional, NULL = identity; FP64 atomics on y). */
 int rsc_trsv_batched(int count, const double *const *L, const int *n, const int *ldl,
                      const double *const *Dinv, double *const *x, int trans, void *stream);
 int rsc_gemv_batched(int count, const double *const *M, const int *rows, const int *cols,
                      const int *ldm, const double *const *x, const int *const *xidx,
-                     double *const *y, const int *const *yidx, int trans, double alpha,
+                     double *const *y, const int *const *yidx, int mode, double alpha,
                      void *stream);
 
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */

@@ -38,9 +38,17 @@ class _Launch:
         _lib.check(self.fn(*self.args, stream), "apply launch")
 
 
-def _trsv(tris, xptrs, trans):
+def _trsv(tris, xptrs, trans, y2p=None, yp=None):
+    """Diagonal solves of a level.  With the explicit inverses built at apply setup,
+    x = L^{-1} b is a row-parallel GEMV (warp per row, no dependency chain):
+    forward reads Linv (lower), backward reads LinvT = Linv^T (upper), both from the
+    snapshot y2 of y taken before the solves, writing y (assign)."""
     if not tris:
         return None
+    if y2p is not None:
+        M = [t.LinvT if trans else t.Linv for t in tris]
+        items = [(m.data_ptr(), t.n, t.n, E.ld(m), y2p + (xp - yp), 0, xp, 0) for m, t, xp in zip(M, tris, xptrs)]
+        return _gemv(items, 4 | (8 if trans else 2), 1.0)
     lib = _lib.load()
     arrs = [int(len(tris)), ptr_array([t.L.data_ptr() for t in tris]), int_array([t.n for t in tris]),
             int_array([E.ld(t.L) for t in tris]), ptr_array([t.Dinv.data_ptr() for t in tris]), ptr_array(xptrs)]
@@ -72,11 +80,17 @@ class _Prog:
         if t is not None and t.numel():
             self.steps.append(("zero", t))
 
+    def copy(self, dst, src):
+        self.steps.append(("copy", dst, src))
+
     def run(self):
         s = E.stream_handle()
         for st in self.steps:
             if isinstance(st, tuple):
-                st[1].zero_()
+                if st[0] == "zero":
+                    st[1].zero_()
+                else:
+                    st[1].copy_(st[2])
             else:
                 st(s)
 
@@ -89,10 +103,12 @@ class DeviceApply:
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
         self.y = E.empty(self.n, 1)
+        self.y2 = E.empty(self.n, 1)  # snapshot of y read by the inverse-based diagonal solves
         self.zbuf = E.empty(self.n)
         self.r_in = E.empty(self.n)
         self.keep = []
         units = F.units
+        self._build_inverses(units)
         uidx = {un.u: i for i, un in enumerate(units)}
         level = [0] * len(units)
         for i, un in enumerate(units):
@@ -113,6 +129,33 @@ class DeviceApply:
         self.calls = 0
 
     # -- program construction ------------------------------------------------------
+    def _build_inverses(self, units):
+        """Linv = L^{-1} (one batched TRSM against identities) and LinvT for every dense
+        diagonal triangle and tree leaf: O(n^3/3) once per factor, after which every
+        apply's diagonal solves are bandwidth-bound GEMVs."""
+        tris = []
+        for u in units:
+            if isinstance(u.diag, DenseTri):
+                tris.append(u.diag)
+            elif isinstance(u.diag, DeviceTree):
+                tris.extend(b for s_, b in u.diag.blocks.items() if u.diag.shape.nodes[s_].is_leaf)
+        tris = [t for t in tris if t.n and t.Linv is None]
+        if not tris:
+            return
+        self.mem = E.Arena()
+        Ls = []
+        for t in tris:
+            I = self.mem.zeros(t.n, t.n)
+            I.fill_diagonal_(1.0)
+            Ls.append(I)
+        E.trsm_batched("left", 0, [t.L.data_ptr() for t in tris], [t.n for t in tris], [E.ld(t.L) for t in tris],
+                       [t.Dinv.data_ptr() for t in tris], [I.data_ptr() for I in Ls], [t.n for t in tris],
+                       [t.n for t in tris])
+        for t, I in zip(tris, Ls):
+            t.Linv = I
+            T = self.mem.empty(t.n, t.n)
+            T.copy_(I.t())
+            t.LinvT = T
     def _rows_ptr(self, plan, un):
         key = ("int", un.u) if un.kind == "interior" else un.j
         return plan.idx.ptr(plan.rows_off[key])
@@ -152,7 +195,9 @@ class DeviceApply:
                         lr.append((b, Xs, Yd, tr))
                 else:
                     dense.append((b, Xs, Yd, tr))
-            self.prog.launch(_trsv([t for t, _ in leaves], [p for _, p in leaves], trans))
+            if leaves:
+                self.prog.copy(self.y2, self.y)
+            self.prog.launch(_trsv([t for t, _ in leaves], [p for _, p in leaves], trans, self.y2.data_ptr(), yp))
             # dense coupling: Y -= B X (forward) or Y -= B^T X (transposed)
             self.prog.launch(_gemv([(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), Xs.data_ptr(), 0, Yd.data_ptr(), 0)
                                     for b, Xs, Yd, tr in dense], trans, -1.0))
@@ -167,13 +212,14 @@ class DeviceApply:
                 second = [((b.U if tr else b.V), Yd, p) for (b, Xs, Yd, tr), p in zip(lr, tp)]
                 self.prog.launch(_gemv([(P.data_ptr(), P.shape[0], P.shape[1], E.ld(P), p, 0, Yd.data_ptr(), 0)
                                         for P, Yd, p in second], 0, -1.0))
-        del yp
 
     def _forward_level(self, us, plan):
         yp = self.y.data_ptr()
         dense = [u for u in us if isinstance(u.diag, DenseTri)]
         trees = [u for u in us if isinstance(u.diag, DeviceTree)]
-        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0))
+        if dense:
+            self.prog.copy(self.y2, self.y)
+        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0, self.y2.data_ptr(), yp))
         if trees:
             self._tree_waves(trees, False)
         dn, lr = [], []
@@ -223,7 +269,9 @@ class DeviceApply:
         if trees:
             self._tree_waves(trees, True)
         dense = [u for u in us if isinstance(u.diag, DenseTri)]
-        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1))
+        if dense:
+            self.prog.copy(self.y2, self.y)
+        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1, self.y2.data_ptr(), yp))
 
     # -- execution ---------------------------------------------------------------
     def _body(self):

@@ -109,7 +109,10 @@ struct GemvArgs {
 constexpr int ROWS_PER_CTA = 64;
 
 // trans = 0: warp per row; trans = 1: CTA owns 64 rows, thread per column
-__global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a, int trans) {
+// mode bit 0: transpose; bit 1: M is lower triangular (read c <= r only);
+// bit 2: assign instead of atomic accumulate (transpose = 0 only: one warp owns a row)
+__global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a, int mode) {
+    const bool trans = mode & 1, lower = mode & 2, assign = mode & 4, upper = mode & 8;
     __shared__ double xr[ROWS_PER_CTA];
     int lo = 0, hi = a.count - 1;
     const long long blk = blockIdx.x;
@@ -130,18 +133,24 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
     if (!trans) {
         for (int r = r0 + w; r < r1; r += 8) {
             const double *Mr = M + (long long)r * ld;
+            const int cend = lower ? min(cols, r + 1) : cols;
+            const int cbeg = upper ? r : 0;
             double s = 0.0;
-            for (int c = lane; c < cols; c += 32) s += Mr[c] * (xi ? x[xi[c]] : x[c]);
+            for (int c = cbeg + lane; c < cend; c += 32) s += Mr[c] * (xi ? x[xi[c]] : x[c]);
             s = warp_sum(s);
-            if (lane == 0) atomicAdd(y + (yi ? yi[r] : r), a.alpha * s);
+            if (lane == 0) {
+                double *dst = y + (yi ? yi[r] : r);
+                if (assign) *dst = a.alpha * s;
+                else atomicAdd(dst, a.alpha * s);
+            }
         }
     } else {
         for (int r = r0 + t; r < r1; r += T) xr[r - r0] = xi ? x[xi[r]] : x[r];
         __syncthreads();
         for (int c = t; c < cols; c += T) {
             double s = 0.0;
-            for (int r = r0; r < r1; ++r) s += M[(long long)r * ld + c] * xr[r - r0];
-            atomicAdd(y + (yi ? yi[c] : c), a.alpha * s);
+            for (int r = lower ? max(r0, c) : r0; r < r1; ++r) s += M[(long long)r * ld + c] * xr[r - r0];
+            if (!lower || c < r1) atomicAdd(y + (yi ? yi[c] : c), a.alpha * s);
         }
     }
 }
@@ -178,7 +187,7 @@ extern "C" int rsc_trsv_batched(int count, const double *const *L, const int *n,
 
 extern "C" int rsc_gemv_batched(int count, const double *const *M, const int *rows, const int *cols,
                                 const int *ldm, const double *const *x, const int *const *xidx,
-                                double *const *y, const int *const *yidx, int trans, double alpha,
+                                double *const *y, const int *const *yidx, int mode, double alpha,
                                 void *stream) {
     if (count < 0) return -1;
     if (count == 0) return 0;
@@ -203,7 +212,7 @@ extern "C" int rsc_gemv_batched(int count, const double *const *M, const int *ro
         }
         if (a.count == 0) continue;
         a.blk_begin[a.count] = blocks;
-        gemv_kernel<<<(unsigned)blocks, T, 0, (cudaStream_t)stream>>>(a, trans);
+        gemv_kernel<<<(unsigned)blocks, T, 0, (cudaStream_t)stream>>>(a, mode);
         RSC_CHECK_LAUNCH();
     }
     return 0;
