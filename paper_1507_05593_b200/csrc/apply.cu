@@ -106,14 +106,19 @@ struct GemvArgs {
     double alpha;
 };
 
-constexpr int ROWS_PER_CTA = 64;
+constexpr int ROWS_T0 = 16;  // transpose 0: 8 warps x 2 rows per CTA
+constexpr int ROWS_T1 = 64;  // transpose 1: 64-row slab, thread per column
 
-// trans = 0: warp per row; trans = 1: CTA owns 64 rows, thread per column
+__device__ __forceinline__ double ldnc(const double *p) { return __ldg(p); }
+
 // mode bit 0: transpose; bit 1: M is lower triangular (read c <= r only);
-// bit 2: assign instead of atomic accumulate (transpose = 0 only: one warp owns a row)
+// bit 2: assign instead of atomic accumulate (transpose 0 only: one warp owns a row);
+// bit 3: M is upper triangular (transpose 0 only: read c >= r only).
+// Inner loops are unrolled 4x so each lane keeps four independent 8-byte loads in
+// flight (the kernel is latency-bound otherwise).
 __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a, int mode) {
     const bool trans = mode & 1, lower = mode & 2, assign = mode & 4, upper = mode & 8;
-    __shared__ double xr[ROWS_PER_CTA];
+    __shared__ double xr[ROWS_T1];
     int lo = 0, hi = a.count - 1;
     const long long blk = blockIdx.x;
     while (lo < hi) {
@@ -121,7 +126,6 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
         if (a.blk_begin[mid] <= blk) lo = mid; else hi = mid - 1;
     }
     const int p = lo;
-    const int r0 = (int)(blk - a.blk_begin[p]) * ROWS_PER_CTA;
     const int rows = a.rows[p], cols = a.cols[p], ld = a.ldm[p];
     const double *M = a.M[p];
     const double *x = a.x[p];
@@ -129,15 +133,36 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
     const int *xi = a.xidx[p];
     const int *yi = a.yidx[p];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int r1 = min(rows, r0 + ROWS_PER_CTA);
     if (!trans) {
+        const int r0 = (int)(blk - a.blk_begin[p]) * ROWS_T0;
+        const int r1 = min(rows, r0 + ROWS_T0);
         for (int r = r0 + w; r < r1; r += 8) {
             const double *Mr = M + (long long)r * ld;
             const int cend = lower ? min(cols, r + 1) : cols;
-            const int cbeg = upper ? r : 0;
-            double s = 0.0;
-            for (int c = cbeg + lane; c < cend; c += 32) s += Mr[c] * (xi ? x[xi[c]] : x[c]);
-            s = warp_sum(s);
+            int c = (upper ? r : 0) + lane;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            if (xi) {
+                for (; c + 96 < cend; c += 128) {
+                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + 32), m2 = ldnc(Mr + c + 64),
+                                 m3 = ldnc(Mr + c + 96);
+                    s0 += m0 * x[xi[c]];
+                    s1 += m1 * x[xi[c + 32]];
+                    s2 += m2 * x[xi[c + 64]];
+                    s3 += m3 * x[xi[c + 96]];
+                }
+                for (; c < cend; c += 32) s0 += ldnc(Mr + c) * x[xi[c]];
+            } else {
+                for (; c + 96 < cend; c += 128) {
+                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + 32), m2 = ldnc(Mr + c + 64),
+                                 m3 = ldnc(Mr + c + 96);
+                    s0 += m0 * x[c];
+                    s1 += m1 * x[c + 32];
+                    s2 += m2 * x[c + 64];
+                    s3 += m3 * x[c + 96];
+                }
+                for (; c < cend; c += 32) s0 += ldnc(Mr + c) * x[c];
+            }
+            const double s = warp_sum((s0 + s1) + (s2 + s3));
             if (lane == 0) {
                 double *dst = y + (yi ? yi[r] : r);
                 if (assign) *dst = a.alpha * s;
@@ -145,12 +170,24 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
             }
         }
     } else {
+        const int r0 = (int)(blk - a.blk_begin[p]) * ROWS_T1;
+        const int r1 = min(rows, r0 + ROWS_T1);
         for (int r = r0 + t; r < r1; r += T) xr[r - r0] = xi ? x[xi[r]] : x[r];
         __syncthreads();
         for (int c = t; c < cols; c += T) {
-            double s = 0.0;
-            for (int r = lower ? max(r0, c) : r0; r < r1; ++r) s += M[(long long)r * ld + c] * xr[r - r0];
-            if (!lower || c < r1) atomicAdd(y + (yi ? yi[c] : c), a.alpha * s);
+            int r = lower ? max(r0, c) : r0;
+            if (r >= r1) continue;
+            const double *Mc = M + (long long)r * ld + c;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            for (; r + 3 < r1; r += 4, Mc += 4LL * ld) {
+                const double m0 = ldnc(Mc), m1 = ldnc(Mc + ld), m2 = ldnc(Mc + 2LL * ld), m3 = ldnc(Mc + 3LL * ld);
+                s0 += m0 * xr[r - r0];
+                s1 += m1 * xr[r + 1 - r0];
+                s2 += m2 * xr[r + 2 - r0];
+                s3 += m3 * xr[r + 3 - r0];
+            }
+            for (; r < r1; ++r, Mc += ld) s0 += ldnc(Mc) * xr[r - r0];
+            atomicAdd(y + (yi ? yi[c] : c), a.alpha * ((s0 + s1) + (s2 + s3)));
         }
     }
 }
@@ -206,7 +243,8 @@ extern "C" int rsc_gemv_batched(int count, const double *const *M, const int *ro
             a.yidx[c] = yidx ? yidx[i] : nullptr;
             a.rows[c] = rows[i]; a.cols[c] = cols[i]; a.ldm[c] = ldm[i];
             a.blk_begin[c] = blocks;
-            blocks += (rows[i] + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+            const int rpc = (mode & 1) ? ROWS_T1 : ROWS_T0;
+            blocks += (rows[i] + rpc - 1) / rpc;
             ++a.count;
             ++i;
         }
