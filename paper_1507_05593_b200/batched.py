@@ -122,10 +122,14 @@ class BatchedSupernodes:
         if pinned is None:
             pinned = self.pinned_staging()
         st = pinned
-        np.copyto(st["D"].numpy(), D)
-        np.copyto(st["B"].numpy(), B)
-        self.D.copy_(st["D"], non_blocking=True)
-        self.B.copy_(st["B"], non_blocking=True)
+        # page-locked caller buffers go straight to the copy engine; pageable numpy
+        # arrays are staged through the pinned buffers first
+        for key, src, dst in (("D", D, self.D), ("B", B, self.B)):
+            if isinstance(src, torch.Tensor) and src.is_pinned():
+                dst.copy_(src, non_blocking=True)
+            else:
+                np.copyto(st[key].numpy(), np.asarray(src))
+                dst.copy_(st[key], non_blocking=True)
         make_sketches(self.nb, self.m, self.r, master=master, threads=threads, out=st["Om"].numpy())
         self.Om.copy_(st["Om"], non_blocking=True)
         self.run()

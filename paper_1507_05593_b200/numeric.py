@@ -441,8 +441,25 @@ class LevelPass(NumericPass):
         return self._lowrank_many(list(zip(Vs, Us)))
 
     # -- diagonal trees, batched over trees ---------------------------------------
+    def _path_probs(self, tree, s, rspan, cspan):
+        """Earlier root-path blocks p < s of the tree: (raw, eff, ld, w, row lo/hi, col lo/hi)
+        in block-local coordinates (diagblocks.py:265-273)."""
+        out = []
+        for raw, eff, a, b, c, d in self._path_terms(tree, s, rspan, cspan):
+            w = raw.shape[1]
+            if w:
+                out.append((raw.data_ptr(), eff.data_ptr(), E.ld(raw), w, a, b, c, d))
+        return out
+
+    def _tmaps(self, j, s):
+        t = self.np.tmap[(j, s)]
+        keep = self.s_w[t["s"]] > 0
+        return {k: v[keep] for k, v in t.items()}
+
     def leaves_many(self, items):
-        """items: (node, s) leaf blocks -> DenseTri (Alg. 6, diagblocks.py:276-300)."""
+        """items: (node, s) leaf blocks -> DenseTri (Alg. 6, diagblocks.py:276-300):
+        window of A, minus all windowed source products, minus root-path products,
+        as one grouped launch; then one batched POTRF."""
         blocks = []
         for node, s in items:
             _, blk, _ = self.np.tree_maps[(node.j, s)]
@@ -450,37 +467,45 @@ class LevelPass(NumericPass):
             k = lf.hi - lf.lo
             blocks.append((blk, k, k))
         Us = self._dense_many(blocks)
-        g = Grouped(False, True)
+        parts = []
         for (node, s), U in zip(items, Us):
             tree = node.diag
-            maps, _, _ = self.np.tree_maps[(node.j, s)]
             lf = tree.shape.nodes[s]
             k = lf.hi - lf.lo
-            for m in maps:
-                raw, eff = self.src_panel[m.s]
-                w = raw.shape[1]
-                if w == 0:
-                    continue
-                ld = E.ld(raw)
-                g.add(eff.data_ptr() + 8 * m.rlo * ld, ld, raw.data_ptr() + 8 * m.clo * ld, ld, U.data_ptr(), k,
-                      m.rhi - m.rlo, m.chi - m.clo, w, -1.0, 1.0, c_rows=self._idx(m.ridx_off),
-                      c_cols=self._idx(m.cidx_off), atomic=1)
-                self.flops += 2.0 * (m.rhi - m.rlo) * (m.chi - m.clo) * w
-            for raw, eff, a, b, c, d in self._path_terms(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi)):
-                w = raw.shape[1]
-                if w == 0:
-                    continue
-                ld = E.ld(raw)
-                g.add(eff.data_ptr() + 8 * a * ld, ld, raw.data_ptr() + 8 * c * ld, ld, U.data_ptr(), k, b - a,
-                      d - c, w, -1.0, 1.0, atomic=1)
-                self.flops += 2.0 * (b - a) * (d - c) * w
-        g.launch()
+            t = self._tmaps(node.j, s)
+            src = t["s"]
+            if src.size:
+                ld, w = self.s_ld[src], self.s_w[src]
+                p = np.zeros(src.size, dtype=GEMM_DTYPE)
+                p["A"] = self.s_eff[src] + (8 * t["rlo"] * ld).astype(np.uint64)
+                p["B"] = self.s_raw[src] + (8 * t["clo"] * ld).astype(np.uint64)
+                p["lda"], p["ldb"], p["K"] = ld, ld, w
+                p["M"], p["N"] = t["rhi"] - t["rlo"], t["chi"] - t["clo"]
+                p["c_rows"] = self.idx_base + (4 * t["ridx"]).astype(np.uint64)
+                p["c_cols"] = self.idx_base + (4 * t["cidx"]).astype(np.uint64)
+                p["C"], p["ldc"] = U.data_ptr(), k
+                parts.append(p)
+            path = self._path_probs(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi))
+            if path:
+                p = np.zeros(len(path), dtype=GEMM_DTYPE)
+                for i, (rawp, effp, ld, w, a0, a1, c0, c1) in enumerate(path):
+                    p[i]["A"], p[i]["B"] = effp + 8 * a0 * ld, rawp + 8 * c0 * ld
+                    p[i]["lda"], p[i]["ldb"], p[i]["K"], p[i]["M"], p[i]["N"] = ld, ld, w, a1 - a0, c1 - c0
+                p["C"], p["ldc"] = U.data_ptr(), k
+                parts.append(p)
+        if parts:
+            P = np.concatenate(parts)
+            P["batch"], P["atomic"], P["alpha"], P["beta"] = 1, 1, -1.0, 1.0
+            E.gemm_grouped(P, False, True)
+            self.flops += float(np.sum(2.0 * P["M"] * P["N"] * P["K"]))
         if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
             Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
         return self._potrf_many([(U, node.u) for (node, s), U in zip(items, Us)])
 
     def diag_mul_many(self, items, Gs, transpose, final=False):
-        """Alg. 5 for several (node, s) internal blocks at once (diagblocks.py:303-346)."""
+        """Alg. 5 for several (node, s) internal blocks at once (diagblocks.py:303-346):
+        batched left-subtree solves, grouped SpMM with the A windows, and all source and
+        root-path terms of all blocks in two grouped launches."""
         mem = self.P if final else self.S
         Ws, srcs, sol, spm = [], [], [], []
         for (node, s), G in zip(items, Gs):
@@ -505,44 +530,62 @@ class LevelPass(NumericPass):
         if sol:
             diag_solve_many(sol, self.S.empty)
         self._spmm_many(spm)
-        g1, g2 = Grouped(True, False), Grouped(False, False)
+        p1s, p2s = [], []
         for (node, s), src, W in zip(items, srcs, Ws):
             tree = node.diag
             (r0, r1), (c0, c1) = tree.shape.span(s)
-            maps, _, _ = self.np.tree_maps[(node.j, s)]
             r = src.shape[1]
-            terms = []
-            for m in maps:
-                raw, eff = self.src_panel[m.s]
-                w = raw.shape[1]
-                if w:
-                    terms.append((raw, eff, w, m.clo, m.chi, m.rlo, m.rhi, self._idx(m.cidx_off),
-                                  self._idx(m.ridx_off)))
-            for raw, eff, a, b, c, d in self._path_terms(tree, s, (r0, r1), (c0, c1)):
-                w = raw.shape[1]
-                if w:
-                    terms.append((raw, eff, w, c, d, a, b, 0, 0))
-            if not terms or r == 0:
+            if r == 0 or W.numel() == 0:
                 continue
-            T = self.S.empty(sum(t[2] for t in terms) * r)
-            o = 0
-            for raw, eff, w, clo, chi, rlo, rhi, cidx, ridx in terms:
-                ld = E.ld(raw)
-                tp = T.data_ptr() + 8 * o
-                o += w * r
-                if not transpose:
-                    g1.add(raw.data_ptr() + 8 * clo * ld, ld, src.data_ptr(), E.ld(src), tp, r, w, r, chi - clo, 1.0,
-                           0.0, b_rows=cidx)
-                    g2.add(eff.data_ptr() + 8 * rlo * ld, ld, tp, r, W.data_ptr(), E.ld(W), rhi - rlo, r, w, -1.0,
-                           1.0, c_rows=ridx, atomic=1)
-                else:
-                    g1.add(eff.data_ptr() + 8 * rlo * ld, ld, src.data_ptr(), E.ld(src), tp, r, w, r, rhi - rlo, 1.0,
-                           0.0, b_rows=ridx)
-                    g2.add(raw.data_ptr() + 8 * clo * ld, ld, tp, r, W.data_ptr(), E.ld(W), chi - clo, r, w, -1.0,
-                           1.0, c_rows=cidx, atomic=1)
-                self.flops += 2.0 * ((chi - clo) + (rhi - rlo)) * w * r
-        g1.launch()
-        g2.launch()
+            t = self._tmaps(node.j, s)
+            sid = t["s"]
+            ld = self.s_ld[sid]
+            w = self.s_w[sid]
+            raw_c = self.s_raw[sid] + (8 * t["clo"] * ld).astype(np.uint64)
+            eff_r = self.s_eff[sid] + (8 * t["rlo"] * ld).astype(np.uint64)
+            nc_, nr_ = t["chi"] - t["clo"], t["rhi"] - t["rlo"]
+            cidx = self.idx_base + (4 * t["cidx"]).astype(np.uint64)
+            ridx = self.idx_base + (4 * t["ridx"]).astype(np.uint64)
+            path = self._path_probs(tree, s, (r0, r1), (c0, c1))
+            if path:
+                pa = np.array(path, dtype=np.int64)
+                # (raw, eff, ld, w, row lo, row hi, col lo, col hi), window-aligned, no index maps
+                ld = np.concatenate([ld, pa[:, 2]])
+                w = np.concatenate([w, pa[:, 3]])
+                raw_c = np.concatenate([raw_c, (pa[:, 0] + 8 * pa[:, 6] * pa[:, 2]).astype(np.uint64)])
+                eff_r = np.concatenate([eff_r, (pa[:, 1] + 8 * pa[:, 4] * pa[:, 2]).astype(np.uint64)])
+                nc_ = np.concatenate([nc_, pa[:, 7] - pa[:, 6]])
+                nr_ = np.concatenate([nr_, pa[:, 5] - pa[:, 4]])
+                cidx = np.concatenate([cidx, np.zeros(len(path), np.uint64)])
+                ridx = np.concatenate([ridx, np.zeros(len(path), np.uint64)])
+            n = w.size
+            if n == 0:
+                continue
+            tsz = w * r
+            toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
+            T = self.S.empty(int(tsz.sum()))
+            tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
+            p1 = np.zeros(n, dtype=GEMM_DTYPE)
+            p2 = np.zeros(n, dtype=GEMM_DTYPE)
+            p1["lda"], p1["M"], p1["N"], p1["C"], p1["ldc"] = ld, w, r, tp, r
+            p1["B"], p1["ldb"] = src.data_ptr(), E.ld(src)
+            p2["lda"], p2["K"], p2["N"], p2["B"], p2["ldb"] = ld, w, r, tp, r
+            p2["C"], p2["ldc"] = W.data_ptr(), E.ld(W)
+            if not transpose:  # T = V[cwin]^T G1[cidx] ; W[ridx] -= E[rwin] T
+                p1["A"], p1["K"], p1["b_rows"] = raw_c, nc_, cidx
+                p2["A"], p2["M"], p2["c_rows"] = eff_r, nr_, ridx
+            else:  # T = E[rwin]^T G[ridx] ; W[cidx] -= V[cwin] T
+                p1["A"], p1["K"], p1["b_rows"] = eff_r, nr_, ridx
+                p2["A"], p2["M"], p2["c_rows"] = raw_c, nc_, cidx
+            p1s.append(p1)
+            p2s.append(p2)
+            self.flops += float(np.sum(2.0 * (nc_ + nr_) * w * r))
+        if p1s:
+            P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
+            P1["batch"], P1["alpha"] = 1, 1.0
+            P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
+            E.gemm_grouped(P1, True, False)
+            E.gemm_grouped(P2, False, False)
         if transpose:
             sol2 = []
             for (node, s), W in zip(items, Ws):

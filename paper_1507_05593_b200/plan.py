@@ -282,6 +282,7 @@ class NumericPlan:
         from .diagtree import TreeShape
 
         self.tree_shapes = {}
+        self.tmap = {}
         for j, split in self.sym.sep_splits.items():
             c0, c1 = part.cols(j)
             shape = TreeShape(c1 - c0, c0, split)
@@ -305,6 +306,15 @@ class NumericPlan:
                 blk = self.csr.add(win)
                 blkT = self.csr.add(win.T.tocsr()) if (gr0, gr1) != (gc0, gc1) else None
                 self.tree_maps[(j, s)] = (maps, blk, blkT)
+                self.tmap[(j, s)] = {
+                    "s": np.array([m.s for m in maps], dtype=np.int64),
+                    "clo": np.array([m.clo for m in maps], dtype=np.int64),
+                    "chi": np.array([m.chi for m in maps], dtype=np.int64),
+                    "rlo": np.array([m.rlo for m in maps], dtype=np.int64),
+                    "rhi": np.array([m.rhi for m in maps], dtype=np.int64),
+                    "cidx": np.array([m.cidx_off for m in maps], dtype=np.int64),
+                    "ridx": np.array([m.ridx_off for m in maps], dtype=np.int64),
+                }
 
 
 def _seed(master, *tags):
