@@ -281,6 +281,103 @@ __global__ void __launch_bounds__(CT) mq_form_q_kernel(const __grid_constant__ Q
     for (int r = lane; r < m; r += 32) d.Q[(long long)r * d.ldq + j] = q[r];
 }
 
+// ---- blocked (compact-WY) Q formation, dorgqr-style, on DMMA GEMMs ----------
+// Q = H_0 ... H_{k-1} [I; 0] = B_0 (B_1 ( ... B_last [I;0])), B_b = I - V_b T_b V_b^T
+// over blocks of QB reflectors; V_b is the explicit unit-lower reflector block and
+// T_b the dlarft triangle.  Applying every reflector (not only the first `rank`)
+// leaves Q[:, :rank] exactly unchanged (reflector i acts on rows >= i, where the
+// first columns are still zero).
+constexpr int QB = 64;
+
+struct VBuild {
+    int count;
+    const double *W[MAXM];
+    const int *perm[MAXM];
+    double *V[MAXM];
+    double *Q[MAXM];
+    int m[MAXM], kmin[MAXM], ldw[MAXM], ldq[MAXM];
+};
+
+// V[r, i] = (r < i ? 0 : r == i ? 1 : W[perm[i]][r]);  Q[r, i] = (r == i)
+// 32x32 tiles through shared memory (coalesced column-major read, row-major write)
+__global__ void build_vq_kernel(const __grid_constant__ VBuild a) {
+    __shared__ double tile[32][33];
+    const int g = blockIdx.z;
+    const int m = a.m[g], km = a.kmin[g];
+    const int r0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    if (r0 >= m || i0 >= km) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int q = ty; q < 32; q += 8) {
+        const int i = i0 + q, r = r0 + tx;
+        double v = 0.0;
+        if (i < km && r < m) v = (r < i) ? 0.0 : (r == i ? 1.0 : a.W[g][(long long)a.perm[g][i] * a.ldw[g] + r]);
+        tile[q][tx] = v;
+    }
+    __syncthreads();
+    for (int q = ty; q < 32; q += 8) {
+        const int r = r0 + q, i = i0 + tx;
+        if (r < m && i < km) {
+            a.V[g][(long long)r * km + i] = tile[tx][q];
+            a.Q[g][(long long)r * a.ldq[g] + i] = (r == i) ? 1.0 : 0.0;
+        }
+    }
+}
+
+struct TArgs {
+    int count, b;
+    const double *G[MAXM];    // Gram of the block (QB x QB, ld QB)
+    const double *tau[MAXM];
+    double *T[MAXM];          // QB x QB, ld QB
+    int kmin[MAXM];
+};
+
+// dlarft (forward, columnwise): T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i,0:i] G[0:i, i]
+__global__ void larft_kernel(const __grid_constant__ TArgs a) {
+    const int g = blockIdx.x;
+    const int j0 = a.b * QB;
+    const int nb = min(QB, a.kmin[g] - j0);
+    if (nb <= 0) return;
+    double *T = a.T[g];
+    const double *G = a.G[g];
+    const double *tau = a.tau[g] + j0;
+    const int t = threadIdx.x;
+    for (int e = t; e < QB * QB; e += blockDim.x) T[e] = 0.0;
+    __syncthreads();
+    for (int i = 0; i < nb; ++i) {
+        // row r < i of column i: -tau_i * sum_{l=r}^{i-1} T[r][l] G[l][i]
+        if (t < i) {
+            double s = 0.0;
+            for (int l = t; l < i; ++l) s += T[t * QB + l] * G[l * QB + i];
+            T[t * QB + i] = -tau[i] * s;
+        }
+        if (t == 0) T[i * QB + i] = tau[i];
+        __syncthreads();
+    }
+}
+
+struct RankArgs {
+    int count;
+    const double *diagR[MAXM];
+    int *rank[MAXM];
+    int m[MAXM], k[MAXM];
+};
+
+__global__ void rank_kernel(const __grid_constant__ RankArgs a) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= a.count) return;
+    const int m = a.m[g], k = a.k[g];
+    const double *d = a.diagR[g];
+    const double d0 = fabs(d[0]);
+    const int kmin = m < k ? m : k;
+    int r = 0;
+    if (d0 != 0.0) {
+        const double cut = (double)(m > k ? m : k) * EPS * d0;
+        for (int i = 0; i < kmin; ++i)
+            if (fabs(d[i]) > cut) ++r;
+    }
+    *a.rank[g] = r;
+}
+
 inline size_t smem_for(int m, int k, int cpc) {
     const size_t ldw = (size_t)(m | 1);
     return (size_t)cpc * ldw * 8 + (size_t)m * 8 + sizeof(int) * 2 * (size_t)k;
@@ -291,7 +388,90 @@ inline size_t smem_for(int m, int k, int cpc) {
 // workspace doubles of one matrix
 long long rsc_qrcp_coop_doubles(int m, int k) {
     const long long ldw = m | 1;
-    return ldw * k + 4LL * k + m + k + 64;
+    const long long kmin = m < k ? m : k;
+    // factorization | explicit V (m x kmin) | W_b (QB x kmin) | Gram, T (QB x QB each)
+    return ldw * k + 4LL * k + m + k + 64 + (long long)m * kmin + QB * kmin + 2LL * QB * QB + 64;
+}
+
+static inline double *wy_base(double *W, int m, int k) {
+    const long long ldw = m | 1;
+    return W + ldw * k + 4LL * k + m + k + 64;
+}
+
+int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *problems, int count, void *stream);
+
+static inline rsc_gemm_problem gp(const double *A, int lda, const double *B, int ldb, double *C, int ldc, int M,
+                                  int N, int K, double alpha, double beta) {
+    rsc_gemm_problem p{};
+    p.A = A; p.B = B; p.C = C; p.lda = lda; p.ldb = ldb; p.ldc = ldc;
+    p.M = M; p.N = N; p.K = K; p.alpha = alpha; p.beta = beta; p.batch = 1;
+    return p;
+}
+
+// Q for the matrices of one launch group: ranks, explicit V, then per block b (from
+// the last): Gram = V_b^T V_b, T_b (dlarft), W = V_b^T Q_b, W = T_b W, Q_b -= V_b W.
+static int form_q_blocked(int cnt, const MatDesc *ds, cudaStream_t s) {
+    static thread_local RankArgs ra;
+    static thread_local VBuild vb;
+    static thread_local TArgs ta;
+    ra.count = cnt;
+    vb.count = cnt;
+    int maxm = 1, maxk = 1;
+    for (int c = 0; c < cnt; ++c) {
+        const MatDesc &d = ds[c];
+        const Ws w = {d.W, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        (void)w;
+        double *diagR = d.W + (long long)d.ldw * d.k + 3LL * d.k;
+        double *vbuf = diagR + d.k;
+        const int *perm = reinterpret_cast<const int *>(vbuf + d.m);
+        const int kmin = d.m < d.k ? d.m : d.k;
+        ra.diagR[c] = diagR; ra.rank[c] = d.rank; ra.m[c] = d.m; ra.k[c] = d.k;
+        vb.W[c] = d.W; vb.perm[c] = perm; vb.V[c] = wy_base(d.W, d.m, d.k); vb.Q[c] = d.Q;
+        vb.m[c] = d.m; vb.kmin[c] = kmin; vb.ldw[c] = d.ldw; vb.ldq[c] = d.ldq;
+        maxm = d.m > maxm ? d.m : maxm;
+        maxk = kmin > maxk ? kmin : maxk;
+    }
+    rank_kernel<<<(cnt + 127) / 128, 128, 0, s>>>(ra);
+    RSC_CHECK_LAUNCH();
+    dim3 grid((maxm + 31) / 32, (maxk + 31) / 32, cnt);
+    build_vq_kernel<<<grid, 256, 0, s>>>(vb);
+    RSC_CHECK_LAUNCH();
+    const int nblocks = (maxk + QB - 1) / QB;
+    std::vector<rsc_gemm_problem> pg, pw, pt, pq;
+    for (int b = nblocks - 1; b >= 0; --b) {
+        pg.clear(); pw.clear(); pt.clear(); pq.clear();
+        ta.count = cnt;
+        ta.b = b;
+        const int j0 = b * QB;
+        for (int c = 0; c < cnt; ++c) {
+            const MatDesc &d = ds[c];
+            const int km = vb.kmin[c];
+            double *V = vb.V[c];
+            double *Wb = V + (long long)d.m * km;
+            double *Gm = Wb + (long long)QB * km;
+            double *Tm = Gm + QB * QB;
+            const double *tau = d.W + (long long)d.ldw * d.k + 2LL * d.k;
+            ta.G[c] = Gm; ta.tau[c] = tau; ta.T[c] = Tm; ta.kmin[c] = km;
+            if (j0 >= km) continue;
+            const int nb = km - j0 < QB ? km - j0 : QB;
+            const int rows = d.m - j0, cols = km - j0;
+            const double *Vb = V + (long long)j0 * km + j0;
+            double *Qb = d.Q + (long long)j0 * d.ldq + j0;
+            pg.push_back(gp(Vb, km, Vb, km, Gm, QB, nb, nb, rows, 1.0, 0.0));          // Gram (TA)
+            pw.push_back(gp(Vb, km, Qb, d.ldq, Wb, km, nb, cols, rows, 1.0, 0.0));     // W = V^T Q (TA)
+            pt.push_back(gp(Tm, QB, Wb, km, Wb, km, nb, cols, nb, 1.0, 0.0));           // W = T W (in place)
+            pq.push_back(gp(Vb, km, Wb, km, Qb, d.ldq, rows, cols, nb, -1.0, 1.0));    // Q -= V W
+        }
+        if (pg.empty()) continue;
+        int rc = rsc_gemm_grouped(1, 0, pg.data(), (int)pg.size(), s);
+        if (rc) return rc;
+        larft_kernel<<<cnt, 64, 0, s>>>(ta);
+        RSC_CHECK_LAUNCH();
+        if ((rc = rsc_gemm_grouped(1, 0, pw.data(), (int)pw.size(), s))) return rc;
+        if ((rc = rsc_gemm_grouped(0, 0, pt.data(), (int)pt.size(), s))) return rc;
+        if ((rc = rsc_gemm_grouped(0, 0, pq.data(), (int)pq.size(), s))) return rc;
+    }
+    return 0;
 }
 
 // Factor `n` matrices (indices into the arrays) concurrently.  work_off[i] is the
@@ -376,26 +556,11 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
                 smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, dim3(b0), dim3(CT), args, sm, s);
             rsc_count_launch();
             if (e != cudaSuccess) return (int)e;
-            // Q formation for the same matrices
-            qa.count = cnt;
-            int q0 = 0;
-            size_t qsm = 0;
-            for (int c = 0; c < cnt; ++c) {
-                const MatDesc &d = ma.d[c];
-                int wpc = (int)(SMEM_BUDGET / ((size_t)d.m * 8));
-                wpc = wpc < 1 ? 1 : (wpc > CT / 32 ? CT / 32 : wpc);
-                if ((size_t)d.m * 8 > SMEM_BUDGET) return 79;
-                QDesc &q = qa.d[c];
-                q.W = d.W; q.Q = d.Q; q.rank = d.rank;
-                q.m = d.m; q.k = d.k; q.ldw = d.ldw; q.ldq = d.ldq;
-                q.wpc = wpc; q.blk0 = q0;
-                const int kmin = d.m < d.k ? d.m : d.k;
-                q.nblk = std::max(1, (kmin + wpc - 1) / wpc);
-                q0 += q.nblk;
-                qsm = std::max(qsm, (size_t)wpc * d.m * 8);
+            // Q formation (blocked compact-WY on DMMA GEMMs) for the same matrices
+            {
+                const int rc = form_q_blocked(cnt, ma.d, s);
+                if (rc) return rc;
             }
-            mq_form_q_kernel<<<q0, CT, qsm, s>>>(qa);
-            RSC_CHECK_LAUNCH();
         }
         // second pass uses fresh counters beyond the first pass's
         if (pass == 0) {

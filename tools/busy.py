@@ -24,7 +24,7 @@ ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 busy = sum(e.device_time for e in ev) / 1e6 if ev else 0.0
 byname = {}
 for e in ev:
-    k = e.name.split("(")[0][-50:]
+    k = e.name.replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0][:60]
     byname[k] = byname.get(k, 0.0) + e.device_time / 1e3
 print(f"wall {wall:.3f}s  kernel-sum {busy:.3f}s  ({100 * busy / wall:.0f}% busy)  kernels {len(ev)}")
 for k, v in sorted(byname.items(), key=lambda x: -x[1])[:12]:
