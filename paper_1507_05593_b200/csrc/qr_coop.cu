@@ -457,8 +457,22 @@ static int form_q_blocked(int cnt, const MatDesc *ds, cudaStream_t s) {
             const int rows = d.m - j0, cols = km - j0;
             const double *Vb = V + (long long)j0 * km + j0;
             double *Qb = d.Q + (long long)j0 * d.ldq + j0;
-            pg.push_back(gp(Vb, km, Vb, km, Gm, QB, nb, nb, rows, 1.0, 0.0));          // Gram (TA)
-            pw.push_back(gp(Vb, km, Qb, d.ldq, Wb, km, nb, cols, rows, 1.0, 0.0));     // W = V^T Q (TA)
+            // Gram = V_b^T V_b and W = V_b^T Q_b have a long K (= rows): split K into
+            // slabs accumulated atomically into zeroed outputs so each matrix gets
+            // rows/KS CTAs per output tile instead of one
+            cudaMemsetAsync(Gm, 0, sizeof(double) * QB * QB, s);
+            cudaMemsetAsync(Wb, 0, sizeof(double) * (size_t)QB * km, s);
+            constexpr int KS = 512;
+            for (int k0 = 0; k0 < rows; k0 += KS) {
+                const int kk = rows - k0 < KS ? rows - k0 : KS;
+                const double *Vk = Vb + (long long)k0 * km;
+                rsc_gemm_problem a = gp(Vk, km, Vk, km, Gm, QB, nb, nb, kk, 1.0, 1.0);  // Gram (TA)
+                a.atomic = 1;
+                pg.push_back(a);
+                rsc_gemm_problem w = gp(Vk, km, Qb + (long long)k0 * d.ldq, d.ldq, Wb, km, nb, cols, kk, 1.0, 1.0);
+                w.atomic = 1;                                                              // W = V^T Q (TA)
+                pw.push_back(w);
+            }
             pt.push_back(gp(Tm, QB, Wb, km, Wb, km, nb, cols, nb, 1.0, 0.0));           // W = T W (in place)
             pq.push_back(gp(Vb, km, Wb, km, Qb, d.ldq, rows, cols, nb, -1.0, 1.0));    // Q -= V W
         }
