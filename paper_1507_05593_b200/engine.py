@@ -164,12 +164,43 @@ class KernelProfile:
 
     def summary(self):
         torch.cuda.synchronize()
-        t = sum(s.elapsed_time(e) for s, e, _ in self.records) * 1e-3
-        f = sum(fl for _, _, fl in self.records)
+        t = sum(r[0].elapsed_time(r[1]) for r in self.records) * 1e-3
+        f = sum(r[2] for r in self.records)
         return {"launch_groups": len(self.records), "seconds": t, "flops": f}
+
+    def by_tag(self):
+        torch.cuda.synchronize()
+        out = {}
+        for s, e, fl, tag in self.records:
+            d = out.setdefault(tag, [0, 0.0, 0.0])
+            d[0] += 1
+            d[1] += s.elapsed_time(e) * 1e-3
+            d[2] += fl
+        return out
 
 
 PROFILE = None
+TAG = "untagged"  # call-site label recorded with each profiled launch
+
+
+class region:
+    """`with region("name"):` -- CUDA-event timing of a host-issued section when a
+    KernelProfile is active (records flops 0, tag = name); free otherwise."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if PROFILE is not None:
+            self.s = torch.cuda.Event(enable_timing=True)
+            self.s.record()
+        return self
+
+    def __exit__(self, *exc):
+        if PROFILE is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            PROFILE.records.append((self.s, e, 0.0, "region:" + self.name))
 
 
 def gemm_grouped(probs, transA=False, transB=False):
@@ -187,7 +218,7 @@ def gemm_grouped(probs, transA=False, transB=False):
     if prof is not None:
         e.record()
         fl = float(np.sum(2.0 * probs["M"].astype(np.float64) * probs["N"] * probs["K"] * probs["batch"]))
-        prof.records.append((s, e, fl))
+        prof.records.append((s, e, fl, TAG))
 
 
 def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):

@@ -759,3 +759,24 @@ class LevelPass(NumericPass):
         self.pending = []
         if worst is not None:
             raise _Indefinite(*worst)
+
+
+# ---------------------------------------------------------------------------
+# optional per-section device timing (active only under engine.PROFILE)
+
+
+def _timed(name, fn):
+    def wrap(*a, **k):
+        with E.region(name):
+            return fn(*a, **k)
+
+    wrap.__name__ = fn.__name__
+    wrap.__doc__ = fn.__doc__
+    return wrap
+
+
+for _name in ("_products_many", "_spmm_many", "_orth_many", "_lowrank_many", "assemble_many", "_potrf_many",
+              "leaves_many", "factor_interiors", "diag_mul_many", "approx_off_many", "approx_diag_many",
+              "trees_many"):
+    setattr(LevelPass, _name, _timed(_name.strip("_"), getattr(LevelPass, _name)))
+diag_solve_many = _timed("diag_solve", diag_solve_many)
