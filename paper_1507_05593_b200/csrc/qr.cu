@@ -41,19 +41,27 @@ __device__ __forceinline__ double col_norm2(const double *c, int r0, int m, int 
     return warp_sum(s);
 }
 
+// One CTA per matrix.  Pivoting is a permutation (pos2phys / posof) instead of
+// column swaps, and each Householder step is two phases separated by a single CTA
+// barrier: (1) warp 0 picks the pivot (first position of the largest partial norm),
+// forms the reflector on that column and publishes tau; (2) every warp applies it to
+// its own unchosen columns and downdates their norms.  dorg2r runs on the first
+// `rank` positions with the same indirection.
 template <bool SMEM>
 __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant__ QrArgs args,
                                                            double *work, int *rank_out) {
     extern __shared__ __align__(16) double dyn[];
-    __shared__ double vn1[QR_MAXK], vn2[QR_MAXK], tau[QR_MAXK];
-    __shared__ double red[32];
-    __shared__ int piv_s;
+    __shared__ int piv_s, rank_s;
 
     const int b = blockIdx.x;
     const int m = args.m[b], k = args.k[b];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = QR_THREADS / 32;
-    double *W = SMEM ? dyn : work + args.woff[b];
     const int ldw = m | 1;  // odd column stride: conflict-free transposed load
+    double *W = SMEM ? dyn : work + args.woff[b];
+    double *vn1 = SMEM ? dyn + (long long)ldw * k : dyn;
+    double *vn2 = vn1 + k, *tau = vn2 + k, *diagR = tau + k;
+    int *pos2phys = reinterpret_cast<int *>(diagR + k);
+    int *posof = pos2phys + k;
     const double *G = args.G[b];
     const int ldg = args.ldg[b];
 
@@ -61,11 +69,11 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         if (t == 0) rank_out[args.base + b] = 0;
         return;
     }
-    // load transposed: W[j*m + i] = G[i, j]
     for (long long e = t; e < (long long)m * k; e += QR_THREADS) {
         const int i = (int)(e / k), j = (int)(e % k);
         W[(long long)j * ldw + i] = G[(long long)i * ldg + j];
     }
+    for (int j = t; j < k; j += QR_THREADS) { pos2phys[j] = j; posof[j] = j; }
     __syncthreads();
     for (int j = warp; j < k; j += nw) {
         const double nrm = sqrt(col_norm2(W + (long long)j * ldw, 0, m, lane));
@@ -75,56 +83,50 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
 
     const int kmin = m < k ? m : k;
     for (int i = 0; i < kmin; ++i) {
-        // pivot: first index of max vn1[j], j >= i (idamax)
         if (warp == 0) {
+            // pivot: first position of the largest partial norm (idamax over positions)
             double best = -1.0;
-            int bi = k;
+            int bp = k;
             for (int j = i + lane; j < k; j += 32) {
-                const double v = vn1[j];
-                if (v > best) { best = v; bi = j; }
+                const double v = vn1[pos2phys[j]];
+                if (v > best) { best = v; bp = j; }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
             }
-            if (lane == 0) piv_s = (bi < k) ? bi : i;  // NaN norms (failed upstream pivot): no swap
+            if (bp >= k) bp = i;  // NaN norms (failed upstream pivot): keep the order
+            const int pc = pos2phys[bp];
+            __syncwarp();
+            if (lane == 0) {
+                const int ci = pos2phys[i];
+                pos2phys[i] = pc; pos2phys[bp] = ci;
+                posof[pc] = i; posof[ci] = bp;
+                piv_s = pc;
+            }
+            // reflector on the pivot column (dlarfg)
+            double *cp = W + (long long)pc * ldw;
+            const double xnorm = sqrt(col_norm2(cp, i + 1, m, lane));
+            const double alpha = cp[i];
+            double tau_i = 0.0, beta = alpha, scal = 0.0;
+            if (xnorm != 0.0) {
+                beta = -copysign(hypot(alpha, xnorm), alpha);
+                tau_i = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+                for (int r = i + 1 + lane; r < m; r += 32) cp[r] *= scal;
+            }
+            __syncwarp();
+            if (lane == 0) { cp[i] = beta; tau[i] = tau_i; diagR[i] = beta; }
         }
         __syncthreads();
-        const int p = piv_s;
-        if (p != i) {
-            double *ci = W + (long long)i * ldw, *cp = W + (long long)p * ldw;
-            for (int r = t; r < m; r += QR_THREADS) {
-                const double x = ci[r];
-                ci[r] = cp[r];
-                cp[r] = x;
-            }
-            if (t == 0) {
-                double x = vn1[i]; vn1[i] = vn1[p]; vn1[p] = x;
-                x = vn2[i]; vn2[i] = vn2[p]; vn2[p] = x;
-            }
-        }
-        __syncthreads();
-        // Householder reflector on W[i:m, i] (dlarfg)
-        double *ci = W + (long long)i * ldw;
-        double part = 0.0;
-        for (int r = i + 1 + t; r < m; r += QR_THREADS) part += ci[r] * ci[r];
-        const double xnorm = sqrt(block_sum(part, red));
-        const double alpha = ci[i];
-        double tau_i = 0.0, beta = alpha, scal = 0.0;
-        if (xnorm != 0.0) {
-            beta = -copysign(hypot(alpha, xnorm), alpha);
-            tau_i = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
-        }
-        __syncthreads();
-        if (xnorm != 0.0)
-            for (int r = i + 1 + t; r < m; r += QR_THREADS) ci[r] *= scal;
-        if (t == 0) { ci[i] = beta; tau[i] = tau_i; }
-        __syncthreads();
-        // apply H^T to the trailing columns and downdate their norms
-        for (int j = i + 1 + warp; j < k; j += nw) {
+        const int pc = piv_s;
+        const double *ci = W + (long long)pc * ldw;
+        const double tau_i = tau[i];
+        // apply H^T to the unchosen columns and downdate their norms
+        for (int j = warp; j < k; j += nw) {
+            if (posof[j] <= i) continue;
             double *cj = W + (long long)j * ldw;
             if (tau_i != 0.0) {
                 double w = 0.0;
@@ -157,14 +159,13 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     }
 
     // rank decision (kernels.py:78-81)
-    __shared__ int rank_s;
     if (t == 0) {
-        const double d0 = fabs(W[0]);
+        const double d0 = fabs(diagR[0]);
         int r = 0;
         if (d0 != 0.0) {
             const double cut = (double)(m > k ? m : k) * EPS * d0;
             for (int i = 0; i < kmin; ++i)
-                if (fabs(W[(long long)i * ldw + i]) > cut) ++r;
+                if (fabs(diagR[i]) > cut) ++r;
         }
         rank_s = r;
         rank_out[args.base + b] = r;
@@ -172,38 +173,42 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     __syncthreads();
     const int rank = rank_s;
 
-    // dorg2r on the first `rank` columns, in place
+    // dorg2r on positions 0..rank-1 (storage of position i = physical pos2phys[i])
     for (int i = rank - 1; i >= 0; --i) {
-        double *ci = W + (long long)i * ldw;
+        double *ci = W + (long long)pos2phys[i] * ldw;
         const double ti = tau[i];
         if (i < rank - 1) {
-            if (t == 0) ci[i] = 1.0;
-            __syncthreads();
-            for (int j = i + 1 + warp; j < rank; j += nw) {
-                double *cj = W + (long long)j * ldw;
+            for (int jp = i + 1 + warp; jp < rank; jp += nw) {
+                double *cj = W + (long long)pos2phys[jp] * ldw;
                 double w = 0.0;
-                for (int r = i + lane; r < m; r += 32) w += ci[r] * cj[r];
-                w = warp_sum(w);
+                for (int r = i + 1 + lane; r < m; r += 32) w += ci[r] * cj[r];
+                w = warp_sum(w) + cj[i];  // v_i[i] = 1
                 const double f = ti * w;
-                for (int r = i + lane; r < m; r += 32) cj[r] -= f * ci[r];
+                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * ci[r];
+                __syncwarp();
+                if (lane == 0) cj[i] -= f;
+                __syncwarp();
             }
             __syncthreads();
         }
         for (int r = i + 1 + t; r < m; r += QR_THREADS) ci[r] *= -ti;
-        __syncthreads();
-        if (t == 0) ci[i] = 1.0 - ti;
         for (int r = t; r < i; r += QR_THREADS) ci[r] = 0.0;
+        if (t == 0) ci[i] = 1.0 - ti;
         __syncthreads();
     }
     double *Q = args.Q[b];
     const int ldq = args.ldq[b];
     for (long long e = t; e < (long long)m * rank; e += QR_THREADS) {
         const int r = (int)(e / rank), j = (int)(e % rank);
-        Q[(long long)r * ldq + j] = W[(long long)j * ldw + r];
+        Q[(long long)r * ldq + j] = W[(long long)pos2phys[j] * ldw + r];
     }
 }
 
-constexpr long long SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
+constexpr long long SMEM_BYTES_MAX = 220 * 1024;
+
+// the one-CTA kernel keeps the sketch plus 4 FP64 + 2 int per-column arrays in smem
+inline long long smem_bytes(int m, int k) { return (long long)(m | 1) * k * 8 + 40LL * k; }
+inline bool fits_smem(int m, int k) { return smem_bytes(m, k) <= SMEM_BYTES_MAX; }
 
 }  // namespace
 
@@ -218,8 +223,7 @@ static inline long long coop_bytes(int m, int k) { return ((rsc_qrcp_coop_double
 extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int *k) {
     long long tot = ((4LL * count + 255) / 256) * 256;  // group-barrier counters
     for (int i = 0; i < count; ++i) {
-        const long long sz = (long long)(m[i] | 1) * k[i];
-        if (sz > SMEM_LIMIT_DOUBLES) tot += coop_bytes(m[i], k[i]);
+        if (!fits_smem(m[i], k[i])) tot += coop_bytes(m[i], k[i]);
     }
     return tot < 256 ? 256 : tot;
 }
@@ -234,13 +238,13 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(qrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(SMEM_LIMIT_DOUBLES * 8));
+                             (int)SMEM_BYTES_MAX);
         attr_set = true;
     }
     std::vector<int> small, big;
     for (int i = 0; i < count; ++i) {
         if (k[i] > QR_MAXK || m[i] < 0 || k[i] < 0) return -4;
-        if ((long long)(m[i] | 1) * k[i] <= SMEM_LIMIT_DOUBLES) small.push_back(i);
+        if (fits_smem(m[i], k[i])) small.push_back(i);
         else big.push_back(i);
     }
     if (!big.empty() && !work_dev) return -10;
@@ -261,14 +265,15 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                 qa.G[c] = G[i]; qa.Q[c] = Q[i];
                 qa.m[c] = m[i]; qa.k[c] = k[i]; qa.ldg[c] = ldg[i]; qa.ldq[c] = ldq[i];
                 const long long sz = (long long)(m[i] | 1) * k[i];
-                maxsz = sz > maxsz ? sz : maxsz;
+                const long long need = smem ? smem_bytes(m[i], k[i]) : 40LL * k[i];
+                maxsz = need > maxsz ? need : maxsz;
                 qa.woff[c] = smem ? 0 : woff / 8;
                 if (!smem) woff += ((sz * 8 + 255) / 256) * 256;
             }
             if (smem) {
-                qrcp_kernel<true><<<qa.count, QR_THREADS, (size_t)(maxsz * 8), s>>>(qa, nullptr, rank_dev);
+                qrcp_kernel<true><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, nullptr, rank_dev);
             } else {
-                qrcp_kernel<false><<<qa.count, QR_THREADS, 0, s>>>(qa, (double *)work_dev, rank_dev);
+                qrcp_kernel<false><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, (double *)work_dev, rank_dev);
             }
             RSC_CHECK_LAUNCH();
         }
