@@ -124,9 +124,10 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         const int pc = piv_s;
         const double *ci = W + (long long)pc * ldw;
         const double tau_i = tau[i];
-        // apply H^T to the unchosen columns and downdate their norms
-        for (int j = warp; j < k; j += nw) {
-            if (posof[j] <= i) continue;
+        // apply H^T to the unchosen columns (positions > i, round-robin over warps for
+        // balance) and downdate their norms
+        for (int jp = i + 1 + warp; jp < k; jp += nw) {
+            const int j = pos2phys[jp];
             double *cj = W + (long long)j * ldw;
             if (tau_i != 0.0) {
                 double w = 0.0;
