@@ -205,6 +205,238 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident QRCP for small sketches (m <= 256, k <= 64, e.g. config[1]'s
+// 256 x 58): the sketch lives in registers -- physical column j belongs to warp
+// j % 16 (slot j / 16), lane l holds rows l, l+32, ..., l+224 -- so a Householder
+// step touches only registers plus one 2 KB reflector broadcast through shared
+// memory.  Every warp keeps a replicated copy of the position permutation (two
+// entries per lane) and evaluates the pivot rule itself, so a step needs exactly two
+// CTA barriers: after the owner of the pivot column publishes its reflector, and
+// after every warp has updated its columns and their partial norms.
+constexpr int RQ_ROWS = 8;   // rows per lane  (m <= 256)
+constexpr int RQ_SLOTS = 4;  // columns per warp (k <= 64)
+constexpr int RQ_WARPS = 16;
+
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+__global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_constant__ QrArgs args,
+                                                                  int *rank_out) {
+    __shared__ double v[RQ_ROWS * 32];
+    __shared__ double vn1[64], vn2[64], tau[64], diagR[64];
+    __shared__ int pc_s, rank_s;
+    const int b = blockIdx.x;
+    const int m = args.m[b], k = args.k[b];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const double *G = args.G[b];
+    const int ldg = args.ldg[b];
+    double a[RQ_SLOTS][RQ_ROWS];
+    int pos[RQ_SLOTS];  // position of my column, or k if unchosen
+#pragma unroll
+    for (int s = 0; s < RQ_SLOTS; ++s) {
+        const int j = warp + RQ_WARPS * s;
+        pos[s] = k;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) {
+            const int r = lane + 32 * q;
+            a[s][q] = (j < k && r < m) ? G[(long long)r * ldg + j] : 0.0;
+        }
+        double nrm = 0.0;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) nrm += a[s][q] * a[s][q];
+        nrm = sqrt(warp_sum(nrm));
+        if (j < k && lane == 0) { vn1[j] = nrm; vn2[j] = nrm; }
+    }
+    // replicated permutation: lane holds positions lane and lane+32
+    int p0 = lane, p1 = lane + 32;
+    __syncthreads();
+    const int kmin = m < k ? m : k;
+    for (int i = 0; i < kmin; ++i) {
+        // pivot rule, evaluated identically by every warp
+        double best = -1.0;
+        int bp = k;
+        if (lane >= i && lane < k) { const double x = vn1[p0]; if (x > best) { best = x; bp = lane; } }
+        if (lane + 32 >= i && lane + 32 < k) { const double x = vn1[p1]; if (x > best) { best = x; bp = lane + 32; } }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+            if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+        }
+        if (bp >= k) bp = i;
+        // swap positions i and bp in the replicated permutation
+        const int pi = __shfl_sync(0xffffffffu, i < 32 ? p0 : p1, i & 31);
+        const int pb = __shfl_sync(0xffffffffu, bp < 32 ? p0 : p1, bp & 31);
+        if (lane == (i & 31)) { if (i < 32) p0 = pb; else p1 = pb; }
+        if (lane == (bp & 31)) { if (bp < 32) p0 = pi; else p1 = pi; }
+        const int pc = pb;  // physical pivot column
+        const int qi = i >> 5, li = i & 31;  // row i lives in register q = qi of lane li
+        if ((pc & (RQ_WARPS - 1)) == warp) {
+            const int sp = pc / RQ_WARPS;
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                if (s != sp) continue;  // compile-time slot index keeps a[][] in registers
+                pos[s] = i;
+                // dlarfg on rows i..m-1 of the pivot column
+                double part = 0.0;
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r > i && r < m) part += a[s][q] * a[s][q];
+                }
+                const double xnorm = sqrt(warp_sum(part));
+                double alpha = 0.0;
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q)
+                    if (q == qi) alpha = shfl(a[s][q], li);
+                double tau_i = 0.0, beta = alpha, scal = 1.0;
+                if (xnorm != 0.0) {
+                    beta = -copysign(hypot(alpha, xnorm), alpha);
+                    tau_i = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r > i && r < m) {
+                        if (xnorm != 0.0) a[s][q] *= scal;
+                        v[r] = a[s][q];
+                    } else if (r == i) {
+                        a[s][q] = beta;
+                    }
+                }
+                if (lane == 0) { tau[i] = tau_i; diagR[i] = beta; pc_s = pc; }
+            }
+        }
+        __syncthreads();
+        const double tau_i = tau[i];
+        // apply H_i to my unchosen columns, downdate their norms
+        if (tau_i != 0.0 || true) {
+            double vr[RQ_ROWS];
+#pragma unroll
+            for (int q = 0; q < RQ_ROWS; ++q) {
+                const int r = lane + 32 * q;
+                vr[q] = (r > i && r < m) ? v[r] : 0.0;
+            }
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                const int j = warp + RQ_WARPS * s;
+                if (j >= k || pos[s] < k) continue;  // absent or already chosen
+                double ai = 0.0;
+                if (tau_i != 0.0) {
+                    double d = 0.0;
+#pragma unroll
+                    for (int q = 0; q < RQ_ROWS; ++q) d += vr[q] * a[s][q];
+#pragma unroll
+                    for (int q = 0; q < RQ_ROWS; ++q)
+                        if (q == qi) ai = shfl(a[s][q], li);
+                    const double f = tau_i * (warp_sum(d) + ai);
+#pragma unroll
+                    for (int q = 0; q < RQ_ROWS; ++q) {
+                        a[s][q] -= f * vr[q];
+                        if (q == qi && lane == li) a[s][q] -= f;
+                    }
+                }
+                ai = 0.0;
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q)
+                    if (q == qi) ai = shfl(a[s][q], li);
+                const double v1 = vn1[j];
+                if (v1 != 0.0) {
+                    double temp = fabs(ai) / v1;
+                    temp = 1.0 - temp * temp;
+                    temp = temp < 0.0 ? 0.0 : temp;
+                    const double ratio = v1 / vn2[j];
+                    const double temp2 = temp * ratio * ratio;
+                    if (temp2 <= TOL3Z) {
+                        double nv = 0.0;
+#pragma unroll
+                        for (int q = 0; q < RQ_ROWS; ++q) {
+                            const int r = lane + 32 * q;
+                            if (r > i && r < m) nv += a[s][q] * a[s][q];
+                        }
+                        nv = (i + 1 < m) ? sqrt(warp_sum(nv)) : 0.0;
+                        if (lane == 0) { vn1[j] = nv; vn2[j] = nv; }
+                    } else if (lane == 0) {
+                        vn1[j] = v1 * sqrt(temp);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        const double d0 = fabs(diagR[0]);
+        int r = 0;
+        if (d0 != 0.0) {
+            const double cut = (double)(m > k ? m : k) * EPS * d0;
+            for (int i = 0; i < kmin; ++i)
+                if (fabs(diagR[i]) > cut) ++r;
+        }
+        rank_s = r;
+        rank_out[args.base + b] = r;
+    }
+    __syncthreads();
+    const int rank = rank_s;
+    // dorg2r on positions rank-1 .. 0
+    for (int i = rank - 1; i >= 0; --i) {
+        const int qi = i >> 5, li = i & 31;
+        // publish v_i from its owner
+#pragma unroll
+        for (int s = 0; s < RQ_SLOTS; ++s) {
+            if (pos[s] != i) continue;
+#pragma unroll
+            for (int q = 0; q < RQ_ROWS; ++q) {
+                const int r = lane + 32 * q;
+                if (r > i && r < m) v[r] = a[s][q];
+            }
+        }
+        __syncthreads();
+        const double ti = tau[i];
+        double vr[RQ_ROWS];
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) {
+            const int r = lane + 32 * q;
+            vr[q] = (r > i && r < m) ? v[r] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < RQ_SLOTS; ++s) {
+            if (pos[s] > i && pos[s] < rank) {
+                double d = 0.0, ai = 0.0;
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) d += vr[q] * a[s][q];
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q)
+                    if (q == qi) ai = shfl(a[s][q], li);
+                const double f = ti * (warp_sum(d) + ai);
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    a[s][q] -= f * vr[q];
+                    if (q == qi && lane == li) a[s][q] -= f;
+                }
+            } else if (pos[s] == i) {
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    const int r = lane + 32 * q;
+                    a[s][q] = (r > i) ? -ti * vr[q] : (r == i ? 1.0 - ti : 0.0);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double *Q = args.Q[b];
+    const int ldq = args.ldq[b];
+#pragma unroll
+    for (int s = 0; s < RQ_SLOTS; ++s) {
+        if (pos[s] >= rank) continue;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) {
+            const int r = lane + 32 * q;
+            if (r < m) Q[(long long)r * ldq + pos[s]] = a[s][q];
+        }
+    }
+}
+
 constexpr long long SMEM_BYTES_MAX = 220 * 1024;
 
 // the one-CTA kernel keeps the sketch plus 4 FP64 + 2 int per-column arrays in smem
@@ -242,10 +474,11 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                              (int)SMEM_BYTES_MAX);
         attr_set = true;
     }
-    std::vector<int> small, big;
+    std::vector<int> tiny, small, big;
     for (int i = 0; i < count; ++i) {
         if (k[i] > QR_MAXK || m[i] < 0 || k[i] < 0) return -4;
-        if (fits_smem(m[i], k[i])) small.push_back(i);
+        if (m[i] <= RQ_ROWS * 32 && k[i] <= RQ_SLOTS * RQ_WARPS) tiny.push_back(i);
+        else if (fits_smem(m[i], k[i])) small.push_back(i);
         else big.push_back(i);
     }
     if (!big.empty() && !work_dev) return -10;
@@ -280,6 +513,23 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
         }
         return 0;
     };
+    // register-resident kernel for the smallest sketches (contiguous runs keep `base`)
+    {
+        size_t pos = 0;
+        while (pos < tiny.size()) {
+            qa.count = 0;
+            qa.base = tiny[pos];
+            while (pos < tiny.size() && qa.count < MAXB && tiny[pos] == qa.base + qa.count) {
+                const int i = tiny[pos++];
+                const int c = qa.count++;
+                qa.G[c] = G[i]; qa.Q[c] = Q[i];
+                qa.m[c] = m[i]; qa.k[c] = k[i]; qa.ldg[c] = ldg[i]; qa.ldq[c] = ldq[i];
+                qa.woff[c] = 0;
+            }
+            qrcp_reg_kernel<<<qa.count, RQ_WARPS * 32, 0, s>>>(qa, rank_dev);
+            RSC_CHECK_LAUNCH();
+        }
+    }
     int rc = run(small, true);
     if (rc) return rc;
     // large sketches: all of them concurrently in cooperative multi-CTA groups;
