@@ -16,7 +16,7 @@
 namespace {
 
 constexpr int NB = 64;
-constexpr int MAXB = 256;
+constexpr int MAXB = 600;  // whole level / batch per launch
 
 struct DiagArgs {
     int count;

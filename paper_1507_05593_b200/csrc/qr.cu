@@ -22,7 +22,7 @@ namespace {
 
 constexpr int QR_THREADS = 512;
 constexpr int QR_MAXK = 1024;
-constexpr int MAXB = 160;
+constexpr int MAXB = 600;  // one launch covers a whole config[1] batch (single partial wave)
 constexpr double EPS = 2.220446049250313e-16;        // np.finfo(float64).eps
 constexpr double TOL3Z = 1.0536712127723509e-08;     // sqrt(dlamch('E')) = sqrt(2^-53)
 
