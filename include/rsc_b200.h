@@ -22,6 +22,9 @@
 #ifndef RSC_B200_H
 #define RSC_B200_H
 
+#include <stddef.h>
+#include <stdint.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -169,6 +172,31 @@ int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_id
 int rsc_sym_postorder(long long n, const long long *parent, long long *post);
 int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *row_idx,
                       const long long *parent, const long long *post, long long *counts);
+
+/* ---- Gaussian sketches (replaces the host draw at reference kernels.py:85-92,
+ * np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r)), seeded per
+ * block by factor.py:324-326 _block_seed) ---------------------------------------
+ *
+ * rsc_pcg64_block_states: for each i, keys[i*width .. +nkeys[i]] = (master, tags...)
+ * -> seed = SeedSequence(keys).generate_state(1, uint64)[0] (seeds_out, optional)
+ * -> PCG64(seed) state as 4 words (state_hi, state_lo, inc_hi, inc_lo).  Host only.
+ * rsc_pcg64_seed_states: the same from ready-made seeds.
+ * rsc_normal_pcg64: out[i][0 .. n[i]) = the first n[i] standard normals of stream i,
+ * bit-identical to numpy's Generator.standard_normal (C order), generated on the
+ * device.  `states` is HOST memory (4 words per stream); work is device memory of
+ * rsc_normal_workspace_bytes(count, n) bytes.
+ * rsc_log1p_fdlibm: the host copy of the device log1p (test hook). */
+int rsc_pcg64_block_states(int count, int width, const uint64_t *keys, const int *nkeys,
+                           uint64_t *seeds_out, uint64_t *states_out);
+int rsc_pcg64_seed_states(int count, const uint64_t *seeds, uint64_t *states_out);
+size_t rsc_normal_workspace_bytes(int count, const long long *n);
+int rsc_normal_pcg64(int count, const unsigned long long *states, const long long *n,
+                     double *const *out, void *work, size_t work_bytes, void *stream);
+double rsc_log1p_fdlibm(double x);
+/* Test hook: cand_cap (0..160) caps the slow positions a chunk may record and
+ * slack = 0 scans only n/2 draws, forcing both exact sequential fallbacks.
+ * Defaults (160, 1) restore the fast path. */
+int rsc_normal_debug_limits(int cand_cap, int slack);
 
 /* Number of kernels this process launched through the library (reset != 0
  * returns the count and zeroes it).  Diagnostic only. */

@@ -48,6 +48,12 @@ EXPORTED = (
     "rsc_sym_etree",
     "rsc_sym_postorder",
     "rsc_sym_colcounts",
+    "rsc_pcg64_block_states",
+    "rsc_pcg64_seed_states",
+    "rsc_normal_workspace_bytes",
+    "rsc_normal_pcg64",
+    "rsc_log1p_fdlibm",
+    "rsc_normal_debug_limits",
     "rsc_launch_counter",
     "rsc_version",
     "rsc_device_arch",
@@ -81,6 +87,12 @@ _SIGS = {
     "rsc_sym_etree": (I, [LL, P, P, P]),
     "rsc_sym_postorder": (I, [LL, P, P]),
     "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
+    "rsc_pcg64_block_states": (I, [I, I, P, P, P, P]),
+    "rsc_pcg64_seed_states": (I, [I, P, P]),
+    "rsc_normal_workspace_bytes": (ctypes.c_size_t, [I, P]),
+    "rsc_normal_pcg64": (I, [I, P, P, P, P, ctypes.c_size_t, P]),
+    "rsc_log1p_fdlibm": (D, [D]),
+    "rsc_normal_debug_limits": (I, [I, I]),
     "rsc_launch_counter": (LL, [I]),
     "rsc_version": (ctypes.c_char_p, []),
     "rsc_device_arch": (I, []),

@@ -3,6 +3,7 @@
 For a batch of independent supernodes (diagonal block D_i, off-diagonal block B_i)
 this runs, entirely on the device and batched across supernodes:
 
+    Omega_i ~ PCG64(_block_seed(master, 0, i)) normals   rsc_normal_pcg64  (kernels.py:85-92)
     L_D = chol(D)                       rsc_potrf_batched      (factor.py:614)
     L_O = B L_D^{-T}                    rsc_trsm_batched        (factor.py:414,633)
     G   = L_O^T Omega                   grouped DMMA GEMM       (kernels.py:107)
@@ -12,7 +13,8 @@ this runs, entirely on the device and batched across supernodes:
 
 which is the reference composition dense_cholesky -> tri_solve -> low_rank_approx
 for every block.  Omega_i are the reference's own PCG64 sketches
-(seed `_block_seed(seed, 0, i)`), generated on host threads and uploaded unchanged.
+(seed `_block_seed(seed, 0, i)`), generated on the device bit-identically to numpy
+(rng.cu), so no sketch crosses PCIe.
 
 The whole batch goes through each stage in one grouped launch (the products
 stream L_O from HBM at ~8 flop/byte, above the FP64 ridge); `chunk` can cut the
@@ -86,10 +88,30 @@ class BatchedSupernodes:
         self.info = E.zeros(nb, dtype=E.I32)
         self.rank = E.zeros(nb, dtype=E.I32)
         self._qr_work = None
+        self._rng_n = np.full(nb, m * r, dtype=np.int64)
+        lib = E.require_cuda()
+        self._rng_work = E.empty(int(lib.rsc_normal_workspace_bytes(nb, self._rng_n.ctypes.data)) // 8 + 1)
+        self._rng_ptrs = [self.Om[i].data_ptr() for i in range(nb)]
 
-    def run(self):
-        """Factor + compress every block (inputs already in self.D / self.B / self.Om)."""
+    def sketch_states(self, master):
+        """PCG64 states of the blocks' sketches (reference seeding, host integer work)."""
+        keys = np.zeros((self.nb, 3), dtype=np.uint64)
+        keys[:, 0] = master
+        keys[:, 2] = np.arange(self.nb, dtype=np.uint64)
+        return E.pcg64_block_states(keys)[1]
+
+    def generate_sketches(self, master=0):
+        """Omega_i = PCG64(_block_seed(master, 0, i)).standard_normal((m, r)) on the device."""
+        w = self._rng_work
+        E.normal_pcg64(self.sketch_states(master), self._rng_n, self._rng_ptrs, alloc=lambda k: w[:k])
+
+    def run(self, master=0, sketches=True):
+        """Factor + compress every block (inputs in self.D / self.B).  The sketches are
+        generated on the device first unless `sketches` is False (then self.Om is used
+        as the caller left it)."""
         n, m, r, q = self.n, self.m, self.r, self.q
+        if sketches:
+            self.generate_sketches(master)
         for c0 in range(0, self.nb, self.chunk):
             c1 = min(self.nb, c0 + self.chunk)
             cnt = c1 - c0
@@ -115,10 +137,10 @@ class BatchedSupernodes:
         if bad.size:
             raise IndefiniteError(int(info[bad[0]]) - 1, f"block {int(bad[0])}: pivot {int(info[bad[0]]) - 1}")
 
-    def factor_compress_host(self, D, B, master=0, threads=8, pinned=None):
-        """Public host-buffer entry point: H2D of D/B (pinned staging), host PCG64
-        sketches generated on `threads` threads while the copies fly, the batched
-        pipeline, then D2H of (L_D, V, U, ranks).  Returns host arrays."""
+    def factor_compress_host(self, D, B, master=0, pinned=None):
+        """Public host-buffer entry point: H2D of D/B (pinned staging), the batched
+        pipeline (sketches generated on the device), then D2H of (L_D, V, U, ranks).
+        Returns host arrays."""
         if pinned is None:
             pinned = self.pinned_staging()
         st = pinned
@@ -130,9 +152,7 @@ class BatchedSupernodes:
             else:
                 np.copyto(st[key].numpy(), np.asarray(src))
                 dst.copy_(st[key], non_blocking=True)
-        make_sketches(self.nb, self.m, self.r, master=master, threads=threads, out=st["Om"].numpy())
-        self.Om.copy_(st["Om"], non_blocking=True)
-        self.run()
+        self.run(master)
         st["LD"].copy_(self.D, non_blocking=True)
         st["V"].copy_(self.V, non_blocking=True)
         st["U"].copy_(self.U, non_blocking=True)
@@ -147,11 +167,11 @@ class BatchedSupernodes:
         def pin(*shape, dtype=torch.float64):
             return torch.empty(*shape, dtype=dtype, pin_memory=True)
 
-        return {"D": pin(nb, n, n), "B": pin(nb, m, n), "Om": pin(nb, m, r), "LD": pin(nb, n, n),
+        return {"D": pin(nb, n, n), "B": pin(nb, m, n), "LD": pin(nb, n, n),
                 "V": pin(nb, m, r), "U": pin(nb, n, r), "rank": pin(nb, dtype=torch.int32)}
 
     def h2d_bytes(self):
-        return 8 * self.nb * (self.n * self.n + self.m * self.n + self.m * self.r)
+        return 8 * self.nb * (self.n * self.n + self.m * self.n)
 
     def d2h_bytes(self):
         return 8 * self.nb * (self.n * self.n + self.m * self.r + self.n * self.r) + 4 * self.nb

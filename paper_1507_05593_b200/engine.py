@@ -348,6 +348,64 @@ def qrcp_batched(Gptrs, m, k, ldg, Qptrs, ldq, rank_out, alloc=None):
 
 
 # ---------------------------------------------------------------------------
+# Gaussian sketches (device PCG64 + numpy ziggurat)
+
+
+def pcg64_block_states(keys):
+    """keys: (master, tag, ...) int tuples, or a 2-D uint64 array of equal-length
+    keys -> (seeds uint64[count], PCG64 states uint64[count, 4]) exactly as the
+    reference seeds each sketch (factor.py:324-326 then np.random.PCG64(seed)).
+    Host integer work in the library, no device."""
+    lib = _lib.load()
+    if isinstance(keys, np.ndarray):
+        K = np.ascontiguousarray(keys, dtype=np.uint64)
+        count, width = K.shape
+        nk = np.full(count, width, dtype=np.int32)
+    else:
+        count = len(keys)
+        width = max((len(k) for k in keys), default=1)
+        K = np.zeros((count, width), dtype=np.uint64)
+        nk = np.empty(count, dtype=np.int32)
+        for i, k in enumerate(keys):
+            K[i, :len(k)] = [int(v) for v in k]
+            nk[i] = len(k)
+    seeds = np.empty(count, dtype=np.uint64)
+    states = np.empty((count, 4), dtype=np.uint64)
+    if count:
+        check(lib.rsc_pcg64_block_states(count, width, addr(K), addr(nk), addr(seeds), addr(states)),
+              "rsc_pcg64_block_states")
+    return seeds, states
+
+
+def pcg64_seed_states(seeds):
+    lib = _lib.load()
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    states = np.empty((seeds.size, 4), dtype=np.uint64)
+    if seeds.size:
+        check(lib.rsc_pcg64_seed_states(int(seeds.size), addr(seeds), addr(states)), "rsc_pcg64_seed_states")
+    return states
+
+
+def normal_pcg64(states, n, out_ptrs, alloc=None):
+    """out_ptrs[i][0:n[i]] <- numpy's standard_normal stream of PCG64 state i
+    (bit-identical), generated on the current stream.  Returns the workspace
+    (keep alive until the stream passes it)."""
+    lib = require_cuda()
+    states = np.ascontiguousarray(np.asarray(states, dtype=np.uint64).reshape(-1, 4))
+    n = np.ascontiguousarray(np.asarray(n, dtype=np.int64))
+    outs = ptr_array(out_ptrs)
+    count = int(n.size)
+    if count == 0:
+        return None
+    wbytes = int(lib.rsc_normal_workspace_bytes(count, addr(n)))
+    nw = max((wbytes + 7) // 8, 1)
+    work = alloc(nw) if alloc is not None else torch.empty(nw, dtype=F64, device=dev())
+    check(lib.rsc_normal_pcg64(count, addr(states), addr(n), addr(outs), work.data_ptr(), nw * 8,
+                               stream_handle()), "rsc_normal_pcg64")
+    return work
+
+
+# ---------------------------------------------------------------------------
 # sparse + vector
 
 

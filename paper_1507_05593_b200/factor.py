@@ -882,7 +882,6 @@ def factorize(A, config=None, coords=None, prepared=None):
             torch.cuda.current_stream().synchronize()
             break
         except _Indefinite as e:
-            ps.sketches.drain()  # host threads may still write the shared pinned buffer
             torch.cuda.current_stream().synchronize()
             if e.trees == 0:
                 raise IndefiniteError(e.pivot) from None

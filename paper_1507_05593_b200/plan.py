@@ -20,7 +20,6 @@ L(rows, C_B) of interior.py:77-95; rows outside off_rows are exact zeros).
 """
 
 import numpy as np
-import torch
 
 from . import engine as E
 
@@ -214,7 +213,7 @@ class NumericPlan:
             self.node_levels[height[u]].append(u)
 
     def sketch_specs(self, cfg, alpha_d):
-        """(key, m, r, seed) of every Gaussian sketch one numeric pass draws, in sweep
+        """(key, m, r, seed key) of every Gaussian sketch one numeric pass draws, in sweep
         order: off-diagonal blocks (seed tag (0, j), factor.py:620-625) and compressed
         diagonal-tree blocks (seed tag (1, j, s), factor.py:605-610)."""
         from .symbolic import block_rank
@@ -237,14 +236,14 @@ class NumericPlan:
                     nr, ncl = nd.hi - nd.split, nd.split - nd.lo
                     r = block_rank(nr, ncl, alpha_d, cfg.oversample)
                     if r < 0.75 * min(nr, ncl):
-                        specs.append((("diag", j, s), nr, min(r, nr, ncl), _seed(cfg.seed, 1, j, s)))
+                        specs.append((("diag", j, s), nr, min(r, nr, ncl), (cfg.seed, 1, j, s)))
             r_off = block_rank(R.size, nc, cfg.alpha_o, cfg.oversample)
             if R.size and r_off < 0.75 * min(R.size, nc):
-                specs.append((("off", j), R.size, min(r_off, R.size, nc), _seed(cfg.seed, 0, j)))
+                specs.append((("off", j), R.size, min(r_off, R.size, nc), (cfg.seed, 0, j)))
         return specs
 
     def sketches_for(self, cfg, alpha_d):
-        return SketchSet(self.sketch_specs(cfg, alpha_d))
+        return DeviceSketches(self.sketch_specs(cfg, alpha_d))
 
 
     def _build_targets(self, part, touched):
@@ -317,53 +316,32 @@ class NumericPlan:
                 }
 
 
-def _seed(master, *tags):
-    """factor.py:324-326."""
-    ss = np.random.SeedSequence((int(master),) + tuple(int(t) for t in tags))
-    return int(ss.generate_state(1, np.uint64)[0])
-
-
-class SketchSet:
-    """Host PCG64 sketches of one pass, generated on a thread pool in sweep order
-    into one pinned buffer while the GPU works (numpy releases the GIL while
-    filling), and copied to the device asynchronously right before use.  The
-    values are the reference's own stream (kernels.py:85-92), unchanged."""
-
-    _pool = None
-    _pinned = None
+class DeviceSketches:
+    """All Gaussian sketches of one numeric pass, generated on the device by one
+    rsc_normal_pcg64 call before the sweep starts, bit-identical to the reference's
+    host draws np.random.Generator(np.random.PCG64(_block_seed(seed, *tags)))
+    .standard_normal((m, r)) (kernels.py:85-92, factor.py:324-326).  The buffer
+    lives in the pass's own arena, released with the pass."""
 
     def __init__(self, specs):
-        import concurrent.futures as cf
-        import os
-
         self.index = {}
+        keys, ns, offs = [], [], []
         off = 0
-        for key, m, r, seed in specs:
-            self.index[key] = (off, m, r, seed)
-            off += m * r
-        total = max(off, 1)
-        if SketchSet._pinned is None or SketchSet._pinned.numel() < total:
-            SketchSet._pinned = torch.empty(total, dtype=torch.float64, pin_memory=True)
-        host = SketchSet._pinned.numpy()
-        if SketchSet._pool is None:
-            SketchSet._pool = cf.ThreadPoolExecutor(max(1, min(8, (os.cpu_count() or 2) - 1)))
+        for key, m, r, seed_key in specs:
+            self.index[key] = (off, m, r)
+            keys.append(seed_key)
+            ns.append(m * r)
+            offs.append(off)
+            off += -(-(m * r) // 32) * 32
+        self.arena = E.Arena(max(off, 32))
+        self.buf = self.arena.empty(max(off, 32))
+        if keys:
+            _, states = E.pcg64_block_states(keys)
+            base = self.buf.data_ptr()
+            ptrs = np.asarray(offs, dtype=np.uint64) * 8 + base
+            E.normal_pcg64(states, ns, ptrs, alloc=self.arena.empty)
 
-        def fill(off, m, r, seed):
-            out = host[off:off + m * r].reshape(m, r)
-            np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r), out=out)
-
-        self.futures = {key: SketchSet._pool.submit(fill, *v) for key, v in self.index.items()}
-        self.host = SketchSet._pinned
-
-    def drain(self):
-        for f in self.futures.values():
-            f.result()
-
-    def device(self, key, m, r, arena):
-        off, m0, r0, _ = self.index[key]
+    def device(self, key, m, r, arena=None):
+        off, m0, r0 = self.index[key]
         assert (m0, r0) == (m, r), (key, m0, r0, m, r)
-        self.futures[key].result()
-        G = arena.empty(m, r)
-        if m * r:
-            G.view(-1).copy_(self.host[off:off + m * r], non_blocking=True)
-        return G
+        return self.buf[off:off + m * r].view(m, r)

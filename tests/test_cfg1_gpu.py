@@ -15,13 +15,13 @@ def test_cfg1_batched_matches_reference(cuda):
 
     nb = 8
     D, B = batched_supernodes(nb=nb)
-    Om = make_sketches(nb, 2048, 58, master=0, threads=4)
     bs = BatchedSupernodes(nb, 256, 2048, 58, q=1, chunk=3)
     bs.D.copy_(torch.from_numpy(D))
     bs.B.copy_(torch.from_numpy(B))
-    bs.Om.copy_(torch.from_numpy(Om))
-    bs.run()
+    bs.run()  # device sketches
     torch.cuda.synchronize()
+    # the device sketches are the reference's host stream, bit for bit
+    assert np.array_equal(bs.Om.cpu().numpy(), make_sketches(nb, 2048, 58, master=0, threads=4))
     bs.check_info()
     g = golden("cfg1.npz")
     for i in range(nb):
@@ -52,7 +52,29 @@ def test_cfg1_indefinite_block_reported(cuda):
     bs.D.copy_(torch.from_numpy(D))
     bs.B.copy_(torch.from_numpy(rng.standard_normal((nb, m, n))))
     bs.Om.copy_(torch.from_numpy(rng.standard_normal((nb, m, r))))
-    bs.run()
+    bs.run(sketches=False)
     with pytest.raises(IndefiniteError) as e:
         bs.check_info()
     assert e.value.pivot == 70
+
+
+def test_cfg1_host_api_round_trip(cuda):
+    """factor_compress_host (pinned H2D, device sketches, D2H) == the device path."""
+    import torch
+    from paper_1507_05593_b200.batched import BatchedSupernodes
+    from paper_1507_05593_b200.problems import batched_supernodes
+
+    nb = 4
+    D, B = batched_supernodes(nb=nb)
+    bs = BatchedSupernodes(nb, 256, 2048, 58, q=1)
+    LD, V, U, rank = bs.factor_compress_host(D, B, master=0)
+    LD, V, U = LD.copy(), V.copy(), U.copy()
+    bs.D.copy_(torch.from_numpy(D))
+    bs.B.copy_(torch.from_numpy(B))
+    bs.run(master=0)
+    torch.cuda.synchronize()
+    assert list(rank) == [48] * nb
+    assert np.array_equal(LD, bs.D.cpu().numpy())
+    # the split-K sketch products accumulate with FP64 atomics: equal up to rounding
+    assert relerr(V, bs.V.cpu().numpy()) < 1e-12
+    assert relerr(U, bs.U.cpu().numpy()) < 1e-12
