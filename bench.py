@@ -218,9 +218,9 @@ def run_b200_cfg1(args, rank, world, torch, dist):
     B0 = torch.from_numpy(B).cuda()
 
     def step():
+        # POTRF is in place: restore D (268 MB); the TRSM reads B0 and writes L_O
         bs.D.copy_(D0)
-        bs.B.copy_(B0)
-        bs.run(master=0)  # includes the device PCG64 sketch generation
+        bs.run(master=0, B_src=B0)  # includes the device PCG64 sketch generation
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -317,8 +317,8 @@ def run_b200_cfg1(args, rank, world, torch, dist):
                    "factor_seconds_per_step": t / args.steps,
                    "fp64_tc_frac_of_step": value / world / 1e3 / peak,
                    "kept_ranks": sorted(set(int(x) for x in ranks)),
-                   "l2": "inputs larger than L2 (2.4 GB/step); step re-copies D,B from a pristine device copy "
-                         "(in-place kernels)"},
+                   "l2": "inputs larger than L2 (2.4 GB/step); each step re-copies D from a pristine device copy "
+                         "(in-place POTRF) and the TRSM reads B from its pristine copy"},
         "roofline": {"bound": "tensor", "achieved": gemm_flops / gemm_t / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": gemm_flops / gemm_t / 1e12 / peak, "traffic": None,
                      "kernel": "gemm_grouped_kernel (sketch products L_O^T Omega, L_O G)",

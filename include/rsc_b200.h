@@ -81,6 +81,15 @@ int rsc_trsm_batched(int side, int trans, int count, const double *const *L,
                      const int *n, const int *ldl, const double *const *Dinv,
                      double *const *B, const int *m, const int *ldb, void *stream);
 
+/* Right-side solve X = Bsrc L^{-T} written to B (Bsrc == NULL: in place), for
+ * panels with n <= 320: one launch, each CTA keeping a 64-row strip resident in
+ * shared memory (rsc_trsm_batched side = 1 uses the same kernel when it can).
+ * Returns -3 if some n > 320.  Replaces kernels.py:42-64 tri_solve at
+ * factor.py:414,633. */
+int rsc_trsm_right_batched(int count, const double *const *L, const int *n, const int *ldl,
+                           const double *const *Dinv, const double *const *Bsrc,
+                           double *const *B, const int *m, const int *ldb, void *stream);
+
 /* Inverses of the 64x64 diagonal blocks of caller-supplied lower triangles
  * (Dinv[i]: n[i] x 64, ld 64), so rsc_trsm_batched can solve with them. */
 int rsc_trtri_diag_batched(int count, const double *const *L, const int *n,

@@ -31,6 +31,7 @@ EXPORTED = (
     "rsc_gemm_grouped",
     "rsc_potrf_batched",
     "rsc_trsm_batched",
+    "rsc_trsm_right_batched",
     "rsc_trtri_diag_batched",
     "rsc_qrcp_workspace_bytes",
     "rsc_qrcp_batched",
@@ -70,6 +71,7 @@ _SIGS = {
     "rsc_gemm_grouped": (I, [I, I, P, I, P]),
     "rsc_potrf_batched": (I, [I, P, P, P, P, P, P]),
     "rsc_trsm_batched": (I, [I, I, I, P, P, P, P, P, P, P, P]),
+    "rsc_trsm_right_batched": (I, [I, P, P, P, P, P, P, P, P, P]),
     "rsc_trtri_diag_batched": (I, [I, P, P, P, P, P]),
     "rsc_qrcp_workspace_bytes": (LL, [I, P, P]),
     "rsc_qrcp_batched": (I, [I, P, P, P, P, P, P, P, P, P]),

@@ -91,7 +91,8 @@ class BatchedSupernodes:
         self._rng_n = np.full(nb, m * r, dtype=np.int64)
         lib = E.require_cuda()
         self._rng_work = E.empty(int(lib.rsc_normal_workspace_bytes(nb, self._rng_n.ctypes.data)) // 8 + 1)
-        self._rng_ptrs = [self.Om[i].data_ptr() for i in range(nb)]
+        self._rng_ptrs = np.asarray([self.Om[i].data_ptr() for i in range(nb)], dtype=np.uint64)
+        self._streams = None
 
     def sketch_states(self, master):
         """PCG64 states of the blocks' sketches (reference seeding, host integer work)."""
@@ -100,27 +101,33 @@ class BatchedSupernodes:
         keys[:, 2] = np.arange(self.nb, dtype=np.uint64)
         return E.pcg64_block_states(keys)[1]
 
-    def generate_sketches(self, master=0):
-        """Omega_i = PCG64(_block_seed(master, 0, i)).standard_normal((m, r)) on the device."""
+    def generate_sketches(self, master=0, lo=0, hi=None, states=None):
+        """Omega_i = PCG64(_block_seed(master, 0, i)).standard_normal((m, r)) on the
+        device, for blocks lo..hi-1."""
+        hi = self.nb if hi is None else hi
+        states = self.sketch_states(master) if states is None else states
         w = self._rng_work
-        E.normal_pcg64(self.sketch_states(master), self._rng_n, self._rng_ptrs, alloc=lambda k: w[:k])
+        E.normal_pcg64(states[lo:hi], self._rng_n[lo:hi], self._rng_ptrs[lo:hi], alloc=lambda k: w[:k])
 
-    def run(self, master=0, sketches=True):
-        """Factor + compress every block (inputs in self.D / self.B).  The sketches are
-        generated on the device first unless `sketches` is False (then self.Om is used
-        as the caller left it)."""
+    def run(self, master=0, sketches=True, lo=0, hi=None, states=None, B_src=None):
+        """Factor + compress blocks lo..hi-1 (inputs in self.D / self.B, or the
+        off-diagonal blocks read from the device tensor B_src and L_O written to
+        self.B).  The sketches are generated on the device first unless `sketches` is
+        False (then self.Om is used as the caller left it)."""
         n, m, r, q = self.n, self.m, self.r, self.q
+        hi = self.nb if hi is None else hi
         if sketches:
-            self.generate_sketches(master)
-        for c0 in range(0, self.nb, self.chunk):
-            c1 = min(self.nb, c0 + self.chunk)
+            self.generate_sketches(master, lo, hi, states)
+        for c0 in range(lo, hi, self.chunk):
+            c1 = min(hi, c0 + self.chunk)
             cnt = c1 - c0
             idx = range(c0, c1)
             Dp = [self.D[i].data_ptr() for i in idx]
             Ip = [self.Dinv[i].data_ptr() for i in idx]
             E.potrf_batched(Dp, [n] * cnt, [n] * cnt, Ip, self.info[c0:c1])
             Bp = [self.B[i].data_ptr() for i in idx]
-            E.trsm_batched("right", 1, Dp, [n] * cnt, [n] * cnt, Ip, Bp, [m] * cnt, [n] * cnt)
+            Sp = None if B_src is None else [B_src[i].data_ptr() for i in idx]
+            E.trsm_right(Dp, [n] * cnt, [n] * cnt, Ip, Sp, Bp, [m] * cnt, [n] * cnt)
             LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
             E.gemm_strided_batched(LO, Om, G, transA=True, splitk=self.splitk)
             for _ in range(q):
@@ -137,27 +144,54 @@ class BatchedSupernodes:
         if bad.size:
             raise IndefiniteError(int(info[bad[0]]) - 1, f"block {int(bad[0])}: pivot {int(info[bad[0]]) - 1}")
 
-    def factor_compress_host(self, D, B, master=0, pinned=None):
-        """Public host-buffer entry point: H2D of D/B (pinned staging), the batched
-        pipeline (sketches generated on the device), then D2H of (L_D, V, U, ranks).
-        Returns host arrays."""
+    def factor_compress_host(self, D, B, master=0, pinned=None, pieces=16):
+        """Public host-buffer entry point: H2D of D/B, the batched pipeline (sketches
+        generated on the device), D2H of (L_D, V, U, ranks); returns host arrays.
+
+        The batch is cut into `pieces` slices pipelined over three streams -- the
+        copy engine uploads slice k+1 while the SMs factor slice k and the other copy
+        engine downloads slice k-1 -- so the step costs about one PCIe pass of the
+        inputs instead of upload + compute + download."""
         if pinned is None:
             pinned = self.pinned_staging()
         st = pinned
         # page-locked caller buffers go straight to the copy engine; pageable numpy
         # arrays are staged through the pinned buffers first
-        for key, src, dst in (("D", D, self.D), ("B", B, self.B)):
-            if isinstance(src, torch.Tensor) and src.is_pinned():
-                dst.copy_(src, non_blocking=True)
+        src = {}
+        for key, a in (("D", D), ("B", B)):
+            if isinstance(a, torch.Tensor) and a.is_pinned():
+                src[key] = a
             else:
-                np.copyto(st[key].numpy(), np.asarray(src))
-                dst.copy_(st[key], non_blocking=True)
-        self.run(master)
-        st["LD"].copy_(self.D, non_blocking=True)
-        st["V"].copy_(self.V, non_blocking=True)
-        st["U"].copy_(self.U, non_blocking=True)
-        st["rank"].copy_(self.rank, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+                np.copyto(st[key].numpy(), np.asarray(a))
+                src[key] = st[key]
+        comp = torch.cuda.current_stream()
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        up, down = self._streams
+        up.wait_stream(comp)  # device buffers are free once earlier work on comp is done
+        states = self.sketch_states(master)
+        k = max(1, min(pieces, self.nb))
+        bounds = [self.nb * i // k for i in range(k + 1)]
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            if hi == lo:
+                continue
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(up):
+                self.D[lo:hi].copy_(src["D"][lo:hi], non_blocking=True)
+                self.B[lo:hi].copy_(src["B"][lo:hi], non_blocking=True)
+                ev.record(up)
+            comp.wait_event(ev)
+            self.run(master, lo=lo, hi=hi, states=states)
+            done = torch.cuda.Event()
+            done.record(comp)
+            down.wait_event(done)
+            with torch.cuda.stream(down):
+                st["LD"][lo:hi].copy_(self.D[lo:hi], non_blocking=True)
+                st["V"][lo:hi].copy_(self.V[lo:hi], non_blocking=True)
+                st["U"][lo:hi].copy_(self.U[lo:hi], non_blocking=True)
+                st["rank"][lo:hi].copy_(self.rank[lo:hi], non_blocking=True)
+        down.synchronize()
+        comp.wait_stream(down)
         self.check_info()
         return st["LD"].numpy(), st["V"].numpy(), st["U"].numpy(), st["rank"].numpy()
 

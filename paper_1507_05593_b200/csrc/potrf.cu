@@ -210,6 +210,20 @@ extern "C" int rsc_potrf_batched(int count, double *const *A, const int *n, cons
     return 0;
 }
 
+int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const int *ldl,
+                         const double *const *Dinv, const double *const *Bsrc, double *const *B,
+                         const int *m, const int *ldb, cudaStream_t s);
+
+extern "C" int rsc_trsm_right_batched(int count, const double *const *L, const int *n, const int *ldl,
+                                      const double *const *Dinv, const double *const *Bsrc,
+                                      double *const *B, const int *m, const int *ldb, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!L || !n || !ldl || !Dinv || !B || !m || !ldb) return -2;
+    const int rc = rsc_trsm_right_fused(count, L, n, ldl, Dinv, Bsrc, B, m, ldb, (cudaStream_t)stream);
+    return rc == -1000 ? -3 : rc;  // some n > 320: use rsc_trsm_batched
+}
+
 extern "C" int rsc_trsm_batched(int side, int trans, int count, const double *const *L,
                                 const int *n, const int *ldl, const double *const *Dinv,
                                 double *const *B, const int *m, const int *ldb, void *stream) {
@@ -219,6 +233,10 @@ extern "C" int rsc_trsm_batched(int side, int trans, int count, const double *co
     if (count < 0) return -3;
     if (count == 0) return 0;
     if (!L || !n || !ldl || !Dinv || !B || !m || !ldb) return -4;
+    if (side == 1) {  // fused strip-resident kernel when every panel has n <= 320
+        const int rc = rsc_trsm_right_fused(count, L, n, ldl, Dinv, nullptr, B, m, ldb, (cudaStream_t)stream);
+        if (rc != -1000) return rc;
+    }
     int maxn = 0;
     for (int i = 0; i < count; ++i) maxn = n[i] > maxn ? n[i] : maxn;
     const int steps = (maxn + NB - 1) / NB;

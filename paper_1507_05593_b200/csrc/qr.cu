@@ -310,57 +310,90 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
         }
         __syncthreads();
         const double tau_i = tau[i];
-        // apply H_i to my unchosen columns, downdate their norms
-        if (tau_i != 0.0 || true) {
-            double vr[RQ_ROWS];
+        // apply H_i to my unchosen columns and downdate their norms; the four slots
+        // run side by side (one interleaved butterfly) instead of one after another
+        double vr[RQ_ROWS];
 #pragma unroll
-            for (int q = 0; q < RQ_ROWS; ++q) {
-                const int r = lane + 32 * q;
-                vr[q] = (r > i && r < m) ? v[r] : 0.0;
-            }
+        for (int q = 0; q < RQ_ROWS; ++q) {
+            const int r = lane + 32 * q;
+            vr[q] = (r > i && r < m) ? v[r] : 0.0;
+        }
+        bool act[RQ_SLOTS];
+        double ai[RQ_SLOTS], v1[RQ_SLOTS], v2[RQ_SLOTS];
+#pragma unroll
+        for (int s = 0; s < RQ_SLOTS; ++s) {
+            const int j = warp + RQ_WARPS * s;
+            act[s] = j < k && pos[s] >= k;  // present and not yet chosen
+            v1[s] = act[s] ? vn1[j] : 0.0;
+            v2[s] = act[s] ? vn2[j] : 1.0;
+            double x = 0.0;
+#pragma unroll
+            for (int q = 0; q < RQ_ROWS; ++q)
+                if (q == qi) x = a[s][q];
+            ai[s] = shfl(x, li);
+        }
+        if (tau_i != 0.0) {
+            double d[RQ_SLOTS];
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
-                const int j = warp + RQ_WARPS * s;
-                if (j >= k || pos[s] < k) continue;  // absent or already chosen
-                double ai = 0.0;
-                if (tau_i != 0.0) {
-                    double d = 0.0;
+                d[s] = 0.0;
 #pragma unroll
-                    for (int q = 0; q < RQ_ROWS; ++q) d += vr[q] * a[s][q];
+                for (int q = 0; q < RQ_ROWS; ++q) d[s] += vr[q] * a[s][q];
+            }
 #pragma unroll
-                    for (int q = 0; q < RQ_ROWS; ++q)
-                        if (q == qi) ai = shfl(a[s][q], li);
-                    const double f = tau_i * (warp_sum(d) + ai);
+            for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-                    for (int q = 0; q < RQ_ROWS; ++q) {
-                        a[s][q] -= f * vr[q];
-                        if (q == qi && lane == li) a[s][q] -= f;
-                    }
+                for (int s = 0; s < RQ_SLOTS; ++s) d[s] += __shfl_xor_sync(0xffffffffu, d[s], o);
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                if (!act[s]) continue;
+                const double f = tau_i * (d[s] + ai[s]);
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    a[s][q] -= f * vr[q];
+                    if (q == qi && lane == li) a[s][q] -= f;
                 }
-                ai = 0.0;
+                ai[s] -= f;  // row i after the update (v_i = 1 there, vr = 0)
+            }
+        }
+        // dlaqp2 partial-norm downdate; recompute when cancellation is too strong
+        bool redo[RQ_SLOTS];
+        bool any_redo = false;
 #pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q)
-                    if (q == qi) ai = shfl(a[s][q], li);
-                const double v1 = vn1[j];
-                if (v1 != 0.0) {
-                    double temp = fabs(ai) / v1;
-                    temp = 1.0 - temp * temp;
-                    temp = temp < 0.0 ? 0.0 : temp;
-                    const double ratio = v1 / vn2[j];
-                    const double temp2 = temp * ratio * ratio;
-                    if (temp2 <= TOL3Z) {
-                        double nv = 0.0;
+        for (int s = 0; s < RQ_SLOTS; ++s) {
+            redo[s] = false;
+            if (!act[s] || v1[s] == 0.0) continue;
+            double temp = fabs(ai[s]) / v1[s];
+            temp = 1.0 - temp * temp;
+            temp = temp < 0.0 ? 0.0 : temp;
+            const double ratio = v1[s] / v2[s];
+            const double temp2 = temp * ratio * ratio;
+            if (temp2 <= TOL3Z) {
+                redo[s] = any_redo = true;
+            } else if (lane == 0) {
+                vn1[warp + RQ_WARPS * s] = v1[s] * sqrt(temp);
+            }
+        }
+        if (any_redo) {
+            double nv[RQ_SLOTS];
 #pragma unroll
-                        for (int q = 0; q < RQ_ROWS; ++q) {
-                            const int r = lane + 32 * q;
-                            if (r > i && r < m) nv += a[s][q] * a[s][q];
-                        }
-                        nv = (i + 1 < m) ? sqrt(warp_sum(nv)) : 0.0;
-                        if (lane == 0) { vn1[j] = nv; vn2[j] = nv; }
-                    } else if (lane == 0) {
-                        vn1[j] = v1 * sqrt(temp);
-                    }
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                nv[s] = 0.0;
+#pragma unroll
+                for (int q = 0; q < RQ_ROWS; ++q) {
+                    const int r = lane + 32 * q;
+                    if (r > i && r < m) nv[s] += a[s][q] * a[s][q];
                 }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int s = 0; s < RQ_SLOTS; ++s) nv[s] += __shfl_xor_sync(0xffffffffu, nv[s], o);
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                if (!redo[s]) continue;
+                const double x = (i + 1 < m) ? sqrt(nv[s]) : 0.0;
+                if (lane == 0) { vn1[warp + RQ_WARPS * s] = x; vn2[warp + RQ_WARPS * s] = x; }
             }
         }
         __syncthreads();

@@ -326,6 +326,18 @@ def trsm_batched(side, trans, Lptrs, n, ldl, dinv_ptrs, Bptrs, m, ldb):
           "rsc_trsm_batched")
 
 
+def trsm_right(Lptrs, n, ldl, dinv_ptrs, src_ptrs, Bptrs, m, ldb):
+    """B = Bsrc L^{-T} (out of place; src_ptrs None = in place), n <= 320."""
+    lib = require_cuda()
+    Lptrs, n, ldl, dinv_ptrs = ptr_array(Lptrs), int_array(n), int_array(ldl), ptr_array(dinv_ptrs)
+    Bptrs, m, ldb = ptr_array(Bptrs), int_array(m), int_array(ldb)
+    src = None if src_ptrs is None else ptr_array(src_ptrs)
+    if n.size == 0:
+        return
+    check(lib.rsc_trsm_right_batched(int(n.size), addr(Lptrs), addr(n), addr(ldl), addr(dinv_ptrs), addr(src),
+                                     addr(Bptrs), addr(m), addr(ldb), stream_handle()), "rsc_trsm_right_batched")
+
+
 # ---------------------------------------------------------------------------
 # QRCP
 

@@ -75,6 +75,7 @@ def test_cfg1_host_api_round_trip(cuda):
     torch.cuda.synchronize()
     assert list(rank) == [48] * nb
     assert np.array_equal(LD, bs.D.cpu().numpy())
-    # the split-K sketch products accumulate with FP64 atomics: equal up to rounding
-    assert relerr(V, bs.V.cpu().numpy()) < 1e-12
-    assert relerr(U, bs.U.cpu().numpy()) < 1e-12
+    # the split-K sketch products accumulate with FP64 atomics: equal up to rounding;
+    # columns past the rank are unspecified
+    assert relerr(V[:, :, :48], bs.V.cpu().numpy()[:, :, :48]) < 1e-12
+    assert relerr(U[:, :, :48], bs.U.cpu().numpy()[:, :, :48]) < 1e-12

@@ -171,3 +171,44 @@ def test_qrcp_batched_mixed_sizes_concurrent(cuda):
         Q = Qd[i][:, :ranks[i]].cpu().numpy()
         assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
     del work
+
+
+@pytest.mark.parametrize("n", [1, 37, 64, 100, 256, 300, 320, 321, 400])
+def test_trsm_right_fused_shapes(cuda, n):
+    """X = B L^{-T} for a batch of panels with ragged m and n (the strip-resident kernel
+    for n <= 320, the blocked path above), in place and out of place."""
+    import torch
+
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(n)
+    ms = [1, 63, 64, 65, 700]
+    Ls, Dinvs, Bs = [], [], []
+    for m in ms:
+        G = rng.standard_normal((n, n))
+        A = G @ G.T / n + np.eye(n)
+        Ad = E.to_dev(A)
+        Dv = E.zeros(max(n, 1), 64)
+        info = E.zeros(1, dtype=E.I32)
+        E.potrf_batched([Ad.data_ptr()], [n], [n], [Dv.data_ptr()], info)
+        Ls.append(Ad)
+        Dinvs.append(Dv)
+        Bs.append(rng.standard_normal((m, n)))
+    Bd = [E.to_dev(B) for B in Bs]
+    Xd = [torch.full_like(b, float("nan")) for b in Bd]
+    args = ([L.data_ptr() for L in Ls], [n] * len(ms), [n] * len(ms), [d.data_ptr() for d in Dinvs])
+    if n <= 320:
+        E.trsm_right(*args, [b.data_ptr() for b in Bd], [x.data_ptr() for x in Xd], ms, [n] * len(ms))
+    E.trsm_batched("right", 1, *args, [b.data_ptr() for b in Bd], ms, [n] * len(ms))  # in place
+    torch.cuda.synchronize()
+    for L, B, b, x in zip(Ls, Bs, Bd, Xd):
+        Lh = np.tril(L.cpu().numpy())
+        ref = np.linalg.solve(Lh, B.T).T  # B L^{-T}
+        assert relerr(b.cpu().numpy(), ref) < 1e-12
+        if n <= 320:
+            assert np.array_equal(x.cpu().numpy(), b.cpu().numpy())  # same kernel, same bits
+    if n > 320:
+        from paper_1507_05593_b200 import _lib
+
+        with pytest.raises(RuntimeError):
+            E.trsm_right(*args, None, [b.data_ptr() for b in Bd], ms, [n] * len(ms))
