@@ -99,7 +99,8 @@ int rsc_trtri_diag_batched(int count, const double *const *L, const int *n,
  * G[i] (m[i] x k[i], ld ldg[i]) is destroyed.  rank_dev[i] receives
  * #{ |R_jj| > max(m,k) * eps * |R_00| } (eps = 2^-52), and Q[i] (m[i] x k[i],
  * ld ldq[i]) receives the first rank_dev[i] columns of the orthonormal factor
- * (remaining columns unspecified).  Pivot selection, Householder vectors and the
+ * and exact zeros in the remaining k[i] - rank_dev[i] columns (so a caller may keep
+ * sketch-width panels without reading the ranks back).  Pivot selection, Householder vectors and the
  * partial-norm downdating follow LAPACK dgeqp3/dlaqp2 + dorg2r, which is what
  * scipy.linalg.qr(pivoting=True) runs.  work_dev: caller workspace of at least
  * rsc_qrcp_workspace_bytes(count, m, k) bytes.

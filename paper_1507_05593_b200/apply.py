@@ -97,7 +97,8 @@ class _Prog:
 
 class DeviceApply:
     def __init__(self, F):
-        self.F = F
+        # no strong reference back to the factor (it owns this program): a cycle would
+        # keep the factor's device arena alive until the cyclic GC runs
         self.n = F.n
         plan = F.plan
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))

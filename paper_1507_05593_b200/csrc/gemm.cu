@@ -18,7 +18,10 @@
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NT = 128;
+#ifndef RSC_GEMM_BK
+#define RSC_GEMM_BK 16
+#endif
+constexpr int BM = 64, BN = 64, BK = RSC_GEMM_BK, NT = 128;
 constexpr int PADK = BK + 4;   // [m][k] / [n][k] row stride (doubles)
 constexpr int PADM = BM + 4;   // [k][m] / [k][n] row stride: 2*PADM = 8 mod 32 banks
 constexpr int A_SZ = (BM * PADK > BK * PADM) ? BM * PADK : BK * PADM;
@@ -42,10 +45,10 @@ __device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const doub
                                            double *sA, double *sB) {
     const int t = threadIdx.x;
     if (!TA) {  // A row-major M x K, contiguous along k
-        const int k = t & 15, mr = t >> 4;
+        const int k = t % BK, mr = t / BK;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int m = mr + 8 * i;
+        for (int i = 0; i < BM * BK / NT; ++i) {
+            const int m = mr + (NT / BK) * i;
             const bool v = (m0 + m < P.M) && (k0 + k < P.K);
             const double *src = v ? A + (long long)(m0 + m) * P.lda + (k0 + k) : A;
             cp_async_8(&sA[m * PADK + k], src, v);
@@ -53,7 +56,7 @@ __device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const doub
     } else {  // A stored K x M, contiguous along m
         const int m = t & 63, kr = t >> 6;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < BK / 2; ++i) {
             const int k = kr + 2 * i;
             const bool v = (m0 + m < P.M) && (k0 + k < P.K);
             const double *src = v ? A + (long long)(k0 + k) * P.lda + (m0 + m) : A;
@@ -63,7 +66,7 @@ __device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const doub
     if (!TB) {  // op(B) = B (K x N), contiguous along n, optional row gather
         const int n = t & 63, kr = t >> 6;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < BK / 2; ++i) {
             const int k = kr + 2 * i;
             const bool v = (n0 + n < P.N) && (k0 + k < P.K);
             const double *src = B;
@@ -74,10 +77,10 @@ __device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const doub
             cp_async_8(&sB[k * PADM + n], src, v);
         }
     } else {  // op(B) = B^T with B stored N x K, contiguous along k
-        const int k = t & 15, nr = t >> 4;
+        const int k = t % BK, nr = t / BK;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int n = nr + 8 * i;
+        for (int i = 0; i < BN * BK / NT; ++i) {
+            const int n = nr + (NT / BK) * i;
             const bool v = (n0 + n < P.N) && (k0 + k < P.K);
             const double *src = v ? B + (long long)(n0 + n) * P.ldb + (k0 + k) : B;
             cp_async_8(&sB[n * PADK + k], src, v);

@@ -494,6 +494,39 @@ extern "C" long long rsc_qrcp_workspace_bytes(int count, const int *m, const int
     return tot < 256 ? 256 : tot;
 }
 
+// Q[:, rank:k] = 0 for every matrix (the factor keeps sketch-width panels whose
+// trailing columns must contribute exact zeros; no host readback of the ranks)
+__global__ void zero_tail_kernel(const __grid_constant__ QrArgs a, const int *rank_dev) {
+    const int b = blockIdx.x;
+    const int r0 = rank_dev[a.base + b], k = a.k[b], m = a.m[b], ldq = a.ldq[b];
+    const int w = k - r0;
+    if (w <= 0) return;
+    double *Q = a.Q[b];
+    for (long long e = threadIdx.x; e < (long long)m * w; e += blockDim.x) {
+        const int r = (int)(e / w), j = r0 + (int)(e % w);
+        Q[(long long)r * ldq + j] = 0.0;
+    }
+}
+
+int qr_zero_tails(int count, const int *m, const int *k, double *const *Q, const int *ldq, int *rank_dev,
+                  cudaStream_t s) {
+    static thread_local QrArgs qa;
+    for (int c0 = 0; c0 < count; c0 += MAXB) {
+        const int cnt = count - c0 < MAXB ? count - c0 : MAXB;
+        qa.count = cnt;
+        qa.base = c0;
+        for (int c = 0; c < cnt; ++c) {
+            qa.Q[c] = Q[c0 + c];
+            qa.m[c] = m[c0 + c];
+            qa.k[c] = k[c0 + c];
+            qa.ldq[c] = ldq[c0 + c];
+        }
+        zero_tail_kernel<<<cnt, 256, 0, s>>>(qa, rank_dev);
+        RSC_CHECK_LAUNCH();
+    }
+    return 0;
+}
+
 extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const int *k,
                                 const int *ldg, double *const *Q, const int *ldq, int *rank_dev,
                                 void *work_dev, void *stream) {
@@ -567,13 +600,16 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     if (rc) return rc;
     // large sketches: all of them concurrently in cooperative multi-CTA groups;
     // workspace = barrier counters, then per-matrix slices in index order
-    if (big.empty()) return 0;
-    std::vector<long long> off(count, 0);
-    long long o = ((4LL * count + 255) / 256) * 256;
-    for (int i : big) {
-        off[i] = o;
-        o += coop_bytes(m[i], k[i]);
+    if (!big.empty()) {
+        std::vector<long long> off(count, 0);
+        long long o = ((4LL * count + 255) / 256) * 256;
+        for (int i : big) {
+            off[i] = o;
+            o += coop_bytes(m[i], k[i]);
+        }
+        rc = rsc_qrcp_multi((int)big.size(), big.data(), G, m, k, ldg, Q, ldq, rank_dev, (char *)work_dev,
+                            off.data(), (unsigned *)work_dev, s);
+        if (rc) return rc;
     }
-    return rsc_qrcp_multi((int)big.size(), big.data(), G, m, k, ldg, Q, ldq, rank_dev, (char *)work_dev,
-                          off.data(), (unsigned *)work_dev, s);
+    return qr_zero_tails(count, m, k, Q, ldq, rank_dev, s);
 }

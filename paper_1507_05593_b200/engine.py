@@ -129,6 +129,10 @@ def scratch(*shape):
     return empty(*shape)
 
 
+def torch_from_numpy(a):
+    return torch.from_numpy(np.ascontiguousarray(a))
+
+
 def to_dev(a, dtype=None):
     t = torch.as_tensor(np.ascontiguousarray(a))
     if dtype is not None:

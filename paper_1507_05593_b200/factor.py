@@ -143,10 +143,11 @@ class DevLR:
     """Low-rank block V U^T (U orthonormal), with E = V (U^T U) kept for the
     eff_rows role of blocks.py:103-113."""
 
-    __slots__ = ("V", "U", "E", "k")
+    __slots__ = ("V", "U", "E", "k", "kslot")
 
     def __init__(self, V, U, Eff):
         self.V, self.U, self.E, self.k = V, U, Eff, U.shape[1]
+        self.kslot = None  # device rank word while the columns are still sketch-padded
 
 
 class DeviceTree:
@@ -847,7 +848,7 @@ def prepare(A, config=None, coords=None):
     t0 = time.perf_counter()
     sym = analyze(A, config.tau_o, config.tau_d, config.interior_blocks, coords=coords)
     t1 = time.perf_counter()
-    plan = NumericPlan(sym, config.interior_blocks)
+    plan = NumericPlan(sym, config.interior_blocks, A)
     t2 = time.perf_counter()
     return (sym, plan, config, t0, t1, t2)
 
@@ -865,8 +866,10 @@ def factorize(A, config=None, coords=None, prepared=None):
         sym, plan, config, t0, t_plan0, t2 = prepared
     else:
         sym, plan, config, _, _, _ = prepared
-        t0 = t_plan0 = t2 = time.perf_counter()
+        t0 = t_plan0 = time.perf_counter()
         sym.t_ordering = sym.t_symbolic = 0.0
+        plan.load_values(A)  # same pattern, possibly new values (refactorization)
+        t2 = time.perf_counter()
     from . import _lib
     from .numeric import LevelPass
 

@@ -4,10 +4,12 @@ The reference sweeps its units one at a time (factor.py:556-639).  A compressed
 separator only reads its update sources -- interior blocks and separators lower in
 the nested-dissection tree -- so all separators of one ND level are independent
 and their work is issued together: every step below is ONE grouped launch (or one
-batched call) over all nodes of the level, and the only host<->device
-synchronisations are one rank readback per batched QR.  Results are identical to
-the unit-by-unit order because each node's arithmetic is unchanged; only its
-interleaving with independent nodes differs.
+batched call) over all nodes of the level.  Compressed blocks stay at sketch width
+(the QR zeroes the columns past the rank), so the whole pass is issued without a
+host<->device synchronisation; one readback at the end trims the blocks to their
+ranks and resolves pivot failures.  Results are identical to the unit-by-unit order
+because each node's arithmetic is unchanged (the padded columns add exact zeros);
+only its interleaving with independent nodes differs.
 
 Per level:
   dense diagonals   A-block scatter + Schur update of all (node, source) pairs,
@@ -163,6 +165,28 @@ class LevelPass(NumericPass):
         self.s_ld = np.ones(ns, dtype=np.int64)
         self.s_w = np.zeros(ns, dtype=np.int64)      # panel width (0 = contributes nothing)
         self.idx_base = np.uint64(plan.idx.dev.data_ptr())
+        self._uslot = {}     # id(U) -> device rank word of a fresh QR factor
+        self._deferred = []  # (ranks key, DevLR) trimmed at the end of the pass
+        self._wterms = []    # flop terms coef * w * r whose widths may be sketch-padded
+        self._price = {}     # data_ptr of a final-product operand -> its U (re-priced at rank)
+
+    def _wflops(self, coef, w=1, wbase=0, r=1, rbase=0):
+        """Count flops coef * w * r where w is a source panel's width (panel base
+        pointer wbase) and r the width of the block being formed (its U at rbase, for
+        final products).  Compressed panels are sketch-padded during the pass;
+        _finalize_ranks re-prices these terms at the kept ranks so model_gflop stays
+        the reference's work model."""
+        if np.ndim(coef) == 0 and np.ndim(w) == 0 and np.ndim(r) == 0:
+            self.flops += float(coef) * float(w) * float(r)
+            if wbase or rbase:
+                self._wterms.append(tuple(np.array([v], dtype=t) for v, t in (
+                    (coef, np.float64), (w, np.int64), (wbase, np.uint64), (r, np.int64), (rbase, np.uint64))))
+            return
+        coef, w, wbase, r, rbase = np.broadcast_arrays(
+            np.asarray(coef, dtype=np.float64), np.asarray(w, dtype=np.int64), np.asarray(wbase, dtype=np.uint64),
+            np.asarray(r, dtype=np.int64), np.asarray(rbase, dtype=np.uint64))
+        self.flops += float(np.sum(coef * w * r))
+        self._wterms.append((coef.copy(), w.copy(), wbase.copy(), r.copy(), rbase.copy()))
 
     def _set_source(self, sid, raw, eff):
         self.src_panel[sid] = (raw, eff)
@@ -246,7 +270,7 @@ class LevelPass(NumericPass):
             lx.append(E.ld(X))
             yp.append(Y.data_ptr())
             ly.append(E.ld(Y))
-            self.flops += 2.0 * blk.nnz * X.shape[1]
+            self._wflops(2.0 * blk.nnz, r=X.shape[1], rbase=self._price.get(X.data_ptr(), 0))
         if nr:
             lib = E.require_cuda()
             from ._lib import int_array, ptr_array
@@ -259,7 +283,10 @@ class LevelPass(NumericPass):
                                              a[8].ctypes.data, E.stream_handle()), "rsc_spmm_csr_batched")
 
     def _orth_many(self, Gs):
-        """One batched pivoted QR over all sketches, one readback of all ranks."""
+        """One batched pivoted QR over all sketches.  The orthonormal factors are kept
+        at sketch width with exact zero columns past the rank (rsc_qrcp_batched zeroes
+        them), so nothing downstream needs the ranks on the host: they are read back
+        once, at the end of the pass, to trim the stored blocks (_finalize_ranks)."""
         Us = [None] * len(Gs)
         live = [(i, G) for i, G in enumerate(Gs) if G.shape[0] and G.shape[1]]
         for i, G in enumerate(Gs):
@@ -267,19 +294,16 @@ class LevelPass(NumericPass):
                 Us[i] = self.P.empty(G.shape[0], 0)
         if not live:
             return Us
-        Qs = [self.S.empty(*G.shape) for _, G in live]
+        Qs = [self.P.empty(*G.shape) for _, G in live]
+        base = self.ipos
         rank = self._ints(len(live))
         E.qrcp_batched([G.data_ptr() for _, G in live], [G.shape[0] for _, G in live],
                        [G.shape[1] for _, G in live], [E.ld(G) for _, G in live], [Q.data_ptr() for Q in Qs],
                        [E.ld(Q) for Q in Qs], rank, alloc=self.S.empty)
-        kept = rank.cpu().numpy()  # the only data-dependent sizes of the level
-        for (i, G), Q, k in zip(live, Qs, kept):
-            m = G.shape[0]
-            U = self.P.empty(m, int(k))
-            if k:
-                U.copy_(Q[:, :int(k)])
-            Us[i] = U
-            self.flops += 4.0 * m * G.shape[1] ** 2
+        for j, ((i, G), Q) in enumerate(zip(live, Qs)):
+            Us[i] = Q
+            self._uslot[id(Q)] = base + j
+            self.flops += 4.0 * G.shape[0] * G.shape[1] ** 2
         return Us
 
     def _lowrank_many(self, VUs):
@@ -293,7 +317,9 @@ class LevelPass(NumericPass):
                 g1.add(U.data_ptr(), E.ld(U), U.data_ptr(), E.ld(U), utu.data_ptr(), k, k, k, U.shape[0], 1.0, 0.0)
                 g2.add(V.data_ptr(), E.ld(V), utu.data_ptr(), k, Eff.data_ptr(), E.ld(Eff), V.shape[0], k, k,
                        1.0, 0.0)
-            out.append(DevLR(V, U, Eff))
+            lr = DevLR(V, U, Eff)
+            lr.kslot = self._uslot.pop(id(U), None)
+            out.append(lr)
         g1.launch()
         g2.launch()
         return out
@@ -345,7 +371,7 @@ class LevelPass(NumericPass):
                 p["c_cols"] = cpos[sel]
                 p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
                 probs.append(p)
-                self.flops += float(np.sum(2.0 * p["M"] * p["N"] * p["K"]))
+                self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s][sel])
         if probs:
             E.gemm_grouped(np.concatenate(probs), False, True)
         return out
@@ -363,10 +389,14 @@ class LevelPass(NumericPass):
                 G1.copy_(G)
             G1s.append(G1)
             sol.append((node, G1, True))
-            self.flops += node.ncols**2 * r
+            rb = G.data_ptr() if final else 0
+            if final:
+                self._price[G1.data_ptr()] = rb
+            self._wflops(node.ncols**2, r=r, rbase=rb)
         diag_solve_many(sol, self.S.empty)
         self._spmm_many([(self.np.node_blocks[n.j][1], G1, W) for n, G1, W in zip(nodes, G1s, Ws)])
         self._products_many(nodes, G1s, Ws, trans=False)
+        self._price.clear()
         return Ws
 
     def off_mul_t_many(self, nodes, Gs):
@@ -390,7 +420,7 @@ class LevelPass(NumericPass):
             t = self._pairs(node.j, need_rd=True, need_ro=True)
             if t["s"].size == 0:
                 continue
-            parts.append((t, r, G.data_ptr(), E.ld(G), W.data_ptr(), E.ld(W)))
+            parts.append((t, r, G.data_ptr(), E.ld(G), W.data_ptr(), E.ld(W), self._price.get(G.data_ptr(), 0)))
         if not parts:
             return
         cat = lambda key: np.concatenate([p[0][key] for p in parts])
@@ -422,7 +452,7 @@ class LevelPass(NumericPass):
             p2["A"], p2["M"], p2["c_rows"] = raw_lo, nrd, cpos
         E.gemm_grouped(p1, True, False)
         E.gemm_grouped(p2, False, False)
-        self.flops += float(np.sum(2.0 * (nrd + nro) * w * r))
+        self._wflops(2.0 * (nrd + nro), w=w, wbase=self.s_raw[s], r=r, rbase=rep(6).astype(np.uint64))
 
     def approx_off_many(self, nodes, ranks):
         """Alg. 3 for every compressed off-diagonal of the level (factor.py:486-505)."""
@@ -467,7 +497,7 @@ class LevelPass(NumericPass):
             k = lf.hi - lf.lo
             blocks.append((blk, k, k))
         Us = self._dense_many(blocks)
-        parts = []
+        parts, bases = [], []
         for (node, s), U in zip(items, Us):
             tree = node.diag
             lf = tree.shape.nodes[s]
@@ -485,6 +515,7 @@ class LevelPass(NumericPass):
                 p["c_cols"] = self.idx_base + (4 * t["cidx"]).astype(np.uint64)
                 p["C"], p["ldc"] = U.data_ptr(), k
                 parts.append(p)
+                bases.append(self.s_raw[src])
             path = self._path_probs(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi))
             if path:
                 p = np.zeros(len(path), dtype=GEMM_DTYPE)
@@ -493,11 +524,12 @@ class LevelPass(NumericPass):
                     p[i]["lda"], p[i]["ldb"], p[i]["K"], p[i]["M"], p[i]["N"] = ld, ld, w, a1 - a0, c1 - c0
                 p["C"], p["ldc"] = U.data_ptr(), k
                 parts.append(p)
+                bases.append(np.array([pt[0] for pt in path], dtype=np.uint64))
         if parts:
             P = np.concatenate(parts)
             P["batch"], P["atomic"], P["alpha"], P["beta"] = 1, 1, -1.0, 1.0
             E.gemm_grouped(P, False, True)
-            self.flops += float(np.sum(2.0 * P["M"] * P["N"] * P["K"]))
+            self._wflops(2.0 * P["M"] * P["N"], w=P["K"], wbase=np.concatenate(bases))
         if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
             Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
         return self._potrf_many([(U, node.u) for (node, s), U in zip(items, Us)])
@@ -518,7 +550,10 @@ class LevelPass(NumericPass):
                 if G.numel():
                     G1.copy_(G)
                 sol.append((node, G1, True, shape.nodes[s].left.s))
-                self.flops += (c1 - c0) ** 2 * r
+                rb = G.data_ptr() if final else 0
+                if final:
+                    self._price[G1.data_ptr()] = rb
+                self._wflops((c1 - c0) ** 2, r=r, rbase=rb)
                 W = mem.empty(r1 - r0, r)
                 spm.append((blk, G1, W))
                 srcs.append(G1)
@@ -541,6 +576,7 @@ class LevelPass(NumericPass):
             sid = t["s"]
             ld = self.s_ld[sid]
             w = self.s_w[sid]
+            base = self.s_raw[sid]
             raw_c = self.s_raw[sid] + (8 * t["clo"] * ld).astype(np.uint64)
             eff_r = self.s_eff[sid] + (8 * t["rlo"] * ld).astype(np.uint64)
             nc_, nr_ = t["chi"] - t["clo"], t["rhi"] - t["rlo"]
@@ -552,6 +588,7 @@ class LevelPass(NumericPass):
                 # (raw, eff, ld, w, row lo, row hi, col lo, col hi), window-aligned, no index maps
                 ld = np.concatenate([ld, pa[:, 2]])
                 w = np.concatenate([w, pa[:, 3]])
+                base = np.concatenate([base, pa[:, 0].astype(np.uint64)])
                 raw_c = np.concatenate([raw_c, (pa[:, 0] + 8 * pa[:, 6] * pa[:, 2]).astype(np.uint64)])
                 eff_r = np.concatenate([eff_r, (pa[:, 1] + 8 * pa[:, 4] * pa[:, 2]).astype(np.uint64)])
                 nc_ = np.concatenate([nc_, pa[:, 7] - pa[:, 6]])
@@ -579,7 +616,7 @@ class LevelPass(NumericPass):
                 p2["A"], p2["M"], p2["c_rows"] = raw_c, nc_, cidx
             p1s.append(p1)
             p2s.append(p2)
-            self.flops += float(np.sum(2.0 * (nc_ + nr_) * w * r))
+            self._wflops(2.0 * (nc_ + nr_), w=w, wbase=base, r=r, rbase=self._price.get(src.data_ptr(), 0))
         if p1s:
             P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
             P1["batch"], P1["alpha"] = 1, 1.0
@@ -651,7 +688,7 @@ class LevelPass(NumericPass):
             if comp:
                 for (node, s), lr in zip(comp, self.approx_diag_many(comp, comp_r)):
                     node.diag.blocks[s] = lr
-                    self.ranks[("diag", node.j, s)] = lr.k
+                    self._deferred.append((("diag", node.j, s), lr))
                     self.counters["compressed_diag"] += 1
 
     # -- the sweep ------------------------------------------------------------------
@@ -729,7 +766,7 @@ class LevelPass(NumericPass):
             if comp:
                 for n, lr in zip(comp, self.approx_off_many(comp, comp_r)):
                     n.off = lr
-                    self.ranks[("off", n.j)] = lr.k
+                    self._deferred.append((("off", n.j), lr))
                     self.counters["compressed_off"] += 1
             for n in nodes:
                 n._UO = None
@@ -738,11 +775,36 @@ class LevelPass(NumericPass):
                     self._set_source(sid, *_raw_eff(n.off))
         self.units = [by_unit[u] for u in range(len(self.sym.units))]
 
+    def _finalize_ranks(self, info):
+        """Trim every compressed block to its kept rank (views; the padded columns are
+        exact zeros) and record the ranks -- the pass's single rank readback."""
+        kept = {}
+        for key, lr in self._deferred:
+            k = int(info[lr.kslot]) if lr.kslot is not None else lr.k
+            kept[lr.V.data_ptr()] = k
+            kept[lr.U.data_ptr()] = k
+            lr.V, lr.U, lr.E, lr.k = lr.V[:, :k], lr.U[:, :k], lr.E[:, :k], k
+            self.ranks[key] = k
+        self._deferred = []
+        if self._wterms and kept:
+            coef, w, wb, r, rb = (np.concatenate([t[i] for t in self._wterms]) for i in range(5))
+            def look(bases, width):
+                ub, inv = np.unique(bases, return_inverse=True)
+                kk = np.array([kept.get(int(b), -1) for b in ub], dtype=np.int64)[inv]
+                return np.where(kk >= 0, kk, width)
+
+            wt, rt = look(wb, w), look(rb, r)
+            self.flops -= float(np.sum(coef * (w * r - wt * rt)))
+        self._wterms = []
+
     def check_pivots(self):
-        """Resolve every recorded pivot failure: the earliest unit in sweep order wins."""
-        if not self.pending:
+        """One readback of the pass's device words (POTRF info + QR ranks): trim the
+        compressed blocks, then resolve every recorded pivot failure (the earliest unit
+        in sweep order wins)."""
+        if not self.pending and not self._deferred:
             return
         info = self.ibuf[: self.ipos].cpu().numpy()
+        self._finalize_ranks(info)
         worst = None
         for rec in self.pending:
             off, cnt, unit, trees = rec[:4]

@@ -94,10 +94,13 @@ class CsrPool:
         self.nnz += S.nnz
         return CsrBlock(self, S.shape[0], S.shape[1], rp_off, nz_off, S.nnz)
 
-    def upload(self):
+    def upload(self, b_values):
+        """Device buffers; the blocks were cut from the position matrix, so their
+        values are 1-based positions into B's storage: pos -> values."""
         self.rp_dev = E.to_dev(np.concatenate(self.rp) if self.rp else np.zeros(1, np.int32))
         self.ci_dev = E.to_dev(np.concatenate(self.ci) if self.ci else np.zeros(1, np.int32))
-        self.v_dev = E.to_dev(np.concatenate(self.v) if self.v else np.zeros(1))
+        self.pos = (np.concatenate(self.v) if self.v else np.ones(1)).astype(np.int64) - 1
+        self.v_dev = E.to_dev(b_values[self.pos] if self.v else np.zeros(1))
 
 
 class CsrBlock:
@@ -130,12 +133,26 @@ class TreeBlockMaps:
 class NumericPlan:
     """Static device-side plan for the numeric phase of one symbolic plan."""
 
-    def __init__(self, sym, interior_enabled):
+    def __init__(self, sym, interior_enabled, A=None):
         self.sym = sym
         part = sym.partition
         B = sym.B
-        full = B.to_csr_full()
+        # Every A block of the plan is cut from a copy of B whose values are 1-based
+        # positions into B's storage, so one gather index maps any matrix with this
+        # pattern onto the device value buffer (load_values: refactorization).
+        from .sparse import SparseSpdMatrix, permute_symmetric
+
+        posB = SparseSpdMatrix(B.n, B.col_ptr, B.row_idx, np.arange(1, B.nnz_lower + 1, dtype=np.float64),
+                               validate=False)
+        full = posB.to_csr_full()
         self.full = full
+        if A is not None:  # B.values = A.values[b_from_a]
+            posA = SparseSpdMatrix(A.n, A.col_ptr, A.row_idx, np.arange(A.nnz_lower, dtype=np.float64),
+                                   validate=False)
+            self.b_from_a = permute_symmetric(posA, sym.perm).values.astype(np.int64)
+        else:
+            self.b_from_a = None
+        self.source = A
         self.idx = IndexPool()
         self.csr = CsrPool()
         self.sources = []
@@ -189,7 +206,7 @@ class NumericPlan:
         self.tree_maps = {}
         self._build_tree_maps(part)
         self.idx.upload()
-        self.csr.upload()
+        self.csr.upload(B.values)
         # unit indices of the nodes that get a diagonal tree (restart rule)
         self.tree_units = np.array(
             [u for u, (k, j) in enumerate(sym.units)
@@ -211,6 +228,19 @@ class NumericPlan:
         self.node_levels = [[] for _ in range(nlev)]
         for u in sorted(height):
             self.node_levels[height[u]].append(u)
+
+    def load_values(self, A):
+        """Refactorization: put the values of A (same pattern as the prepared matrix)
+        into the plan's device A blocks -- one host gather and one copy."""
+        if A is self.source:
+            return
+        if self.b_from_a is None:
+            raise ValueError("plan was prepared without its source matrix; cannot load new values")
+        if A.n != self.sym.B.n or A.nnz_lower != self.b_from_a.size:
+            raise ValueError("matrix pattern differs from the prepared one")
+        vals = np.asarray(A.values)[self.b_from_a][self.csr.pos]
+        self.csr.v_dev.copy_(E.torch_from_numpy(vals))
+        self.source = A
 
     def sketch_specs(self, cfg, alpha_d):
         """(key, m, r, seed key) of every Gaussian sketch one numeric pass draws, in sweep
