@@ -133,30 +133,37 @@ class DeviceApply:
     def _build_inverses(self, units):
         """Linv = L^{-1} (one batched TRSM against identities) and LinvT for every dense
         diagonal triangle and tree leaf: O(n^3/3) once per factor, after which every
-        apply's diagonal solves are bandwidth-bound GEMVs."""
+        apply's diagonal solves are bandwidth-bound GEMVs.  The buffers hang on the
+        triangles and are rewritten in place, so refresh_inverses() re-derives them
+        after a graph replay has overwritten the factor with new values."""
         tris = []
         for u in units:
             if isinstance(u.diag, DenseTri):
                 tris.append(u.diag)
             elif isinstance(u.diag, DeviceTree):
                 tris.extend(b for s_, b in u.diag.blocks.items() if u.diag.shape.nodes[s_].is_leaf)
-        tris = [t for t in tris if t.n and t.Linv is None]
+        self.tris = [t for t in tris if t.n]
+        if any(t.Linv is None for t in self.tris):
+            self.mem = E.Arena()
+            for t in self.tris:
+                if t.Linv is None:
+                    t.Linv = self.mem.empty(t.n, t.n)
+                    t.LinvT = self.mem.empty(t.n, t.n)
+        self.refresh_inverses()
+
+    def refresh_inverses(self):
+        tris = self.tris
         if not tris:
             return
-        self.mem = E.Arena()
-        Ls = []
         for t in tris:
-            I = self.mem.zeros(t.n, t.n)
-            I.fill_diagonal_(1.0)
-            Ls.append(I)
+            t.Linv.zero_()
+            t.Linv.fill_diagonal_(1.0)
         E.trsm_batched("left", 0, [t.L.data_ptr() for t in tris], [t.n for t in tris], [E.ld(t.L) for t in tris],
-                       [t.Dinv.data_ptr() for t in tris], [I.data_ptr() for I in Ls], [t.n for t in tris],
+                       [t.Dinv.data_ptr() for t in tris], [t.Linv.data_ptr() for t in tris], [t.n for t in tris],
                        [t.n for t in tris])
-        for t, I in zip(tris, Ls):
-            t.Linv = I
-            T = self.mem.empty(t.n, t.n)
-            T.copy_(I.t())
-            t.LinvT = T
+        for t in tris:
+            t.LinvT.copy_(t.Linv.t())
+
     def _rows_ptr(self, plan, un):
         key = ("int", un.u) if un.kind == "interior" else un.j
         return plan.idx.ptr(plan.rows_off[key])

@@ -1,7 +1,9 @@
 """bench.py --config 0|2|3|4: factor + PCG to rel-res 1e-6 on a sparse config.
 
 value   = device-timed numeric factorization + PCG (symbolic plan prepared, A and b
-          resident in HBM) in seconds -- the BASELINE metric "factor+PCG time".
+          resident in HBM) in seconds -- the BASELINE metric "factor+PCG time".  Each
+          step drops the previous factor, so from the third step on the numeric sweep
+          is the plan's recorded CUDA graph replayed on the matrix (refactorization).
 e2e     = the public API end to end: factorize(A, config, coords) (host ordering +
           symbolic + plan upload + numeric) and pcg_solve(A, b) with host b in and
           host x out.
@@ -82,7 +84,9 @@ def run_sparse(args, rank, world, torch, dist):
         x, rep = pcg_solve_device(A, bd, preconditioner=F, tol=1e-6)
         return F, rep
 
+    F = None
     for _ in range(max(args.warmup, 1)):
+        F = None  # a refactorization loop drops the previous factor (graph replay reuses its memory)
         F, rep = step()
     torch.cuda.synchronize()
     with B.ClockSampler(torch.cuda.current_device()) as clk:
@@ -94,6 +98,7 @@ def run_sparse(args, rank, world, torch, dist):
         tf = []
         ev0.record()
         for _ in range(args.steps):
+            F = None
             F, rep = step()
             tf.append(F.stats.phase_times["numeric"])
         ev1.record()
@@ -106,12 +111,32 @@ def run_sparse(args, rank, world, torch, dist):
         tt = torch.tensor([t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    work = F.stats.model_gflop
-    # dominant kernel: the grouped DMMA GEMM, timed per launch with CUDA events
+    st = F.stats
+    work = st.model_gflop
+    graph_nodes = st.gpu_launches if getattr(F, "_entry", None) is not None else 0
+    # dominant kernel: the grouped DMMA GEMM.  Its flops come from the launch
+    # descriptors of an ordinary pass; its device time from CUPTI kernel records
+    # (torch.profiler) of one timed-path step (the replayed graph) -- per-launch CUDA
+    # events would also count the host issue gaps between launches
+    import paper_1507_05593_b200.factor as FM
+    from torch.profiler import ProfilerActivity, profile
+
+    F = None
+    g0, FM.GRAPH_REFACTOR = FM.GRAPH_REFACTOR, False
     E.PROFILE = E.KernelProfile()
     step()
-    prof = E.PROFILE.summary()
+    gemm_flops = E.PROFILE.summary()["flops"]
     E.PROFILE = None
+    FM.GRAPH_REFACTOR = g0
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as kp:
+        F = None
+        F, _ = step()
+        torch.cuda.synchronize()
+    kev = [e for e in kp.events() if e.device_type.name == "CUDA"]
+    gemm_s = sum(e.device_time for e in kev if "gemm_grouped_kernel" in e.name) / 1e6
+    busy_s = sum(e.device_time for e in kev) / 1e6
+    prof = {"flops": gemm_flops, "seconds": gemm_s}
     peak = B.fp64_peak_tflops(torch)
     # end to end through the public API (host A, coords, b in; host x out)
     t0 = time.perf_counter()
@@ -143,18 +168,19 @@ def run_sparse(args, rank, world, torch, dist):
                    "pcg_iterations": rep.iterations, "final_relres": rep.relative_residual,
                    "numeric_factor_s": float(np.median(tf)), "symbolic_prepare_s": t_prep,
                    "modeled_gflop": work, "factor_gflops": work / float(np.median(tf)),
-                   "restarts": F.stats.restarts, "compressed_offdiag": F.stats.compressed_offdiag,
-                   "compressed_diag": F.stats.compressed_diag, "stored_scalars": F.stats.stored_scalars},
+                   "restarts": st.restarts, "compressed_offdiag": st.compressed_offdiag,
+                   "compressed_diag": st.compressed_diag, "stored_scalars": st.stored_scalars},
         "roofline": {"bound": "tensor", "achieved": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12,
                      "peak": peak, "unit": "TFLOP/s",
                      "frac": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12 / peak, "traffic": None,
                      "kernel": "gemm_grouped_kernel (all grouped GEMM launches of one factor+PCG)",
                      "kernel_seconds": prof["seconds"], "kernel_share_of_step": prof["seconds"] / t,
+                     "all_kernels_seconds": busy_s,
                      "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run"},
         "cpu_baseline": cpu,
         "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(8 * (A.nnz_lower * 2 + n)),
                 "d2h_bytes_per_step": int(8 * n)},
-        "gpu_launches": launches // args.steps,
+        "gpu_launches": launches // args.steps + graph_nodes,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

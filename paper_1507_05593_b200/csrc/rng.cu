@@ -78,10 +78,9 @@ struct ChunkMeta {
     int spec_exit;   // first try start past the chunk end - CH, same assumption
 };
 
-// jump tables: M^(2^k) and G_k = sum_{i < 2^k} M^i, so that k steps from s are
-// M^k s + inc * G(k) -- stream independent (host-computed, rsc_normal_pcg64)
-__constant__ unsigned long long c_jm[64][2];
-__constant__ unsigned long long c_jg[64][2];
+// jump tables c_jm / c_jg (build/ziggurat_tables.h): M^(2^k) and G_k = sum_{i < 2^k}
+// M^i, so that k steps from s are M^k s + inc * G(k) -- stream independent,
+// initialized with the module (no runtime upload, so every call is capture-safe)
 
 __device__ __forceinline__ u128 mk(unsigned long long hi, unsigned long long lo) {
     return ((u128)hi << 64) | lo;
@@ -517,23 +516,6 @@ extern "C" int rsc_normal_pcg64(int count, const unsigned long long *states, con
     if (!states || !n || !out || !work) return -2;
     if (work_bytes < rsc_normal_workspace_bytes(count, n)) return -3;
     cudaStream_t sm = (cudaStream_t)stream;
-    static bool tables = false;
-    if (!tables) {
-        unsigned long long jm[64][2], jg[64][2];
-        u128 m = ((u128)0x2360ed051fc65da4ULL << 64) | 0x4385df649fccf645ULL, g = 1;
-        for (int k = 0; k < 64; ++k) {
-            jm[k][0] = (unsigned long long)(m >> 64);
-            jm[k][1] = (unsigned long long)m;
-            jg[k][0] = (unsigned long long)(g >> 64);
-            jg[k][1] = (unsigned long long)g;
-            g = g * (m + 1);
-            m = m * m;
-        }
-        if (cudaMemcpyToSymbol(c_jm, jm, sizeof(jm)) != cudaSuccess ||
-            cudaMemcpyToSymbol(c_jg, jg, sizeof(jg)) != cudaSuccess)
-            return (int)cudaGetLastError();
-        tables = true;
-    }
     static thread_local RngArgs a;
     for (int g0 = 0; g0 < count; g0 += MAXS) {
         const int g1 = g0 + MAXS < count ? g0 + MAXS : count;

@@ -242,7 +242,14 @@ int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const 
     for (int i = 0; i < count; ++i) maxn = n[i] > maxn ? n[i] : maxn;
     if (maxn > TMAXN) return RSC_TRSM_TOO_WIDE;
     static thread_local TrsmArgs a;
-    static int attr_bytes = 0;
+    // the dynamic shared-memory cap is raised once, to the widest panel, so no
+    // attribute call happens later (e.g. inside a CUDA-graph capture)
+    static bool attr = false;
+    if (!attr) {
+        const int maxbytes = (SM_ROWS * (TMAXN + 4) + 2 * 64 * BPAD) * (int)sizeof(double);
+        cudaFuncSetAttribute(trsm_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxbytes);
+        attr = true;
+    }
     for (int c0 = 0; c0 < count;) {
         a.count = 0;
         long long tiles = 0;
@@ -266,10 +273,6 @@ int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const 
         a.tile_begin[a.count] = tiles;
         a.lds = ((mx + 63) & ~63) + 4;
         const int bytes = (SM_ROWS * a.lds + 2 * 64 * BPAD) * (int)sizeof(double);
-        if (bytes > attr_bytes) {
-            cudaFuncSetAttribute(trsm_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-            attr_bytes = bytes;
-        }
         trsm_right_kernel<<<(unsigned)tiles, TNT, bytes, s>>>(a);
         RSC_CHECK_LAUNCH();
     }

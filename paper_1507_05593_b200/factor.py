@@ -21,7 +21,9 @@ sm_100a kernels through the C ABI; all numeric data stays in HBM:
 """
 
 import math
+import os
 import time
+import weakref
 import warnings
 from dataclasses import dataclass, field
 
@@ -374,26 +376,30 @@ class NumericPass:
             Ys.append(self._dense_from_csr(A_off, off_rows.size, c1 - c0))
         return Ls, Ys
 
-    def factor_interiors(self):
+    def factor_interiors(self, defer=False):
         """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
-        Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM."""
+        Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM.  defer=True records the
+        POTRF info words as pending pivot checks instead of reading them back."""
         ints = self.np.interior
         self.first_interior_failure = None
         if not ints:
             return {}
         Ls, Ys = self._interior_mats(ints)
         Ds = [self.P.empty(max(c1 - c0, 1), 64) for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints]
+        info_off = self.ipos
         info = self._ints(len(ints))
         E.potrf_batched([L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
                         [D.data_ptr() for D in Ds], info)
         E.trsm_batched("right", 1, [L.data_ptr() for L in Ls], [L.shape[0] for L in Ls], [E.ld(L) for L in Ls],
                        [D.data_ptr() for D in Ds], [Y.data_ptr() for Y in Ys], [Y.shape[0] for Y in Ys],
                        [E.ld(Y) for Y in Ys])
-        iv = info.cpu().numpy()
+        iv = None if defer else info.cpu().numpy()
         out = {}
         self.first_interior_failure = None
         for i, (u, ids, c0, c1, off_rows, A_off, A_BB) in enumerate(ints):
-            if iv[i] and self.first_interior_failure is None:
+            if defer:
+                self.pending.append((info_off + i, 1, u, self._trees_before(u)))
+            elif iv[i] and self.first_interior_failure is None:
                 self.first_interior_failure = (u, int(iv[i]) - 1, self._trees_before(u))
             nb = c1 - c0
             stored = (A_off.nnz if A_off is not None else 0)
@@ -760,7 +766,13 @@ class RankStructuredFactor:
 
         if self._apply is None:
             self._apply = DeviceApply(self)
+            entry = getattr(self, "_entry", None)
+            if entry is not None:  # reusable by later replays with the same ranks
+                entry.apply, entry.apply_key = self._apply, self._apply_key()
         return self._apply(r_dev, out)
+
+    def _apply_key(self):
+        return tuple(sorted(self.ranks.items(), key=repr))
 
     # -- inspection ------------------------------------------------------------
     def stored_scalars(self):
@@ -838,6 +850,46 @@ class RankStructuredFactor:
                              shape=(self.n, self.n))
 
 
+# Refactorization through CUDA graphs: with a reused plan (factorize(..., prepared=)),
+# the sweep for a given alpha_d is captured once and replayed for every later matrix
+# of the same pattern -- the same kernels on the new values, without the host
+# re-issuing ~4k launches.  The replay rewrites the captured pass's memory, so it is
+# used only while no earlier factor from that graph is alive (otherwise an ordinary
+# pass runs on fresh memory).  RSC_GRAPH=0 disables it.
+GRAPH_REFACTOR = os.environ.get("RSC_GRAPH", "1") != "0"
+
+
+class _GraphEntry:
+    __slots__ = ("ps", "owner", "apply", "apply_key")
+
+    def __init__(self, ps):
+        self.ps, self.owner, self.apply, self.apply_key = ps, None, None, None
+
+
+def _numeric_pass(plan, config, alpha_d, use_graph):
+    """One numeric pass at alpha_d -> (pass, graph entry or None); raises _Indefinite."""
+    from .numeric import LevelPass
+
+    if use_graph:
+        graphs = plan.__dict__.setdefault("graphs", {})
+        entry = graphs.get(alpha_d)
+        if entry is None and alpha_d in plan.__dict__.setdefault("eager_seen", set()):
+            # second pass at this alpha_d: every kernel has run eagerly once (function
+            # attributes set, tables initialised), so the sweep can be recorded
+            ps = LevelPass(plan, config, alpha_d)
+            ps.capture()
+            entry = graphs[alpha_d] = _GraphEntry(ps)
+            ps.replay()
+            return ps, entry
+        if entry is not None and (entry.owner is None or entry.owner() is None):
+            entry.ps.replay()
+            return entry.ps, entry
+        plan.eager_seen.add(alpha_d)
+    ps = LevelPass(plan, config, alpha_d)
+    ps.run()
+    return ps, None
+
+
 def prepare(A, config=None, coords=None):
     """Host half of factorize: ordering + symbolic + device plan upload.  The
     result can be reused by factorize(..., prepared=...) for repeated numeric
@@ -861,6 +913,7 @@ def factorize(A, config=None, coords=None, prepared=None):
     pivot once a diagonal tree is in play, TooManyRestarts after max_restarts.
     """
     A = as_spd(A)
+    reuse = prepared is not None
     if prepared is None:
         prepared = prepare(A, config, coords)
         sym, plan, config, t0, t_plan0, t2 = prepared
@@ -871,17 +924,16 @@ def factorize(A, config=None, coords=None, prepared=None):
         plan.load_values(A)  # same pattern, possibly new values (refactorization)
         t2 = time.perf_counter()
     from . import _lib
-    from .numeric import LevelPass
 
     lib = _lib.load()
     launches0 = int(lib.rsc_launch_counter(0))
     alpha_d = config.alpha_d
     history = [alpha_d]
     restarts = 0
+    use_graph = reuse and GRAPH_REFACTOR
     while True:
-        ps = LevelPass(plan, config, alpha_d)
         try:
-            ps.run()
+            ps, entry = _numeric_pass(plan, config, alpha_d, use_graph)
             torch.cuda.current_stream().synchronize()
             break
         except _Indefinite as e:
@@ -900,6 +952,12 @@ def factorize(A, config=None, coords=None, prepared=None):
     F.units = ps.units
     F._mem = ps.P  # the factor owns its arena: chunks return to the pool only when F dies
     F.ranks = ps.ranks
+    if entry is not None:
+        entry.owner = weakref.ref(F)  # the graph may rewrite this memory once F is gone
+        F._entry = entry
+        if entry.apply is not None and entry.apply_key == F._apply_key():
+            F._apply = entry.apply  # same memory, same ranks: the apply program still holds
+            F._apply.refresh_inverses()  # ... once its explicit inverses are re-derived
     part = sym.partition
     st = F.stats
     st.n, st.nnz_lower = A.n, A.nnz_lower
@@ -914,6 +972,8 @@ def factorize(A, config=None, coords=None, prepared=None):
     st.alpha_d_final = alpha_d
     st.alpha_d_history = history
     st.gpu_launches = int(lib.rsc_launch_counter(0)) - launches0
+    if entry is not None:
+        st.gpu_launches = ps.launches  # kernel nodes of the replayed graph
     st.model_gflop = ps.flops / 1e9
     st.phase_times = {"ordering": sym.t_ordering, "symbolic": sym.t_symbolic + (t2 - t_plan0),
                       "numeric": t3 - t2, "total": t3 - t0}

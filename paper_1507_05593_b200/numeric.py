@@ -167,6 +167,9 @@ class LevelPass(NumericPass):
         self.idx_base = np.uint64(plan.idx.dev.data_ptr())
         self._uslot = {}     # id(U) -> device rank word of a fresh QR factor
         self._deferred = []  # (ranks key, DevLR) trimmed at the end of the pass
+        self._final = None   # frozen (key, DevLR, padded V, U, E) after the first trim
+        self.graph = None
+        self.launches = None
         self._wterms = []    # flop terms coef * w * r whose widths may be sketch-padded
         self._price = {}     # data_ptr of a final-product operand -> its U (re-priced at rank)
 
@@ -695,10 +698,7 @@ class LevelPass(NumericPass):
     def _run(self):
         part = self.sym.partition
         cfg = self.cfg
-        interiors = self.factor_interiors()
-        fail = self.first_interior_failure
-        if fail is not None:
-            self.pending.append((-1, 0, fail[0], fail[2], fail[1]))
+        interiors = self.factor_interiors(defer=True)
         by_unit = {}
         for u, iu in interiors.items():
             by_unit[u] = iu
@@ -777,17 +777,28 @@ class LevelPass(NumericPass):
 
     def _finalize_ranks(self, info):
         """Trim every compressed block to its kept rank (views; the padded columns are
-        exact zeros) and record the ranks -- the pass's single rank readback."""
+        exact zeros) and record the ranks -- the pass's single rank readback.  The
+        padded tensors and the width-dependent flop terms are kept, so a CUDA-graph
+        replay of the pass (new values, possibly new ranks) can trim again."""
+        if self._final is None:
+            self._final = [(key, lr, lr.V, lr.U, lr.E) for key, lr in self._deferred]
+            self._deferred = []
+            self._flops_padded = self.flops
+            self._wt = tuple(np.concatenate([t[i] for t in self._wterms]) for i in range(5)) \
+                if self._wterms else None
+            self._wterms = []
         kept = {}
-        for key, lr in self._deferred:
-            k = int(info[lr.kslot]) if lr.kslot is not None else lr.k
-            kept[lr.V.data_ptr()] = k
-            kept[lr.U.data_ptr()] = k
-            lr.V, lr.U, lr.E, lr.k = lr.V[:, :k], lr.U[:, :k], lr.E[:, :k], k
+        self.ranks = {}
+        for key, lr, V, U, Ef in self._final:
+            k = int(info[lr.kslot]) if lr.kslot is not None else V.shape[1]
+            kept[V.data_ptr()] = k
+            kept[U.data_ptr()] = k
+            lr.V, lr.U, lr.E, lr.k = V[:, :k], U[:, :k], Ef[:, :k], k
             self.ranks[key] = k
-        self._deferred = []
-        if self._wterms and kept:
-            coef, w, wb, r, rb = (np.concatenate([t[i] for t in self._wterms]) for i in range(5))
+        self.flops = self._flops_padded
+        if self._wt is not None and kept:
+            coef, w, wb, r, rb = self._wt
+
             def look(bases, width):
                 ub, inv = np.unique(bases, return_inverse=True)
                 kk = np.array([kept.get(int(b), -1) for b in ub], dtype=np.int64)[inv]
@@ -795,14 +806,11 @@ class LevelPass(NumericPass):
 
             wt, rt = look(wb, w), look(rb, r)
             self.flops -= float(np.sum(coef * (w * r - wt * rt)))
-        self._wterms = []
 
     def check_pivots(self):
         """One readback of the pass's device words (POTRF info + QR ranks): trim the
         compressed blocks, then resolve every recorded pivot failure (the earliest unit
         in sweep order wins)."""
-        if not self.pending and not self._deferred:
-            return
         info = self.ibuf[: self.ipos].cpu().numpy()
         self._finalize_ranks(info)
         worst = None
@@ -818,9 +826,36 @@ class LevelPass(NumericPass):
                 cand = (unit, int(v[bad[0]]) - 1, trees)
             if worst is None or cand[0] < worst[0]:
                 worst = cand
-        self.pending = []
         if worst is not None:
             raise _Indefinite(*worst)
+
+    # -- CUDA-graph refactorization ---------------------------------------------------
+    def capture(self):
+        """Record the whole sweep (no host synchronisation inside) as one CUDA graph.
+        Nothing executes until replay(); the Python structure of the factor (units,
+        blocks, arenas) is built once here and stays valid for every replay, which
+        rewrites the same device memory."""
+        import torch
+
+        from . import _lib
+
+        lib = _lib.load()
+        n0 = int(lib.rsc_launch_counter(0))
+        self.graph = torch.cuda.CUDAGraph()
+        prev = E.SCRATCH
+        E.SCRATCH = self.S
+        try:
+            with torch.cuda.graph(self.graph):
+                self._run()
+        finally:
+            E.SCRATCH = prev
+        self.launches = int(lib.rsc_launch_counter(0)) - n0
+
+    def replay(self):
+        """Run the recorded sweep on the current values of the plan's A blocks, then
+        the single readback (ranks + pivots)."""
+        self.graph.replay()
+        self.check_pivots()
 
 
 # ---------------------------------------------------------------------------

@@ -157,3 +157,49 @@ def test_refactorization_with_new_values(cuda):
     assert relerr(F2.apply(r), z1) > 1e-3  # the values really changed
     F1b = factorize(A1, prepared=prep)  # and back
     assert relerr(F1b.apply(r), z1) < 3e-8
+
+
+def test_graph_refactorization_replays(cuda):
+    """With a reused plan the sweep is captured once and replayed: dropping the previous
+    factor lets the next factorize replay the graph on new values; the result equals a
+    fresh (eager) factorization, and a factor that is still alive is never overwritten."""
+    import weakref
+
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.factor import SolverConfig, prepare
+    from paper_1507_05593_b200.problems import laplacian_3d
+    from paper_1507_05593_b200.sparse import SparseSpdMatrix
+
+    A1, coords = laplacian_3d(14)
+    cfg = SolverConfig(tau_o=32, oversample=10, alpha_o=1.0, alpha_d=0.5, tau_d=64, power_iters=1, seed=0)
+    rng = np.random.default_rng(5)
+    v = A1.values.copy()
+    off = np.ones(v.size, dtype=bool)
+    off[A1.col_ptr[:-1]] = False
+    v[off] *= 0.8
+    A2 = SparseSpdMatrix(A1.n, A1.col_ptr, A1.row_idx, v)
+    r = rng.standard_normal(A1.n)
+    ref1 = factorize(A1, cfg, coords=coords).apply(r)
+    ref2 = factorize(A2, cfg, coords=coords).apply(r)
+    prep = prepare(A1, cfg, coords)
+    plan = prep[1]
+    F0 = factorize(A1, prepared=prep)          # first pass at this alpha_d: eager
+    assert getattr(F0, "_entry", None) is None
+    del F0
+    F = factorize(A1, prepared=prep)           # capture + first replay
+    assert plan.graphs and F._entry is not None
+    assert relerr(F.apply(r), ref1) < 3e-8
+    keep = F                                    # alive: the next call must not replay over it
+    G = factorize(A2, prepared=prep)
+    assert getattr(G, "_entry", None) is None   # ordinary pass on fresh memory
+    assert relerr(keep.apply(r), ref1) < 3e-8
+    assert relerr(G.apply(r), ref2) < 3e-8
+    w = weakref.ref(F)
+    del F, keep, G
+    assert w() is None
+    H = factorize(A2, prepared=prep)           # replay on the new values
+    assert H._entry is not None
+    assert relerr(H.apply(r), ref2) < 3e-8
+    del H
+    K = factorize(A1, prepared=prep)           # and back
+    assert relerr(K.apply(r), ref1) < 3e-8
