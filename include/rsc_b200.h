@@ -148,6 +148,14 @@ int rsc_gemv_batched(int count, const double *const *M, const int *rows, const i
                      const int *ldm, const double *const *x, const int *const *xidx,
                      double *const *y, const int *const *yidx, int mode, double alpha,
                      void *stream);
+/* rsc_gemv_multi: the same products with a mode and alpha per problem, so one launch
+ * covers a whole phase of an apply level (diagonal solves with mode 6 next to
+ * couplings with mode 0, low-rank U^T w with mode 1, ...). */
+int rsc_gemv_multi(int count, const double *const *M, const int *rows, const int *cols,
+                   const int *ldm, const double *const *x, const int *const *xidx,
+                   double *const *y, const int *const *yidx, const int *modes,
+                   const double *alphas, void *stream);
+
 
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */
 int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,

@@ -41,6 +41,7 @@ EXPORTED = (
     "rsc_spmv_csr",
     "rsc_trsv_batched",
     "rsc_gemv_batched",
+    "rsc_gemv_multi",
     "rsc_gather_rows",
     "rsc_scatter_add_rows",
     "rsc_dot",
@@ -81,6 +82,8 @@ _SIGS = {
     "rsc_spmv_csr": (I, [I, P, P, P, P, P, P]),
     "rsc_trsv_batched": (I, [I, P, P, P, P, P, I, P]),
     "rsc_gemv_batched": (I, [I, P, P, P, P, P, P, P, P, I, D, P]),
+    "rsc_gemv_multi": (I, [I, P, P, P, P, P, P, P, P, P, P, P]),
+
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),
     "rsc_dot": (I, [I, P, P, P, P, P]),

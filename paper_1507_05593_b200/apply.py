@@ -9,12 +9,18 @@ dense branch, so every unit runs the same kernels.
 
 Level scheduling: a unit depends only on the units whose rows reach into its
 columns (its update sources), so units are grouped by height in that DAG.  Each
-level is a handful of launches of the HBM-streaming kernels of csrc/apply.cu:
-one batched TRSV over all dense diagonals of the level, one batched gather/scatter
-GEMV for all dense couplings, two for all low-rank couplings, and the diagonal
-trees of the level advanced in lock-step waves (Alg. 4 flattened).  All launch
-descriptors are static after factorization and built once; after a few eager
-applies the whole sweep is replayed from a CUDA graph.
+level is a few *phases* of the mixed-mode GEMV: the diagonal solves (explicit
+inverses, row-parallel), then the dense couplings together with the first factor of
+every low-rank coupling, then the second low-rank factor; diagonal trees of the
+level advance in lock-step waves (Alg. 4 flattened), two phases per wave.  Each
+phase is ONE launch of rsc_gemv_multi (mode and alpha per problem).  (A persistent
+single-launch executor with grid barriers between phases measured no faster: the
+phases are latency-bound, not launch-bound.)  Two vectors alternate roles instead of
+copying: in the forward sweep the right-hand sides accumulate in `y` and every
+solved block is written to `y2` (couplings read solved values from `y2`); the
+backward sweep starts from `y2` and writes `y`.  All low-rank intermediates live in
+one buffer zeroed once per apply.  Descriptors are static after factorization and
+built once; after a few eager applies the whole sweep is replayed from a CUDA graph.
 """
 
 import numpy as np
@@ -26,73 +32,17 @@ from ._lib import int_array, ptr_array
 from .factor import DenseTri, DeviceTree, DevLR
 
 
-class _Launch:
-    """One pre-built batched launch (host descriptor arrays kept alive)."""
 
-    def __init__(self, fn, arrays, scalars):
-        self.fn = fn
-        self.arrays = arrays
-        self.args = [a.ctypes.data if isinstance(a, np.ndarray) else a for a in arrays] + scalars
-
-    def __call__(self, stream):
-        _lib.check(self.fn(*self.args, stream), "apply launch")
-
-
-def _trsv(tris, xptrs, trans, y2p=None, yp=None):
-    """Diagonal solves of a level.  With the explicit inverses built at apply setup,
-    x = L^{-1} b is a row-parallel GEMV (warp per row, no dependency chain):
-    forward reads Linv (lower), backward reads LinvT = Linv^T (upper), both from the
-    snapshot y2 of y taken before the solves, writing y (assign)."""
-    if not tris:
-        return None
-    if y2p is not None:
-        M = [t.LinvT if trans else t.Linv for t in tris]
-        items = [(m.data_ptr(), t.n, t.n, E.ld(m), y2p + (xp - yp), 0, xp, 0) for m, t, xp in zip(M, tris, xptrs)]
-        return _gemv(items, 4 | (8 if trans else 2), 1.0)
-    lib = _lib.load()
-    arrs = [int(len(tris)), ptr_array([t.L.data_ptr() for t in tris]), int_array([t.n for t in tris]),
-            int_array([E.ld(t.L) for t in tris]), ptr_array([t.Dinv.data_ptr() for t in tris]), ptr_array(xptrs)]
-    return _Launch(lib.rsc_trsv_batched, arrs, [int(trans)])
-
-
-def _gemv(items, trans, alpha):
-    """items: (M ptr, rows, cols, ldm, x ptr, xidx ptr|0, y ptr, yidx ptr|0)."""
-    if not items:
-        return None
-    lib = _lib.load()
-    cols = list(zip(*items))
-    arrs = [int(len(items)), ptr_array(cols[0]), int_array(cols[1]), int_array(cols[2]), int_array(cols[3]),
-            ptr_array(cols[4]), ptr_array(cols[5]), ptr_array(cols[6]), ptr_array(cols[7])]
-    return _Launch(lib.rsc_gemv_batched, arrs, [int(trans), float(alpha)])
-
-
-class _Prog:
-    """Ordered list of launches and zero-fills (a static program)."""
+class _Phase:
+    """Problems of one phase of the apply program (no dependencies among them):
+    (M ptr, rows, cols, ldm, x ptr, xidx ptr|0, y ptr, yidx ptr|0, mode, alpha)."""
 
     def __init__(self):
-        self.steps = []
+        self.items = []
 
-    def launch(self, l):
-        if l is not None:
-            self.steps.append(l)
-
-    def zero(self, t):
-        if t is not None and t.numel():
-            self.steps.append(("zero", t))
-
-    def copy(self, dst, src):
-        self.steps.append(("copy", dst, src))
-
-    def run(self):
-        s = E.stream_handle()
-        for st in self.steps:
-            if isinstance(st, tuple):
-                if st[0] == "zero":
-                    st[1].zero_()
-                else:
-                    st[1].copy_(st[2])
-            else:
-                st(s)
+    def add(self, *item):
+        if item[1] > 0 and item[2] > 0:
+            self.items.append(item)
 
 
 class DeviceApply:
@@ -104,12 +54,20 @@ class DeviceApply:
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
         self.y = E.empty(self.n, 1)
-        self.y2 = E.empty(self.n, 1)  # snapshot of y read by the inverse-based diagonal solves
+        self.y2 = E.empty(self.n, 1)
         self.zbuf = E.empty(self.n)
         self.r_in = E.empty(self.n)
-        self.keep = []
         units = F.units
         self._build_inverses(units)
+        # every low-rank block is used once per sweep: 2 * sum(k) intermediates
+        ksum = 0
+        for u in units:
+            if isinstance(u.off, DevLR):
+                ksum += u.off.k
+            if isinstance(u.diag, DeviceTree):
+                ksum += sum(b.k for b in u.diag.blocks.values() if isinstance(b, DevLR))
+        self.tall = E.empty(max(2 * ksum, 1))
+        self._toff = 0
         uidx = {un.u: i for i, un in enumerate(units)}
         level = [0] * len(units)
         for i, un in enumerate(units):
@@ -121,13 +79,36 @@ class DeviceApply:
                 level[i] = lv
         nlev = max(level) + 1 if units else 0
         groups = [[units[i] for i in range(len(units)) if level[i] == lv] for lv in range(nlev)]
-        self.prog = _Prog()
+        self.phases = []
+        yb, y2b = self.y.data_ptr(), self.y2.data_ptr()
         for us in groups:
-            self._forward_level(us, plan)
+            self._level(us, plan, yb, y2b, backward=False)
         for us in reversed(groups):
-            self._backward_level(us, plan)
+            self._level(us, plan, y2b, yb, backward=True)
+        self._pack()
         self.graph = None
         self.calls = 0
+
+    def _emit(self, ph):
+        if ph.items:
+            self.phases.append(ph)
+
+    def _pack(self):
+        """Every phase -> one prebuilt rsc_gemv_multi launch (host arrays kept)."""
+        lib = _lib.load()
+        self.launches = []
+        for ph in self.phases:
+            c = list(zip(*ph.items))
+            arrs = [ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3]), ptr_array(c[4]),
+                    ptr_array(c[5]), ptr_array(c[6]), ptr_array(c[7]), int_array(c[8]),
+                    np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))]
+            self.launches.append((len(ph.items), arrs, [a.ctypes.data for a in arrs]))
+        self._fn = lib.rsc_gemv_multi
+
+    def _run_program(self):
+        s = E.stream_handle()
+        for n, _, args in self.launches:
+            _lib.check(self._fn(n, *args, s), "rsc_gemv_multi")
 
     # -- program construction ------------------------------------------------------
     def _build_inverses(self, units):
@@ -168,124 +149,106 @@ class DeviceApply:
         key = ("int", un.u) if un.kind == "interior" else un.j
         return plan.idx.ptr(plan.rows_off[key])
 
-    def _tbuf(self, sizes):
-        """One zero-initialised buffer carved into per-problem t vectors."""
-        tot = sum(sizes)
-        if tot == 0:
-            return None, []
-        t = E.empty(tot)
-        self.keep.append(t)
-        offs = np.concatenate([[0], np.cumsum(sizes)[:-1]])
-        return t, [t.data_ptr() + 8 * int(o) for o in offs]
+    def _t(self, k):
+        p = self.tall.data_ptr() + 8 * self._toff
+        self._toff += k
+        return p
 
-    def _tree_waves(self, trees, trans):
-        """Alg. 4 of every tree in `trees` on its slice of y, in lock-step waves."""
+    @staticmethod
+    def _solve(ph, tri, xp, yp, backward):
+        """out = L^{-1} rhs (forward, Linv lower) or L^{-T} rhs (backward, LinvT upper)."""
+        M = tri.LinvT if backward else tri.Linv
+        ph.add(M.data_ptr(), tri.n, tri.n, E.ld(M), xp, 0, yp, 0, 12 if backward else 6, 1.0)
+
+    def _level(self, us, plan, rhs, out, backward):
+        """One level of a sweep; right-hand sides accumulate in `rhs`, solved blocks are
+        written to `out` (base addresses of y / y2)."""
+        dense = [u for u in us if isinstance(u.diag, DenseTri)]
+        trees = [u for u in us if isinstance(u.diag, DeviceTree)]
+        cpl = [u for u in us if u.rows.size and u.off is not None and
+               (not isinstance(u.off, DevLR) or u.off.k)]
+        if not backward:
+            first = _Phase()
+            for u in dense:
+                self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, False)
+            first = self._tree_waves(trees, rhs, out, False, first)
+            self._emit(first)
+            self._couplings(cpl, plan, rhs, out, False)
+        else:
+            self._couplings(cpl, plan, rhs, out, True)
+            first = _Phase()
+            for u in dense:
+                self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, True)
+            first = self._tree_waves(trees, rhs, out, True, first)
+            self._emit(first)
+
+    def _couplings(self, cpl, plan, rhs, out, backward):
+        a, b = _Phase(), _Phase()
+        for u in cpl:
+            rows = self._rows_ptr(plan, u)
+            c0 = 8 * u.c0
+            if isinstance(u.off, DevLR):
+                k, t = u.off.k, self._t(u.off.k)
+                U, V = u.off.U, u.off.V
+                if not backward:  # t = U^T w ; y[R] -= V t
+                    a.add(U.data_ptr(), u.ncols, k, E.ld(U), out + c0, 0, t, 0, 1, 1.0)
+                    b.add(V.data_ptr(), u.rows.size, k, E.ld(V), t, 0, rhs, rows, 0, -1.0)
+                else:  # t = V^T y[R] ; w -= U t
+                    a.add(V.data_ptr(), u.rows.size, k, E.ld(V), out, rows, t, 0, 1, 1.0)
+                    b.add(U.data_ptr(), u.ncols, k, E.ld(U), t, 0, rhs + c0, 0, 0, -1.0)
+            elif not backward:  # y[R] -= L_O w
+                a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out + c0, 0, rhs, rows, 0, -1.0)
+            else:  # w -= L_O^T y[R]
+                a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out, rows, rhs + c0, 0, 1, -1.0)
+        self._emit(a)
+        self._emit(b)
+
+    def _tree_waves(self, trees, rhs, out, backward, first):
+        """Alg. 4 of every tree in `trees`, in lock-step waves; wave w's leaf solves,
+        dense couplings and first low-rank factors share one launch, the second
+        low-rank factors a second one.  `first` (the level's own first phase) is
+        merged into wave 0; returns the phase still to be launched."""
         from .numeric import tree_ops
 
-        yp = self.y.data_ptr()
-        seqs = [tree_ops(u.diag, None, self.y[u.c0:u.c1], trans) for u in trees]
+        ybase = self.y.data_ptr()
+        off = lambda v: v.data_ptr() - ybase  # tree_ops hands out views of self.y
+        seqs = [tree_ops(u.diag, None, self.y[u.c0:u.c1], backward) for u in trees]
         seqs = [s for s in seqs if s]
         if not seqs:
-            return
+            return first
+        cur = first
         for w in range(max(len(s) for s in seqs)):
-            leaves, dense, lr = [], [], []
+            second = _Phase()
             for s in seqs:
                 if w >= len(s):
                     continue
                 op = s[w]
                 if op[0] == "leaf":
                     if op[1].n:
-                        leaves.append((op[1], op[2].data_ptr()))
+                        self._solve(cur, op[1], rhs + off(op[2]), out + off(op[2]), backward)
                     continue
                 _, b, Xs, Yd, tr = op
+                xp, yp = out + off(Xs), rhs + off(Yd)
                 if isinstance(b, DevLR):
-                    if b.k:
-                        lr.append((b, Xs, Yd, tr))
-                else:
-                    dense.append((b, Xs, Yd, tr))
-            if leaves:
-                self.prog.copy(self.y2, self.y)
-            self.prog.launch(_trsv([t for t, _ in leaves], [p for _, p in leaves], trans, self.y2.data_ptr(), yp))
-            # dense coupling: Y -= B X (forward) or Y -= B^T X (transposed)
-            self.prog.launch(_gemv([(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), Xs.data_ptr(), 0, Yd.data_ptr(), 0)
-                                    for b, Xs, Yd, tr in dense], trans, -1.0))
-            if lr:
-                t, tp = self._tbuf([b.k for b, _, _, _ in lr])
-                self.prog.zero(t)
-                # t = U^T X (forward) or V^T X (transposed)
-                first = [((b.V if tr else b.U), Xs, p) for (b, Xs, Yd, tr), p in zip(lr, tp)]
-                self.prog.launch(_gemv([(P.data_ptr(), P.shape[0], P.shape[1], E.ld(P), Xs.data_ptr(), 0, p, 0)
-                                        for P, Xs, p in first], 1, 1.0))
-                # Y -= V t (forward) or U t (transposed)
-                second = [((b.U if tr else b.V), Yd, p) for (b, Xs, Yd, tr), p in zip(lr, tp)]
-                self.prog.launch(_gemv([(P.data_ptr(), P.shape[0], P.shape[1], E.ld(P), p, 0, Yd.data_ptr(), 0)
-                                        for P, Yd, p in second], 0, -1.0))
-
-    def _forward_level(self, us, plan):
-        yp = self.y.data_ptr()
-        dense = [u for u in us if isinstance(u.diag, DenseTri)]
-        trees = [u for u in us if isinstance(u.diag, DeviceTree)]
-        if dense:
-            self.prog.copy(self.y2, self.y)
-        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 0, self.y2.data_ptr(), yp))
-        if trees:
-            self._tree_waves(trees, False)
-        dn, lr = [], []
-        for u in us:
-            if not u.rows.size or u.off is None:
-                continue
-            if isinstance(u.off, DevLR):
-                if u.off.k:
-                    lr.append(u)
-            else:
-                dn.append(u)
-        # y[R] -= L_O w
-        self.prog.launch(_gemv([(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), yp + 8 * u.c0, 0, yp,
-                                 self._rows_ptr(plan, u)) for u in dn], 0, -1.0))
-        if lr:
-            t, tp = self._tbuf([u.off.k for u in lr])
-            self.prog.zero(t)
-            # t = U^T w ; y[R] -= V t
-            self.prog.launch(_gemv([(u.off.U.data_ptr(), u.ncols, u.off.k, E.ld(u.off.U), yp + 8 * u.c0, 0, p, 0)
-                                    for u, p in zip(lr, tp)], 1, 1.0))
-            self.prog.launch(_gemv([(u.off.V.data_ptr(), u.rows.size, u.off.k, E.ld(u.off.V), p, 0, yp,
-                                     self._rows_ptr(plan, u)) for u, p in zip(lr, tp)], 0, -1.0))
-
-    def _backward_level(self, us, plan):
-        yp = self.y.data_ptr()
-        dn, lr = [], []
-        for u in us:
-            if not u.rows.size or u.off is None:
-                continue
-            if isinstance(u.off, DevLR):
-                if u.off.k:
-                    lr.append(u)
-            else:
-                dn.append(u)
-        # w -= L_O^T y[R]
-        self.prog.launch(_gemv([(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), yp, self._rows_ptr(plan, u),
-                                 yp + 8 * u.c0, 0) for u in dn], 1, -1.0))
-        if lr:
-            t, tp = self._tbuf([u.off.k for u in lr])
-            self.prog.zero(t)
-            # t = V^T y[R] ; w -= U t
-            self.prog.launch(_gemv([(u.off.V.data_ptr(), u.rows.size, u.off.k, E.ld(u.off.V), yp,
-                                     self._rows_ptr(plan, u), p, 0) for u, p in zip(lr, tp)], 1, 1.0))
-            self.prog.launch(_gemv([(u.off.U.data_ptr(), u.ncols, u.off.k, E.ld(u.off.U), p, 0, yp + 8 * u.c0, 0)
-                                    for u, p in zip(lr, tp)], 0, -1.0))
-        trees = [u for u in us if isinstance(u.diag, DeviceTree)]
-        if trees:
-            self._tree_waves(trees, True)
-        dense = [u for u in us if isinstance(u.diag, DenseTri)]
-        if dense:
-            self.prog.copy(self.y2, self.y)
-        self.prog.launch(_trsv([u.diag for u in dense], [yp + 8 * u.c0 for u in dense], 1, self.y2.data_ptr(), yp))
+                    if not b.k:
+                        continue
+                    t = self._t(b.k)
+                    P1, P2 = (b.V, b.U) if tr else (b.U, b.V)
+                    cur.add(P1.data_ptr(), P1.shape[0], b.k, E.ld(P1), xp, 0, t, 0, 1, 1.0)
+                    second.add(P2.data_ptr(), P2.shape[0], b.k, E.ld(P2), t, 0, yp, 0, 0, -1.0)
+                else:  # Y -= B X (forward) or Y -= B^T X (transposed)
+                    cur.add(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), xp, 0, yp, 0, 1 if tr else 0, -1.0)
+            self._emit(cur)
+            self._emit(second)
+            cur = _Phase()
+        return cur
 
     # -- execution ---------------------------------------------------------------
     def _body(self):
         n = self.n
+        self.tall.zero_()
         E.gather_rows(self.inv, self.r_in.reshape(n, 1), self.y)
-        self.prog.run()
+        self._run_program()
         E.gather_rows(self.fwd, self.y, self.zbuf.reshape(n, 1))
 
     # eager applies before the sweep is captured into a CUDA graph (capture costs

@@ -94,102 +94,187 @@ __global__ void __launch_bounds__(T) trsv_kernel(const __grid_constant__ TrsvArg
     for (int i = t; i < n; i += T) x[i] = xs[i];
 }
 
-struct GemvArgs {
-    int count;
-    long long blk_begin[MAXP + 1];
-    const double *M[MAXP];
-    const double *x[MAXP];
-    double *y[MAXP];
-    const int *xidx[MAXP];
-    const int *yidx[MAXP];
-    int rows[MAXP], cols[MAXP], ldm[MAXP];
+// One launch can mix problems of different modes and scales (a whole phase of a
+// level of the apply): mode and alpha are per problem.
+//
+// mode bit 0: transpose; bit 1: M is lower triangular (read c <= r only);
+// bit 2: assign instead of atomic accumulate (transpose 0 only: one segment owns a
+// row); bit 3: M is upper triangular (transpose 0 only: read c >= r only).
+//
+// transpose 0: a row is owned by a segment of `lpr` lanes (8 / 16 / 32 by width), so
+//   narrow panels (the low-rank factors, k ~ 20-60 columns) still keep every lane
+//   busy; each lane keeps four independent loads in flight.
+// transpose 1: a CTA owns a 64-row slab x up to 256 columns; columns narrower than
+//   the CTA are covered by several row subgroups whose partial sums meet in shared
+//   memory before one atomic per column.
+constexpr int GMAXP = 224;
+constexpr int SLAB = 64;     // rows per CTA, transpose 1
+constexpr int CTILE = 256;   // columns per CTA, transpose 1
+
+struct GemvProb {
+    const double *M;
+    const double *x;
+    double *y;
+    const int *xidx;
+    const int *yidx;
     double alpha;
+    long long blk_begin;        // first block of this problem (within its launch / phase)
+    int rows, cols, ld;
+    int mode, lpr;              // lanes per row (transpose 0) / column tile width (transpose 1)
 };
 
-constexpr int ROWS_T0 = 16;  // transpose 0: 8 warps x 2 rows per CTA
-constexpr int ROWS_T1 = 64;  // transpose 1: 64-row slab, thread per column
+struct GemvArgs {
+    int count;
+    long long total;
+    GemvProb p[GMAXP];
+};
 
 __device__ __forceinline__ double ldnc(const double *p) { return __ldg(p); }
 
-// mode bit 0: transpose; bit 1: M is lower triangular (read c <= r only);
-// bit 2: assign instead of atomic accumulate (transpose 0 only: one warp owns a row);
-// bit 3: M is upper triangular (transpose 0 only: read c >= r only).
-// Inner loops are unrolled 4x so each lane keeps four independent 8-byte loads in
-// flight (the kernel is latency-bound otherwise).
-__global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a, int mode) {
+// one CTA-block of work of problem d (block index lb within the problem)
+__device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, double *xr, double *part) {
+    const int mode = d.mode;
     const bool trans = mode & 1, lower = mode & 2, assign = mode & 4, upper = mode & 8;
-    __shared__ double xr[ROWS_T1];
-    int lo = 0, hi = a.count - 1;
-    const long long blk = blockIdx.x;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (a.blk_begin[mid] <= blk) lo = mid; else hi = mid - 1;
-    }
-    const int p = lo;
-    const int rows = a.rows[p], cols = a.cols[p], ld = a.ldm[p];
-    const double *M = a.M[p];
-    const double *x = a.x[p];
-    double *y = a.y[p];
-    const int *xi = a.xidx[p];
-    const int *yi = a.yidx[p];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int rows = d.rows, cols = d.cols, ld = d.ld;
+    const double alpha = d.alpha;
+    const double *M = d.M;
+    const double *x = d.x;
+    double *y = d.y;
+    const int *xi = d.xidx;
+    const int *yi = d.yidx;
+    const int t = threadIdx.x;
     if (!trans) {
-        const int r0 = (int)(blk - a.blk_begin[p]) * ROWS_T0;
-        const int r1 = min(rows, r0 + ROWS_T0);
-        for (int r = r0 + w; r < r1; r += 8) {
+        const int lpr = d.lpr;                    // 8, 16 or 32
+        const int seg = t / lpr, sub = t % lpr;   // T / lpr segments per CTA
+        const int nseg = T / lpr;
+        const int r = (int)lb * nseg + seg;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (r < rows) {
             const double *Mr = M + (long long)r * ld;
             const int cend = lower ? min(cols, r + 1) : cols;
-            int c = (upper ? r : 0) + lane;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int c = (upper ? r : 0) + sub;
+            const int step = 4 * lpr;
             if (xi) {
-                for (; c + 96 < cend; c += 128) {
-                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + 32), m2 = ldnc(Mr + c + 64),
-                                 m3 = ldnc(Mr + c + 96);
-                    s0 += m0 * x[xi[c]];
-                    s1 += m1 * x[xi[c + 32]];
-                    s2 += m2 * x[xi[c + 64]];
-                    s3 += m3 * x[xi[c + 96]];
+                for (; c + 3 * lpr < cend; c += step) {
+                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + lpr), m2 = ldnc(Mr + c + 2 * lpr),
+                                 m3 = ldnc(Mr + c + 3 * lpr);
+                    s0 += m0 * x[__ldg(xi + c)];
+                    s1 += m1 * x[__ldg(xi + c + lpr)];
+                    s2 += m2 * x[__ldg(xi + c + 2 * lpr)];
+                    s3 += m3 * x[__ldg(xi + c + 3 * lpr)];
                 }
-                for (; c < cend; c += 32) s0 += ldnc(Mr + c) * x[xi[c]];
+                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * x[__ldg(xi + c)];
             } else {
-                for (; c + 96 < cend; c += 128) {
-                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + 32), m2 = ldnc(Mr + c + 64),
-                                 m3 = ldnc(Mr + c + 96);
+                for (; c + 3 * lpr < cend; c += step) {
+                    const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + lpr), m2 = ldnc(Mr + c + 2 * lpr),
+                                 m3 = ldnc(Mr + c + 3 * lpr);
                     s0 += m0 * x[c];
-                    s1 += m1 * x[c + 32];
-                    s2 += m2 * x[c + 64];
-                    s3 += m3 * x[c + 96];
+                    s1 += m1 * x[c + lpr];
+                    s2 += m2 * x[c + 2 * lpr];
+                    s3 += m3 * x[c + 3 * lpr];
                 }
-                for (; c < cend; c += 32) s0 += ldnc(Mr + c) * x[c];
+                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * x[c];
             }
-            const double s = warp_sum((s0 + s1) + (s2 + s3));
-            if (lane == 0) {
-                double *dst = y + (yi ? yi[r] : r);
-                if (assign) *dst = a.alpha * s;
-                else atomicAdd(dst, a.alpha * s);
-            }
+        }
+        double s = (s0 + s1) + (s2 + s3);
+        for (int o = lpr >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (r < rows && sub == 0) {
+            double *dst = y + (yi ? __ldg(yi + r) : r);
+            if (assign) *dst = alpha * s;
+            else atomicAdd(dst, alpha * s);
         }
     } else {
-        const int r0 = (int)(blk - a.blk_begin[p]) * ROWS_T1;
-        const int r1 = min(rows, r0 + ROWS_T1);
-        for (int r = r0 + t; r < r1; r += T) xr[r - r0] = xi ? x[xi[r]] : x[r];
+        const int cw = d.lpr;                     // column tile width: 32 .. 256 (power of 2)
+        const int ntile = (cols + CTILE - 1) / CTILE;
+        const int slab = (int)(lb / ntile), tile = (int)(lb % ntile);
+        const int r0 = slab * SLAB, r1 = min(rows, r0 + SLAB);
+        for (int r = r0 + t; r < r1; r += T) xr[r - r0] = x[xi ? __ldg(xi + r) : r];
         __syncthreads();
-        for (int c = t; c < cols; c += T) {
-            int r = lower ? max(r0, c) : r0;
-            if (r >= r1) continue;
+        const int nsub = T / cw;                  // row subgroups
+        const int sub = t / cw, c = tile * CTILE + (t % cw);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (c < cols) {
+            int r = r0 + sub;
+            if (lower && r < c) r += ((c - r + nsub - 1) / nsub) * nsub;  // rows >= c only
             const double *Mc = M + (long long)r * ld + c;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            for (; r + 3 < r1; r += 4, Mc += 4LL * ld) {
-                const double m0 = ldnc(Mc), m1 = ldnc(Mc + ld), m2 = ldnc(Mc + 2LL * ld), m3 = ldnc(Mc + 3LL * ld);
+            const long long st = (long long)nsub * ld;
+            for (; r + 3 * nsub < r1; r += 4 * nsub, Mc += 4 * st) {
+                const double m0 = ldnc(Mc), m1 = ldnc(Mc + st), m2 = ldnc(Mc + 2 * st), m3 = ldnc(Mc + 3 * st);
                 s0 += m0 * xr[r - r0];
-                s1 += m1 * xr[r + 1 - r0];
-                s2 += m2 * xr[r + 2 - r0];
-                s3 += m3 * xr[r + 3 - r0];
+                s1 += m1 * xr[r + nsub - r0];
+                s2 += m2 * xr[r + 2 * nsub - r0];
+                s3 += m3 * xr[r + 3 * nsub - r0];
             }
-            for (; r < r1; ++r, Mc += ld) s0 += ldnc(Mc) * xr[r - r0];
-            atomicAdd(y + (yi ? yi[c] : c), a.alpha * ((s0 + s1) + (s2 + s3)));
+            for (; r < r1; r += nsub, Mc += st) s0 += ldnc(Mc) * xr[r - r0];
+        }
+        part[t] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (sub == 0 && c < cols) {
+            double s = part[t];
+            for (int q = 1; q < nsub; ++q) s += part[t + q * cw];
+            atomicAdd(y + (yi ? __ldg(yi + c) : c), alpha * s);
         }
     }
+}
+
+__device__ __forceinline__ int find_prob(const GemvProb *p, int lo, int hi, long long blk) {
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p[mid].blk_begin <= blk) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a) {
+    __shared__ double xr[SLAB];
+    __shared__ double part[T];
+    const long long blk = blockIdx.x;
+    const int p = find_prob(a.p, 0, a.count - 1, blk);
+    gemv_block(a.p[p], blk - a.p[p].blk_begin, xr, part);
+}
+
+inline int pow2ceil(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// problem descriptor + its block count
+inline long long describe(GemvProb &d, const double *M, int rows, int cols, int ld, const double *x, const int *xi,
+                          double *y, const int *yi, int mode, double alpha) {
+    d.M = M; d.x = x; d.y = y; d.xidx = xi; d.yidx = yi;
+    d.rows = rows; d.cols = cols; d.ld = ld; d.mode = mode; d.alpha = alpha;
+    if (mode & 1) {
+        d.lpr = cols >= CTILE ? CTILE : (pow2ceil(cols) < 32 ? 32 : pow2ceil(cols));
+        return (long long)((rows + SLAB - 1) / SLAB) * ((cols + CTILE - 1) / CTILE);
+    }
+    d.lpr = cols <= 64 ? 8 : (cols <= 256 ? 16 : 32);  // (lpr 32 from 65 columns measured slower)
+    const int nseg = T / d.lpr;
+    return (rows + nseg - 1) / nseg;
+}
+
+int gemv_launch(int count, const double *const *M, const int *rows, const int *cols, const int *ldm,
+                const double *const *x, const int *const *xidx, double *const *y, const int *const *yidx,
+                const int *modes, int mode_all, const double *alphas, double alpha_all, cudaStream_t s) {
+    static thread_local GemvArgs a;
+    int i = 0;
+    while (i < count) {
+        a.count = 0;
+        long long blocks = 0;
+        while (i < count && a.count < GMAXP) {
+            if (rows[i] <= 0 || cols[i] <= 0) { ++i; continue; }
+            GemvProb &d = a.p[a.count++];
+            d.blk_begin = blocks;
+            blocks += describe(d, M[i], rows[i], cols[i], ldm[i], x[i], xidx ? xidx[i] : nullptr, y[i],
+                               yidx ? yidx[i] : nullptr, modes ? modes[i] : mode_all, alphas ? alphas[i] : alpha_all);
+            ++i;
+        }
+        if (a.count == 0) continue;
+        a.total = blocks;
+        gemv_kernel<<<(unsigned)blocks, T, 0, s>>>(a);
+        RSC_CHECK_LAUNCH();
+    }
+    return 0;
 }
 
 }  // namespace
@@ -229,29 +314,17 @@ extern "C" int rsc_gemv_batched(int count, const double *const *M, const int *ro
     if (count < 0) return -1;
     if (count == 0) return 0;
     if (!M || !rows || !cols || !ldm || !x || !y) return -2;
-    static thread_local GemvArgs a;
-    int i = 0;
-    while (i < count) {
-        a.count = 0;
-        a.alpha = alpha;
-        long long blocks = 0;
-        while (i < count && a.count < MAXP) {
-            const int c = a.count;
-            if (rows[i] <= 0 || cols[i] <= 0) { ++i; continue; }
-            a.M[c] = M[i]; a.x[c] = x[i]; a.y[c] = y[i];
-            a.xidx[c] = xidx ? xidx[i] : nullptr;
-            a.yidx[c] = yidx ? yidx[i] : nullptr;
-            a.rows[c] = rows[i]; a.cols[c] = cols[i]; a.ldm[c] = ldm[i];
-            a.blk_begin[c] = blocks;
-            const int rpc = (mode & 1) ? ROWS_T1 : ROWS_T0;
-            blocks += (rows[i] + rpc - 1) / rpc;
-            ++a.count;
-            ++i;
-        }
-        if (a.count == 0) continue;
-        a.blk_begin[a.count] = blocks;
-        gemv_kernel<<<(unsigned)blocks, T, 0, (cudaStream_t)stream>>>(a, mode);
-        RSC_CHECK_LAUNCH();
-    }
-    return 0;
+    return gemv_launch(count, M, rows, cols, ldm, x, xidx, y, yidx, nullptr, mode, nullptr, alpha,
+                       (cudaStream_t)stream);
 }
+
+extern "C" int rsc_gemv_multi(int count, const double *const *M, const int *rows, const int *cols,
+                              const int *ldm, const double *const *x, const int *const *xidx,
+                              double *const *y, const int *const *yidx, const int *modes,
+                              const double *alphas, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!M || !rows || !cols || !ldm || !x || !y || !modes || !alphas) return -2;
+    return gemv_launch(count, M, rows, cols, ldm, x, xidx, y, yidx, modes, 0, alphas, 0.0, (cudaStream_t)stream);
+}
+

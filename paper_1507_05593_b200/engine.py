@@ -225,6 +225,34 @@ def gemm_grouped(probs, transA=False, transB=False):
         prof.records.append((s, e, fl, TAG))
 
 
+def split_k(p, transA, transB, ks):
+    """Cut every problem's K into slabs of at most `ks`, accumulated with FP64 atomics
+    into C: tall-K products (few output tiles, long K) then spread over many CTAs.
+    Problems that get split must have C zeroed by the caller (their beta is dropped:
+    every slab adds).  Handles the b_rows gather (the index pointer advances)."""
+    K = p["K"].astype(np.int64)
+    nsl = np.maximum(1, -(-K // ks))
+    if (nsl == 1).all():
+        return p
+    idx = np.repeat(np.arange(p.size), nsl)
+    q = p[idx].copy()
+    first = np.repeat(np.cumsum(nsl) - nsl, nsl)
+    k0 = ((np.arange(q.size) - first) * ks).astype(np.int64)
+    q["K"] = np.minimum(ks, K[idx] - k0)
+    k0u = k0.astype(np.uint64)
+    q["A"] = q["A"] + (k0u * q["lda"].astype(np.uint64) * np.uint64(8) if transA else k0u * np.uint64(8))
+    if transB:
+        q["B"] = q["B"] + k0u * np.uint64(8)
+    else:
+        rows = q["b_rows"] != 0
+        q["B"] = np.where(rows, q["B"], q["B"] + k0u * q["ldb"].astype(np.uint64) * np.uint64(8))
+        q["b_rows"] = np.where(rows, q["b_rows"] + k0u * np.uint64(4), q["b_rows"])
+    split = nsl[idx] > 1
+    q["atomic"] = np.where(split, 1, q["atomic"])
+    q["beta"] = np.where(split, 1.0, q["beta"])
+    return q
+
+
 def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
     """C = alpha op(A) op(B) + beta C for 2-D tensors (views allowed)."""
     M = A.shape[1] if transA else A.shape[0]

@@ -43,6 +43,8 @@ from .factor import (
 )
 from .symbolic import block_rank
 
+KSPLIT = 256  # K slab of the tall-K source products T = V^T G (see engine.split_k)
+
 
 # ---------------------------------------------------------------------------
 # lock-step batched Alg. 4
@@ -436,7 +438,7 @@ class LevelPass(NumericPass):
         w, ld = self.s_w[s], self.s_ld[s]
         tsz = w * r
         toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
-        T = self.S.empty(int(tsz.sum()))
+        T = self.S.zeros(int(tsz.sum()))  # p1 is split along its tall K (atomic slabs)
         tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
         raw_lo = self.s_raw[s] + (8 * lo * ld).astype(np.uint64)
         eff_hi = self.s_eff[s] + (8 * hi * ld).astype(np.uint64)
@@ -453,7 +455,7 @@ class LevelPass(NumericPass):
         else:  # T = E[hi:]^T G[rpos] ; W[cpos] -= V[lo:hi] T
             p1["A"], p1["K"], p1["b_rows"] = eff_hi, nro, rpos
             p2["A"], p2["M"], p2["c_rows"] = raw_lo, nrd, cpos
-        E.gemm_grouped(p1, True, False)
+        E.gemm_grouped(E.split_k(p1, True, False, KSPLIT), True, False)
         E.gemm_grouped(p2, False, False)
         self._wflops(2.0 * (nrd + nro), w=w, wbase=self.s_raw[s], r=r, rbase=rep(6).astype(np.uint64))
 
@@ -603,7 +605,7 @@ class LevelPass(NumericPass):
                 continue
             tsz = w * r
             toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
-            T = self.S.empty(int(tsz.sum()))
+            T = self.S.zeros(int(tsz.sum()))  # p1 is split along its tall K (atomic slabs)
             tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
             p1 = np.zeros(n, dtype=GEMM_DTYPE)
             p2 = np.zeros(n, dtype=GEMM_DTYPE)
@@ -624,7 +626,7 @@ class LevelPass(NumericPass):
             P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
             P1["batch"], P1["alpha"] = 1, 1.0
             P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
-            E.gemm_grouped(P1, True, False)
+            E.gemm_grouped(E.split_k(P1, True, False, KSPLIT), True, False)
             E.gemm_grouped(P2, False, False)
         if transpose:
             sol2 = []
