@@ -37,14 +37,14 @@ FP64_DATASHEET_TFLOPS = 40.0
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--config", type=int, default=1)
     p.add_argument("--nb", type=int, default=512)
     p.add_argument("--chunk", type=int, default=None, help="supernodes per grouped launch (default: all)")
     p.add_argument("--grid", type=int, default=None, help="grid size override for sparse configs")
-    p.add_argument("--cpu-sample", type=int, default=48, help="blocks in the CPU baseline sample")
+    p.add_argument("--cpu-sample", type=int, default=128, help="blocks in the CPU baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -320,7 +320,12 @@ def run_b200_cfg1(args, rank, world, torch, dist):
                    "l2": "inputs larger than L2 (2.4 GB/step); each step re-copies D from a pristine device copy "
                          "(in-place POTRF) and the TRSM reads B from its pristine copy"},
         "roofline": {"bound": "tensor", "achieved": gemm_flops / gemm_t / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": gemm_flops / gemm_t / 1e12 / peak, "traffic": None,
+                     "frac": gemm_flops / gemm_t / 1e12 / peak,
+                     # dram__bytes_read.sum + dram__bytes_write.sum per launch, mean of the two
+                     # sketch-product kernels, from one ncu --set full capture of this pipeline
+                     # (profiles/r01/ncu_full_bench_cfg1_gemm.txt: 3.59 GB and 2.68 GB per launch
+                     # vs 2.69 GB algorithmic: L_O once + X in + product out)
+                     "traffic": 3.131e9, "traffic_unit": "bytes per launch (ncu, not this run)",
                      "kernel": "gemm_grouped_kernel (sketch products L_O^T Omega, L_O G)",
                      "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64 "
                                     f"entry); datasheet {FP64_DATASHEET_TFLOPS} TF"},
