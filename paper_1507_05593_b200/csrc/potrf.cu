@@ -213,6 +213,9 @@ extern "C" int rsc_potrf_batched(int count, double *const *A, const int *n, cons
 int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const int *ldl,
                          const double *const *Dinv, const double *const *Bsrc, double *const *B,
                          const int *m, const int *ldb, cudaStream_t s);
+int rsc_trsm_left_fused(int trans, int count, const double *const *L, const int *n, const int *ldl,
+                        const double *const *Dinv, double *const *B, const int *m, const int *ldb,
+                        cudaStream_t s);
 
 extern "C" int rsc_trsm_right_batched(int count, const double *const *L, const int *n, const int *ldl,
                                       const double *const *Dinv, const double *const *Bsrc,
@@ -233,8 +236,11 @@ extern "C" int rsc_trsm_batched(int side, int trans, int count, const double *co
     if (count < 0) return -3;
     if (count == 0) return 0;
     if (!L || !n || !ldl || !Dinv || !B || !m || !ldb) return -4;
-    if (side == 1) {  // fused strip-resident kernel when every panel has n <= 320
+    if (side == 1) {  // fused strip-resident kernels when every triangle has n <= 320
         const int rc = rsc_trsm_right_fused(count, L, n, ldl, Dinv, nullptr, B, m, ldb, (cudaStream_t)stream);
+        if (rc != -1000) return rc;
+    } else {
+        const int rc = rsc_trsm_left_fused(trans, count, L, n, ldl, Dinv, B, m, ldb, (cudaStream_t)stream);
         if (rc != -1000) return rc;
     }
     int maxn = 0;

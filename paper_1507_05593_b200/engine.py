@@ -253,6 +253,28 @@ def split_k(p, transA, transB, ks):
     return q
 
 
+GEMM_CONCURRENT_CTAS = 148 * 5  # resident 64x64 GEMM CTAs on a B200 (5 per SM)
+
+
+def balance_k(p, transA, transB, ctas=GEMM_CONCURRENT_CTAS):
+    """Split the K of problems whose single-tile k-loop would outlast the launch.
+
+    A grouped launch finishes with its longest CTA.  In the sparse sweep one launch
+    mixes tall-K products with many small ones (the longest CTA bound was 2.6x the
+    balanced time on config[2]), so every problem that accumulates (atomic, or
+    beta = 1) and whose K exceeds ~1.5x the balanced per-CTA share is cut into K
+    slabs of that share, accumulated with FP64 atomics (split_k)."""
+    if p.size == 0:
+        return p
+    tiles = np.ceil(p["M"] / 64.0) * np.ceil(p["N"] / 64.0) * p["batch"]
+    ks = np.ceil(p["K"] / 16.0)
+    target = max(8, int(np.ceil(float((tiles * ks).sum()) / ctas)))
+    need = ((p["atomic"] == 1) | (p["beta"] == 1.0)) & (ks > 1.5 * target)
+    if not need.any():
+        return p
+    return np.concatenate([p[~need], split_k(p[need], transA, transB, 16 * target)])
+
+
 def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
     """C = alpha op(A) op(B) + beta C for 2-D tensors (views allowed)."""
     M = A.shape[1] if transA else A.shape[0]

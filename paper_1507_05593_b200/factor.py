@@ -225,7 +225,7 @@ class Grouped:
 
     def launch(self):
         if self.rows:
-            E.gemm_grouped(np.array(self.rows, dtype=GEMM_DTYPE), self.tA, self.tB)
+            E.gemm_grouped(E.balance_k(np.array(self.rows, dtype=GEMM_DTYPE), self.tA, self.tB), self.tA, self.tB)
             self.rows = []
 
 

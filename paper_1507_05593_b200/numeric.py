@@ -43,7 +43,6 @@ from .factor import (
 )
 from .symbolic import block_rank
 
-KSPLIT = 256  # K slab of the tall-K source products T = V^T G (see engine.split_k)
 
 
 # ---------------------------------------------------------------------------
@@ -76,16 +75,22 @@ def tree_ops(tree, s, X, transpose):
 
 
 def run_waves(seqs, scratch):
-    """Execute op sequences in lock-step: wave w runs op w of every sequence."""
+    """Execute op sequences in lock-step: wave w runs op w of every sequence.
+
+    The ops of one wave belong to different trees, so they are independent: per wave
+    the leaf solves are one batched TRSM per direction, every transposed-A product
+    (dense couplings in the transposed sweep and the first factor t = P1^T X of every
+    low-rank coupling) is one grouped launch, and every plain product (dense
+    couplings of the forward sweep and the second factor Y -= P2 t) is one more."""
     seqs = [s for s in seqs if s]
     if not seqs:
         return
     for w in range(max(len(s) for s in seqs)):
         keep = []  # temporaries must outlive the launches below (torch may recycle freed blocks)
         leaves = {0: [], 1: []}
-        dense = {False: Grouped(False, False), True: Grouped(True, False)}
-        lr1 = {False: Grouped(True, False), True: Grouped(True, False)}
-        lr2 = Grouped(False, False)
+        g_t = Grouped(True, False)    # transposed-A products (independent of each other)
+        g_n = Grouped(False, False)   # plain products (the low-rank ones need g_t's t)
+        lr = []
         for seq in seqs:
             if w >= len(seq):
                 continue
@@ -102,30 +107,35 @@ def run_waves(seqs, scratch):
             if isinstance(b, DevLR):
                 if b.k == 0:
                     continue
-                t = scratch(b.k, r)
-                keep.append(t)
+                lr.append((b, Xs, Yd, tr, r))
+            elif tr:
+                g_t.add(b.data_ptr(), E.ld(b), Xs.data_ptr(), E.ld(Xs), Yd.data_ptr(), E.ld(Yd), b.shape[1], r,
+                        b.shape[0], -1.0, 1.0)
+            else:
+                g_n.add(b.data_ptr(), E.ld(b), Xs.data_ptr(), E.ld(Xs), Yd.data_ptr(), E.ld(Yd), b.shape[0], r,
+                        b.shape[1], -1.0, 1.0)
+        if lr:
+            ts = scratch(sum(b.k * r for b, _, _, _, r in lr))
+            ts.zero_()  # t = P1^T X accumulates (atomic): balance_k may split its tall K
+            keep.append(ts)
+            off = 0
+            for b, Xs, Yd, tr, r in lr:
+                tp = ts.data_ptr() + 8 * off
+                off += b.k * r
                 # t = U^T X (forward) or V^T X (transposed); then Y -= V t or U t
                 P1 = b.V if tr else b.U
                 P2 = b.U if tr else b.V
-                lr1[tr].add(P1.data_ptr(), E.ld(P1), Xs.data_ptr(), E.ld(Xs), t.data_ptr(), r, b.k, r,
-                            Xs.shape[0], 1.0, 0.0)
-                lr2.add(P2.data_ptr(), E.ld(P2), t.data_ptr(), r, Yd.data_ptr(), E.ld(Yd), Yd.shape[0], r, b.k,
-                        -1.0, 1.0)
-            else:
-                M, K = (b.shape[1], b.shape[0]) if tr else (b.shape[0], b.shape[1])
-                dense[tr].add(b.data_ptr(), E.ld(b), Xs.data_ptr(), E.ld(Xs), Yd.data_ptr(), E.ld(Yd), M, r, K,
-                              -1.0, 1.0)
+                g_t.add(P1.data_ptr(), E.ld(P1), Xs.data_ptr(), E.ld(Xs), tp, r, b.k, r, Xs.shape[0], 1.0, 0.0,
+                        atomic=1)
+                g_n.add(P2.data_ptr(), E.ld(P2), tp, r, Yd.data_ptr(), E.ld(Yd), Yd.shape[0], r, b.k, -1.0, 1.0)
         for tr, lst in leaves.items():
             if lst:
                 E.trsm_batched("left", tr, [t.L.data_ptr() for t, _ in lst], [t.n for t, _ in lst],
                                [E.ld(t.L) for t, _ in lst], [t.Dinv.data_ptr() for t, _ in lst],
                                [X.data_ptr() for _, X in lst], [X.shape[1] for _, X in lst],
                                [E.ld(X) for _, X in lst])
-        dense[False].launch()
-        dense[True].launch()
-        lr1[False].launch()
-        lr1[True].launch()
-        lr2.launch()
+        g_t.launch()
+        g_n.launch()
 
 
 def diag_solve_many(items, scratch):
@@ -314,12 +324,15 @@ class LevelPass(NumericPass):
     def _lowrank_many(self, VUs):
         out = []
         g1, g2 = Grouped(True, False), Grouped(False, False)
-        for V, U in VUs:
+        # U^T U has a tall K (the rows of U) and few tiles: accumulate it into zeroed
+        # buffers so balance_k can split that K across CTAs
+        utus = self.S.zeros_many([(max(U.shape[1], 1), max(U.shape[1], 1)) for _, U in VUs])
+        for (V, U), utu in zip(VUs, utus):
             k = U.shape[1]
-            utu = self.S.empty(max(k, 1), max(k, 1))
             Eff = self.P.empty(V.shape[0], k)
             if k:
-                g1.add(U.data_ptr(), E.ld(U), U.data_ptr(), E.ld(U), utu.data_ptr(), k, k, k, U.shape[0], 1.0, 0.0)
+                g1.add(U.data_ptr(), E.ld(U), U.data_ptr(), E.ld(U), utu.data_ptr(), k, k, k, U.shape[0], 1.0, 0.0,
+                       atomic=1)
                 g2.add(V.data_ptr(), E.ld(V), utu.data_ptr(), k, Eff.data_ptr(), E.ld(Eff), V.shape[0], k, k,
                        1.0, 0.0)
             lr = DevLR(V, U, Eff)
@@ -378,7 +391,7 @@ class LevelPass(NumericPass):
                 probs.append(p)
                 self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s][sel])
         if probs:
-            E.gemm_grouped(np.concatenate(probs), False, True)
+            E.gemm_grouped(E.balance_k(np.concatenate(probs), False, True), False, True)
         return out
 
     # -- implicit products, batched over nodes -----------------------------------
@@ -438,7 +451,7 @@ class LevelPass(NumericPass):
         w, ld = self.s_w[s], self.s_ld[s]
         tsz = w * r
         toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
-        T = self.S.zeros(int(tsz.sum()))  # p1 is split along its tall K (atomic slabs)
+        T = self.S.zeros(int(tsz.sum()))  # p1 accumulates into it (K may be split)
         tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
         raw_lo = self.s_raw[s] + (8 * lo * ld).astype(np.uint64)
         eff_hi = self.s_eff[s] + (8 * hi * ld).astype(np.uint64)
@@ -455,8 +468,9 @@ class LevelPass(NumericPass):
         else:  # T = E[hi:]^T G[rpos] ; W[cpos] -= V[lo:hi] T
             p1["A"], p1["K"], p1["b_rows"] = eff_hi, nro, rpos
             p2["A"], p2["M"], p2["c_rows"] = raw_lo, nrd, cpos
-        E.gemm_grouped(E.split_k(p1, True, False, KSPLIT), True, False)
-        E.gemm_grouped(p2, False, False)
+        p1["atomic"] = 1  # T is zeroed: p1 accumulates, so its tall K may be split
+        E.gemm_grouped(E.balance_k(p1, True, False), True, False)
+        E.gemm_grouped(E.balance_k(p2, False, False), False, False)
         self._wflops(2.0 * (nrd + nro), w=w, wbase=self.s_raw[s], r=r, rbase=rep(6).astype(np.uint64))
 
     def approx_off_many(self, nodes, ranks):
@@ -533,7 +547,7 @@ class LevelPass(NumericPass):
         if parts:
             P = np.concatenate(parts)
             P["batch"], P["atomic"], P["alpha"], P["beta"] = 1, 1, -1.0, 1.0
-            E.gemm_grouped(P, False, True)
+            E.gemm_grouped(E.balance_k(P, False, True), False, True)
             self._wflops(2.0 * P["M"] * P["N"], w=P["K"], wbase=np.concatenate(bases))
         if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
             Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
@@ -605,7 +619,7 @@ class LevelPass(NumericPass):
                 continue
             tsz = w * r
             toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
-            T = self.S.zeros(int(tsz.sum()))  # p1 is split along its tall K (atomic slabs)
+            T = self.S.zeros(int(tsz.sum()))  # p1 accumulates into it (K may be split)
             tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
             p1 = np.zeros(n, dtype=GEMM_DTYPE)
             p2 = np.zeros(n, dtype=GEMM_DTYPE)
@@ -626,8 +640,9 @@ class LevelPass(NumericPass):
             P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
             P1["batch"], P1["alpha"] = 1, 1.0
             P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
-            E.gemm_grouped(E.split_k(P1, True, False, KSPLIT), True, False)
-            E.gemm_grouped(P2, False, False)
+            P1["atomic"] = 1  # T is zeroed: P1 accumulates, so its tall K may be split
+            E.gemm_grouped(E.balance_k(P1, True, False), True, False)
+            E.gemm_grouped(E.balance_k(P2, False, False), False, False)
         if transpose:
             sol2 = []
             for (node, s), W in zip(items, Ws):

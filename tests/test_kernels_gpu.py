@@ -270,3 +270,36 @@ def test_gemv_multi_modes_against_numpy(cuda):
     torch.cuda.synchronize()
     for yd, ref in refs:
         assert relerr(yd.cpu().numpy(), ref) < 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 37, 64, 100, 256, 300, 320, 400])
+def test_trsm_left_shapes(cuda, n):
+    """L X = B and L^T X = B for batches with ragged n and column counts (the
+    strip-resident kernel for n <= 320, the blocked GEMM chain above)."""
+    import torch
+
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(100 + n)
+    ms = [1, 31, 32, 33, 200]
+    Ls, Dv = [], []
+    for _ in ms:
+        G = rng.standard_normal((n, n))
+        Ad = E.to_dev(G @ G.T / n + np.eye(n))
+        D = E.zeros(max(n, 1), 64)
+        info = E.zeros(1, dtype=E.I32)
+        E.potrf_batched([Ad.data_ptr()], [n], [n], [D.data_ptr()], info)
+        Ls.append(Ad)
+        Dv.append(D)
+    for trans in (0, 1):
+        Bs = [rng.standard_normal((n, m + 3)) for m in ms]   # ld > cols
+        Bd = [E.to_dev(B) for B in Bs]
+        E.trsm_batched("left", trans, [L.data_ptr() for L in Ls], [n] * len(ms), [n] * len(ms),
+                       [d.data_ptr() for d in Dv], [b.data_ptr() for b in Bd], ms, [m + 3 for m in ms])
+        torch.cuda.synchronize()
+        for L, B, b, m in zip(Ls, Bs, Bd, ms):
+            Lh = np.tril(L.cpu().numpy())
+            ref = np.linalg.solve(Lh.T if trans else Lh, B[:, :m])
+            got = b.cpu().numpy()
+            assert relerr(got[:, :m], ref) < 1e-11
+            assert np.array_equal(got[:, m:], B[:, m:])  # columns past m untouched

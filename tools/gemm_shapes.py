@@ -73,3 +73,30 @@ for ta, tb in ((False, False), (True, False), (False, True)):
     if sel.any():
         print(f"  TA={ta:d} TB={tb:d}: {sel.sum()} calls {tm[sel].sum()*1e3:.1f} ms {fls[sel].sum()/1e9:.1f} GF "
               f"{fls[sel].sum()/tm[sel].sum()/1e12:.2f} TF/s")
+# load balance: a launch cannot finish before its longest CTA (its largest K, in
+# 16-wide k-steps) nor before total tile-steps / (740 concurrent CTAs)
+lb_sum, ideal_sum = 0.0, 0.0
+for l in log:
+    p = l[0]
+    tiles = (np.ceil(p["M"] / 64) * np.ceil(p["N"] / 64) * p["batch"]).astype(float)
+    ksteps = np.ceil(p["K"] / 16).astype(float)
+    total = float((tiles * ksteps).sum())
+    lb = max(total / 740.0, float(ksteps.max()))
+    lb_sum += lb
+    ideal_sum += total / 740.0
+print(f"  launch-time lower bound from the longest CTA vs perfect balance: {lb_sum:.0f} vs {ideal_sum:.0f} "
+      f"k-step units ({lb_sum/ideal_sum:.2f}x)")
+rows = []
+for l in log:
+    p = l[0]
+    tiles = (np.ceil(p["M"] / 64) * np.ceil(p["N"] / 64) * p["batch"]).astype(float)
+    ksteps = np.ceil(p["K"] / 16).astype(float)
+    total = float((tiles * ksteps).sum())
+    lb = max(total / 740.0, float(ksteps.max()))
+    i = int(np.argmax(ksteps))
+    rows.append((lb - total / 740.0, len(p), int(p["M"][i]), int(p["N"][i]), int(p["K"][i]), int(p["atomic"][i]),
+                 float(p["beta"][i]), l[1], l[2], total / 740.0))
+rows.sort(reverse=True)
+print("  worst launches (excess k-steps, nprob, M N K atomic beta of the longest, TA TB, balanced):")
+for r in rows[:12]:
+    print("   ", r)
