@@ -39,54 +39,119 @@ struct GemmArgs {
     rsc_gemm_problem p[MAXP];
 };
 
+// Per-thread operand loader: the 8 A and 8 B elements a thread stages per k-tile sit
+// at fixed (row, column) offsets of the tile, so their addresses, smem slots and the
+// M / N validity are computed once per CTA; a k-tile only advances the pointers and
+// checks the K bound.  (Recomputing all of that per element per tile, with a branch
+// per gathered row, had the k-loop at ~11 instructions per DMMA.)
 template <bool TA, bool TB>
-__device__ __forceinline__ void load_tiles(const rsc_gemm_problem &P, const double *A,
-                                           const double *B, int m0, int n0, int k0,
-                                           double *sA, double *sB) {
-    const int t = threadIdx.x;
-    if (!TA) {  // A row-major M x K, contiguous along k
-        const int k = t % BK, mr = t / BK;
+struct Loader {
+    const double *a;      // element 0 of this thread's A slots at k0 = 0
+    const double *b;      // element 0 of this thread's B slots (no gather) / column base (gather)
+    const int *rows;      // b_rows (gather) or nullptr
+    long long a_i, a_k;   // A: stride between the 8 slots, advance per k-tile
+    long long b_i, b_k;
+    long long ldb;
+    unsigned amask, bmask;  // M / N validity of the 8 slots
+    int ka, kb;           // k offset of slot 0 within the tile (A / B); slots add 2*i when k varies
+    int sa, sb;           // smem offset of slot 0; slot stride below
+    int K;
+
+    __device__ __forceinline__ void init(const rsc_gemm_problem &P, const double *A, const double *B, int m0,
+                                         int n0) {
+        const int t = threadIdx.x;
+        K = P.K;
+        amask = bmask = 0;
+        if (!TA) {  // A row-major M x K: slot i = row (t/BK) + 8i, column k = t%BK
+            const int k = t % BK, mr = t / BK;
+            a = A + (long long)(m0 + mr) * P.lda + k;
+            a_i = (long long)(NT / BK) * P.lda;
+            a_k = BK;
+            ka = k;
+            sa = mr * PADK + k;
 #pragma unroll
-        for (int i = 0; i < BM * BK / NT; ++i) {
-            const int m = mr + (NT / BK) * i;
-            const bool v = (m0 + m < P.M) && (k0 + k < P.K);
-            const double *src = v ? A + (long long)(m0 + m) * P.lda + (k0 + k) : A;
-            cp_async_8(&sA[m * PADK + k], src, v);
+            for (int i = 0; i < BM * BK / NT; ++i)
+                if (m0 + mr + (NT / BK) * i < P.M) amask |= 1u << i;
+        } else {    // A stored K x M: slot i = k row (t>>6) + 2i, column m = t&63
+            const int m = t & 63, kr = t >> 6;
+            a = A + (long long)kr * P.lda + m0 + m;
+            a_i = 2LL * P.lda;
+            a_k = (long long)BK * P.lda;
+            ka = kr;
+            sa = kr * PADM + m;
+            if (m0 + m < P.M) amask = 0xffu;
         }
-    } else {  // A stored K x M, contiguous along m
-        const int m = t & 63, kr = t >> 6;
+        rows = nullptr;
+        ldb = P.ldb;
+        if (!TB) {  // op(B) = B (K x N): slot i = k row (t>>6) + 2i, column n = t&63
+            const int n = t & 63, kr = t >> 6;
+            rows = P.b_rows;
+            b = rows ? B + n0 + n : B + (long long)kr * P.ldb + n0 + n;
+            b_i = 2LL * P.ldb;
+            b_k = (long long)BK * P.ldb;
+            kb = kr;
+            sb = kr * PADM + n;
+            if (n0 + n < P.N) bmask = 0xffu;
+        } else {    // op(B) = B^T, B stored N x K: slot i = row (t/BK) + 8i, column k = t%BK
+            const int k = t % BK, nr = t / BK;
+            b = B + (long long)(n0 + nr) * P.ldb + k;
+            b_i = (long long)(NT / BK) * P.ldb;
+            b_k = BK;
+            kb = k;
+            sb = nr * PADK + k;
 #pragma unroll
-        for (int i = 0; i < BK / 2; ++i) {
-            const int k = kr + 2 * i;
-            const bool v = (m0 + m < P.M) && (k0 + k < P.K);
-            const double *src = v ? A + (long long)(k0 + k) * P.lda + (m0 + m) : A;
-            cp_async_8(&sA[k * PADM + m], src, v);
+            for (int i = 0; i < BN * BK / NT; ++i)
+                if (n0 + nr + (NT / BK) * i < P.N) bmask |= 1u << i;
         }
     }
-    if (!TB) {  // op(B) = B (K x N), contiguous along n, optional row gather
-        const int n = t & 63, kr = t >> 6;
+
+    // stage k-tile kt into sA / sB
+    __device__ __forceinline__ void load(int kt, double *sA, double *sB) const {
+        const int k0 = kt * BK;
+        if (!TA) {
+            const double *p = a + (long long)kt * a_k;
+            const bool kv = k0 + ka < K;
 #pragma unroll
-        for (int i = 0; i < BK / 2; ++i) {
-            const int k = kr + 2 * i;
-            const bool v = (n0 + n < P.N) && (k0 + k < P.K);
-            const double *src = B;
-            if (v) {
-                const int row = P.b_rows ? __ldg(P.b_rows + k0 + k) : (k0 + k);
-                src = B + (long long)row * P.ldb + (n0 + n);
+            for (int i = 0; i < 8; ++i) {
+                const bool v = kv && ((amask >> i) & 1);
+                cp_async_8(&sA[sa + i * (NT / BK) * PADK], v ? p + i * a_i : a, v);
             }
-            cp_async_8(&sB[k * PADM + n], src, v);
-        }
-    } else {  // op(B) = B^T with B stored N x K, contiguous along k
-        const int k = t % BK, nr = t / BK;
+        } else {
+            const double *p = a + (long long)kt * a_k;
 #pragma unroll
-        for (int i = 0; i < BN * BK / NT; ++i) {
-            const int n = nr + (NT / BK) * i;
-            const bool v = (n0 + n < P.N) && (k0 + k < P.K);
-            const double *src = v ? B + (long long)(n0 + n) * P.ldb + (k0 + k) : B;
-            cp_async_8(&sB[n * PADK + k], src, v);
+            for (int i = 0; i < 8; ++i) {
+                const bool v = (amask & 1) && (k0 + ka + 2 * i < K);
+                cp_async_8(&sA[sa + 2 * i * PADM], v ? p + i * a_i : a, v);
+            }
+        }
+        if (!TB) {
+            if (rows) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = k0 + kb + 2 * i;
+                    const bool v = (bmask & 1) && k < K;
+                    const int r = v ? __ldg(rows + k) : 0;
+                    cp_async_8(&sB[sb + 2 * i * PADM], b + (long long)r * ldb, v);
+                }
+            } else {
+                const double *p = b + (long long)kt * b_k;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool v = (bmask & 1) && (k0 + kb + 2 * i < K);
+                    cp_async_8(&sB[sb + 2 * i * PADM], v ? p + i * b_i : b, v);
+                }
+            }
+        } else {
+            const double *p = b + (long long)kt * b_k;
+            const bool kv = k0 + kb < K;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool v = kv && ((bmask >> i) & 1);
+                cp_async_8(&sB[sb + i * (NT / BK) * PADK], v ? p + i * b_i : b, v);
+            }
         }
     }
-}
+};
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant__ GemmArgs args) {
@@ -123,18 +188,20 @@ __global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant_
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (P.K + BK - 1) / BK;
+    Loader<TA, TB> ld;
+    ld.init(P, A, B, m0, n0);
     if (nk > 0) {
         // STAGES-deep cp.async pipeline, one CTA barrier per k-tile
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk) load_tiles<TA, TB>(P, A, B, m0, n0, s * BK, sA[s], sB[s]);
+            if (s < nk) ld.load(s, sA[s], sB[s]);
             cp_async_commit();
         }
         for (int kt = 0; kt < nk; ++kt) {
             cp_async_wait<STAGES - 2>();
             __syncthreads();  // tile kt landed; everyone is done with tile kt-1's stage
             const int pf = kt + STAGES - 1;
-            if (pf < nk) load_tiles<TA, TB>(P, A, B, m0, n0, pf * BK, sA[pf % STAGES], sB[pf % STAGES]);
+            if (pf < nk) ld.load(pf, sA[pf % STAGES], sB[pf % STAGES]);
             cp_async_commit();
             const double *a_s = sA[kt % STAGES];
             const double *b_s = sB[kt % STAGES];
