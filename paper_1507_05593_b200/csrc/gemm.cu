@@ -154,7 +154,10 @@ struct Loader {
 };
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(NT) gemm_grouped_kernel(const __grid_constant__ GemmArgs args) {
+#ifndef RSC_GEMM_MINB
+#define RSC_GEMM_MINB 1
+#endif
+__global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const __grid_constant__ GemmArgs args) {
     extern __shared__ __align__(16) double gsm[];
     double(*sA)[A_SZ] = reinterpret_cast<double(*)[A_SZ]>(gsm);
     double(*sB)[B_SZ] = reinterpret_cast<double(*)[B_SZ]>(gsm + STAGES * A_SZ);
