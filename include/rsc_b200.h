@@ -190,6 +190,27 @@ int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_id
 int rsc_sym_postorder(long long n, const long long *parent, long long *post);
 int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *row_idx,
                       const long long *parent, const long long *post, long long *counts);
+/* One geometric bisection step of nested dissection (ordering.py:182-192): the
+ * vertices are split at the median along the widest coordinate axis (ties by id);
+ * the second half's members adjacent to the first form the separator.  indptr /
+ * indices: full adjacency CSR without the diagonal; xyz: n x dim row-major;
+ * mark: n zero bytes of scratch.  out <- side1 | separator | side2, counts <- sizes.
+ * Returns 1 when a side is empty (no split). */
+int rsc_nd_split_geometric(long long nv, const long long *verts, int dim, const double *xyz,
+                           const long long *indptr, const long long *indices, unsigned char *mark,
+                           long long *out, long long *counts);
+/* Batched window cut of a CSR matrix (n rows, ascending column indices) whose
+ * values are 1-based positions: request q = rows sel[r_off[q]..+r_n[q]) (or the
+ * range [r_lo[q], +r_n[q]) when r_off[q] < 0) x columns likewise (ascending
+ * lists), block-local numbering.  Pass 1 (rowptr == NULL) writes nnz[q]; pass 2
+ * (nz_off = exclusive scan of nnz, rp_off[q] = sum of r_n[i]+1 over i < q) writes
+ * rowptr (int32), colidx (int32) and val = position - 1 (int32).  Host threads. */
+int rsc_csr_windows(long long nq, long long n, const long long *indptr, const long long *indices,
+                    const double *data, const long long *sel, const long long *r_off,
+                    const long long *r_n, const long long *r_lo, const long long *c_off,
+                    const long long *c_n, const long long *c_lo, long long *nnz,
+                    const long long *rp_off, const long long *nz_off, int *rowptr, int *colidx,
+                    int *val);
 
 /* ---- Gaussian sketches (replaces the host draw at reference kernels.py:85-92,
  * np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r)), seeded per

@@ -50,6 +50,8 @@ EXPORTED = (
     "rsc_sym_etree",
     "rsc_sym_postorder",
     "rsc_sym_colcounts",
+    "rsc_nd_split_geometric",
+    "rsc_csr_windows",
     "rsc_pcg64_block_states",
     "rsc_pcg64_seed_states",
     "rsc_normal_workspace_bytes",
@@ -92,6 +94,8 @@ _SIGS = {
     "rsc_sym_etree": (I, [LL, P, P, P]),
     "rsc_sym_postorder": (I, [LL, P, P]),
     "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
+    "rsc_nd_split_geometric": (I, [LL, P, ctypes.c_int, P, P, P, P, P, P]),
+    "rsc_csr_windows": (I, [LL, LL] + [P] * 16),
     "rsc_pcg64_block_states": (I, [I, I, P, P, P, P]),
     "rsc_pcg64_seed_states": (I, [I, P, P]),
     "rsc_normal_workspace_bytes": (ctypes.c_size_t, [I, P]),

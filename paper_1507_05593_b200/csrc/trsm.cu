@@ -31,7 +31,11 @@ namespace {
 #endif
 constexpr int SM_ROWS = RSC_TRSM_ROWS;  // strip height (32: two CTAs per SM)
 constexpr int TNT = 128;
-constexpr int KB = SM_ROWS == 32 ? 32 : 64;  // k extent of one chunk
+#ifndef RSC_TRSM_STAGES
+#define RSC_TRSM_STAGES 2
+#endif
+constexpr int RST = RSC_TRSM_STAGES;          // operand pipeline depth (right solve)
+constexpr int KB = RST == 3 ? 16 : (SM_ROWS == 32 ? 32 : 64);  // k extent of one chunk
 constexpr int KPB = 64 / KB;                 // chunks per 64-wide operand block
 constexpr int BPAD = KB + 4;  // [n][k] row stride of a staged operand block
 constexpr int WTM = SM_ROWS / 2;             // warp tile rows (2 x 2 warps)
@@ -173,7 +177,8 @@ __global__ void __launch_bounds__(TNT) trsm_right_kernel(const __grid_constant__
     load_block(0);
     if (nblk > 1) load_block(1);
     cp_async_commit();
-    prefetch(0);
+#pragma unroll
+    for (int st = 0; st < RST - 1; ++st) prefetch(st);
 
     double acc[FI][4][2];
 #pragma unroll
@@ -183,9 +188,9 @@ __global__ void __launch_bounds__(TNT) trsm_right_kernel(const __grid_constant__
 
     int cj = 0, ci = 0, stage = 0;  // chunk being computed
     while (cj < nblk) {
-        cp_async_wait<0>();
-        __syncthreads();  // chunk landed; the other stage is free; S writes are visible
-        prefetch(stage ^ 1);
+        cp_async_wait<RST - 2>();
+        __syncthreads();  // chunk landed; the stage to refill is free; S writes are visible
+        prefetch((stage + RST - 1) % RST);
         if (ci == 0 && cj >= 1) store_block(cj - 1);  // X_{cj-1} is final
         const int nu = KPB * cj;
         const bool diag = ci >= nu;
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(TNT) trsm_right_kernel(const __grid_constant__
                         acc[i][j][e] = 0.0;
                     }
         }
-        stage ^= 1;
+        stage = (stage + 1) % RST;
         if (++ci >= KPB * (cj + 1)) {
             ++cj;
             ci = 0;
@@ -417,7 +422,7 @@ int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const 
     // attribute call happens later (e.g. inside a CUDA-graph capture)
     static bool attr = false;
     if (!attr) {
-        const int maxbytes = (SM_ROWS * (TMAXN + 4) + 2 * 64 * BPAD) * (int)sizeof(double);
+        const int maxbytes = (SM_ROWS * (TMAXN + 4) + RST * 64 * BPAD) * (int)sizeof(double);
         cudaFuncSetAttribute(trsm_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxbytes);
         attr = true;
     }
@@ -443,7 +448,7 @@ int rsc_trsm_right_fused(int count, const double *const *L, const int *n, const 
         if (!a.count) continue;
         a.tile_begin[a.count] = tiles;
         a.lds = ((mx + 63) & ~63) + 4;
-        const int bytes = (SM_ROWS * a.lds + 2 * 64 * BPAD) * (int)sizeof(double);
+        const int bytes = (SM_ROWS * a.lds + RST * 64 * BPAD) * (int)sizeof(double);
         trsm_right_kernel<<<(unsigned)tiles, TNT, bytes, s>>>(a);
         RSC_CHECK_LAUNCH();
     }

@@ -20,6 +20,7 @@ L(rows, C_B) of interior.py:77-95; rows outside off_rows are exact zeros).
 """
 
 import numpy as np
+import torch
 
 from . import engine as E
 
@@ -77,30 +78,83 @@ class IndexPool:
 
 class CsrPool:
     """Many small CSR blocks in three device buffers (rowptr int32 per block,
-    colidx int32, values f64)."""
+    colidx int32, values f64).  Blocks are windows of one host CSR matrix (`full`),
+    requested with `add` and cut together by one rsc_csr_windows call at upload."""
 
-    def __init__(self):
-        self.rp, self.ci, self.v = [], [], []
-        self.nrp = self.nnz = 0
+    def __init__(self, full=None):
+        self.full = full
+        self.sel, self.nsel = [], 0
+        self.req, self.blocks = [], []
+        self.nrp = 0
 
-    def add(self, S):
-        S = S.tocsr()
-        S.sort_indices()
-        rp_off, nz_off = self.nrp, self.nnz
-        self.rp.append(S.indptr.astype(np.int32))
-        self.ci.append(S.indices.astype(np.int32))
-        self.v.append(S.data.astype(np.float64))
-        self.nrp += S.shape[0] + 1
-        self.nnz += S.nnz
-        return CsrBlock(self, S.shape[0], S.shape[1], rp_off, nz_off, S.nnz)
+    def _spec(self, x):
+        if isinstance(x, tuple):  # contiguous range [lo, hi)
+            return -1, x[1] - x[0], x[0]
+        x = np.ascontiguousarray(x, dtype=np.int64)
+        off = self.nsel
+        self.sel.append(x)
+        self.nsel += x.size
+        return off, x.size, 0
+
+    def add(self, rows, cols):
+        """Block full[rows, cols]; rows / cols = (lo, hi) ranges or ascending index arrays."""
+        ro, rn, rl = self._spec(rows)
+        co, cn, cl = self._spec(cols)
+        blk = CsrBlock(self, rn, cn, self.nrp, 0, 0)
+        self.nrp += rn + 1
+        self.req.append((ro, rn, rl, co, cn, cl))
+        self.blocks.append(blk)
+        return blk
+
+    def cut(self):
+        """Host arrays of every requested block (two passes of rsc_csr_windows).
+        The windows are cut from the position matrix: values are 1-based positions
+        into B's storage, returned 0-based in `pos`."""
+        from . import _lib
+
+        lib = _lib.load()
+        full = self.full
+        if full.nnz >= 2**31 - 1:
+            raise ValueError("matrix too large for int32 block positions")
+        indptr = np.ascontiguousarray(full.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(full.indices, dtype=np.int64)
+        data = np.ascontiguousarray(full.data, dtype=np.float64)
+        sel = np.concatenate(self.sel) if self.sel else np.zeros(1, np.int64)
+        q = np.array(self.req, dtype=np.int64).reshape(-1, 6).T.copy()
+        nq = q.shape[1]
+        nnz = np.zeros(max(nq, 1), dtype=np.int64)
+        rp_off = np.array([b.rp_off for b in self.blocks] or [0], dtype=np.int64)
+        args = [nq, full.shape[0], indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, sel.ctypes.data]
+        args += [q[i].ctypes.data for i in range(6)] + [nnz.ctypes.data, rp_off.ctypes.data]
+        _lib.check(lib.rsc_csr_windows(*args, None, None, None, None), "rsc_csr_windows")
+        offs = np.concatenate(([0], np.cumsum(nnz[:nq])))
+        tot = int(offs[-1])
+        self.rp = np.zeros(max(self.nrp, 1), dtype=np.int32)
+        self.ci = np.empty(max(tot, 1), dtype=np.int32)
+        self.pos = np.empty(max(tot, 1), dtype=np.int32)
+        if tot == 0:
+            self.ci[:] = 0
+            self.pos[:] = 0
+        _lib.check(lib.rsc_csr_windows(*args, offs.ctypes.data, self.rp.ctypes.data, self.ci.ctypes.data,
+                                       self.pos.ctypes.data), "rsc_csr_windows")
+        for blk, o, z in zip(self.blocks, offs[:nq].tolist(), nnz[:nq].tolist()):
+            blk.nz_off, blk.nnz = o, z
+        self.nnz = tot
 
     def upload(self, b_values):
-        """Device buffers; the blocks were cut from the position matrix, so their
-        values are 1-based positions into B's storage: pos -> values."""
-        self.rp_dev = E.to_dev(np.concatenate(self.rp) if self.rp else np.zeros(1, np.int32))
-        self.ci_dev = E.to_dev(np.concatenate(self.ci) if self.ci else np.zeros(1, np.int32))
-        self.pos = (np.concatenate(self.v) if self.v else np.ones(1)).astype(np.int64) - 1
-        self.v_dev = E.to_dev(b_values[self.pos] if self.v else np.zeros(1))
+        """Device buffers; the values are gathered on the device (pos -> values)."""
+        self.cut()
+        self.rp_dev = E.to_dev(self.rp)
+        self.ci_dev = E.to_dev(self.ci)
+        self.pos_dev = E.to_dev(self.pos)  # int32
+        self.v_dev = torch.empty(self.pos.size, dtype=torch.float64, device=E.dev())
+        self.gather(E.to_dev(np.asarray(b_values)), self.pos_dev)
+
+    def gather(self, vals_dev, index_dev):
+        if self.nnz:
+            torch.index_select(vals_dev, 0, index_dev, out=self.v_dev)
+        else:
+            self.v_dev.zero_()
 
 
 class CsrBlock:
@@ -140,21 +194,17 @@ class NumericPlan:
         # Every A block of the plan is cut from a copy of B whose values are 1-based
         # positions into B's storage, so one gather index maps any matrix with this
         # pattern onto the device value buffer (load_values: refactorization).
-        from .sparse import SparseSpdMatrix, permute_symmetric
+        from .sparse import SparseSpdMatrix
 
         posB = SparseSpdMatrix(B.n, B.col_ptr, B.row_idx, np.arange(1, B.nnz_lower + 1, dtype=np.float64),
                                validate=False)
         full = posB.to_csr_full()
         self.full = full
-        if A is not None:  # B.values = A.values[b_from_a]
-            posA = SparseSpdMatrix(A.n, A.col_ptr, A.row_idx, np.arange(A.nnz_lower, dtype=np.float64),
-                                   validate=False)
-            self.b_from_a = permute_symmetric(posA, sym.perm).values.astype(np.int64)
-        else:
-            self.b_from_a = None
+        # B.values = A.values[b_from_a] (the gather analyze used to permute A)
+        self.b_from_a = getattr(sym, "b_from_a", None) if A is not None else None
         self.source = A
         self.idx = IndexPool()
-        self.csr = CsrPool()
+        self.csr = CsrPool(full)
         self.sources = []
         self.unit_source = {}      # unit index -> source id
         self.targets = {}          # node j -> [Pair] (reference order)
@@ -175,8 +225,8 @@ class NumericPlan:
                     if rj.size > nib:
                         tails.append(rj[nib:])
                 off_rows = np.unique(np.concatenate(tails)) if tails else np.empty(0, np.int64)
-                A_BB = self.csr.add(full[c0:c1, c0:c1])
-                A_off = self.csr.add(full[off_rows, c0:c1]) if off_rows.size else None
+                A_BB = self.csr.add((c0, c1), (c0, c1))
+                A_off = self.csr.add(off_rows, (c0, c1)) if off_rows.size else None
                 roff = self.idx.add(off_rows)
                 self.rows_off[("int", u)] = roff
                 self.interior.append((u, ids, c0, c1, off_rows, A_off, A_BB))
@@ -189,9 +239,9 @@ class NumericPlan:
             c0, c1 = part.cols(j)
             R = part.rows[j]
             self.targets[j] = []
-            A_CC = self.csr.add(full[c0:c1, c0:c1])
-            A_RC = self.csr.add(full[R, c0:c1]) if R.size else None
-            A_CR = self.csr.add(full[R, c0:c1].T.tocsr()) if R.size else None
+            A_CC = self.csr.add((c0, c1), (c0, c1))
+            A_RC = self.csr.add(R, (c0, c1)) if R.size else None
+            A_CR = self.csr.add((c0, c1), R) if R.size else None  # full[R, C]^T (symmetric)
             self.node_blocks[j] = (A_CC, A_RC, A_CR)
             self.rows_off[j] = self.idx.add(R)
             if R.size:
@@ -238,8 +288,9 @@ class NumericPlan:
             raise ValueError("plan was prepared without its source matrix; cannot load new values")
         if A.n != self.sym.B.n or A.nnz_lower != self.b_from_a.size:
             raise ValueError("matrix pattern differs from the prepared one")
-        vals = np.asarray(A.values)[self.b_from_a][self.csr.pos]
-        self.csr.v_dev.copy_(E.torch_from_numpy(vals))
+        if getattr(self, "_a_index", None) is None:  # A position of every block entry
+            self._a_index = E.to_dev(self.b_from_a.astype(np.int32))[self.csr.pos_dev.long()]
+        self.csr.gather(E.to_dev(np.asarray(A.values)), self._a_index)
         self.source = A
 
     def sketch_specs(self, cfg, alpha_d):
@@ -307,43 +358,55 @@ class NumericPlan:
 
     def _build_tree_maps(self, part):
         """Window maps for every (tree node j, block s, source) with both windows
-        non-empty (diagblocks.py:231-234, 252-255), plus the A windows."""
+        non-empty (diagblocks.py:231-234, 252-255), plus the A windows.  Vectorized
+        per source: one searchsorted of all block bounds, one index chunk."""
         from .diagtree import TreeShape
 
         self.tree_shapes = {}
         self.tmap = {}
+        keys = ("s", "clo", "chi", "rlo", "rhi", "cidx", "ridx")
         for j, split in self.sym.sep_splits.items():
             c0, c1 = part.cols(j)
             shape = TreeShape(c1 - c0, c0, split)
             self.tree_shapes[j] = shape
-            for s in shape.order:
-                (r0, r1), (cc0, cc1) = shape.span(s)
-                gr0, gr1, gc0, gc1 = c0 + r0, c0 + r1, c0 + cc0, c0 + cc1
-                maps = []
-                for pr in self.targets[j]:
-                    rows = self.sources[pr.s].rows
-                    clo, chi = np.searchsorted(rows, (gc0, gc1))
-                    rlo, rhi = np.searchsorted(rows, (gr0, gr1))
-                    if clo == chi or rlo == rhi:
-                        continue
+            order = list(shape.order)
+            nb = len(order)
+            spans = np.array([shape.span(s) for s in order], dtype=np.int64).reshape(nb, 4) + c0
+            gr0, gr1, gc0, gc1 = spans.T
+            bounds = np.concatenate((gc0, gc1, gr0, gr1))
+            per = [[] for _ in range(nb)]
+            for pr in self.targets[j]:
+                rows = self.sources[pr.s].rows
+                clo, chi, rlo, rhi = np.searchsorted(rows, bounds).reshape(4, nb)
+                ok = np.nonzero((clo < chi) & (rlo < rhi))[0]
+                if ok.size == 0:
+                    continue
+                # one index chunk: [cidx of every kept block] then [ridx of every kept block]
+                cl, ch, rl, rh = clo[ok], chi[ok], rlo[ok], rhi[ok]
+                nc, nr = ch - cl, rh - rl
+                lens = np.concatenate((nc, nr))
+                starts = np.concatenate((cl, rl))
+                base = np.concatenate((gc0[ok], gr0[ok]))
+                first = np.cumsum(lens) - lens
+                tot = int(lens.sum())
+                src = np.repeat(starts - first, lens) + np.arange(tot)
+                chunk = rows[src] - np.repeat(base, lens)
+                off0 = self.idx.add(chunk)
+                offs = off0 + first
+                for t, k in enumerate(ok.tolist()):
                     m = TreeBlockMaps()
-                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(clo), int(chi), int(rlo), int(rhi)
-                    m.cidx_off = self.idx.add(rows[clo:chi] - gc0)
-                    m.ridx_off = self.idx.add(rows[rlo:rhi] - gr0)
-                    maps.append(m)
-                win = self.full[gr0:gr1, gc0:gc1]
-                blk = self.csr.add(win)
-                blkT = self.csr.add(win.T.tocsr()) if (gr0, gr1) != (gc0, gc1) else None
+                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(cl[t]), int(ch[t]), int(rl[t]), int(rh[t])
+                    m.cidx_off, m.ridx_off = int(offs[t]), int(offs[ok.size + t])
+                    per[k].append(m)
+            for k, s in enumerate(order):
+                g = (int(gr0[k]), int(gr1[k])), (int(gc0[k]), int(gc1[k]))
+                blk = self.csr.add(g[0], g[1])
+                blkT = self.csr.add(g[1], g[0]) if g[0] != g[1] else None
+                maps = per[k]
                 self.tree_maps[(j, s)] = (maps, blk, blkT)
-                self.tmap[(j, s)] = {
-                    "s": np.array([m.s for m in maps], dtype=np.int64),
-                    "clo": np.array([m.clo for m in maps], dtype=np.int64),
-                    "chi": np.array([m.chi for m in maps], dtype=np.int64),
-                    "rlo": np.array([m.rlo for m in maps], dtype=np.int64),
-                    "rhi": np.array([m.rhi for m in maps], dtype=np.int64),
-                    "cidx": np.array([m.cidx_off for m in maps], dtype=np.int64),
-                    "ridx": np.array([m.ridx_off for m in maps], dtype=np.int64),
-                }
+                vals = np.array([[m.s, m.clo, m.chi, m.rlo, m.rhi, m.cidx_off, m.ridx_off] for m in maps],
+                                dtype=np.int64).reshape(len(maps), 7)
+                self.tmap[(j, s)] = {kk: vals[:, i].copy() for i, kk in enumerate(keys)}
 
 
 class DeviceSketches:

@@ -174,16 +174,31 @@ class Permutation:
         return f"Permutation(n={self.n})"
 
 
+def _permuted_lower(A, p):
+    """Lower-storage (row, col) of every entry of A under p, sorted by (col, row),
+    and the source position of each: one counting pass by column plus a per-column
+    row sort (scipy's C++ csr kernels) instead of a 2-key lexsort."""
+    n = A.n
+    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(A.col_ptr))
+    nr, nc = p[A.row_idx], p[cols]
+    r, c = np.maximum(nr, nc), np.minimum(nr, nc)
+    if n == 0 or r.size == 0:
+        return r, c, np.arange(r.size, dtype=np.int64)
+    # positions as data (exact in f64 below 2^53); entries are distinct, so the
+    # transpose (csr of the (c, r) pairs) never sums duplicates
+    pos = np.arange(r.size, dtype=np.float64)
+    m = sp.csr_matrix((pos, (c, r)), shape=(n, n))
+    m.sort_indices()
+    order = m.data.astype(np.int64)
+    return m.indices.astype(np.int64), np.repeat(np.arange(n, dtype=np.int64), np.diff(m.indptr)), order
+
+
 def permute_symmetric(A, perm):
     """B[p(i), p(j)] = A[i, j], kept in lower storage (sparse.py:171-189)."""
     if perm.n != A.n:
         raise DimensionMismatch(f"permutation size {perm.n} != matrix size {A.n}")
-    p = perm.forward
-    cols = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.col_ptr))
-    nr, nc = p[A.row_idx], p[cols]
-    r, c = np.maximum(nr, nc), np.minimum(nr, nc)
-    order = np.lexsort((r, c))
-    r, c, v = r[order], c[order], A.values[order]
+    r, c, order = _permuted_lower(A, perm.forward)
+    v = A.values[order]
     col_ptr = np.zeros(A.n + 1, dtype=np.int64)
     np.cumsum(np.bincount(c, minlength=A.n), out=col_ptr[1:])
     return SparseSpdMatrix(A.n, col_ptr, r, v, validate=False)

@@ -23,7 +23,7 @@ import scipy.sparse as sp
 from . import _lib
 from .errors import MissingCoordinates
 from .problems import Coordinates
-from .sparse import Permutation, permute_symmetric
+from .sparse import Permutation, SparseSpdMatrix, _permuted_lower
 
 DEFAULT_LEAF_SIZE = 64
 DIAG_TREE_FACTOR = 1
@@ -114,6 +114,12 @@ class _Dissector:
         self.indices = adj.indices.astype(np.int64)
         self.deg = np.diff(self.indptr)
         self.xyz = xyz
+        self._nd = None
+        if method == "geometric" and xyz.ndim == 2 and xyz.shape[1] >= 1 and np.isfinite(xyz).all():
+            from . import _lib
+
+            self.xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+            self._nd = _lib.load().rsc_nd_split_geometric
         self.method = method
         self.leaf = leaf_size
         self.order = np.empty(self.n, dtype=np.int64)
@@ -129,22 +135,24 @@ class _Dissector:
         return lo, lo + k
 
     def _neighbors(self, vs):
-        """Flattened neighbour lists of vs and the owning position of each entry."""
+        """Flattened neighbour lists of vs (CSR rows gathered in order)."""
         starts, cnt = self.indptr[vs], self.deg[vs]
         tot = int(cnt.sum())
         if tot == 0:
-            return np.empty(0, np.int64), np.empty(0, np.int64)
-        own = np.repeat(np.arange(len(vs)), cnt)
-        offs = np.arange(tot) - np.repeat(np.cumsum(cnt) - cnt, cnt)
-        return self.indices[np.repeat(starts, cnt) + offs], own
+            return np.empty(0, np.int64), cnt
+        first = np.cumsum(cnt) - cnt
+        return self.indices[np.repeat(starts - first, cnt) + np.arange(tot)], cnt
 
     def boundary(self, side1, cand):
         """Members of `cand` (in order) with a neighbour in side1 (ordering.py:182-192)."""
         self.mark[side1] = True
-        nb, own = self._neighbors(cand)
+        nb, cnt = self._neighbors(cand)
         hit = np.zeros(len(cand), dtype=bool)
         if nb.size:
-            np.logical_or.at(hit, own, self.mark[nb])
+            # per-candidate count of marked neighbours: segment sums over the CSR rows
+            c = np.concatenate(([0], np.cumsum(self.mark[nb], dtype=np.int64)))
+            ends = np.cumsum(cnt)
+            hit = c[ends] > c[ends - cnt]
         self.mark[side1] = False
         return hit
 
@@ -160,6 +168,19 @@ class _Dissector:
         return verts[s1], verts[sep], verts[s2]
 
     def bisect_geometric(self, verts):
+        if self._nd is not None:  # C++ split (csrc/nd.cpp), same result as below
+            verts = np.ascontiguousarray(verts, dtype=np.int64)
+            out = np.empty(len(verts), dtype=np.int64)
+            cnt = np.empty(3, dtype=np.int64)
+            rc = self._nd(len(verts), verts.ctypes.data, self.xyz.shape[1], self.xyz.ctypes.data,
+                          self.indptr.ctypes.data, self.indices.ctypes.data, self.mark.ctypes.data,
+                          out.ctypes.data, cnt.ctypes.data)
+            if rc < 0:
+                raise RuntimeError(f"rsc_nd_split_geometric failed ({rc})")
+            if rc == 1:
+                return None
+            a, b = int(cnt[0]), int(cnt[0] + cnt[1])
+            return out[:a], out[a:b], out[b:]
         pts = self.xyz[verts]
         axis = int(np.argmax(pts.max(axis=0) - pts.min(axis=0)))
         return self.split_by_order(verts, np.lexsort((verts, pts[:, axis])))
@@ -513,7 +534,10 @@ def analyze(A, tau_o, tau_d, interior_blocks=True, coords=None):
             fwd[reordered] = np.arange(nd.lo, nd.hi, dtype=np.int64)
             splits_by_range[(nd.lo, nd.hi)] = split
     perm = Permutation(fwd)
-    B = permute_symmetric(A, perm)
+    r, c, b_from_a = _permuted_lower(A, perm.forward)
+    col_ptr = np.zeros(A.n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(c, minlength=A.n), out=col_ptr[1:])
+    B = SparseSpdMatrix(A.n, col_ptr, r, A.values[b_from_a], validate=False)
     t1 = time.perf_counter()
     parent, post, counts = etree_postorder_counts(B)
     part = form_supernodes(B.n, parent, counts, septree, tau_o)
@@ -522,7 +546,7 @@ def analyze(A, tau_o, tau_d, interior_blocks=True, coords=None):
     units = build_units(septree, part, tau_o, interior_blocks)
     t2 = time.perf_counter()
     return SymbolicPlan(perm=perm, B=B, septree=septree, partition=part, sep_splits=sep_splits, units=units,
-                        parent=parent, counts=counts, t_ordering=t1 - t0, t_symbolic=t2 - t1)
+                        b_from_a=b_from_a, parent=parent, counts=counts, t_ordering=t1 - t0, t_symbolic=t2 - t1)
 
 
 def block_rank(m, n, alpha, p):

@@ -25,11 +25,30 @@ def logged(Gp, m, k, ldg, Qp, ldq, rank, alloc=None):
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    if os.environ.get("QR_COND"):
+        for gp, mm, kk, ll in zip(Gp, m, k, ldg):
+            if mm * kk >= 64 * 64:
+                t = _dev_view(int(gp), int(mm), int(kk), int(ll))
+                sv = torch.linalg.svdvals(t)
+                conds.append((int(mm), int(kk), float(sv[0] / sv[-1])))
     r = orig(Gp, m, k, ldg, Qp, ldq, rank, alloc)
     e.record()
     torch.cuda.synchronize()
     log.append((np.asarray(m), np.asarray(k), s.elapsed_time(e)))
     return r
+
+
+conds = []
+
+
+class _CAI:
+    def __init__(self, ptr, shape, strides):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr, False),
+                                         "strides": strides, "version": 3}
+
+
+def _dev_view(ptr, m, k, ld):
+    return torch.as_tensor(_CAI(ptr, (m, k), (8 * ld, 8)), device="cuda").clone()
 
 
 NM.E.qrcp_batched = logged
@@ -43,3 +62,9 @@ for m, k, ms in sorted(log, key=lambda x: -x[2])[:15]:
     big = len(m) - reg - sm
     print(f"  {ms:7.2f} ms  n={len(m):4d} (reg {reg}, smem {sm}, coop {big})  max m {m.max()} max k {k.max()}  "
           f"median m {int(np.median(m))} k {int(np.median(k))}")
+
+if conds:
+    c = np.array([x[2] for x in conds])
+    sz = np.array([x[0] * x[1] for x in conds], dtype=float)
+    for lim in (1e4, 1e6, 1e8, 1e10, 1e12):
+        print(f"  cond <= {lim:.0e}: {int((c <= lim).sum())} of {c.size} sketches, {100 * sz[c <= lim].sum() / sz.sum():.0f}% of entries")
