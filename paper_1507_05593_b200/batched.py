@@ -121,22 +121,26 @@ class BatchedSupernodes:
         for c0 in range(lo, hi, self.chunk):
             c1 = min(hi, c0 + self.chunk)
             cnt = c1 - c0
-            idx = range(c0, c1)
-            Dp = [self.D[i].data_ptr() for i in idx]
-            Ip = [self.Dinv[i].data_ptr() for i in idx]
+            Dp, Ip, Bp = self._ptrs(self.D, c0, c1), self._ptrs(self.Dinv, c0, c1), self._ptrs(self.B, c0, c1)
             E.potrf_batched(Dp, [n] * cnt, [n] * cnt, Ip, self.info[c0:c1])
-            Bp = [self.B[i].data_ptr() for i in idx]
-            Sp = None if B_src is None else [B_src[i].data_ptr() for i in idx]
+            Sp = None if B_src is None else self._ptrs(B_src, c0, c1)
             E.trsm_right(Dp, [n] * cnt, [n] * cnt, Ip, Sp, Bp, [m] * cnt, [n] * cnt)
             LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
             E.gemm_strided_batched(LO, Om, G, transA=True, splitk=self.splitk)
             for _ in range(q):
                 E.gemm_strided_batched(LO, G, H)
                 E.gemm_strided_batched(LO, H, G, transA=True, splitk=self.splitk)
-            self._qr_work = E.qrcp_batched([self.G[i].data_ptr() for i in idx], [n] * cnt, [r] * cnt,
-                                           [r] * cnt, [self.U[i].data_ptr() for i in idx], [r] * cnt,
+            self._qr_work = E.qrcp_batched(self._ptrs(self.G, c0, c1), [n] * cnt, [r] * cnt,
+                                           [r] * cnt, self._ptrs(self.U, c0, c1), [r] * cnt,
                                            self.rank[c0:c1])
             E.gemm_strided_batched(LO, self.U[c0:c1], self.V[c0:c1])
+
+    @staticmethod
+    def _ptrs(T, lo, hi):
+        """Device addresses of T[lo:hi] (3-D contiguous), computed arithmetically (no
+        per-block tensor indexing on the host)."""
+        step = T.stride(0) * T.element_size()
+        return np.uint64(T.data_ptr()) + np.arange(lo, hi, dtype=np.uint64) * np.uint64(step)
 
     def check_info(self):
         info = self.info.cpu().numpy()

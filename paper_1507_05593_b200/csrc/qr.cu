@@ -212,47 +212,31 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
 // step touches only registers plus one 2 KB reflector broadcast through shared
 // memory.  Every warp keeps a replicated copy of the position permutation (two
 // entries per lane) and evaluates the pivot rule itself, so a step needs exactly two
-// CTA barriers: after the owner of the pivot column publishes its reflector, and
-// after every warp has updated its columns and their partial norms.
+// CTA barriers (dorg2r: one, with a double-buffered reflector).
+//
+// Row i of step i lives in register q = i / 32 of lane i % 32.  The steps are
+// generated per register index QI (template), so every "row > i" mask and every
+// extraction of row i is resolved at compile time except inside register QI: no
+// runtime-indexed register selects (which made the first version instruction-bound).
+// The sketch is loaded and Q stored through a shared-memory tile (coalesced global
+// access), and Q's columns past the kept rank are written as zeros here.
 constexpr int RQ_ROWS = 8;   // rows per lane  (m <= 256)
 constexpr int RQ_SLOTS = 4;  // columns per warp (k <= 64)
 constexpr int RQ_WARPS = 16;
+constexpr int RQ_LDT = 65;   // staging tile stride in doubles (odd: conflict-free)
+constexpr int RQ_SMEM = RQ_ROWS * 32 * RQ_LDT * 8;
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-__global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_constant__ QrArgs args,
-                                                                  int *rank_out) {
-    __shared__ double v[RQ_ROWS * 32];
-    __shared__ double vn1[64], vn2[64], tau[64], diagR[64];
-    __shared__ int pc_s, rank_s;
-    const int b = blockIdx.x;
-    const int m = args.m[b], k = args.k[b];
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const double *G = args.G[b];
-    const int ldg = args.ldg[b];
+struct RegQr {
     double a[RQ_SLOTS][RQ_ROWS];
     int pos[RQ_SLOTS];  // position of my column, or k if unchosen
-#pragma unroll
-    for (int s = 0; s < RQ_SLOTS; ++s) {
-        const int j = warp + RQ_WARPS * s;
-        pos[s] = k;
-#pragma unroll
-        for (int q = 0; q < RQ_ROWS; ++q) {
-            const int r = lane + 32 * q;
-            a[s][q] = (j < k && r < m) ? G[(long long)r * ldg + j] : 0.0;
-        }
-        double nrm = 0.0;
-#pragma unroll
-        for (int q = 0; q < RQ_ROWS; ++q) nrm += a[s][q] * a[s][q];
-        nrm = sqrt(warp_sum(nrm));
-        if (j < k && lane == 0) { vn1[j] = nrm; vn2[j] = nrm; }
-    }
-    // replicated permutation: lane holds positions lane and lane+32
-    int p0 = lane, p1 = lane + 32;
-    __syncthreads();
-    const int kmin = m < k ? m : k;
-    for (int i = 0; i < kmin; ++i) {
-        // pivot rule, evaluated identically by every warp
+    int p0, p1;         // replicated permutation: positions lane and lane + 32
+    int lane, warp, k;
+
+    // pivot rule (first position of the largest partial norm), evaluated identically
+    // by every warp; swaps positions i and the winner, returns the physical column
+    __device__ __forceinline__ int pivot(int i, const double *vn1) {
         double best = -1.0;
         int bp = k;
         if (lane >= i && lane < k) { const double x = vn1[p0]; if (x > best) { best = x; bp = lane; } }
@@ -263,74 +247,57 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
             const int op = __shfl_xor_sync(0xffffffffu, bp, o);
             if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
         }
-        if (bp >= k) bp = i;
-        // swap positions i and bp in the replicated permutation
+        if (bp >= k) bp = i;  // NaN norms (failed upstream pivot): keep the order
         const int pi = __shfl_sync(0xffffffffu, i < 32 ? p0 : p1, i & 31);
         const int pb = __shfl_sync(0xffffffffu, bp < 32 ? p0 : p1, bp & 31);
         if (lane == (i & 31)) { if (i < 32) p0 = pb; else p1 = pb; }
         if (lane == (bp & 31)) { if (bp < 32) p0 = pi; else p1 = pi; }
-        const int pc = pb;  // physical pivot column
-        const int qi = i >> 5, li = i & 31;  // row i lives in register q = qi of lane li
-        if ((pc & (RQ_WARPS - 1)) == warp) {
-            const int sp = pc / RQ_WARPS;
+        return pb;
+    }
+
+    // dlarfg on rows i..m-1 of my slot-S column (the pivot); v gets rows > i
+    template <int QI, int S>
+    __device__ __forceinline__ void reflect(int i, int li, double *v, double *tau, double *diagR) {
+        pos[S] = i;
+        double part = 0.0;
 #pragma unroll
-            for (int s = 0; s < RQ_SLOTS; ++s) {
-                if (s != sp) continue;  // compile-time slot index keeps a[][] in registers
-                pos[s] = i;
-                // dlarfg on rows i..m-1 of the pivot column
-                double part = 0.0;
+        for (int q = QI; q < RQ_ROWS; ++q)
+            if (q > QI || lane > li) part += a[S][q] * a[S][q];
+        const double xnorm = sqrt(warp_sum(part));
+        const double alpha = shfl(a[S][QI], li);
+        double tau_i = 0.0, beta = alpha, scal = 1.0;
+        if (xnorm != 0.0) {
+            beta = -copysign(hypot(alpha, xnorm), alpha);
+            tau_i = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
 #pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    const int r = lane + 32 * q;
-                    if (r > i && r < m) part += a[s][q] * a[s][q];
-                }
-                const double xnorm = sqrt(warp_sum(part));
-                double alpha = 0.0;
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q)
-                    if (q == qi) alpha = shfl(a[s][q], li);
-                double tau_i = 0.0, beta = alpha, scal = 1.0;
-                if (xnorm != 0.0) {
-                    beta = -copysign(hypot(alpha, xnorm), alpha);
-                    tau_i = (beta - alpha) / beta;
-                    scal = 1.0 / (alpha - beta);
-                }
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    const int r = lane + 32 * q;
-                    if (r > i && r < m) {
-                        if (xnorm != 0.0) a[s][q] *= scal;
-                        v[r] = a[s][q];
-                    } else if (r == i) {
-                        a[s][q] = beta;
-                    }
-                }
-                if (lane == 0) { tau[i] = tau_i; diagR[i] = beta; pc_s = pc; }
+        for (int q = QI; q < RQ_ROWS; ++q) {
+            if (q > QI || lane > li) {
+                if (xnorm != 0.0) a[S][q] *= scal;
+                v[lane + 32 * q] = a[S][q];
+            } else if (lane == li) {
+                a[S][q] = beta;
             }
         }
-        __syncthreads();
-        const double tau_i = tau[i];
-        // apply H_i to my unchosen columns and downdate their norms; the four slots
-        // run side by side (one interleaved butterfly) instead of one after another
+        if (lane == 0) { tau[i] = tau_i; diagR[i] = beta; }
+    }
+
+    // H_i applied to my unchosen columns, then the dlaqp2 partial-norm downdate
+    template <int QI>
+    __device__ __forceinline__ void update(int i, int li, const double *v, double tau_i, double *vn1, double *vn2) {
         double vr[RQ_ROWS];
 #pragma unroll
-        for (int q = 0; q < RQ_ROWS; ++q) {
-            const int r = lane + 32 * q;
-            vr[q] = (r > i && r < m) ? v[r] : 0.0;
-        }
+        for (int q = QI; q < RQ_ROWS; ++q) vr[q] = (q > QI || lane > li) ? v[lane + 32 * q] : 0.0;
         bool act[RQ_SLOTS];
         double ai[RQ_SLOTS], v1[RQ_SLOTS], v2[RQ_SLOTS];
 #pragma unroll
         for (int s = 0; s < RQ_SLOTS; ++s) {
             const int j = warp + RQ_WARPS * s;
-            act[s] = j < k && pos[s] >= k;  // present and not yet chosen
+            act[s] = j < k && pos[s] >= k;
             v1[s] = act[s] ? vn1[j] : 0.0;
             v2[s] = act[s] ? vn2[j] : 1.0;
-            double x = 0.0;
-#pragma unroll
-            for (int q = 0; q < RQ_ROWS; ++q)
-                if (q == qi) x = a[s][q];
-            ai[s] = shfl(x, li);
+            ai[s] = shfl(a[s][QI], li);
         }
         if (tau_i != 0.0) {
             double d[RQ_SLOTS];
@@ -338,7 +305,7 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 d[s] = 0.0;
 #pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) d[s] += vr[q] * a[s][q];
+                for (int q = QI; q < RQ_ROWS; ++q) d[s] += vr[q] * a[s][q];
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
@@ -349,14 +316,11 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
                 if (!act[s]) continue;
                 const double f = tau_i * (d[s] + ai[s]);
 #pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    a[s][q] -= f * vr[q];
-                    if (q == qi && lane == li) a[s][q] -= f;
-                }
-                ai[s] -= f;  // row i after the update (v_i = 1 there, vr = 0)
+                for (int q = QI; q < RQ_ROWS; ++q) a[s][q] -= f * vr[q];
+                if (lane == li) a[s][QI] -= f;  // v_i = 1 on row i (vr = 0 there)
+                ai[s] -= f;
             }
         }
-        // dlaqp2 partial-norm downdate; recompute when cancellation is too strong
         bool redo[RQ_SLOTS];
         bool any_redo = false;
 #pragma unroll
@@ -374,16 +338,14 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
                 vn1[warp + RQ_WARPS * s] = v1[s] * sqrt(temp);
             }
         }
-        if (any_redo) {
+        if (__any_sync(0xffffffffu, any_redo)) {
             double nv[RQ_SLOTS];
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 nv[s] = 0.0;
 #pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    const int r = lane + 32 * q;
-                    if (r > i && r < m) nv[s] += a[s][q] * a[s][q];
-                }
+                for (int q = QI; q < RQ_ROWS; ++q)
+                    if (q > QI || lane > li) nv[s] += a[s][q] * a[s][q];
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
@@ -392,14 +354,127 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 if (!redo[s]) continue;
-                const double x = (i + 1 < m) ? sqrt(nv[s]) : 0.0;
+                const double x = sqrt(nv[s]);  // rows > i exist: i + 1 < m is implied by zero padding
                 if (lane == 0) { vn1[warp + RQ_WARPS * s] = x; vn2[warp + RQ_WARPS * s] = x; }
             }
         }
-        __syncthreads();
     }
+
+    // Householder steps i0 <= i < i1 whose row lives in register QI
+    template <int QI>
+    __device__ __forceinline__ void factor_range(int i0, int i1, double *v, double *vn1, double *vn2,
+                                                 double *tau, double *diagR) {
+        for (int i = i0; i < i1; ++i) {
+            const int li = i - 32 * QI;
+            const int pc = pivot(i, vn1);
+            if ((pc & (RQ_WARPS - 1)) == warp) {
+                switch (pc / RQ_WARPS) {
+                    case 0: reflect<QI, 0>(i, li, v, tau, diagR); break;
+                    case 1: reflect<QI, 1>(i, li, v, tau, diagR); break;
+                    case 2: reflect<QI, 2>(i, li, v, tau, diagR); break;
+                    default: reflect<QI, 3>(i, li, v, tau, diagR); break;
+                }
+            }
+            __syncthreads();
+            update<QI>(i, li, v, tau[i], vn1, vn2);
+            __syncthreads();
+        }
+    }
+
+    // dorg2r steps i1-1 >= i >= i0 (rows in register QI); positions >= rank are idle
+    template <int QI>
+    __device__ __forceinline__ void form_range(int i0, int i1, int rank, double (*v)[RQ_ROWS * 32],
+                                               const double *tau) {
+        for (int i = i1 - 1; i >= i0; --i) {
+            const int li = i - 32 * QI;
+            double *vb = v[i & 1];
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                if (pos[s] != i) continue;
+#pragma unroll
+                for (int q = QI; q < RQ_ROWS; ++q)
+                    if (q > QI || lane > li) vb[lane + 32 * q] = a[s][q];
+            }
+            __syncthreads();
+            const double ti = tau[i];
+            double vr[RQ_ROWS];
+#pragma unroll
+            for (int q = QI; q < RQ_ROWS; ++q) vr[q] = (q > QI || lane > li) ? vb[lane + 32 * q] : 0.0;
+            double d[RQ_SLOTS], ai[RQ_SLOTS];
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                d[s] = 0.0;
+#pragma unroll
+                for (int q = QI; q < RQ_ROWS; ++q) d[s] += vr[q] * a[s][q];
+                ai[s] = shfl(a[s][QI], li);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int s = 0; s < RQ_SLOTS; ++s) d[s] += __shfl_xor_sync(0xffffffffu, d[s], o);
+#pragma unroll
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                if (pos[s] > i && pos[s] < rank) {
+                    const double f = ti * (d[s] + ai[s]);
+#pragma unroll
+                    for (int q = QI; q < RQ_ROWS; ++q) a[s][q] -= f * vr[q];
+                    if (lane == li) a[s][QI] -= f;
+                } else if (pos[s] == i) {
+#pragma unroll
+                    for (int q = 0; q < RQ_ROWS; ++q) {
+                        if (q < QI) a[s][q] = 0.0;
+                        else if (q > QI) a[s][q] = -ti * vr[q];
+                        else a[s][q] = lane > li ? -ti * vr[q] : (lane == li ? 1.0 - ti : 0.0);
+                    }
+                }
+            }
+        }
+    }
+};
+
+__global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_constant__ QrArgs args,
+                                                                  int *rank_out) {
+    extern __shared__ __align__(16) double tile[];  // [RQ_ROWS*32][RQ_LDT]
+    __shared__ double v[2][RQ_ROWS * 32];
+    __shared__ double vn1[64], vn2[64], tau[64], diagR[64];
+    __shared__ int rank_s;
+    const int b = blockIdx.x;
+    const int m = args.m[b], k = args.k[b];
+    const int t = threadIdx.x;
+    RegQr st;
+    st.lane = t & 31;
+    st.warp = t >> 5;
+    st.k = k;
+    const int lane = st.lane, warp = st.warp;
+    const double *G = args.G[b];
+    const int ldg = args.ldg[b];
+    // coalesced load of the row-major sketch into the tile, zero padded to 256 x 64
+    for (int e = t; e < RQ_ROWS * 32 * 64; e += RQ_WARPS * 32) {
+        const int r = e >> 6, j = e & 63;
+        tile[r * RQ_LDT + j] = (r < m && j < k) ? G[(long long)r * ldg + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < RQ_SLOTS; ++s) {
+        const int j = warp + RQ_WARPS * s;
+        st.pos[s] = k;
+        double nrm = 0.0;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) {
+            st.a[s][q] = tile[(lane + 32 * q) * RQ_LDT + j];
+            nrm += st.a[s][q] * st.a[s][q];
+        }
+        nrm = sqrt(warp_sum(nrm));
+        if (j < k && lane == 0) { vn1[j] = nrm; vn2[j] = nrm; }
+    }
+    st.p0 = lane;
+    st.p1 = lane + 32;
+    __syncthreads();
+    const int kmin = m < k ? m : k;
+    st.factor_range<0>(0, kmin < 32 ? kmin : 32, v[0], vn1, vn2, tau, diagR);
+    st.factor_range<1>(32, kmin, v[0], vn1, vn2, tau, diagR);
     if (t == 0) {
-        const double d0 = fabs(diagR[0]);
+        const double d0 = kmin > 0 ? fabs(diagR[0]) : 0.0;
         int r = 0;
         if (d0 != 0.0) {
             const double cut = (double)(m > k ? m : k) * EPS * d0;
@@ -411,62 +486,21 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
     }
     __syncthreads();
     const int rank = rank_s;
-    // dorg2r on positions rank-1 .. 0
-    for (int i = rank - 1; i >= 0; --i) {
-        const int qi = i >> 5, li = i & 31;
-        // publish v_i from its owner
-#pragma unroll
-        for (int s = 0; s < RQ_SLOTS; ++s) {
-            if (pos[s] != i) continue;
-#pragma unroll
-            for (int q = 0; q < RQ_ROWS; ++q) {
-                const int r = lane + 32 * q;
-                if (r > i && r < m) v[r] = a[s][q];
-            }
-        }
-        __syncthreads();
-        const double ti = tau[i];
-        double vr[RQ_ROWS];
-#pragma unroll
-        for (int q = 0; q < RQ_ROWS; ++q) {
-            const int r = lane + 32 * q;
-            vr[q] = (r > i && r < m) ? v[r] : 0.0;
-        }
-#pragma unroll
-        for (int s = 0; s < RQ_SLOTS; ++s) {
-            if (pos[s] > i && pos[s] < rank) {
-                double d = 0.0, ai = 0.0;
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) d += vr[q] * a[s][q];
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q)
-                    if (q == qi) ai = shfl(a[s][q], li);
-                const double f = ti * (warp_sum(d) + ai);
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    a[s][q] -= f * vr[q];
-                    if (q == qi && lane == li) a[s][q] -= f;
-                }
-            } else if (pos[s] == i) {
-#pragma unroll
-                for (int q = 0; q < RQ_ROWS; ++q) {
-                    const int r = lane + 32 * q;
-                    a[s][q] = (r > i) ? -ti * vr[q] : (r == i ? 1.0 - ti : 0.0);
-                }
-            }
-        }
-        __syncthreads();
-    }
-    double *Q = args.Q[b];
-    const int ldq = args.ldq[b];
+    st.form_range<1>(32, rank, rank, v, tau);
+    st.form_range<0>(0, rank < 32 ? rank : 32, rank, v, tau);
+    // Q[:, :rank] through the tile (columns rank..k-1 zero), coalesced store
 #pragma unroll
     for (int s = 0; s < RQ_SLOTS; ++s) {
-        if (pos[s] >= rank) continue;
+        if (st.pos[s] >= rank) continue;
 #pragma unroll
-        for (int q = 0; q < RQ_ROWS; ++q) {
-            const int r = lane + 32 * q;
-            if (r < m) Q[(long long)r * ldq + pos[s]] = a[s][q];
-        }
+        for (int q = 0; q < RQ_ROWS; ++q) tile[(lane + 32 * q) * RQ_LDT + st.pos[s]] = st.a[s][q];
+    }
+    __syncthreads();
+    double *Q = args.Q[b];
+    const int ldq = args.ldq[b];
+    for (int e = t; e < m * k; e += RQ_WARPS * 32) {
+        const int r = e / k, j = e - r * k;
+        Q[(long long)r * ldq + j] = j < rank ? tile[r * RQ_LDT + j] : 0.0;
     }
 }
 
@@ -538,6 +572,7 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     if (!attr_set) {
         cudaFuncSetAttribute(qrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SMEM_BYTES_MAX);
+        cudaFuncSetAttribute(qrcp_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, RQ_SMEM);
         attr_set = true;
     }
     std::vector<int> tiny, small, big;
@@ -592,7 +627,7 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                 qa.m[c] = m[i]; qa.k[c] = k[i]; qa.ldg[c] = ldg[i]; qa.ldq[c] = ldq[i];
                 qa.woff[c] = 0;
             }
-            qrcp_reg_kernel<<<qa.count, RQ_WARPS * 32, 0, s>>>(qa, rank_dev);
+            qrcp_reg_kernel<<<qa.count, RQ_WARPS * 32, RQ_SMEM, s>>>(qa, rank_dev);
             RSC_CHECK_LAUNCH();
         }
     }
@@ -611,5 +646,6 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                             off.data(), (unsigned *)work_dev, s);
         if (rc) return rc;
     }
+    if (tiny.size() == (size_t)count) return 0;  // the register kernel wrote its zero tails
     return qr_zero_tails(count, m, k, Q, ldq, rank_dev, s);
 }
