@@ -72,9 +72,11 @@ def model_flops(nb, n, m, r, q):
 class BatchedSupernodes:
     """Device workspace for a batch of `nb` supernodes of shape (n, m) with sketch width r."""
 
-    def __init__(self, nb, n, m, r, q=1, chunk=None, splitk=None):
+    def __init__(self, nb, n, m, r, q=1, chunk=None, splitk=None, pipeline=1):
         self.nb, self.n, self.m, self.r, self.q = nb, n, m, r, q
         self.chunk = nb if chunk is None else max(1, min(chunk, nb))
+        self.pipeline = pipeline
+        self._streams_side = None
         # split the tall K = m of L_O^T X so a launch has >= ~4 CTAs per SM
         self.splitk = splitk if splitk is not None else max(1, min(m // 256, 16))
         self.D = E.empty(nb, n, n)
@@ -87,7 +89,7 @@ class BatchedSupernodes:
         self.V = E.empty(nb, m, r)
         self.info = E.zeros(nb, dtype=E.I32)
         self.rank = E.zeros(nb, dtype=E.I32)
-        self._qr_work = None
+        self._qr_work = []
         self._rng_n = np.full(nb, m * r, dtype=np.int64)
         lib = E.require_cuda()
         self._rng_work = E.empty(int(lib.rsc_normal_workspace_bytes(nb, self._rng_n.ctypes.data)) // 8 + 1)
@@ -112,28 +114,62 @@ class BatchedSupernodes:
     def run(self, master=0, sketches=True, lo=0, hi=None, states=None, B_src=None):
         """Factor + compress blocks lo..hi-1 (inputs in self.D / self.B, or the
         off-diagonal blocks read from the device tensor B_src and L_O written to
-        self.B).  The sketches are generated on the device first unless `sketches` is
-        False (then self.Om is used as the caller left it)."""
-        n, m, r, q = self.n, self.m, self.r, self.q
+        self.B).  The sketches are generated on the device unless `sketches` is False
+        (then self.Om is used as the caller left it).
+
+        Stream schedule: the sketch generator (integer-ALU bound) runs on a side
+        stream under the latency-bound POTRF and the TRSM, and joins before the first
+        sketch product.  With `pipeline` > 1 the chunks of the batch rotate over that
+        many streams, so one chunk's latency-bound stages (POTRF, QRCP) overlap another
+        chunk's DMMA-bound TRSM and products."""
         hi = self.nb if hi is None else hi
+        main = torch.cuda.current_stream()
+        rng_done = None
         if sketches:
-            self.generate_sketches(master, lo, hi, states)
-        for c0 in range(lo, hi, self.chunk):
-            c1 = min(hi, c0 + self.chunk)
-            cnt = c1 - c0
-            Dp, Ip, Bp = self._ptrs(self.D, c0, c1), self._ptrs(self.Dinv, c0, c1), self._ptrs(self.B, c0, c1)
-            E.potrf_batched(Dp, [n] * cnt, [n] * cnt, Ip, self.info[c0:c1])
-            Sp = None if B_src is None else self._ptrs(B_src, c0, c1)
-            E.trsm_right(Dp, [n] * cnt, [n] * cnt, Ip, Sp, Bp, [m] * cnt, [n] * cnt)
-            LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
-            E.gemm_strided_batched(LO, Om, G, transA=True, splitk=self.splitk)
-            for _ in range(q):
-                E.gemm_strided_batched(LO, G, H)
-                E.gemm_strided_batched(LO, H, G, transA=True, splitk=self.splitk)
-            self._qr_work = E.qrcp_batched(self._ptrs(self.G, c0, c1), [n] * cnt, [r] * cnt,
-                                           [r] * cnt, self._ptrs(self.U, c0, c1), [r] * cnt,
-                                           self.rank[c0:c1])
-            E.gemm_strided_batched(LO, self.U[c0:c1], self.V[c0:c1])
+            side = self._side_streams(1)[0]
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.generate_sketches(master, lo, hi, states)
+            rng_done = torch.cuda.Event()
+            rng_done.record(side)
+        chunks = list(range(lo, hi, self.chunk))
+        self._qr_work = []  # workspaces stay alive until the next run
+        pipes = [main] if self.pipeline <= 1 or len(chunks) <= 1 else self._side_streams(1 + self.pipeline)[1:]
+        for p in pipes:
+            if p is not main:
+                p.wait_stream(main)
+        for ci, c0 in enumerate(chunks):
+            with torch.cuda.stream(pipes[ci % len(pipes)]):
+                self._run_chunk(c0, min(hi, c0 + self.chunk), rng_done, B_src)
+        for p in pipes:
+            if p is not main:
+                main.wait_stream(p)
+        if rng_done is not None:
+            main.wait_event(rng_done)
+
+    def _side_streams(self, k):
+        if self._streams_side is None or len(self._streams_side) < k:
+            self._streams_side = [torch.cuda.Stream() for _ in range(k)]
+        return self._streams_side
+
+    def _run_chunk(self, c0, c1, rng_done, B_src):
+        n, m, r, q = self.n, self.m, self.r, self.q
+        cnt = c1 - c0
+        Dp, Ip, Bp = self._ptrs(self.D, c0, c1), self._ptrs(self.Dinv, c0, c1), self._ptrs(self.B, c0, c1)
+        E.potrf_batched(Dp, [n] * cnt, [n] * cnt, Ip, self.info[c0:c1])
+        Sp = None if B_src is None else self._ptrs(B_src, c0, c1)
+        E.trsm_right(Dp, [n] * cnt, [n] * cnt, Ip, Sp, Bp, [m] * cnt, [n] * cnt)
+        if rng_done is not None:
+            torch.cuda.current_stream().wait_event(rng_done)
+        LO, G, H, Om = self.B[c0:c1], self.G[c0:c1], self.H[c0:c1], self.Om[c0:c1]
+        E.gemm_strided_batched(LO, Om, G, transA=True, splitk=self.splitk)
+        for _ in range(q):
+            E.gemm_strided_batched(LO, G, H)
+            E.gemm_strided_batched(LO, H, G, transA=True, splitk=self.splitk)
+        self._qr_work.append(E.qrcp_batched(self._ptrs(self.G, c0, c1), [n] * cnt, [r] * cnt,
+                                            [r] * cnt, self._ptrs(self.U, c0, c1), [r] * cnt,
+                                            self.rank[c0:c1]))
+        E.gemm_strided_batched(LO, self.U[c0:c1], self.V[c0:c1])
 
     @staticmethod
     def _ptrs(T, lo, hi):

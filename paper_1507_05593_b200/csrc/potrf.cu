@@ -10,6 +10,7 @@
 // substitution.  Pivot failure follows LAPACK dpotrf: info = 1-based column of the
 // first pivot that is not > 0 (NaN included); the failing matrix is then skipped.
 // Reference: kernels.py:22-39 (dense_cholesky), kernels.py:42-64 (tri_solve).
+#include <cstdlib>
 #include <vector>
 #include "common.cuh"
 
@@ -144,6 +145,9 @@ inline rsc_gemm_problem make_prob(const double *A, int lda, const double *B, int
 
 }  // namespace
 
+int rsc_potrf_fused(int count, double *const *A, const int *n, const int *lda, double *const *Dinv,
+                    int *info_dev, cudaStream_t s);
+
 extern "C" int rsc_potrf_batched(int count, double *const *A, const int *n, const int *lda,
                                  double *const *Dinv, int *info_dev, void *stream) {
     if (count < 0) return -1;
@@ -160,6 +164,7 @@ extern "C" int rsc_potrf_batched(int count, double *const *A, const int *n, cons
         maxn = n[i] > maxn ? n[i] : maxn;
     }
     cudaMemsetAsync(info_dev, 0, sizeof(int) * count, s);
+    if (maxn <= 256 && !getenv("RSC_POTRF_UNFUSED")) return rsc_potrf_fused(count, A, n, lda, Dinv, info_dev, s);
     const int steps = (maxn + NB - 1) / NB;
     std::vector<rsc_gemm_problem> probs;
     probs.reserve(count);

@@ -303,3 +303,50 @@ def test_trsm_left_shapes(cuda, n):
             got = b.cpu().numpy()
             assert relerr(got[:, :m], ref) < 1e-11
             assert np.array_equal(got[:, m:], B[:, m:])  # columns past m untouched
+
+
+def test_potrf_fused_batch_mixed_sizes_lda_and_failures(cuda):
+    """One batched call over orders 1..256 (the fused one-CTA path), odd and padded
+    leading dimensions, failing pivots in several 64-blocks: L vs numpy (lower, upper
+    zeroed), the stored inverse diagonal blocks, and LAPACK-style 1-based info."""
+    import torch
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(7)
+    sizes = [1, 2, 7, 31, 63, 64, 65, 96, 127, 128, 129, 191, 200, 255, 256, 256, 100, 130]
+    fail_at = {2: 0, 12: 5, 13: 70, 14: 255, 16: 64}  # batch index -> 0-based pivot
+    mats, lds, ptrs, dinv = [], [], [], []
+    for i, n in enumerate(sizes):
+        G = rng.standard_normal((n, n))
+        S = G @ G.T / max(n, 1) + np.eye(n)
+        if i in fail_at:
+            p = fail_at[i]
+            S[p, p] = -1.0 if p == 0 else S[p, p] - 1e6
+        ld = n + (i % 3)  # odd / padded leading dimensions
+        buf = np.full((n, ld), np.nan)
+        buf[:, :n] = S
+        t = E.to_dev(buf)
+        mats.append((S, t))
+        lds.append(ld)
+        ptrs.append(t.data_ptr())
+        d = torch.full((max(n, 1), 64), float("nan"), dtype=torch.float64, device="cuda")
+        dinv.append(d)
+    info = torch.zeros(len(sizes), dtype=torch.int32, device="cuda")
+    E.potrf_batched(ptrs, sizes, lds, [d.data_ptr() for d in dinv], info)
+    torch.cuda.synchronize()
+    info = info.cpu().numpy()
+    for i, (n, (S, t)) in enumerate(zip(sizes, mats)):
+        if i in fail_at:
+            assert info[i] == fail_at[i] + 1, (i, n, info[i])
+            continue
+        assert info[i] == 0, (i, n, info[i])
+        L = t.cpu().numpy()[:, :n]
+        Lref = np.linalg.cholesky(S)
+        assert relerr(L, Lref) < 1e-13, (i, n, relerr(L, Lref))
+        D = dinv[i].cpu().numpy()
+        for j0 in range(0, n, 64):
+            nb = min(64, n - j0)
+            blk = D[j0:j0 + nb, :]
+            inv = np.linalg.inv(Lref[j0:j0 + nb, j0:j0 + nb])
+            assert relerr(blk[:, :nb], inv) < 1e-12, (i, n, j0)
+            assert np.all(blk[:, nb:] == 0.0) and np.all(np.triu(blk[:, :nb], 1) == 0.0)
