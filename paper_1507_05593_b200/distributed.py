@@ -104,3 +104,235 @@ def allreduce_partial(tensor, group=None):
 
     dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
     return tensor
+
+
+# ---------------------------------------------------------------------------
+# moving factor blocks between ranks
+
+
+class _Packer:
+    """Pickle an object graph with its tensors replaced by slots of one flat
+    buffer per dtype (the buffers then travel as single collectives; the host only
+    carries the small structural payload)."""
+
+    def __init__(self):
+        self.slots = {}    # id(tensor) -> slot
+        self.tensors = []  # slot -> tensor
+
+    def persistent_id(self, obj):
+        import torch
+
+        if isinstance(obj, torch.Tensor):
+            k = self.slots.get(id(obj))
+            if k is None:
+                k = self.slots[id(obj)] = len(self.tensors)
+                self.tensors.append(obj)
+            return ("rsc_tensor", k)
+        return None
+
+    def dumps(self, obj):
+        import io
+        import pickle
+
+        f = io.BytesIO()
+        p = pickle.Pickler(f, protocol=pickle.HIGHEST_PROTOCOL)
+        p.persistent_id = self.persistent_id
+        p.dump(obj)
+        return f.getvalue()
+
+
+def pack_tensors(obj, device):
+    """obj -> (payload bytes, layout, {dtype name: flat buffer})."""
+    import torch
+
+    pk = _Packer()
+    payload = pk.dumps(obj)
+    groups, layout = {}, []
+    for t in pk.tensors:
+        key = str(t.dtype).replace("torch.", "")
+        lst = groups.setdefault(key, [])
+        off = sum(x.numel() for x in lst)
+        lst.append(t.reshape(-1))
+        layout.append((key, off, tuple(t.shape)))
+    bufs = {k: torch.cat(v) if v else torch.empty(0) for k, v in groups.items()}
+    sizes = {k: (int(b.numel()), k) for k, b in bufs.items()}
+    return payload, layout, sizes, bufs
+
+
+def unpack_tensors(payload, layout, bufs):
+    import io
+    import pickle
+
+    views = []
+    for key, off, shape in layout:
+        n = 1
+        for d in shape:
+            n *= d
+        views.append(bufs[key][off:off + n].view(shape))
+
+    up = pickle.Unpickler(io.BytesIO(payload))
+    up.persistent_load = lambda pid: views[pid[1]]
+    return up.load()
+
+
+def _bcast(buf, src, group):
+    """Broadcast a (device) tensor; gloo groups stage CUDA tensors through the host."""
+    import torch.distributed as dist
+
+    if buf.is_cuda and dist.get_backend(group) == "gloo":
+        h = buf.cpu()
+        dist.broadcast(h, src, group=group)
+        if dist.get_rank(group) != src:
+            buf.copy_(h)
+        return
+    dist.broadcast(buf, src, group=group)
+
+
+def all_gather_blocks(obj, device, group=None):
+    """Every rank contributes an object graph holding device tensors; returns the
+    list of all ranks' objects, the remote ones rebuilt as views of one received
+    buffer per (rank, dtype) -- one broadcast per rank and dtype."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    payload, layout, sizes, bufs = pack_tensors(obj, device)
+    metas = [None] * world
+    dist.all_gather_object(metas, (payload, layout, sizes), group=group)
+    out = []
+    for src in range(world):
+        p, lay, sz = metas[src]
+        if src == rank:
+            rb = bufs
+        else:
+            rb = {k: torch.empty(n, dtype=getattr(torch, k), device=device) for k, (n, _) in sz.items()}
+        for k in sorted(sz):
+            if sz[k][0]:
+                _bcast(rb[k] if src != rank else bufs[k], src, group)
+        out.append(obj if src == rank else unpack_tensors(p, lay, rb))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the sharded factorization
+
+
+def factorize_distributed(A, config=None, coords=None, group=None, prepared=None):
+    """Multi-GPU factorize (one process per GPU, torch.distributed initialised).
+
+    Every rank runs the (deterministic) host symbolic phase, then
+      1. sweeps the units of its own nested-dissection subtrees (unit_ranks) --
+         no communication: a subtree's sources all lie inside it;
+      2. all-gathers the source panels of those units (one broadcast per rank);
+      3. sweeps the shared top separators (replicated on every rank -- every
+         product a top separator forms reads sources from all subtrees);
+      4. agrees on the earliest pivot failure in sweep order (restart protocol of
+         factor.py:702-718, identical on all ranks);
+      5. all-gathers the finished unit blocks, so every rank holds the whole factor
+         and can run the preconditioned solve.
+    Results equal the single-GPU factorization: the same kernels on the same
+    operands (the top separators' source sums are formed in the same order)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    from .errors import IndefiniteError, TooManyRestarts
+    from .factor import RankStructuredFactor, SolverConfig, _Indefinite, prepare
+    from .numeric import LevelPass
+    from .sparse import as_spd
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    A = as_spd(A)
+    if prepared is None:
+        prepared = prepare(A, config if config is not None else SolverConfig(), coords)
+        sym, plan, config, t0, t_plan0, t2 = prepared
+    else:
+        sym, plan, config, _, _, _ = prepared
+        t0 = t_plan0 = time.perf_counter()
+        sym.t_ordering = sym.t_symbolic = 0.0
+        plan.load_values(A)
+        t2 = time.perf_counter()
+    owner = unit_ranks(sym, world)
+    node_unit = {payload: u for u, (kind, payload) in enumerate(sym.units) if kind == "node"}
+    device = torch.device("cuda", torch.cuda.current_device())
+    alpha_d = config.alpha_d
+    history, restarts = [alpha_d], 0
+    while True:
+        ps = LevelPass(plan, config, alpha_d)
+        ps._by_unit = {}
+        ps._run_units(lambda u: owner[u] == rank)
+        ps.mark_phase()
+        counters_a = dict(ps.counters)
+        mine = {sid: ps.src_panel[sid] for u, sid in plan.unit_source.items()
+                if owner[u] == rank and sid in ps.src_panel}
+        remote = {}
+        for r, got in enumerate(all_gather_blocks(mine, device, group)):
+            if r != rank:
+                for sid, (raw, eff) in got.items():
+                    ps._set_source(sid, raw, eff)
+                    remote[sid] = raw
+        ps._run_units(lambda u: owner[u] == -1)
+        try:
+            ps.check_pivots()
+            cand = None
+        except _Indefinite as e:
+            cand = (e.unit, e.pivot, e.trees)
+        torch.cuda.current_stream().synchronize()
+        cands = [None] * world
+        dist.all_gather_object(cands, cand, group=group)
+        fails = [c for c in cands if c is not None]
+        if not fails:
+            break
+        unit, pivot, trees = min(fails)
+        if trees == 0:
+            raise IndefiniteError(pivot)
+        restarts += 1
+        if restarts > config.max_restarts:
+            raise TooManyRestarts(
+                f"still indefinite after {config.max_restarts} restarts (alpha_d reached {alpha_d:g})")
+        alpha_d *= config.alpha_d_growth
+        history.append(alpha_d)
+    counters_top = {k: ps.counters[k] - counters_a[k] for k in ps.counters}
+    own_units = {u: ps._by_unit[u] for u in range(len(sym.units)) if owner[u] == rank}
+    own_ranks = {k: v for k, v in ps.ranks.items() if owner[node_unit[k[1]]] == rank}
+    gathered = all_gather_blocks((own_units, own_ranks, counters_a), device, group)
+    ranks_all = dict(ps.ranks)
+    counters = dict(counters_top)
+    for r, (units_r, ranks_r, cnt_r) in enumerate(gathered):
+        for k in counters:
+            counters[k] += cnt_r[k]
+        if r != rank:
+            ps._by_unit.update(units_r)
+            ranks_all.update(ranks_r)
+    # price the top separators' products with remote panels at the owners' ranks
+    src_key = {sid: ("off", sym.units[u][1]) for u, sid in plan.unit_source.items()
+               if sym.units[u][0] == "node"}
+    ps.extra_kept = {int(raw.data_ptr()): ranks_all[src_key[sid]] for sid, raw in remote.items()
+                     if sid in src_key and src_key[sid] in ranks_all}
+    ps._finalize_ranks(ps._last_info)
+    flops_a = [0.0] * world
+    dist.all_gather_object(flops_a, ps.flops_phase_a, group=group)
+    t3 = time.perf_counter()
+    F = RankStructuredFactor(A.n, sym, plan, config)
+    F.units = [ps._by_unit[u] for u in range(len(sym.units))]
+    F._mem = (ps.P, gathered)
+    F.ranks = ranks_all
+    part = sym.partition
+    st = F.stats
+    st.n, st.nnz_lower = A.n, A.nnz_lower
+    st.supernodes = part.count
+    st.separator_supernodes = int(part.is_separator.sum())
+    st.interior_block_count = len(plan.interior)
+    st.compressed_offdiag = counters["compressed_off"]
+    st.compressed_diag = counters["compressed_diag"]
+    st.dense_fallback = counters["dense_fallback"]
+    st.stored_scalars = F.stored_scalars()
+    st.restarts = restarts
+    st.alpha_d_final = alpha_d
+    st.alpha_d_history = history
+    st.model_gflop = (sum(flops_a) + ps.flops - ps.flops_phase_a) / 1e9
+    st.phase_times = {"ordering": sym.t_ordering, "symbolic": sym.t_symbolic + (t2 - t_plan0),
+                      "numeric": t3 - t2, "total": t3 - t0}
+    F.world = world
+    return F

@@ -376,11 +376,14 @@ class NumericPass:
             Ys.append(self._dense_from_csr(A_off, off_rows.size, c1 - c0))
         return Ls, Ys
 
-    def factor_interiors(self, defer=False):
+    def factor_interiors(self, defer=False, keep=None):
         """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
         Y_B = A(off_rows, C_B) L_B^{-T} by one batched TRSM.  defer=True records the
-        POTRF info words as pending pivot checks instead of reading them back."""
+        POTRF info words as pending pivot checks instead of reading them back;
+        keep(u) restricts the batch (multi-GPU: the rank's own subtrees)."""
         ints = self.np.interior
+        if keep is not None:
+            ints = [x for x in ints if keep(x[0])]
         self.first_interior_failure = None
         if not ints:
             return {}

@@ -713,16 +713,28 @@ class LevelPass(NumericPass):
 
     # -- the sweep ------------------------------------------------------------------
     def _run(self):
+        self._by_unit = {}
+        self._run_units(None)
+        self.units = [self._by_unit[u] for u in range(len(self.sym.units))]
+
+    def _run_units(self, keep):
+        """Sweep the units u with keep(u) (all when keep is None), in level order.
+        The multi-GPU driver (distributed.factorize_distributed) runs the owned
+        subtree units first and the shared top separators after the source exchange."""
         part = self.sym.partition
         cfg = self.cfg
-        interiors = self.factor_interiors(defer=True)
-        by_unit = {}
+        interiors = self.factor_interiors(defer=True, keep=keep)
+        by_unit = self._by_unit
         for u, iu in interiors.items():
             by_unit[u] = iu
             sid = self.np.unit_source.get(u)
             if sid is not None:
                 self._set_source(sid, iu.off, iu.off)
         for level in self.np.node_levels:
+            if keep is not None:
+                level = [u for u in level if keep(u)]
+                if not level:
+                    continue
             self.S.reset()
             nodes, trees, dense, off_dense, off_tree, comp, comp_r = [], [], [], [], [], [], []
             for u in level:
@@ -790,7 +802,6 @@ class LevelPass(NumericPass):
                 sid = self.np.unit_source.get(n.u)
                 if sid is not None:
                     self._set_source(sid, *_raw_eff(n.off))
-        self.units = [by_unit[u] for u in range(len(self.sym.units))]
 
     def _finalize_ranks(self, info):
         """Trim every compressed block to its kept rank (views; the padded columns are
@@ -813,6 +824,10 @@ class LevelPass(NumericPass):
             lr.V, lr.U, lr.E, lr.k = V[:, :k], U[:, :k], Ef[:, :k], k
             self.ranks[key] = k
         self.flops = self._flops_padded
+        kept.update(getattr(self, "extra_kept", {}))  # panels received from other ranks
+        mark = getattr(self, "phase_mark", None)  # (padded flops, term count) after phase A
+        if mark is not None:
+            self.flops_phase_a = mark[0]
         if self._wt is not None and kept:
             coef, w, wb, r, rb = self._wt
 
@@ -822,13 +837,21 @@ class LevelPass(NumericPass):
                 return np.where(kk >= 0, kk, width)
 
             wt, rt = look(wb, w), look(rb, r)
-            self.flops -= float(np.sum(coef * (w * r - wt * rt)))
+            d = coef * (w * r - wt * rt)
+            self.flops -= float(np.sum(d))
+            if mark is not None:
+                self.flops_phase_a = mark[0] - float(np.sum(d[: mark[1]]))
+
+    def mark_phase(self):
+        """Record the flop-model position after the multi-GPU subtree phase."""
+        self.phase_mark = (self.flops, int(sum(len(t[0]) for t in self._wterms)))
 
     def check_pivots(self):
         """One readback of the pass's device words (POTRF info + QR ranks): trim the
         compressed blocks, then resolve every recorded pivot failure (the earliest unit
         in sweep order wins)."""
         info = self.ibuf[: self.ipos].cpu().numpy()
+        self._last_info = info
         self._finalize_ranks(info)
         worst = None
         for rec in self.pending:

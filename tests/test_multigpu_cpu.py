@@ -96,3 +96,58 @@ def test_shard_blocks_cover_batch():
         spans = [shard_blocks(512, r, world) for r in range(world)]
         assert spans[0][0] == 0 and spans[-1][1] == 512
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _block_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1507_05593_b200.distributed import all_gather_blocks
+        from paper_1507_05593_b200.factor import DenseTri, DevLR, NodeUnit
+
+        g = torch.Generator().manual_seed(rank)
+        L = torch.randn(5, 5, generator=g, dtype=torch.float64)
+        V = torch.randn(7, 6, generator=g, dtype=torch.float64)[:, :3]  # trimmed (non-contiguous) view
+        U = torch.randn(4, 3, generator=g, dtype=torch.float64)
+        un = NodeUnit(10 + rank, rank, 0, 4, np.arange(rank, rank + 7))
+        un.diag = DenseTri(L, torch.zeros(5, 64, dtype=torch.float64))
+        un.off = DevLR(V, U, V * 2)
+        obj = {"unit": un, "twice": (U, U), "ranks": {("off", rank): 3}, "ints": torch.arange(rank + 2, dtype=torch.int32)}
+        got = all_gather_blocks(obj, torch.device("cpu"))
+        res = []
+        for r, o in enumerate(got):
+            g = torch.Generator().manual_seed(r)
+            L = torch.randn(5, 5, generator=g, dtype=torch.float64)
+            V = torch.randn(7, 6, generator=g, dtype=torch.float64)[:, :3]
+            U = torch.randn(4, 3, generator=g, dtype=torch.float64)
+            u = o["unit"]
+            res.append(bool(torch.equal(u.diag.L, L) and torch.equal(u.off.V, V) and torch.equal(u.off.E, 2 * V)
+                            and torch.equal(u.off.U, U) and u.u == 10 + r and np.array_equal(u.rows, np.arange(r, r + 7))
+                            and o["twice"][0] is o["twice"][1] and o["ranks"] == {("off", r): 3}
+                            and torch.equal(o["ints"], torch.arange(r + 2, dtype=torch.int32))))
+        out.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_all_gather_blocks_gloo_world2():
+    """Factor blocks (unit records holding tensors, trimmed views, shared tensors,
+    int tensors) travel between ranks as one flat buffer per dtype + a pickled
+    structure, and come back identical on every rank."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok in res:
+        assert ok == [True, True], (rank, ok)
