@@ -47,7 +47,7 @@ __device__ __forceinline__ double col_norm2(const double *c, int r0, int m, int 
 // forms the reflector on that column and publishes tau; (2) every warp applies it to
 // its own unchosen columns and downdates their norms.  dorg2r runs on the first
 // `rank` positions with the same indirection.
-template <bool SMEM>
+template <bool SMEM, int RPL>
 __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant__ QrArgs args,
                                                            double *work, int *rank_out) {
     extern __shared__ __align__(16) double dyn[];
@@ -126,6 +126,105 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         const double tau_i = tau[i];
         // apply H^T to the unchosen columns (positions > i, round-robin over warps for
         // balance) and downdate their norms
+        if constexpr (RPL > 0) {
+            // m <= 32 RPL: the reflector is held in registers for every column of the
+            // step, rows unrolled at compile time (same per-lane summation order)
+            double vr[RPL];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int r = lane + 32 * q;
+                vr[q] = (r > i && r < m) ? ci[r] : 0.0;
+            }
+            // four columns of the warp at a time, interleaved: their loads, dot
+            // products, butterflies and downdates overlap instead of running back to back
+            constexpr int CB = 4;
+            for (int jp0 = i + 1 + warp; jp0 < k; jp0 += CB * nw) {
+                int jj[CB];
+                bool on[CB];
+                double *cj[CB];
+                double x[CB][RPL], cji[CB], w[CB];
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    const int jp = jp0 + c * nw;
+                    on[c] = jp < k;
+                    jj[c] = on[c] ? pos2phys[jp] : 0;
+                    cj[c] = W + (long long)jj[c] * ldw;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        const int r = lane + 32 * q;
+                        x[c][q] = (on[c] && r < m) ? cj[c][r] : 0.0;
+                    }
+                    cji[c] = on[c] ? cj[c][i] : 0.0;
+                    w[c] = 0.0;
+                }
+                if (tau_i != 0.0) {
+#pragma unroll
+                    for (int c = 0; c < CB; ++c)
+#pragma unroll
+                        for (int q = 0; q < RPL; ++q) w[c] = fma(vr[q], x[c][q], w[c]);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int c = 0; c < CB; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+                    for (int c = 0; c < CB; ++c) {
+                        if (!on[c]) continue;
+                        const double f = tau_i * (w[c] + cji[c]);
+#pragma unroll
+                        for (int q = 0; q < RPL; ++q) {
+                            const int r = lane + 32 * q;
+                            if (r > i && r < m) {
+                                x[c][q] = fma(-f, vr[q], x[c][q]);
+                                cj[c][r] = x[c][q];
+                            }
+                        }
+                        cji[c] -= f;
+                        if (lane == 0) cj[c][i] = cji[c];
+                    }
+                }
+                bool redo[CB], any_redo = false;
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    redo[c] = false;
+                    if (!on[c]) continue;
+                    const double v1 = vn1[jj[c]];
+                    if (v1 == 0.0) continue;
+                    double temp = fabs(cji[c]) / v1;
+                    temp = 1.0 - temp * temp;
+                    temp = temp < 0.0 ? 0.0 : temp;
+                    const double ratio = v1 / vn2[jj[c]];
+                    const double temp2 = temp * ratio * ratio;
+                    if (temp2 <= TOL3Z) {
+                        redo[c] = any_redo = true;
+                    } else if (lane == 0) {
+                        vn1[jj[c]] = v1 * sqrt(temp);
+                    }
+                }
+                if (any_redo) {  // uniform: every lane evaluated the same values
+                    double nv[CB];
+#pragma unroll
+                    for (int c = 0; c < CB; ++c) {
+                        nv[c] = 0.0;
+#pragma unroll
+                        for (int q = 0; q < RPL; ++q) {
+                            const int r = lane + 32 * q;
+                            if (r > i && r < m) nv[c] = fma(x[c][q], x[c][q], nv[c]);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int c = 0; c < CB; ++c) nv[c] += __shfl_xor_sync(0xffffffffu, nv[c], o);
+#pragma unroll
+                    for (int c = 0; c < CB; ++c) {
+                        if (!redo[c]) continue;
+                        const double x2 = (i + 1 < m) ? sqrt(nv[c]) : 0.0;
+                        if (lane == 0) { vn1[jj[c]] = x2; vn2[jj[c]] = x2; }
+                    }
+                }
+                __syncwarp();
+            }
+        } else {
         for (int jp = i + 1 + warp; jp < k; jp += nw) {
             const int j = pos2phys[jp];
             double *cj = W + (long long)j * ldw;
@@ -156,6 +255,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
             }
             __syncwarp();
         }
+        }
         __syncthreads();
     }
 
@@ -174,6 +274,38 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
     __syncthreads();
     const int rank = rank_s;
 
+    double *Q = args.Q[b];
+    const int ldq = args.ldq[b];
+    if constexpr (RPL > 0) {
+        // Q column j = H_0 H_1 ... H_j e_j (what dorg2r forms for column j, in the same
+        // reflector order), one warp per column, no CTA barriers: the reflectors stay
+        // in the tile, read-only
+        for (int j = warp; j < rank; j += nw) {
+            double qv[RPL];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) qv[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+            for (int i = j; i >= 0; --i) {
+                const double *vi = W + (long long)pos2phys[i] * ldw;
+                const double ti = tau[i];
+                double vr[RPL], d = 0.0;
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    const int r = lane + 32 * q;
+                    vr[q] = (r > i && r < m) ? vi[r] : (r == i ? 1.0 : 0.0);
+                    d = fma(vr[q], qv[q], d);
+                }
+                d = ti * warp_sum(d);
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) qv[q] = fma(-d, vr[q], qv[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int r = lane + 32 * q;
+                if (r < m) Q[(long long)r * ldq + j] = qv[q];
+            }
+        }
+        return;
+    }
     // dorg2r on positions 0..rank-1 (storage of position i = physical pos2phys[i])
     for (int i = rank - 1; i >= 0; --i) {
         double *ci = W + (long long)pos2phys[i] * ldw;
@@ -197,8 +329,6 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
         if (t == 0) ci[i] = 1.0 - ti;
         __syncthreads();
     }
-    double *Q = args.Q[b];
-    const int ldq = args.ldq[b];
     for (long long e = t; e < (long long)m * rank; e += QR_THREADS) {
         const int r = (int)(e / rank), j = (int)(e % rank);
         Q[(long long)r * ldq + j] = W[(long long)pos2phys[j] * ldw + r];
@@ -570,8 +700,13 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
     cudaStream_t s = (cudaStream_t)stream;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(qrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(qrcp_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SMEM_BYTES_MAX);
+#define RSC_QR_ATTR(R) \
+    cudaFuncSetAttribute(qrcp_kernel<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES_MAX);
+        RSC_QR_ATTR(1) RSC_QR_ATTR(2) RSC_QR_ATTR(3) RSC_QR_ATTR(4)
+        RSC_QR_ATTR(5) RSC_QR_ATTR(6) RSC_QR_ATTR(7) RSC_QR_ATTR(8)
+#undef RSC_QR_ATTR
         cudaFuncSetAttribute(qrcp_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, RQ_SMEM);
         attr_set = true;
     }
@@ -606,9 +741,22 @@ extern "C" int rsc_qrcp_batched(int count, double *const *G, const int *m, const
                 if (!smem) woff += ((sz * 8 + 255) / 256) * 256;
             }
             if (smem) {
-                qrcp_kernel<true><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, nullptr, rank_dev);
+                int maxm = 0;
+                for (int c = 0; c < qa.count; ++c) maxm = qa.m[c] > maxm ? qa.m[c] : maxm;
+                const int rpl = (maxm + 31) / 32;
+                switch (rpl) {
+#define RSC_QR_CASE(R)                                                                           \
+    case R:                                                                                      \
+        qrcp_kernel<true, R><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, nullptr, rank_dev); \
+        break;
+                    RSC_QR_CASE(1) RSC_QR_CASE(2) RSC_QR_CASE(3) RSC_QR_CASE(4)
+                    RSC_QR_CASE(5) RSC_QR_CASE(6) RSC_QR_CASE(7) RSC_QR_CASE(8)
+#undef RSC_QR_CASE
+                    default:
+                        qrcp_kernel<true, 0><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, nullptr, rank_dev);
+                }
             } else {
-                qrcp_kernel<false><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, (double *)work_dev, rank_dev);
+                qrcp_kernel<false, 0><<<qa.count, QR_THREADS, (size_t)maxsz, s>>>(qa, (double *)work_dev, rank_dev);
             }
             RSC_CHECK_LAUNCH();
         }
