@@ -616,14 +616,44 @@ __global__ void __launch_bounds__(RQ_WARPS * 32) qrcp_reg_kernel(const __grid_co
     }
     __syncthreads();
     const int rank = rank_s;
-    st.form_range<1>(32, rank, rank, v, tau);
-    st.form_range<0>(0, rank < 32 ? rank : 32, rank, v, tau);
-    // Q[:, :rank] through the tile (columns rank..k-1 zero), coalesced store
+    // Q column j = H_0 ... H_j e_j (dorg2r's reflector order), formed per warp with no
+    // CTA barriers: the reflectors go to the tile (column = position), every warp
+    // builds its Q columns in registers, then they replace the reflectors in the tile
 #pragma unroll
     for (int s = 0; s < RQ_SLOTS; ++s) {
         if (st.pos[s] >= rank) continue;
 #pragma unroll
         for (int q = 0; q < RQ_ROWS; ++q) tile[(lane + 32 * q) * RQ_LDT + st.pos[s]] = st.a[s][q];
+    }
+    __syncthreads();
+    double qv[RQ_SLOTS][RQ_ROWS];
+#pragma unroll
+    for (int c = 0; c < RQ_SLOTS; ++c) {
+        const int j = warp + RQ_WARPS * c;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) qv[c][q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+        if (j >= rank) continue;
+        for (int i = j; i >= 0; --i) {
+            const double ti = tau[i];
+            double vr[RQ_ROWS], d = 0.0;
+#pragma unroll
+            for (int q = 0; q < RQ_ROWS; ++q) {
+                const int r = lane + 32 * q;
+                vr[q] = r > i ? tile[r * RQ_LDT + i] : (r == i ? 1.0 : 0.0);
+                d = fma(vr[q], qv[c][q], d);
+            }
+            d = ti * warp_sum(d);
+#pragma unroll
+            for (int q = 0; q < RQ_ROWS; ++q) qv[c][q] = fma(-d, vr[q], qv[c][q]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < RQ_SLOTS; ++c) {
+        const int j = warp + RQ_WARPS * c;
+        if (j >= rank) continue;
+#pragma unroll
+        for (int q = 0; q < RQ_ROWS; ++q) tile[(lane + 32 * q) * RQ_LDT + j] = qv[c][q];
     }
     __syncthreads();
     double *Q = args.Q[b];
