@@ -18,7 +18,10 @@
 //
 // Q is formed afterwards (qr_form_q_kernel): column j of Q is H_0 ... H_j e_j
 // applied right-to-left (dorg2r order), one warp per column.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 #include "common.cuh"
 
@@ -217,6 +220,292 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
         for (long long e = t; e < (long long)ldw * (c1 - c0); e += CT) w.cols[(long long)c0 * ldw + e] = cols[e];
     if (lb == 0)
         for (int j = t; j < k; j += CT) w.perm[j] = pos2phys[j];
+}
+
+
+// ---- thread-block-cluster QRCP ------------------------------------------------
+// The same algorithm for sketches that fit the shared memory of one cluster (<= 16
+// CTAs): CTA b of the cluster owns physical columns [b*cpc, (b+1)*cpc) as in
+// mqrcp_kernel, but the per-matrix state lives in every CTA's shared memory and
+// moves through distributed shared memory: the owner of the pivot column PUSHES the
+// reflector, tau and beta into every CTA's buffers, every CTA pushes the downdated
+// norms of its columns into every replica, and the two synchronisations per column
+// are hardware cluster barriers (release/acquire) instead of global-memory counters
+// -- the pivot search then reads only local shared memory.
+constexpr int QC_MAXC = 8;  // 16-CTA clusters measured slower than the cooperative kernel
+
+struct QcArgs {
+    int count;
+    int C;
+    MatDesc d[MAXM];
+};
+
+inline size_t cluster_smem(int m, int k, int cpc) {
+    return (size_t)cpc * (size_t)(m | 1) * 8 + (size_t)m * 8 + 4 * (size_t)k * 8 + 2 * sizeof(int) * (size_t)k + 16;
+}
+
+__device__ unsigned long long qc_phase_cycles[32];  // RSC_QR_TIMING diagnostics
+
+// Update of this warp's owned, still unchosen columns for Householder step i
+// (apply H_i^T, dlaqp2 downdate, push the norms into every replica).  CB columns
+// are processed interleaved; with RPL > 0 (m <= 32 RPL) rows are unrolled and the
+// reflector sits in registers.
+template <int RPL, int CB, class Cl>
+__device__ __forceinline__ void qc_update(Cl &cl, int C, int i, int m, int k, int ldw, int lb, int nloc,
+                                          double *cols, const double *v, double tau_i, double *vn1,
+                                          double *vn2, const int *posof, int warp, int lane, int nw) {
+    constexpr int R = RPL > 0 ? RPL : 1;
+    double vr[R];
+    if (RPL > 0) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int r = lane + 32 * q;
+            vr[q] = (r > i && r < m) ? v[r] : 0.0;
+        }
+    }
+    for (int jl0 = warp; jl0 < nloc; jl0 += CB * nw) {
+        int phys[CB];
+        bool on[CB];
+        double *cj[CB];
+        double x[CB][R], cji[CB], w[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            const int jl = jl0 + c * nw;
+            phys[c] = lb + C * jl;
+            on[c] = jl < nloc && phys[c] < k && posof[phys[c]] > i;
+            cj[c] = cols + (long long)(on[c] ? jl : 0) * ldw;
+            cji[c] = on[c] ? cj[c][i] : 0.0;
+            w[c] = 0.0;
+            if (RPL > 0) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int r = lane + 32 * q;
+                    x[c][q] = (on[c] && r < m) ? cj[c][r] : 0.0;
+                }
+            }
+        }
+        if (tau_i != 0.0) {
+            if (RPL > 0) {
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+#pragma unroll
+                    for (int q = 0; q < R; ++q) w[c] = fma(vr[q], x[c][q], w[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (on[c])
+                        for (int r = i + 1 + lane; r < m; r += 32) w[c] += v[r] * cj[c][r];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int c = 0; c < CB; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                const double f = tau_i * (w[c] + cji[c]);
+                if (RPL > 0) {
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int r = lane + 32 * q;
+                        if (r > i && r < m) {
+                            x[c][q] = fma(-f, vr[q], x[c][q]);
+                            cj[c][r] = x[c][q];
+                        }
+                    }
+                } else {
+                    for (int r = i + 1 + lane; r < m; r += 32) cj[c][r] -= f * v[r];
+                }
+                cji[c] -= f;
+                if (lane == 0) cj[c][i] = cji[c];
+            }
+        }
+        bool redo[CB], any_redo = false;
+        double nv1[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            redo[c] = false;
+            nv1[c] = -1.0;
+            if (!on[c]) continue;
+            const double v1 = vn1[phys[c]];
+            if (v1 == 0.0) continue;
+            double temp = fabs(cji[c]) / v1;
+            temp = 1.0 - temp * temp;
+            temp = temp < 0.0 ? 0.0 : temp;
+            const double ratio = v1 / vn2[phys[c]];
+            const double temp2 = temp * ratio * ratio;
+            if (temp2 <= TOL3Z) redo[c] = any_redo = true;
+            else nv1[c] = v1 * sqrt(temp);
+        }
+        if (any_redo) {  // uniform across the warp
+            __syncwarp();
+            double nv[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                nv[c] = 0.0;
+                if (!redo[c]) continue;
+                if (RPL > 0) {
+#pragma unroll
+                    for (int q = 0; q < R; ++q) {
+                        const int r = lane + 32 * q;
+                        if (r > i && r < m) nv[c] = fma(x[c][q], x[c][q], nv[c]);
+                    }
+                } else {
+                    for (int r = i + 1 + lane; r < m; r += 32) nv[c] += cj[c][r] * cj[c][r];
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int c = 0; c < CB; ++c) nv[c] += __shfl_xor_sync(0xffffffffu, nv[c], o);
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!redo[c]) continue;
+                const double x2 = (i + 1 < m) ? sqrt(nv[c]) : 0.0;
+                if (lane < C) {
+                    cl.map_shared_rank(vn1, lane)[phys[c]] = x2;
+                    cl.map_shared_rank(vn2, lane)[phys[c]] = x2;
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (nv1[c] >= 0.0 && lane < C) cl.map_shared_rank(vn1, lane)[phys[c]] = nv1[c];
+        __syncwarp();
+    }
+}
+
+// RPL > 0: m <= 32 RPL (rows unrolled); 0: any m.  Columns are dealt cyclically to
+// the CTAs of the cluster (physical column j -> CTA j mod C), so the pivoting, which
+// retires columns in data order, keeps the CTAs' remaining work balanced.
+template <bool TIMING, int RPL>
+__global__ void __launch_bounds__(CT) qrcp_cluster_kernel(const __grid_constant__ QcArgs a) {
+    namespace cg = cooperative_groups;
+    long long tp = TIMING ? clock64() : 0;
+    auto mark = [&](int ph) {
+        if (TIMING && threadIdx.x == 0 && blockIdx.x == 0) {
+            const long long now = clock64();
+            atomicAdd(&qc_phase_cycles[ph], (unsigned long long)(now - tp));
+            tp = now;
+        }
+    };
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[32];
+    __shared__ int piv_s;
+    const int C = a.C;
+    const int g = blockIdx.x / C;
+    const int lb = (int)cl.block_rank();
+    const MatDesc &d = a.d[g];
+    const Ws w = carve(d);
+    const int m = d.m, k = d.k, ldw = d.ldw, cpc = d.cpc;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = CT / 32;
+    const int nloc = (k - lb + C - 1) / C;  // owned columns: lb, lb + C, ...
+    double *cols = sm;
+    double *v = cols + (size_t)cpc * ldw;
+    double *vn1 = v + m, *vn2 = vn1 + k, *tau = vn2 + k, *diagR = tau + k;
+    int *pos2phys = reinterpret_cast<int *>(diagR + k);
+    int *posof = pos2phys + k;
+
+    for (long long e = t; e < (long long)m * nloc; e += CT) {
+        const int r = (int)(e / nloc), jl = (int)(e % nloc);
+        cols[(long long)jl * ldw + r] = d.G[(long long)r * d.ldg + lb + C * jl];
+    }
+    for (int j = t; j < k; j += CT) { pos2phys[j] = j; posof[j] = j; }
+    cl.sync();  // every CTA of the cluster is running before any DSMEM store
+    for (int jl = warp; jl < nloc; jl += nw) {
+        const double *cj = cols + (long long)jl * ldw;
+        double s = 0.0;
+        for (int r = lane; r < m; r += 32) s += cj[r] * cj[r];
+        s = sqrt(warp_sum(s));
+        if (lane < C) {
+            cl.map_shared_rank(vn1, lane)[lb + C * jl] = s;
+            cl.map_shared_rank(vn2, lane)[lb + C * jl] = s;
+        }
+    }
+    cl.sync();
+
+    const int kmin = m < k ? m : k;
+    for (int i = 0; i < kmin; ++i) {
+        // 1. pivot from the local replica of the norms (identical in every CTA)
+        if (warp == 0) {
+            double best = -1.0;
+            int bp = k;
+            for (int j = i + lane; j < k; j += 32) {
+                const double vv = vn1[pos2phys[j]];
+                if (vv > best) { best = vv; bp = j; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+            }
+            if (lane == 0) {
+                if (bp >= k) bp = i;  // NaN norms (failed upstream pivot): keep the order
+                const int ci = pos2phys[i], cp = pos2phys[bp];
+                pos2phys[i] = cp; pos2phys[bp] = ci;
+                posof[cp] = i; posof[ci] = bp;
+                piv_s = cp;
+            }
+        }
+        __syncthreads();
+        mark(0);
+        const int pc = piv_s;
+        // 2. the owner forms the reflector (dlarfg) and pushes it to every CTA
+        if (pc % C == lb) {
+            double *ci = cols + (long long)(pc / C) * ldw;
+            double part = 0.0;
+            for (int r = i + 1 + t; r < m; r += CT) part += ci[r] * ci[r];
+            const double xnorm = sqrt(block_sum(part, red));
+            const double alpha = ci[i];
+            double tau_i = 0.0, beta = alpha, scal = 0.0;
+            if (xnorm != 0.0) {
+                beta = -copysign(hypot(alpha, xnorm), alpha);
+                tau_i = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            __syncthreads();
+            for (int r = i + 1 + t; r < m; r += CT) {
+                const double x = (xnorm != 0.0) ? ci[r] * scal : ci[r];
+                ci[r] = x;
+                for (int q = 0; q < C; ++q) cl.map_shared_rank(v, q)[r] = x;
+            }
+            if (t < C) {
+                cl.map_shared_rank(tau, t)[i] = tau_i;
+                cl.map_shared_rank(diagR, t)[i] = beta;
+            }
+            if (t == 0) ci[i] = beta;
+        }
+        mark(1);
+        cl.sync();
+        mark(2);
+        // 3. apply H_i^T to the unchosen owned columns, downdate and push their norms
+        const long long tw0 = TIMING ? clock64() : 0;
+        qc_update<RPL, 4>(cl, C, i, m, k, ldw, lb, nloc, cols, v, tau[i], vn1, vn2, posof, warp, lane, nw);
+        if (TIMING && lane == 0 && blockIdx.x < 2)
+            atomicAdd(&qc_phase_cycles[8 + 8 * blockIdx.x + warp], (unsigned long long)(clock64() - tw0));
+        mark(3);
+        cl.sync();
+        mark(4);
+    }
+    // spill the reflector columns, the permutation, tau and R's diagonal to the
+    // workspace the Q formation reads
+    for (long long e = t; e < (long long)ldw * nloc; e += CT) {
+        const int jl = (int)(e / ldw), r = (int)(e % ldw);
+        w.cols[(long long)(lb + C * jl) * ldw + r] = cols[e];
+    }
+    if (lb == 0) {
+        for (int j = t; j < k; j += CT) {
+            w.perm[j] = pos2phys[j];
+            w.vn1[j] = vn1[j];
+            w.vn2[j] = vn2[j];
+        }
+        for (int j = t; j < kmin; j += CT) {
+            w.tau[j] = tau[j];
+            w.diagR[j] = diagR[j];
+        }
+    }
 }
 
 struct QDesc {
@@ -523,6 +812,121 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
         cpc = (k[i] + nsm - 1) / nsm;  // global-memory columns, one group over all SMs
         plans.push_back({i, cpc, (k[i] + cpc - 1) / cpc, false, sizeof(int) * 2 * (size_t)k[i]});
     }
+    // sketches that fit one thread-block cluster: cluster kernel (DSMEM + hardware
+    // cluster barriers); the rest stays on the cooperative kernel
+    {
+        static bool cattr = false;
+        if (!cattr) {
+            for (void *f : {(void *)qrcp_cluster_kernel<false, 0>, (void *)qrcp_cluster_kernel<true, 0>,
+                            (void *)qrcp_cluster_kernel<false, 8>, (void *)qrcp_cluster_kernel<true, 8>,
+                            (void *)qrcp_cluster_kernel<false, 16>, (void *)qrcp_cluster_kernel<true, 16>}) {
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            }
+            cattr = true;
+        }
+        static thread_local QcArgs qc;
+        std::vector<std::pair<int, int>> cl_list;  // (C, plan index)
+        std::vector<size_t> cl_sm(plans.size(), 0);
+        std::vector<char> done(plans.size(), 0);
+        if (!getenv("RSC_QR_NOCLUSTER")) {
+            // smallest cluster whose shared memory holds the sketch, widened so the
+            // batch's clusters cover the SMs (fewer owned columns per CTA)
+            std::vector<int> cmin(plans.size(), 0);
+            int neligible = 0;
+            for (size_t pi = 0; pi < plans.size(); ++pi) {
+                const int i = plans[pi].i;
+                for (int C = 2; C <= QC_MAXC && C <= k[i]; ++C)
+                    if (cluster_smem(m[i], k[i], (k[i] + C - 1) / C) <= 220 * 1024) { cmin[pi] = C; break; }
+                if (cmin[pi]) ++neligible;
+            }
+            // (widening the clusters to cover all SMs measured slower: more DSMEM
+            // pushes and cluster-barrier participants per column)
+            const int cwide = 0;
+            (void)neligible;
+            for (size_t pi = 0; pi < plans.size(); ++pi) {
+                if (!cmin[pi]) continue;
+                const int i = plans[pi].i;
+                const int chi = std::max(cmin[pi], std::min(cwide, k[i] / 4));
+                for (int C = chi; C >= cmin[pi]; --C) {
+                    const int cpc = (k[i] + C - 1) / C;
+                    const size_t smb = cluster_smem(m[i], k[i], cpc);
+                    cudaLaunchConfig_t cfg = {};
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeClusterDimension;
+                    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                    cfg.gridDim = dim3(C);
+                    cfg.blockDim = dim3(CT);
+                    cfg.dynamicSmemBytes = smb;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    int ncl = 0;
+                    if (cudaOccupancyMaxActiveClusters(&ncl, (void *)qrcp_cluster_kernel<false, 0>, &cfg) != cudaSuccess ||
+                        ncl < 1) {
+                        cudaGetLastError();
+                        continue;
+                    }
+                    cl_list.push_back({C, (int)pi});
+                    cl_sm[pi] = smb;
+                    done[pi] = 1;
+                    break;
+                }
+            }
+        }
+        std::sort(cl_list.begin(), cl_list.end());
+        size_t pos = 0;
+        while (pos < cl_list.size()) {
+            const int C = cl_list[pos].first;
+            int cnt = 0;
+            size_t smb = 0;
+            while (pos < cl_list.size() && cl_list[pos].first == C && cnt < MAXM) {
+                const P &p = plans[cl_list[pos].second];
+                const int i = p.i;
+                MatDesc &d = qc.d[cnt];
+                d.G = G[i]; d.Q = Q[i];
+                d.W = reinterpret_cast<double *>(work + work_off[i]);
+                d.rank = rank_dev + i;
+                d.m = m[i]; d.k = k[i]; d.ldg = ldg[i]; d.ldq = ldq[i]; d.ldw = m[i] | 1;
+                d.cpc = (k[i] + C - 1) / C; d.nblk = C; d.blk0 = cnt * C;
+                smb = std::max(smb, cl_sm[cl_list[pos].second]);
+                ++cnt;
+                ++pos;
+            }
+            qc.count = cnt;
+            qc.C = C;
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(cnt * C);
+            cfg.blockDim = dim3(CT);
+            cfg.dynamicSmemBytes = smb;
+            cfg.stream = s;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            static const bool timing = getenv("RSC_QR_TIMING") != nullptr;
+            int maxm = 0;
+            for (int c = 0; c < cnt; ++c) maxm = std::max(maxm, qc.d[c].m);
+            cudaError_t e;
+            if (maxm <= 256)
+                e = timing ? cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<true, 8>, qc)
+                           : cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<false, 8>, qc);
+            else if (maxm <= 512)
+                e = timing ? cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<true, 16>, qc)
+                           : cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<false, 16>, qc);
+            else
+                e = timing ? cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<true, 0>, qc)
+                           : cudaLaunchKernelEx(&cfg, qrcp_cluster_kernel<false, 0>, qc);
+            rsc_count_launch();
+            if (e != cudaSuccess) return (int)e;
+            const int rc = form_q_blocked(cnt, qc.d, s);
+            if (rc) return rc;
+        }
+        std::vector<P> rest;
+        for (size_t pi = 0; pi < plans.size(); ++pi)
+            if (!done[pi]) rest.push_back(plans[pi]);
+        plans.swap(rest);
+    }
     cudaMemsetAsync(bar, 0, sizeof(unsigned) * (size_t)std::max(n, 1), s);
     static thread_local MArgs ma;
     static thread_local QArgs qa;
@@ -582,4 +986,13 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
         }
     }
     return 0;
+}
+
+extern "C" int rsc_qr_phase_cycles(unsigned long long *out8, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out8, qc_phase_cycles, 32 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(qc_phase_cycles, z, sizeof(z));
+    }
+    return (int)e;
 }
