@@ -190,6 +190,18 @@ int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_id
 int rsc_sym_postorder(long long n, const long long *parent, long long *post);
 int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *row_idx,
                       const long long *parent, const long long *post, long long *counts);
+/* Relaxed amalgamation of one gap of fundamental supernodes (symbolic.py:244-277):
+ * bounds[0..nb] fundamental boundaries, tiers (tw[i] max width or -1, tb[i] bound);
+ * writes the kept starts to out and returns their count (<0: bad argument). */
+long long rsc_sym_amalgamate(long long nb, const long long *bounds, const long long *parent,
+                             const long long *counts, int ntier, const long long *tw, const double *tb,
+                             long long *out);
+/* Row structures of the M supernodes (symbolic.py:280-306), two calls: compute
+ * returns a handle and the total row count, fetch writes ptr[M+1] and rows[total]
+ * and frees the handle. */
+void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
+                           const long long *row_idx, long long *total);
+int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows);
 /* One geometric bisection step of nested dissection (ordering.py:182-192): the
  * vertices are split at the median along the widest coordinate axis (ties by id);
  * the second half's members adjacent to the first form the separator.  indptr /

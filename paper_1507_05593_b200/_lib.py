@@ -50,6 +50,9 @@ EXPORTED = (
     "rsc_sym_etree",
     "rsc_sym_postorder",
     "rsc_sym_colcounts",
+    "rsc_sym_amalgamate",
+    "rsc_sym_rows_compute",
+    "rsc_sym_rows_fetch",
     "rsc_nd_split_geometric",
     "rsc_csr_windows",
     "rsc_pcg64_block_states",
@@ -94,6 +97,9 @@ _SIGS = {
     "rsc_sym_etree": (I, [LL, P, P, P]),
     "rsc_sym_postorder": (I, [LL, P, P]),
     "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
+    "rsc_sym_amalgamate": (LL, [LL, P, P, P, I, P, P, P]),
+    "rsc_sym_rows_compute": (ctypes.c_void_p, [LL, P, P, P, P]),
+    "rsc_sym_rows_fetch": (I, [ctypes.c_void_p, P, P]),
     "rsc_nd_split_geometric": (I, [LL, P, ctypes.c_int, P, P, P, P, P, P]),
     "rsc_csr_windows": (I, [LL, LL] + [P] * 16),
     "rsc_pcg64_block_states": (I, [I, I, P, P, P, P]),

@@ -4,6 +4,7 @@
 // (reference symbolic.py:44-151); their results are unique for a given pattern,
 // so any correct algorithm is bit-exact with the reference.
 #include <cstdint>
+#include <algorithm>
 #include <vector>
 
 extern "C" {
@@ -106,3 +107,101 @@ int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *ro
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Relaxed supernode amalgamation of one gap of fundamental supernodes
+// (symbolic.py:_amalgamate, reference symbolic.py:244-277): merge a supernode into
+// its successor while the successor is the parent of its last column and the
+// explicit-zero fraction stays under the width tier's bound.  bounds[0..nb] are the
+// fundamental boundaries; the kept starts are written to out (count returned).
+// tiers: ntier (width, bound) pairs, width < 0 = unbounded.  The fraction is the same
+// IEEE double division Python performs on the exact integers.
+extern "C" long long rsc_sym_amalgamate(long long nb, const long long *bounds, const long long *parent,
+                                        const long long *counts, int ntier, const long long *tw,
+                                        const double *tb, long long *out) {
+    if (nb < 0) return -1;
+    std::vector<long long> st, nc, nr, zr;
+    st.reserve(nb);
+    for (long long i = 0; i < nb; ++i) {
+        st.push_back(bounds[i]);
+        nc.push_back(bounds[i + 1] - bounds[i]);
+        nr.push_back(counts[bounds[i]] - (bounds[i + 1] - bounds[i]));
+        zr.push_back(0);
+    }
+    // singly linked list over the surviving supernodes (Python deletes from lists)
+    std::vector<long long> nxt(nb);
+    for (long long i = 0; i < nb; ++i) nxt[i] = i + 1;
+    long long i = 0;
+    while (i < nb && nxt[i] < nb) {
+        const long long s = nxt[i];
+        const long long last = st[i] + nc[i] - 1;
+        if (parent[last] != st[s]) { i = s; continue; }
+        const long long ns = nc[i], nt = nc[s], rs = nr[i], rt = nr[s];
+        const long long mc = ns + nt;
+        const long long tot = zr[i] + zr[s] + ns * (nt + rt - rs);
+        const double frac = (double)tot / (double)(mc * (mc + 1) / 2 + mc * rt);
+        bool ok = false;
+        for (int q = 0; q < ntier; ++q) {
+            if (tw[q] < 0 || mc <= tw[q]) {
+                ok = frac < tb[q] || tb[q] >= 1.0;
+                break;
+            }
+        }
+        if (ok) {
+            nc[i] = mc; nr[i] = rt; zr[i] = tot;
+            nxt[i] = nxt[s];
+        } else {
+            i = s;
+        }
+    }
+    long long k = 0;
+    for (long long j = 0; j < nb; j = nxt[j]) out[k++] = st[j];
+    return k;
+}
+
+// Row structures R_j of every supernode (symbolic.py:compute_row_structures,
+// reference symbolic.py:280-306): the rows >= c1 of A's columns c0..c1 united with
+// the pieces the children pass up (their rows beyond the parent's columns).
+// Two calls: compute (returns a handle and the total row count), then fetch
+// (ptr[M+1], rows[total]) which frees the handle.
+struct RowStructs {
+    std::vector<long long> ptr, rows;
+};
+
+extern "C" void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
+                                      const long long *row_idx, long long *total) {
+    auto *h = new RowStructs();
+    h->ptr.assign(M + 1, 0);
+    std::vector<std::vector<long long>> pending(M);
+    std::vector<long long> buf;
+    for (long long j = 0; j < M; ++j) {
+        const long long c0 = starts[j], c1 = starts[j + 1];
+        buf.swap(pending[j]);
+        std::vector<long long>().swap(pending[j]);
+        for (long long p = col_ptr[c0]; p < col_ptr[c1]; ++p)
+            if (row_idx[p] >= c1) buf.push_back(row_idx[p]);
+        std::sort(buf.begin(), buf.end());
+        buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+        h->rows.insert(h->rows.end(), buf.begin(), buf.end());
+        h->ptr[j + 1] = (long long)h->rows.size();
+        if (!buf.empty()) {
+            // supernode t containing the first row; pass up the rows beyond its columns
+            const long long t = (long long)(std::upper_bound(starts, starts + M + 1, buf[0]) - starts) - 1;
+            const long long t1 = starts[t + 1];
+            auto it = std::lower_bound(buf.begin(), buf.end(), t1);
+            pending[t].insert(pending[t].end(), it, buf.end());
+        }
+        buf.clear();
+    }
+    *total = (long long)h->rows.size();
+    return h;
+}
+
+extern "C" int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows) {
+    auto *h = static_cast<RowStructs *>(handle);
+    if (!h) return -1;
+    std::copy(h->ptr.begin(), h->ptr.end(), ptr);
+    std::copy(h->rows.begin(), h->rows.end(), rows);
+    delete h;
+    return 0;
+}

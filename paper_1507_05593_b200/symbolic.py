@@ -403,31 +403,23 @@ def _fundamental(lo, hi, parent, counts):
 
 
 def _amalgamate(bounds, parent, counts):
-    ncols = [bounds[i + 1] - bounds[i] for i in range(len(bounds) - 1)]
-    nrows = [int(counts[bounds[i]]) - ncols[i] for i in range(len(bounds) - 1)]
-    zeros = [0] * len(ncols)
-    starts = list(bounds[:-1])
-    i = 0
-    while i < len(starts) - 1:
-        last = starts[i] + ncols[i] - 1
-        if parent[last] != starts[i + 1]:
-            i += 1
-            continue
-        ns, nt, rs, rt = ncols[i], ncols[i + 1], nrows[i], nrows[i + 1]
-        mc = ns + nt
-        tot = zeros[i] + zeros[i + 1] + ns * (nt + rt - rs)
-        frac = tot / (mc * (mc + 1) // 2 + mc * rt)
-        ok = False
-        for width, bound in AMALG_TIERS:
-            if width is None or mc <= width:
-                ok = frac < bound or bound >= 1.0
-                break
-        if ok:
-            ncols[i], nrows[i], zeros[i] = mc, rt, tot
-            del starts[i + 1], ncols[i + 1], nrows[i + 1], zeros[i + 1]
-        else:
-            i += 1
-    return starts
+    """Relaxed amalgamation of one gap of fundamental supernodes (C++:
+    rsc_sym_amalgamate; the same merge rule and IEEE fraction as the reference
+    loop, symbolic.py:244-277)."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    nb = len(b) - 1
+    if nb <= 0:
+        return []
+    par = np.ascontiguousarray(parent, dtype=np.int64)
+    cnt = np.ascontiguousarray(counts, dtype=np.int64)
+    tw = np.array([-1 if w is None else w for w, _ in AMALG_TIERS], dtype=np.int64)
+    tb = np.array([bd for _, bd in AMALG_TIERS], dtype=np.float64)
+    out = np.empty(nb, dtype=np.int64)
+    k = _lib.load().rsc_sym_amalgamate(nb, b.ctypes.data, par.ctypes.data, cnt.ctypes.data, len(tw),
+                                       tw.ctypes.data, tb.ctypes.data, out.ctypes.data)
+    if k < 0:
+        raise RuntimeError(f"rsc_sym_amalgamate failed ({k})")
+    return out[:k].tolist()
 
 
 def form_supernodes(n, parent, counts, septree, tau_o, relax=True):
@@ -451,24 +443,21 @@ def form_supernodes(n, parent, counts, septree, tau_o, relax=True):
 
 def compute_row_structures(B, part):
     """R_j = A's below-block rows of C_j  U  children's rows beyond their parent's
-    columns (symbolic.py:280-306)."""
+    columns (symbolic.py:280-306); the merge sweep runs in C++
+    (rsc_sym_rows_compute / rsc_sym_rows_fetch), R_j are views of one array."""
+    import ctypes
+
     M = part.count
-    cp, ri = B.col_ptr, B.row_idx
-    pending = [[] for _ in range(M)]
-    rows = [None] * M
-    st = part.starts
-    for j in range(M):
-        c0, c1 = int(st[j]), int(st[j + 1])
-        a = ri[cp[c0]:cp[c1]]
-        pieces = pending[j]
-        pieces.append(a[a >= c1])
-        merged = np.unique(np.concatenate(pieces)) if len(pieces) > 1 else np.unique(pieces[0])
-        rows[j] = merged.astype(np.int64, copy=False)
-        pending[j] = None
-        if merged.size:
-            t = int(np.searchsorted(st, merged[0], side="right") - 1)
-            t1 = st[t + 1]
-            pending[t].append(merged[np.searchsorted(merged, t1):])
+    lib = _lib.load()
+    st = np.ascontiguousarray(part.starts, dtype=np.int64)
+    cp = np.ascontiguousarray(B.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(B.row_idx, dtype=np.int64)
+    total = ctypes.c_longlong(0)
+    h = lib.rsc_sym_rows_compute(M, st.ctypes.data, cp.ctypes.data, ri.ctypes.data, ctypes.byref(total))
+    ptr = np.empty(M + 1, dtype=np.int64)
+    allrows = np.empty(max(total.value, 1), dtype=np.int64)
+    _lib.check(lib.rsc_sym_rows_fetch(h, ptr.ctypes.data, allrows.ctypes.data), "rsc_sym_rows_fetch")
+    rows = [allrows[ptr[j]:ptr[j + 1]] for j in range(M)]
     part.rows = rows
     return rows
 
