@@ -202,6 +202,17 @@ long long rsc_sym_amalgamate(long long nb, const long long *bounds, const long l
 void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
                            const long long *row_idx, long long *total);
 int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows);
+/* Full symmetric CSR of a lower-CSC matrix, rows sorted, stored zeros dropped
+ * (sparse.py:86-97 _csr_full); adjacency != 0 also drops the diagonal (the ND
+ * graph, ordering.py:113-119).  indices/data need 2*nnz_lower capacity; returns
+ * the entry count. */
+long long rsc_sym_full_csr(long long n, const long long *col_ptr, const long long *row_idx,
+                           const double *values, int adjacency, long long *indptr, long long *indices,
+                           double *data);
+/* Symmetric permutation in lower storage (sparse.py:171-189): new rows / columns of
+ * every entry sorted by (column, row) and the source position of each. */
+int rsc_sym_permute_lower(long long n, const long long *col_ptr, const long long *row_idx, const long long *p,
+                          long long *out_rows, long long *out_cols, long long *order);
 /* One geometric bisection step of nested dissection (ordering.py:182-192): the
  * vertices are split at the median along the widest coordinate axis (ties by id);
  * the second half's members adjacent to the first form the separator.  indptr /

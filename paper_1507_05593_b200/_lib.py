@@ -53,6 +53,8 @@ EXPORTED = (
     "rsc_sym_amalgamate",
     "rsc_sym_rows_compute",
     "rsc_sym_rows_fetch",
+    "rsc_sym_full_csr",
+    "rsc_sym_permute_lower",
     "rsc_nd_split_geometric",
     "rsc_csr_windows",
     "rsc_pcg64_block_states",
@@ -100,6 +102,8 @@ _SIGS = {
     "rsc_sym_amalgamate": (LL, [LL, P, P, P, I, P, P, P]),
     "rsc_sym_rows_compute": (ctypes.c_void_p, [LL, P, P, P, P]),
     "rsc_sym_rows_fetch": (I, [ctypes.c_void_p, P, P]),
+    "rsc_sym_full_csr": (LL, [LL, P, P, P, I, P, P, P]),
+    "rsc_sym_permute_lower": (I, [LL, P, P, P, P, P, P]),
     "rsc_nd_split_geometric": (I, [LL, P, ctypes.c_int, P, P, P, P, P, P]),
     "rsc_csr_windows": (I, [LL, LL] + [P] * 16),
     "rsc_pcg64_block_states": (I, [I, I, P, P, P, P]),

@@ -205,3 +205,78 @@ extern "C" int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows)
     delete h;
     return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Full symmetric CSR (both triangles, rows sorted) of a lower-CSC matrix in one
+// column-order pass: column j appends j to the rows of its entries (i, j), i >= j,
+// and its entries i > j to row j -- rows come out sorted without a sort.
+// With values, stored zeros are dropped (what scipy's low + tril(low, -1).T does);
+// adjacency != 0 also drops the diagonal ((full - diag(full)).eliminate_zeros(), the
+// ND adjacency of symbolic.py:_adjacency).  values may be null (pattern only).
+// Returns the entry count (<0: bad argument).
+extern "C" long long rsc_sym_full_csr(long long n, const long long *col_ptr, const long long *row_idx,
+                                      const double *values, int adjacency, long long *indptr,
+                                      long long *indices, double *data) {
+    if (n < 0 || !col_ptr || !row_idx || !indptr || !indices) return -1;
+    if (adjacency && !values) return -2;
+    std::vector<long long> cnt(n + 1, 0);
+    for (long long j = 0; j < n; ++j)
+        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            const long long i = row_idx[p];
+            if ((values && values[p] == 0.0) || (adjacency && i == j)) continue;
+            cnt[i + 1]++;
+            if (i != j) cnt[j + 1]++;
+        }
+    for (long long i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::copy(cnt.begin(), cnt.end(), indptr);
+    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+    for (long long j = 0; j < n; ++j)
+        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            const long long i = row_idx[p];
+            if ((values && values[p] == 0.0) || (adjacency && i == j)) continue;
+            const long long q = pos[i]++;
+            indices[q] = j;
+            if (data) data[q] = values[p];
+            if (i != j) {
+                const long long q2 = pos[j]++;
+                indices[q2] = i;
+                if (data) data[q2] = values[p];
+            }
+        }
+    return cnt[n];
+}
+
+// Symmetric permutation in lower storage (sparse.py:_permuted_lower): entry e of A
+// (row row_idx[e], column col(e)) lands at (max, min) of (p[row], p[col]); outputs
+// the new rows / columns sorted by (column, row) and the source position of each.
+extern "C" int rsc_sym_permute_lower(long long n, const long long *col_ptr, const long long *row_idx,
+                                     const long long *p, long long *out_rows, long long *out_cols,
+                                     long long *order) {
+    if (n < 0 || !col_ptr || !row_idx || !p) return -1;
+    const long long nnz = col_ptr[n];
+    std::vector<long long> cnt(n + 1, 0);
+    for (long long j = 0; j < n; ++j)
+        for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
+            const long long a = p[row_idx[e]], b = p[j];
+            cnt[(a < b ? a : b) + 1]++;
+        }
+    for (long long c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
+    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+    std::vector<std::pair<long long, long long>> tmp(nnz);
+    for (long long j = 0; j < n; ++j)
+        for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
+            const long long a = p[row_idx[e]], b = p[j];
+            const long long c = a < b ? a : b, r = a < b ? b : a;
+            tmp[pos[c]++] = {r, e};
+        }
+    for (long long c = 0; c < n; ++c) {
+        std::sort(tmp.begin() + cnt[c], tmp.begin() + cnt[c + 1]);
+        for (long long q = cnt[c]; q < cnt[c + 1]; ++q) {
+            out_rows[q] = tmp[q].first;
+            out_cols[q] = c;
+            order[q] = tmp[q].second;
+        }
+    }
+    (void)nnz;
+    return 0;
+}

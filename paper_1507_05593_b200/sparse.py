@@ -80,12 +80,11 @@ class SparseSpdMatrix:
         return self._csc_lower
 
     def to_csr_full(self):
-        """Full symmetric CSR (both triangles), cached, indices sorted."""
+        """Full symmetric CSR (both triangles, stored zeros dropped), cached, indices
+        sorted -- one O(nnz) C++ pass (rsc_sym_full_csr) instead of scipy's
+        add + convert + sort."""
         if self._csr_full is None:
-            low = self.to_csc_lower()
-            full = (low + sp.tril(low, -1).T).tocsr()
-            full.sort_indices()
-            self._csr_full = full
+            self._csr_full = full_csr(self, adjacency=False)
         return self._csr_full
 
     def device_csr(self):
@@ -174,23 +173,47 @@ class Permutation:
         return f"Permutation(n={self.n})"
 
 
+def full_csr(A, adjacency=False):
+    """scipy CSR of the symmetric full matrix (adjacency=True: without the diagonal)."""
+    from . import _lib
+
+    n = A.n
+    cp = np.ascontiguousarray(A.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(A.row_idx, dtype=np.int64)
+    va = np.ascontiguousarray(A.values, dtype=np.float64)
+    cap = 2 * ri.size
+    indptr = np.empty(n + 1, dtype=np.int64)
+    indices = np.empty(max(cap, 1), dtype=np.int64)
+    data = np.empty(max(cap, 1), dtype=np.float64)
+    nnz = _lib.load().rsc_sym_full_csr(n, cp.ctypes.data, ri.ctypes.data, va.ctypes.data, int(adjacency),
+                                       indptr.ctypes.data, indices.ctypes.data, data.ctypes.data)
+    if nnz < 0:
+        raise RuntimeError(f"rsc_sym_full_csr failed ({nnz})")
+    it = np.int32 if nnz < 2**31 - 1 else np.int64
+    m = sp.csr_matrix((data[:nnz], indices[:nnz].astype(it), indptr.astype(it)), shape=(n, n))
+    m.has_sorted_indices = True
+    return m
+
+
 def _permuted_lower(A, p):
     """Lower-storage (row, col) of every entry of A under p, sorted by (col, row),
     and the source position of each: one counting pass by column plus a per-column
-    row sort (scipy's C++ csr kernels) instead of a 2-key lexsort."""
+    row sort in C++ (rsc_sym_permute_lower) instead of a 2-key lexsort."""
+    from . import _lib
+
     n = A.n
-    cols = np.repeat(np.arange(n, dtype=np.int64), np.diff(A.col_ptr))
-    nr, nc = p[A.row_idx], p[cols]
-    r, c = np.maximum(nr, nc), np.minimum(nr, nc)
-    if n == 0 or r.size == 0:
-        return r, c, np.arange(r.size, dtype=np.int64)
-    # positions as data (exact in f64 below 2^53); entries are distinct, so the
-    # transpose (csr of the (c, r) pairs) never sums duplicates
-    pos = np.arange(r.size, dtype=np.float64)
-    m = sp.csr_matrix((pos, (c, r)), shape=(n, n))
-    m.sort_indices()
-    order = m.data.astype(np.int64)
-    return m.indices.astype(np.int64), np.repeat(np.arange(n, dtype=np.int64), np.diff(m.indptr)), order
+    nnz = int(A.row_idx.size)
+    r = np.empty(nnz, dtype=np.int64)
+    c = np.empty(nnz, dtype=np.int64)
+    order = np.empty(nnz, dtype=np.int64)
+    if n == 0 or nnz == 0:
+        return r, c, np.arange(nnz, dtype=np.int64)
+    cp = np.ascontiguousarray(A.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(A.row_idx, dtype=np.int64)
+    pp = np.ascontiguousarray(p, dtype=np.int64)
+    _lib.check(_lib.load().rsc_sym_permute_lower(n, cp.ctypes.data, ri.ctypes.data, pp.ctypes.data, r.ctypes.data,
+                                                 c.ctypes.data, order.ctypes.data), "rsc_sym_permute_lower")
+    return r, c, order
 
 
 def permute_symmetric(A, perm):

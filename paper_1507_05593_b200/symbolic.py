@@ -93,10 +93,10 @@ class SplitTree:
 
 
 def _adjacency(A):
-    full = A.to_csr_full()
-    adj = (full - sp.diags(full.diagonal())).tocsr()
-    adj.eliminate_zeros()
-    return adj
+    """Graph of A without the diagonal and stored zeros (C++ rsc_sym_full_csr)."""
+    from .sparse import full_csr
+
+    return full_csr(A, adjacency=True)
 
 
 def _coords_xyz(coords, n):
