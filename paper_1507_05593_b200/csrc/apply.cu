@@ -230,6 +230,11 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
     __shared__ double part[T];
     const long long blk = blockIdx.x;
     const int p = find_prob(a.p, 0, a.count - 1, blk);
+    // programmatic dependent launch: the apply's phases are chains of these launches;
+    // let the next phase's CTAs be scheduled now, and wait here until the previous
+    // phase (whose outputs are this phase's inputs) has completed and flushed
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(a.p[p], blk - a.p[p].blk_begin, xr, part);
 }
 
@@ -271,8 +276,18 @@ int gemv_launch(int count, const double *const *M, const int *rows, const int *c
         }
         if (a.count == 0) continue;
         a.total = blocks;
-        gemv_kernel<<<(unsigned)blocks, T, 0, s>>>(a);
-        RSC_CHECK_LAUNCH();
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3(T);
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_kernel, a);
+        rsc_count_launch();
+        if (e != cudaSuccess) return (int)e;
     }
     return 0;
 }

@@ -272,7 +272,13 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
                 for sid, (raw, eff) in got.items():
                     ps._set_source(sid, raw, eff)
                     remote[sid] = raw
+        # shared top separators: every rank forms the partial sums over the sources of
+        # its own subtrees (rank 0 also the A-matrix, root-path and top-source terms),
+        # all-reduced before each diagonal solve / POTRF / QRCP, which run replicated
+        src_owner = np.array([max(int(owner[src.unit]), 0) for src in plan.sources], dtype=np.int64)
+        ps.split = (rank, world, src_owner, group)
         ps._run_units(lambda u: owner[u] == -1)
+        ps.split = None
         try:
             ps.check_pivots()
             cand = None

@@ -184,6 +184,40 @@ class LevelPass(NumericPass):
         self.launches = None
         self._wterms = []    # flop terms coef * w * r whose widths may be sketch-padded
         self._price = {}     # data_ptr of a final-product operand -> its U (re-priced at rank)
+        # multi-GPU split of the shared top separators (distributed.factorize_distributed):
+        # (rank, world, owner rank of every source id, process group) -- each rank
+        # launches only the source terms of the sources it owns, rank 0 the A-matrix
+        # and root-path terms, and every accumulated block is all-reduced before the
+        # step that consumes it.  Flop accounting always covers the full sums.
+        self.split = None
+
+    def _mine(self, sids):
+        """Mask of the source terms this rank launches (all of them when not split)."""
+        if self.split is None:
+            return np.ones(len(sids), dtype=bool)
+        rank, _, owner, _ = self.split
+        return owner[np.asarray(sids, dtype=np.int64)] == rank
+
+    def _lead(self):
+        """This rank launches the A-matrix and root-path terms."""
+        return self.split is None or self.split[0] == 0
+
+    def _reduce(self, tensors):
+        """Sum the per-rank partial blocks (NCCL all-reduce; gloo stages via the host)."""
+        if self.split is None:
+            return
+        import torch.distributed as dist
+
+        group = self.split[3]
+        for t in tensors:
+            if t is None or t.numel() == 0:
+                continue
+            if t.is_cuda and dist.get_backend(group) == "gloo":
+                h = t.cpu()
+                dist.all_reduce(h, group=group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, group=group)
 
     def _wflops(self, coef, w=1, wbase=0, r=1, rbase=0):
         """Count flops coef * w * r where w is a source panel's width (panel base
@@ -243,7 +277,7 @@ class LevelPass(NumericPass):
                 nr.append(blk.nrows)
                 dp.append(D.data_ptr())
                 ld.append(E.ld(D))
-        if nr:
+        if nr and self._lead():
             E.csr_to_dense_batched(rp, ci, va, nr, dp, ld)
         return outs
 
@@ -286,6 +320,12 @@ class LevelPass(NumericPass):
             yp.append(Y.data_ptr())
             ly.append(E.ld(Y))
             self._wflops(2.0 * blk.nnz, r=X.shape[1], rbase=self._price.get(X.data_ptr(), 0))
+        if nr and not self._lead():
+            if beta == 0.0:
+                for Y in [it[2] for it in items]:
+                    if Y.numel():
+                        Y.zero_()
+            return
         if nr:
             lib = E.require_cuda()
             from ._lib import int_array, ptr_array
@@ -388,10 +428,13 @@ class LevelPass(NumericPass):
                     self.idx_base + (4 * t["rpos"][sel]).astype(np.uint64))
                 p["c_cols"] = cpos[sel]
                 p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
-                probs.append(p)
                 self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s][sel])
+                probs.append(p[self._mine(s[sel])])
         if probs:
-            E.gemm_grouped(E.balance_k(np.concatenate(probs), False, True), False, True)
+            P = np.concatenate(probs)
+            if P.size:
+                E.gemm_grouped(E.balance_k(P, False, True), False, True)
+        self._reduce([t for pair in out for t in pair])
         return out
 
     # -- implicit products, batched over nodes -----------------------------------
@@ -414,6 +457,7 @@ class LevelPass(NumericPass):
         diag_solve_many(sol, self.S.empty)
         self._spmm_many([(self.np.node_blocks[n.j][1], G1, W) for n, G1, W in zip(nodes, G1s, Ws)])
         self._products_many(nodes, G1s, Ws, trans=False)
+        self._reduce(Ws)
         self._price.clear()
         return Ws
 
@@ -421,6 +465,7 @@ class LevelPass(NumericPass):
         Ws = [self.S.empty(n.ncols, G.shape[1]) for n, G in zip(nodes, Gs)]
         self._spmm_many([(self.np.node_blocks[n.j][2], G, W) for n, G, W in zip(nodes, Gs, Ws)])
         self._products_many(nodes, Gs, Ws, trans=True)
+        self._reduce(Ws)
         diag_solve_many([(n, W, False) for n, W in zip(nodes, Ws)], self.S.empty)
         for n, W in zip(nodes, Ws):
             self.flops += n.ncols**2 * W.shape[1]
@@ -469,9 +514,12 @@ class LevelPass(NumericPass):
             p1["A"], p1["K"], p1["b_rows"] = eff_hi, nro, rpos
             p2["A"], p2["M"], p2["c_rows"] = raw_lo, nrd, cpos
         p1["atomic"] = 1  # T is zeroed: p1 accumulates, so its tall K may be split
-        E.gemm_grouped(E.balance_k(p1, True, False), True, False)
-        E.gemm_grouped(E.balance_k(p2, False, False), False, False)
         self._wflops(2.0 * (nrd + nro), w=w, wbase=self.s_raw[s], r=r, rbase=rep(6).astype(np.uint64))
+        keep = self._mine(s)
+        p1, p2 = p1[keep], p2[keep]
+        if p1.size:
+            E.gemm_grouped(E.balance_k(p1, True, False), True, False)
+            E.gemm_grouped(E.balance_k(p2, False, False), False, False)
 
     def approx_off_many(self, nodes, ranks):
         """Alg. 3 for every compressed off-diagonal of the level (factor.py:486-505)."""
@@ -516,7 +564,7 @@ class LevelPass(NumericPass):
             k = lf.hi - lf.lo
             blocks.append((blk, k, k))
         Us = self._dense_many(blocks)
-        parts, bases = [], []
+        parts, bases, keeps = [], [], []
         for (node, s), U in zip(items, Us):
             tree = node.diag
             lf = tree.shape.nodes[s]
@@ -535,6 +583,7 @@ class LevelPass(NumericPass):
                 p["C"], p["ldc"] = U.data_ptr(), k
                 parts.append(p)
                 bases.append(self.s_raw[src])
+                keeps.append(self._mine(src))
             path = self._path_probs(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi))
             if path:
                 p = np.zeros(len(path), dtype=GEMM_DTYPE)
@@ -544,11 +593,15 @@ class LevelPass(NumericPass):
                 p["C"], p["ldc"] = U.data_ptr(), k
                 parts.append(p)
                 bases.append(np.array([pt[0] for pt in path], dtype=np.uint64))
+                keeps.append(np.full(len(path), self._lead()))
         if parts:
             P = np.concatenate(parts)
             P["batch"], P["atomic"], P["alpha"], P["beta"] = 1, 1, -1.0, 1.0
-            E.gemm_grouped(E.balance_k(P, False, True), False, True)
             self._wflops(2.0 * P["M"] * P["N"], w=P["K"], wbase=np.concatenate(bases))
+            P = P[np.concatenate(keeps)]
+            if P.size:
+                E.gemm_grouped(E.balance_k(P, False, True), False, True)
+        self._reduce(Us)
         if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
             Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
         return self._potrf_many([(U, node.u) for (node, s), U in zip(items, Us)])
@@ -617,6 +670,7 @@ class LevelPass(NumericPass):
             n = w.size
             if n == 0:
                 continue
+            keep = np.concatenate([self._mine(sid), np.full(n - sid.size, self._lead())])
             tsz = w * r
             toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
             T = self.S.zeros(int(tsz.sum()))  # p1 accumulates into it (K may be split)
@@ -633,16 +687,18 @@ class LevelPass(NumericPass):
             else:  # T = E[rwin]^T G[ridx] ; W[cidx] -= V[cwin] T
                 p1["A"], p1["K"], p1["b_rows"] = eff_r, nr_, ridx
                 p2["A"], p2["M"], p2["c_rows"] = raw_c, nc_, cidx
-            p1s.append(p1)
-            p2s.append(p2)
             self._wflops(2.0 * (nc_ + nr_), w=w, wbase=base, r=r, rbase=self._price.get(src.data_ptr(), 0))
+            p1s.append(p1[keep])
+            p2s.append(p2[keep])
         if p1s:
             P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
             P1["batch"], P1["alpha"] = 1, 1.0
             P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
             P1["atomic"] = 1  # T is zeroed: P1 accumulates, so its tall K may be split
-            E.gemm_grouped(E.balance_k(P1, True, False), True, False)
-            E.gemm_grouped(E.balance_k(P2, False, False), False, False)
+            if P1.size:
+                E.gemm_grouped(E.balance_k(P1, True, False), True, False)
+                E.gemm_grouped(E.balance_k(P2, False, False), False, False)
+        self._reduce(Ws)
         if transpose:
             sol2 = []
             for (node, s), W in zip(items, Ws):
