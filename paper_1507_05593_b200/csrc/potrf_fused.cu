@@ -23,6 +23,8 @@
 // The matrix (<= 512 KB) stays L2-resident between the phases, so the panel rows
 // round-trip through L2, not HBM.  Rows past n of a partial last panel are treated
 // as identity rows, so the 64-row algorithm needs no special case.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -147,6 +149,9 @@ __device__ int chol_inv_32(double *Ds, double *Is, int o, double *rsv) {
     return -1;
 }
 
+__device__ unsigned long long pf_phase_cycles[8];  // RSC_POTRF_TIMING diagnostics (CTA 0)
+
+template <bool TIMING>
 __global__ void __launch_bounds__(PF_THREADS, 1) potrf_fused_kernel(const __grid_constant__ PfArgs args,
                                                                      int *info) {
     extern __shared__ __align__(16) double sm[];
@@ -166,7 +171,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1) potrf_fused_kernel(const __grid
     const int g = lane >> 2, q = lane & 3;
     const bool vec16 = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
 
+    long long tp = TIMING ? clock64() : 0;
+    auto mark = [&](int ph) {
+        if (TIMING && threadIdx.x == 0 && blockIdx.x == 0) {
+            const long long now = clock64();
+            atomicAdd(&pf_phase_cycles[ph], (unsigned long long)(now - tp));
+            tp = now;
+        }
+    };
     for (int j0 = 0; j0 < n; j0 += 64) {
+        mark(7);
         const int M = n - j0;             // panel rows
         const int nb = M < 64 ? M : 64;   // panel columns
         double *P = A + (long long)j0 * lda + j0;  // panel origin
@@ -225,6 +239,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) potrf_fused_kernel(const __grid
                 }
         }
         __syncthreads();
+        mark(0);
         // ---- 2. factor + invert the diagonal block (all 256 threads) -----------------
         // 2x2 blocks of 32: chol+inv(D11); L21 = A21 inv11^T; A22 -= L21 L21^T;
         // chol+inv(A22); X21 = -inv22 L21 inv11.  Rows past nb are identity rows.
@@ -309,6 +324,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) potrf_fused_kernel(const __grid
             }
         }
         __syncthreads();
+        mark(1);
         if (*fail_s >= 0) return;
         // diagonal block (upper zeroed), its inverse, and the clean strict upper part
         for (int e = t; e < nb * 64; e += PF_THREADS) {
@@ -321,6 +337,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) potrf_fused_kernel(const __grid
             const int i = e / rest, j = e - i * rest;
             P[(long long)i * lda + nb + j] = 0.0;
         }
+        mark(2);
         // ---- 3. rows below the diagonal block: X = P_below Dinv^T ---------------------
         const int M3 = M - 64;
         if (M3 > 0) {
@@ -372,7 +389,8 @@ int rsc_potrf_fused(int count, double *const *A, const int *n, const int *lda, d
                     int *info_dev, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(potrf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
+        cudaFuncSetAttribute(potrf_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
+        cudaFuncSetAttribute(potrf_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
         attr = true;
     }
     static thread_local PfArgs pa;
@@ -386,8 +404,19 @@ int rsc_potrf_fused(int count, double *const *A, const int *n, const int *lda, d
             pa.n[i] = n[c0 + i];
             pa.lda[i] = lda[c0 + i];
         }
-        potrf_fused_kernel<<<cnt, PF_THREADS, PF_SMEM, s>>>(pa, info_dev);
+        static const bool timing = getenv("RSC_POTRF_TIMING") != nullptr;
+        if (timing) potrf_fused_kernel<true><<<cnt, PF_THREADS, PF_SMEM, s>>>(pa, info_dev);
+        else potrf_fused_kernel<false><<<cnt, PF_THREADS, PF_SMEM, s>>>(pa, info_dev);
         RSC_CHECK_LAUNCH();
     }
     return 0;
+}
+
+extern "C" int rsc_potrf_phase_cycles(unsigned long long *out8, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out8, pf_phase_cycles, 8 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(pf_phase_cycles, z, sizeof(z));
+    }
+    return (int)e;
 }
