@@ -164,6 +164,11 @@ int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,
 
 /* Gather / scatter of rows: dst[i, :] = src[idx[i], :]  (gather)
  *                           dst[idx[i], :] += alpha*src[i, :]  (scatter_add) */
+/* Batched n x n identity fill / transpose (dst = src^T) of device squares: the apply
+ * program's explicit inverses (apply.py refresh_inverses) in one launch each. */
+int rsc_identity_batched(int count, double *const *dst, const int *n, const int *ldd, void *stream);
+int rsc_transpose_batched(int count, const double *const *src, double *const *dst, const int *n,
+                          const int *lds, const int *ldd, void *stream);
 int rsc_gather_rows(int nrows, int ncols, const int *idx_dev, const double *src_dev,
                     int lds, double *dst_dev, int ldd, void *stream);
 int rsc_scatter_add_rows(int nrows, int ncols, const int *idx_dev, double alpha,

@@ -42,6 +42,8 @@ EXPORTED = (
     "rsc_trsv_batched",
     "rsc_gemv_batched",
     "rsc_gemv_multi",
+    "rsc_identity_batched",
+    "rsc_transpose_batched",
     "rsc_gather_rows",
     "rsc_scatter_add_rows",
     "rsc_dot",
@@ -92,6 +94,8 @@ _SIGS = {
     "rsc_gemv_multi": (I, [I, P, P, P, P, P, P, P, P, P, P, P]),
 
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
+    "rsc_identity_batched": (I, [I, P, P, P, P]),
+    "rsc_transpose_batched": (I, [I, P, P, P, P, P, P]),
     "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),
     "rsc_dot": (I, [I, P, P, P, P, P]),
     "rsc_pcg_update_xr": (I, [I, P, P, P, P, P, P, P]),

@@ -124,6 +124,7 @@ class DeviceApply:
             elif isinstance(u.diag, DeviceTree):
                 tris.extend(b for s_, b in u.diag.blocks.items() if u.diag.shape.nodes[s_].is_leaf)
         self.tris = [t for t in tris if t.n]
+        self._sq = None
         if any(t.Linv is None for t in self.tris):
             self.mem = E.Arena()
             for t in self.tris:
@@ -136,14 +137,21 @@ class DeviceApply:
         tris = self.tris
         if not tris:
             return
-        for t in tris:
-            t.Linv.zero_()
-            t.Linv.fill_diagonal_(1.0)
+        lib = _lib.load()
+        if self._sq is None:
+            ns = [t.n for t in tris]
+            self._sq = (int_array(ns), ptr_array([t.Linv.data_ptr() for t in tris]),
+                        ptr_array([t.LinvT.data_ptr() for t in tris]), int_array([E.ld(t.Linv) for t in tris]),
+                        int_array([E.ld(t.LinvT) for t in tris]))
+        n_, li, lt, ldi, ldt = self._sq
+        s = E.stream_handle()
+        _lib.check(lib.rsc_identity_batched(len(tris), li.ctypes.data, n_.ctypes.data, ldi.ctypes.data, s),
+                   "rsc_identity_batched")
         E.trsm_batched("left", 0, [t.L.data_ptr() for t in tris], [t.n for t in tris], [E.ld(t.L) for t in tris],
                        [t.Dinv.data_ptr() for t in tris], [t.Linv.data_ptr() for t in tris], [t.n for t in tris],
                        [t.n for t in tris])
-        for t in tris:
-            t.LinvT.copy_(t.Linv.t())
+        _lib.check(lib.rsc_transpose_batched(len(tris), li.ctypes.data, lt.ctypes.data, n_.ctypes.data,
+                                             ldi.ctypes.data, ldt.ctypes.data, s), "rsc_transpose_batched")
 
     def _rows_ptr(self, plan, un):
         key = ("int", un.u) if un.kind == "interior" else un.j

@@ -343,3 +343,85 @@ extern "C" int rsc_gemv_multi(int count, const double *const *M, const int *rows
     return gemv_launch(count, M, rows, cols, ldm, x, xidx, y, yidx, modes, 0, alphas, 0.0, (cudaStream_t)stream);
 }
 
+
+// ---------------------------------------------------------------------------
+// Batched identity / transpose for the apply program's explicit inverses (one
+// launch each instead of two torch kernels per triangle): refresh after every
+// refactorization re-derives Linv = L^{-1} (TRSM against I) and LinvT.
+namespace {
+constexpr int BMAX = 1024;
+struct SqArgs {
+    int count;
+    const double *src[BMAX];
+    double *dst[BMAX];
+    int n[BMAX], lds[BMAX], ldd[BMAX];
+};
+
+__global__ void __launch_bounds__(256) eye_kernel(const __grid_constant__ SqArgs a) {
+    const int b = blockIdx.x;
+    const int n = a.n[b], ld = a.ldd[b];
+    double *D = a.dst[b];
+    for (long long e = threadIdx.x; e < (long long)n * n; e += 256) {
+        const int i = (int)(e / n), j = (int)(e - (long long)i * n);
+        D[(long long)i * ld + j] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+// dst = src^T through 32x32 shared-memory tiles (coalesced both ways)
+__global__ void __launch_bounds__(256) transpose_kernel(const __grid_constant__ SqArgs a) {
+    __shared__ double tile[32][33];
+    const int b = blockIdx.x;
+    const int n = a.n[b], lds = a.lds[b], ldd = a.ldd[b];
+    const double *S = a.src[b];
+    double *D = a.dst[b];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int i0 = 0; i0 < n; i0 += 32)
+        for (int j0 = 0; j0 < n; j0 += 32) {
+            for (int q = ty; q < 32; q += 8) {
+                const int i = i0 + q, j = j0 + tx;
+                tile[q][tx] = (i < n && j < n) ? S[(long long)i * lds + j] : 0.0;
+            }
+            __syncthreads();
+            for (int q = ty; q < 32; q += 8) {
+                const int i = j0 + q, j = i0 + tx;  // D[i][j] = S[j][i]
+                if (i < n && j < n) D[(long long)i * ldd + j] = tile[tx][q];
+            }
+            __syncthreads();
+        }
+}
+
+int sq_launch(int mode, int count, const double *const *src, double *const *dst, const int *n, const int *lds,
+              const int *ldd, cudaStream_t s) {
+    static thread_local SqArgs a;
+    for (int c0 = 0; c0 < count; c0 += BMAX) {
+        const int cnt = count - c0 < BMAX ? count - c0 : BMAX;
+        a.count = cnt;
+        for (int i = 0; i < cnt; ++i) {
+            a.src[i] = src ? src[c0 + i] : nullptr;
+            a.dst[i] = dst[c0 + i];
+            a.n[i] = n[c0 + i];
+            a.lds[i] = lds ? lds[c0 + i] : 0;
+            a.ldd[i] = ldd[c0 + i];
+        }
+        if (mode == 0) eye_kernel<<<cnt, 256, 0, s>>>(a);
+        else transpose_kernel<<<cnt, 256, 0, s>>>(a);
+        RSC_CHECK_LAUNCH();
+    }
+    return 0;
+}
+}  // namespace
+
+extern "C" int rsc_identity_batched(int count, double *const *dst, const int *n, const int *ldd, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!dst || !n || !ldd) return -2;
+    return sq_launch(0, count, nullptr, dst, n, nullptr, ldd, (cudaStream_t)stream);
+}
+
+extern "C" int rsc_transpose_batched(int count, const double *const *src, double *const *dst, const int *n,
+                                     const int *lds, const int *ldd, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!src || !dst || !n || !lds || !ldd) return -2;
+    return sq_launch(1, count, src, dst, n, lds, ldd, (cudaStream_t)stream);
+}
