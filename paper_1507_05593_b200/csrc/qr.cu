@@ -413,21 +413,39 @@ struct RegQr {
         if (lane == 0) { tau[i] = tau_i; diagR[i] = beta; }
     }
 
-    // H_i applied to my unchosen columns, then the dlaqp2 partial-norm downdate
+    // Sum of four per-lane values over the warp, result broadcast: a reduce-scatter
+    // butterfly (2 + 1 + 1 + 1 + 1 exchanges) and 4 broadcasts -- 10 double shuffles
+    // instead of 20 (the shuffle pipe bounds this kernel).
+    __device__ __forceinline__ void sum4(double (&d)[RQ_SLOTS]) const {
+        const bool h16 = lane & 16, h8 = lane & 8;
+        double k0 = h16 ? d[2] : d[0], k1 = h16 ? d[3] : d[1];
+        const double s0 = h16 ? d[0] : d[2], s1 = h16 ? d[1] : d[3];
+        k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+        double kk = h8 ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+#pragma unroll
+        for (int s = 0; s < RQ_SLOTS; ++s) d[s] = __shfl_sync(0xffffffffu, kk, 8 * s);
+    }
+
+    // H_i applied to my unchosen columns, then the dlaqp2 partial-norm downdate.  The
+    // reflector carries its implicit 1 on row i, so one reduction gives v^T a
+    // including row i, and row i of every column is updated in place by the lane
+    // that holds it -- that lane also evaluates the downdate (no broadcast of row i).
     template <int QI>
     __device__ __forceinline__ void update(int i, int li, const double *v, double tau_i, double *vn1, double *vn2) {
         double vr[RQ_ROWS];
 #pragma unroll
-        for (int q = QI; q < RQ_ROWS; ++q) vr[q] = (q > QI || lane > li) ? v[lane + 32 * q] : 0.0;
+        for (int q = QI; q < RQ_ROWS; ++q)
+            vr[q] = (q > QI || lane > li) ? v[lane + 32 * q] : ((q == QI && lane == li) ? 1.0 : 0.0);
         bool act[RQ_SLOTS];
-        double ai[RQ_SLOTS], v1[RQ_SLOTS], v2[RQ_SLOTS];
 #pragma unroll
         for (int s = 0; s < RQ_SLOTS; ++s) {
             const int j = warp + RQ_WARPS * s;
             act[s] = j < k && pos[s] >= k;
-            v1[s] = act[s] ? vn1[j] : 0.0;
-            v2[s] = act[s] ? vn2[j] : 1.0;
-            ai[s] = shfl(a[s][QI], li);
         }
         if (tau_i != 0.0) {
             double d[RQ_SLOTS];
@@ -435,55 +453,49 @@ struct RegQr {
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 d[s] = 0.0;
 #pragma unroll
-                for (int q = QI; q < RQ_ROWS; ++q) d[s] += vr[q] * a[s][q];
+                for (int q = QI; q < RQ_ROWS; ++q) d[s] = fma(vr[q], a[s][q], d[s]);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int s = 0; s < RQ_SLOTS; ++s) d[s] += __shfl_xor_sync(0xffffffffu, d[s], o);
+            sum4(d);
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 if (!act[s]) continue;
-                const double f = tau_i * (d[s] + ai[s]);
+                const double f = tau_i * d[s];
 #pragma unroll
-                for (int q = QI; q < RQ_ROWS; ++q) a[s][q] -= f * vr[q];
-                if (lane == li) a[s][QI] -= f;  // v_i = 1 on row i (vr = 0 there)
-                ai[s] -= f;
+                for (int q = QI; q < RQ_ROWS; ++q) a[s][q] = fma(-f, vr[q], a[s][q]);
             }
         }
-        bool redo[RQ_SLOTS];
-        bool any_redo = false;
+        // downdate on the lane holding row i; the recompute decision is broadcast
+        unsigned redo_bits = 0;
+        if (lane == li) {
 #pragma unroll
-        for (int s = 0; s < RQ_SLOTS; ++s) {
-            redo[s] = false;
-            if (!act[s] || v1[s] == 0.0) continue;
-            double temp = fabs(ai[s]) / v1[s];
-            temp = 1.0 - temp * temp;
-            temp = temp < 0.0 ? 0.0 : temp;
-            const double ratio = v1[s] / v2[s];
-            const double temp2 = temp * ratio * ratio;
-            if (temp2 <= TOL3Z) {
-                redo[s] = any_redo = true;
-            } else if (lane == 0) {
-                vn1[warp + RQ_WARPS * s] = v1[s] * sqrt(temp);
+            for (int s = 0; s < RQ_SLOTS; ++s) {
+                const int j = warp + RQ_WARPS * s;
+                if (!act[s]) continue;
+                const double v1 = vn1[j];
+                if (v1 == 0.0) continue;
+                double temp = fabs(a[s][QI]) / v1;
+                temp = 1.0 - temp * temp;
+                temp = temp < 0.0 ? 0.0 : temp;
+                const double ratio = v1 / vn2[j];
+                const double temp2 = temp * ratio * ratio;
+                if (temp2 <= TOL3Z) redo_bits |= 1u << s;
+                else vn1[j] = v1 * sqrt(temp);
             }
         }
-        if (__any_sync(0xffffffffu, any_redo)) {
+        redo_bits = __shfl_sync(0xffffffffu, redo_bits, li);
+        if (redo_bits) {
             double nv[RQ_SLOTS];
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 nv[s] = 0.0;
 #pragma unroll
                 for (int q = QI; q < RQ_ROWS; ++q)
-                    if (q > QI || lane > li) nv[s] += a[s][q] * a[s][q];
+                    if (q > QI || lane > li) nv[s] = fma(a[s][q], a[s][q], nv[s]);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int s = 0; s < RQ_SLOTS; ++s) nv[s] += __shfl_xor_sync(0xffffffffu, nv[s], o);
+            sum4(nv);
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
-                if (!redo[s]) continue;
+                if (!((redo_bits >> s) & 1u)) continue;
                 const double x = sqrt(nv[s]);  // rows > i exist: i + 1 < m is implied by zero padding
                 if (lane == 0) { vn1[warp + RQ_WARPS * s] = x; vn2[warp + RQ_WARPS * s] = x; }
             }
