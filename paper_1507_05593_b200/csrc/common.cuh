@@ -44,6 +44,25 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Warp sums of four per-lane values, all lanes get all four: a reduce-scatter
+// butterfly (2 + 1 + 1 + 1 + 1 exchanges) plus 4 broadcasts -- 10 double shuffles
+// instead of the 20 of four independent butterflies.
+__device__ __forceinline__ void warp_sum4(double (&d)[4]) {
+    const int lane = threadIdx.x & 31;
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double k0 = h16 ? d[2] : d[0], k1 = h16 ? d[3] : d[1];
+    const double s0 = h16 ? d[0] : d[2], s1 = h16 ? d[1] : d[3];
+    k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+    k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+    double kk = h8 ? k1 : k0;
+    kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) d[s] = __shfl_sync(0xffffffffu, kk, 8 * s);
+}
+
 // Block-wide sum; `red` must hold >= 32 doubles.  Result broadcast to all threads.
 __device__ __forceinline__ double block_sum(double v, double *red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;

@@ -162,10 +162,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
                     for (int c = 0; c < CB; ++c)
 #pragma unroll
                         for (int q = 0; q < RPL; ++q) w[c] = fma(vr[q], x[c][q], w[c]);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                        for (int c = 0; c < CB; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+                    warp_sum4(w);
 #pragma unroll
                     for (int c = 0; c < CB; ++c) {
                         if (!on[c]) continue;
@@ -211,10 +208,7 @@ __global__ void __launch_bounds__(QR_THREADS) qrcp_kernel(const __grid_constant_
                             if (r > i && r < m) nv[c] = fma(x[c][q], x[c][q], nv[c]);
                         }
                     }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                        for (int c = 0; c < CB; ++c) nv[c] += __shfl_xor_sync(0xffffffffu, nv[c], o);
+                    warp_sum4(nv);
 #pragma unroll
                     for (int c = 0; c < CB; ++c) {
                         if (!redo[c]) continue;
@@ -413,24 +407,6 @@ struct RegQr {
         if (lane == 0) { tau[i] = tau_i; diagR[i] = beta; }
     }
 
-    // Sum of four per-lane values over the warp, result broadcast: a reduce-scatter
-    // butterfly (2 + 1 + 1 + 1 + 1 exchanges) and 4 broadcasts -- 10 double shuffles
-    // instead of 20 (the shuffle pipe bounds this kernel).
-    __device__ __forceinline__ void sum4(double (&d)[RQ_SLOTS]) const {
-        const bool h16 = lane & 16, h8 = lane & 8;
-        double k0 = h16 ? d[2] : d[0], k1 = h16 ? d[3] : d[1];
-        const double s0 = h16 ? d[0] : d[2], s1 = h16 ? d[1] : d[3];
-        k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-        k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-        double kk = h8 ? k1 : k0;
-        kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-        kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-#pragma unroll
-        for (int s = 0; s < RQ_SLOTS; ++s) d[s] = __shfl_sync(0xffffffffu, kk, 8 * s);
-    }
-
     // H_i applied to my unchosen columns, then the dlaqp2 partial-norm downdate.  The
     // reflector carries its implicit 1 on row i, so one reduction gives v^T a
     // including row i, and row i of every column is updated in place by the lane
@@ -455,7 +431,7 @@ struct RegQr {
 #pragma unroll
                 for (int q = QI; q < RQ_ROWS; ++q) d[s] = fma(vr[q], a[s][q], d[s]);
             }
-            sum4(d);
+            warp_sum4(d);
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 if (!act[s]) continue;
@@ -492,7 +468,7 @@ struct RegQr {
                 for (int q = QI; q < RQ_ROWS; ++q)
                     if (q > QI || lane > li) nv[s] = fma(a[s][q], a[s][q], nv[s]);
             }
-            sum4(nv);
+            warp_sum4(nv);
 #pragma unroll
             for (int s = 0; s < RQ_SLOTS; ++s) {
                 if (!((redo_bits >> s) & 1u)) continue;

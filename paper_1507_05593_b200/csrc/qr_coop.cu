@@ -296,10 +296,7 @@ __device__ __forceinline__ void qc_update(Cl &cl, int C, int i, int m, int k, in
                     if (on[c])
                         for (int r = i + 1 + lane; r < m; r += 32) w[c] += v[r] * cj[c][r];
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int c = 0; c < CB; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+            warp_sum4(w);
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
                 if (!on[c]) continue;
@@ -354,10 +351,7 @@ __device__ __forceinline__ void qc_update(Cl &cl, int C, int i, int m, int k, in
                     for (int r = i + 1 + lane; r < m; r += 32) nv[c] += cj[c][r] * cj[c][r];
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int c = 0; c < CB; ++c) nv[c] += __shfl_xor_sync(0xffffffffu, nv[c], o);
+            warp_sum4(nv);
 #pragma unroll
             for (int c = 0; c < CB; ++c) {
                 if (!redo[c]) continue;
