@@ -44,7 +44,7 @@ struct GemmArgs {
 // M / N validity are computed once per CTA; a k-tile only advances the pointers and
 // checks the K bound.  (Recomputing all of that per element per tile, with a branch
 // per gathered row, had the k-loop at ~11 instructions per DMMA.)
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool GATHER>
 struct Loader {
     const double *a;      // element 0 of this thread's A slots at k0 = 0
     const double *b;      // element 0 of this thread's B slots (no gather) / column base (gather)
@@ -56,6 +56,18 @@ struct Loader {
     int ka, kb;           // k offset of slot 0 within the tile (A / B); slots add 2*i when k varies
     int sa, sb;           // smem offset of slot 0; slot stride below
     int K;
+    int grow[8];          // gathered B rows of the NEXT load() (prefetched one k-tile ahead)
+
+    // indices of the 8 gathered op(B) rows this thread stages for k-tile kt: loaded
+    // one load() ahead so the dependent index read never sits in front of the
+    // cp.async issue (it cost 10-20% on the gathered sweep products)
+    __device__ __forceinline__ void fetch_rows(int kt) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = kt * BK + kb + 2 * i;
+            grow[i] = ((bmask & 1) && k < K) ? __ldg(rows + k) : -1;
+        }
+    }
 
     __device__ __forceinline__ void init(const rsc_gemm_problem &P, const double *A, const double *B, int m0,
                                          int n0) {
@@ -85,13 +97,14 @@ struct Loader {
         ldb = P.ldb;
         if (!TB) {  // op(B) = B (K x N): slot i = k row (t>>6) + 2i, column n = t&63
             const int n = t & 63, kr = t >> 6;
-            rows = P.b_rows;
+            rows = GATHER ? P.b_rows : nullptr;
             b = rows ? B + n0 + n : B + (long long)kr * P.ldb + n0 + n;
             b_i = 2LL * P.ldb;
             b_k = (long long)BK * P.ldb;
             kb = kr;
             sb = kr * PADM + n;
             if (n0 + n < P.N) bmask = 0xffu;
+            if (GATHER && rows) fetch_rows(0);
         } else {    // op(B) = B^T, B stored N x K: slot i = row (t/BK) + 8i, column k = t%BK
             const int k = t % BK, nr = t / BK;
             b = B + (long long)(n0 + nr) * P.ldb + k;
@@ -106,7 +119,7 @@ struct Loader {
     }
 
     // stage k-tile kt into sA / sB
-    __device__ __forceinline__ void load(int kt, double *sA, double *sB) const {
+    __device__ __forceinline__ void load(int kt, double *sA, double *sB) {
         const int k0 = kt * BK;
         if (!TA) {
             const double *p = a + (long long)kt * a_k;
@@ -125,14 +138,13 @@ struct Loader {
             }
         }
         if (!TB) {
-            if (rows) {
+            if (GATHER && rows) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const int k = k0 + kb + 2 * i;
-                    const bool v = (bmask & 1) && k < K;
-                    const int r = v ? __ldg(rows + k) : 0;
-                    cp_async_8(&sB[sb + 2 * i * PADM], b + (long long)r * ldb, v);
+                    const bool v = grow[i] >= 0;
+                    cp_async_8(&sB[sb + 2 * i * PADM], b + (long long)(v ? grow[i] : 0) * ldb, v);
                 }
+                fetch_rows(kt + 1);  // load() is called for consecutive k-tiles
             } else {
                 const double *p = b + (long long)kt * b_k;
 #pragma unroll
@@ -153,7 +165,7 @@ struct Loader {
     }
 };
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool GATHER>
 #ifndef RSC_GEMM_MINB
 #define RSC_GEMM_MINB 1
 #endif
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (P.K + BK - 1) / BK;
-    Loader<TA, TB> ld;
+    Loader<TA, TB, GATHER> ld;
     ld.init(P, A, B, m0, n0);
     if (nk > 0) {
         // STAGES-deep cp.async pipeline, one CTA barrier per k-tile
@@ -257,15 +269,15 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
     }
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool GATHER>
 int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
     if (tiles <= 0) return 0;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_grouped_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        cudaFuncSetAttribute(gemm_grouped_kernel<TA, TB, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
         attr = true;
     }
-    gemm_grouped_kernel<TA, TB><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
+    gemm_grouped_kernel<TA, TB, GATHER><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
     RSC_CHECK_LAUNCH();
     return 0;
 }
@@ -283,6 +295,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
     while (i < count) {
         args.count = 0;
         long long tiles = 0;
+        bool gather = false;
         while (i < count && args.count < MAXP) {
             const rsc_gemm_problem &p = problems[i++];
             if (p.M <= 0 || p.N <= 0 || p.batch <= 0) continue;
@@ -291,16 +304,21 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
             const long long tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
             args.tile_begin[args.count] = tiles;
             args.p[args.count] = p;
+            gather |= p.b_rows != nullptr;
             tiles += tm * tn * p.batch;
             args.count++;
         }
         if (args.count == 0) continue;
         args.tile_begin[args.count] = tiles;
         int rc;
-        if (!transA && !transB) rc = launch_chunk<false, false>(args, tiles, s);
-        else if (!transA && transB) rc = launch_chunk<false, true>(args, tiles, s);
-        else if (transA && !transB) rc = launch_chunk<true, false>(args, tiles, s);
-        else rc = launch_chunk<true, true>(args, tiles, s);
+        // the gathered-B loader is its own instantiation: its index prefetch costs the
+        // plain kernels ~2.5% (registers), it is only used for launches that gather
+        if (!transA && !transB) rc = gather ? launch_chunk<false, false, true>(args, tiles, s)
+                                            : launch_chunk<false, false, false>(args, tiles, s);
+        else if (!transA && transB) rc = launch_chunk<false, true, false>(args, tiles, s);
+        else if (transA && !transB) rc = gather ? launch_chunk<true, false, true>(args, tiles, s)
+                                                : launch_chunk<true, false, false>(args, tiles, s);
+        else rc = launch_chunk<true, true, false>(args, tiles, s);
         if (rc) return rc;
     }
     return 0;

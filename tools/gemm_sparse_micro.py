@@ -43,11 +43,12 @@ def bench(nprob, M, N, K, transA=False, atomic=False, gather=False, scatter=Fals
     return 2.0 * nprob * M * N * K / ms / 1e9
 
 
-for (n, M, N, K) in ((150, 512, 256, 448), (150, 512, 64, 448), (150, 2048, 128, 96), (150, 128, 128, 2048)):
-    for ta in (False, True):
-        base = bench(n, M, N, K, ta)
-        at = bench(n, M, N, K, ta, atomic=True)
-        ga = bench(n, M, N, K, ta, gather=True)
-        sc = bench(n, M, N, K, ta, atomic=True, scatter=True)
-        print(f"{n}x M{M} N{N} K{K} TA={int(ta)}: plain {base:5.1f}  atomic {at:5.1f}  gather {ga:5.1f}  "
-              f"atomic+scatter {sc:5.1f} TF/s")
+if __name__ == "__main__":
+    for (n, M, N, K) in ((150, 512, 256, 448), (150, 512, 64, 448), (150, 2048, 128, 96), (150, 128, 128, 2048)):
+        for ta in (False, True):
+            base = bench(n, M, N, K, ta)
+            at = bench(n, M, N, K, ta, atomic=True)
+            ga = bench(n, M, N, K, ta, gather=True)
+            sc = bench(n, M, N, K, ta, atomic=True, scatter=True)
+            print(f"{n}x M{M} N{N} K{K} TA={int(ta)}: plain {base:5.1f}  atomic {at:5.1f}  gather {ga:5.1f}  "
+                  f"atomic+scatter {sc:5.1f} TF/s")
