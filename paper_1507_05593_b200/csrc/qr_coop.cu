@@ -50,7 +50,11 @@ struct MArgs {
 struct Ws {
     double *cols, *vn1, *vn2, *tau, *diagR, *vbuf;
     int *perm;
+    double *cand_v;  // per-CTA pivot candidate of the next step: largest vn1 ...
+    int *cand_p;     // ... and its position (CQ_MAX slots each)
 };
+
+constexpr int CQ_MAX = 256;  // >= CTAs of one matrix group (<= SM count)
 
 __device__ __forceinline__ Ws carve(const MatDesc &d) {
     Ws w;
@@ -61,6 +65,8 @@ __device__ __forceinline__ Ws carve(const MatDesc &d) {
     w.diagR = w.tau + d.k;
     w.vbuf = w.diagR + d.k;
     w.perm = reinterpret_cast<int *>(w.vbuf + d.m);
+    w.cand_v = w.vbuf + d.m + d.k;
+    w.cand_p = reinterpret_cast<int *>(w.cand_v + CQ_MAX);
     return w;
 }
 
@@ -81,10 +87,43 @@ __device__ __forceinline__ void group_barrier(unsigned *ctr, int nblk, unsigned 
     ++epoch;
 }
 
+// This CTA's pivot candidate for step i: the largest vn1 among its owned columns
+// still at positions >= i (first position on ties; NaN never wins), published to
+// cand[lb] for the group.  The next pivot search then reads one candidate per CTA
+// instead of walking all k norms through L2 (a serial chain of ~k/32 dependent L2
+// loads per column step on the large sketches).
+__device__ __forceinline__ void publish_candidate(const Ws &w, const int *posof, int c0, int c1, int i, int lb,
+                                                  double *red, int *redp) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    double best = -1.0;
+    int bp = 0x7fffffff;
+    for (int phys = c0 + t; phys < c1; phys += CT) {
+        const int ps = posof[phys];
+        if (ps < i) continue;
+        const double vv = w.vn1[phys];
+        if (vv > best || (vv == best && ps < bp)) { best = vv; bp = ps; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+    }
+    if (lane == 0) { red[warp] = best; redp[warp] = bp; }
+    __syncthreads();
+    if (t == 0) {
+        for (int q = 1; q < CT / 32; ++q)
+            if (red[q] > best || (red[q] == best && redp[q] < bp)) { best = red[q]; bp = redp[q]; }
+        w.cand_v[lb] = best;
+        w.cand_p[lb] = bp;
+    }
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[32];
+    __shared__ int redp[32];
     __shared__ int piv_s;
     // locate this CTA's matrix
     int g = 0;
@@ -115,17 +154,21 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
         s = sqrt(warp_sum(s));
         if (lane == 0) { w.vn1[c0 + j] = s; w.vn2[c0 + j] = s; }
     }
+    __syncthreads();
+    publish_candidate(w, posof, c0, c1, 0, lb, red, redp);
     group_barrier(bar, nblk, epoch);
 
     const int kmin = m < k ? m : k;
     for (int i = 0; i < kmin; ++i) {
-        // 1. pivot: first position j >= i with the largest vn1 (identical in every CTA)
+        // 1. pivot: first position j >= i with the largest vn1 (identical in every CTA),
+        // reduced over the group's per-CTA candidates
         if (warp == 0) {
             double best = -1.0;
             int bp = k;
-            for (int j = i + lane; j < k; j += 32) {
-                const double vv = __ldcg(w.vn1 + pos2phys[j]);
-                if (vv > best) { best = vv; bp = j; }
+            for (int b = lane; b < nblk; b += 32) {
+                const double vv = __ldcg(w.cand_v + b);
+                const int pp = __ldcg(w.cand_p + b);
+                if (vv > best || (vv == best && pp < bp)) { best = vv; bp = pp; }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -212,6 +255,10 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
                 }
             }
             __syncwarp();
+        }
+        if (i + 1 < kmin) {
+            __syncthreads();
+            publish_candidate(w, posof, c0, c1, i + 1, lb, red, redp);
         }
         group_barrier(bar, nblk, epoch);
     }
@@ -673,12 +720,12 @@ long long rsc_qrcp_coop_doubles(int m, int k) {
     const long long ldw = m | 1;
     const long long kmin = m < k ? m : k;
     // factorization | explicit V (m x kmin) | W_b (QB x kmin) | Gram, T (QB x QB each)
-    return ldw * k + 4LL * k + m + k + 64 + (long long)m * kmin + QB * kmin + 2LL * QB * QB + 64;
+    return ldw * k + 4LL * k + m + k + 2 * CQ_MAX + 64 + (long long)m * kmin + QB * kmin + 2LL * QB * QB + 64;
 }
 
 static inline double *wy_base(double *W, int m, int k) {
     const long long ldw = m | 1;
-    return W + ldw * k + 4LL * k + m + k + 64;
+    return W + ldw * k + 4LL * k + m + k + 2 * CQ_MAX + 64;
 }
 
 int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *problems, int count, void *stream);

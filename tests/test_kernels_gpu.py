@@ -146,6 +146,28 @@ def test_orthonormalize_multi_cta_path(cuda, m, k, true_rank):
     assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
 
 
+@pytest.mark.parametrize("m,k,true_rank", [(4096, 600, 250), (1000, 300, None), (30000, 96, 40)])
+def test_orthonormalize_cooperative_kernel(cuda, monkeypatch, m, k, true_rank):
+    """The cooperative multi-CTA QRCP itself (cluster path disabled): shared-memory
+    column groups of ~100 CTAs (4096 x 600: more per-CTA pivot candidates than one
+    warp's lanes) and the global-memory column path (30000 x 96).  Kept rank exact,
+    span to 1e-10 against the oracle."""
+    from oracle import kernels as ok
+    from paper_1507_05593_b200 import kernels as K
+
+    monkeypatch.setenv("RSC_QR_NOCLUSTER", "1")
+    rng = np.random.default_rng(m + 7 * k)
+    if true_rank is None:
+        G = rng.standard_normal((m, k))
+    else:
+        G = rng.standard_normal((m, true_rank)) @ rng.standard_normal((true_rank, k))
+    Q = K.orthonormalize(G)
+    Qo = ok.orth(G)
+    assert Q.shape == Qo.shape
+    assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() < 1e-12
+    assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
+
+
 def test_qrcp_batched_mixed_sizes_concurrent(cuda):
     """One batched call mixing one-CTA sketches and multi-CTA groups (run concurrently)."""
     import torch

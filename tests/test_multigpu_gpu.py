@@ -39,4 +39,8 @@ def test_sharded_factorization_matches_single_gpu(cuda, world):
         assert abs(g1 - gd) <= 1e-9 * g1, (name, c)
         # compressed blocks: the same band as two single-GPU runs (FP64 atomic sums)
         assert c["apply_relerr"] < max(1e-8, 10 * c["apply_relerr_self"]), (name, c)
-        assert abs(c["pcg_its"][0] - c["pcg_its"][1]) <= 1 and c["x_relerr"] < 1e-8, (name, c)
+        # PCG stops at relres 1e-6, so x inherits the preconditioner's run-to-run noise
+        # amplified by the solve: the same band rule as the apply (sharded vs single
+        # GPU measured 1.0-1.15e-8 on l3d20 in some runs, below 1e-8 in others)
+        assert abs(c["pcg_its"][0] - c["pcg_its"][1]) <= 1, (name, c)
+        assert c["x_relerr"] < max(1e-8, 10 * c["x_relerr_self"]), (name, c)

@@ -37,6 +37,7 @@ def main():
         z2 = F2.apply(b)
         x1, r1 = pcg_solve(A, b, preconditioner=F1, tol=1e-6)
         xd, rd = pcg_solve(A, b, preconditioner=Fd, tol=1e-6)
+        x2, _ = pcg_solve(A, b, preconditioner=F2, tol=1e-6)
         out[name] = {
             "n": A.n,
             "owned_units": int((owners == rank).sum()), "top_units": int((owners == -1).sum()),
@@ -49,6 +50,7 @@ def main():
             "apply_relerr_self": float(np.linalg.norm(z2 - z1) / np.linalg.norm(z1)),
             "pcg_its": [r1.iterations, rd.iterations],
             "x_relerr": float(np.linalg.norm(xd - x1) / np.linalg.norm(x1)),
+            "x_relerr_self": float(np.linalg.norm(x2 - x1) / np.linalg.norm(x1)),
         }
     if rank == 0:
         print(json.dumps({"world": world, "backend": backend, "cases": out}), flush=True)
