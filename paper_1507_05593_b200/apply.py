@@ -39,10 +39,22 @@ class _Phase:
 
     def __init__(self):
         self.items = []
+        self.lr = []  # (item index, U data_ptr) of the low-rank factor items: cols = rank
 
-    def add(self, *item):
-        if item[1] > 0 and item[2] > 0:
+    def add(self, *item, lr=None):
+        if lr is not None:  # kept even at rank 0: a later refactorization may raise it
+            if item[1] > 0:
+                self.lr.append((len(self.items), lr))
+                self.items.append(item)
+        elif item[1] > 0 and item[2] > 0:
             self.items.append(item)
+
+
+def _cap(lr):
+    """Column capacity of a low-rank block: its U / V are views of the sketch-padded
+    buffers (numeric._finalize_ranks), so a refactorization's rank fits this."""
+    U = lr.U
+    return U.stride(0) if U.dim() == 2 and U.stride(1) == 1 else lr.k
 
 
 class DeviceApply:
@@ -50,6 +62,7 @@ class DeviceApply:
         # no strong reference back to the factor (it owns this program): a cycle would
         # keep the factor's device arena alive until the cyclic GC runs
         self.n = F.n
+        self.nunits = len(F.units)
         plan = F.plan
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
@@ -63,9 +76,9 @@ class DeviceApply:
         ksum = 0
         for u in units:
             if isinstance(u.off, DevLR):
-                ksum += u.off.k
+                ksum += _cap(u.off)
             if isinstance(u.diag, DeviceTree):
-                ksum += sum(b.k for b in u.diag.blocks.values() if isinstance(b, DevLR))
+                ksum += sum(_cap(b) for b in u.diag.blocks.values() if isinstance(b, DevLR))
         self.tall = E.empty(max(2 * ksum, 1))
         self._toff = 0
         uidx = {un.u: i for i, un in enumerate(units)}
@@ -97,13 +110,38 @@ class DeviceApply:
         """Every phase -> one prebuilt rsc_gemv_multi launch (host arrays kept)."""
         lib = _lib.load()
         self.launches = []
+        self._lr_index = []  # (launch, item, U ptr): the items whose cols is a rank
         for ph in self.phases:
+            self._lr_index.extend((len(self.launches), i, key) for i, key in ph.lr)
             c = list(zip(*ph.items))
             arrs = [ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3]), ptr_array(c[4]),
                     ptr_array(c[5]), ptr_array(c[6]), ptr_array(c[7]), int_array(c[8]),
                     np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))]
             self.launches.append((len(ph.items), arrs, [a.ctypes.data for a in arrs]))
         self._fn = lib.rsc_gemv_multi
+
+    def rekey(self, F):
+        """Adopt a refactorization whose kept ranks differ from this program's (the
+        QRCP cutoff sits on rounding-level |R_ii|, so FP64 atomic sums move a few ranks
+        between replays).  Same memory (graph replay), same block structure: only the
+        rank dimension of the low-rank items changes -- patch it in the packed launch
+        arrays and re-capture the graph instead of rebuilding the program (0.2-0.4 s
+        on config[4]).  False if the blocks do not match (caller rebuilds)."""
+        ks = {}
+        for u in F.units:
+            if isinstance(u.off, DevLR):
+                ks[u.off.U.data_ptr()] = u.off.k
+            if isinstance(u.diag, DeviceTree):
+                for b in u.diag.blocks.values():
+                    if isinstance(b, DevLR):
+                        ks[b.U.data_ptr()] = b.k
+        if set(ks) != {key for _, _, key in self._lr_index} or len(F.units) != self.nunits:
+            return False
+        for li, ii, key in self._lr_index:
+            self.launches[li][1][2][ii] = ks[key]
+        self.graph = None
+        self.calls = min(self.calls, self.GRAPH_AFTER)
+        return True
 
     def _run_program(self):
         s = E.stream_handle()
@@ -173,8 +211,7 @@ class DeviceApply:
         written to `out` (base addresses of y / y2)."""
         dense = [u for u in us if isinstance(u.diag, DenseTri)]
         trees = [u for u in us if isinstance(u.diag, DeviceTree)]
-        cpl = [u for u in us if u.rows.size and u.off is not None and
-               (not isinstance(u.off, DevLR) or u.off.k)]
+        cpl = [u for u in us if u.rows.size and u.off is not None]
         if not backward:
             first = _Phase()
             for u in dense:
@@ -196,14 +233,15 @@ class DeviceApply:
             rows = self._rows_ptr(plan, u)
             c0 = 8 * u.c0
             if isinstance(u.off, DevLR):
-                k, t = u.off.k, self._t(u.off.k)
+                k, t = u.off.k, self._t(_cap(u.off))
                 U, V = u.off.U, u.off.V
+                key = U.data_ptr()
                 if not backward:  # t = U^T w ; y[R] -= V t
-                    a.add(U.data_ptr(), u.ncols, k, E.ld(U), out + c0, 0, t, 0, 1, 1.0)
-                    b.add(V.data_ptr(), u.rows.size, k, E.ld(V), t, 0, rhs, rows, 0, -1.0)
+                    a.add(U.data_ptr(), u.ncols, k, E.ld(U), out + c0, 0, t, 0, 1, 1.0, lr=key)
+                    b.add(V.data_ptr(), u.rows.size, k, E.ld(V), t, 0, rhs, rows, 0, -1.0, lr=key)
                 else:  # t = V^T y[R] ; w -= U t
-                    a.add(V.data_ptr(), u.rows.size, k, E.ld(V), out, rows, t, 0, 1, 1.0)
-                    b.add(U.data_ptr(), u.ncols, k, E.ld(U), t, 0, rhs + c0, 0, 0, -1.0)
+                    a.add(V.data_ptr(), u.rows.size, k, E.ld(V), out, rows, t, 0, 1, 1.0, lr=key)
+                    b.add(U.data_ptr(), u.ncols, k, E.ld(U), t, 0, rhs + c0, 0, 0, -1.0, lr=key)
             elif not backward:  # y[R] -= L_O w
                 a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out + c0, 0, rhs, rows, 0, -1.0)
             else:  # w -= L_O^T y[R]
@@ -238,12 +276,11 @@ class DeviceApply:
                 _, b, Xs, Yd, tr = op
                 xp, yp = out + off(Xs), rhs + off(Yd)
                 if isinstance(b, DevLR):
-                    if not b.k:
-                        continue
-                    t = self._t(b.k)
+                    t = self._t(_cap(b))
                     P1, P2 = (b.V, b.U) if tr else (b.U, b.V)
-                    cur.add(P1.data_ptr(), P1.shape[0], b.k, E.ld(P1), xp, 0, t, 0, 1, 1.0)
-                    second.add(P2.data_ptr(), P2.shape[0], b.k, E.ld(P2), t, 0, yp, 0, 0, -1.0)
+                    key = b.U.data_ptr()
+                    cur.add(P1.data_ptr(), P1.shape[0], b.k, E.ld(P1), xp, 0, t, 0, 1, 1.0, lr=key)
+                    second.add(P2.data_ptr(), P2.shape[0], b.k, E.ld(P2), t, 0, yp, 0, 0, -1.0, lr=key)
                 else:  # Y -= B X (forward) or Y -= B^T X (transposed)
                     cur.add(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), xp, 0, yp, 0, 1 if tr else 0, -1.0)
             self._emit(cur)

@@ -958,9 +958,14 @@ def factorize(A, config=None, coords=None, prepared=None):
     if entry is not None:
         entry.owner = weakref.ref(F)  # the graph may rewrite this memory once F is gone
         F._entry = entry
-        if entry.apply is not None and entry.apply_key == F._apply_key():
-            F._apply = entry.apply  # same memory, same ranks: the apply program still holds
-            F._apply.refresh_inverses()  # ... once its explicit inverses are re-derived
+        if entry.apply is not None:
+            key = F._apply_key()
+            # same memory, same ranks: the apply program still holds once its explicit
+            # inverses are re-derived; other ranks: patch its rank dimensions first
+            if entry.apply_key == key or entry.apply.rekey(F):
+                F._apply = entry.apply
+                F._apply.refresh_inverses()
+                entry.apply_key = key
     part = sym.partition
     st = F.stats
     st.n, st.nnz_lower = A.n, A.nnz_lower

@@ -203,3 +203,42 @@ def test_graph_refactorization_replays(cuda):
     del H
     K = factorize(A1, prepared=prep)           # and back
     assert relerr(K.apply(r), ref1) < 3e-8
+
+
+def test_graph_refactorization_new_ranks_patches_apply(cuda):
+    """A replay whose kept ranks differ from the previous factor's keeps the apply
+    program (its rank dimensions patched, graph re-captured) and still equals a fresh
+    factorization's apply."""
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.factor import SolverConfig, prepare
+    from paper_1507_05593_b200.problems import laplacian_3d
+    from paper_1507_05593_b200.sparse import SparseSpdMatrix
+
+    A1, coords = laplacian_3d(14)
+    cfg = SolverConfig(tau_o=32, oversample=10, alpha_o=1.0, alpha_d=0.5, tau_d=64, power_iters=1, seed=0)
+    rng = np.random.default_rng(8)
+    v = A1.values.copy()
+    off = np.ones(v.size, dtype=bool)
+    off[A1.col_ptr[:-1]] = False
+    v[off] *= rng.uniform(0.05, 1.0, off.sum())  # strongly varying coefficients: other ranks
+    A2 = SparseSpdMatrix(A1.n, A1.col_ptr, A1.row_idx, v)
+    r = rng.standard_normal(A1.n)
+    F2ref = factorize(A2, cfg, coords=coords)
+    ref2 = F2ref.apply(r)
+    prep = prepare(A1, cfg, coords)
+    del F2ref
+    F0 = factorize(A1, prepared=prep)  # eager
+    del F0
+    F = factorize(A1, prepared=prep)   # capture + replay
+    ranks1 = dict(F.ranks)
+    for _ in range(5):                 # builds the apply program and captures its graph
+        F.apply(r)
+    prog = F._apply
+    assert prog.graph not in (None, False)
+    del F
+    H = factorize(A2, prepared=prep)   # replay on new values
+    assert H.ranks != ranks1
+    assert H._apply is prog            # patched, not rebuilt
+    for _ in range(5):                 # eager, then the re-captured graph
+        assert relerr(H.apply(r), ref2) < 3e-8
+    assert prog.graph not in (None, False)
