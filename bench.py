@@ -287,6 +287,23 @@ def run_b200_cfg1(args, rank, world, torch, dist):
             te = float(tt.item())
         e2e = {"value": world * flops / te / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": bs.h2d_bytes(),
                "d2h_bytes_per_step": bs.d2h_bytes(), "seconds_per_step": te}
+        # the e2e pass is host-link bound: its roofline is the pinned H2D copy rate of
+        # this box (one 1 GiB pinned -> device copy, CUDA events, best of 3)
+        del Dh, Bh
+        hb = torch.empty(1 << 27, dtype=torch.float64).pin_memory()
+        db = torch.empty(1 << 27, dtype=torch.float64, device="cuda")
+        best = 0.0
+        for _ in range(3):
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            db.copy_(hb, non_blocking=True)
+            s1.record()
+            torch.cuda.synchronize()
+            best = max(best, hb.numel() * 8 / (s0.elapsed_time(s1) * 1e-3) / 1e9)
+        del hb, db
+        ach = bs.h2d_bytes() / te / 1e9
+        e2e["link_roofline"] = {"bound": "pcie_h2d", "achieved": ach, "peak": best, "unit": "GB/s",
+                                "frac": ach / best, "peak_source": "pinned 1 GiB H2D copy measured in this run"}
 
     if rank != 0:
         return

@@ -145,6 +145,36 @@ def run_sparse(args, rank, world, torch, dist):
     busy_s = sum(e.device_time for e in kev) / 1e6
     prof = {"flops": gemm_flops, "seconds": gemm_s}
     peak = B.fp64_peak_tflops(torch)
+    # HBM-bound kernels of the PCG: the preconditioner apply (its replayed graph) and
+    # the CSR SpMV, CUDA events around 20 back-to-back calls each.  Algorithmic bytes
+    # (SURVEY §8(d)): apply = 16 B per stored factor scalar (read once in each sweep)
+    # + 48 B per row of vectors; SpMV = 12 B per stored nonzero + 4(n+1) + 16n.
+    hbm, hbm_src = B.hbm_peak()
+    zd, yd = torch.empty_like(bd), torch.empty_like(bd)
+    S = A.device_csr()
+
+    def timed(fn, reps=20):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / reps
+
+    t_ap = timed(lambda: F.apply_device(bd, zd))
+    t_sp = timed(lambda: E.spmv(S, bd, yd))
+    b_ap = 16.0 * st.stored_scalars + 48.0 * n
+    b_sp = 12.0 * S.nnz + 4.0 * (n + 1) + 16.0 * n
+    hbm_line = {
+        "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": hbm_src,
+        "apply": {"seconds": t_ap, "bytes": b_ap, "achieved": b_ap / t_ap / 1e9, "frac": b_ap / t_ap / 1e9 / hbm},
+        "spmv": {"seconds": t_sp, "bytes": b_sp, "achieved": b_sp / t_sp / 1e9, "frac": b_sp / t_sp / 1e9 / hbm,
+                 "l2_resident": bool(b_sp < 100e6)},
+    }
     # end to end through the public API (host A, coords, b in; host x out)
     t0 = time.perf_counter()
     for _ in range(max(1, min(args.steps, 2))):
@@ -186,6 +216,7 @@ def run_sparse(args, rank, world, torch, dist):
                      "kernel_seconds": prof["seconds"], "kernel_share_of_step": prof["seconds"] / t,
                      "all_kernels_seconds": busy_s,
                      "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run"},
+        "hbm_roofline": hbm_line,
         "cpu_baseline": cpu,
         "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(8 * (A.nnz_lower * 2 + n)),
                 "d2h_bytes_per_step": int(8 * n)},
