@@ -155,6 +155,18 @@ int rsc_gemv_multi(int count, const double *const *M, const int *rows, const int
                    const int *ldm, const double *const *x, const int *const *xidx,
                    double *const *y, const int *const *yidx, const int *modes,
                    const double *alphas, void *stream);
+/* Device-resident form of one rsc_gemv_multi phase for phases with more problems than
+ * one kernel parameter block holds (the apply program is static after factorization,
+ * factor.py:175-218): rsc_gemv_describe fills `desc` (count x rsc_gemv_desc_bytes()
+ * bytes, host memory; the caller uploads it) and blocks[i] = CTAs of problem i;
+ * rsc_gemv_multi_dev runs the phase as one launch from the uploaded descriptors and a
+ * block -> problem map (int32, total_blocks entries = the repeat of i by blocks[i]). */
+int rsc_gemv_desc_bytes(void);
+int rsc_gemv_describe(int count, const double *const *M, const int *rows, const int *cols,
+                      const int *ldm, const double *const *x, const int *const *xidx,
+                      double *const *y, const int *const *yidx, const int *modes,
+                      const double *alphas, void *desc, long long *blocks);
+int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long long total_blocks, void *stream);
 
 
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */

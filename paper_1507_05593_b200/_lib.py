@@ -42,6 +42,9 @@ EXPORTED = (
     "rsc_trsv_batched",
     "rsc_gemv_batched",
     "rsc_gemv_multi",
+    "rsc_gemv_desc_bytes",
+    "rsc_gemv_describe",
+    "rsc_gemv_multi_dev",
     "rsc_identity_batched",
     "rsc_transpose_batched",
     "rsc_gather_rows",
@@ -92,6 +95,9 @@ _SIGS = {
     "rsc_trsv_batched": (I, [I, P, P, P, P, P, I, P]),
     "rsc_gemv_batched": (I, [I, P, P, P, P, P, P, P, P, I, D, P]),
     "rsc_gemv_multi": (I, [I, P, P, P, P, P, P, P, P, P, P, P]),
+    "rsc_gemv_desc_bytes": (I, []),
+    "rsc_gemv_describe": (I, [I, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "rsc_gemv_multi_dev": (I, [P, P, LL, P]),
 
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_identity_batched": (I, [I, P, P, P, P]),

@@ -119,6 +119,24 @@ class DeviceApply:
                     np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))]
             self.launches.append((len(ph.items), arrs, [a.ctypes.data for a in arrs]))
         self._fn = lib.rsc_gemv_multi
+        self._build_dev()
+
+    DEV_MIN = 225  # phases with more problems than one parameter block (GMAXP = 224)
+
+    def _build_dev(self):
+        """Large phases run from device-resident descriptors: one launch per phase
+        (rsc_gemv_multi_dev) instead of one per 224 problems."""
+        lib = _lib.load()
+        db = lib.rsc_gemv_desc_bytes()
+        self.dev = {}
+        for li, (n, _, args) in enumerate(self.launches):
+            if n < self.DEV_MIN:
+                continue
+            desc = np.empty(n * db, dtype=np.uint8)
+            blocks = np.empty(n, dtype=np.int64)
+            _lib.check(lib.rsc_gemv_describe(n, *args, desc.ctypes.data, blocks.ctypes.data), "rsc_gemv_describe")
+            b2p = np.repeat(np.arange(n, dtype=np.int32), blocks)
+            self.dev[li] = (E.to_dev(desc), E.to_dev(b2p), int(b2p.size))
 
     def rekey(self, F):
         """Adopt a refactorization whose kept ranks differ from this program's (the
@@ -139,14 +157,20 @@ class DeviceApply:
             return False
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]
+        self._build_dev()  # the device descriptors carry the ranks too
         self.graph = None
         self.calls = min(self.calls, self.GRAPH_AFTER)
         return True
 
     def _run_program(self):
         s = E.stream_handle()
-        for n, _, args in self.launches:
-            _lib.check(self._fn(n, *args, s), "rsc_gemv_multi")
+        dev, fdev = self.dev, _lib.load().rsc_gemv_multi_dev
+        for li, (n, _, args) in enumerate(self.launches):
+            if li in dev:
+                d, b2p, tot = dev[li]
+                _lib.check(fdev(d.data_ptr(), b2p.data_ptr(), tot, s), "rsc_gemv_multi_dev")
+            else:
+                _lib.check(self._fn(n, *args, s), "rsc_gemv_multi")
 
     # -- program construction ------------------------------------------------------
     def _build_inverses(self, units):

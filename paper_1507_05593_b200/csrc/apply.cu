@@ -10,6 +10,8 @@
 //  gemv_batched : y[yidx[r]] += alpha * M[r,:] . x[xidx]     (trans = 0, warp per row)
 //                 y[c]       += alpha * sum_r M[r,c] x[xidx[r]]  (trans = 1, thread per column)
 //                 FP64 atomics on the output (units of one level share target rows).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -238,6 +240,22 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
     gemv_block(a.p[p], blk - a.p[p].blk_begin, xr, part);
 }
 
+// The same block for phases with more problems than one parameter block holds: the
+// descriptors live in device memory (static after factorization, uploaded once) with a
+// block -> problem map, so a whole phase is ONE launch instead of ceil(count / GMAXP)
+// back-to-back launches (config[4]'s interior-coupling phases have 4546 problems: 21
+// launches of ~19 us, each paying its own ramp and tail).  The descriptor does not
+// depend on the previous phase, so it is fetched before the dependency wait.
+__global__ void __launch_bounds__(T) gemv_dev_kernel(const GemvProb *__restrict__ P, const int *__restrict__ b2p) {
+    __shared__ double xr[SLAB];
+    __shared__ double part[T];
+    const long long blk = blockIdx.x;
+    const GemvProb d = P[__ldg(b2p + blk)];
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    gemv_block(d, blk - d.blk_begin, xr, part);
+}
+
 inline int pow2ceil(int v) {
     int p = 1;
     while (p < v) p <<= 1;
@@ -278,8 +296,11 @@ int gemv_launch(int count, const double *const *M, const int *rows, const int *c
         a.total = blocks;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
+        // RSC_APPLY_NO_PDL: plain stream order (profiling only: with PDL a launch's
+        // recorded duration includes its wait for the previous phase)
+        static const bool no_pdl = getenv("RSC_APPLY_NO_PDL") != nullptr;
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
+        at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
         cfg.gridDim = dim3((unsigned)blocks);
         cfg.blockDim = dim3(T);
         cfg.stream = s;
@@ -331,6 +352,47 @@ extern "C" int rsc_gemv_batched(int count, const double *const *M, const int *ro
     if (!M || !rows || !cols || !ldm || !x || !y) return -2;
     return gemv_launch(count, M, rows, cols, ldm, x, xidx, y, yidx, nullptr, mode, nullptr, alpha,
                        (cudaStream_t)stream);
+}
+
+extern "C" int rsc_gemv_desc_bytes(void) { return (int)sizeof(GemvProb); }
+
+extern "C" int rsc_gemv_describe(int count, const double *const *M, const int *rows, const int *cols,
+                                 const int *ldm, const double *const *x, const int *const *xidx,
+                                 double *const *y, const int *const *yidx, const int *modes,
+                                 const double *alphas, void *desc, long long *blocks) {
+    if (count < 0) return -1;
+    if (count > 0 && (!M || !rows || !cols || !ldm || !x || !y || !modes || !alphas || !desc || !blocks)) return -2;
+    GemvProb *d = static_cast<GemvProb *>(desc);
+    long long total = 0;
+    for (int i = 0; i < count; ++i) {
+        d[i] = GemvProb{};
+        d[i].blk_begin = total;
+        if (rows[i] <= 0 || cols[i] <= 0) { blocks[i] = 0; continue; }
+        blocks[i] = describe(d[i], M[i], rows[i], cols[i], ldm[i], x[i], xidx ? xidx[i] : nullptr, y[i],
+                             yidx ? yidx[i] : nullptr, modes[i], alphas[i]);
+        d[i].blk_begin = total;
+        total += blocks[i];
+    }
+    return 0;
+}
+
+extern "C" int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long long total_blocks, void *stream) {
+    if (total_blocks < 0) return -1;
+    if (total_blocks == 0) return 0;
+    if (!desc || !blk2prob || total_blocks > 0x7fffffffLL) return -2;
+    static const bool no_pdl = getenv("RSC_APPLY_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.gridDim = dim3((unsigned)total_blocks);
+    cfg.blockDim = dim3(T);
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_dev_kernel, static_cast<const GemvProb *>(desc), blk2prob);
+    rsc_count_launch();
+    return e == cudaSuccess ? 0 : (int)e;
 }
 
 extern "C" int rsc_gemv_multi(int count, const double *const *M, const int *rows, const int *cols,
