@@ -26,6 +26,12 @@ if freeze:
 gcs = []
 gc.callbacks.append(lambda phase, info: gcs.append((phase, info["generation"], time.perf_counter())))
 F = None
+
+
+class step_var_prev:
+    ap = None
+
+
 for it in range(8):
     F = None
     torch.cuda.synchronize()
@@ -38,8 +44,16 @@ for it in range(8):
     x, rep = pcg_solve_device(A, bd, preconditioner=F, tol=1e-6)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
+    ap = getattr(F, "_apply", None)
+    same = ap is not None and ap is getattr(step_var_prev, "ap", None)
+    step_var_prev.ap = ap
+    t4 = time.perf_counter()
+    F.apply_device(bd, x)  # one more apply, timed on the host (graph replay or re-capture)
+    torch.cuda.synchronize()
+    t5 = time.perf_counter()
     g = gcs[n0:]
     gen2 = sum(1 for p, gen, _ in g if p == "start" and gen == 2)
     gct = sum(b[2] - a[2] for a, b in zip(g[::2], g[1::2]))
     print(f"{'freeze' if freeze else 'gc'} step {it}: factorize host {t1 - t0:.3f} +sync {t2 - t1:.3f}  pcg {t3 - t2:.3f} "
-          f"({rep.iterations} its)  gc runs {len(g) // 2} (gen2 {gen2}) {gct:.3f}s", flush=True)
+          f"({rep.iterations} its; program {'reused' if same else 'new'}, next apply {1e3 * (t5 - t4):.1f} ms, "
+          f"pcg phases {getattr(rep, 'wall_times', None)})  gc runs {len(g) // 2} (gen2 {gen2}) {gct:.3f}s", flush=True)
