@@ -36,8 +36,15 @@ extern "C" {
  *   b_rows : row k of op(B) is read from B row b_rows[k]        (transB == 0 only)
  *   c_rows : row m of the result goes to C row c_rows[m]
  *   c_cols : column n of the result goes to C column c_cols[n]
- * atomic != 0: C += alpha*op(A)op(B) with FP64 atomics (beta ignored) so that
- * several problems of one launch may scatter into the same target block. */
+ * atomic != 0: C += alpha*op(A)op(B) (beta ignored), and several problems of one
+ * launch may scatter into the same target block.  These sums are DETERMINISTIC:
+ * each such problem's product is stored to a private partial in the stream's GEMM
+ * workspace (rsc_gemm_set_workspace), then an ordered reduction adds the partials
+ * into C in problem order (for every element of C: C + P_first + ... + P_last,
+ * the left-to-right order of rschol's `UD -= ...` loops, factor.py:389-398).
+ * c_rows / c_cols of accumulating problems must be strictly increasing, and
+ * ext_r x ext_c gives the extent of the target block C (rows x columns reachable
+ * through the maps; 0 = M x N, allowed only without maps). */
 typedef struct {
     const double *A;
     const double *B;
@@ -51,7 +58,15 @@ typedef struct {
     int batch;
     int atomic;
     double alpha, beta;
+    int ext_r, ext_c;
 } rsc_gemm_problem;
+
+/* Device workspace for the ordered accumulation of a stream's grouped GEMMs
+ * (partials of every atomic problem of a launch chunk).  as_default != 0 registers
+ * it for every stream without its own workspace.  A launch whose chunk does not
+ * fit is cut into several ordered chunks; a single problem larger than the
+ * workspace returns -6.  No workspace and an atomic problem: -6. */
+int rsc_gemm_set_workspace(void *stream, void *ws_dev, long long bytes, int as_default);
 
 /* Grouped FP64 tensor-core (DMMA) GEMM.  Replaces every numpy `@` on the
  * factorization path: factor.py:383-398 (_assemble_schur), factor.py:444-455 and

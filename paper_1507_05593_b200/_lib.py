@@ -12,7 +12,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RSC_B200_LIB", os.path.join(_HERE, "librsc_b200.so"))  # override: experiments only
 
-# numpy mirror of rsc_gemm_problem (include/rsc_b200.h); 120 bytes, naturally aligned
+# numpy mirror of rsc_gemm_problem (include/rsc_b200.h); 128 bytes, naturally aligned
 GEMM_DTYPE = np.dtype(
     [
         ("A", "u8"), ("B", "u8"), ("C", "u8"),
@@ -22,13 +22,15 @@ GEMM_DTYPE = np.dtype(
         ("lda", "i4"), ("ldb", "i4"), ("ldc", "i4"),
         ("batch", "i4"), ("atomic", "i4"),
         ("alpha", "f8"), ("beta", "f8"),
+        ("ext_r", "i4"), ("ext_c", "i4"),
     ]
 )
-assert GEMM_DTYPE.itemsize == 120
+assert GEMM_DTYPE.itemsize == 128
 
 # every symbol include/rsc_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "rsc_gemm_grouped",
+    "rsc_gemm_set_workspace",
     "rsc_potrf_batched",
     "rsc_trsm_batched",
     "rsc_trsm_right_batched",
@@ -82,6 +84,7 @@ LL = ctypes.c_longlong
 
 _SIGS = {
     "rsc_gemm_grouped": (I, [I, I, P, I, P]),
+    "rsc_gemm_set_workspace": (I, [P, P, LL, I]),
     "rsc_potrf_batched": (I, [I, P, P, P, P, P, P]),
     "rsc_trsm_batched": (I, [I, I, I, P, P, P, P, P, P, P, P]),
     "rsc_trsm_right_batched": (I, [I, P, P, P, P, P, P, P, P, P]),

@@ -1,12 +1,13 @@
 // Grouped FP64 DMMA GEMM with optional gather (rows of op(B)) and scatter (rows /
-// columns of C) index maps and an atomic-accumulate epilogue.
+// columns of C) index maps, and a DETERMINISTIC ordered accumulation for problems
+// that share a target block.
 //
 // This is the workhorse of the numeric factorization: every Schur update
 // (gather panel rows -> DMMA -> scatter-subtract into the target block), every
 // implicit sketch product and every blocked triangular solve step is one problem of
 // a grouped launch.  One CTA computes one 64x64 tile of one problem; the problem
 // descriptors travel in the kernel parameter block (__grid_constant__, up to
-// RSC_GEMM_MAXP per launch), so a launch needs no descriptor upload.
+// MAXP per launch), so a launch needs no descriptor upload.
 //
 // Tile: 64x64x16, 128 threads = 2x2 warps of 32x32 (4x4 DMMA.8x8x4 fragments,
 // 32 FP64 accumulators per thread).  Operands are staged global->shared with
@@ -14,7 +15,23 @@
 // shared layouts are chosen per transpose case so both the cp.async stores and the
 // fragment loads are bank-conflict-free (a 32-lane FP64 fragment load = 2
 // wavefronts, the minimum).
+//
+// Accumulating problems (atomic != 0: Schur sums over update sources, implicit
+// products over sources, split-K slabs) never race on C.  The host wrapper
+// redirects each such problem's product to a private dense partial in the stream's
+// workspace (plain coalesced stores), and ordered_reduce_kernel then adds the
+// partials into C: one CTA owns a band of TR target rows of one target block and
+// walks that block's problems in launch order, so every element of C receives
+// C + P_1 + P_2 + ... in a fixed order -- the left-to-right `UD -= ...` order of
+// the reference loops (factor.py:389-398, 445-455; diagblocks.py:231-262), and
+// bit-identical results from run to run.  (Round 1 used FP64 atomicAdd here; the
+// summation order then varied between runs and moved QRCP rank decisions that sit
+// within rounding of the cutoff.)
 #include "common.cuh"
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
 
 namespace {
 
@@ -241,7 +258,8 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
         }
     }
 
-    // epilogue
+    // epilogue (accumulating problems were redirected to private partials by the
+    // host wrapper: here every problem is a plain store / read-modify-write)
     const double alpha = P.alpha, beta = P.beta;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -257,15 +275,95 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
                 const int ccol = P.c_cols ? __ldg(P.c_cols + col) : col;
                 double *dst = C + crow + ccol;
                 const double v = alpha * acc[i][j][e];
-                if (P.atomic) {
-                    atomicAdd(dst, v);
-                } else if (beta == 0.0) {
+                if (beta == 0.0) {
                     *dst = v;
                 } else {
                     *dst = v + beta * (*dst);
                 }
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ordered reduction of the partials of accumulating problems
+
+struct RedProb {
+    const double *P;      // partial: batch x M x N, dense
+    const int *c_rows;    // strictly increasing (or null = identity)
+    const int *c_cols;
+    int M, N;
+};
+
+struct RedGroup {
+    double *C;            // target block (all problems of the group share it)
+    long long sC;         // batch stride of C
+    int ldc, ext_r, batch, TR, p0, np;
+};
+
+struct RedArgs {
+    int count;            // groups
+    long long cta_begin[MAXP + 1];
+    RedGroup g[MAXP];
+    RedProb p[MAXP];
+};
+
+constexpr int RT = 256;
+
+__device__ __forceinline__ int lower_bound_dev(const int *a, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constant__ RedArgs a) {
+    __shared__ int s_i0[MAXP], s_i1[MAXP];
+    const long long cta = blockIdx.x;
+    int lo = 0, hi = a.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.cta_begin[mid] <= cta) lo = mid; else hi = mid - 1;
+    }
+    const RedGroup &G = a.g[lo];
+    const long long local = cta - a.cta_begin[lo];
+    const int nt = (G.ext_r + G.TR - 1) / G.TR;
+    const int b = (int)(local / nt);
+    const int t0 = (int)(local - (long long)b * nt) * G.TR;
+    const int t1 = min(t0 + G.TR, G.ext_r);
+    // local row range of every problem inside this band (maps are increasing)
+    for (int q = threadIdx.x; q < G.np; q += RT) {
+        const RedProb &P = a.p[G.p0 + q];
+        int i0, i1;
+        if (P.c_rows) {
+            i0 = lower_bound_dev(P.c_rows, P.M, t0);
+            i1 = i0 + lower_bound_dev(P.c_rows + i0, P.M - i0, t1);
+        } else {
+            i0 = min(t0, P.M);
+            i1 = min(t1, P.M);
+        }
+        s_i0[q] = i0;
+        s_i1[q] = i1;
+    }
+    __syncthreads();
+    double *C = G.C + (long long)b * G.sC;
+    for (int q = 0; q < G.np; ++q) {
+        const int i0 = s_i0[q], i1 = s_i1[q];
+        if (i0 >= i1) continue;  // block-uniform
+        const RedProb &P = a.p[G.p0 + q];
+        const int n = P.N;
+        const double *src = P.P + (long long)b * P.M * n;
+        const int cnt = (i1 - i0) * n;
+        for (int e = threadIdx.x; e < cnt; e += RT) {
+            const int di = e / n;
+            const int i = i0 + di, j = e - di * n;
+            const int r = P.c_rows ? __ldg(P.c_rows + i) : i;
+            const int c = P.c_cols ? __ldg(P.c_cols + j) : j;
+            C[(long long)r * G.ldc + c] += src[(long long)i * n + j];
+        }
+        __syncthreads();  // problem q+1 may hit the same elements through other threads
     }
 }
 
@@ -282,7 +380,101 @@ int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
     return 0;
 }
 
+struct WsEntry {
+    void *stream;
+    char *ptr;
+    long long bytes;
+};
+std::mutex g_ws_mu;
+std::vector<WsEntry> g_ws;
+WsEntry g_ws_default{nullptr, nullptr, 0};
+
+WsEntry lookup_ws(void *stream) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (const WsEntry &e : g_ws)
+        if (e.stream == stream) return e;
+    return g_ws_default;
+}
+
+// Build and launch the ordered reduction for the accumulating problems of one chunk
+// (reds, in launch order).  Groups = distinct (C, strideC, batch) targets, each
+// keeping its problems in order.
+int launch_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<const double *> &parts,
+                  cudaStream_t s) {
+    static thread_local RedArgs ra;
+    const int n = (int)reds.size();
+    std::vector<int> gid(n, -1);
+    std::vector<int> gfirst;
+    for (int i = 0; i < n; ++i) {
+        const rsc_gemm_problem &p = reds[i];
+        int g = -1;
+        for (int k = (int)gfirst.size() - 1; k >= 0; --k) {
+            const rsc_gemm_problem &f = reds[gfirst[k]];
+            if (f.C == p.C && f.strideC == p.strideC && f.batch == p.batch) { g = k; break; }
+        }
+        if (g < 0) {
+            g = (int)gfirst.size();
+            gfirst.push_back(i);
+        }
+        gid[i] = g;
+    }
+    ra.count = (int)gfirst.size();
+    long long ctas = 0;
+    int pos = 0;
+    for (int g = 0; g < ra.count; ++g) {
+        const rsc_gemm_problem &f = reds[gfirst[g]];
+        RedGroup &G = ra.g[g];
+        G.C = f.C;
+        G.sC = f.strideC;
+        G.ldc = f.ldc;
+        G.batch = f.batch;
+        G.p0 = pos;
+        int er = 0, ec = 0;
+        for (int i = 0; i < n; ++i) {
+            if (gid[i] != g) continue;
+            const rsc_gemm_problem &p = reds[i];
+            if (p.ldc != f.ldc) return -7;
+            if ((p.c_rows && p.ext_r <= 0) || (p.c_cols && p.ext_c <= 0)) return -3;
+            er = std::max(er, p.ext_r > 0 ? p.ext_r : p.M);
+            ec = std::max(ec, p.ext_c > 0 ? p.ext_c : p.N);
+            RedProb &rp = ra.p[pos++];
+            rp.P = parts[i];
+            rp.c_rows = p.c_rows;
+            rp.c_cols = p.c_cols;
+            rp.M = p.M;
+            rp.N = p.N;
+        }
+        G.np = pos - G.p0;
+        G.ext_r = er;
+        G.TR = std::max(4, std::min(64, 2048 / std::max(ec, 1)));
+        ra.cta_begin[g] = ctas;
+        ctas += (long long)((er + G.TR - 1) / G.TR) * G.batch;
+    }
+    ra.cta_begin[ra.count] = ctas;
+    if (ctas <= 0) return 0;
+    ordered_reduce_kernel<<<(unsigned)ctas, RT, 0, s>>>(ra);
+    RSC_CHECK_LAUNCH();
+    return 0;
+}
+
 }  // namespace
+
+extern "C" int rsc_gemm_set_workspace(void *stream, void *ws_dev, long long bytes, int as_default) {
+    if (bytes < 0) return -3;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (as_default) {
+        g_ws_default = {nullptr, (char *)ws_dev, bytes};
+        return 0;
+    }
+    for (WsEntry &e : g_ws)
+        if (e.stream == stream) {
+            e.ptr = (char *)ws_dev;
+            e.bytes = bytes;
+            return 0;
+        }
+    g_ws.push_back({stream, (char *)ws_dev, bytes});
+    return 0;
+}
 
 extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *problems,
                                 int count, void *stream) {
@@ -291,19 +483,44 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
     if (!problems) return -3;
     cudaStream_t s = (cudaStream_t)stream;
     static thread_local GemmArgs args;  // ~30 KB; copied into the launch parameter block
+    static thread_local std::vector<rsc_gemm_problem> reds;
+    static thread_local std::vector<const double *> parts;
+    WsEntry ws{nullptr, nullptr, 0};
+    bool ws_looked = false;
     int i = 0;
     while (i < count) {
         args.count = 0;
-        long long tiles = 0;
+        reds.clear();
+        parts.clear();
+        long long tiles = 0, used = 0;
         bool gather = false;
         while (i < count && args.count < MAXP) {
-            const rsc_gemm_problem &p = problems[i++];
-            if (p.M <= 0 || p.N <= 0 || p.batch <= 0) continue;
+            const rsc_gemm_problem &p = problems[i];
+            if (p.M <= 0 || p.N <= 0 || p.batch <= 0) { ++i; continue; }
             if (transB && p.b_rows) return -3;
             if (p.K < 0) return -3;
+            rsc_gemm_problem q = p;
+            if (p.atomic) {
+                if (!ws_looked) { ws = lookup_ws(stream); ws_looked = true; }
+                const long long need = (((long long)p.M * p.N * p.batch * 8) + 255) / 256 * 256;
+                if (!ws.ptr || need > ws.bytes) return -6;
+                if (used + need > ws.bytes) break;  // close the chunk; the rest follows in order
+                double *part = (double *)(ws.ptr + used);
+                used += need;
+                reds.push_back(p);
+                parts.push_back(part);
+                q.C = part;
+                q.ldc = p.N;
+                q.strideC = (long long)p.M * p.N;
+                q.c_rows = nullptr;
+                q.c_cols = nullptr;
+                q.atomic = 0;
+                q.beta = 0.0;
+            }
+            ++i;
             const long long tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
             args.tile_begin[args.count] = tiles;
-            args.p[args.count] = p;
+            args.p[args.count] = q;
             gather |= p.b_rows != nullptr;
             tiles += tm * tn * p.batch;
             args.count++;
@@ -320,6 +537,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
                                                 : launch_chunk<true, false, false>(args, tiles, s);
         else rc = launch_chunk<true, true, false>(args, tiles, s);
         if (rc) return rc;
+        if (!reds.empty() && (rc = launch_reduce(reds, parts, s))) return rc;
     }
     return 0;
 }

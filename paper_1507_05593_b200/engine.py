@@ -5,6 +5,8 @@ librsc_b200.so.  Matrices are row-major FP64 views `(tensor, rows, cols, ld)` or
 plain 2-D tensors with unit column stride.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -207,12 +209,37 @@ class region:
             PROFILE.records.append((self.s, e, 0.0, "region:" + self.name))
 
 
-def gemm_grouped(probs, transA=False, transB=False):
-    """Launch a grouped DMMA GEMM from a GEMM_DTYPE numpy array of problems."""
+GEMM_WS_BYTES = int(os.environ.get("RSC_GEMM_WS_MB", "512")) << 20
+_GEMM_WS = {}  # stream handle (None = device default) -> workspace tensor
+
+
+def ensure_gemm_workspace():
+    """Register the current stream's ordered-accumulation workspace (the partials of
+    a launch's accumulating problems, rsc_gemm_set_workspace).  A device-wide default
+    is registered on first use; streams seen outside graph capture get their own so
+    that concurrent streams never share partials.  During capture the stream uses
+    the default (nothing is allocated inside a capture)."""
     lib = require_cuda()
+    if None not in _GEMM_WS:
+        t = torch.empty(GEMM_WS_BYTES // 8, dtype=F64, device=dev())
+        check(lib.rsc_gemm_set_workspace(None, t.data_ptr(), GEMM_WS_BYTES, 1), "rsc_gemm_set_workspace")
+        _GEMM_WS[None] = t
+    h = stream_handle()
+    if h not in _GEMM_WS and not torch.cuda.is_current_stream_capturing():
+        t = torch.empty(GEMM_WS_BYTES // 8, dtype=F64, device=dev())
+        check(lib.rsc_gemm_set_workspace(h, t.data_ptr(), GEMM_WS_BYTES, 0), "rsc_gemm_set_workspace")
+        _GEMM_WS[h] = t
+    return lib
+
+
+def gemm_grouped(probs, transA=False, transB=False):
+    """Launch a grouped DMMA GEMM from a GEMM_DTYPE numpy array of problems.
+    Accumulating problems (atomic=1) are summed deterministically in array order
+    (see rsc_gemm_grouped); mapped ones need ext_r/ext_c = their target's extent."""
     probs = np.ascontiguousarray(probs, dtype=GEMM_DTYPE)
     if probs.size == 0:
         return
+    lib = ensure_gemm_workspace() if (probs["atomic"] != 0).any() else require_cuda()
     prof = PROFILE
     if prof is not None:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -226,19 +253,26 @@ def gemm_grouped(probs, transA=False, transB=False):
 
 
 def split_k(p, transA, transB, ks):
-    """Cut every problem's K into slabs of at most `ks`, accumulated with FP64 atomics
-    into C: tall-K products (few output tiles, long K) then spread over many CTAs.
-    Problems that get split must have C zeroed by the caller (their beta is dropped:
-    every slab adds).  Handles the b_rows gather (the index pointer advances)."""
+    """Cut every problem's K into slabs of at most `ks`, accumulated (in slab order,
+    deterministically) into C: tall-K products (few output tiles, long K) then spread
+    over many CTAs.  Problems that get split must have C zeroed by the caller (their
+    beta is dropped: every slab adds).  Handles the b_rows gather (the index pointer
+    advances).  Problem order is preserved (slabs replace their problem in place)."""
+    return split_k_var(p, transA, transB, np.full(p.size, int(ks), dtype=np.int64))
+
+
+def split_k_var(p, transA, transB, ks):
+    """split_k with a per-problem slab length ks[i]."""
     K = p["K"].astype(np.int64)
+    ks = np.asarray(ks, dtype=np.int64)
     nsl = np.maximum(1, -(-K // ks))
     if (nsl == 1).all():
         return p
     idx = np.repeat(np.arange(p.size), nsl)
     q = p[idx].copy()
     first = np.repeat(np.cumsum(nsl) - nsl, nsl)
-    k0 = ((np.arange(q.size) - first) * ks).astype(np.int64)
-    q["K"] = np.minimum(ks, K[idx] - k0)
+    k0 = ((np.arange(q.size) - first) * ks[idx]).astype(np.int64)
+    q["K"] = np.minimum(ks[idx], K[idx] - k0)
     k0u = k0.astype(np.uint64)
     q["A"] = q["A"] + (k0u * q["lda"].astype(np.uint64) * np.uint64(8) if transA else k0u * np.uint64(8))
     if transB:
@@ -263,7 +297,7 @@ def balance_k(p, transA, transB, ctas=GEMM_CONCURRENT_CTAS):
     mixes tall-K products with many small ones (the longest CTA bound was 2.6x the
     balanced time on config[2]), so every problem that accumulates (atomic, or
     beta = 1) and whose K exceeds ~1.5x the balanced per-CTA share is cut into K
-    slabs of that share, accumulated with FP64 atomics (split_k)."""
+    slabs of that share, accumulated in slab order (split_k)."""
     if p.size == 0:
         return p
     tiles = np.ceil(p["M"] / 64.0) * np.ceil(p["N"] / 64.0) * p["batch"]
@@ -272,7 +306,10 @@ def balance_k(p, transA, transB, ctas=GEMM_CONCURRENT_CTAS):
     need = ((p["atomic"] == 1) | (p["beta"] == 1.0)) & (ks > 1.5 * target)
     if not need.any():
         return p
-    return np.concatenate([p[~need], split_k(p[need], transA, transB, 16 * target)])
+    # split in place: accumulation order stays the launch order (deterministic sums)
+    K = p["K"].astype(np.int64)
+    lim = np.where(need, 16 * target, np.maximum(K, 1))
+    return split_k_var(p, transA, transB, lim)
 
 
 def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
@@ -293,7 +330,7 @@ def gemm(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0):
 def gemm_strided_batched(A, B, C, transA=False, transB=False, alpha=1.0, beta=0.0, splitk=1):
     """Batched GEMM over the leading dim of 3-D contiguous tensors.
 
-    splitk > 1 cuts K into `splitk` slabs accumulated with FP64 atomics (C is
+    splitk > 1 cuts K into `splitk` slabs accumulated in slab order (C is
     zeroed first when beta == 0) -- for the tall-K sketch products L_O^T X whose
     output tile count alone cannot fill 148 SMs."""
     nb = A.shape[0]

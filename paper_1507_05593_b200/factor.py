@@ -9,7 +9,8 @@ sm_100a kernels through the C ABI; all numeric data stays in HBM:
   Schur assembly     gather -> DMMA -> scatter-subtract, one grouped launch over all
                      sources of the target (factor.py:372-399, diagblocks.py:220-238)
   implicit products  two grouped launches per product: T_s = X_s^T G[map] for all
-                     sources, then W[map] -= Y_s T_s with FP64 atomics
+                     sources, then W[map] -= Y_s T_s summed over sources in
+                     reference order by an ordered (deterministic) reduction
                      (factor.py:427-483, diagblocks.py:241-346)
   compression        host PCG64 sketch -> products -> pivoted QR (rank cutoff) ->
                      projection V = L_O U  (factor.py:486-505, diagblocks.py:349-370)
@@ -221,7 +222,7 @@ class Grouped:
     def add(self, A, lda, B, ldb, C, ldc, M, N, K, alpha, beta, b_rows=0, c_rows=0, c_cols=0, atomic=0):
         if M > 0 and N > 0:
             self.rows.append((A, B, C, 0, 0, 0, b_rows, c_rows, c_cols, M, N, K, max(lda, 1), max(ldb, 1),
-                              max(ldc, 1), 1, atomic, alpha, beta))
+                              max(ldc, 1), 1, atomic, alpha, beta, 0, 0))
 
     def launch(self):
         if self.rows:
@@ -274,7 +275,9 @@ class _Indefinite(Exception):
 
 
 class NumericPass:
-    """One left-to-right sweep on the device (factor.py:538-639)."""
+    """State shared by the numeric sweep (factor.py:538-639): arenas, the device
+    info/rank words, pending pivot checks, the sketches, interior blocks.  The sweep
+    itself is numeric.LevelPass (level-batched; it is the only driver)."""
 
     def __init__(self, plan, cfg, alpha_d):
         self.np = plan
@@ -294,87 +297,10 @@ class NumericPass:
         self.pending = []             # (info offset, count, unit, diag trees started so far)
         self.sketches = plan.sketches_for(cfg, alpha_d)
 
-    # -- helpers -----------------------------------------------------------
     def _ints(self, n):
         t = self.ibuf[self.ipos:self.ipos + n]
         self.ipos += n
         return t
-
-    def check_pivots(self):
-        """Deferred POTRF info check: raise for the earliest failing unit in sweep
-        order, with the diagonal-tree count as of that unit (factor.py:705-710)."""
-        if not self.pending:
-            return
-        info = self.ibuf[: self.ipos].cpu().numpy()
-        for off, cnt, unit, trees in self.pending:
-            v = info[off:off + cnt]
-            bad = np.nonzero(v)[0]
-            if bad.size:
-                raise _Indefinite(unit, int(v[bad[0]]) - 1, trees)
-        self.pending = []
-
-    def _potrf(self, M, unit):
-        n = M.shape[0]
-        Dinv = self.P.empty(max(n, 1), 64)
-        if n:
-            info = self._ints(1)
-            E.potrf_batched([M.data_ptr()], [n], [E.ld(M)], [Dinv.data_ptr()], info)
-            self.pending.append((self.ipos - 1, 1, unit, self.counters["diag_trees"]))
-        self.flops += n**3 / 3.0
-        return DenseTri(M, Dinv)
-
-    def _dense_from_csr(self, blk, nrows, ncols):
-        D = self.P.zeros(nrows, ncols)
-        if blk is not None and blk.nnz and nrows and ncols:
-            E.csr_to_dense_batched([blk.indptr_ptr], [blk.indices_ptr], [blk.data_ptr], [blk.nrows],
-                                   [D.data_ptr()], [E.ld(D)])
-        return D
-
-    def _spmm(self, blk, X, Y, alpha=1.0, beta=0.0):
-        if blk is None or blk.nrows == 0 or X.shape[1] == 0:
-            if beta == 0.0:
-                Y.zero_()
-            return
-        lib = E.require_cuda()
-        E.check(lib.rsc_spmm_csr(blk.nrows, int(X.shape[1]), blk.indptr_ptr, blk.indices_ptr, blk.data_ptr,
-                                    X.data_ptr(), E.ld(X), float(alpha), float(beta), Y.data_ptr(), E.ld(Y),
-                                    E.stream_handle()), "rsc_spmm_csr")
-        self.flops += 2.0 * blk.nnz * X.shape[1]
-
-    def _orth(self, G):
-        """Pivoted QR + reference cutoff -> U (m x kept) (kernels.py:67-82)."""
-        m, k = G.shape
-        if m == 0 or k == 0:
-            return self.P.empty(m, 0)
-        Q = self.S.empty(m, k)
-        rank = self._ints(1)
-        E.qrcp_batched([G.data_ptr()], [m], [k], [E.ld(G)], [Q.data_ptr()], [E.ld(Q)], rank, alloc=self.S.empty)
-        kept = int(rank.item())  # the only data-dependent size: one readback per compression
-        self.check_pivots()
-        self.flops += 4.0 * m * k * k
-        U = self.P.empty(m, kept)
-        if kept:
-            U.copy_(Q[:, :kept])
-        return U
-
-    def _lowrank(self, V, U):
-        k = U.shape[1]
-        utu = self.S.empty(k, k)
-        _gemm1(U, U, utu, transA=True)
-        Eff = self.P.empty(V.shape[0], k)
-        _gemm1(V, utu, Eff)
-        return DevLR(V, U, Eff)
-
-    def _idx(self, off):
-        return self.np.idx.ptr(off)
-
-    # -- interior blocks -----------------------------------------------------
-    def _interior_mats(self, ints):
-        Ls, Ys = [], []
-        for (u, ids, c0, c1, off_rows, A_off, A_BB) in ints:
-            Ls.append(self._dense_from_csr(A_BB, c1 - c0, c1 - c0))
-            Ys.append(self._dense_from_csr(A_off, off_rows.size, c1 - c0))
-        return Ls, Ys
 
     def factor_interiors(self, defer=False, keep=None):
         """All interior blocks at once: dense A(C_B,C_B) -> batched POTRF, then
@@ -416,116 +342,6 @@ class NumericPass:
             self.flops += nb**3 / 3.0 + off_rows.size * nb * nb
         return out
 
-    # -- Schur assembly of a non-tree node (factor.py:372-399) -----------------
-    def assemble(self, node, pairs, want_off, want_diag=True):
-        j = node.j
-        nc = node.ncols
-        A_CC, A_RC, _ = self.np.node_blocks[j]
-        R = node.rows
-        want_off = want_off and R.size > 0
-        UD = self._dense_from_csr(A_CC, nc, nc) if want_diag else None
-        UO = self._dense_from_csr(A_RC, R.size, nc) if want_off else None
-        g = Grouped(False, True)
-        for pr in pairs:
-            raw, eff = self.src_panel[pr.s]
-            w = raw.shape[1]
-            if w == 0 or pr.n_rd == 0:
-                continue
-            ld = E.ld(raw)
-            cpos = self._idx(pr.cpos_off)
-            Q = raw.data_ptr() + 8 * pr.lo * ld
-            if want_diag:
-                g.add(eff.data_ptr() + 8 * pr.lo * ld, ld, Q, ld, UD.data_ptr(), nc, pr.n_rd, pr.n_rd, w,
-                      -1.0, 1.0, c_rows=cpos, c_cols=cpos, atomic=1)
-                self.flops += 2.0 * pr.n_rd * pr.n_rd * w
-            if want_off and pr.n_ro > 0:
-                g.add(eff.data_ptr() + 8 * pr.hi * ld, ld, Q, ld, UO.data_ptr(), nc, pr.n_ro, pr.n_rd, w,
-                      -1.0, 1.0, c_rows=self._idx(pr.rpos_off), c_cols=cpos, atomic=1)
-                self.flops += 2.0 * pr.n_ro * pr.n_rd * w
-        g.launch()
-        return UD, UO
-
-    # -- diagonal solve of node j (dense or tree) ------------------------------
-    @staticmethod
-    def diag_solve(node, X, transpose, s=None):
-        if isinstance(node.diag, DeviceTree):
-            node.diag.solve(X, transpose, s)
-        else:
-            node.diag.solve(X, transpose)
-
-    # -- implicit off-diagonal products (factor.py:427-483) --------------------
-    def off_mul(self, node, pairs, G, final=False):
-        """W = L_O G without forming L_O (G: nc x r)."""
-        R = node.rows
-        r = G.shape[1]
-        W = (self.P if final else self.S).empty(R.size, r)
-        if R.size == 0 or r == 0:
-            return W.zero_() if W.numel() else W
-        G1 = self.S.empty(*G.shape)
-        G1.copy_(G)
-        self.diag_solve(node, G1, transpose=True)
-        self.flops += node.ncols**2 * r
-        _, A_RC, _ = self.np.node_blocks[node.j]
-        self._spmm(A_RC, G1, W)
-        self._source_products(pairs, G1, W, r, trans=False)
-        return W
-
-    def off_mul_t(self, node, pairs, G):
-        """W = L_O^T G (G: |R| x r), diagonal solve last."""
-        r = G.shape[1]
-        nc = node.ncols
-        W = self.S.empty(nc, r)
-        if r == 0:
-            return W
-        _, _, A_CR = self.np.node_blocks[node.j]
-        self._spmm(A_CR, G, W)
-        self._source_products(pairs, G, W, r, trans=True)
-        self.diag_solve(node, W, transpose=False)
-        self.flops += nc * nc * r
-        return W
-
-    def _source_products(self, pairs, G, W, r, trans):
-        use = [p for p in pairs if p.n_rd > 0 and p.n_ro > 0 and self.src_panel[p.s][0].shape[1] > 0]
-        if not use:
-            return
-        widths = [self.src_panel[p.s][0].shape[1] for p in use]
-        offs = np.concatenate([[0], np.cumsum(np.asarray(widths) * r)])
-        T = self.S.empty(int(offs[-1]))
-        g1, g2 = Grouped(True, False), Grouped(False, False)
-        for p, w, o in zip(use, widths, offs[:-1]):
-            raw, eff = self.src_panel[p.s]
-            ld = E.ld(raw)
-            tp = T.data_ptr() + 8 * int(o)
-            cpos, rpos = self._idx(p.cpos_off), self._idx(p.rpos_off)
-            if not trans:
-                # T = V[lo:hi]^T G1[cpos] ; W[rpos] -= E[hi:] T
-                g1.add(raw.data_ptr() + 8 * p.lo * ld, ld, G.data_ptr(), r, tp, r, w, r, p.n_rd, 1.0, 0.0,
-                       b_rows=cpos)
-                g2.add(eff.data_ptr() + 8 * p.hi * ld, ld, tp, r, W.data_ptr(), r, p.n_ro, r, w, -1.0, 1.0,
-                       c_rows=rpos, atomic=1)
-            else:
-                # T = E[hi:]^T G[rpos] ; W[cpos] -= V[lo:hi] T
-                g1.add(eff.data_ptr() + 8 * p.hi * ld, ld, G.data_ptr(), r, tp, r, w, r, p.n_ro, 1.0, 0.0,
-                       b_rows=rpos)
-                g2.add(raw.data_ptr() + 8 * p.lo * ld, ld, tp, r, W.data_ptr(), r, p.n_rd, r, w, -1.0, 1.0,
-                       c_rows=cpos, atomic=1)
-            self.flops += 2.0 * (p.n_rd + p.n_ro) * w * r
-        g1.launch()
-        g2.launch()
-
-    def approx_off(self, node, pairs, rank):
-        """Alg. 3 (factor.py:486-505)."""
-        R = node.rows
-        rank = min(rank, R.size, node.ncols)
-        G = self.sketches.device(("off", node.j), R.size, rank, self.S)
-        G = self.off_mul_t(node, pairs, G)
-        for _ in range(self.cfg.power_iters):
-            G = self.off_mul_t(node, pairs, self.off_mul(node, pairs, G))
-        U = self._orth(G)
-        V = self.off_mul(node, pairs, U, final=True)
-        return self._lowrank(V, U)
-
-    # -- diagonal trees (diagblocks.py) ----------------------------------------
     def _path_terms(self, tree, s, rspan, cspan):
         out = []
         for p in tree.shape.path_above(s):
@@ -534,128 +350,6 @@ class NumericPass:
             out.append((raw, eff, rspan[0] - base, rspan[1] - base, cspan[0] - base, cspan[1] - base))
         return out
 
-    def factor_leaf(self, node, s):
-        tree = node.diag
-        j = node.j
-        maps, blk, _ = self.np.tree_maps[(j, s)]
-        lf = tree.shape.nodes[s]
-        k = lf.hi - lf.lo
-        U = self._dense_from_csr(blk, k, k)
-        g = Grouped(False, True)
-        for m in maps:
-            raw, eff = self.src_panel[m.s]
-            w = raw.shape[1]
-            if w == 0:
-                continue
-            ld = E.ld(raw)
-            g.add(eff.data_ptr() + 8 * m.rlo * ld, ld, raw.data_ptr() + 8 * m.clo * ld, ld, U.data_ptr(), k,
-                  m.rhi - m.rlo, m.chi - m.clo, w, -1.0, 1.0, c_rows=self._idx(m.ridx_off),
-                  c_cols=self._idx(m.cidx_off), atomic=1)
-            self.flops += 2.0 * (m.rhi - m.rlo) * (m.chi - m.clo) * w
-        for raw, eff, a, b, c, d in self._path_terms(tree, s, (lf.lo, lf.hi), (lf.lo, lf.hi)):
-            w = raw.shape[1]
-            if w == 0:
-                continue
-            ld = E.ld(raw)
-            g.add(eff.data_ptr() + 8 * a * ld, ld, raw.data_ptr() + 8 * c * ld, ld, U.data_ptr(), k, b - a,
-                  d - c, w, -1.0, 1.0, atomic=1)
-            self.flops += 2.0 * (b - a) * (d - c) * w
-        g.launch()
-        return self._potrf(U, node.u)
-
-    def diag_mul(self, node, s, G, transpose, final=False):
-        """Alg. 5: product of internal tree block s with G (diagblocks.py:303-346)."""
-        tree = node.diag
-        shape = tree.shape
-        blk_nd = shape.nodes[s]
-        (r0, r1), (c0, c1) = shape.span(s)
-        maps, blk, blkT = self.np.tree_maps[(node.j, s)]
-        r = G.shape[1]
-        g1, g2 = Grouped(True, False), Grouped(False, False)
-        terms = []
-        mem = self.P if final else self.S
-        if not transpose:
-            G1 = self.S.empty(*G.shape)
-            G1.copy_(G)
-            tree.solve(G1, transpose=True, s=blk_nd.left.s)
-            self.flops += (c1 - c0) ** 2 * r
-            W = mem.empty(r1 - r0, r)
-            self._spmm(blk, G1, W)
-            src = G1
-        else:
-            W = mem.empty(c1 - c0, r)
-            self._spmm(blkT, G, W)
-            src = G
-        for m in maps:
-            raw, eff = self.src_panel[m.s]
-            w = raw.shape[1]
-            if w:
-                terms.append((raw, eff, w, m.clo, m.chi, m.rlo, m.rhi, self._idx(m.cidx_off), self._idx(m.ridx_off)))
-        for raw, eff, a, b, c, d in self._path_terms(tree, s, (r0, r1), (c0, c1)):
-            w = raw.shape[1]
-            if w:
-                terms.append((raw, eff, w, c, d, a, b, 0, 0))
-        if terms:
-            widths = np.array([t[2] for t in terms])
-            offs = np.concatenate([[0], np.cumsum(widths * r)])
-            T = self.S.empty(int(offs[-1]))
-            for (raw, eff, w, clo, chi, rlo, rhi, cidx, ridx), o in zip(terms, offs[:-1]):
-                ld = E.ld(raw)
-                tp = T.data_ptr() + 8 * int(o)
-                if not transpose:
-                    g1.add(raw.data_ptr() + 8 * clo * ld, ld, src.data_ptr(), r, tp, r, w, r, chi - clo, 1.0, 0.0,
-                           b_rows=cidx)
-                    g2.add(eff.data_ptr() + 8 * rlo * ld, ld, tp, r, W.data_ptr(), r, rhi - rlo, r, w, -1.0, 1.0,
-                           c_rows=ridx, atomic=1)
-                else:
-                    g1.add(eff.data_ptr() + 8 * rlo * ld, ld, src.data_ptr(), r, tp, r, w, r, rhi - rlo, 1.0, 0.0,
-                           b_rows=ridx)
-                    g2.add(raw.data_ptr() + 8 * clo * ld, ld, tp, r, W.data_ptr(), r, chi - clo, r, w, -1.0, 1.0,
-                           c_rows=cidx, atomic=1)
-                self.flops += 2.0 * ((chi - clo) + (rhi - rlo)) * w * r
-            g1.launch()
-            g2.launch()
-        if transpose:
-            tree.solve(W, transpose=False, s=blk_nd.left.s)
-            self.flops += (c1 - c0) ** 2 * r
-        return W
-
-    def approx_diag(self, node, s, rank):
-        (r0, r1), (c0, c1) = node.diag.shape.span(s)
-        rank = min(rank, r1 - r0, c1 - c0)
-        G = self.sketches.device(("diag", node.j, s), r1 - r0, rank, self.S)
-        G = self.diag_mul(node, s, G, True)
-        for _ in range(self.cfg.power_iters):
-            G = self.diag_mul(node, s, self.diag_mul(node, s, G, False), True)
-        U = self._orth(G)
-        V = self.diag_mul(node, s, U, False, final=True)
-        return self._lowrank(V, U)
-
-    def factor_tree(self, node):
-        from .diagtree import TreeShape  # noqa: F401
-
-        shape = self.np.tree_shapes[node.j]
-        tree = DeviceTree(shape)
-        node.diag = tree
-        for s in shape.order:
-            self.S.reset()  # block outputs are persistent; transients of the last block are dead
-            tn = shape.nodes[s]
-            if tn.is_leaf:
-                tree.blocks[s] = self.factor_leaf(node, s)
-                continue
-            nrows, ncols = tn.hi - tn.split, tn.split - tn.lo
-            r = block_rank(nrows, ncols, self.alpha_d, self.cfg.oversample)
-            if r >= DENSE_FALLBACK_FRACTION * min(nrows, ncols):
-                eye = self.S.zeros(ncols, ncols)
-                eye.fill_diagonal_(1.0)
-                tree.blocks[s] = self.diag_mul(node, s, eye, False, final=True)
-                self.counters["dense_fallback"] += 1
-            else:
-                tree.blocks[s] = self.approx_diag(node, s, r)
-                self.ranks[("diag", node.j, s)] = tree.blocks[s].k
-                self.counters["compressed_diag"] += 1
-
-    # -- the sweep -------------------------------------------------------------
     def _trees_before(self, u):
         """Diagonal trees started before unit u (the restart test of factor.py:709)."""
         # the tree counter is bumped before a tree node's own leaf POTRFs (factor.py:587-588)
@@ -669,67 +363,6 @@ class NumericPass:
             self.check_pivots()
         finally:
             E.SCRATCH = prev
-
-    def _run(self):
-        part = self.sym.partition
-        cfg = self.cfg
-        interiors = self.factor_interiors()
-        fail = self.first_interior_failure
-        for u, (kind, payload) in enumerate(self.sym.units):
-            self.S.reset()
-            if fail is not None and u >= fail[0]:
-                self.check_pivots()
-                raise _Indefinite(*fail)
-            if kind == "interior":
-                iu = interiors[u]
-                self.units.append(iu)
-                sid = self.np.unit_source.get(u)
-                if sid is not None:
-                    self.src_panel[sid] = (iu.off, iu.off)
-                continue
-            j = payload
-            c0, c1 = part.cols(j)
-            nc = c1 - c0
-            R = part.rows[j]
-            pairs = self.np.targets[j]
-            compress = bool(part.is_separator[j])
-            node = NodeUnit(u, j, c0, c1, R)
-            tree_diag = compress and j in self.sym.sep_splits
-            r_off = block_rank(R.size, nc, cfg.alpha_o, cfg.oversample)
-            compress_off = bool(compress and R.size and r_off < DENSE_FALLBACK_FRACTION * min(R.size, nc))
-            UO = None
-            if tree_diag:
-                self.counters["diag_trees"] += 1
-                self.factor_tree(node)
-            else:
-                UD, UO = self.assemble(node, pairs, want_off=not compress_off)
-                node.diag = self._potrf(UD, u)
-            if R.size == 0:
-                node.off = None
-            elif compress_off:
-                node.off = self.approx_off(node, pairs, r_off)
-                self.ranks[("off", j)] = node.off.k
-                self.counters["compressed_off"] += 1
-            else:
-                if compress:
-                    self.counters["dense_fallback"] += 1
-                if tree_diag:
-                    _, UO = self.assemble(node, pairs, want_off=True, want_diag=False)
-                    X = self.S.empty(nc, R.size)
-                    X.copy_(UO.t())
-                    node.diag.solve(X, transpose=False)
-                    node.off = self.P.empty(R.size, nc)
-                    node.off.copy_(X.t())
-                else:
-                    E.trsm_batched("right", 1, [node.diag.L.data_ptr()], [nc], [E.ld(node.diag.L)],
-                                   [node.diag.Dinv.data_ptr()], [UO.data_ptr()], [UO.shape[0]], [E.ld(UO)])
-                    node.off = UO
-                self.flops += R.size * nc * nc
-            self.units.append(node)
-            sid = self.np.unit_source.get(u)
-            if sid is not None:
-                raw, eff = _raw_eff(node.off)
-                self.src_panel[sid] = (raw, eff)
 
 
 # ---------------------------------------------------------------------------

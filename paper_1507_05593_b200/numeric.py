@@ -116,7 +116,7 @@ def run_waves(seqs, scratch):
                         b.shape[1], -1.0, 1.0)
         if lr:
             ts = scratch(sum(b.k * r for b, _, _, _, r in lr))
-            ts.zero_()  # t = P1^T X accumulates (atomic): balance_k may split its tall K
+            ts.zero_()  # t = P1^T X accumulates (ordered): balance_k may split its tall K
             keep.append(ts)
             off = 0
             for b, Xs, Yd, tr, r in lr:
@@ -428,6 +428,7 @@ class LevelPass(NumericPass):
                     self.idx_base + (4 * t["rpos"][sel]).astype(np.uint64))
                 p["c_cols"] = cpos[sel]
                 p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
+                p["ext_r"], p["ext_c"] = tgt.shape
                 self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s][sel])
                 probs.append(p[self._mine(s[sel])])
         if probs:
@@ -483,7 +484,8 @@ class LevelPass(NumericPass):
             t = self._pairs(node.j, need_rd=True, need_ro=True)
             if t["s"].size == 0:
                 continue
-            parts.append((t, r, G.data_ptr(), E.ld(G), W.data_ptr(), E.ld(W), self._price.get(G.data_ptr(), 0)))
+            parts.append((t, r, G.data_ptr(), E.ld(G), W.data_ptr(), E.ld(W), self._price.get(G.data_ptr(), 0),
+                          W.shape[0], W.shape[1]))
         if not parts:
             return
         cat = lambda key: np.concatenate([p[0][key] for p in parts])
@@ -507,6 +509,7 @@ class LevelPass(NumericPass):
         p1["lda"], p1["batch"], p1["alpha"] = ld, 1, 1.0
         p2["B"], p2["ldb"], p2["C"], p2["ldc"], p2["N"], p2["K"] = tp, r, wp, ldw, r, w
         p2["lda"], p2["batch"], p2["alpha"], p2["beta"], p2["atomic"] = ld, 1, -1.0, 1.0, 1
+        p2["ext_r"], p2["ext_c"] = rep(7), rep(8)
         if not trans:  # T = V[lo:hi]^T G1[cpos] ; W[rpos] -= E[hi:] T
             p1["A"], p1["K"], p1["b_rows"] = raw_lo, nrd, cpos
             p2["A"], p2["M"], p2["c_rows"] = eff_hi, nro, rpos
@@ -581,6 +584,7 @@ class LevelPass(NumericPass):
                 p["c_rows"] = self.idx_base + (4 * t["ridx"]).astype(np.uint64)
                 p["c_cols"] = self.idx_base + (4 * t["cidx"]).astype(np.uint64)
                 p["C"], p["ldc"] = U.data_ptr(), k
+                p["ext_r"], p["ext_c"] = k, k
                 parts.append(p)
                 bases.append(self.s_raw[src])
                 keeps.append(self._mine(src))
@@ -591,6 +595,7 @@ class LevelPass(NumericPass):
                     p[i]["A"], p[i]["B"] = effp + 8 * a0 * ld, rawp + 8 * c0 * ld
                     p[i]["lda"], p[i]["ldb"], p[i]["K"], p[i]["M"], p[i]["N"] = ld, ld, w, a1 - a0, c1 - c0
                 p["C"], p["ldc"] = U.data_ptr(), k
+                p["ext_r"], p["ext_c"] = k, k
                 parts.append(p)
                 bases.append(np.array([pt[0] for pt in path], dtype=np.uint64))
                 keeps.append(np.full(len(path), self._lead()))
@@ -681,6 +686,7 @@ class LevelPass(NumericPass):
             p1["B"], p1["ldb"] = src.data_ptr(), E.ld(src)
             p2["lda"], p2["K"], p2["N"], p2["B"], p2["ldb"] = ld, w, r, tp, r
             p2["C"], p2["ldc"] = W.data_ptr(), E.ld(W)
+            p2["ext_r"], p2["ext_c"] = W.shape
             if not transpose:  # T = V[cwin]^T G1[cidx] ; W[ridx] -= E[rwin] T
                 p1["A"], p1["K"], p1["b_rows"] = raw_c, nc_, cidx
                 p2["A"], p2["M"], p2["c_rows"] = eff_r, nr_, ridx

@@ -43,5 +43,6 @@ def test_bad_arguments_rejected_without_gpu():
 def test_gemm_descriptor_layout_matches_header():
     from paper_1507_05593_b200._lib import GEMM_DTYPE
 
-    assert GEMM_DTYPE.itemsize == 120
+    assert GEMM_DTYPE.itemsize == 128
     assert GEMM_DTYPE.fields["alpha"][1] == 104
+    assert GEMM_DTYPE.fields["ext_r"][1] == 120
