@@ -42,9 +42,10 @@ extern "C" {
  * workspace (rsc_gemm_set_workspace), then an ordered reduction adds the partials
  * into C in problem order (for every element of C: C + P_first + ... + P_last,
  * the left-to-right order of rschol's `UD -= ...` loops, factor.py:389-398).
- * c_rows / c_cols of accumulating problems must be strictly increasing, and
- * ext_r x ext_c gives the extent of the target block C (rows x columns reachable
- * through the maps; 0 = M x N, allowed only without maps). */
+ * For accumulating problems c_cols must be strictly increasing and c_rows
+ * non-decreasing (a repeated row is summed by one thread); ext_r x ext_c is the
+ * extent of the target block C (0 = M x N, allowed only without maps), and rows
+ * mapped at or beyond ext_r are dropped. */
 typedef struct {
     const double *A;
     const double *B;

@@ -30,6 +30,8 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -275,7 +277,9 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
                 const int ccol = P.c_cols ? __ldg(P.c_cols + col) : col;
                 double *dst = C + crow + ccol;
                 const double v = alpha * acc[i][j][e];
-                if (beta == 0.0) {
+                if (P.atomic) {  // diagnostic only (RSC_GEMM_ATOMIC=1): unordered FP64 atomics
+                    atomicAdd(dst, v);
+                } else if (beta == 0.0) {
                     *dst = v;
                 } else {
                     *dst = v + beta * (*dst);
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
 
 struct RedProb {
     const double *P;      // partial: batch x M x N, dense
-    const int *c_rows;    // strictly increasing (or null = identity)
+    const int *c_rows;    // non-decreasing (or null = identity)
     const int *c_cols;
     int M, N;
 };
@@ -359,9 +363,20 @@ __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constan
         for (int e = threadIdx.x; e < cnt; e += RT) {
             const int di = e / n;
             const int i = i0 + di, j = e - di * n;
-            const int r = P.c_rows ? __ldg(P.c_rows + i) : i;
             const int c = P.c_cols ? __ldg(P.c_cols + j) : j;
-            C[(long long)r * G.ldc + c] += src[(long long)i * n + j];
+            if (!P.c_rows) {
+                C[(long long)i * G.ldc + c] += src[(long long)i * n + j];
+                continue;
+            }
+            // Row maps are non-decreasing but may repeat: searchsorted maps of
+            // interior-block rows outside the target's structure (their products are
+            // exact zeros, see plan._build_targets).  The first local row of a run
+            // sums the whole run, so no two threads ever update the same element.
+            const int r = __ldg(P.c_rows + i);
+            if (i > i0 && __ldg(P.c_rows + i - 1) == r) continue;
+            double v = src[(long long)i * n + j];
+            for (int k = i + 1; k < i1 && __ldg(P.c_rows + k) == r; ++k) v += src[(long long)k * n + j];
+            C[(long long)r * G.ldc + c] += v;
         }
         __syncthreads();  // problem q+1 may hit the same elements through other threads
     }
@@ -451,6 +466,41 @@ int launch_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<c
         ctas += (long long)((er + G.TR - 1) / G.TR) * G.batch;
     }
     ra.cta_begin[ra.count] = ctas;
+    static const bool dbg = getenv("RSC_GEMM_DEBUG") != nullptr;
+    if (dbg) {  // diagnostics: target overlap between groups, map monotonicity and range
+        cudaStreamSynchronize(s);
+        for (int g = 0; g < ra.count; ++g) {
+            const RedGroup &G = ra.g[g];
+            const char *lo1 = (const char *)G.C;
+            const char *hi1 = lo1 + 8 * ((long long)(G.ext_r - 1) * G.ldc + 1);
+            for (int h = g + 1; h < ra.count; ++h) {
+                const RedGroup &H = ra.g[h];
+                const char *lo2 = (const char *)H.C;
+                const char *hi2 = lo2 + 8 * ((long long)(H.ext_r - 1) * H.ldc + 1);
+                if (lo1 < hi2 && lo2 < hi1)
+                    fprintf(stderr, "RSC_GEMM_DEBUG: groups %d/%d overlap (C %p ext %d ld %d / C %p ext %d ld %d)\n",
+                            g, h, (void *)G.C, G.ext_r, G.ldc, (void *)H.C, H.ext_r, H.ldc);
+            }
+            for (int q = G.p0; q < G.p0 + G.np; ++q) {
+                const RedProb &P = ra.p[q];
+                for (int w = 0; w < 2; ++w) {
+                    const int *mp = w ? P.c_cols : P.c_rows;
+                    const int len = w ? P.N : P.M;
+                    if (!mp) continue;
+                    std::vector<int> hv(len);
+                    cudaMemcpy(hv.data(), mp, sizeof(int) * len, cudaMemcpyDeviceToHost);
+                    for (int t = 0; t < len; ++t) {
+                        const bool bad = (t && (w ? hv[t] <= hv[t - 1] : hv[t] < hv[t - 1])) || hv[t] < 0;
+                        if (bad) {
+                            fprintf(stderr, "RSC_GEMM_DEBUG: group %d prob %d %s map bad at %d: %d (prev %d, ext_r %d)\n",
+                                    g, q, w ? "col" : "row", t, hv[t], t ? hv[t - 1] : -1, G.ext_r);
+                            break;
+                        }
+                    }
+                }
+            }
+        }
+    }
     if (ctas <= 0) return 0;
     ordered_reduce_kernel<<<(unsigned)ctas, RT, 0, s>>>(ra);
     RSC_CHECK_LAUNCH();
@@ -485,6 +535,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
     static thread_local GemmArgs args;  // ~30 KB; copied into the launch parameter block
     static thread_local std::vector<rsc_gemm_problem> reds;
     static thread_local std::vector<const double *> parts;
+    static const bool atomic_diag = getenv("RSC_GEMM_ATOMIC") != nullptr;  // A/B diagnostics only
     WsEntry ws{nullptr, nullptr, 0};
     bool ws_looked = false;
     int i = 0;
@@ -500,7 +551,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
             if (transB && p.b_rows) return -3;
             if (p.K < 0) return -3;
             rsc_gemm_problem q = p;
-            if (p.atomic) {
+            if (p.atomic && !atomic_diag) {
                 if (!ws_looked) { ws = lookup_ws(stream); ws_looked = true; }
                 const long long need = (((long long)p.M * p.N * p.batch * 8) + 255) / 256 * 256;
                 if (!ws.ptr || need > ws.bytes) return -6;

@@ -97,6 +97,44 @@ def hutchinson(A, F):
     return float(np.linalg.norm(BZ - LLtZ) / np.sqrt(HUTCH_K) / a_fro)
 
 
+def factor_digest(F):
+    """Order-sensitive 64-bit digest of every numeric block of the device factor
+    (bitwise: two factors agree iff every stored FP64 word agrees, up to hash
+    collisions)."""
+    import torch
+
+    from paper_1507_05593_b200.factor import DeviceTree, DevLR
+
+    acc = torch.zeros((), dtype=torch.int64, device="cuda")
+    k = 0
+
+    def mix(t):
+        nonlocal acc, k
+        if t is None or t.numel() == 0:
+            return
+        x = t.contiguous().view(-1).view(torch.int64)
+        w = torch.arange(1, x.numel() + 1, device=x.device, dtype=torch.int64) * 2654435761 + k
+        acc = acc + ((x ^ (x >> 31)) * w).sum()
+        k += 1
+
+    for un in F.units:
+        blocks = []
+        if isinstance(un.diag, DeviceTree):
+            for s in sorted(un.diag.blocks):
+                blocks.append(un.diag.blocks[s])
+        else:
+            blocks.append(un.diag)
+        blocks.append(un.off)
+        for b in blocks:
+            if isinstance(b, DevLR):
+                mix(b.V), mix(b.U)
+            elif hasattr(b, "L"):
+                mix(b.L)
+            elif b is not None:
+                mix(b)
+    return int(acc.item())
+
+
 def rank_list(F):
     return sorted((k[1], k[2] if k[0] == "diag" else -1, r) for k, r in F.ranks.items())
 

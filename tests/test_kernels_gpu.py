@@ -39,10 +39,64 @@ def test_gemm_grouped_all_transposes_and_maps(cuda):
         p[i]["M"], p[i]["N"], p[i]["K"] = M, N, K
         p[i]["lda"], p[i]["ldb"], p[i]["ldc"] = K, N, 70
         p[i]["batch"], p[i]["atomic"], p[i]["alpha"] = 1, 1, -1.0
+        p[i]["ext_r"], p[i]["ext_c"] = 90, 70
     E.gemm_grouped(p)
     ref = np.zeros((90, 70))
     ref[np.ix_(crow, ccol)] -= 2 * (A @ Bbig[brow])
     assert relerr(Cd.cpu().numpy(), ref) < 1e-14
+
+
+def test_gemm_ordered_accumulation_deterministic(cuda):
+    """Many accumulating problems scattered into shared targets (interleaved groups,
+    split-K slabs, several chunks through a small workspace): the result equals the
+    sequential sum C + P_1 + P_2 + ... in problem order, bit-identically on every
+    launch (rsc_gemm_grouped's ordered reduction replaces FP64 atomics)."""
+    from paper_1507_05593_b200 import _lib
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(11)
+    T = 3  # targets
+    shapes = [(300, 120), (97, 64), (1000, 37)]
+    C0 = [rng.standard_normal(s) for s in shapes]
+    Cd = [E.to_dev(c) for c in C0]
+    keep, probs, ref = [], [], [c.copy() for c in C0]
+    for n in range(60):
+        t = n % T
+        er, ec = shapes[t]
+        M, N, K = int(rng.integers(1, min(er, 130))), int(rng.integers(1, ec)), int(rng.integers(1, 300))
+        rows = np.sort(rng.choice(er, M, replace=False)).astype(np.int32)
+        cols = np.sort(rng.choice(ec, N, replace=False)).astype(np.int32)
+        A, B = rng.standard_normal((M, K)), rng.standard_normal((K, N))
+        dA, dB, dr, dc = E.to_dev(A), E.to_dev(B), E.to_dev(rows), E.to_dev(cols)
+        keep += [dA, dB, dr, dc]
+        q = E.gemm_problems(1)
+        q["A"], q["B"], q["C"], q["c_rows"], q["c_cols"] = dA.data_ptr(), dB.data_ptr(), Cd[t].data_ptr(), \
+            dr.data_ptr(), dc.data_ptr()
+        q["M"], q["N"], q["K"], q["lda"], q["ldb"], q["ldc"] = M, N, K, K, N, ec
+        q["batch"], q["atomic"], q["alpha"], q["beta"], q["ext_r"], q["ext_c"] = 1, 1, -0.5, 1.0, er, ec
+        probs.append(q)
+        ref[t][np.ix_(rows, cols)] += -0.5 * (A @ B)
+    P = np.concatenate(probs)
+    P = E.balance_k(P, False, False, ctas=8)  # force split-K slabs (kept in place)
+    lib = _lib.load()
+    outs = []
+    for ws_mb in (512, 1):  # 1 MB: the launch is cut into several ordered chunks
+        ws = E.empty((ws_mb << 20) // 8)
+        E.check(lib.rsc_gemm_set_workspace(E.stream_handle(), ws.data_ptr(), ws_mb << 20, 0), "ws")
+        for _ in range(3):
+            for t in range(T):
+                Cd[t].copy_(E.to_dev(C0[t]))
+            E.gemm_grouped(P)
+            outs.append([c.cpu().numpy() for c in Cd])
+        E._GEMM_WS.pop(E.stream_handle(), None)
+        E.ensure_gemm_workspace()
+    E.check(lib.rsc_gemm_set_workspace(E.stream_handle(), E._GEMM_WS[E.stream_handle()].data_ptr(),
+                                       E.GEMM_WS_BYTES, 0), "ws")
+    for o in outs[1:]:
+        for t in range(T):
+            assert np.array_equal(o[t], outs[0][t])
+    for t in range(T):
+        assert relerr(outs[0][t], ref[t]) < 1e-14
 
 
 def test_dense_cholesky_golden(cuda):

@@ -38,15 +38,16 @@ def main():
         t = time.perf_counter()
         F = factorize(A, conf, coords=coords)
         res["oneshot_s"] = time.perf_counter() - t
-        runs.append((FS.rank_list(F), F.apply(r), F))
+        runs.append((FS.rank_list(F), F.apply(r), FS.factor_digest(F)))
         prep = prepare(A, conf, coords)
         for i in range(2):
             t = time.perf_counter()
             F2 = factorize(A, prepared=prep)
             res[f"refactor{i}_s"] = time.perf_counter() - t
-            runs.append((FS.rank_list(F2), F2.apply(r), None))
+            runs.append((FS.rank_list(F2), F2.apply(r), FS.factor_digest(F2)))
             del F2
         res["ranks_identical"] = all(x[0] == runs[0][0] for x in runs)
+        res["factor_digest_identical"] = all(x[2] == runs[0][2] for x in runs)
         res["apply_bits_identical"] = all(np.array_equal(x[1], runs[0][1]) for x in runs)
         res["apply_maxrel_between_runs"] = max(float(np.abs(x[1] - runs[0][1]).max() / np.abs(runs[0][1]).max())
                                                 for x in runs)
