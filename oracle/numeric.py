@@ -27,6 +27,25 @@ from .kernels import OracleIndefinite, block_seed, chol, gauss, orth, trisolve
 
 DENSE_FALLBACK = 0.75
 
+# Algorithmic work census: when COUNT is a dict, every operation of
+# the reference algorithm adds its flops under a category; _CAT is the category of
+# the enclosing compression (off-diagonal / diagonal-tree sketch products).
+COUNT = None
+_CAT = ["off_sketch"]
+
+
+def _f(cat, val):
+    if COUNT is not None:
+        COUNT[cat] = COUNT.get(cat, 0.0) + float(val)
+
+
+def _nnzL(blk):
+    return sum((m.c1 - m.c0) * (m.c1 - m.c0 + 1) // 2 + (m.c1 - m.c0) * (m.nib or 0) for m in blk.members)
+
+
+def _nnz(full, rows, c0, c1):
+    return full[np.asarray(rows, dtype=np.int64), c0:c1].nnz
+
 
 @dataclass
 class Config:
@@ -134,6 +153,10 @@ class Interior:
     def multiply(self, full, R, C, G, transpose=False):
         if transpose:
             R, C = C, R
+        if COUNT is not None:
+            k = np.shape(G)[1] if np.ndim(G) == 2 else 1
+            _f(_CAT[-1], 2.0 * k * (_nnz(full, C, self.c0, self.c1) + _nnz(full, R, self.c0, self.c1))
+               + 4.0 * _nnzL(self) * k)
         T = full[np.asarray(C, dtype=np.int64), self.c0 : self.c1].T @ G
         T = self.solve(self.solve(T), transpose=True)
         return full[np.asarray(R, dtype=np.int64), self.c0 : self.c1] @ T
@@ -163,6 +186,9 @@ def factor_interior(full, part, ids, bid):
                 UO[np.ix_(np.searchsorted(rows, rk[hi:]), cpos)] -= s.off[hi:] @ Bd.T
             if hi < rk.shape[0]:
                 buckets.setdefault(part.supernode_of(int(rk[hi])), []).append(k)
+        if COUNT is not None:
+            ncj = j1 - j0
+            _f("potrf_trsm", ncj**3 / 3.0 + nib * ncj * ncj + nib * nib * ncj)
         nd = Node(j, j0, j1, rows)
         nd.diag = chol(UD)
         nd.off = trisolve(nd.diag, UO.T).T if nib else UO
@@ -293,6 +319,9 @@ def _win_update(U, src, rw, cw, full):
     if src.kind == "interior":
         Yc = src.blk.factor_rows(full, np.arange(c0, c1))
         Yr = Yc if (r0, r1) == (c0, c1) else src.blk.factor_rows(full, np.arange(r0, r1))
+        nl = _nnzL(src.blk) if COUNT is not None else 0
+        _f("leaf_interior", 2.0 * nl * ((c1 - c0) + (0 if (r0, r1) == (c0, c1) else (r1 - r0)))
+           + 2.0 * (r1 - r0) * (c1 - c0) * (src.blk.c1 - src.blk.c0))
         U -= Yr @ Yc.T
         return
     rows = src.rows
@@ -301,6 +330,8 @@ def _win_update(U, src, rw, cw, full):
     if clo == chi or rlo == rhi:
         return
     off = src.node.off
+    w = off.V.shape[1] if isinstance(off, LR) else off.shape[1]
+    _f("leaf_syrk", 2.0 * (rhi - rlo) * (chi - clo) * w)
     U[np.ix_(rows[rlo:rhi] - r0, rows[clo:chi] - c0)] -= eff(off, slice(rlo, rhi)) @ raw(off, slice(clo, chi)).T
 
 
@@ -318,6 +349,8 @@ def _win_multiply(W, src, rw, cw, G, transpose, full):
     if clo == chi or rlo == rhi:
         return
     off = src.node.off
+    w = off.V.shape[1] if isinstance(off, LR) else off.shape[1]
+    _f(_CAT[-1], 2.0 * ((rhi - rlo) + (chi - clo)) * w * G.shape[1])
     if transpose:
         T = eff(off, slice(rlo, rhi)).T @ G[rows[rlo:rhi] - r0]
         W[rows[clo:chi] - c0] -= raw(off, slice(clo, chi)) @ T
@@ -341,7 +374,9 @@ def factor_leaf(full, node, s, srcs):
         _win_update(U, src, (g0, g1), (g0, g1), full)
     for p in tree.path_above(s):
         P, Q = _path_pair(tree, p, (lf.lo, lf.hi), (lf.lo, lf.hi))
+        _f("leaf_path", 2.0 * P.shape[0] * Q.shape[0] * P.shape[1])
         U -= P @ Q.T
+    _f("potrf_trsm", (g1 - g0) ** 3 / 3.0)
     return chol(U)
 
 
@@ -351,6 +386,8 @@ def diag_multiply(full, node, s, G, transpose, srcs):
     (r0, r1), (c0, c1) = tree.span(s)
     gr, gc = (tree.g0 + r0, tree.g0 + r1), (tree.g0 + c0, tree.g0 + c1)
     G = np.atleast_2d(np.asarray(G, dtype=np.float64))
+    _f("sketch_diag_solve", (c1 - c0) ** 2 * G.shape[1])
+    _f(_CAT[-1], 2.0 * full[gr[0]:gr[1], gc[0]:gc[1]].nnz * G.shape[1])
     if not transpose:
         G1 = diag_solve(node, G, transpose=True, s=blk.left.s)
         W = full[gr[0] : gr[1], gc[0] : gc[1]] @ G1
@@ -358,6 +395,7 @@ def diag_multiply(full, node, s, G, transpose, srcs):
             _win_multiply(W, src, gr, gc, G1, False, full)
         for p in tree.path_above(s):
             P, Q = _path_pair(tree, p, (r0, r1), (c0, c1))
+            _f(_CAT[-1], 2.0 * (P.shape[0] + Q.shape[0]) * P.shape[1] * G1.shape[1])
             W -= P @ (Q.T @ G1)
         return W
     W = full[gr[0] : gr[1], gc[0] : gc[1]].T @ G
@@ -365,6 +403,7 @@ def diag_multiply(full, node, s, G, transpose, srcs):
         _win_multiply(W, src, gr, gc, G, True, full)
     for p in tree.path_above(s):
         P, Q = _path_pair(tree, p, (r0, r1), (c0, c1))
+        _f(_CAT[-1], 2.0 * (P.shape[0] + Q.shape[0]) * P.shape[1] * G.shape[1])
         W -= Q @ (P.T @ G)
     return diag_solve(node, W, transpose=False, s=blk.left.s)
 
@@ -372,11 +411,16 @@ def diag_multiply(full, node, s, G, transpose, srcs):
 def approx_diag_block(full, node, s, rank, q, seed, srcs):
     (r0, r1), (c0, c1) = node.diag.span(s)
     rank = min(rank, r1 - r0, c1 - c0)
-    G = diag_multiply(full, node, s, gauss(r1 - r0, rank, seed), True, srcs)
-    for _ in range(q):
-        G = diag_multiply(full, node, s, diag_multiply(full, node, s, G, False, srcs), True, srcs)
-    U = orth(G)
-    return LR(diag_multiply(full, node, s, U, False, srcs), U)
+    _CAT.append("diag_sketch")
+    try:
+        G = diag_multiply(full, node, s, gauss(r1 - r0, rank, seed), True, srcs)
+        for _ in range(q):
+            G = diag_multiply(full, node, s, diag_multiply(full, node, s, G, False, srcs), True, srcs)
+        _f("qrcp", 4.0 * G.shape[0] * G.shape[1] ** 2)
+        U = orth(G)
+        return LR(diag_multiply(full, node, s, U, False, srcs), U)
+    finally:
+        _CAT.pop()
 
 
 # ---------------------------------------------------------------------------
@@ -391,6 +435,10 @@ def assemble_schur(full, node, R, srcs, want_off=True):
     for src in srcs:
         if src.kind == "interior":
             Yc = src.blk.factor_rows(full, np.arange(c0, c1))
+            if COUNT is not None:
+                nl, nb, nc = _nnzL(src.blk), src.blk.c1 - src.blk.c0, c1 - c0
+                _f("interior_solve", 2.0 * nl * (nc + (R.size if want_off else 0)))
+                _f("interior_gemm", 2.0 * nc * nc * nb + (2.0 * R.size * nc * nb if want_off else 0.0))
             UD -= Yc @ Yc.T
             if want_off:
                 UO -= src.blk.factor_rows(full, R) @ Yc.T
@@ -402,6 +450,8 @@ def assemble_schur(full, node, R, srcs, want_off=True):
         cpos = rows[lo:hi] - c0
         off = src.node.off
         Q = raw(off, slice(lo, hi))
+        _f("node_syrk_gemm", 2.0 * (hi - lo) ** 2 * Q.shape[1]
+           + (2.0 * (rows.shape[0] - hi) * (hi - lo) * Q.shape[1] if (hi < rows.shape[0] and want_off) else 0.0))
         UD[np.ix_(cpos, cpos)] -= eff(off, slice(lo, hi)) @ Q.T
         if hi < rows.shape[0] and want_off:
             UO[np.ix_(np.searchsorted(R, rows[hi:]), cpos)] -= eff(off, slice(hi, None)) @ Q.T
@@ -413,8 +463,10 @@ def off_mul(full, node, G, srcs):
     G = np.atleast_2d(np.asarray(G, dtype=np.float64))
     if R.size == 0 or G.shape[1] == 0:
         return np.zeros((R.size, G.shape[1]))
+    _f("sketch_diag_solve", (c1 - c0) ** 2 * G.shape[1])
     G1 = diag_solve(node, G, transpose=True)
     W = full[R, c0:c1] @ G1
+    _f(_CAT[-1], 2.0 * W.shape[1] * full[R, c0:c1].nnz if COUNT is not None else 0.0)
     for src in srcs:
         if src.kind == "interior":
             W -= src.blk.multiply(full, R, np.arange(c0, c1), G1)
@@ -424,6 +476,7 @@ def off_mul(full, node, G, srcs):
         if lo == hi or hi == rows.shape[0]:
             continue
         off = src.node.off
+        _f(_CAT[-1], 2.0 * (rows.shape[0] - lo) * raw(off, slice(lo, hi)).shape[1] * G1.shape[1])
         T = raw(off, slice(lo, hi)).T @ G1[rows[lo:hi] - c0]
         W[np.searchsorted(R, rows[hi:])] -= eff(off, slice(hi, None)) @ T
     return W
@@ -435,6 +488,8 @@ def off_mul_t(full, node, G, srcs):
     if G.shape[1] == 0:
         return np.zeros((c1 - c0, 0))
     W = full[R, c0:c1].T @ G
+    _f(_CAT[-1], 2.0 * G.shape[1] * full[R, c0:c1].nnz if COUNT is not None else 0.0)
+    _f("sketch_diag_solve", (c1 - c0) ** 2 * G.shape[1])
     for src in srcs:
         if src.kind == "interior":
             W -= src.blk.multiply(full, np.arange(c0, c1), R, G)
@@ -444,6 +499,7 @@ def off_mul_t(full, node, G, srcs):
         if lo == hi or hi == rows.shape[0]:
             continue
         off = src.node.off
+        _f(_CAT[-1], 2.0 * (rows.shape[0] - lo) * raw(off, slice(lo, hi)).shape[1] * G.shape[1])
         T = eff(off, slice(hi, None)).T @ G[np.searchsorted(R, rows[hi:])]
         W[rows[lo:hi] - c0] -= raw(off, slice(lo, hi)) @ T
     return diag_solve(node, W, transpose=False)
@@ -455,6 +511,7 @@ def approx_off(full, node, rank, q, seed, srcs):
     G = off_mul_t(full, node, gauss(R.size, rank, seed), srcs)
     for _ in range(q):
         G = off_mul_t(full, node, off_mul(full, node, G, srcs), srcs)
+    _f("qrcp", 4.0 * G.shape[0] * G.shape[1] ** 2)
     U = orth(G)
     return LR(off_mul(full, node, U, srcs), U)
 
@@ -577,7 +634,9 @@ def numeric_pass(full, F, cfg, alpha_d, counters):
                 nr, ncl = tn.hi - tn.split, tn.split - tn.lo
                 r = block_rank(nr, ncl, alpha_d, cfg.oversample)
                 if r >= DENSE_FALLBACK * min(nr, ncl):
+                    _CAT.append("diag_sketch")
                     tree.blocks[s] = diag_multiply(full, node, s, np.eye(ncl), False, srcs)
+                    _CAT.pop()
                     counters["dense_fallback"] += 1
                 else:
                     tree.blocks[s] = approx_diag_block(full, node, s, r, cfg.power_iters,
@@ -586,6 +645,7 @@ def numeric_pass(full, F, cfg, alpha_d, counters):
                     counters["compressed_diag"] += 1
         else:
             UD, UO = assemble_schur(full, node, R, srcs, want_off=not compress_off)
+            _f("potrf_trsm", nc**3 / 3.0)
             node.diag = chol(UD)
         if R.size == 0:
             node.off = None
@@ -601,6 +661,7 @@ def numeric_pass(full, F, cfg, alpha_d, counters):
                 node.off = diag_solve(node, UO2.T).T if UO2.shape[0] else UO2
             else:
                 node.off = trisolve(node.diag, UO.T).T
+            _f("potrf_trsm", R.size * nc * nc)
         F.units.append(("node", node))
         for src in srcs:
             hi = np.searchsorted(src.rows, c1)

@@ -193,6 +193,7 @@ class DeviceApply:
                 if t.Linv is None:
                     t.Linv = self.mem.empty(t.n, t.n)
                     t.LinvT = self.mem.empty(t.n, t.n)
+                    t.inv_mem = self.mem  # a later program may reuse these views
         self.refresh_inverses()
 
     def refresh_inverses(self):

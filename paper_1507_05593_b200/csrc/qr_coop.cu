@@ -826,6 +826,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nsm = std::min(nsm, CQ_MAX);  // a group never has more CTAs than pivot-candidate slots
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(mqrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);

@@ -128,11 +128,12 @@ def _gaussian(m, n, seed):
 class DenseTri:
     """Dense lower triangle + inverse 64x64 diagonal blocks."""
 
-    __slots__ = ("L", "Dinv", "n", "Linv", "LinvT")
+    __slots__ = ("L", "Dinv", "n", "Linv", "LinvT", "inv_mem")
 
     def __init__(self, L, Dinv):
         self.L, self.Dinv, self.n = L, Dinv, L.shape[0]
         self.Linv = self.LinvT = None  # explicit inverse (and its transpose), built for the apply
+        self.inv_mem = None  # the arena Linv/LinvT were carved from (kept alive with them)
 
     def solve(self, X, transpose=False):
         """X <- L^{-1} X (or L^{-T} X) in place; X is an n x r row-major view."""

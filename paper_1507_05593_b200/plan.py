@@ -25,6 +25,15 @@ import torch
 from . import engine as E
 
 
+def _pattern_key(A):
+    """Digest of a lower-CSC sparsity pattern (col_ptr, row_idx)."""
+    import hashlib
+
+    h = hashlib.sha1(np.ascontiguousarray(A.col_ptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(A.row_idx, dtype=np.int64).tobytes())
+    return (A.n, h.hexdigest())
+
+
 class Source:
     """One update source: an interior block (rows = off_rows) or a compressed
     supernode (rows = R_j).  `order` is its first column (factor.py:565,639)."""
@@ -203,6 +212,7 @@ class NumericPlan:
         # B.values = A.values[b_from_a] (the gather analyze used to permute A)
         self.b_from_a = getattr(sym, "b_from_a", None) if A is not None else None
         self.source = A
+        self.pattern_key = _pattern_key(A) if A is not None else None  # load_values checks it
         self.idx = IndexPool()
         self.csr = CsrPool(full)
         self.sources = []
@@ -286,7 +296,7 @@ class NumericPlan:
             return
         if self.b_from_a is None:
             raise ValueError("plan was prepared without its source matrix; cannot load new values")
-        if A.n != self.sym.B.n or A.nnz_lower != self.b_from_a.size:
+        if A.n != self.sym.B.n or A.nnz_lower != self.b_from_a.size or _pattern_key(A) != self.pattern_key:
             raise ValueError("matrix pattern differs from the prepared one")
         if getattr(self, "_a_index", None) is None:  # A position of every block entry
             self._a_index = E.to_dev(self.b_from_a.astype(np.int32))[self.csr.pos_dev.long()]

@@ -242,3 +242,28 @@ def test_graph_refactorization_new_ranks_patches_apply(cuda):
     for _ in range(5):                 # eager, then the re-captured graph
         assert relerr(H.apply(r), ref2) < 3e-8
     assert prog.graph not in (None, False)
+
+
+def test_prepared_plan_rejects_other_pattern(cuda):
+    """factorize(prepared=) checks the full sparsity pattern, not only n and nnz
+    (ADVICE r01): an equal-nnz matrix with one entry moved raises ValueError."""
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.factor import SolverConfig, prepare
+    from paper_1507_05593_b200.problems import laplacian_3d
+    from paper_1507_05593_b200.sparse import SparseSpdMatrix
+
+    A, coords = laplacian_3d(8)
+    conf = SolverConfig(tau_o=16, tau_d=32, oversample=4)
+    prep = prepare(A, conf, coords)
+    F = factorize(A, prepared=prep)  # same matrix: fine
+    assert F.n == A.n
+    cols = np.repeat(np.arange(A.n), np.diff(A.col_ptr))
+    rows = A.row_idx.copy()
+    k = int(np.nonzero(rows > cols)[0][-1])  # an off-diagonal entry of the last such column
+    j = int(cols[k])
+    free = sorted(set(range(j + 1, A.n)) - set(rows[cols == j].tolist()))
+    rows[k] = free[0]
+    B = SparseSpdMatrix.from_coo(A.n, rows, cols, A.values)
+    assert B.nnz_lower == A.nnz_lower
+    with pytest.raises(ValueError):
+        factorize(B, prepared=prep)
