@@ -259,7 +259,7 @@ def test_prepared_plan_rejects_other_pattern(cuda):
     assert F.n == A.n
     cols = np.repeat(np.arange(A.n), np.diff(A.col_ptr))
     rows = A.row_idx.copy()
-    k = int(np.nonzero(rows > cols)[0][-1])  # an off-diagonal entry of the last such column
+    k = int(np.nonzero(rows > cols)[0][0])  # the first off-diagonal entry (column 0)
     j = int(cols[k])
     free = sorted(set(range(j + 1, A.n)) - set(rows[cols == j].tolist()))
     rows[k] = free[0]
