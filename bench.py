@@ -1,18 +1,22 @@
 """Benchmark of the B200 rank-structured Cholesky hot path (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 4]
 
-Default workload: BASELINE config[1] -- 512 independent supernodes (256x256 SPD
-diagonal, 2048x256 rank-48+noise off-diagonal): POTRF + TRSM + Gaussian sketch
-(r=58, q=1) + pivoted-QR compression, i.e. the reference composition
-dense_cholesky -> tri_solve -> low_rank_approx per block.  A step is one pass over
-the whole batch.  value = aggregate factor GFLOP/s (algorithmic FLOPs of SURVEY
-§8(d) / device time), inputs resident in HBM; e2e = the same through the host
-API (H2D of inputs, host PCG64 sketches, D2H of the factor).
+Default workload: BASELINE config[4] (3D linear elasticity, 64^3 hexahedral elements,
+n = 811,200, stored zeros stripped) -- the largest single-GPU config by work and nnz.
+A step is one numeric factorization + PCG to relative residual 1e-6; value = its
+device-timed seconds (the BASELINE metric "factor+PCG time"), e2e = the one-shot
+public API (ordering + symbolic + numeric + PCG, host buffers in and out).  The
+reference arm times the full-size oracle factor + PCG on the host (bench_sparse.py).
+`--config 2|3|0` selects the other sparse configs, `--config 1` the batched
+supernode micro-benchmark (512 independent 256x256 supernodes: POTRF + TRSM + sketch
+r=58 + pivoted-QR compression, GFLOP/s).
 
-Multi-GPU: one process per GPU (torchrun), each rank factors its own batch of
-512 supernodes (the config shards by independent supernodes; no collective on the
-data path) -> scaling "weak"; time = max over ranks of the device-timed region.
+Multi-GPU: `--gpus N` without a torchrun environment relaunches itself under
+`torch.distributed.run` with N processes (one per GPU).  The sparse configs shard by
+nested-dissection subtree (distributed.py); config[1] by independent supernodes
+(weak scaling, no data-path collective).  Time = max over ranks of the device-timed
+region.
 """
 
 import argparse
@@ -40,12 +44,14 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--config", type=int, default=4)
     p.add_argument("--nb", type=int, default=512)
     p.add_argument("--chunk", type=int, default=None, help="supernodes per grouped launch (default: all)")
     p.add_argument("--grid", type=int, default=None, help="grid size override for sparse configs")
     p.add_argument("--cpu-sample", type=int, default=128, help="blocks in the CPU baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-budget", type=float, default=1560.0,
+                   help="reference arm: wall seconds before the remaining sweep is extrapolated")
     return p.parse_args()
 
 
@@ -269,7 +275,7 @@ def run_b200_cfg1(args, rank, world, torch, dist):
 
     # end to end through the host API
     e2e = None
-    if rank == 0 or True:
+    if True:  # every rank measures its own e2e (max over ranks below)
         st = bs.pinned_staging()
         # the caller's host inputs live in page-locked memory (what a serving process
         # would allocate for a stream of factorizations)
@@ -354,12 +360,31 @@ def run_b200_cfg1(args, rank, world, torch, dist):
     print(json.dumps(line), flush=True)
 
 
+def _relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        if args.config == 1:
+            run_reference(args, rank)
+        else:
+            from bench_sparse import run_reference_sparse
+
+            run_reference_sparse(args, rank)
         return
     import torch
 
@@ -374,7 +399,7 @@ def main():
         if args.config == 1:
             run_b200_cfg1(args, rank, world, torch, dist)
         else:
-            from paper_1507_05593_b200.benchsparse import run_sparse
+            from bench_sparse import run_sparse
 
             run_sparse(args, rank, world, torch, dist)
     finally:

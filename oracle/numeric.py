@@ -90,8 +90,15 @@ class LR:
         return self.V @ self.U.T
 
 
-def eff(off, sl):
-    return off.V[sl] @ off.utu if isinstance(off, LR) else off[sl]
+def eff(off, sl, cat=None):
+    """eff_rows (blocks.py:103-113): V[sl] (U^T U) for a low-rank block -- a GEMM the
+    reference executes on every use (counted under `cat`)."""
+    if isinstance(off, LR):
+        out = off.V[sl] @ off.utu
+        if cat is not None:
+            _f(cat, 2.0 * out.shape[0] * off.V.shape[1] ** 2)
+        return out
+    return off[sl]
 
 
 def raw(off, sl):
@@ -332,7 +339,7 @@ def _win_update(U, src, rw, cw, full):
     off = src.node.off
     w = off.V.shape[1] if isinstance(off, LR) else off.shape[1]
     _f("leaf_syrk", 2.0 * (rhi - rlo) * (chi - clo) * w)
-    U[np.ix_(rows[rlo:rhi] - r0, rows[clo:chi] - c0)] -= eff(off, slice(rlo, rhi)) @ raw(off, slice(clo, chi)).T
+    U[np.ix_(rows[rlo:rhi] - r0, rows[clo:chi] - c0)] -= eff(off, slice(rlo, rhi), "leaf_syrk") @ raw(off, slice(clo, chi)).T
 
 
 def _win_multiply(W, src, rw, cw, G, transpose, full):
@@ -352,17 +359,17 @@ def _win_multiply(W, src, rw, cw, G, transpose, full):
     w = off.V.shape[1] if isinstance(off, LR) else off.shape[1]
     _f(_CAT[-1], 2.0 * ((rhi - rlo) + (chi - clo)) * w * G.shape[1])
     if transpose:
-        T = eff(off, slice(rlo, rhi)).T @ G[rows[rlo:rhi] - r0]
+        T = eff(off, slice(rlo, rhi), _CAT[-1]).T @ G[rows[rlo:rhi] - r0]
         W[rows[clo:chi] - c0] -= raw(off, slice(clo, chi)) @ T
     else:
         T = raw(off, slice(clo, chi)).T @ G[rows[clo:chi] - c0]
-        W[rows[rlo:rhi] - r0] -= eff(off, slice(rlo, rhi)) @ T
+        W[rows[rlo:rhi] - r0] -= eff(off, slice(rlo, rhi), _CAT[-1]) @ T
 
 
-def _path_pair(tree, p, rspan, cspan):
+def _path_pair(tree, p, rspan, cspan, cat=None):
     base = tree.nodes[p].split
     b = tree.blocks[p]
-    return eff(b, slice(rspan[0] - base, rspan[1] - base)), raw(b, slice(cspan[0] - base, cspan[1] - base))
+    return eff(b, slice(rspan[0] - base, rspan[1] - base), cat), raw(b, slice(cspan[0] - base, cspan[1] - base))
 
 
 def factor_leaf(full, node, s, srcs):
@@ -373,7 +380,7 @@ def factor_leaf(full, node, s, srcs):
     for src in srcs:
         _win_update(U, src, (g0, g1), (g0, g1), full)
     for p in tree.path_above(s):
-        P, Q = _path_pair(tree, p, (lf.lo, lf.hi), (lf.lo, lf.hi))
+        P, Q = _path_pair(tree, p, (lf.lo, lf.hi), (lf.lo, lf.hi), "leaf_path")
         _f("leaf_path", 2.0 * P.shape[0] * Q.shape[0] * P.shape[1])
         U -= P @ Q.T
     _f("potrf_trsm", (g1 - g0) ** 3 / 3.0)
@@ -394,7 +401,7 @@ def diag_multiply(full, node, s, G, transpose, srcs):
         for src in srcs:
             _win_multiply(W, src, gr, gc, G1, False, full)
         for p in tree.path_above(s):
-            P, Q = _path_pair(tree, p, (r0, r1), (c0, c1))
+            P, Q = _path_pair(tree, p, (r0, r1), (c0, c1), _CAT[-1])
             _f(_CAT[-1], 2.0 * (P.shape[0] + Q.shape[0]) * P.shape[1] * G1.shape[1])
             W -= P @ (Q.T @ G1)
         return W
@@ -402,7 +409,7 @@ def diag_multiply(full, node, s, G, transpose, srcs):
     for src in srcs:
         _win_multiply(W, src, gr, gc, G, True, full)
     for p in tree.path_above(s):
-        P, Q = _path_pair(tree, p, (r0, r1), (c0, c1))
+        P, Q = _path_pair(tree, p, (r0, r1), (c0, c1), _CAT[-1])
         _f(_CAT[-1], 2.0 * (P.shape[0] + Q.shape[0]) * P.shape[1] * G.shape[1])
         W -= Q @ (P.T @ G)
     return diag_solve(node, W, transpose=False, s=blk.left.s)
@@ -452,9 +459,9 @@ def assemble_schur(full, node, R, srcs, want_off=True):
         Q = raw(off, slice(lo, hi))
         _f("node_syrk_gemm", 2.0 * (hi - lo) ** 2 * Q.shape[1]
            + (2.0 * (rows.shape[0] - hi) * (hi - lo) * Q.shape[1] if (hi < rows.shape[0] and want_off) else 0.0))
-        UD[np.ix_(cpos, cpos)] -= eff(off, slice(lo, hi)) @ Q.T
+        UD[np.ix_(cpos, cpos)] -= eff(off, slice(lo, hi), "node_syrk_gemm") @ Q.T
         if hi < rows.shape[0] and want_off:
-            UO[np.ix_(np.searchsorted(R, rows[hi:]), cpos)] -= eff(off, slice(hi, None)) @ Q.T
+            UO[np.ix_(np.searchsorted(R, rows[hi:]), cpos)] -= eff(off, slice(hi, None), "node_syrk_gemm") @ Q.T
     return UD, UO
 
 
@@ -478,7 +485,7 @@ def off_mul(full, node, G, srcs):
         off = src.node.off
         _f(_CAT[-1], 2.0 * (rows.shape[0] - lo) * raw(off, slice(lo, hi)).shape[1] * G1.shape[1])
         T = raw(off, slice(lo, hi)).T @ G1[rows[lo:hi] - c0]
-        W[np.searchsorted(R, rows[hi:])] -= eff(off, slice(hi, None)) @ T
+        W[np.searchsorted(R, rows[hi:])] -= eff(off, slice(hi, None), _CAT[-1]) @ T
     return W
 
 
@@ -500,7 +507,7 @@ def off_mul_t(full, node, G, srcs):
             continue
         off = src.node.off
         _f(_CAT[-1], 2.0 * (rows.shape[0] - lo) * raw(off, slice(lo, hi)).shape[1] * G.shape[1])
-        T = eff(off, slice(hi, None)).T @ G[np.searchsorted(R, rows[hi:])]
+        T = eff(off, slice(hi, None), _CAT[-1]).T @ G[np.searchsorted(R, rows[hi:])]
         W[rows[lo:hi] - c0] -= raw(off, slice(lo, hi)) @ T
     return diag_solve(node, W, transpose=False)
 
@@ -587,7 +594,7 @@ class Factor:
         return L
 
 
-def numeric_pass(full, F, cfg, alpha_d, counters):
+def numeric_pass(full, F, cfg, alpha_d, counters, on_unit=None):
     plan = F.plan
     part = plan.partition
     M = part.count
@@ -599,7 +606,9 @@ def numeric_pass(full, F, cfg, alpha_d, counters):
         if src.rows.size:
             buckets[part.supernode_of(int(src.rows[0]))].append(src)
 
-    for kind, payload in plan.units:
+    for u, (kind, payload) in enumerate(plan.units):
+        if on_unit is not None:  # bench hook: per-unit timestamps / BLAS thread policy
+            on_unit(u, kind, payload)
         if kind == "interior":
             blk = factor_interior(full, part, payload, len(F.interior))
             F.interior.append(blk)
@@ -671,7 +680,7 @@ def numeric_pass(full, F, cfg, alpha_d, counters):
             file(Src("node", R, c0, node=node))
 
 
-def factorize(A, cfg=None, coords=None, plan=None):
+def factorize(A, cfg=None, coords=None, plan=None, on_unit=None):
     """Oracle factorization (factor.py:642-740) on the product's symbolic plan."""
     from paper_1507_05593_b200.symbolic import analyze
 
@@ -688,7 +697,7 @@ def factorize(A, cfg=None, coords=None, plan=None):
     while True:
         counters = {"diag_trees": 0, "compressed_off": 0, "compressed_diag": 0, "dense_fallback": 0}
         try:
-            numeric_pass(full, F, cfg, alpha_d, counters)
+            numeric_pass(full, F, cfg, alpha_d, counters, on_unit)
             break
         except OracleIndefinite:
             if counters["diag_trees"] == 0:

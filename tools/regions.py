@@ -7,7 +7,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1507_05593_b200 import engine as E  # noqa: E402
-from paper_1507_05593_b200.benchsparse import KNOBS, _problem  # noqa: E402
+from bench_sparse import KNOBS, _problem  # noqa: E402
 from paper_1507_05593_b200.factor import SolverConfig, factorize, prepare  # noqa: E402
 
 cfg, grid = int(sys.argv[1]), int(sys.argv[2])

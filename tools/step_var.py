@@ -10,7 +10,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1507_05593_b200 import engine as E  # noqa: E402
-from paper_1507_05593_b200.benchsparse import GRID, KNOBS, _problem  # noqa: E402
+from bench_sparse import GRID, KNOBS, _problem  # noqa: E402
 from paper_1507_05593_b200.factor import SolverConfig, factorize, prepare  # noqa: E402
 from paper_1507_05593_b200.pcg import pcg_solve_device  # noqa: E402
 
