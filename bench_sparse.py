@@ -249,7 +249,7 @@ def run_sparse(args, rank, world, torch, dist):
     busy_s = sum(e.device_time for e in kev) / 1e6
     by_kernel = {}
     for e in kev:
-        nm = e.name.split("<")[0].split("(")[0]
+        nm = e.name.replace("void ", "").replace("(anonymous namespace)::", "").split("<")[0].split("(")[0]
         by_kernel[nm] = by_kernel.get(nm, 0.0) + e.device_time / 1e6
     top = sorted(by_kernel.items(), key=lambda x: -x[1])[:8]
     prof = {"flops": gemm_flops, "seconds": gemm_s}

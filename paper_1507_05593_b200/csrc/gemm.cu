@@ -295,36 +295,74 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
 struct RedProb {
     const double *P;      // partial: batch x M x N, dense
     const int *c_rows;    // non-decreasing (or null = identity)
-    const int *c_cols;
-    int M, N;
+    const int *c_cols;    // strictly increasing (or null = identity)
+    int M, N, g;          // g: group index
 };
 
 struct RedGroup {
     double *C;            // target block (all problems of the group share it)
     long long sC;         // batch stride of C
-    int ldc, ext_r, batch, TR, p0, np;
+    int *rtab;            // [ext_r][np]: first local row of problem q mapped to target row t, or -1
+    int *ctab;            // [np][ext_c]: local column of problem q mapped to target column c, or -1
+    int ldc, ext_r, ext_c, batch, p0, np, TR, CW;
 };
 
 struct RedArgs {
     int count;            // groups
+    int nprob;
     long long cta_begin[MAXP + 1];
     RedGroup g[MAXP];
     RedProb p[MAXP];
 };
 
 constexpr int RT = 256;
+#ifndef RED_EPT
+#define RED_EPT 1  // target elements per reduce thread
+#endif
+#ifndef RED_U
+#define RED_U 16   // partial loads in flight per element
+#endif
+constexpr int TR_MAX = 64;
+constexpr int MW = (MAXP + 31) / 32;  // problem-mask words per row
 
-__device__ __forceinline__ int lower_bound_dev(const int *a, int n, int x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+// Inverse maps of every mapped problem of the chunk (tables pre-set to -1).
+__global__ void __launch_bounds__(RT) reduce_tables_kernel(const __grid_constant__ RedArgs a) {
+    const RedProb &P = a.p[blockIdx.x];
+    const RedGroup &G = a.g[P.g];
+    const int q = blockIdx.x - G.p0;
+    if (G.rtab) {
+        for (int i = threadIdx.x; i < P.M; i += RT) {
+            const int t = P.c_rows ? __ldg(P.c_rows + i) : i;
+            // a run of repeated rows is represented by its first local row; the run
+            // length rides in the high 8 bits (repeats: interior-block rows outside
+            // the target structure, whose products are exact zeros)
+            if (t < G.ext_r && (i == 0 || !P.c_rows || __ldg(P.c_rows + i - 1) != t)) {
+                int run = 1;
+                if (P.c_rows)
+                    while (i + run < P.M && run < 255 && __ldg(P.c_rows + i + run) == t) ++run;
+                G.rtab[(long long)t * G.np + q] = i | (run << 24);
+            }
+        }
     }
-    return lo;
+    if (G.ctab) {
+        for (int j = threadIdx.x; j < P.N; j += RT) {
+            const int c = P.c_cols ? __ldg(P.c_cols + j) : j;
+            if (c < G.ext_c) G.ctab[(long long)q * G.ext_c + c] = j;
+        }
+    }
 }
 
+// One CTA owns a TR x CW tile of one target block; every element is a register sum
+// C + P_q1 + P_q2 + ... over the problems that reach it, in problem order.  Per row
+// of the tile the contributing (problem, first local row, run length) entries are
+// collected once, in problem order, into shared memory by one warp per row (ballot
+// + popc compaction), so the element loop issues only independent partial loads.
+constexpr int LIST_MAX = 4096;  // entries per CTA (TR x np bounded by the host)
+
 __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constant__ RedArgs a) {
-    __shared__ int s_i0[MAXP], s_i1[MAXP];
+    __shared__ int s_q[LIST_MAX];
+    __shared__ int s_i[LIST_MAX];
+    __shared__ int s_cnt[TR_MAX];
     const long long cta = blockIdx.x;
     int lo = 0, hi = a.count - 1;
     while (lo < hi) {
@@ -333,52 +371,74 @@ __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constan
     }
     const RedGroup &G = a.g[lo];
     const long long local = cta - a.cta_begin[lo];
-    const int nt = (G.ext_r + G.TR - 1) / G.TR;
-    const int b = (int)(local / nt);
-    const int t0 = (int)(local - (long long)b * nt) * G.TR;
-    const int t1 = min(t0 + G.TR, G.ext_r);
-    // local row range of every problem inside this band (maps are increasing)
-    for (int q = threadIdx.x; q < G.np; q += RT) {
-        const RedProb &P = a.p[G.p0 + q];
-        int i0, i1;
-        if (P.c_rows) {
-            i0 = lower_bound_dev(P.c_rows, P.M, t0);
-            i1 = i0 + lower_bound_dev(P.c_rows + i0, P.M - i0, t1);
-        } else {
-            i0 = min(t0, P.M);
-            i1 = min(t1, P.M);
+    const int nbr = (G.ext_r + G.TR - 1) / G.TR, nbc = (G.ext_c + G.CW - 1) / G.CW;
+    const int b = (int)(local / ((long long)nbr * nbc));
+    const int rem = (int)(local - (long long)b * nbr * nbc);
+    const int t0 = (rem / nbc) * G.TR, c0 = (rem % nbc) * G.CW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // per-row contributor lists: row tt owns s_q/s_i[tt * np ...]; s_i packs the first
+    // local row (low 24 bits) and the run length of repeated rows (high 8 bits)
+    for (int tt = warp; tt < G.TR; tt += RT / 32) {
+        const int t = t0 + tt;
+        int n = 0;
+        if (t < G.ext_r) {
+            for (int q0 = 0; q0 < G.np; q0 += 32) {
+                const int q = q0 + lane;
+                int i = -1;  // packed: first local row | run length << 24
+                if (q < G.np) {
+                    if (G.rtab) i = __ldg(G.rtab + (long long)t * G.np + q);
+                    else i = t < a.p[G.p0 + q].M ? (t | (1 << 24)) : -1;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, i >= 0);
+                if (i >= 0) {
+                    const int pos = tt * G.np + n + __popc(bal & ((1u << lane) - 1u));
+                    s_q[pos] = q;
+                    s_i[pos] = i;
+                }
+                n += __popc(bal);
+            }
         }
-        s_i0[q] = i0;
-        s_i1[q] = i1;
+        if (lane == 0) s_cnt[tt] = n;
     }
     __syncthreads();
     double *C = G.C + (long long)b * G.sC;
-    for (int q = 0; q < G.np; ++q) {
-        const int i0 = s_i0[q], i1 = s_i1[q];
-        if (i0 >= i1) continue;  // block-uniform
-        const RedProb &P = a.p[G.p0 + q];
-        const int n = P.N;
-        const double *src = P.P + (long long)b * P.M * n;
-        const int cnt = (i1 - i0) * n;
-        for (int e = threadIdx.x; e < cnt; e += RT) {
-            const int di = e / n;
-            const int i = i0 + di, j = e - di * n;
-            const int c = P.c_cols ? __ldg(P.c_cols + j) : j;
-            if (!P.c_rows) {
-                C[(long long)i * G.ldc + c] += src[(long long)i * n + j];
-                continue;
+    constexpr int U = RED_U;
+    for (int e = threadIdx.x; e < G.TR * G.CW; e += RT) {
+        const int tt = e / G.CW, t = t0 + tt, c = c0 + (e - tt * G.CW);
+        const int n = s_cnt[tt];
+        if (n == 0 || t >= G.ext_r || c >= G.ext_c) continue;
+        const int *lq = s_q + tt * G.np, *li = s_i + tt * G.np;
+        double *dst = C + (long long)t * G.ldc + c;
+        double acc = *dst;
+        unsigned any = 0;
+        for (int k0 = 0; k0 < n; k0 += U) {
+            // U independent partial loads in flight, then the in-order sum
+            double v[U];
+            unsigned ok = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                v[u] = 0.0;
+                const int k = k0 + u;
+                if (k < n) {
+                    const int q = lq[k];
+                    const RedProb &P = a.p[G.p0 + q];
+                    const int j = G.ctab ? __ldg(G.ctab + (long long)q * G.ext_c + c) : (c < P.N ? c : -1);
+                    if (j >= 0) {
+                        const int packed = li[k], i = packed & 0xffffff, run = (unsigned)packed >> 24;
+                        const double *src = P.P + (long long)b * P.M * P.N + (long long)i * P.N + j;
+                        double x = src[0];
+                        for (int r = 1; r < run; ++r) x += src[(long long)r * P.N];  // exact-zero repeats
+                        v[u] = x;
+                        ok |= 1u << u;
+                    }
+                }
             }
-            // Row maps are non-decreasing but may repeat: searchsorted maps of
-            // interior-block rows outside the target's structure (their products are
-            // exact zeros, see plan._build_targets).  The first local row of a run
-            // sums the whole run, so no two threads ever update the same element.
-            const int r = __ldg(P.c_rows + i);
-            if (i > i0 && __ldg(P.c_rows + i - 1) == r) continue;
-            double v = src[(long long)i * n + j];
-            for (int k = i + 1; k < i1 && __ldg(P.c_rows + k) == r; ++k) v += src[(long long)k * n + j];
-            C[(long long)r * G.ldc + c] += v;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if ((ok >> u) & 1u) acc += v[u];
+            any |= ok;
         }
-        __syncthreads();  // problem q+1 may hit the same elements through other threads
+        if (any) *dst = acc;
     }
 }
 
@@ -412,11 +472,14 @@ WsEntry lookup_ws(void *stream) {
 }
 
 // Build and launch the ordered reduction for the accumulating problems of one chunk
-// (reds, in launch order).  Groups = distinct (C, strideC, batch) targets, each
-// keeping its problems in order.
-int launch_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<const double *> &parts,
-                  cudaStream_t s) {
-    static thread_local RedArgs ra;
+// (reds, in launch order; argi = their slot in the GEMM launch).  Groups = distinct
+// (C, strideC, batch) targets, each keeping its problems in order.  A group with a
+// single unmapped problem needs no ordering: that problem is switched back to a
+// direct C += alpha op(A) op(B) in the GEMM launch itself (returned in `direct`).
+// Tables for the inverse maps are carved from `tab` (bytes available: tab_bytes).
+int plan_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<const double *> &parts,
+                char *tab, long long tab_bytes, RedArgs &ra, std::vector<int> &direct, long long &ctas,
+                long long &tab_used) {
     const int n = (int)reds.size();
     std::vector<int> gid(n, -1);
     std::vector<int> gfirst;
@@ -433,18 +496,15 @@ int launch_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<c
         }
         gid[i] = g;
     }
-    ra.count = (int)gfirst.size();
-    long long ctas = 0;
-    int pos = 0;
-    for (int g = 0; g < ra.count; ++g) {
+    ra.count = 0;
+    ra.nprob = 0;
+    ctas = 0;
+    tab_used = 0;
+    direct.clear();
+    for (int g = 0; g < (int)gfirst.size(); ++g) {
         const rsc_gemm_problem &f = reds[gfirst[g]];
-        RedGroup &G = ra.g[g];
-        G.C = f.C;
-        G.sC = f.strideC;
-        G.ldc = f.ldc;
-        G.batch = f.batch;
-        G.p0 = pos;
-        int er = 0, ec = 0;
+        int np = 0, er = 0, ec = 0;
+        bool rmap = false, cmap = false;
         for (int i = 0; i < n; ++i) {
             if (gid[i] != g) continue;
             const rsc_gemm_problem &p = reds[i];
@@ -452,56 +512,105 @@ int launch_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<c
             if ((p.c_rows && p.ext_r <= 0) || (p.c_cols && p.ext_c <= 0)) return -3;
             er = std::max(er, p.ext_r > 0 ? p.ext_r : p.M);
             ec = std::max(ec, p.ext_c > 0 ? p.ext_c : p.N);
-            RedProb &rp = ra.p[pos++];
+            rmap |= p.c_rows != nullptr;
+            cmap |= p.c_cols != nullptr;
+            ++np;
+        }
+        if (np == 1 && !rmap && !cmap) {
+            direct.push_back(gfirst[g]);
+            continue;
+        }
+        RedGroup &G = ra.g[ra.count];
+        G.C = f.C;
+        G.sC = f.strideC;
+        G.ldc = f.ldc;
+        G.batch = f.batch;
+        G.ext_r = er;
+        G.ext_c = ec;
+        G.p0 = ra.nprob;
+        G.np = np;
+        G.CW = std::min(ec, RT);
+        G.TR = std::max(1, std::min(std::min(TR_MAX, (RT * RED_EPT) / G.CW), LIST_MAX / np));
+        G.rtab = G.ctab = nullptr;
+        const long long rb = rmap ? ((long long)er * np * 4 + 255) / 256 * 256 : 0;
+        const long long cb = cmap ? ((long long)ec * np * 4 + 255) / 256 * 256 : 0;
+        if (tab_used + rb + cb > tab_bytes) return -6;
+        if (rmap) G.rtab = (int *)(tab + tab_used);
+        if (cmap) G.ctab = (int *)(tab + tab_used + rb);
+        tab_used += rb + cb;
+        for (int i = 0; i < n; ++i) {
+            if (gid[i] != g) continue;
+            const rsc_gemm_problem &p = reds[i];
+            RedProb &rp = ra.p[ra.nprob++];
             rp.P = parts[i];
             rp.c_rows = p.c_rows;
             rp.c_cols = p.c_cols;
             rp.M = p.M;
             rp.N = p.N;
+            rp.g = ra.count;
         }
-        G.np = pos - G.p0;
-        G.ext_r = er;
-        G.TR = std::max(4, std::min(64, 2048 / std::max(ec, 1)));
-        ra.cta_begin[g] = ctas;
-        ctas += (long long)((er + G.TR - 1) / G.TR) * G.batch;
+        ra.cta_begin[ra.count] = ctas;
+        ctas += (long long)((er + G.TR - 1) / G.TR) * ((ec + G.CW - 1) / G.CW) * G.batch;
+        ++ra.count;
     }
     ra.cta_begin[ra.count] = ctas;
-    static const bool dbg = getenv("RSC_GEMM_DEBUG") != nullptr;
-    if (dbg) {  // diagnostics: target overlap between groups, map monotonicity and range
-        cudaStreamSynchronize(s);
-        for (int g = 0; g < ra.count; ++g) {
-            const RedGroup &G = ra.g[g];
-            const char *lo1 = (const char *)G.C;
-            const char *hi1 = lo1 + 8 * ((long long)(G.ext_r - 1) * G.ldc + 1);
-            for (int h = g + 1; h < ra.count; ++h) {
-                const RedGroup &H = ra.g[h];
-                const char *lo2 = (const char *)H.C;
-                const char *hi2 = lo2 + 8 * ((long long)(H.ext_r - 1) * H.ldc + 1);
-                if (lo1 < hi2 && lo2 < hi1)
-                    fprintf(stderr, "RSC_GEMM_DEBUG: groups %d/%d overlap (C %p ext %d ld %d / C %p ext %d ld %d)\n",
-                            g, h, (void *)G.C, G.ext_r, G.ldc, (void *)H.C, H.ext_r, H.ldc);
-            }
-            for (int q = G.p0; q < G.p0 + G.np; ++q) {
-                const RedProb &P = ra.p[q];
-                for (int w = 0; w < 2; ++w) {
-                    const int *mp = w ? P.c_cols : P.c_rows;
-                    const int len = w ? P.N : P.M;
-                    if (!mp) continue;
-                    std::vector<int> hv(len);
-                    cudaMemcpy(hv.data(), mp, sizeof(int) * len, cudaMemcpyDeviceToHost);
-                    for (int t = 0; t < len; ++t) {
-                        const bool bad = (t && (w ? hv[t] <= hv[t - 1] : hv[t] < hv[t - 1])) || hv[t] < 0;
-                        if (bad) {
-                            fprintf(stderr, "RSC_GEMM_DEBUG: group %d prob %d %s map bad at %d: %d (prev %d, ext_r %d)\n",
-                                    g, q, w ? "col" : "row", t, hv[t], t ? hv[t - 1] : -1, G.ext_r);
-                            break;
-                        }
-                    }
-                }
-            }
+    return 0;
+}
+
+struct RedStats {
+    long long launches = 0, ctas = 0, groups = 0, probs = 0, target_el = 0, partial_el = 0, direct = 0;
+    long long hist[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // launches by CTA count: <8, <64, <512, <4096, ...
+    ~RedStats() {
+        if (!getenv("RSC_GEMM_STATS")) return;
+        fprintf(stderr, "RSC_GEMM_STATS reduce launches %lld ctas %lld groups %lld probs %lld target_el %lld "
+                "partial_el %lld direct %lld\n", launches, ctas, groups, probs, target_el, partial_el, direct);
+        fprintf(stderr, "RSC_GEMM_STATS cta hist <8:%lld <64:%lld <512:%lld <4k:%lld <32k:%lld more:%lld\n", hist[0],
+                hist[1], hist[2], hist[3], hist[4], hist[5]);
+    }
+};
+RedStats g_rstats;
+
+int launch_reduce(RedArgs &ra, long long ctas, char *tab, long long tab_used, cudaStream_t s) {
+    if (ra.count == 0 || ctas <= 0) return 0;
+    {
+        g_rstats.launches++;
+        g_rstats.ctas += ctas;
+        g_rstats.groups += ra.count;
+        g_rstats.probs += ra.nprob;
+        for (int g = 0; g < ra.count; ++g) g_rstats.target_el += (long long)ra.g[g].ext_r * ra.g[g].ext_c * ra.g[g].batch;
+        for (int q = 0; q < ra.nprob; ++q) g_rstats.partial_el += (long long)ra.p[q].M * ra.p[q].N;
+        int h = 0;
+        for (long long c = ctas; c >= 8 && h < 5; c >>= 3) ++h;
+        g_rstats.hist[h]++;
+        static const bool big = getenv("RSC_GEMM_STATS") != nullptr;
+        if (big) {
+            long long te = 0, pe = 0, mrow = 0;
+            for (int g = 0; g < ra.count; ++g) te += (long long)ra.g[g].ext_r * ra.g[g].ext_c * ra.g[g].batch;
+            for (int q = 0; q < ra.nprob; ++q) pe += (long long)ra.p[q].M * ra.p[q].N;
+            for (int g = 0; g < ra.count; ++g) mrow = std::max(mrow, (long long)ra.g[g].np);
+            if (pe > 20000000)
+                fprintf(stderr, "RSC_GEMM_BIG groups %d probs %d maxnp %lld target_el %lld partial_el %lld ctas %lld "
+                        "ext %dx%d TR %d CW %d rtab %d ctab %d\n", ra.count, ra.nprob, mrow, te, pe, ctas,
+                        ra.g[0].ext_r, ra.g[0].ext_c, ra.g[0].TR, ra.g[0].CW, ra.g[0].rtab != nullptr,
+                        ra.g[0].ctab != nullptr);
         }
     }
-    if (ctas <= 0) return 0;
+    static const bool dbg = getenv("RSC_GEMM_DEBUG") != nullptr;
+    if (dbg) {  // diagnostics (syncs; not capturable): target overlap between groups
+        for (int g = 0; g < ra.count; ++g)
+            for (int h = g + 1; h < ra.count; ++h) {
+                const RedGroup &G = ra.g[g], &H = ra.g[h];
+                const char *lo1 = (const char *)G.C, *hi1 = lo1 + 8 * ((long long)(G.ext_r - 1) * G.ldc + G.ext_c);
+                const char *lo2 = (const char *)H.C, *hi2 = lo2 + 8 * ((long long)(H.ext_r - 1) * H.ldc + H.ext_c);
+                if (lo1 < hi2 && lo2 < hi1 && G.sC == 0 && H.sC == 0)
+                    fprintf(stderr, "RSC_GEMM_DEBUG: groups %d/%d overlap\n", g, h);
+            }
+    }
+    if (tab_used > 0) {
+        cudaMemsetAsync(tab, 0xff, (size_t)tab_used, s);  // every table entry = -1
+        reduce_tables_kernel<<<ra.nprob, RT, 0, s>>>(ra);
+        RSC_CHECK_LAUNCH();
+    }
     ordered_reduce_kernel<<<(unsigned)ctas, RT, 0, s>>>(ra);
     RSC_CHECK_LAUNCH();
     return 0;
@@ -535,6 +644,8 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
     static thread_local GemmArgs args;  // ~30 KB; copied into the launch parameter block
     static thread_local std::vector<rsc_gemm_problem> reds;
     static thread_local std::vector<const double *> parts;
+    static thread_local std::vector<int> argi, direct;
+    static thread_local RedArgs ra;
     static const bool atomic_diag = getenv("RSC_GEMM_ATOMIC") != nullptr;  // A/B diagnostics only
     WsEntry ws{nullptr, nullptr, 0};
     bool ws_looked = false;
@@ -543,7 +654,9 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
         args.count = 0;
         reds.clear();
         parts.clear();
+        argi.clear();
         long long tiles = 0, used = 0;
+        long long max_ext = 0;  // largest target extent (rows + cols) of the chunk's accumulating problems
         bool gather = false;
         while (i < count && args.count < MAXP) {
             const rsc_gemm_problem &p = problems[i];
@@ -554,12 +667,17 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
             if (p.atomic && !atomic_diag) {
                 if (!ws_looked) { ws = lookup_ws(stream); ws_looked = true; }
                 const long long need = (((long long)p.M * p.N * p.batch * 8) + 255) / 256 * 256;
-                if (!ws.ptr || need > ws.bytes) return -6;
-                if (used + need > ws.bytes) break;  // close the chunk; the rest follows in order
+                const long long ext = (long long)(p.ext_r > 0 ? p.ext_r : p.M) + (p.ext_c > 0 ? p.ext_c : p.N);
+                // tables of the chunk: sum_g (ext_r + ext_c) np_g <= max ext x problems
+                const long long tab2 = (4LL * std::max(max_ext, ext) + 512) * (long long)(reds.size() + 1);
+                if (!ws.ptr || need + 4 * ext + 512 > ws.bytes) return -6;
+                if (used + need + tab2 > ws.bytes) break;  // close the chunk; the rest follows in order
+                max_ext = std::max(max_ext, ext);
                 double *part = (double *)(ws.ptr + used);
                 used += need;
                 reds.push_back(p);
                 parts.push_back(part);
+                argi.push_back(args.count);
                 q.C = part;
                 q.ldc = p.N;
                 q.strideC = (long long)p.M * p.N;
@@ -578,7 +696,21 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
         }
         if (args.count == 0) continue;
         args.tile_begin[args.count] = tiles;
-        int rc;
+        long long rctas = 0, tab_used = 0;
+        int rc = 0;
+        if (!reds.empty()) {
+            rc = plan_reduce(reds, parts, ws.ptr + used, ws.bytes - used, ra, direct, rctas, tab_used);
+            if (rc) return rc;
+            g_rstats.direct += (long long)direct.size();
+            for (int k : direct) {  // sole unmapped writer of its target: accumulate in place
+                rsc_gemm_problem &q = args.p[argi[k]];
+                const rsc_gemm_problem &p = reds[k];
+                q.C = p.C;
+                q.ldc = p.ldc;
+                q.strideC = p.strideC;
+                q.beta = 1.0;
+            }
+        }
         // the gathered-B loader is its own instantiation: its index prefetch costs the
         // plain kernels ~2.5% (registers), it is only used for launches that gather
         if (!transA && !transB) rc = gather ? launch_chunk<false, false, true>(args, tiles, s)
@@ -588,7 +720,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
                                                 : launch_chunk<true, false, false>(args, tiles, s);
         else rc = launch_chunk<true, true, false>(args, tiles, s);
         if (rc) return rc;
-        if (!reds.empty() && (rc = launch_reduce(reds, parts, s))) return rc;
+        if (!reds.empty() && (rc = launch_reduce(ra, rctas, ws.ptr + used, tab_used, s))) return rc;
     }
     return 0;
 }

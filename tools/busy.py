@@ -27,5 +27,5 @@ for e in ev:
     k = e.name.replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0][:60]
     byname[k] = byname.get(k, 0.0) + e.device_time / 1e3
 print(f"wall {wall:.3f}s  kernel-sum {busy:.3f}s  ({100 * busy / wall:.0f}% busy)  kernels {len(ev)}")
-for k, v in sorted(byname.items(), key=lambda x: -x[1])[:12]:
+for k, v in sorted(byname.items(), key=lambda x: -x[1])[:20]:
     print(f"  {v:9.1f} ms  {k}")
