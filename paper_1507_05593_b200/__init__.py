@@ -41,6 +41,16 @@ def __getattr__(name):
         "FactorStats": "factor", "block_rank": "factor",
         "pcg_solve": "pcg", "SolveReport": "pcg", "jacobi_preconditioner": "pcg",
         "apply_preconditioner": "pcg",
+        # algorithm-level API of rschol/__init__.py:34-58, on the device factor
+        "collect_sources": "alg", "factor_supernode": "alg", "off_diagonal_multiply": "alg",
+        "off_diagonal_multiply_trans": "alg", "approximate_off_diagonal": "alg", "diagonal_solve": "alg",
+        "diagonal_multiply": "alg", "factor_diagonal": "alg", "approximate_diagonal_block": "alg",
+        "factor_interior_block": "alg", "build_diag_tree": "alg",
+        # reference-shaped factor containers (views over the device blocks)
+        "LowRankBlock": "views", "SupernodeFactor": "views", "InteriorBlock": "views",
+        "DiagBlockTree": "views", "UpdateSource": "views",
+        "read_matrix_market": "mmio", "write_matrix_market": "mmio", "read_coordinates": "mmio",
+        "write_coordinates": "mmio", "compare_solvers": "mmio",
     }
     if name in lazy:
         mod = importlib.import_module(f".{lazy[name]}", __name__)

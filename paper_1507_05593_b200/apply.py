@@ -62,7 +62,7 @@ class DeviceApply:
         # no strong reference back to the factor (it owns this program): a cycle would
         # keep the factor's device arena alive until the cyclic GC runs
         self.n = F.n
-        self.nunits = len(F.units)
+        self.nunits = len(F.dunits)
         plan = F.plan
         self.fwd = E.to_dev(np.asarray(F.perm.forward, dtype=np.int32))
         self.inv = E.to_dev(np.asarray(F.perm.inverse, dtype=np.int32))
@@ -70,7 +70,7 @@ class DeviceApply:
         self.y2 = E.empty(self.n, 1)
         self.zbuf = E.empty(self.n)
         self.r_in = E.empty(self.n)
-        units = F.units
+        units = F.dunits
         self._build_inverses(units)
         # every low-rank block is used once per sweep: 2 * sum(k) intermediates
         ksum = 0
@@ -146,14 +146,14 @@ class DeviceApply:
         arrays and re-capture the graph instead of rebuilding the program (0.2-0.4 s
         on config[4]).  False if the blocks do not match (caller rebuilds)."""
         ks = {}
-        for u in F.units:
+        for u in F.dunits:
             if isinstance(u.off, DevLR):
                 ks[u.off.U.data_ptr()] = u.off.k
             if isinstance(u.diag, DeviceTree):
                 for b in u.diag.blocks.values():
                     if isinstance(b, DevLR):
                         ks[b.U.data_ptr()] = b.k
-        if set(ks) != {key for _, _, key in self._lr_index} or len(F.units) != self.nunits:
+        if set(ks) != {key for _, _, key in self._lr_index} or len(F.dunits) != self.nunits:
             return False
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]

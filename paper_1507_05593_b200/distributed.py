@@ -243,7 +243,9 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
     from .sparse import as_spd
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    A = as_spd(A)
+    from .factor import _normalize
+
+    A = _normalize(as_spd(A))
     if prepared is None:
         prepared = prepare(A, config if config is not None else SolverConfig(), coords)
         sym, plan, config, t0, t_plan0, t2 = prepared

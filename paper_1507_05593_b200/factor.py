@@ -381,10 +381,63 @@ class RankStructuredFactor:
         self.perm = sym.perm
         self.partition = sym.partition
         self.config = config
-        self.units = []
+        self.dunits = []
         self.ranks = {}
         self.stats = FactorStats(n=n, seed=config.seed)
         self._apply = None
+
+    # -- reference object model (factor.py:163-172): lazy host views ------------
+    def _build_views(self):
+        from .views import DiagBlockTree, InteriorBlock, LowRankBlock, SupernodeFactor
+
+        part = self.partition
+        nodes = [None] * part.count
+        interior, units = [], []
+        for un in self.dunits:
+            if un.kind == "interior":
+                blk = InteriorBlock(len(interior), un, part, self.sym.B)
+                interior.append(blk)
+                for m in blk.members:
+                    nodes[m.j] = m
+                units.append(("interior", blk))
+                continue
+            if isinstance(un.diag, DeviceTree):
+                diag = DiagBlockTree(un.diag.shape, un.diag)
+            else:
+                diag = (lambda t=un.diag: np.tril(t.L.cpu().numpy()))
+            if un.off is None:
+                off = None
+            elif isinstance(un.off, DevLR):
+                off = LowRankBlock(un.off)
+            else:
+                off = (lambda t=un.off: t.cpu().numpy())
+            nd = SupernodeFactor(un.j, un.c0, un.c1, un.rows, diag, off)
+            nd._dev = un
+            nodes[un.j] = nd
+            units.append(("node", nd))
+        self._views = (nodes, interior, units)
+
+    @property
+    def nodes(self):
+        """One SupernodeFactor per supernode (reference factor.py:168)."""
+        if getattr(self, "_views", None) is None:
+            self._build_views()
+        return self._views[0]
+
+    @property
+    def interior(self):
+        """The interior blocks, in sweep order (reference factor.py:169)."""
+        if getattr(self, "_views", None) is None:
+            self._build_views()
+        return self._views[1]
+
+    @property
+    def units(self):
+        """("interior", InteriorBlock) / ("node", SupernodeFactor) in sweep order
+        (reference factor.py:170, 559-639)."""
+        if getattr(self, "_views", None) is None:
+            self._build_views()
+        return self._views[2]
 
     # -- application -----------------------------------------------------------
     def apply(self, r):
@@ -414,7 +467,7 @@ class RankStructuredFactor:
     # -- inspection ------------------------------------------------------------
     def stored_scalars(self):
         total = 0
-        for un in self.units:
+        for un in self.dunits:
             if un.kind == "interior":
                 total += un._stored
                 continue
@@ -461,7 +514,7 @@ class RankStructuredFactor:
     def dense_lower(self):
         """Explicit lower-triangular factor (small problems, testing)."""
         L = np.zeros((self.n, self.n))
-        for un in self.units:
+        for un in self.dunits:
             L[un.c0:un.c1, un.c0:un.c1] = self._diag_dense(un)
             if un.rows.size and un.off is not None:
                 L[un.rows, un.c0:un.c1] = self._off_dense(un)
@@ -471,7 +524,7 @@ class RankStructuredFactor:
         import scipy.sparse as sp
 
         rows, cols, vals = [], [], []
-        for un in self.units:
+        for un in self.dunits:
             cr = np.arange(un.c0, un.c1)
             for blk, rr in ((self._diag_dense(un), cr),
                             (self._off_dense(un) if (un.rows.size and un.off is not None) else None, un.rows)):
@@ -527,12 +580,36 @@ def _numeric_pass(plan, config, alpha_d, use_graph):
     return ps, None
 
 
+def _normalize(A):
+    """Stored explicit zeros are dropped before ordering and symbolic analysis.  The
+    reference orders on the zero-free graph (ordering.py:113-119) but builds the
+    elimination tree and row structures from the stored pattern (symbolic.py:52,296),
+    so interior-block update sources land in buckets no supernode drains
+    (factor.py:547-554) and the factor silently loses Schur terms (SURVEY Appendix
+    A.1).  Dropping them makes both agree; the operator is unchanged."""
+    if getattr(A, "_zero_free", False):
+        return A
+    nz = int(np.count_nonzero(A.values == 0.0))
+    if not nz:
+        try:
+            A._zero_free = True  # immutable matrix (sparse.py:47-48): checked once
+        except AttributeError:
+            pass
+    if nz:
+        from .sparse import strip_explicit_zeros
+
+        warnings.warn(f"factorize: dropped {nz} stored zeros before the symbolic analysis "
+                      "(SURVEY Appendix A.1)", RuntimeWarning, stacklevel=3)
+        A = strip_explicit_zeros(A)
+    return A
+
+
 def prepare(A, config=None, coords=None):
     """Host half of factorize: ordering + symbolic + device plan upload.  The
     result can be reused by factorize(..., prepared=...) for repeated numeric
     factorizations of matrices with the same pattern (quasi-static load steps)."""
     E.require_cuda()
-    A = as_spd(A)
+    A = _normalize(as_spd(A))
     config = config if config is not None else SolverConfig()
     t0 = time.perf_counter()
     sym = analyze(A, config.tau_o, config.tau_d, config.interior_blocks, coords=coords)
@@ -549,7 +626,7 @@ def factorize(A, config=None, coords=None, prepared=None):
     sweep on the device, restart with alpha_d *= alpha_d_growth on an indefinite
     pivot once a diagonal tree is in play, TooManyRestarts after max_restarts.
     """
-    A = as_spd(A)
+    A = _normalize(as_spd(A))
     reuse = prepared is not None
     if prepared is None:
         prepared = prepare(A, config, coords)
@@ -586,7 +663,7 @@ def factorize(A, config=None, coords=None, prepared=None):
             history.append(alpha_d)
     t3 = time.perf_counter()
     F = RankStructuredFactor(A.n, sym, plan, config)
-    F.units = ps.units
+    F.dunits = ps.units
     F._mem = ps.P  # the factor owns its arena: chunks return to the pool only when F dies
     F.ranks = ps.ranks
     if entry is not None:

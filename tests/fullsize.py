@@ -57,7 +57,7 @@ def lower_mul(F, X, transpose=False):
         else:
             Y.index_add_(0, rr, block @ X[c0:c1])
 
-    for un in F.units:
+    for un in F.dunits:
         c0, c1 = un.c0, un.c1
         if isinstance(un.diag, DeviceTree):
             shape = un.diag.shape
@@ -117,7 +117,7 @@ def factor_digest(F):
         acc = acc + ((x ^ (x >> 31)) * w).sum()
         k += 1
 
-    for un in F.units:
+    for un in F.dunits:
         blocks = []
         if isinstance(un.diag, DeviceTree):
             for s in sorted(un.diag.blocks):

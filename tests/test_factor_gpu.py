@@ -267,3 +267,23 @@ def test_prepared_plan_rejects_other_pattern(cuda):
     assert B.nnz_lower == A.nnz_lower
     with pytest.raises(ValueError):
         factorize(B, prepared=prep)
+
+
+def test_stored_zeros_are_dropped(cuda):
+    """factorize drops stored zeros (with a
+    warning) so interior-block sources are never lost; the result equals the
+    factorization of the zero-stripped matrix."""
+    from paper_1507_05593_b200 import factorize
+    from paper_1507_05593_b200.factor import SolverConfig
+    from paper_1507_05593_b200.problems import elasticity_3d
+
+    A0, coords = elasticity_3d(7)
+    assert (A0.values == 0).any()
+    A1, _ = elasticity_3d(7, strip_zeros=True)
+    conf = SolverConfig(tau_o=32, oversample=10, tau_d=64)
+    with pytest.warns(RuntimeWarning, match="stored zeros"):
+        F0 = factorize(A0, conf, coords=coords)
+    F1 = factorize(A1, conf, coords=coords)
+    assert F0.ranks == F1.ranks and F0.stored_scalars() == F1.stored_scalars()
+    r = np.random.default_rng(2).standard_normal(A0.n)
+    assert np.array_equal(F0.apply(r), F1.apply(r)) or relerr(F0.apply(r), F1.apply(r)) < 1e-13
