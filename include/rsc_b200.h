@@ -184,6 +184,17 @@ int rsc_gemv_describe(int count, const double *const *M, const int *rows, const 
                       const double *alphas, void *desc, long long *blocks);
 int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long long total_blocks, void *stream);
 
+/* Subtree tasks of the preconditioner apply (factor.py:187-218): CTA t runs the
+ * GEMV ops [task_ptr_dev[t], task_ptr_dev[t+1]) of descriptor array `ops` (from
+ * rsc_gemv_describe over all tasks' ops followed by one empty sentinel op) in order,
+ * a CTA barrier between ops.  One task = one nested-dissection subtree's interior
+ * blocks and small separators (their update sources never leave the subtree);
+ * mode bit 4 marks ops whose target rows the task owns (plain accumulate), other
+ * accumulating ops use FP64 atomics.  Replaces the per-level launches of the
+ * small units: one launch per sweep. */
+int rsc_apply_tasks(const void *ops, const int *task_ptr_dev, int ntasks, void *stream);
+
+
 
 /* y = A x for the full symmetric CSR (pcg.py:105,116; sparse.py:86-97). */
 int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,

@@ -47,6 +47,7 @@ EXPORTED = (
     "rsc_gemv_desc_bytes",
     "rsc_gemv_describe",
     "rsc_gemv_multi_dev",
+    "rsc_apply_tasks",
     "rsc_identity_batched",
     "rsc_transpose_batched",
     "rsc_gather_rows",
@@ -101,6 +102,7 @@ _SIGS = {
     "rsc_gemv_desc_bytes": (I, []),
     "rsc_gemv_describe": (I, [I, P, P, P, P, P, P, P, P, P, P, P, P]),
     "rsc_gemv_multi_dev": (I, [P, P, LL, P]),
+    "rsc_apply_tasks": (I, [P, P, I, P]),
 
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_identity_batched": (I, [I, P, P, P, P]),

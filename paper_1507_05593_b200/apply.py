@@ -23,6 +23,8 @@ one buffer zeroed once per apply.  Descriptors are static after factorization an
 built once; after a few eager applies the whole sweep is replayed from a CUDA graph.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -82,25 +84,102 @@ class DeviceApply:
         self.tall = E.empty(max(2 * ksum, 1))
         self._toff = 0
         uidx = {un.u: i for i, un in enumerate(units)}
+        task_of = self._subtree_tasks(units, plan)
         level = [0] * len(units)
         for i, un in enumerate(units):
-            if un.kind == "node":
+            if un.kind == "node" and task_of[i] < 0:
                 lv = 0
                 for p in plan.targets[un.j]:
                     su = uidx[plan.sources[p.s].unit]
-                    lv = max(lv, level[su] + 1)
+                    if task_of[su] < 0:  # sources inside subtree tasks are done before the phases
+                        lv = max(lv, level[su] + 1)
                 level[i] = lv
-        nlev = max(level) + 1 if units else 0
-        groups = [[units[i] for i in range(len(units)) if level[i] == lv] for lv in range(nlev)]
+        top = [i for i in range(len(units)) if task_of[i] < 0]
+        nlev = max((level[i] for i in top), default=-1) + 1
+        groups = [[units[i] for i in top if level[i] == lv] for lv in range(nlev)]
         self.phases = []
         yb, y2b = self.y.data_ptr(), self.y2.data_ptr()
+        self.tasks = {False: self._task_ops(units, task_of, plan, yb, y2b, False),
+                      True: self._task_ops(units, task_of, plan, y2b, yb, True)}
+        self.n_fwd = 0
         for us in groups:
             self._level(us, plan, yb, y2b, backward=False)
+        self.n_fwd = len(self.phases)
         for us in reversed(groups):
             self._level(us, plan, y2b, yb, backward=True)
         self._pack()
         self.graph = None
         self.calls = 0
+
+    # -- subtree tasks -------------------------------------------------------------
+    TASK_BYTES = int(float(os.environ.get("RSC_APPLY_TASK_MB", "2")) * (1 << 20))
+
+    def _subtree_tasks(self, units, plan):
+        """Unit forest (parent = the unit holding the first row of a unit's row
+        structure, i.e. its first update target) and the maximal subtrees of at most
+        TASK_BYTES factor bytes: task_of[i] = index of the task's root unit, or -1
+        for the top units that run as level phases."""
+        part = plan.sym.partition
+        owner = np.full(part.count, -1, dtype=np.int64)
+        for i, un in enumerate(units):
+            if un.kind == "node":
+                owner[un.j] = i
+            else:
+                owner[np.asarray(un.members)] = i
+        nb = np.zeros(len(units))
+        parent = np.full(len(units), -1, dtype=np.int64)
+        for i, un in enumerate(units):
+            nc = un.ncols
+            b = nc * (nc + 1) / 2.0
+            if isinstance(un.off, DevLR):
+                b += (un.rows.size + nc) * un.off.k
+            elif un.off is not None:
+                b += un.off.numel()
+            if isinstance(un.diag, DeviceTree):
+                b = 1e30  # diagonal trees stay in the level phases (their waves are wide)
+            nb[i] = 8.0 * b
+            if un.rows.size:
+                parent[i] = owner[part.supernode_of(int(un.rows[0]))]
+        sub = nb.copy()
+        for i in range(len(units)):  # units are in post-order: children first
+            if parent[i] >= 0:
+                sub[parent[i]] += sub[i]
+        small = sub <= self.TASK_BYTES
+        task_of = np.full(len(units), -1, dtype=np.int64)
+        for i in range(len(units) - 1, -1, -1):
+            if not small[i]:
+                continue
+            p = parent[i]
+            task_of[i] = task_of[p] if (p >= 0 and small[p]) else i
+        self.n_tasks = int(np.sum(small & ((parent < 0) | ~small[np.maximum(parent, 0)])))
+        return task_of
+
+    def _task_ops(self, units, task_of, plan, rhs, out, backward):
+        """Op lists of every subtree task (forward: units in sweep order; backward:
+        reversed), each op a _Phase item; returns [(task root, _Phase)] largest first."""
+        cols_task = np.full(self.n, -1, dtype=np.int64)
+        for i, un in enumerate(units):
+            if task_of[i] >= 0:
+                cols_task[un.c0:un.c1] = task_of[i]
+        tasks = {}
+        order = range(len(units)) if not backward else range(len(units) - 1, -1, -1)
+        for i in order:
+            t = task_of[i]
+            if t < 0:
+                continue
+            ph = tasks.setdefault(t, _Phase())
+            un = units[i]
+            own = bool(un.rows.size == 0 or np.all(cols_task[un.rows] == t))
+            if not backward:
+                self._solve(ph, un.diag, rhs + 8 * un.c0, out + 8 * un.c0, False)
+                if un.rows.size and un.off is not None:
+                    self._couplings_into(ph, ph, un, plan, rhs, out, False, 16 if own else 0)
+            else:
+                if un.rows.size and un.off is not None:
+                    self._couplings_into(ph, ph, un, plan, rhs, out, True, 16)
+                self._solve(ph, un.diag, rhs + 8 * un.c0, out + 8 * un.c0, True)
+        lst = sorted(tasks.items(), key=lambda kv: -sum(it[1] * it[2] for it in kv[1].items))
+        return lst
 
     def _emit(self, ph):
         if ph.items:
@@ -120,6 +199,34 @@ class DeviceApply:
             self.launches.append((len(ph.items), arrs, [a.ctypes.data for a in arrs]))
         self._fn = lib.rsc_gemv_multi
         self._build_dev()
+        self._build_tasks()
+
+    def _build_tasks(self):
+        """Device descriptors of the subtree tasks of both sweeps (rsc_apply_tasks)."""
+        lib = _lib.load()
+        db = lib.rsc_gemv_desc_bytes()
+        self.task_dev = {}
+        self._task_lr = []  # (direction, op index, U ptr)
+        for bw, lst in self.tasks.items():
+            items, ptr = [], [0]
+            for _, ph in lst:
+                base = len(items)
+                self._task_lr.extend((bw, base + i, key) for i, key in ph.lr)
+                items.extend(ph.items)
+                ptr.append(len(items))
+            if not lst:
+                continue
+            items = items + [(items[0][0], 0, 0, 1, items[0][4], 0, items[0][6], 0, 0, 0.0)]  # sentinel
+            c = list(zip(*items))
+            arrs = [ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3]), ptr_array(c[4]),
+                    ptr_array(c[5]), ptr_array(c[6]), ptr_array(c[7]), int_array(c[8]),
+                    np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))]
+            n = len(items)
+            desc = np.empty(n * db, dtype=np.uint8)
+            blocks = np.empty(n, dtype=np.int64)
+            _lib.check(lib.rsc_gemv_describe(n, *[a.ctypes.data for a in arrs], desc.ctypes.data,
+                                             blocks.ctypes.data), "rsc_gemv_describe")
+            self.task_dev[bw] = (E.to_dev(desc), E.to_dev(np.asarray(ptr, dtype=np.int32)), len(lst), arrs)
 
     DEV_MIN = 225  # phases with more problems than one parameter block (GMAXP = 224)
 
@@ -155,22 +262,40 @@ class DeviceApply:
                         ks[b.U.data_ptr()] = b.k
         if set(ks) != {key for _, _, key in self._lr_index} or len(F.dunits) != self.nunits:
             return False
+        if {key for _, _, key in self._task_lr} - set(ks):
+            return False
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]
         self._build_dev()  # the device descriptors carry the ranks too
+        for bw, lst in self.tasks.items():  # task ops: rebuild with the new ranks
+            for _, ph in lst:
+                for i, key in ph.lr:
+                    it = list(ph.items[i])
+                    it[2] = ks[key]
+                    ph.items[i] = tuple(it)
+        self._build_tasks()
         self.graph = None
         self.calls = min(self.calls, self.GRAPH_AFTER)
         return True
 
     def _run_program(self):
         s = E.stream_handle()
-        dev, fdev = self.dev, _lib.load().rsc_gemv_multi_dev
+        lib = _lib.load()
+        dev, fdev = self.dev, lib.rsc_gemv_multi_dev
+
+        def tasks(bw):
+            t = self.task_dev.get(bw)
+            if t is not None:
+                _lib.check(lib.rsc_apply_tasks(t[0].data_ptr(), t[1].data_ptr(), t[2], s), "rsc_apply_tasks")
+
+        tasks(False)  # forward: the subtrees first, then the top levels
         for li, (n, _, args) in enumerate(self.launches):
             if li in dev:
                 d, b2p, tot = dev[li]
                 _lib.check(fdev(d.data_ptr(), b2p.data_ptr(), tot, s), "rsc_gemv_multi_dev")
             else:
                 _lib.check(self._fn(n, *args, s), "rsc_gemv_multi")
+        tasks(True)  # backward: the top levels first, then the subtrees
 
     # -- program construction ------------------------------------------------------
     def _build_inverses(self, units):
@@ -255,24 +380,31 @@ class DeviceApply:
     def _couplings(self, cpl, plan, rhs, out, backward):
         a, b = _Phase(), _Phase()
         for u in cpl:
-            rows = self._rows_ptr(plan, u)
-            c0 = 8 * u.c0
-            if isinstance(u.off, DevLR):
-                k, t = u.off.k, self._t(_cap(u.off))
-                U, V = u.off.U, u.off.V
-                key = U.data_ptr()
-                if not backward:  # t = U^T w ; y[R] -= V t
-                    a.add(U.data_ptr(), u.ncols, k, E.ld(U), out + c0, 0, t, 0, 1, 1.0, lr=key)
-                    b.add(V.data_ptr(), u.rows.size, k, E.ld(V), t, 0, rhs, rows, 0, -1.0, lr=key)
-                else:  # t = V^T y[R] ; w -= U t
-                    a.add(V.data_ptr(), u.rows.size, k, E.ld(V), out, rows, t, 0, 1, 1.0, lr=key)
-                    b.add(U.data_ptr(), u.ncols, k, E.ld(U), t, 0, rhs + c0, 0, 0, -1.0, lr=key)
-            elif not backward:  # y[R] -= L_O w
-                a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out + c0, 0, rhs, rows, 0, -1.0)
-            else:  # w -= L_O^T y[R]
-                a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out, rows, rhs + c0, 0, 1, -1.0)
+            self._couplings_into(a, b, u, plan, rhs, out, backward, 0)
         self._emit(a)
         self._emit(b)
+
+    def _couplings_into(self, a, b, u, plan, rhs, out, backward, excl):
+        """Coupling update of unit u: items of the first factor into `a`, second into
+        `b` (the same list for a subtree task, whose ops run in order).  `excl` = 16
+        when the target rows belong to the caller alone (plain accumulate)."""
+        rows = self._rows_ptr(plan, u)
+        c0 = 8 * u.c0
+        if isinstance(u.off, DevLR):
+            k, t = u.off.k, self._t(_cap(u.off))
+            U, V = u.off.U, u.off.V
+            key = U.data_ptr()
+            own_t = 16 if a is b else 0  # t is private: exclusive when the ops are ordered
+            if not backward:  # t = U^T w ; y[R] -= V t
+                a.add(U.data_ptr(), u.ncols, k, E.ld(U), out + c0, 0, t, 0, 1 | own_t, 1.0, lr=key)
+                b.add(V.data_ptr(), u.rows.size, k, E.ld(V), t, 0, rhs, rows, 0 | excl, -1.0, lr=key)
+            else:  # t = V^T y[R] ; w -= U t
+                a.add(V.data_ptr(), u.rows.size, k, E.ld(V), out, rows, t, 0, 1 | own_t, 1.0, lr=key)
+                b.add(U.data_ptr(), u.ncols, k, E.ld(U), t, 0, rhs + c0, 0, 0 | excl, -1.0, lr=key)
+        elif not backward:  # y[R] -= L_O w
+            a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out + c0, 0, rhs, rows, 0 | excl, -1.0)
+        else:  # w -= L_O^T y[R]
+            a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out, rows, rhs + c0, 0, 1 | excl, -1.0)
 
     def _tree_waves(self, trees, rhs, out, backward, first):
         """Alg. 4 of every tree in `trees`, in lock-step waves; wave w's leaf solves,

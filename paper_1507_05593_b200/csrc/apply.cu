@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(T) trsv_kernel(const __grid_constant__ TrsvArg
 //
 // mode bit 0: transpose; bit 1: M is lower triangular (read c <= r only);
 // bit 2: assign instead of atomic accumulate (transpose 0 only: one segment owns a
-// row); bit 3: M is upper triangular (transpose 0 only: read c >= r only).
+// row); bit 3: M is upper triangular (transpose 0 only: read c >= r only); bit 4:
+// plain read-modify-write accumulate (the CTA is the only writer: subtree tasks).
 //
 // transpose 0: a row is owned by a segment of `lpr` lanes (8 / 16 / 32 by width), so
 //   narrow panels (the low-rank factors, k ~ 20-60 columns) still keep every lane
@@ -183,6 +184,7 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
         if (r < rows && sub == 0) {
             double *dst = y + (yi ? __ldg(yi + r) : r);
             if (assign) *dst = alpha * s;
+            else if (mode & 16) *dst += alpha * s;  // exclusive owner (subtree task)
             else atomicAdd(dst, alpha * s);
         }
     } else {
@@ -214,7 +216,9 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
         if (sub == 0 && c < cols) {
             double s = part[t];
             for (int q = 1; q < nsub; ++q) s += part[t + q * cw];
-            atomicAdd(y + (yi ? __ldg(yi + c) : c), alpha * s);
+            double *dst = y + (yi ? __ldg(yi + c) : c);
+            if (mode & 16) *dst += alpha * s;  // exclusive owner (subtree task)
+            else atomicAdd(dst, alpha * s);
         }
     }
 }
@@ -254,6 +258,30 @@ __global__ void __launch_bounds__(T) gemv_dev_kernel(const GemvProb *__restrict_
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(d, blk - d.blk_begin, xr, part);
+}
+
+// Subtree tasks: one CTA runs the whole op list of one nested-dissection subtree
+// (its interior blocks and small separators, bottom-up for the forward sweep,
+// top-down for the backward one).  A unit's update sources all lie in its own
+// subtree, so a task depends on nothing outside it; inside, the ops run in order
+// with a CTA barrier between them (the CTA owns every row of its subtree, bit 4),
+// and only couplings into ancestor rows outside the subtree use FP64 atomics.
+// This replaces the ~800 latency-bound level phases of the small units with one
+// launch per sweep.  Op descriptors come from rsc_gemv_describe over all tasks'
+// ops plus one empty sentinel (block counts = successive blk_begin differences).
+__global__ void __launch_bounds__(T) apply_tasks_kernel(const GemvProb *__restrict__ ops,
+                                                         const int *__restrict__ task_ptr) {
+    __shared__ double xr[SLAB];
+    __shared__ double part[T];
+    const int o0 = __ldg(task_ptr + blockIdx.x), o1 = __ldg(task_ptr + blockIdx.x + 1);
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    for (int o = o0; o < o1; ++o) {
+        const GemvProb d = ops[o];
+        const long long nb = ops[o + 1].blk_begin - d.blk_begin;  // ops end with a sentinel
+        for (long long lb = 0; lb < nb; ++lb) gemv_block(d, lb, xr, part);
+        __syncthreads();  // the next op reads this op's results
+    }
 }
 
 inline int pow2ceil(int v) {
@@ -391,6 +419,26 @@ extern "C" int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long lo
     cfg.attrs = at;
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_dev_kernel, static_cast<const GemvProb *>(desc), blk2prob);
+    rsc_count_launch();
+    return e == cudaSuccess ? 0 : (int)e;
+}
+
+extern "C" int rsc_apply_tasks(const void *ops, const int *task_ptr_dev, int ntasks, void *stream) {
+    if (ntasks < 0) return -3;
+    if (ntasks == 0) return 0;
+    if (!ops || !task_ptr_dev) return -1;
+    static const bool no_pdl = getenv("RSC_APPLY_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.gridDim = dim3((unsigned)ntasks);
+    cfg.blockDim = dim3(T);
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, apply_tasks_kernel, static_cast<const GemvProb *>(ops),
+                                             task_ptr_dev);
     rsc_count_launch();
     return e == cudaSuccess ? 0 : (int)e;
 }
