@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <vector>
 
+#include "host_par.h"
+
 extern "C" {
 
 // parent[j] = min{ i > j : L(i,j) != 0 } or -1 (Liu's algorithm with path
@@ -219,64 +221,142 @@ extern "C" long long rsc_sym_full_csr(long long n, const long long *col_ptr, con
                                       long long *indices, double *data) {
     if (n < 0 || !col_ptr || !row_idx || !indptr || !indices) return -1;
     if (adjacency && !values) return -2;
-    std::vector<long long> cnt(n + 1, 0);
-    for (long long j = 0; j < n; ++j)
-        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
-            const long long i = row_idx[p];
-            if ((values && values[p] == 0.0) || (adjacency && i == j)) continue;
-            cnt[i + 1]++;
-            if (i != j) cnt[j + 1]++;
-        }
-    for (long long i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-    std::copy(cnt.begin(), cnt.end(), indptr);
-    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
-    for (long long j = 0; j < n; ++j)
-        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
-            const long long i = row_idx[p];
-            if ((values && values[p] == 0.0) || (adjacency && i == j)) continue;
-            const long long q = pos[i]++;
-            indices[q] = j;
-            if (data) data[q] = values[p];
-            if (i != j) {
-                const long long q2 = pos[j]++;
-                indices[q2] = i;
-                if (data) data[q2] = values[p];
+    // Row r of the full matrix = [j < r : (r, j) stored in column j] ascending j
+    //                           ++ [i >= r : (i, r) stored in column r] ascending i.
+    // The first part is a transpose of the strict lower triangle, done in parallel
+    // over column chunks with per-chunk row counts (chunk t's entries of row r go
+    // after chunks < t, columns ascending inside a chunk: rows come out sorted and
+    // the result is independent of the thread count).
+    auto keep = [&](long long p, long long i, long long j) {
+        return !((values && values[p] == 0.0) || (adjacency && i == j));
+    };
+    const int T = (int)std::min<long long>(rsc_host_threads(), std::max<long long>(1, col_ptr[n] / 200000));
+    const std::vector<long long> cut = rsc_balanced_cuts(n, col_ptr, T);
+    std::vector<std::vector<int>> cnt(T);
+    std::vector<long long> bcnt(n, 0);
+    rsc_parallel_chunks(T, T, [&](int, long long t0, long long t1) {
+        for (long long t = t0; t < t1; ++t) {
+            cnt[t].assign(n, 0);
+            for (long long j = cut[t]; j < cut[t + 1]; ++j) {
+                long long b = 0;
+                for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+                    const long long i = row_idx[p];
+                    if (!keep(p, i, j)) continue;
+                    if (i > j) cnt[t][i]++;
+                    if (i >= j) ++b;
+                }
+                bcnt[j] = b;
             }
         }
-    return cnt[n];
+    });
+    // row sizes and per-chunk offsets
+    indptr[0] = 0;
+    std::vector<long long> acnt(n, 0);
+    rsc_parallel_chunks(n, T, [&](int, long long r0, long long r1) {
+        for (long long r = r0; r < r1; ++r) {
+            long long a = 0;
+            for (int t = 0; t < T; ++t) a += cnt[t][r];
+            acnt[r] = a;
+        }
+    });
+    for (long long r = 0; r < n; ++r) indptr[r + 1] = indptr[r] + acnt[r] + bcnt[r];
+    rsc_parallel_chunks(n, T, [&](int, long long r0, long long r1) {
+        for (long long r = r0; r < r1; ++r) {
+            long long o = indptr[r];
+            for (int t = 0; t < T; ++t) {
+                const int c = cnt[t][r];
+                cnt[t][r] = (int)(o - indptr[r]);  // chunk t's first slot in row r (offset)
+                o += c;
+            }
+        }
+    });
+    rsc_parallel_chunks(T, T, [&](int, long long t0, long long t1) {
+        for (long long t = t0; t < t1; ++t)
+            for (long long j = cut[t]; j < cut[t + 1]; ++j) {
+                long long q2 = indptr[j] + acnt[j];  // this column's own row j: rows i >= j
+                for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+                    const long long i = row_idx[p];
+                    if (!keep(p, i, j)) continue;
+                    if (i > j) {
+                        const long long q = indptr[i] + cnt[t][i]++;
+                        indices[q] = j;
+                        if (data) data[q] = values[p];
+                    }
+                    if (i >= j) {
+                        indices[q2] = i;
+                        if (data) data[q2] = values[p];
+                        ++q2;
+                    }
+                }
+            }
+    });
+    return indptr[n];
 }
 
-// Symmetric permutation in lower storage (sparse.py:_permuted_lower): entry e of A
-// (row row_idx[e], column col(e)) lands at (max, min) of (p[row], p[col]); outputs
-// the new rows / columns sorted by (column, row) and the source position of each.
+// Lower-storage (row, col) of every entry of A under the permutation p, sorted by
+// (col, row), with the source position of each (symmetric permutation,
+// sparse.py:171-189): a counting pass by permuted column, then per-column row sorts
+// in parallel.
 extern "C" int rsc_sym_permute_lower(long long n, const long long *col_ptr, const long long *row_idx,
                                      const long long *p, long long *out_rows, long long *out_cols,
                                      long long *order) {
     if (n < 0 || !col_ptr || !row_idx || !p) return -1;
     const long long nnz = col_ptr[n];
-    std::vector<long long> cnt(n + 1, 0);
-    for (long long j = 0; j < n; ++j)
-        for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
-            const long long a = p[row_idx[e]], b = p[j];
-            cnt[(a < b ? a : b) + 1]++;
+    const int T = (int)std::min<long long>(rsc_host_threads(), std::max<long long>(1, nnz / 200000));
+    const std::vector<long long> src = rsc_balanced_cuts(n, col_ptr, T);  // source-column chunks
+    // per-chunk counts of every permuted column (chunk order = source order, so the
+    // unsorted runs are deterministic; the per-column sort fixes the final order)
+    std::vector<std::vector<int>> cnt(T);
+    rsc_parallel_chunks(T, T, [&](int, long long t0, long long t1) {
+        for (long long t = t0; t < t1; ++t) {
+            cnt[t].assign(n, 0);
+            for (long long j = src[t]; j < src[t + 1]; ++j)
+                for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
+                    const long long a = p[row_idx[e]], b = p[j];
+                    cnt[t][a < b ? a : b]++;
+                }
         }
-    for (long long c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
-    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+    });
+    std::vector<long long> cp(n + 1, 0);
+    rsc_parallel_chunks(n, T, [&](int, long long c0, long long c1) {
+        for (long long c = c0; c < c1; ++c) {
+            long long s = 0;
+            for (int t = 0; t < T; ++t) s += cnt[t][c];
+            cp[c + 1] = s;
+        }
+    });
+    for (long long c = 0; c < n; ++c) cp[c + 1] += cp[c];
+    rsc_parallel_chunks(n, T, [&](int, long long c0, long long c1) {
+        for (long long c = c0; c < c1; ++c) {
+            long long o = cp[c];
+            for (int t = 0; t < T; ++t) {
+                const int k = cnt[t][c];
+                cnt[t][c] = (int)(o - cp[c]);
+                o += k;
+            }
+        }
+    });
     std::vector<std::pair<long long, long long>> tmp(nnz);
-    for (long long j = 0; j < n; ++j)
-        for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
-            const long long a = p[row_idx[e]], b = p[j];
-            const long long c = a < b ? a : b, r = a < b ? b : a;
-            tmp[pos[c]++] = {r, e};
-        }
-    for (long long c = 0; c < n; ++c) {
-        std::sort(tmp.begin() + cnt[c], tmp.begin() + cnt[c + 1]);
-        for (long long q = cnt[c]; q < cnt[c + 1]; ++q) {
-            out_rows[q] = tmp[q].first;
-            out_cols[q] = c;
-            order[q] = tmp[q].second;
-        }
-    }
-    (void)nnz;
+    rsc_parallel_chunks(T, T, [&](int, long long t0, long long t1) {
+        for (long long t = t0; t < t1; ++t)
+            for (long long j = src[t]; j < src[t + 1]; ++j)
+                for (long long e = col_ptr[j]; e < col_ptr[j + 1]; ++e) {
+                    const long long a = p[row_idx[e]], b = p[j];
+                    const long long c = a < b ? a : b, r = a < b ? b : a;
+                    tmp[cp[c] + cnt[t][c]++] = {r, e};
+                }
+    });
+    const std::vector<long long> cut = rsc_balanced_cuts(n, cp.data(), T);
+    rsc_parallel_chunks(T, T, [&](int, long long t0, long long t1) {
+        for (long long t = t0; t < t1; ++t)
+            for (long long c = cut[t]; c < cut[t + 1]; ++c) {
+                std::sort(tmp.begin() + cp[c], tmp.begin() + cp[c + 1]);
+                for (long long q = cp[c]; q < cp[c + 1]; ++q) {
+                    out_rows[q] = tmp[q].first;
+                    out_cols[q] = c;
+                    order[q] = tmp[q].second;
+                }
+            }
+    });
     return 0;
 }

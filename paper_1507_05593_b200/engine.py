@@ -143,14 +143,17 @@ def to_dev(a, dtype=None):
 
 
 def ld(t):
-    """Leading dimension (row stride) of a 2-D row-major tensor view."""
-    if t.dim() != 2:
-        raise ValueError("expected a 2-D tensor")
-    if t.numel() == 0:
-        return max(int(t.shape[1]), 1)
-    if t.shape[1] > 1 and t.stride(1) != 1:
+    """Leading dimension (row stride) of a 2-D row-major tensor view (called for
+    every operand of every launch: one shape and one stride query)."""
+    try:
+        (r, c), (s0, s1) = t.shape, t.stride()
+    except ValueError:
+        raise ValueError("expected a 2-D tensor") from None
+    if r == 0 or c == 0:
+        return c if c > 1 else 1
+    if c > 1 and s1 != 1:
         raise ValueError("tensor must have unit column stride")
-    return max(int(t.stride(0)), int(t.shape[1]), 1)
+    return s0 if s0 > c else (c if c > 1 else 1)
 
 
 # ---------------------------------------------------------------------------
