@@ -60,6 +60,15 @@ def _cap(lr):
 
 
 class DeviceApply:
+    """The apply program of a factor.  For a factor sharded by ND subtree
+    (distributed.factorize_distributed, F.dist set) every rank holds its own subtree
+    units plus the replicated top separators: the program runs the local units'
+    forward sweep, sums the top separators' right-hand sides over the ranks (one
+    all-reduce of the top rows; rank 0 contributes r there, the others only their
+    coupling updates), runs the top units' forward and backward sweeps (identical on
+    every rank), then the local backward sweep.  The result is exact on the rank's
+    own rows and the top rows (pcg combines the ranks' rows)."""
+
     def __init__(self, F):
         # no strong reference back to the factor (it owns this program): a cycle would
         # keep the factor's device arena alive until the cyclic GC runs
@@ -84,29 +93,50 @@ class DeviceApply:
         self.tall = E.empty(max(2 * ksum, 1))
         self._toff = 0
         uidx = {un.u: i for i, un in enumerate(units)}
-        task_of = self._subtree_tasks(units, plan)
-        level = [0] * len(units)
-        for i, un in enumerate(units):
-            if un.kind == "node" and task_of[i] < 0:
-                lv = 0
-                for p in plan.targets[un.j]:
-                    su = uidx[plan.sources[p.s].unit]
-                    if task_of[su] < 0:  # sources inside subtree tasks are done before the phases
-                        lv = max(lv, level[su] + 1)
-                level[i] = lv
-        top = [i for i in range(len(units)) if task_of[i] < 0]
-        nlev = max((level[i] for i in top), default=-1) + 1
-        groups = [[units[i] for i in top if level[i] == lv] for lv in range(nlev)]
+        self.dist = getattr(F, "dist", None)
+        shared = set(self.dist["top_units"]) if self.dist else set()
+        task_of = self._subtree_tasks(units, plan) if not self.dist else np.full(len(units), -1, dtype=np.int64)
+
+        def levels(members):
+            lv = {}
+            for i in members:
+                un = units[i]
+                v = 0
+                if un.kind == "node":
+                    for p in plan.targets[un.j]:
+                        su = uidx.get(plan.sources[p.s].unit)
+                        if su is not None and su in lv:  # sources outside `members` run before
+                            v = max(v, lv[su] + 1)
+                lv[i] = v
+            n = max(lv.values(), default=-1) + 1
+            return [[units[i] for i in members if lv[i] == k] for k in range(n)]
+
+        local = [i for i in range(len(units)) if task_of[i] < 0 and units[i].u not in shared]
+        top = [i for i in range(len(units)) if units[i].u in shared]
+        g_local, g_top = levels(local), levels(top)
         self.phases = []
         yb, y2b = self.y.data_ptr(), self.y2.data_ptr()
         self.tasks = {False: self._task_ops(units, task_of, plan, yb, y2b, False),
                       True: self._task_ops(units, task_of, plan, y2b, yb, True)}
-        self.n_fwd = 0
-        for us in groups:
+        for us in g_local:
+            self._level(us, plan, yb, y2b, backward=False)
+        self.n_local_fwd = len(self.phases)  # the top rows are all-reduced here (sharded factor)
+        for us in g_top:
             self._level(us, plan, yb, y2b, backward=False)
         self.n_fwd = len(self.phases)
-        for us in reversed(groups):
+        for us in reversed(g_top):
             self._level(us, plan, y2b, yb, backward=True)
+        for us in reversed(g_local):
+            self._level(us, plan, y2b, yb, backward=True)
+        if self.dist:
+            cols = np.concatenate([np.arange(units[i].c0, units[i].c1) for i in top]) if top else \
+                np.zeros(0, np.int64)
+            self.top_cols = E.to_dev(cols.astype(np.int32))
+            self.top_buf = E.empty(max(cols.size, 1), 1)
+            own = np.concatenate([np.arange(units[i].c0, units[i].c1) for i in local]) if local else \
+                np.zeros(0, np.int64)
+            # rows (in the permuted order) this rank's result is exact on: its own + the top
+            self.exact_cols = np.concatenate([own, cols]).astype(np.int64)
         self._pack()
         self.graph = None
         self.calls = 0
@@ -290,12 +320,34 @@ class DeviceApply:
 
         tasks(False)  # forward: the subtrees first, then the top levels
         for li, (n, _, args) in enumerate(self.launches):
+            if li == self.n_local_fwd and self.dist:
+                self._reduce_top()
             if li in dev:
                 d, b2p, tot = dev[li]
                 _lib.check(fdev(d.data_ptr(), b2p.data_ptr(), tot, s), "rsc_gemv_multi_dev")
             else:
                 _lib.check(self._fn(n, *args, s), "rsc_gemv_multi")
+        if self.dist and self.n_local_fwd >= len(self.launches):
+            self._reduce_top()
         tasks(True)  # backward: the top levels first, then the subtrees
+
+    def _reduce_top(self):
+        """Sum the top separators' forward right-hand sides over the ranks."""
+        import torch.distributed as dist
+
+        if self.top_cols.numel() == 0:
+            return
+        E.gather_rows(self.top_cols, self.y, self.top_buf)
+        grp = self.dist["group"]
+        if dist.get_backend(grp) == "gloo":
+            h = self.top_buf.cpu()
+            dist.all_reduce(h, group=grp)
+            self.top_buf.copy_(h)
+        else:
+            dist.all_reduce(self.top_buf, group=grp)
+        # y[top] = sum: scatter-add onto zeroed rows
+        self.y[self.top_cols.long()] = 0.0
+        E.scatter_add_rows(self.top_cols, self.top_buf, self.y)
 
     # -- program construction ------------------------------------------------------
     def _build_inverses(self, units):
@@ -450,6 +502,8 @@ class DeviceApply:
         n = self.n
         self.tall.zero_()
         E.gather_rows(self.inv, self.r_in.reshape(n, 1), self.y)
+        if self.dist and self.dist["rank"] != 0 and self.top_cols.numel():
+            self.y[self.top_cols.long()] = 0.0  # rank 0 alone brings r to the top rows' sum
         self._run_program()
         E.gather_rows(self.fwd, self.y, self.zbuf.reshape(n, 1))
 
@@ -460,7 +514,7 @@ class DeviceApply:
     def __call__(self, r_dev, out=None):
         self.r_in.copy_(r_dev.reshape(-1))
         self.calls += 1
-        if self.graph is None and self.calls > self.GRAPH_AFTER:
+        if self.graph is None and self.calls > self.GRAPH_AFTER and not self.dist:
             try:
                 s = torch.cuda.Stream()
                 s.wait_stream(torch.cuda.current_stream())

@@ -222,29 +222,34 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
 
     Every rank runs the (deterministic) host symbolic phase, then
       1. sweeps the units of its own nested-dissection subtrees (unit_ranks) --
-         no communication: a subtree's sources all lie inside it;
-      2. all-gathers the source panels of those units (one broadcast per rank);
-      3. sweeps the shared top separators (replicated on every rank -- every
-         product a top separator forms reads sources from all subtrees);
+         no communication: a subtree's update sources all lie inside it;
+      2. exchanges only the source panels the shared top separators read (one
+         broadcast per rank and dtype; the rest of a subtree never leaves its GPU);
+      3. sweeps the top separators with their source sums split: every sum over
+         update sources (Schur assembly, Alg. 2/5 implicit products, leaf windows)
+         is launched on each rank for the sources it owns, rank 0 adds the A-matrix
+         and root-path terms, and each accumulated block is all-reduced before the
+         step that consumes it; diagonal solves, POTRFs and QRCPs on the summed
+         blocks run replicated (SURVEY §8(e));
       4. agrees on the earliest pivot failure in sweep order (restart protocol of
-         factor.py:702-718, identical on all ranks);
-      5. all-gathers the finished unit blocks, so every rank holds the whole factor
-         and can run the preconditioned solve.
-    Results equal the single-GPU factorization: the same kernels on the same
-    operands (the top separators' source sums are formed in the same order)."""
+         factor.py:702-718, identical on all ranks).
+    The factor stays distributed: each rank keeps its subtrees' blocks and the top
+    separators (F.dist); F.apply and pcg_solve run the distributed solve (local
+    sweeps, one all-reduce of the top rows per application).  The split sums add
+    each rank's partial in a different order than one GPU would, so kept ranks can
+    differ from the single-GPU factor only where a QRCP decision sits within
+    rounding of the cutoff."""
     import time
 
     import torch
     import torch.distributed as dist
 
     from .errors import IndefiniteError, TooManyRestarts
-    from .factor import RankStructuredFactor, SolverConfig, _Indefinite, prepare
+    from .factor import RankStructuredFactor, SolverConfig, _Indefinite, _normalize, prepare
     from .numeric import LevelPass
     from .sparse import as_spd
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    from .factor import _normalize
-
     A = _normalize(as_spd(A))
     if prepared is None:
         prepared = prepare(A, config if config is not None else SolverConfig(), coords)
@@ -256,10 +261,16 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
         plan.load_values(A)
         t2 = time.perf_counter()
     owner = unit_ranks(sym, world)
-    node_unit = {payload: u for u, (kind, payload) in enumerate(sym.units) if kind == "node"}
     device = torch.device("cuda", torch.cuda.current_device())
+    # the update sources any shared top separator reads (their panels are the only
+    # factor data that crosses GPUs)
+    top_src = set()
+    for u, (kind, j) in enumerate(sym.units):
+        if kind == "node" and owner[u] == -1:
+            top_src.update(p.s for p in plan.targets[j])
     alpha_d = config.alpha_d
     history, restarts = [alpha_d], 0
+    sent = 0
     while True:
         ps = LevelPass(plan, config, alpha_d)
         ps._by_unit = {}
@@ -267,16 +278,14 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
         ps.mark_phase()
         counters_a = dict(ps.counters)
         mine = {sid: ps.src_panel[sid] for u, sid in plan.unit_source.items()
-                if owner[u] == rank and sid in ps.src_panel}
+                if owner[u] == rank and sid in ps.src_panel and sid in top_src}
+        sent = sum(int(t.numel()) * 8 for pr in mine.values() for t in {id(x): x for x in pr}.values())
         remote = {}
         for r, got in enumerate(all_gather_blocks(mine, device, group)):
             if r != rank:
                 for sid, (raw, eff) in got.items():
                     ps._set_source(sid, raw, eff)
                     remote[sid] = raw
-        # shared top separators: every rank forms the partial sums over the sources of
-        # its own subtrees (rank 0 also the A-matrix, root-path and top-source terms),
-        # all-reduced before each diagonal solve / POTRF / QRCP, which run replicated
         src_owner = np.array([max(int(owner[src.unit]), 0) for src in plan.sources], dtype=np.int64)
         ps.split = (rank, world, src_owner, group)
         ps._run_units(lambda u: owner[u] == -1)
@@ -302,30 +311,43 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
         alpha_d *= config.alpha_d_growth
         history.append(alpha_d)
     counters_top = {k: ps.counters[k] - counters_a[k] for k in ps.counters}
-    own_units = {u: ps._by_unit[u] for u in range(len(sym.units)) if owner[u] == rank}
+    node_unit = {payload: u for u, (kind, payload) in enumerate(sym.units) if kind == "node"}
     own_ranks = {k: v for k, v in ps.ranks.items() if owner[node_unit[k[1]]] == rank}
-    gathered = all_gather_blocks((own_units, own_ranks, counters_a), device, group)
+    keep = [u for u in range(len(sym.units)) if owner[u] in (rank, -1)]
+    local_stored = 0
+    F = RankStructuredFactor(A.n, sym, plan, config)
+    F.dunits = [ps._by_unit[u] for u in keep]
+    F._mem = ps.P
+    mine_units = [ps._by_unit[u] for u in keep if owner[u] == rank]
+    top_units = [ps._by_unit[u] for u in keep if owner[u] == -1]
+    G = RankStructuredFactor(A.n, sym, plan, config)
+    G.dunits = mine_units
+    local_stored = G.stored_scalars()
+    G.dunits = top_units
+    top_stored = G.stored_scalars()
+    # small per-rank summaries (host objects): kept ranks, counters, stored scalars
+    info = [None] * world
+    dist.all_gather_object(info, (own_ranks, counters_a, local_stored, sent), group=group)
     ranks_all = dict(ps.ranks)
     counters = dict(counters_top)
-    for r, (units_r, ranks_r, cnt_r) in enumerate(gathered):
+    stored = top_stored
+    for r, (ranks_r, cnt_r, st_r, _) in enumerate(info):
         for k in counters:
             counters[k] += cnt_r[k]
+        stored += st_r
         if r != rank:
-            ps._by_unit.update(units_r)
             ranks_all.update(ranks_r)
-    # price the top separators' products with remote panels at the owners' ranks
-    src_key = {sid: ("off", sym.units[u][1]) for u, sid in plan.unit_source.items()
-               if sym.units[u][0] == "node"}
+    src_key = {sid: ("off", sym.units[u][1]) for u, sid in plan.unit_source.items() if sym.units[u][0] == "node"}
     ps.extra_kept = {int(raw.data_ptr()): ranks_all[src_key[sid]] for sid, raw in remote.items()
                      if sid in src_key and src_key[sid] in ranks_all}
     ps._finalize_ranks(ps._last_info)
     flops_a = [0.0] * world
     dist.all_gather_object(flops_a, ps.flops_phase_a, group=group)
     t3 = time.perf_counter()
-    F = RankStructuredFactor(A.n, sym, plan, config)
-    F.units = [ps._by_unit[u] for u in range(len(sym.units))]
-    F._mem = (ps.P, gathered)
     F.ranks = ranks_all
+    F.source_matrix = A
+    F.dist = {"rank": rank, "world": world, "group": group, "top_units": [un.u for un in top_units],
+              "local_units": [un.u for un in mine_units], "exchanged_bytes": [x[3] for x in info]}
     part = sym.partition
     st = F.stats
     st.n, st.nnz_lower = A.n, A.nnz_lower
@@ -335,7 +357,7 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
     st.compressed_offdiag = counters["compressed_off"]
     st.compressed_diag = counters["compressed_diag"]
     st.dense_fallback = counters["dense_fallback"]
-    st.stored_scalars = F.stored_scalars()
+    st.stored_scalars = stored
     st.restarts = restarts
     st.alpha_d_final = alpha_d
     st.alpha_d_history = history

@@ -447,6 +447,12 @@ class RankStructuredFactor:
             raise DimensionMismatch(f"expected vector of length {self.n}")
         y = E.to_dev(r)
         z = self.apply_device(y)
+        if getattr(self, "dist", None):  # sharded factor: assemble z from every rank's rows
+            from .pcg import _DistOps
+
+            if getattr(self, "_dist_ops", None) is None:
+                self._dist_ops = _DistOps(self.source_matrix, self)
+            self._dist_ops.combine(z)
         return z.cpu().numpy()
 
     __call__ = apply
@@ -466,6 +472,8 @@ class RankStructuredFactor:
 
     # -- inspection ------------------------------------------------------------
     def stored_scalars(self):
+        if getattr(self, "dist", None):  # a sharded factor: summed over the ranks at factorization
+            return self.stats.stored_scalars
         total = 0
         for un in self.dunits:
             if un.kind == "interior":

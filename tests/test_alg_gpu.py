@@ -86,7 +86,7 @@ def test_factor_object_model(cuda):
     """.nodes / .interior / .units mirror rschol's containers (factor.py:163-172)."""
     from paper_1507_05593_b200 import DiagBlockTree, InteriorBlock, LowRankBlock, SupernodeFactor
 
-    F, B = _factor(12, tau_d=64)
+    F, B = _factor(16, tau_d=64)
     kinds = [k for k, _ in F.units]
     assert len(F.units) == len(F.sym.units) and set(kinds) <= {"interior", "node"}
     assert all(isinstance(o, InteriorBlock) for k, o in F.units if k == "interior")
@@ -121,7 +121,7 @@ def test_alg_products_against_stored_factor(cuda):
                                        off_diagonal_multiply, off_diagonal_multiply_trans)
     from paper_1507_05593_b200.factor import _block_seed
 
-    F, B = _factor(12, tau_d=64)
+    F, B = _factor(16, tau_d=64)
     comp = [o for k, o in F.units if k == "node" and isinstance(o.offdiag, LowRankBlock)]
     assert comp
     rng = np.random.default_rng(3)
@@ -151,7 +151,7 @@ def test_alg_supernode_and_tree_functions(cuda):
     from paper_1507_05593_b200.factor import _block_seed
     from paper_1507_05593_b200.symbolic import block_rank
 
-    F, B = _factor(12, tau_d=64)
+    F, B = _factor(16, tau_d=64)
     nodes = [o for k, o in F.units if k == "node"]
     dense = [o for o in nodes if not isinstance(o.diag, DiagBlockTree) and not isinstance(o.offdiag, LowRankBlock)]
     for o in dense[:3]:
@@ -190,7 +190,7 @@ def test_factor_interior_block_matches_factor(cuda):
     """interior.py:105-156: the block factor equals the sweep's interior unit."""
     from paper_1507_05593_b200 import factor_interior_block
 
-    F, B = _factor(12, tau_d=64)
+    F, B = _factor(16, tau_d=64)
     blk = F.interior[0]
     ids = [m.j for m in blk.members]
     mine = factor_interior_block(B, F.partition, ids, block_id=0)

@@ -34,13 +34,15 @@ def test_sharded_factorization_matches_single_gpu(cuda, world):
     assert out["world"] == world
     for name, c in out["cases"].items():
         assert c["top_units"] >= 1 and c["owned_units"] >= 1, (name, c)
-        assert c["ranks_equal"] and c["stored_equal"] and c["counters_equal"], (name, c)
-        g1, gd = c["model_gflop"]
-        assert abs(g1 - gd) <= 1e-9 * g1, (name, c)
-        # compressed blocks: the same band as two single-GPU runs (FP64 atomic sums)
-        assert c["apply_relerr"] < max(1e-8, 10 * c["apply_relerr_self"]), (name, c)
-        # PCG stops at relres 1e-6, so x inherits the preconditioner's run-to-run noise
-        # amplified by the solve: the same band rule as the apply (sharded vs single
-        # GPU measured 1.0-1.15e-8 on l3d20 in some runs, below 1e-8 in others)
+        # the factor stays sharded: each rank keeps its subtrees + the top separators
+        assert c["kept_units"] == c["local_units"] + c["top_units"], (name, c)
+        # only the panels the top separators read cross ranks (a fraction of the factor)
+        assert max(c["exchanged_bytes"]) < c["factor_bytes_total"], (name, c)
+        # split source sums are added in a different order than on one GPU: kept
+        # ranks may move only at knife-edge QRCP decisions
+        assert c["rank_mismatches"] <= 2, (name, c)
+        if c["ranks_equal"]:
+            assert c["stored_equal"] and c["counters_equal"], (name, c)
+        assert c["apply_relerr"] < 1e-8, (name, c)
         assert abs(c["pcg_its"][0] - c["pcg_its"][1]) <= 1, (name, c)
-        assert c["x_relerr"] < max(1e-8, 10 * c["x_relerr_self"]), (name, c)
+        assert c["x_relerr"] < 1e-8, (name, c)

@@ -38,10 +38,11 @@ def main():
         x1, r1 = pcg_solve(A, b, preconditioner=F1, tol=1e-6)
         xd, rd = pcg_solve(A, b, preconditioner=Fd, tol=1e-6)
         x2, _ = pcg_solve(A, b, preconditioner=F2, tol=1e-6)
+        mism = sorted(set(F1.ranks.items()) ^ set(Fd.ranks.items()))
         out[name] = {
             "n": A.n,
             "owned_units": int((owners == rank).sum()), "top_units": int((owners == -1).sum()),
-            "ranks_equal": F1.ranks == Fd.ranks,
+            "ranks_equal": F1.ranks == Fd.ranks, "rank_mismatches": len(mism) // 2,
             "stored_equal": F1.stats.stored_scalars == Fd.stats.stored_scalars,
             "counters_equal": (F1.stats.compressed_offdiag, F1.stats.compressed_diag, F1.stats.dense_fallback)
             == (Fd.stats.compressed_offdiag, Fd.stats.compressed_diag, Fd.stats.dense_fallback),
@@ -51,6 +52,9 @@ def main():
             "pcg_its": [r1.iterations, rd.iterations],
             "x_relerr": float(np.linalg.norm(xd - x1) / np.linalg.norm(x1)),
             "x_relerr_self": float(np.linalg.norm(x2 - x1) / np.linalg.norm(x1)),
+            "exchanged_bytes": Fd.dist["exchanged_bytes"],
+            "factor_bytes_total": 8 * F1.stats.stored_scalars,
+            "local_units": len(Fd.dist["local_units"]), "kept_units": len(Fd.dunits),
         }
     if rank == 0:
         print(json.dumps({"world": world, "backend": backend, "cases": out}), flush=True)
