@@ -245,6 +245,11 @@ long long rsc_sym_amalgamate(long long nb, const long long *bounds, const long l
  * and frees the handle. */
 void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
                            const long long *row_idx, long long *total);
+/* The same with nr supernode ranges [ranges[2i], ranges[2i+1]) (disjoint ND
+ * subtrees) swept on host threads first; falls back to the sequential sweep when a
+ * range is not closed under the pass-up.  Identical output. */
+void *rsc_sym_rows_compute_par(long long M, const long long *starts, const long long *col_ptr,
+                               const long long *row_idx, long long nr, const long long *ranges, long long *total);
 int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows);
 /* Full symmetric CSR of a lower-CSC matrix, rows sorted, stored zeros dropped
  * (sparse.py:86-97 _csr_full); adjacency != 0 also drops the diagonal (the ND
@@ -266,6 +271,15 @@ int rsc_sym_permute_lower(long long n, const long long *col_ptr, const long long
 int rsc_nd_split_geometric(long long nv, const long long *verts, int dim, const double *xyz,
                            const long long *indptr, const long long *indices, unsigned char *mark,
                            long long *out, long long *counts);
+/* Whole geometric nested dissection (ordering.py:277-368, replaces the Python
+ * recursion over rsc_nd_split_geometric): subtrees run on host threads.
+ * order[pos] <- vertex; separator-tree nodes in the arrays of capacity cap
+ * (lo, hi, subtree_lo, level, left, right; -1 children = leaf), *root <- root id.
+ * Returns the node count, -1 bad arguments, -3 capacity too small. */
+long long rsc_nd_geometric(long long n, int dim, const double *xyz, const long long *indptr,
+                           const long long *indices, long long leaf, long long *order, long long cap,
+                           long long *n_lo, long long *n_hi, long long *n_sub, long long *n_lev,
+                           long long *n_left, long long *n_right, long long *root);
 /* Batched window cut of a CSR matrix (n rows, ascending column indices) whose
  * values are 1-based positions: request q = rows sel[r_off[q]..+r_n[q]) (or the
  * range [r_lo[q], +r_n[q]) when r_off[q] < 0) x columns likewise (ascending
@@ -278,6 +292,32 @@ int rsc_csr_windows(long long nq, long long n, const long long *indptr, const lo
                     const long long *c_n, const long long *c_lo, long long *nnz,
                     const long long *rp_off, const long long *nz_off, int *rowptr, int *colidx,
                     int *val);
+
+/* ---- Plan compiler (plan.py NumericPlan; host threads) --------------------------
+ * rsc_plan_pairs: every (target supernode j, update source s) pair with a row of s
+ * inside C_j (is_target[j] != 0), grouped by target, sources by src_order within a
+ * target (the bucket order of factor.py:545-554,572); lo/hi = the run of s's rows
+ * in C_j; an int32 index chunk with cpos = rows[lo:hi] - c0 and
+ * rpos = searchsorted(R_j, rows[hi:]) per pair (factor.py:389-398, 450-455).
+ * Returns a handle; rsc_plan_pairs_fetch copies tgt, src, lo, hi, cpos offset,
+ * rpos offset (npairs each) and the chunk (nidx ints), then frees it.
+ * rsc_plan_tree_maps: the window maps of diagonal-tree blocks (diagblocks.py:
+ * 231-262) for blocks with global spans (row lo, row hi, col lo, col hi) and the
+ * pairs of each tree; rsc_plan_tree_maps_fetch writes 9 arrays (tree, block, src,
+ * clo, chi, rlo, rhi, cidx offset, ridx offset) grouped by (tree, block), and the
+ * chunk. */
+void *rsc_plan_pairs(long long nsrc, const long long *src_ptr, const long long *src_rows,
+                     const long long *src_order, long long M, const long long *starts,
+                     const unsigned char *is_target, const long long *R_ptr, const long long *R_rows,
+                     long long *npairs, long long *nidx);
+int rsc_plan_pairs_fetch(void *h, long long *tgt, long long *src, long long *lo, long long *hi, long long *cpos,
+                         long long *rpos, int *idx);
+void *rsc_plan_tree_maps(long long ntree, const long long *blk_ptr, const long long *spans,
+                         const long long *pair_ptr, const long long *pair_src, const long long *src_ptr,
+                         const long long *src_rows, long long *nmaps, long long *nidx);
+int rsc_plan_tree_maps_fetch(void *h, long long *const *out, int *idx);
+/* 64-bit digest of a byte buffer (the pattern key load_values compares). */
+unsigned long long rsc_hash64(const void *data, long long nbytes);
 
 /* ---- Gaussian sketches (replaces the host draw at reference kernels.py:85-92,
  * np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r)), seeded per

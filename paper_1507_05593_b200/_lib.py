@@ -60,11 +60,18 @@ EXPORTED = (
     "rsc_sym_colcounts",
     "rsc_sym_amalgamate",
     "rsc_sym_rows_compute",
+    "rsc_sym_rows_compute_par",
     "rsc_sym_rows_fetch",
     "rsc_sym_full_csr",
     "rsc_sym_permute_lower",
     "rsc_nd_split_geometric",
+    "rsc_nd_geometric",
     "rsc_csr_windows",
+    "rsc_plan_pairs",
+    "rsc_hash64",
+    "rsc_plan_pairs_fetch",
+    "rsc_plan_tree_maps",
+    "rsc_plan_tree_maps_fetch",
     "rsc_pcg64_block_states",
     "rsc_pcg64_seed_states",
     "rsc_normal_workspace_bytes",
@@ -116,11 +123,18 @@ _SIGS = {
     "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
     "rsc_sym_amalgamate": (LL, [LL, P, P, P, I, P, P, P]),
     "rsc_sym_rows_compute": (ctypes.c_void_p, [LL, P, P, P, P]),
+    "rsc_sym_rows_compute_par": (ctypes.c_void_p, [LL, P, P, P, LL, P, P]),
     "rsc_sym_rows_fetch": (I, [ctypes.c_void_p, P, P]),
     "rsc_sym_full_csr": (LL, [LL, P, P, P, I, P, P, P]),
     "rsc_sym_permute_lower": (I, [LL, P, P, P, P, P, P]),
     "rsc_nd_split_geometric": (I, [LL, P, ctypes.c_int, P, P, P, P, P, P]),
+    "rsc_nd_geometric": (LL, [LL, ctypes.c_int, P, P, P, LL, P, LL, P, P, P, P, P, P, P]),
     "rsc_csr_windows": (I, [LL, LL] + [P] * 16),
+    "rsc_hash64": (ctypes.c_ulonglong, [P, LL]),
+    "rsc_plan_pairs": (ctypes.c_void_p, [LL, P, P, P, LL, P, P, P, P, P, P]),
+    "rsc_plan_pairs_fetch": (I, [ctypes.c_void_p] + [P] * 7),
+    "rsc_plan_tree_maps": (ctypes.c_void_p, [LL, P, P, P, P, P, P, P, P]),
+    "rsc_plan_tree_maps_fetch": (I, [ctypes.c_void_p, P, P]),
     "rsc_pcg64_block_states": (I, [I, I, P, P, P, P]),
     "rsc_pcg64_seed_states": (I, [I, P, P]),
     "rsc_normal_workspace_bytes": (ctypes.c_size_t, [I, P]),

@@ -103,8 +103,8 @@ class DeviceApply:
                 un = units[i]
                 v = 0
                 if un.kind == "node":
-                    for p in plan.targets[un.j]:
-                        su = uidx.get(plan.sources[p.s].unit)
+                    for ps in plan.tarr[un.j]["s"].tolist():
+                        su = uidx.get(plan.sources[ps].unit)
                         if su is not None and su in lv:  # sources outside `members` run before
                             v = max(v, lv[su] + 1)
                 lv[i] = v

@@ -5,6 +5,7 @@
 // separator tree stay in Python.  Results are a pure function of the inputs
 // (unique sort keys), so they are identical to the numpy formulation.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -63,6 +64,150 @@ int rsc_nd_split_geometric(long long nv, const long long *verts, int dim, const 
     counts[2] = (long long)s2.size();
     std::copy(s2.begin(), s2.end(), out + k);
     return (half == 0 || s2.empty()) ? 1 : 0;
+}
+
+}  // extern "C"
+
+// Whole geometric nested dissection (ordering.py:277-368 with the geometric split
+// above): the recursion of symbolic.py _Dissector.dissect in one call, subtrees on
+// host threads.  A subtree over `verts` (ascending) owns order[base, base+nv): its
+// left part, then its right part, then its separator -- positions depend only on
+// the part sizes, so subtrees are independent.  Each split is O(nv): the half with
+// the smallest (coordinate, vertex id) keys comes from nth_element (the keys are
+// unique, so the set equals the sorted prefix the Python formulation takes) and is
+// marked in a stamp array (a unique stamp per split, so concurrent subtrees never
+// see each other's marks).
+#include <atomic>
+#include <thread>
+
+namespace {
+
+struct NdCtx {
+    int dim;
+    const double *xyz;
+    const long long *indptr, *indices;
+    long long leaf;
+    long long *order;
+    int *stamp;                    // n ints, last split stamp that marked the vertex
+    std::atomic<int> next_stamp{0};
+    std::atomic<long long> next_node{0};
+    long long cap;
+    long long *n_lo, *n_hi, *n_sub, *n_lev, *n_left, *n_right;
+    std::atomic<int> err{0};
+    int par_depth;
+};
+
+long long nd_node(NdCtx &c, long long lo, long long hi, long long sub, long long lev, long long l, long long r) {
+    const long long id = c.next_node.fetch_add(1);
+    if (id >= c.cap) { c.err.store(-3); return -1; }
+    c.n_lo[id] = lo; c.n_hi[id] = hi; c.n_sub[id] = sub; c.n_lev[id] = lev; c.n_left[id] = l; c.n_right[id] = r;
+    return id;
+}
+
+// split verts (ascending) into side1 / sep / side2 (each ascending); false = no split
+bool nd_split(NdCtx &c, const std::vector<long long> &verts, std::vector<long long> &s1, std::vector<long long> &sep,
+              std::vector<long long> &s2) {
+    const long long nv = (long long)verts.size();
+    const int dim = c.dim;
+    const double *xyz = c.xyz;
+    int axis = 0;
+    double best = -1.0;
+    for (int d = 0; d < dim; ++d) {
+        double lo = xyz[verts[0] * dim + d], hi = lo;
+        for (long long i = 1; i < nv; ++i) {
+            const double v = xyz[verts[i] * dim + d];
+            lo = v < lo ? v : lo;
+            hi = v > hi ? v : hi;
+        }
+        const double w = hi - lo;
+        if (d == 0 || w > best) { best = w; axis = d; }
+    }
+    const long long half = (nv + 1) / 2;
+    if (half == 0 || half == nv) return false;
+    std::vector<long long> ord(nv);
+    for (long long i = 0; i < nv; ++i) ord[i] = i;
+    auto less = [&](long long a, long long b) {
+        const double xa = xyz[verts[a] * dim + axis], xb = xyz[verts[b] * dim + axis];
+        if (xa < xb) return true;
+        if (xb < xa) return false;
+        return verts[a] < verts[b];
+    };
+    std::nth_element(ord.begin(), ord.begin() + half, ord.end(), less);
+    std::vector<unsigned char> first(nv, 0);
+    for (long long i = 0; i < half; ++i) first[ord[i]] = 1;
+    const int st = c.next_stamp.fetch_add(1) + 1;
+    s1.clear(); sep.clear(); s2.clear();
+    s1.reserve(half);
+    for (long long i = 0; i < nv; ++i)
+        if (first[i]) {
+            s1.push_back(verts[i]);
+            __atomic_store_n(&c.stamp[verts[i]], st, __ATOMIC_RELAXED);
+        }
+    for (long long i = 0; i < nv; ++i) {
+        if (first[i]) continue;
+        const long long v = verts[i];
+        bool hit = false;
+        for (long long p = c.indptr[v]; p < c.indptr[v + 1]; ++p)
+            if (__atomic_load_n(&c.stamp[c.indices[p]], __ATOMIC_RELAXED) == st) { hit = true; break; }
+        (hit ? sep : s2).push_back(v);
+    }
+    return !s2.empty();
+}
+
+long long nd_dissect(NdCtx &c, std::vector<long long> verts, long long base, long long level, int depth) {
+    const long long nv = (long long)verts.size();
+    if (c.err.load()) return -1;
+    std::vector<long long> s1, sep, s2;
+    if (nv <= c.leaf || !nd_split(c, verts, s1, sep, s2)) {
+        std::copy(verts.begin(), verts.end(), c.order + base);
+        return nd_node(c, base, base + nv, base, level, -1, -1);
+    }
+    std::vector<long long>().swap(verts);
+    const long long n1 = (long long)s1.size(), n2 = (long long)s2.size();
+    long long left = -1, right = -1;
+    if (depth < c.par_depth && n1 + n2 > 4096) {
+        std::thread th([&] { left = nd_dissect(c, std::move(s1), base, level + 1, depth + 1); });
+        right = nd_dissect(c, std::move(s2), base + n1, level + 1, depth + 1);
+        th.join();
+    } else {
+        left = nd_dissect(c, std::move(s1), base, level + 1, depth + 1);
+        right = nd_dissect(c, std::move(s2), base + n1, level + 1, depth + 1);
+    }
+    const long long lo = base + n1 + n2;
+    std::copy(sep.begin(), sep.end(), c.order + lo);
+    return nd_node(c, lo, lo + (long long)sep.size(), base, level, left, right);
+}
+
+}  // namespace
+
+extern "C" {
+
+// order[n] <- dissection order (order[pos] = vertex); node arrays (capacity cap):
+// lo, hi, subtree_lo, level, left, right (-1 = leaf).  Returns the node count
+// (root in *root) or < 0 (-1 bad args, -3 capacity).
+long long rsc_nd_geometric(long long n, int dim, const double *xyz, const long long *indptr,
+                           const long long *indices, long long leaf, long long *order, long long cap, long long *n_lo,
+                           long long *n_hi, long long *n_sub, long long *n_lev, long long *n_left,
+                           long long *n_right, long long *root) {
+    if (n < 1 || dim < 1 || leaf < 1) return -1;
+    NdCtx c;
+    c.dim = dim; c.xyz = xyz; c.indptr = indptr; c.indices = indices; c.leaf = leaf; c.order = order;
+    std::vector<int> stamp(n, 0);
+    c.stamp = stamp.data();
+    c.cap = cap;
+    c.n_lo = n_lo; c.n_hi = n_hi; c.n_sub = n_sub; c.n_lev = n_lev; c.n_left = n_left; c.n_right = n_right;
+    unsigned hw = std::thread::hardware_concurrency();
+    const char *e = getenv("RSC_HOST_THREADS");
+    int T = e ? atoi(e) : (int)(hw ? hw : 1);
+    T = std::max(1, std::min(T, 64));
+    int d = 0;
+    while ((1 << d) < 2 * T) ++d;  // ~2 subtrees per thread at the fork frontier
+    c.par_depth = T > 1 ? d : 0;
+    std::vector<long long> all(n);
+    for (long long i = 0; i < n; ++i) all[i] = i;
+    *root = nd_dissect(c, std::move(all), 0, 0, 0);
+    if (c.err.load()) return c.err.load();
+    return c.next_node.load();
 }
 
 }  // extern "C"

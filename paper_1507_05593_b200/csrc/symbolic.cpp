@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <atomic>
+#include <thread>
 #include "host_par.h"
 
 extern "C" {
@@ -170,13 +172,17 @@ struct RowStructs {
     std::vector<long long> ptr, rows;
 };
 
-extern "C" void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
-                                      const long long *row_idx, long long *total) {
-    auto *h = new RowStructs();
-    h->ptr.assign(M + 1, 0);
-    std::vector<std::vector<long long>> pending(M);
+namespace {
+
+// The sequential sweep over supernodes [j0, j1): R_j into rows[j], pieces for
+// targets t in [j0, j1) into pending[t], pieces for targets outside into outbox.
+void rows_sweep(long long j0, long long j1, long long M, const long long *starts, const long long *col_ptr,
+                const long long *row_idx, std::vector<std::vector<long long>> &pending,
+                std::vector<std::vector<long long>> &rows,
+                std::vector<std::pair<long long, std::vector<long long>>> *outbox, const char *done = nullptr,
+                bool *bad = nullptr) {
     std::vector<long long> buf;
-    for (long long j = 0; j < M; ++j) {
+    for (long long j = j0; j < j1; ++j) {
         const long long c0 = starts[j], c1 = starts[j + 1];
         buf.swap(pending[j]);
         std::vector<long long>().swap(pending[j]);
@@ -184,19 +190,80 @@ extern "C" void *rsc_sym_rows_compute(long long M, const long long *starts, cons
             if (row_idx[p] >= c1) buf.push_back(row_idx[p]);
         std::sort(buf.begin(), buf.end());
         buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
-        h->rows.insert(h->rows.end(), buf.begin(), buf.end());
-        h->ptr[j + 1] = (long long)h->rows.size();
+        rows[j].assign(buf.begin(), buf.end());
         if (!buf.empty()) {
             // supernode t containing the first row; pass up the rows beyond its columns
             const long long t = (long long)(std::upper_bound(starts, starts + M + 1, buf[0]) - starts) - 1;
             const long long t1 = starts[t + 1];
             auto it = std::lower_bound(buf.begin(), buf.end(), t1);
-            pending[t].insert(pending[t].end(), it, buf.end());
+            if (done && done[t]) *bad = true;  // a piece for an already swept range
+            if (t < j1 || !outbox) pending[t].insert(pending[t].end(), it, buf.end());
+            else if (it != buf.end()) outbox->emplace_back(t, std::vector<long long>(it, buf.end()));
         }
         buf.clear();
     }
-    *total = (long long)h->rows.size();
+}
+
+}  // namespace
+
+// nr disjoint supernode ranges [ranges[2i], ranges[2i+1]) closed under the
+// pass-up (ND subtrees: every piece goes to a supernode inside the range or after
+// it) are swept on host threads first; the rest sequentially after merging the
+// ranges' outgoing pieces.  A piece's content does not depend on the order pieces
+// arrive (each R_j is sorted and de-duplicated), so the result equals the
+// sequential sweep.  nr = 0: fully sequential.
+extern "C" void *rsc_sym_rows_compute_par(long long M, const long long *starts, const long long *col_ptr,
+                                          const long long *row_idx, long long nr, const long long *ranges,
+                                          long long *total) {
+    auto *h = new RowStructs();
+    h->ptr.assign(M + 1, 0);
+    std::vector<std::vector<long long>> pending(M), rows(M);
+    std::vector<char> done(M, 0);
+    if (nr > 0) {
+        std::vector<std::vector<std::pair<long long, std::vector<long long>>>> out(nr);
+        const int T = std::max(1, std::min<int>(rsc_host_threads(), (int)nr));
+        std::atomic<long long> next{0};
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&] {
+                for (long long r; (r = next.fetch_add(1)) < nr;)
+                    rows_sweep(ranges[2 * r], ranges[2 * r + 1], M, starts, col_ptr, row_idx, pending, rows, &out[r]);
+            });
+        for (auto &x : th) x.join();
+        for (long long r = 0; r < nr; ++r)
+            for (long long j = ranges[2 * r]; j < ranges[2 * r + 1]; ++j) done[j] = 1;
+        bool bad = false;
+        for (long long r = 0; r < nr; ++r)
+            for (auto &pc : out[r]) {
+                bad |= done[pc.first] != 0;
+                pending[pc.first].insert(pending[pc.first].end(), pc.second.begin(), pc.second.end());
+            }
+        for (long long j = 0; j < M && !bad;) {  // the remaining supernodes, in order
+            if (done[j]) { ++j; continue; }
+            long long e = j;
+            while (e < M && !done[e]) ++e;
+            rows_sweep(j, e, M, starts, col_ptr, row_idx, pending, rows, nullptr, done.data(), &bad);
+            j = e;
+        }
+        if (bad) {  // the ranges were not closed under the pass-up: sequential sweep
+            for (auto &v : pending) std::vector<long long>().swap(v);
+            rows_sweep(0, M, M, starts, col_ptr, row_idx, pending, rows, nullptr);
+        }
+    } else {
+        rows_sweep(0, M, M, starts, col_ptr, row_idx, pending, rows, nullptr);
+    }
+    for (long long j = 0; j < M; ++j) h->ptr[j + 1] = h->ptr[j] + (long long)rows[j].size();
+    h->rows.resize(h->ptr[M]);
+    rsc_parallel_chunks(M, rsc_host_threads(), [&](int, long long lo, long long hi) {
+        for (long long j = lo; j < hi; ++j) std::copy(rows[j].begin(), rows[j].end(), h->rows.begin() + h->ptr[j]);
+    });
+    *total = h->ptr[M];
     return h;
+}
+
+extern "C" void *rsc_sym_rows_compute(long long M, const long long *starts, const long long *col_ptr,
+                                      const long long *row_idx, long long *total) {
+    return rsc_sym_rows_compute_par(M, starts, col_ptr, row_idx, 0, nullptr, total);
 }
 
 extern "C" int rsc_sym_rows_fetch(void *handle, long long *ptr, long long *rows) {

@@ -267,7 +267,7 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
     top_src = set()
     for u, (kind, j) in enumerate(sym.units):
         if kind == "node" and owner[u] == -1:
-            top_src.update(p.s for p in plan.targets[j])
+            top_src.update(plan.tarr[j]["s"].tolist())
     alpha_d = config.alpha_d
     history, restarts = [alpha_d], 0
     sent = 0
@@ -361,7 +361,9 @@ def factorize_distributed(A, config=None, coords=None, group=None, prepared=None
     st.restarts = restarts
     st.alpha_d_final = alpha_d
     st.alpha_d_history = history
-    st.model_gflop = (sum(flops_a) + ps.flops - ps.flops_phase_a) / 1e9
+    from . import numeric as _nm
+
+    st.model_gflop = (sum(flops_a) + ps.flops - ps.flops_phase_a) / 1e9 if _nm.FLOP_MODEL else float("nan")
     st.phase_times = {"ordering": sym.t_ordering, "symbolic": sym.t_symbolic + (t2 - t_plan0),
                       "numeric": t3 - t2, "total": t3 - t0}
     F.world = world

@@ -701,7 +701,9 @@ def factorize(A, config=None, coords=None, prepared=None):
     st.gpu_launches = int(lib.rsc_launch_counter(0)) - launches0
     if entry is not None:
         st.gpu_launches = ps.launches  # kernel nodes of the replayed graph
-    st.model_gflop = ps.flops / 1e9
+    from . import numeric as _nm
+
+    st.model_gflop = ps.flops / 1e9 if _nm.FLOP_MODEL else float("nan")  # RSC_FLOP_MODEL=1
     st.phase_times = {"ordering": sym.t_ordering, "symbolic": sym.t_symbolic + (t2 - t_plan0),
                       "numeric": t3 - t2, "total": t3 - t0}
     return F

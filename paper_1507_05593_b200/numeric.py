@@ -25,6 +25,8 @@ Pivot failures are collected and resolved at the end of the pass in sweep order
 (the earliest failing unit decides restart vs. re-raise, factor.py:705-710).
 """
 
+import os
+
 import numpy as np
 
 from . import engine as E
@@ -42,6 +44,8 @@ from .factor import (
     _raw_eff,
 )
 from .symbolic import block_rank
+
+FLOP_MODEL = os.environ.get("RSC_FLOP_MODEL", "0") == "1"
 
 
 
@@ -224,7 +228,11 @@ class LevelPass(NumericPass):
         pointer wbase) and r the width of the block being formed (its U at rbase, for
         final products).  Compressed panels are sketch-padded during the pass;
         _finalize_ranks re-prices these terms at the kept ranks so model_gflop stays
-        the reference's work model."""
+        the reference's work model.  Off unless RSC_FLOP_MODEL=1 (census.py is the
+        reference work model the bench reports; this per-launch bookkeeping costs
+        host time on the one-shot path)."""
+        if not FLOP_MODEL:
+            return
         if np.ndim(coef) == 0 and np.ndim(w) == 0 and np.ndim(r) == 0:
             self.flops += float(coef) * float(w) * float(r)
             if wbase or rbase:

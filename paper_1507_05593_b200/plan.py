@@ -26,12 +26,15 @@ from . import engine as E
 
 
 def _pattern_key(A):
-    """Digest of a lower-CSC sparsity pattern (col_ptr, row_idx)."""
-    import hashlib
+    """Digest of a lower-CSC sparsity pattern (col_ptr, row_idx): two 64-bit
+    chunked multiply-xor hashes (rsc_hash64, host threads)."""
+    from . import _lib
 
-    h = hashlib.sha1(np.ascontiguousarray(A.col_ptr, dtype=np.int64).tobytes())
-    h.update(np.ascontiguousarray(A.row_idx, dtype=np.int64).tobytes())
-    return (A.n, h.hexdigest())
+    lib = _lib.load()
+    cp = np.ascontiguousarray(A.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(A.row_idx, dtype=np.int64)
+    return (A.n, cp.size, ri.size, int(lib.rsc_hash64(cp.ctypes.data, cp.nbytes)),
+            int(lib.rsc_hash64(ri.ctypes.data, ri.nbytes)))
 
 
 class Source:
@@ -221,9 +224,6 @@ class NumericPlan:
         self.node_blocks = {}      # node j -> (A_CC, A_RC, A_CR)
         self.rows_off = {}         # node j / ("int", u) -> index offset of its row set
         self.interior = []         # (unit index, members, c0, c1, off_rows, A_off csr, A_BB csr)
-        supernode_of = lambda cols: np.searchsorted(part.starts, cols, side="right") - 1
-
-        touched = {}  # j -> list of source ids
         for u, (kind, payload) in enumerate(sym.units):
             if kind == "interior":
                 ids = payload
@@ -258,11 +258,7 @@ class NumericPlan:
                 sid = len(self.sources)
                 self.sources.append(Source(sid, "node", u, R, c0, c1))
                 self.unit_source[u] = sid
-        # every supernode a source's rows fall into is a target of that source
-        for src in self.sources:
-            for j in np.unique(supernode_of(src.rows)):
-                touched.setdefault(int(j), []).append(src.sid)
-        self._build_targets(part, touched)
+        self._build_targets(part)
         self.tree_maps = {}
         self._build_tree_maps(part)
         self.idx.upload()
@@ -279,8 +275,8 @@ class NumericPlan:
             if k != "node":
                 continue
             h = 0
-            for p in self.targets[j]:
-                su = self.sources[p.s].unit
+            for ps in self.tarr[j]["s"].tolist():
+                su = self.sources[ps].unit
                 if su in height:
                     h = max(h, height[su] + 1)
             height[u] = h
@@ -337,86 +333,160 @@ class NumericPlan:
         return DeviceSketches(self.sketch_specs(cfg, alpha_d))
 
 
-    def _build_targets(self, part, touched):
-        for j in list(self.targets):
-            c0, c1 = part.cols(j)
-            R = part.rows[j]
-            pairs = []
-            for sid in touched.get(j, []):
-                src = self.sources[sid]
-                rows = src.rows
-                lo, hi = np.searchsorted(rows, (c0, c1))
-                if lo == hi:
-                    continue
-                cpos = rows[lo:hi] - c0
-                rpos = np.searchsorted(R, rows[hi:])
-                pairs.append(Pair(sid, int(lo), int(hi), self.idx.add(cpos), self.idx.add(rpos), rows.size))
-            pairs.sort(key=lambda p: self.sources[p.s].order)
-            self.targets[j] = pairs
-        # the same maps as flat arrays per target (vectorized descriptor builds)
+    def _build_targets(self, part):
+        """Descendant maps of every (source, target) pair (rsc_plan_pairs, host
+        threads): the pairs of target j in reference order (sources by first column,
+        factor.py:545-554,572), lo/hi = the run of the source's rows inside C_j,
+        cpos = rows[lo:hi] - c0, rpos = searchsorted(R_j, rows[hi:])."""
+        import ctypes
+
+        from . import _lib
+
+        lib = _lib.load()
+        srcs = self.sources
+        nsrc = len(srcs)
+        src_len = np.fromiter((x.rows.size for x in srcs), dtype=np.int64, count=nsrc)
+        src_ptr = np.zeros(nsrc + 1, dtype=np.int64)
+        np.cumsum(src_len, out=src_ptr[1:])
+        src_rows = np.concatenate([x.rows for x in srcs]).astype(np.int64) if nsrc else np.zeros(1, np.int64)
+        src_order = np.fromiter((x.order for x in srcs), dtype=np.int64, count=nsrc)
+        M = part.count
+        is_t = np.zeros(max(M, 1), dtype=np.uint8)
+        tj = np.fromiter(self.targets.keys(), dtype=np.int64, count=len(self.targets))
+        is_t[tj] = 1
+        R_ptr, R_rows = _rows_flat(part)
+        st = np.ascontiguousarray(part.starts, dtype=np.int64)
+        npairs, nidx = ctypes.c_longlong(0), ctypes.c_longlong(0)
+        h = lib.rsc_plan_pairs(nsrc, src_ptr.ctypes.data, src_rows.ctypes.data, src_order.ctypes.data, M,
+                               st.ctypes.data, is_t.ctypes.data, R_ptr.ctypes.data, R_rows.ctypes.data,
+                               ctypes.byref(npairs), ctypes.byref(nidx))
+        npr = npairs.value
+        out = [np.empty(max(npr, 1), dtype=np.int64) for _ in range(6)]
+        chunk = np.empty(max(nidx.value, 1), dtype=np.int32)
+        _lib.check(lib.rsc_plan_pairs_fetch(h, *[o.ctypes.data for o in out], chunk.ctypes.data),
+                   "rsc_plan_pairs_fetch")
+        tgt, sid, lo, hi, cpos, rpos = (o[:npr] for o in out)
+        base = self.idx.add(chunk[:nidx.value])
+        cpos = cpos + base
+        rpos = rpos + base
+        nro = src_len[sid] - hi
+        self._src_ptr, self._src_rows = src_ptr, src_rows
+        self.pair_arrays = {"tgt": tgt, "s": sid, "lo": lo, "hi": hi, "cpos": cpos, "rpos": rpos}
+        bnd = np.searchsorted(tgt, tj, side="left"), np.searchsorted(tgt, tj, side="right")
+        self.pair_range = {}
         self.tarr = {}
-        for j, pairs in self.targets.items():
-            self.tarr[j] = {
-                "s": np.array([p.s for p in pairs], dtype=np.int64),
-                "lo": np.array([p.lo for p in pairs], dtype=np.int64),
-                "hi": np.array([p.hi for p in pairs], dtype=np.int64),
-                "nrd": np.array([p.n_rd for p in pairs], dtype=np.int64),
-                "nro": np.array([p.n_ro for p in pairs], dtype=np.int64),
-                "cpos": np.array([p.cpos_off for p in pairs], dtype=np.int64),
-                "rpos": np.array([p.rpos_off for p in pairs], dtype=np.int64),
-            }
+        for j, a, b in zip(tj.tolist(), bnd[0].tolist(), bnd[1].tolist()):
+            self.pair_range[j] = (a, b)
+            self.tarr[j] = {"s": sid[a:b], "lo": lo[a:b], "hi": hi[a:b], "nrd": hi[a:b] - lo[a:b],
+                            "nro": nro[a:b], "cpos": cpos[a:b], "rpos": rpos[a:b]}
+        self.targets = _TargetPairs(self.tarr)
 
     def _build_tree_maps(self, part):
         """Window maps for every (tree node j, block s, source) with both windows
-        non-empty (diagblocks.py:231-234, 252-255), plus the A windows.  Vectorized
-        per source: one searchsorted of all block bounds, one index chunk."""
+        non-empty (diagblocks.py:231-234, 252-255; rsc_plan_tree_maps, host threads),
+        plus the A windows of every tree block."""
+        import ctypes
+
+        from . import _lib
         from .diagtree import TreeShape
 
+        lib = _lib.load()
         self.tree_shapes = {}
         self.tmap = {}
-        keys = ("s", "clo", "chi", "rlo", "rhi", "cidx", "ridx")
+        trees = []
+        spans_all, blk_ptr, pair_ptr = [], [0], []
         for j, split in self.sym.sep_splits.items():
             c0, c1 = part.cols(j)
             shape = TreeShape(c1 - c0, c0, split)
             self.tree_shapes[j] = shape
             order = list(shape.order)
-            nb = len(order)
-            spans = np.array([shape.span(s) for s in order], dtype=np.int64).reshape(nb, 4) + c0
+            spans = np.array([shape.span(s) for s in order], dtype=np.int64).reshape(len(order), 4) + c0
+            trees.append((j, order, spans))
+            spans_all.append(spans)
+            blk_ptr.append(blk_ptr[-1] + len(order))
+            pair_ptr.append(self.pair_range[j])
+        keys = ("s", "clo", "chi", "rlo", "rhi", "cidx", "ridx")
+        if trees:
+            spans_c = np.ascontiguousarray(np.concatenate(spans_all), dtype=np.int64)
+            bp = np.asarray(blk_ptr, dtype=np.int64)
+            # pairs of tree t = [pp[2t], pp[2t+1]) in the global pair arrays: pass a
+            # per-tree copy of those source ids so the ranges are contiguous
+            psrc = np.concatenate([self.pair_arrays["s"][a:b] for a, b in pair_ptr]).astype(np.int64)
+            pp = np.zeros(len(pair_ptr) + 1, dtype=np.int64)
+            np.cumsum([b - a for a, b in pair_ptr], out=pp[1:])
+            nm, ni = ctypes.c_longlong(0), ctypes.c_longlong(0)
+            h = lib.rsc_plan_tree_maps(len(trees), bp.ctypes.data, spans_c.ctypes.data, pp.ctypes.data,
+                                       psrc.ctypes.data, self._src_ptr.ctypes.data, self._src_rows.ctypes.data,
+                                       ctypes.byref(nm), ctypes.byref(ni))
+            out = [np.empty(max(nm.value, 1), dtype=np.int64) for _ in range(9)]
+            chunk = np.empty(max(ni.value, 1), dtype=np.int32)
+            ptrs = (ctypes.c_void_p * 9)(*[o.ctypes.data for o in out])
+            _lib.check(lib.rsc_plan_tree_maps_fetch(h, ptrs, chunk.ctypes.data), "rsc_plan_tree_maps_fetch")
+            out = [o[:nm.value] for o in out]
+            base = self.idx.add(chunk[:ni.value])
+            gblk = bp[out[0]] + out[1]  # global block index: maps are grouped by it
+            cut = np.searchsorted(gblk, np.arange(bp[-1] + 1), side="left")
+            cols = [out[2], out[3], out[4], out[5], out[6], out[7] + base, out[8] + base]
+        for t, (j, order, spans) in enumerate(trees):
             gr0, gr1, gc0, gc1 = spans.T
-            bounds = np.concatenate((gc0, gc1, gr0, gr1))
-            per = [[] for _ in range(nb)]
-            for pr in self.targets[j]:
-                rows = self.sources[pr.s].rows
-                clo, chi, rlo, rhi = np.searchsorted(rows, bounds).reshape(4, nb)
-                ok = np.nonzero((clo < chi) & (rlo < rhi))[0]
-                if ok.size == 0:
-                    continue
-                # one index chunk: [cidx of every kept block] then [ridx of every kept block]
-                cl, ch, rl, rh = clo[ok], chi[ok], rlo[ok], rhi[ok]
-                nc, nr = ch - cl, rh - rl
-                lens = np.concatenate((nc, nr))
-                starts = np.concatenate((cl, rl))
-                base = np.concatenate((gc0[ok], gr0[ok]))
-                first = np.cumsum(lens) - lens
-                tot = int(lens.sum())
-                src = np.repeat(starts - first, lens) + np.arange(tot)
-                chunk = rows[src] - np.repeat(base, lens)
-                off0 = self.idx.add(chunk)
-                offs = off0 + first
-                for t, k in enumerate(ok.tolist()):
-                    m = TreeBlockMaps()
-                    m.s, m.clo, m.chi, m.rlo, m.rhi = pr.s, int(cl[t]), int(ch[t]), int(rl[t]), int(rh[t])
-                    m.cidx_off, m.ridx_off = int(offs[t]), int(offs[ok.size + t])
-                    per[k].append(m)
             for k, s in enumerate(order):
                 g = (int(gr0[k]), int(gr1[k])), (int(gc0[k]), int(gc1[k]))
                 blk = self.csr.add(g[0], g[1])
                 blkT = self.csr.add(g[1], g[0]) if g[0] != g[1] else None
-                maps = per[k]
-                self.tree_maps[(j, s)] = (maps, blk, blkT)
-                vals = np.array([[m.s, m.clo, m.chi, m.rlo, m.rhi, m.cidx_off, m.ridx_off] for m in maps],
-                                dtype=np.int64).reshape(len(maps), 7)
-                self.tmap[(j, s)] = {kk: vals[:, i].copy() for i, kk in enumerate(keys)}
+                self.tree_maps[(j, s)] = (None, blk, blkT)
+                a, b = int(cut[blk_ptr[t] + k]), int(cut[blk_ptr[t] + k + 1])
+                self.tmap[(j, s)] = {kk: cols[i][a:b] for i, kk in enumerate(keys)}
+
+
+def _rows_flat(part):
+    """(ptr[M+1], rows) of the row structures R_j (one array when
+    compute_row_structures made them)."""
+    fl = getattr(part, "rows_flat", None)
+    if fl is not None:
+        return fl
+    lens = np.fromiter((r.size for r in part.rows), dtype=np.int64, count=len(part.rows))
+    ptr = np.zeros(len(part.rows) + 1, dtype=np.int64)
+    np.cumsum(lens, out=ptr[1:])
+    rows = np.concatenate(part.rows).astype(np.int64) if part.rows else np.zeros(1, np.int64)
+    return ptr, rows
+
+
+class _TargetPairs:
+    """targets[j] -> [Pair] in reference order, built on first access from the
+    plan's flat pair arrays (tarr)."""
+
+    def __init__(self, tarr):
+        self._tarr = tarr
+        self._cache = {}
+
+    def __getitem__(self, j):
+        got = self._cache.get(j)
+        if got is None:
+            t = self._tarr[j]
+            got = [Pair(s, lo, hi, c, r, hi + nro)
+                   for s, lo, hi, c, r, nrd, nro in zip(t["s"].tolist(), t["lo"].tolist(), t["hi"].tolist(),
+                                                        t["cpos"].tolist(), t["rpos"].tolist(),
+                                                        t["nrd"].tolist(), t["nro"].tolist())]
+            self._cache[j] = got
+        return got
+
+    def __contains__(self, j):
+        return j in self._tarr
+
+    def __iter__(self):
+        return iter(self._tarr)
+
+    def __len__(self):
+        return len(self._tarr)
+
+    def keys(self):
+        return self._tarr.keys()
+
+    def items(self):
+        return ((j, self[j]) for j in self._tarr)
+
+    def values(self):
+        return (self[j] for j in self._tarr)
 
 
 class DeviceSketches:

@@ -316,6 +316,8 @@ def nested_dissection(A, leaf_size=DEFAULT_LEAF_SIZE, coords=None, method="auto"
     if A.n == 0:
         return Permutation.identity(0), SeparatorTree(0, None)
     d = _Dissector(A, leaf_size, xyz, method)
+    if d._nd is not None:
+        return _nd_geometric_native(d)
     import sys
 
     sys.setrecursionlimit(max(sys.getrecursionlimit(), 10000))
@@ -323,6 +325,39 @@ def nested_dissection(A, leaf_size=DEFAULT_LEAF_SIZE, coords=None, method="auto"
     fwd = np.empty(A.n, dtype=np.int64)
     fwd[d.order] = np.arange(A.n, dtype=np.int64)
     return Permutation(fwd), SeparatorTree(A.n, root)
+
+
+def _nd_geometric_native(d):
+    """The geometric recursion in one C++ call (rsc_nd_geometric, subtrees on host
+    threads); the same order and tree as _Dissector.dissect."""
+    n = d.n
+    cap = 2 * n + 1
+    order = np.empty(n, dtype=np.int64)
+    nodes = np.empty((6, cap), dtype=np.int64)
+    root = np.zeros(1, dtype=np.int64)
+    cnt = _lib.load().rsc_nd_geometric(n, d.xyz.shape[1], d.xyz.ctypes.data, d.indptr.ctypes.data,
+                                       d.indices.ctypes.data, d.leaf, order.ctypes.data, cap,
+                                       *[nodes[i].ctypes.data for i in range(6)], root.ctypes.data)
+    if cnt < 0:
+        raise RuntimeError(f"rsc_nd_geometric failed ({cnt})")
+    lo, hi, sub, lev, left, right = (nodes[i, :cnt].tolist() for i in range(6))
+    objs = [None] * cnt
+    # children are created before their parent (post-order ids within a subtree) is
+    # not guaranteed across threads: build by explicit stack from the root
+    stack = [(int(root[0]), False)]
+    while stack:
+        i, done = stack.pop()
+        if left[i] < 0:
+            objs[i] = SeparatorNode(lo[i], hi[i], sub[i], lev[i])
+        elif done:
+            objs[i] = SeparatorNode(lo[i], hi[i], sub[i], lev[i], objs[left[i]], objs[right[i]])
+        else:
+            stack.append((i, True))
+            stack.append((right[i], False))
+            stack.append((left[i], False))
+    fwd = np.empty(n, dtype=np.int64)
+    fwd[order] = np.arange(n, dtype=np.int64)
+    return Permutation(fwd), SeparatorTree(n, objs[int(root[0])])
 
 
 def partition_separator(coords, C, tau_d):
@@ -441,7 +476,33 @@ def form_supernodes(n, parent, counts, septree, tau_o, relax=True):
     return SupernodePartition(n, starts, flags)
 
 
-def compute_row_structures(B, part):
+def _subtree_ranges(part, septree, target=64):
+    """Supernode ranges of disjoint ND subtrees (about `target` of them, largest
+    first split) for the threaded row-structure sweep: a subtree's pieces only go to
+    its own supernodes or to ancestor separators after it."""
+    if septree.root is None:
+        return np.zeros(0, dtype=np.int64)
+    front = [septree.root]
+    while len(front) < target:
+        big = max((nd for nd in front if nd.is_separator), key=lambda nd: nd.hi - nd.subtree_lo, default=None)
+        if big is None:
+            break
+        front.remove(big)
+        front += [big.left, big.right]
+    st = part.starts
+    out = []
+    for nd in front:
+        lo, hi = nd.subtree_lo, nd.hi
+        if hi - lo < 2:
+            continue
+        j0 = int(np.searchsorted(st, lo, side="left"))
+        j1 = int(np.searchsorted(st, hi, side="left"))
+        if j0 < j1 and st[j0] == lo and j1 < st.size and st[j1] == hi:
+            out += [j0, j1]
+    return np.asarray(sorted(out), dtype=np.int64)
+
+
+def compute_row_structures(B, part, septree=None):
     """R_j = A's below-block rows of C_j  U  children's rows beyond their parent's
     columns (symbolic.py:280-306); the merge sweep runs in C++
     (rsc_sym_rows_compute / rsc_sym_rows_fetch), R_j are views of one array."""
@@ -453,12 +514,15 @@ def compute_row_structures(B, part):
     cp = np.ascontiguousarray(B.col_ptr, dtype=np.int64)
     ri = np.ascontiguousarray(B.row_idx, dtype=np.int64)
     total = ctypes.c_longlong(0)
-    h = lib.rsc_sym_rows_compute(M, st.ctypes.data, cp.ctypes.data, ri.ctypes.data, ctypes.byref(total))
+    rg = _subtree_ranges(part, septree) if septree is not None else np.zeros(0, dtype=np.int64)
+    h = lib.rsc_sym_rows_compute_par(M, st.ctypes.data, cp.ctypes.data, ri.ctypes.data, rg.size // 2,
+                                     rg.ctypes.data, ctypes.byref(total))
     ptr = np.empty(M + 1, dtype=np.int64)
     allrows = np.empty(max(total.value, 1), dtype=np.int64)
     _lib.check(lib.rsc_sym_rows_fetch(h, ptr.ctypes.data, allrows.ctypes.data), "rsc_sym_rows_fetch")
     rows = [allrows[ptr[j]:ptr[j + 1]] for j in range(M)]
     part.rows = rows
+    part.rows_flat = (ptr, allrows)
     return rows
 
 
@@ -530,7 +594,7 @@ def analyze(A, tau_o, tau_d, interior_blocks=True, coords=None):
     t1 = time.perf_counter()
     parent, post, counts = etree_postorder_counts(B)
     part = form_supernodes(B.n, parent, counts, septree, tau_o)
-    compute_row_structures(B, part)
+    compute_row_structures(B, part, septree)
     sep_splits = {part.supernode_of(lo): s for (lo, hi), s in splits_by_range.items()}
     units = build_units(septree, part, tau_o, interior_blocks)
     t2 = time.perf_counter()
