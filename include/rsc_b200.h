@@ -231,6 +231,11 @@ int rsc_pcg_update_p(int n, const double *rznew_dev, const double *rz_dev,
  * colcounts: nonzeros per column of the Cholesky factor, diagonal included. */
 int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_idx,
                   long long *parent);
+/* The same etree with the rows of nr disjoint ND-subtree column ranges
+ * [ranges[2r], ranges[2r+1]) on host threads first; returns 1 when the ranges are
+ * not closed (parent then untouched: call rsc_sym_etree). */
+int rsc_sym_etree_par(long long n, const long long *col_ptr, const long long *row_idx, long long nr,
+                      const long long *ranges, long long *parent);
 int rsc_sym_postorder(long long n, const long long *parent, long long *post);
 int rsc_sym_colcounts(long long n, const long long *col_ptr, const long long *row_idx,
                       const long long *parent, const long long *post, long long *counts);

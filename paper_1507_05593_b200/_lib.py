@@ -56,6 +56,7 @@ EXPORTED = (
     "rsc_pcg_update_xr",
     "rsc_pcg_update_p",
     "rsc_sym_etree",
+    "rsc_sym_etree_par",
     "rsc_sym_postorder",
     "rsc_sym_colcounts",
     "rsc_sym_amalgamate",
@@ -119,6 +120,7 @@ _SIGS = {
     "rsc_pcg_update_xr": (I, [I, P, P, P, P, P, P, P]),
     "rsc_pcg_update_p": (I, [I, P, P, P, P, P]),
     "rsc_sym_etree": (I, [LL, P, P, P]),
+    "rsc_sym_etree_par": (I, [LL, P, P, LL, P, P]),
     "rsc_sym_postorder": (I, [LL, P, P]),
     "rsc_sym_colcounts": (I, [LL, P, P, P, P, P]),
     "rsc_sym_amalgamate": (LL, [LL, P, P, P, I, P, P, P]),

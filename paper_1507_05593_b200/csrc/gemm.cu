@@ -190,6 +190,9 @@ template <bool TA, bool TB, bool GATHER>
 #endif
 __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const __grid_constant__ GemmArgs args) {
     extern __shared__ __align__(16) double gsm[];
+    // a dependent ordered reduce (launched with programmatic stream serialization)
+    // may start its list building while the last GEMM tiles run
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     double(*sA)[A_SZ] = reinterpret_cast<double(*)[A_SZ]>(gsm);
     double(*sB)[B_SZ] = reinterpret_cast<double(*)[B_SZ]>(gsm + STAGES * A_SZ);
 
@@ -305,6 +308,7 @@ struct RedGroup {
     int *rtab;            // [ext_r][np]: first local row of problem q mapped to target row t, or -1
     int *ctab;            // [np][ext_c]: local column of problem q mapped to target column c, or -1
     int ldc, ext_r, ext_c, batch, p0, np, TR, CW;
+    int uniform;          // no column maps and every partial is ext_c wide (row-sweep fast path)
 };
 
 struct RedArgs {
@@ -356,13 +360,19 @@ __global__ void __launch_bounds__(RT) reduce_tables_kernel(const __grid_constant
 // C + P_q1 + P_q2 + ... over the problems that reach it, in problem order.  Per row
 // of the tile the contributing (problem, first local row, run length) entries are
 // collected once, in problem order, into shared memory by one warp per row (ballot
-// + popc compaction), so the element loop issues only independent partial loads.
+// + popc compaction).
+//   Groups without column maps (the common case: sketch products scattered by row)
+// store each entry as the address of the partial row itself (run length in the top
+// byte): per partial element one shared-memory list read and one coalesced load, no
+// map or descriptor lookups (the kernel was issue-bound at ~20 instructions per
+// partial element).  Column-mapped groups keep the per-element lookup.
 constexpr int LIST_MAX = 4096;  // entries per CTA (TR x np bounded by the host)
 
 __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constant__ RedArgs a) {
-    __shared__ int s_q[LIST_MAX];
-    __shared__ int s_i[LIST_MAX];
+    __shared__ unsigned long long s_buf[LIST_MAX];  // fast path: packed row pointers; else s_q | s_i
     __shared__ int s_cnt[TR_MAX];
+    int *s_q = reinterpret_cast<int *>(s_buf);
+    int *s_i = s_q + LIST_MAX;
     const long long cta = blockIdx.x;
     int lo = 0, hi = a.count - 1;
     while (lo < hi) {
@@ -376,8 +386,77 @@ __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constan
     const int rem = (int)(local - (long long)b * nbr * nbc);
     const int t0 = (rem / nbc) * G.TR, c0 = (rem % nbc) * G.CW;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per-row contributor lists: row tt owns s_q/s_i[tt * np ...]; s_i packs the first
-    // local row (low 24 bits) and the run length of repeated rows (high 8 bits)
+    const bool fast = G.uniform != 0;
+    if (fast) {
+        // uniform group (no column maps, every partial ext_c wide): target column c is
+        // column c of every contributing partial row.  One warp per tile row collects
+        // the row's contributor list as packed partial-row addresses (the rtab row is
+        // read in one go: every round's load in flight before the ballots); then the
+        // tile's elements are dealt to threads, UF partial loads in flight per
+        // element, summed in problem order.
+        constexpr int UF = 8, QMAX = (MAXP + 31) / 32;
+        for (int tt = warp; tt < G.TR; tt += RT / 32) {
+            const int t = t0 + tt;
+            int n = 0;
+            if (t < G.ext_r) {
+                int pre[QMAX];
+#pragma unroll
+                for (int r = 0; r < QMAX; ++r) {
+                    const int q = r * 32 + lane;
+                    pre[r] = -1;
+                    if (q < G.np) {
+                        if (G.rtab) pre[r] = __ldg(G.rtab + (long long)t * G.np + q);
+                        else pre[r] = t < a.p[G.p0 + q].M ? (t | (1 << 24)) : -1;
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < QMAX; ++r) {
+                    const int q = r * 32 + lane, i = pre[r];
+                    const unsigned bal = __ballot_sync(0xffffffffu, i >= 0);
+                    if (i >= 0) {
+                        const RedProb &P = a.p[G.p0 + q];
+                        const double *row = P.P + (long long)b * P.M * P.N + (long long)(i & 0xffffff) * P.N;
+                        s_buf[tt * G.np + n + __popc(bal & ((1u << lane) - 1u))] =
+                            (unsigned long long)row | ((unsigned long long)((unsigned)i >> 24) << 56);
+                    }
+                    n += __popc(bal);
+                }
+            }
+            if (lane == 0) s_cnt[tt] = n;
+        }
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the partials are written
+        __syncthreads();
+        const long long N = G.ext_c;
+        double *C = G.C + (long long)b * G.sC;
+        for (int e = threadIdx.x; e < G.TR * G.CW; e += RT) {
+            const int tt = e / G.CW, t = t0 + tt, c = c0 + (e - tt * G.CW);
+            const int n = s_cnt[tt];
+            if (n == 0 || t >= G.ext_r || c >= G.ext_c) continue;
+            const unsigned long long *lst = s_buf + tt * G.np;
+            double *dst = C + (long long)t * G.ldc + c;
+            double acc = *dst;
+            for (int k0 = 0; k0 < n; k0 += UF) {
+                double x[UF];
+#pragma unroll
+                for (int u = 0; u < UF; ++u) {
+                    x[u] = 0.0;
+                    if (k0 + u < n) {
+                        const unsigned long long en = lst[k0 + u];
+                        const double *src = reinterpret_cast<const double *>(en & 0x00ffffffffffffffULL) + c;
+                        x[u] = src[0];
+                        const int run = (int)(en >> 56);
+                        for (int r = 1; r < run; ++r) x[u] += src[r * N];  // exact-zero repeats
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UF; ++u)
+                    if (k0 + u < n) acc += x[u];
+            }
+            *dst = acc;
+        }
+        return;
+    }
+    // per-row contributor lists: row tt owns entries [tt * np, tt * np + s_cnt[tt])
     for (int tt = warp; tt < G.TR; tt += RT / 32) {
         const int t = t0 + tt;
         int n = 0;
@@ -400,6 +479,7 @@ __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constan
         }
         if (lane == 0) s_cnt[tt] = n;
     }
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the partials are written
     __syncthreads();
     double *C = G.C + (long long)b * G.sC;
     constexpr int U = RED_U;
@@ -504,7 +584,7 @@ int plan_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<con
     for (int g = 0; g < (int)gfirst.size(); ++g) {
         const rsc_gemm_problem &f = reds[gfirst[g]];
         int np = 0, er = 0, ec = 0;
-        bool rmap = false, cmap = false;
+        bool rmap = false, cmap = false, sameN = true;
         for (int i = 0; i < n; ++i) {
             if (gid[i] != g) continue;
             const rsc_gemm_problem &p = reds[i];
@@ -514,6 +594,7 @@ int plan_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<con
             ec = std::max(ec, p.ext_c > 0 ? p.ext_c : p.N);
             rmap |= p.c_rows != nullptr;
             cmap |= p.c_cols != nullptr;
+            sameN &= p.N == f.N;
             ++np;
         }
         if (np == 1 && !rmap && !cmap) {
@@ -529,8 +610,14 @@ int plan_reduce(const std::vector<rsc_gemm_problem> &reds, const std::vector<con
         G.ext_c = ec;
         G.p0 = ra.nprob;
         G.np = np;
-        G.CW = std::min(ec, RT);
-        G.TR = std::max(1, std::min(std::min(TR_MAX, (RT * RED_EPT) / G.CW), LIST_MAX / np));
+        G.uniform = !cmap && sameN && f.N == ec;
+        if (G.uniform) {  // ~4 target elements per thread, at most one row per warp
+            G.CW = std::min(ec, 4 * RT);
+            G.TR = std::max(1, std::min(std::min(RT / 32, std::max(1, 4 * RT / G.CW)), LIST_MAX / np));
+        } else {
+            G.CW = std::min(ec, RT);
+            G.TR = std::max(1, std::min(std::min(TR_MAX, (RT * RED_EPT) / G.CW), LIST_MAX / np));
+        }
         G.rtab = G.ctab = nullptr;
         const long long rb = rmap ? ((long long)er * np * 4 + 255) / 256 * 256 : 0;
         const long long cb = cmap ? ((long long)ec * np * 4 + 255) / 256 * 256 : 0;
@@ -606,12 +693,27 @@ int launch_reduce(RedArgs &ra, long long ctas, char *tab, long long tab_used, cu
                     fprintf(stderr, "RSC_GEMM_DEBUG: groups %d/%d overlap\n", g, h);
             }
     }
-    if (tab_used > 0) {
-        cudaMemsetAsync(tab, 0xff, (size_t)tab_used, s);  // every table entry = -1
-        reduce_tables_kernel<<<ra.nprob, RT, 0, s>>>(ra);
-        RSC_CHECK_LAUNCH();
-    }
-    ordered_reduce_kernel<<<(unsigned)ctas, RT, 0, s>>>(ra);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    static const bool no_pdl = getenv("RSC_GEMM_NO_PDL") != nullptr;  // profiling: plain stream order
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(RT);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, ordered_reduce_kernel, ra);
+    rsc_count_launch();
+    return e == cudaSuccess ? 0 : (int)e;
+}
+
+// inverse-map tables of a chunk's reduce: depend only on the problems' maps, so they
+// are built before the GEMM launch (the reduce then follows the GEMM directly)
+int launch_reduce_tables(RedArgs &ra, char *tab, long long tab_used, cudaStream_t s) {
+    if (ra.count == 0 || tab_used <= 0) return 0;
+    cudaMemsetAsync(tab, 0xff, (size_t)tab_used, s);  // every table entry = -1
+    reduce_tables_kernel<<<ra.nprob, RT, 0, s>>>(ra);
     RSC_CHECK_LAUNCH();
     return 0;
 }
@@ -711,6 +813,7 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
                 q.beta = 1.0;
             }
         }
+        if (!reds.empty() && (rc = launch_reduce_tables(ra, ws.ptr + used, tab_used, s))) return rc;
         // the gathered-B loader is its own instantiation: its index prefetch costs the
         // plain kernels ~2.5% (registers), it is only used for launches that gather
         if (!transA && !transB) rc = gather ? launch_chunk<false, false, true>(args, tiles, s)

@@ -21,6 +21,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 #include "common.cuh"
@@ -39,6 +41,7 @@ struct MatDesc {
     double *W;  // per-matrix workspace: cols (ldw*k) | vn1 | vn2 | tau | diagR | vbuf(m) | perm(k ints)
     int *rank;
     int m, k, ldg, ldq, ldw, cpc, nblk, blk0;
+    int vsm;    // global-column variant: the reflector is staged in shared memory
 };
 
 struct MArgs {
@@ -50,11 +53,24 @@ struct MArgs {
 struct Ws {
     double *cols, *vn1, *vn2, *tau, *diagR, *vbuf;
     int *perm;
-    double *cand_v;  // per-CTA pivot candidate of the next step: largest vn1 ...
-    int *cand_p;     // ... and its position (CQ_MAX slots each)
+    double *cand_v;    // per-CTA pivot candidate of the next step: largest vn1 ...
+    int *cand_p;       // ... its position ...
+    int *cand_pc;      // ... and its physical column (-1: none); all three double-buffered by step parity
+    double *cand_col;  // the candidate column itself (rows >= the step), [parity][CTA][ldw]
+    int cq2;           // CTAs per parity slot of cand_col
 };
 
 constexpr int CQ_MAX = 256;  // >= CTAs of one matrix group (<= SM count)
+constexpr int QB_WY = 64;    // = QB, the compact-WY block of the Q formation below
+
+// start (in doubles) of the candidate region, after the factorization workspace and
+// the WY region of the Q formation (rsc_qrcp_coop_doubles)
+__host__ __device__ inline long long coop_cand_base(int m, int k) {
+    const long long ldw = m | 1;
+    const long long kmin = m < k ? m : k;
+    return ldw * k + 4LL * k + m + k + 2 * CQ_MAX + 64 + (long long)m * kmin + QB_WY * kmin +
+           2LL * QB_WY * QB_WY + 64;
+}
 
 __device__ __forceinline__ Ws carve(const MatDesc &d) {
     Ws w;
@@ -65,8 +81,12 @@ __device__ __forceinline__ Ws carve(const MatDesc &d) {
     w.diagR = w.tau + d.k;
     w.vbuf = w.diagR + d.k;
     w.perm = reinterpret_cast<int *>(w.vbuf + d.m);
-    w.cand_v = w.vbuf + d.m + d.k;
-    w.cand_p = reinterpret_cast<int *>(w.cand_v + CQ_MAX);
+    double *ext = d.W + coop_cand_base(d.m, d.k);
+    w.cand_v = ext;
+    w.cand_p = reinterpret_cast<int *>(ext + 2 * CQ_MAX);
+    w.cand_pc = w.cand_p + 2 * CQ_MAX;
+    w.cand_col = ext + 4 * CQ_MAX;
+    w.cq2 = d.k < CQ_MAX ? d.k : CQ_MAX;
     return w;
 }
 
@@ -74,8 +94,10 @@ __device__ __forceinline__ void group_barrier(unsigned *ctr, int nblk, unsigned 
     __syncthreads();
     if (nblk > 1) {
         if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(ctr, 1u);
+            // release-increment (orders this CTA's prior writes, which bar.sync made
+            // visible to this thread, before the arrival) instead of a full
+            // __threadfence + atomicAdd; acquire-poll for the last arrival
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
             const unsigned target = (epoch + 1) * (unsigned)nblk;
             unsigned v;
             do {
@@ -89,33 +111,168 @@ __device__ __forceinline__ void group_barrier(unsigned *ctr, int nblk, unsigned 
 
 // This CTA's pivot candidate for step i: the largest vn1 among its owned columns
 // still at positions >= i (first position on ties; NaN never wins), published to
-// cand[lb] for the group.  The next pivot search then reads one candidate per CTA
-// instead of walking all k norms through L2 (a serial chain of ~k/32 dependent L2
-// loads per column step on the large sketches).
-__device__ __forceinline__ void publish_candidate(const Ws &w, const int *posof, int c0, int c1, int i, int lb,
-                                                  double *red, int *redp) {
+// slot `par` of cand_v / cand_p / cand_pc.  The next pivot search then reads one
+// candidate per CTA instead of walking all k norms through L2.  With pub_col the
+// candidate column's rows [i, m) are published too (cand_col), so every CTA can form
+// the next reflector itself when this candidate wins -- no second group barrier per
+// column step.
+__device__ __forceinline__ void publish_candidate(const Ws &w, const double *vn1, const int *posof, int c0, int c1,
+                                                  int i, int lb, double *red, int *redp, int par, const double *cols,
+                                                  int ldw, int m, bool pub_col) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double best = -1.0;
-    int bp = 0x7fffffff;
+    int bp = 0x7fffffff, bph = -1;
     for (int phys = c0 + t; phys < c1; phys += CT) {
         const int ps = posof[phys];
         if (ps < i) continue;
-        const double vv = w.vn1[phys];
-        if (vv > best || (vv == best && ps < bp)) { best = vv; bp = ps; }
+        const double vv = vn1[phys];
+        if (vv > best || (vv == best && ps < bp)) { best = vv; bp = ps; bph = phys; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+        const int oh = __shfl_xor_sync(0xffffffffu, bph, o);
+        if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; bph = oh; }
     }
-    if (lane == 0) { red[warp] = best; redp[warp] = bp; }
+    __shared__ int s_bph;
+    if (lane == 0) { red[warp] = best; redp[warp] = bp; redp[16 + warp] = bph; }
     __syncthreads();
     if (t == 0) {
         for (int q = 1; q < CT / 32; ++q)
-            if (red[q] > best || (red[q] == best && redp[q] < bp)) { best = red[q]; bp = redp[q]; }
-        w.cand_v[lb] = best;
-        w.cand_p[lb] = bp;
+            if (red[q] > best || (red[q] == best && redp[q] < bp)) { best = red[q]; bp = redp[q]; bph = redp[16 + q]; }
+        w.cand_v[par * CQ_MAX + lb] = best;
+        w.cand_p[par * CQ_MAX + lb] = bp;
+        w.cand_pc[par * CQ_MAX + lb] = (best >= 0.0) ? bph : -1;
+        s_bph = (best >= 0.0) ? bph : -1;
+    }
+    if (pub_col) {
+        __syncthreads();
+        const int ph = s_bph;
+        if (ph >= 0) {
+            const double *src = cols + (long long)(ph - c0) * ldw;
+            double *dst = w.cand_col + ((long long)par * w.cq2 + lb) * ldw;
+            for (int r = i + t; r < m; r += CT) dst[r] = src[r];
+        }
+    }
+}
+
+// CB block sums at once (one pass through shared memory); results broadcast.
+// red must hold >= CB * CT/32 doubles.
+template <int CB>
+__device__ __forceinline__ void block_sum_n(double (&x)[CB], double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = CT / 32;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) x[c] = warp_sum(x[c]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < CB; ++c) red[c * NW + warp] = x[c];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) t += red[c * NW + q];  // same order in every thread
+        x[c] = t;
+    }
+}
+
+// Householder step i on this CTA's global-memory columns [c0, c1) (mqrcp_kernel,
+// !SMEM): apply H_i^T = I - tau v v^T (v[i] = 1 implicit, v[i+1..m) in `vs`) to the
+// columns still unchosen, then the dlaqp2 norm downdate with the sqrt(eps)
+// recomputation test.  CB columns per pass; every sum is a fixed-order block sum.
+__device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *cols, const double *vs, bool vsm,
+                                            const int *posof, int c0, int c1, int i, int m, int ldw, double tau,
+                                            double *red) {
+    constexpr int CB = 4;
+    __shared__ int s_redo[CB];
+    const int t = threadIdx.x;
+    for (int jb = c0; jb < c1; jb += CB) {
+        bool on[CB];
+        double *cj[CB];
+        bool any = false;
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            const int phys = jb + c;
+            on[c] = phys < c1 && posof[phys] > i;  // posof is replicated: uniform in the CTA
+            cj[c] = cols + (long long)(on[c] ? phys - c0 : 0) * ldw;
+            any |= on[c];
+        }
+        if (!any) continue;
+        double f[CB], cji0[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) cji0[c] = on[c] ? cj[c][i] : 0.0;  // before thread 0 rewrites row i
+        if (tau != 0.0) {
+            double x[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) x[c] = 0.0;
+#pragma unroll 4
+            for (int r = i + 1 + t; r < m; r += CT) {
+                const double vr = vsm ? vs[r] : __ldcg(vs + r);
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (on[c]) x[c] = fma(vr, cj[c][r], x[c]);
+            }
+            block_sum_n<CB>(x, red);
+#pragma unroll
+            for (int c = 0; c < CB; ++c) f[c] = on[c] ? tau * (x[c] + cji0[c]) : 0.0;
+#pragma unroll 4
+            for (int r = i + 1 + t; r < m; r += CT) {
+                const double vr = vsm ? vs[r] : __ldcg(vs + r);
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (on[c]) cj[c][r] -= f[c] * vr;
+            }
+        }
+        if (t == 0) {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                s_redo[c] = 0;
+                if (!on[c]) continue;
+                double cji = cji0[c];
+                if (tau != 0.0) {
+                    cji -= f[c];
+                    cj[c][i] = cji;
+                }
+                const int phys = jb + c;
+                const double v1 = vn1[phys];
+                if (v1 == 0.0) continue;
+                double temp = fabs(cji) / v1;
+                temp = 1.0 - temp * temp;
+                temp = temp < 0.0 ? 0.0 : temp;
+                const double ratio = v1 / vn2[phys];
+                const double temp2 = temp * ratio * ratio;
+                if (temp2 <= TOL3Z) s_redo[c] = 1;
+                else vn1[phys] = v1 * sqrt(temp);
+            }
+        }
+        __syncthreads();  // the updated rows of this pass and the recompute flags
+        bool redo[CB], anyr = false;
+#pragma unroll
+        for (int c = 0; c < CB; ++c) { redo[c] = s_redo[c] != 0; anyr |= redo[c]; }
+        if (anyr) {
+            double x[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) x[c] = 0.0;
+#pragma unroll 4
+            for (int r = i + 1 + t; r < m; r += CT) {
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (redo[c]) x[c] = fma(cj[c][r], cj[c][r], x[c]);
+            }
+            block_sum_n<CB>(x, red);
+            if (t == 0)
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (redo[c]) {
+                        const double x2 = (i + 1 < m) ? sqrt(x[c]) : 0.0;
+                        vn1[jb + c] = x2;
+                        vn2[jb + c] = x2;
+                    }
+        }
+        __syncthreads();  // s_redo / red reused by the next pass
     }
 }
 
@@ -136,9 +293,14 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = CT / 32;
     const int c0 = lb * cpc, c1 = min(k, c0 + cpc);
     double *cols = SMEM ? sm : w.cols + (long long)c0 * ldw;
-    double *v = SMEM ? sm + (long long)cpc * ldw : nullptr;
-    int *pos2phys = reinterpret_cast<int *>(SMEM ? v + m : sm);
+    const bool vsm = !SMEM && d.vsm;
+    double *v = SMEM ? sm + (long long)cpc * ldw : (vsm ? sm : nullptr);
+    int *pos2phys = reinterpret_cast<int *>(SMEM ? v + m : (vsm ? sm + m : sm));
     int *posof = pos2phys + k;
+    // partial column norms of the owned columns in shared memory, indexed by the
+    // physical column (the pivot search and the downdates never leave the SM)
+    double *vn1 = reinterpret_cast<double *>(posof + k) - c0;
+    double *vn2 = vn1 + cpc;
     unsigned epoch = 0;
 
     for (long long e = t; e < (long long)m * (c1 - c0); e += CT) {
@@ -152,29 +314,48 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
         double s = 0.0;
         for (int r = lane; r < m; r += 32) s += cj[r] * cj[r];
         s = sqrt(warp_sum(s));
-        if (lane == 0) { w.vn1[c0 + j] = s; w.vn2[c0 + j] = s; }
+        if (lane == 0) { vn1[c0 + j] = s; vn2[c0 + j] = s; }
     }
     __syncthreads();
-    publish_candidate(w, posof, c0, c1, 0, lb, red, redp);
+    // one group barrier per column step when the reflector can be staged in shared
+    // memory: every CTA forms it from the published winning candidate column
+    // (shared-memory columns publish a copy of their candidate column; global-memory
+    // columns are read in place, and the owner writes the scaled reflector back into
+    // its column only after the next barrier, when every CTA has read it)
+    const bool onebar = nblk > 1 && (SMEM || vsm);
+    __shared__ int fast_s;
+    publish_candidate(w, vn1, posof, c0, c1, 0, lb, red, redp, 0, cols, ldw, m, onebar && SMEM);
     group_barrier(bar, nblk, epoch);
 
     const int kmin = m < k ? m : k;
+    int pend_c = -1, pend_i = 0;  // deferred reflector write-back (global columns)
+    double pend_beta = 0.0;
     for (int i = 0; i < kmin; ++i) {
+        const int par = i & 1;
+        if (!SMEM && pend_c >= 0) {  // v still holds step pend_i's reflector
+            double *ci = cols + (long long)(pend_c - c0) * ldw;
+            for (int r = pend_i + 1 + t; r < m; r += CT) ci[r] = v[r];
+            if (t == 0) ci[pend_i] = pend_beta;
+            pend_c = -1;
+            __syncthreads();
+        }
         // 1. pivot: first position j >= i with the largest vn1 (identical in every CTA),
         // reduced over the group's per-CTA candidates
         if (warp == 0) {
             double best = -1.0;
-            int bp = k;
+            int bp = k, bpc = -1;  // bpc: the column the winning CTA published
             for (int b = lane; b < nblk; b += 32) {
-                const double vv = __ldcg(w.cand_v + b);
-                const int pp = __ldcg(w.cand_p + b);
-                if (vv > best || (vv == best && pp < bp)) { best = vv; bp = pp; }
+                const double vv = __ldcg(w.cand_v + par * CQ_MAX + b);
+                const int pp = __ldcg(w.cand_p + par * CQ_MAX + b);
+                const int pcv = __ldcg(w.cand_pc + par * CQ_MAX + b);
+                if (vv > best || (vv == best && pp < bp)) { best = vv; bp = pp; bpc = pcv; }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, best, o);
                 const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+                const int oc = __shfl_xor_sync(0xffffffffu, bpc, o);
+                if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; bpc = oc; }
             }
             if (lane == 0) {
                 if (bp >= k) bp = i;  // NaN norms (failed upstream pivot): keep the order
@@ -182,85 +363,136 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
                 pos2phys[i] = cp; pos2phys[bp] = ci;
                 posof[cp] = i; posof[ci] = bp;
                 piv_s = cp;
+                // the owner published exactly this column as its candidate (else: the
+                // NaN fallback above -- take the two-barrier path for this step)
+                fast_s = onebar && bpc == cp;
             }
         }
         __syncthreads();
         const int pc = piv_s;
-        // 2. the owner of the pivot column forms and publishes the reflector (dlarfg)
-        if (pc >= c0 && pc < c1) {
-            double *ci = cols + (long long)(pc - c0) * ldw;
+        const bool fast = fast_s != 0;
+        double tau;
+        if (fast) {
+            // 2'. every CTA forms the reflector (dlarfg) from the published column, in
+            // the same order the owner would: identical tau / beta / v everywhere
+            const bool own = pc >= c0 && pc < c1;
+            const double *src = own ? cols + (long long)(pc - c0) * ldw
+                                : SMEM ? w.cand_col + ((long long)par * w.cq2 + pc / cpc) * ldw
+                                       : w.cols + (long long)pc * ldw;
+#pragma unroll 4
+            for (int r = i + t; r < m; r += CT) v[r] = own ? src[r] : __ldcg(src + r);
+            __syncthreads();
             double part = 0.0;
-            for (int r = i + 1 + t; r < m; r += CT) part += ci[r] * ci[r];
+            for (int r = i + 1 + t; r < m; r += CT) part += v[r] * v[r];
             const double xnorm = sqrt(block_sum(part, red));
-            const double alpha = ci[i];
-            double tau = 0.0, beta = alpha, scal = 0.0;
+            const double alpha = v[i];
+            double beta = alpha, scal = 0.0;
+            tau = 0.0;
             if (xnorm != 0.0) {
                 beta = -copysign(hypot(alpha, xnorm), alpha);
                 tau = (beta - alpha) / beta;
                 scal = 1.0 / (alpha - beta);
             }
-            __syncthreads();
+            double *ci = (own && SMEM) ? cols + (long long)(pc - c0) * ldw : nullptr;
             for (int r = i + 1 + t; r < m; r += CT) {
-                const double x = (xnorm != 0.0) ? ci[r] * scal : ci[r];
-                ci[r] = x;
-                if (nblk > 1) w.vbuf[r] = x;
+                const double x = (xnorm != 0.0) ? v[r] * scal : v[r];
+                v[r] = x;
+                if (ci) ci[r] = x;
             }
-            if (t == 0) {
-                ci[i] = beta;
+            if (own && t == 0) {
+                if (ci) ci[i] = beta;
                 w.tau[i] = tau;
                 w.diagR[i] = beta;
             }
-        }
-        group_barrier(bar, nblk, epoch);
-        // 3. apply H_i^T to the unchosen owned columns, downdate their norms
-        const double tau = __ldcg(w.tau + i);
-        const double *vsrc;
-        if (nblk == 1) {
-            vsrc = cols + (long long)(pc - c0) * ldw;  // the reflector lives in this CTA
-        } else if (SMEM) {
-            for (int r = i + 1 + t; r < m; r += CT) v[r] = __ldcg(w.vbuf + r);
+            if (own && !SMEM) { pend_c = pc; pend_i = i; pend_beta = beta; }
             __syncthreads();
-            vsrc = v;
         } else {
-            vsrc = w.vbuf;
+            // 2. the owner of the pivot column forms and publishes the reflector (dlarfg)
+            if (pc >= c0 && pc < c1) {
+                double *ci = cols + (long long)(pc - c0) * ldw;
+                double part = 0.0;
+                for (int r = i + 1 + t; r < m; r += CT) part += ci[r] * ci[r];
+                const double xnorm = sqrt(block_sum(part, red));
+                const double alpha = ci[i];
+                double tau0 = 0.0, beta = alpha, scal = 0.0;
+                if (xnorm != 0.0) {
+                    beta = -copysign(hypot(alpha, xnorm), alpha);
+                    tau0 = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+                __syncthreads();
+                for (int r = i + 1 + t; r < m; r += CT) {
+                    const double x = (xnorm != 0.0) ? ci[r] * scal : ci[r];
+                    ci[r] = x;
+                    if (nblk > 1) w.vbuf[r] = x;
+                }
+                if (t == 0) {
+                    ci[i] = beta;
+                    w.tau[i] = tau0;
+                    w.diagR[i] = beta;
+                }
+            }
+            group_barrier(bar, nblk, epoch);
+            tau = __ldcg(w.tau + i);
+            if (nblk > 1 && (SMEM || vsm)) {
+                for (int r = i + 1 + t; r < m; r += CT) v[r] = __ldcg(w.vbuf + r);
+                __syncthreads();
+            }
         }
+        // 3. apply H_i^T to the unchosen owned columns, downdate their norms
+        if (!SMEM && nblk > 1) {
+            // global-memory columns: the whole CTA works on its columns together
+            // (rows spread over all threads, CB columns per pass, block reductions),
+            // so every step keeps ~CT x CB independent L2 loads in flight instead of
+            // one warp walking one column serially through L2
+            coop_update(vn1, vn2, cols, vsm ? v : w.vbuf, vsm, posof, c0, c1, i, m, ldw, tau, red);
+        } else {
+        const double *vsrc = (nblk == 1) ? cols + (long long)(pc - c0) * ldw  // the reflector lives in this CTA
+                                         : v;
         for (int j = warp; j < c1 - c0; j += nw) {
             const int phys = c0 + j;
             if (posof[phys] <= i) continue;
             double *cj = cols + (long long)j * ldw;
             if (tau != 0.0) {
                 double s = 0.0;
-                for (int r = i + 1 + lane; r < m; r += 32) s += ((SMEM || nblk == 1) ? vsrc[r] : __ldcg(vsrc + r)) * cj[r];
+                for (int r = i + 1 + lane; r < m; r += 32) s += vsrc[r] * cj[r];
                 s = warp_sum(s) + cj[i];
                 const double f = tau * s;
-                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * ((SMEM || nblk == 1) ? vsrc[r] : __ldcg(vsrc + r));
+                for (int r = i + 1 + lane; r < m; r += 32) cj[r] -= f * vsrc[r];
                 __syncwarp();
                 if (lane == 0) cj[i] -= f;
                 __syncwarp();
             }
-            const double v1 = w.vn1[phys];
+            const double v1 = vn1[phys];
             if (v1 != 0.0) {
                 double temp = fabs(cj[i]) / v1;
                 temp = 1.0 - temp * temp;
                 temp = temp < 0.0 ? 0.0 : temp;
-                const double ratio = v1 / w.vn2[phys];
+                const double ratio = v1 / vn2[phys];
                 const double temp2 = temp * ratio * ratio;
                 if (temp2 <= TOL3Z) {
                     double s = 0.0;
                     for (int r = i + 1 + lane; r < m; r += 32) s += cj[r] * cj[r];
                     s = (i + 1 < m) ? sqrt(warp_sum(s)) : 0.0;
-                    if (lane == 0) { w.vn1[phys] = s; w.vn2[phys] = s; }
+                    if (lane == 0) { vn1[phys] = s; vn2[phys] = s; }
                 } else if (lane == 0) {
-                    w.vn1[phys] = v1 * sqrt(temp);
+                    vn1[phys] = v1 * sqrt(temp);
                 }
             }
             __syncwarp();
         }
+        }
         if (i + 1 < kmin) {
             __syncthreads();
-            publish_candidate(w, posof, c0, c1, i + 1, lb, red, redp);
+            publish_candidate(w, vn1, posof, c0, c1, i + 1, lb, red, redp, par ^ 1, cols, ldw, m, onebar && SMEM);
         }
         group_barrier(bar, nblk, epoch);
+    }
+    if (!SMEM && pend_c >= 0) {  // the last deferred reflector
+        double *ci = cols + (long long)(pend_c - c0) * ldw;
+        for (int r = pend_i + 1 + t; r < m; r += CT) ci[r] = v[r];
+        if (t == 0) ci[pend_i] = pend_beta;
+        __syncthreads();
     }
     // spill the owned columns (reflectors) for the Q kernel; publish the permutation
     if (SMEM)
@@ -661,8 +893,17 @@ struct TArgs {
     int kmin[MAXM];
 };
 
-// dlarft (forward, columnwise): T[i][i] = tau_i, T[0:i, i] = -tau_i T[0:i,0:i] G[0:i, i]
-__global__ void larft_kernel(const __grid_constant__ TArgs a) {
+// dlarft (forward, columnwise) for one QB = 64 block: the T of I - V T V^T.
+// Blocked: the four 16-column diagonal blocks run the column recurrence
+// T[0:i, i] = -tau_i T[0:i, 0:i] G[0:i, i] concurrently (one warp each), then the
+// off-diagonal blocks are joined pairwise, T12 = -T11 (G12 T22) (the product of two
+// compact-WY blocks: (I - V1 T11 V1^T)(I - V2 T22 V2^T)), 16 -> 32 -> 64.
+// G = V^T V (QB x QB).  One shared array holds T in its upper triangle and G's
+// strict upper triangle transposed into its strict lower triangle (M[y][x] = G[x][y],
+// x < y); one CTA of 256 threads per matrix.
+__global__ void __launch_bounds__(256) larft_kernel(const __grid_constant__ TArgs a) {
+    __shared__ double M[QB][QB + 1];
+    __shared__ double X[QB * QB / 4];  // G12 T22 of the pairs being joined
     const int g = blockIdx.x;
     const int j0 = a.b * QB;
     const int nb = min(QB, a.kmin[g] - j0);
@@ -671,17 +912,55 @@ __global__ void larft_kernel(const __grid_constant__ TArgs a) {
     const double *G = a.G[g];
     const double *tau = a.tau[g] + j0;
     const int t = threadIdx.x;
-    for (int e = t; e < QB * QB; e += blockDim.x) T[e] = 0.0;
+    for (int e = t; e < QB * QB; e += blockDim.x) {
+        const int r = e / QB, c = e % QB;
+        M[r][c] = (r > c && r < nb) ? G[c * QB + r] : 0.0;
+    }
     __syncthreads();
-    for (int i = 0; i < nb; ++i) {
-        // row r < i of column i: -tau_i * sum_{l=r}^{i-1} T[r][l] G[l][i]
-        if (t < i) {
+    // 1. diagonal 16-blocks, one warp each (lane = row within the block)
+    constexpr int L = 16;
+    {
+        const int blk = t >> 5, r = t & 31;
+        const int b0 = blk * L;
+        if (blk < QB / L)
+            for (int i = 0; i < L; ++i) {
+                const int ci = b0 + i;
+                if (ci < nb) {
+                    if (r < i) {
+                        double s = 0.0;
+                        for (int l = r; l < i; ++l) s += M[b0 + r][b0 + l] * M[ci][b0 + l];
+                        M[b0 + r][ci] = -tau[ci] * s;
+                    }
+                    if (r == i) M[ci][ci] = tau[ci];
+                }
+                __syncwarp();
+            }
+    }
+    __syncthreads();
+    // 2. join: block size h = 16, then 32; pair p has T11 at b0 = 2hp, T22 at b1 = b0 + h
+    for (int h = L; h < QB; h *= 2) {
+        const int work = (QB / (2 * h)) * h * h;
+        for (int e = t; e < work; e += blockDim.x) {  // X = G12 T22
+            const int pr = e / (h * h), r = (e / h) % h, c = e % h;
+            const int b0 = pr * 2 * h, b1 = b0 + h;
             double s = 0.0;
-            for (int l = t; l < i; ++l) s += T[t * QB + l] * G[l * QB + i];
-            T[t * QB + i] = -tau[i] * s;
+            for (int l = 0; l <= c; ++l) s += M[b1 + l][b0 + r] * M[b1 + l][b1 + c];
+            X[e] = s;
         }
-        if (t == 0) T[i * QB + i] = tau[i];
         __syncthreads();
+        for (int e = t; e < work; e += blockDim.x) {  // T12 = -T11 X
+            const int pr = e / (h * h), r = (e / h) % h, c = e % h;
+            const int b0 = pr * 2 * h, b1 = b0 + h;
+            const double *Xp = X + pr * h * h;
+            double s = 0.0;
+            for (int l = r; l < h; ++l) s += M[b0 + r][b0 + l] * Xp[l * h + c];
+            M[b0 + r][b1 + c] = -s;
+        }
+        __syncthreads();
+    }
+    for (int e = t; e < QB * QB; e += blockDim.x) {
+        const int r = e / QB, c = e % QB;
+        T[e] = (r <= c && c < nb) ? M[r][c] : 0.0;
     }
 }
 
@@ -710,7 +989,7 @@ __global__ void rank_kernel(const __grid_constant__ RankArgs a) {
 
 inline size_t smem_for(int m, int k, int cpc) {
     const size_t ldw = (size_t)(m | 1);
-    return (size_t)cpc * ldw * 8 + (size_t)m * 8 + sizeof(int) * 2 * (size_t)k;
+    return (size_t)cpc * ldw * 8 + (size_t)m * 8 + sizeof(int) * 2 * (size_t)k + 16 * (size_t)cpc;
 }
 
 }  // namespace
@@ -720,7 +999,10 @@ long long rsc_qrcp_coop_doubles(int m, int k) {
     const long long ldw = m | 1;
     const long long kmin = m < k ? m : k;
     // factorization | explicit V (m x kmin) | W_b (QB x kmin) | Gram, T (QB x QB each)
-    return ldw * k + 4LL * k + m + k + 2 * CQ_MAX + 64 + (long long)m * kmin + QB * kmin + 2LL * QB * QB + 64;
+    static_assert(QB == QB_WY, "candidate region offset assumes the WY block size");
+    (void)kmin;
+    // ... then the double-buffered pivot candidates and candidate columns
+    return coop_cand_base(m, k) + 4LL * CQ_MAX + 2LL * (k < CQ_MAX ? k : CQ_MAX) * ldw;
 }
 
 static inline double *wy_base(double *W, int m, int k) {
@@ -809,7 +1091,7 @@ static int form_q_blocked(int cnt, const MatDesc *ds, cudaStream_t s) {
         if (pg.empty()) continue;
         int rc = rsc_gemm_grouped(1, 0, pg.data(), (int)pg.size(), s);
         if (rc) return rc;
-        larft_kernel<<<cnt, 64, 0, s>>>(ta);
+        larft_kernel<<<cnt, 256, 0, s>>>(ta);
         RSC_CHECK_LAUNCH();
         if ((rc = rsc_gemm_grouped(1, 0, pw.data(), (int)pw.size(), s))) return rc;
         if ((rc = rsc_gemm_grouped(0, 0, pt.data(), (int)pt.size(), s))) return rc;
@@ -830,7 +1112,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(mqrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
-        cudaFuncSetAttribute(mqrcp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        cudaFuncSetAttribute(mqrcp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
         cudaFuncSetAttribute(mq_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET);
         attr = true;
     }
@@ -841,7 +1123,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
         const int i = ids[t];
         if (m[i] <= 0 || k[i] <= 0) continue;
         const size_t fixed = (size_t)m[i] * 8 + sizeof(int) * 2 * (size_t)k[i];
-        const size_t per_col = (size_t)(m[i] | 1) * 8;
+        const size_t per_col = (size_t)(m[i] | 1) * 8 + 16;  // column + its two partial norms
         int cpc = fixed < SMEM_BUDGET ? (int)((SMEM_BUDGET - fixed) / per_col) : 0;
         if (cpc >= 1) {
             cpc = std::min(cpc, k[i]);
@@ -852,7 +1134,10 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
             }
         }
         cpc = (k[i] + nsm - 1) / nsm;  // global-memory columns, one group over all SMs
-        plans.push_back({i, cpc, (k[i] + cpc - 1) / cpc, false, sizeof(int) * 2 * (size_t)k[i]});
+        // the reflector is staged in shared memory when it fits (vsm)
+        const size_t base = sizeof(int) * 2 * (size_t)k[i] + 16 * (size_t)cpc;
+        const size_t gsm = (size_t)m[i] * 8 + base;
+        plans.push_back({i, cpc, (k[i] + cpc - 1) / cpc, false, gsm <= SMEM_BUDGET ? gsm : base});
     }
     // sketches that fit one thread-block cluster: cluster kernel (DSMEM + hardware
     // cluster barriers); the rest stays on the cooperative kernel
@@ -902,12 +1187,26 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
                     cfg.dynamicSmemBytes = smb;
                     cfg.attrs = at;
                     cfg.numAttrs = 1;
+                    // occupancy queries cost tens of microseconds of host time: memoized
+                    // per (cluster size, shared memory bytes)
+                    static std::map<std::pair<int, size_t>, int> occ_cl;
+                    static std::mutex occ_mu;
                     int ncl = 0;
-                    if (cudaOccupancyMaxActiveClusters(&ncl, (void *)qrcp_cluster_kernel<false, 0>, &cfg) != cudaSuccess ||
-                        ncl < 1) {
-                        cudaGetLastError();
-                        continue;
+                    {
+                        std::lock_guard<std::mutex> lk(occ_mu);
+                        auto it = occ_cl.find({C, smb});
+                        if (it != occ_cl.end()) {
+                            ncl = it->second;
+                        } else {
+                            if (cudaOccupancyMaxActiveClusters(&ncl, (void *)qrcp_cluster_kernel<false, 0>, &cfg) !=
+                                cudaSuccess) {
+                                cudaGetLastError();
+                                ncl = 0;
+                            }
+                            occ_cl[{C, smb}] = ncl;
+                        }
                     }
+                    if (ncl < 1) continue;
                     cl_list.push_back({C, (int)pi});
                     cl_sm[pi] = smb;
                     done[pi] = 1;
@@ -985,9 +1284,20 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
             size_t start = pos;
             while (pos < sel.size() && cnt < MAXM) {
                 const size_t sm2 = std::max(sm, sel[pos].sm);
+                static std::map<std::pair<int, size_t>, int> occ_b;
+                static std::mutex occ_bmu;
                 int per_sm = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                    &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, CT, sm2);
+                {
+                    std::lock_guard<std::mutex> lk(occ_bmu);
+                    auto it = occ_b.find({(int)smem, sm2});
+                    if (it != occ_b.end()) {
+                        per_sm = it->second;
+                    } else {
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                            &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, CT, sm2);
+                        occ_b[{(int)smem, sm2}] = per_sm;
+                    }
+                }
                 if (per_sm < 1) return 77;
                 if (cnt > 0 && blocks + sel[pos].nblk > nsm * per_sm) break;
                 sm = sm2;
@@ -1007,6 +1317,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
                 d.rank = rank_dev + i;
                 d.m = m[i]; d.k = k[i]; d.ldg = ldg[i]; d.ldq = ldq[i]; d.ldw = m[i] | 1;
                 d.cpc = p.cpc; d.nblk = p.nblk; d.blk0 = b0;
+                d.vsm = !smem && p.sm > sizeof(int) * 2 * (size_t)k[i] + 16 * (size_t)p.cpc;
                 b0 += p.nblk;
             }
             // distinct barrier counter per matrix of this launch

@@ -47,6 +47,84 @@ int rsc_sym_etree(long long n, const long long *col_ptr, const long long *row_id
     return 0;
 }
 
+// The same elimination tree with the rows of nr disjoint column ranges (ND
+// subtrees: an entry (i, j), j < i, with j inside a range has i inside it or in no
+// range) processed on host threads first, each range's own row lists transposed
+// locally; the remaining rows follow in ascending order.  Liu's row sweep gives the
+// unique etree in any processing order that keeps each row's ancestors current, and
+// a range's walks only touch its own columns.  Returns 1 (parent untouched) when the
+// ranges are not closed, so the caller can fall back.
+int rsc_sym_etree_par(long long n, const long long *col_ptr, const long long *row_idx, long long nr,
+                      const long long *ranges, long long *parent) {
+    if (n < 0) return -1;
+    if (!col_ptr || !row_idx || !parent) return -2;
+    std::vector<int> rng(n, -1);
+    for (long long r = 0; r < nr; ++r)
+        for (long long c = ranges[2 * r]; c < ranges[2 * r + 1]; ++c) rng[c] = (int)r;
+    std::vector<long long> anc(n, -1);
+    for (long long i = 0; i < n; ++i) parent[i] = -1;
+    auto walk = [&](long long i, long long j) {
+        while (true) {
+            const long long a = anc[j];
+            anc[j] = i;
+            if (a == -1) { parent[j] = i; break; }
+            if (a == i) break;
+            j = a;
+        }
+    };
+    std::atomic<bool> bad{false};
+    {
+        std::atomic<long long> next{0};
+        const int T = std::max(1, std::min<int>(rsc_host_threads(), (int)nr));
+        std::vector<std::thread> th;
+        for (int w = 0; w < T; ++w)
+            th.emplace_back([&] {
+                std::vector<long long> cnt, cols;
+                for (long long r; (r = next.fetch_add(1)) < nr;) {
+                    const long long lo = ranges[2 * r], hi = ranges[2 * r + 1];
+                    cnt.assign(hi - lo + 1, 0);
+                    for (long long j = lo; j < hi; ++j)
+                        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+                            const long long i = row_idx[p];
+                            if (i <= j) continue;
+                            if (i < hi) cnt[i - lo + 1]++;
+                            else if (rng[i] >= 0) bad = true;  // reaches another range
+                        }
+                    for (long long q = 0; q < hi - lo; ++q) cnt[q + 1] += cnt[q];
+                    cols.resize(cnt[hi - lo]);
+                    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+                    for (long long j = lo; j < hi; ++j)
+                        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+                            const long long i = row_idx[p];
+                            if (i > j && i < hi) cols[pos[i - lo]++] = j;
+                        }
+                    for (long long i = lo; i < hi; ++i)
+                        for (long long q = cnt[i - lo]; q < cnt[i - lo + 1]; ++q) walk(i, cols[q]);
+                }
+            });
+        for (auto &x : th) x.join();
+    }
+    if (bad) return 1;
+    // rows outside every range, ascending: their (strict lower) entries from all columns
+    std::vector<long long> cnt(n + 1, 0);
+    for (long long j = 0; j < n; ++j)
+        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            const long long i = row_idx[p];
+            if (i > j && rng[i] < 0) cnt[i + 1]++;
+        }
+    for (long long i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::vector<long long> pos(cnt.begin(), cnt.end() - 1), cols(cnt[n]);
+    for (long long j = 0; j < n; ++j)
+        for (long long p = col_ptr[j]; p < col_ptr[j + 1]; ++p) {
+            const long long i = row_idx[p];
+            if (i > j && rng[i] < 0) cols[pos[i]++] = j;
+        }
+    for (long long i = 0; i < n; ++i)
+        if (rng[i] < 0)
+            for (long long q = cnt[i]; q < cnt[i + 1]; ++q) walk(i, cols[q]);
+    return 0;
+}
+
 // postorder of the forest, children visited in ascending index, roots ascending
 int rsc_sym_postorder(long long n, const long long *parent, long long *post) {
     if (n < 0) return -1;

@@ -164,6 +164,14 @@ def gemm_problems(n):
     return np.zeros(n, dtype=GEMM_DTYPE)
 
 
+def gcat(parts):
+    """Concatenate GEMM_DTYPE problem arrays through byte views (np.concatenate on
+    structured arrays runs numpy's field promotion per call: ~20x slower)."""
+    if len(parts) == 1:
+        return parts[0]
+    return np.concatenate([np.ascontiguousarray(q).view(np.uint8) for q in parts]).view(GEMM_DTYPE)
+
+
 class KernelProfile:
     """Optional CUDA-event timing of every grouped-GEMM launch (bench.py roofline):
     records (start, end, flops) with flops = sum of 2 M N K * batch of the launch."""

@@ -406,41 +406,63 @@ class LevelPass(NumericPass):
                 blocks.append((A_RC, R.size, nc))
         dense = self._dense_many(blocks)
         out = []
-        probs = []
+        # every (node, source) pair of the batch in one set of flat arrays; problems
+        # of different targets may interleave (the ordered reduction groups them by
+        # target and keeps each target's sources in reference order)
+        cols = {k: [] for k in ("s", "lo", "hi", "nrd", "nro", "cpos", "rpos")}
+        per = {k: [] for k in ("ud", "uo", "nc", "nr", "cnt")}
         for (node, wd, wo), (iD, iO) in zip(items, layout):
             UD = dense[iD] if iD is not None else None
             UO = dense[iO] if iO is not None else None
             out.append((UD, UO))
-            nc = node.ncols
-            t = self._pairs(node.j, need_rd=True)
-            if t["s"].size == 0:
+            t = self.np.tarr[node.j]
+            for k in cols:
+                cols[k].append(t[k])
+            per["ud"].append(UD.data_ptr() if UD is not None else 0)
+            per["uo"].append(UO.data_ptr() if UO is not None else 0)
+            per["nc"].append(node.ncols)
+            per["nr"].append(UO.shape[0] if UO is not None else 0)
+            per["cnt"].append(t["s"].size)
+        if not items or sum(per["cnt"]) == 0:
+            self._reduce([t for pair in out for t in pair])
+            return out
+        c = {k: np.concatenate(v) for k, v in cols.items()}
+        cnt = np.asarray(per["cnt"], dtype=np.int64)
+        ud = np.repeat(np.asarray(per["ud"], dtype=np.uint64), cnt)
+        uo = np.repeat(np.asarray(per["uo"], dtype=np.uint64), cnt)
+        nc = np.repeat(np.asarray(per["nc"], dtype=np.int64), cnt)
+        nr = np.repeat(np.asarray(per["nr"], dtype=np.int64), cnt)
+        s_ = c["s"]
+        w, ld = self.s_w[s_], self.s_ld[s_]
+        base = (w > 0) & (c["nrd"] > 0) & self._mine(s_)
+        cpos = self.idx_base + (4 * c["cpos"]).astype(np.uint64)
+        Qp = self.s_raw[s_] + (8 * c["lo"] * ld).astype(np.uint64)
+        probs = []
+        for which in ("ud", "uo"):
+            tgt = ud if which == "ud" else uo
+            sel = base & (tgt != 0)
+            if which == "uo":
+                sel &= c["nro"] > 0
+            n = int(sel.sum())
+            if n == 0:
                 continue
-            s = t["s"]
-            w, ld = self.s_w[s], self.s_ld[s]
-            cpos = self.idx_base + (4 * t["cpos"]).astype(np.uint64)
-            Qp = self.s_raw[s] + (8 * t["lo"] * ld).astype(np.uint64)
-            for tgt, rows_sel in ((UD, None), (UO, "ro")):
-                if tgt is None:
-                    continue
-                sel = np.ones(s.size, dtype=bool) if rows_sel is None else t["nro"] > 0
-                if not sel.any():
-                    continue
-                p = np.zeros(int(sel.sum()), dtype=GEMM_DTYPE)
-                row0 = t["lo"] if rows_sel is None else t["hi"]
-                p["A"] = self.s_eff[s][sel] + (8 * row0[sel] * ld[sel]).astype(np.uint64)
-                p["lda"], p["ldb"] = ld[sel], ld[sel]
-                p["B"], p["C"], p["ldc"] = Qp[sel], tgt.data_ptr(), nc
-                p["M"] = t["nrd"][sel] if rows_sel is None else t["nro"][sel]
-                p["N"], p["K"] = t["nrd"][sel], w[sel]
-                p["c_rows"] = cpos[sel] if rows_sel is None else (
-                    self.idx_base + (4 * t["rpos"][sel]).astype(np.uint64))
-                p["c_cols"] = cpos[sel]
-                p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
-                p["ext_r"], p["ext_c"] = tgt.shape
-                self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s][sel])
-                probs.append(p[self._mine(s[sel])])
+            p = np.zeros(n, dtype=GEMM_DTYPE)
+            row0 = c["lo"] if which == "ud" else c["hi"]
+            ldk = ld[sel]
+            p["A"] = self.s_eff[s_[sel]] + (8 * row0[sel] * ldk).astype(np.uint64)
+            p["lda"], p["ldb"] = ldk, ldk
+            p["B"], p["C"], p["ldc"] = Qp[sel], tgt[sel], nc[sel]
+            p["M"] = c["nrd"][sel] if which == "ud" else c["nro"][sel]
+            p["N"], p["K"] = c["nrd"][sel], w[sel]
+            p["c_rows"] = cpos[sel] if which == "ud" else self.idx_base + (4 * c["rpos"][sel]).astype(np.uint64)
+            p["c_cols"] = cpos[sel]
+            p["batch"], p["atomic"], p["alpha"], p["beta"] = 1, 1, -1.0, 1.0
+            p["ext_r"] = nc[sel] if which == "ud" else nr[sel]
+            p["ext_c"] = nc[sel]
+            self._wflops(2.0 * p["M"] * p["N"], w=p["K"], wbase=self.s_raw[s_[sel]])
+            probs.append(p)
         if probs:
-            P = np.concatenate(probs)
+            P = E.gcat(probs)
             if P.size:
                 E.gemm_grouped(E.balance_k(P, False, True), False, True)
         self._reduce([t for pair in out for t in pair])
@@ -608,7 +630,7 @@ class LevelPass(NumericPass):
                 bases.append(np.array([pt[0] for pt in path], dtype=np.uint64))
                 keeps.append(np.full(len(path), self._lead()))
         if parts:
-            P = np.concatenate(parts)
+            P = E.gcat(parts)
             P["batch"], P["atomic"], P["alpha"], P["beta"] = 1, 1, -1.0, 1.0
             self._wflops(2.0 * P["M"] * P["N"], w=P["K"], wbase=np.concatenate(bases))
             P = P[np.concatenate(keeps)]
@@ -650,7 +672,10 @@ class LevelPass(NumericPass):
         if sol:
             diag_solve_many(sol, self.S.empty)
         self._spmm_many(spm)
-        p1s, p2s = [], []
+        # all source-window and root-path terms of all blocks as two flat problem sets
+        # (per block: its pairs in reference order, then its path terms)
+        acc = {k: [] for k in ("ld", "w", "base", "raw_c", "eff_r", "nc", "nr", "cidx", "ridx", "keep")}
+        per = []  # (count, r, src ptr, ld src, W ptr, ld W, W rows, W cols, price)
         for (node, s), src, W in zip(items, srcs, Ws):
             tree = node.diag
             (r0, r1), (c0, c1) = tree.shape.span(s)
@@ -660,52 +685,62 @@ class LevelPass(NumericPass):
             t = self._tmaps(node.j, s)
             sid = t["s"]
             ld = self.s_ld[sid]
-            w = self.s_w[sid]
-            base = self.s_raw[sid]
-            raw_c = self.s_raw[sid] + (8 * t["clo"] * ld).astype(np.uint64)
-            eff_r = self.s_eff[sid] + (8 * t["rlo"] * ld).astype(np.uint64)
-            nc_, nr_ = t["chi"] - t["clo"], t["rhi"] - t["rlo"]
-            cidx = self.idx_base + (4 * t["cidx"]).astype(np.uint64)
-            ridx = self.idx_base + (4 * t["ridx"]).astype(np.uint64)
             path = self._path_probs(tree, s, (r0, r1), (c0, c1))
+            acc["ld"].append(ld)
+            acc["w"].append(self.s_w[sid])
+            acc["base"].append(self.s_raw[sid])
+            acc["raw_c"].append(self.s_raw[sid] + (8 * t["clo"] * ld).astype(np.uint64))
+            acc["eff_r"].append(self.s_eff[sid] + (8 * t["rlo"] * ld).astype(np.uint64))
+            acc["nc"].append(t["chi"] - t["clo"])
+            acc["nr"].append(t["rhi"] - t["rlo"])
+            acc["cidx"].append(self.idx_base + (4 * t["cidx"]).astype(np.uint64))
+            acc["ridx"].append(self.idx_base + (4 * t["ridx"]).astype(np.uint64))
+            acc["keep"].append(self._mine(sid))
             if path:
-                pa = np.array(path, dtype=np.int64)
                 # (raw, eff, ld, w, row lo, row hi, col lo, col hi), window-aligned, no index maps
-                ld = np.concatenate([ld, pa[:, 2]])
-                w = np.concatenate([w, pa[:, 3]])
-                base = np.concatenate([base, pa[:, 0].astype(np.uint64)])
-                raw_c = np.concatenate([raw_c, (pa[:, 0] + 8 * pa[:, 6] * pa[:, 2]).astype(np.uint64)])
-                eff_r = np.concatenate([eff_r, (pa[:, 1] + 8 * pa[:, 4] * pa[:, 2]).astype(np.uint64)])
-                nc_ = np.concatenate([nc_, pa[:, 7] - pa[:, 6]])
-                nr_ = np.concatenate([nr_, pa[:, 5] - pa[:, 4]])
-                cidx = np.concatenate([cidx, np.zeros(len(path), np.uint64)])
-                ridx = np.concatenate([ridx, np.zeros(len(path), np.uint64)])
-            n = w.size
-            if n == 0:
-                continue
-            keep = np.concatenate([self._mine(sid), np.full(n - sid.size, self._lead())])
-            tsz = w * r
-            toff = np.concatenate([[0], np.cumsum(tsz)[:-1]])
+                pa = np.array(path, dtype=np.int64)
+                acc["ld"].append(pa[:, 2])
+                acc["w"].append(pa[:, 3])
+                acc["base"].append(pa[:, 0].astype(np.uint64))
+                acc["raw_c"].append((pa[:, 0] + 8 * pa[:, 6] * pa[:, 2]).astype(np.uint64))
+                acc["eff_r"].append((pa[:, 1] + 8 * pa[:, 4] * pa[:, 2]).astype(np.uint64))
+                acc["nc"].append(pa[:, 7] - pa[:, 6])
+                acc["nr"].append(pa[:, 5] - pa[:, 4])
+                acc["cidx"].append(np.zeros(len(path), np.uint64))
+                acc["ridx"].append(np.zeros(len(path), np.uint64))
+                acc["keep"].append(np.full(len(path), self._lead()))
+            n = sid.size + len(path)
+            if n:
+                per.append((n, r, src.data_ptr(), E.ld(src), W.data_ptr(), E.ld(W), W.shape[0], W.shape[1],
+                            self._price.get(src.data_ptr(), 0)))
+        if per:
+            c = {k: np.concatenate(v) for k, v in acc.items()}
+            cnt = np.array([x[0] for x in per], dtype=np.int64)
+            rep = lambda i, dt=np.int64: np.repeat(np.array([x[i] for x in per], dtype=dt), cnt)
+            r_, sp, sld = rep(1), rep(2, np.uint64), rep(3)
+            wp, wld, wr, wc = rep(4, np.uint64), rep(5), rep(6), rep(7)
+            w, ld = c["w"], c["ld"]
+            tsz = w * r_
+            toff = np.cumsum(tsz) - tsz
             T = self.S.zeros(int(tsz.sum()))  # p1 accumulates into it (K may be split)
             tp = np.uint64(T.data_ptr()) + (8 * toff).astype(np.uint64)
+            n = w.size
             p1 = np.zeros(n, dtype=GEMM_DTYPE)
             p2 = np.zeros(n, dtype=GEMM_DTYPE)
-            p1["lda"], p1["M"], p1["N"], p1["C"], p1["ldc"] = ld, w, r, tp, r
-            p1["B"], p1["ldb"] = src.data_ptr(), E.ld(src)
-            p2["lda"], p2["K"], p2["N"], p2["B"], p2["ldb"] = ld, w, r, tp, r
-            p2["C"], p2["ldc"] = W.data_ptr(), E.ld(W)
-            p2["ext_r"], p2["ext_c"] = W.shape
+            p1["lda"], p1["M"], p1["N"], p1["C"], p1["ldc"] = ld, w, r_, tp, r_
+            p1["B"], p1["ldb"] = sp, sld
+            p2["lda"], p2["K"], p2["N"], p2["B"], p2["ldb"] = ld, w, r_, tp, r_
+            p2["C"], p2["ldc"] = wp, wld
+            p2["ext_r"], p2["ext_c"] = wr, wc
             if not transpose:  # T = V[cwin]^T G1[cidx] ; W[ridx] -= E[rwin] T
-                p1["A"], p1["K"], p1["b_rows"] = raw_c, nc_, cidx
-                p2["A"], p2["M"], p2["c_rows"] = eff_r, nr_, ridx
+                p1["A"], p1["K"], p1["b_rows"] = c["raw_c"], c["nc"], c["cidx"]
+                p2["A"], p2["M"], p2["c_rows"] = c["eff_r"], c["nr"], c["ridx"]
             else:  # T = E[rwin]^T G[ridx] ; W[cidx] -= V[cwin] T
-                p1["A"], p1["K"], p1["b_rows"] = eff_r, nr_, ridx
-                p2["A"], p2["M"], p2["c_rows"] = raw_c, nc_, cidx
-            self._wflops(2.0 * (nc_ + nr_), w=w, wbase=base, r=r, rbase=self._price.get(src.data_ptr(), 0))
-            p1s.append(p1[keep])
-            p2s.append(p2[keep])
-        if p1s:
-            P1, P2 = np.concatenate(p1s), np.concatenate(p2s)
+                p1["A"], p1["K"], p1["b_rows"] = c["eff_r"], c["nr"], c["ridx"]
+                p2["A"], p2["M"], p2["c_rows"] = c["raw_c"], c["nc"], c["cidx"]
+            self._wflops(2.0 * (c["nc"] + c["nr"]), w=w, wbase=c["base"], r=r_, rbase=rep(8, np.uint64))
+            keep = c["keep"]
+            P1, P2 = p1[keep], p2[keep]
             P1["batch"], P1["alpha"] = 1, 1.0
             P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
             P1["atomic"] = 1  # T is zeroed: P1 accumulates, so its tall K may be split

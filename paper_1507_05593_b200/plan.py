@@ -224,6 +224,9 @@ class NumericPlan:
         self.node_blocks = {}      # node j -> (A_CC, A_RC, A_CR)
         self.rows_off = {}         # node j / ("int", u) -> index offset of its row set
         self.interior = []         # (unit index, members, c0, c1, off_rows, A_off csr, A_BB csr)
+        # every row structure R_j enters the index pool once, as one chunk
+        R_ptr, R_all = _rows_flat(part)
+        rows_base = self.idx.add(R_all[:int(R_ptr[-1])])
         for u, (kind, payload) in enumerate(sym.units):
             if kind == "interior":
                 ids = payload
@@ -253,7 +256,7 @@ class NumericPlan:
             A_RC = self.csr.add(R, (c0, c1)) if R.size else None
             A_CR = self.csr.add((c0, c1), R) if R.size else None  # full[R, C]^T (symmetric)
             self.node_blocks[j] = (A_CC, A_RC, A_CR)
-            self.rows_off[j] = self.idx.add(R)
+            self.rows_off[j] = rows_base + int(R_ptr[j])
             if R.size:
                 sid = len(self.sources)
                 self.sources.append(Source(sid, "node", u, R, c0, c1))
@@ -472,6 +475,9 @@ class _TargetPairs:
 
     def __contains__(self, j):
         return j in self._tarr
+
+    def get(self, j, default=None):
+        return self[j] if j in self._tarr else default
 
     def __iter__(self):
         return iter(self._tarr)

@@ -331,13 +331,17 @@ def _nd_geometric_native(d):
     """The geometric recursion in one C++ call (rsc_nd_geometric, subtrees on host
     threads); the same order and tree as _Dissector.dissect."""
     n = d.n
-    cap = 2 * n + 1
     order = np.empty(n, dtype=np.int64)
-    nodes = np.empty((6, cap), dtype=np.int64)
     root = np.zeros(1, dtype=np.int64)
-    cnt = _lib.load().rsc_nd_geometric(n, d.xyz.shape[1], d.xyz.ctypes.data, d.indptr.ctypes.data,
-                                       d.indices.ctypes.data, d.leaf, order.ctypes.data, cap,
-                                       *[nodes[i].ctypes.data for i in range(6)], root.ctypes.data)
+    # node capacity: a generous estimate first (the tree has ~4n/leaf nodes), the
+    # worst case 2n+1 only if that overflows (-3)
+    for cap in (min(2 * n + 1, 8 * (n // max(d.leaf, 1)) + 4096), 2 * n + 1):
+        nodes = np.empty((6, cap), dtype=np.int64)
+        cnt = _lib.load().rsc_nd_geometric(n, d.xyz.shape[1], d.xyz.ctypes.data, d.indptr.ctypes.data,
+                                           d.indices.ctypes.data, d.leaf, order.ctypes.data, cap,
+                                           *[nodes[i].ctypes.data for i in range(6)], root.ctypes.data)
+        if cnt != -3:
+            break
     if cnt < 0:
         raise RuntimeError(f"rsc_nd_geometric failed ({cnt})")
     lo, hi, sub, lev, left, right = (nodes[i, :cnt].tolist() for i in range(6))
@@ -388,8 +392,9 @@ def partition_separator(coords, C, tau_d):
 # elimination tree, supernodes, structures
 
 
-def etree_postorder_counts(B):
-    """(parent, post, counts) of the permuted lower-CSC matrix (C++ host kernels)."""
+def etree_postorder_counts(B, septree=None):
+    """(parent, post, counts) of the permuted lower-CSC matrix (C++ host kernels; the
+    etree's rows of disjoint ND subtrees on host threads when the tree is given)."""
     lib = _lib.load()
     n = B.n
     cp = np.ascontiguousarray(B.col_ptr, dtype=np.int64)
@@ -397,7 +402,16 @@ def etree_postorder_counts(B):
     parent = np.empty(n, dtype=np.int64)
     post = np.empty(n, dtype=np.int64)
     counts = np.empty(n, dtype=np.int64)
-    _lib.check(lib.rsc_sym_etree(n, cp.ctypes.data, ri.ctypes.data, parent.ctypes.data), "rsc_sym_etree")
+    rc = 1
+    if septree is not None and septree.root is not None:
+        rg = _subtree_col_ranges(septree)
+        if rg.size:
+            rc = lib.rsc_sym_etree_par(n, cp.ctypes.data, ri.ctypes.data, rg.size // 2, rg.ctypes.data,
+                                       parent.ctypes.data)
+            if rc < 0:
+                raise RuntimeError(f"rsc_sym_etree_par failed ({rc})")
+    if rc != 0:
+        _lib.check(lib.rsc_sym_etree(n, cp.ctypes.data, ri.ctypes.data, parent.ctypes.data), "rsc_sym_etree")
     _lib.check(lib.rsc_sym_postorder(n, parent.ctypes.data, post.ctypes.data), "rsc_sym_postorder")
     _lib.check(lib.rsc_sym_colcounts(n, cp.ctypes.data, ri.ctypes.data, parent.ctypes.data, post.ctypes.data,
                                      counts.ctypes.data), "rsc_sym_colcounts")
@@ -474,6 +488,27 @@ def form_supernodes(n, parent, counts, septree, tau_o, relax=True):
         pos = hi
     starts.append(n)
     return SupernodePartition(n, starts, flags)
+
+
+def _subtree_front(septree, target=64):
+    """~target disjoint ND subtrees: the largest subtree split first."""
+    front = [septree.root]
+    while len(front) < target:
+        big = max((nd for nd in front if nd.is_separator), key=lambda nd: nd.hi - nd.subtree_lo, default=None)
+        if big is None:
+            break
+        front.remove(big)
+        front += [big.left, big.right]
+    return front
+
+
+def _subtree_col_ranges(septree, target=64):
+    """Column ranges [subtree_lo, hi) of disjoint ND subtrees (flattened pairs)."""
+    out = []
+    for nd in _subtree_front(septree, target):
+        if nd.hi - nd.subtree_lo >= 2:
+            out += [nd.subtree_lo, nd.hi]
+    return np.asarray(sorted(out), dtype=np.int64).reshape(-1)
 
 
 def _subtree_ranges(part, septree, target=64):
@@ -592,7 +627,7 @@ def analyze(A, tau_o, tau_d, interior_blocks=True, coords=None):
     np.cumsum(np.bincount(c, minlength=A.n), out=col_ptr[1:])
     B = SparseSpdMatrix(A.n, col_ptr, r, A.values[b_from_a], validate=False)
     t1 = time.perf_counter()
-    parent, post, counts = etree_postorder_counts(B)
+    parent, post, counts = etree_postorder_counts(B, septree)
     part = form_supernodes(B.n, parent, counts, septree, tau_o)
     compute_row_structures(B, part, septree)
     sep_splits = {part.supernode_of(lo): s for (lo, hi), s in splits_by_range.items()}

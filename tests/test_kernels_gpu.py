@@ -99,6 +99,55 @@ def test_gemm_ordered_accumulation_deterministic(cuda):
         assert relerr(outs[0][t], ref[t]) < 1e-14
 
 
+def test_gemm_ordered_accumulation_row_mapped(cuda):
+    """Accumulating problems scattered by row only, every partial as wide as its
+    target (the sketch-product shape, ordered_reduce_kernel's row-sweep path),
+    including repeated target rows whose extra products are exact zeros: equals the
+    sequential sum in problem order, bit-identical on every launch."""
+    from paper_1507_05593_b200 import engine as E
+
+    rng = np.random.default_rng(5)
+    shapes = [(700, 64), (300, 130), (90, 1100)]  # 1100 > one row-sweep tile (1024 columns)
+    C0 = [rng.standard_normal(sh) for sh in shapes]
+    Cd = [E.to_dev(c) for c in C0]
+    keep, probs, ref = [], [], [c.copy() for c in C0]
+    for n in range(45):
+        t = n % 3
+        er, ec = shapes[t]
+        M, K = int(rng.integers(1, min(er, 200))), int(rng.integers(1, 120))
+        rows = np.sort(rng.choice(er, M, replace=False))
+        A = rng.standard_normal((M, K))
+        if n % 4 == 0 and M > 3:  # repeated target rows carrying exact-zero products
+            rows[1:3] = rows[0]
+            A[1:3] = 0.0
+            rows = np.sort(rows)
+            A[1:3] = 0.0
+        rows = rows.astype(np.int32)
+        B = rng.standard_normal((K, ec))
+        dA, dB, dr = E.to_dev(A), E.to_dev(B), E.to_dev(rows)
+        keep += [dA, dB, dr]
+        q = E.gemm_problems(1)
+        q["A"], q["B"], q["C"], q["c_rows"] = dA.data_ptr(), dB.data_ptr(), Cd[t].data_ptr(), dr.data_ptr()
+        q["M"], q["N"], q["K"], q["lda"], q["ldb"], q["ldc"] = M, ec, K, K, ec, ec
+        q["batch"], q["atomic"], q["alpha"], q["beta"], q["ext_r"], q["ext_c"] = 1, 1, 1.0, 1.0, er, ec
+        probs.append(q)
+        prod = A @ B
+        for i, r in enumerate(rows):
+            ref[t][r] += prod[i]
+    P = np.concatenate(probs)
+    outs = []
+    for _ in range(3):
+        for t in range(3):
+            Cd[t].copy_(E.to_dev(C0[t]))
+        E.gemm_grouped(P)
+        outs.append([c.cpu().numpy() for c in Cd])
+    for o in outs[1:]:
+        for t in range(3):
+            assert np.array_equal(o[t], outs[0][t])
+    for t in range(3):
+        assert relerr(outs[0][t], ref[t]) < 1e-14
+
+
 def test_dense_cholesky_golden(cuda):
     from paper_1507_05593_b200 import kernels as K
 
@@ -200,11 +249,14 @@ def test_orthonormalize_multi_cta_path(cuda, m, k, true_rank):
     assert relerr(Q @ (Q.T @ G), Qo @ (Qo.T @ G)) < 1e-10
 
 
-@pytest.mark.parametrize("m,k,true_rank", [(4096, 600, 250), (1000, 300, None), (30000, 96, 40)])
+@pytest.mark.parametrize("m,k,true_rank", [(4096, 600, 250), (1000, 300, None), (30000, 96, 40),
+                                             (8000, 1000, 300), (6000, 700, None)])
 def test_orthonormalize_cooperative_kernel(cuda, monkeypatch, m, k, true_rank):
     """The cooperative multi-CTA QRCP itself (cluster path disabled): shared-memory
     column groups of ~100 CTAs (4096 x 600: more per-CTA pivot candidates than one
-    warp's lanes) and the global-memory column path (30000 x 96).  Kept rank exact,
+    warp's lanes) and the global-memory column path (30000 x 96: one column per CTA;
+    8000 x 1000 and 6000 x 700: 5-7 columns per CTA, the CTA-cooperative update with
+    the reflector staged in shared memory).  Kept rank exact,
     span to 1e-10 against the oracle."""
     from oracle import kernels as ok
     from paper_1507_05593_b200 import kernels as K
