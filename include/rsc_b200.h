@@ -324,6 +324,60 @@ int rsc_plan_tree_maps_fetch(void *h, long long *const *out, int *idx);
 /* 64-bit digest of a byte buffer (the pattern key load_values compares). */
 unsigned long long rsc_hash64(const void *data, long long nbytes);
 
+/* ---- Plan-level numeric steps ------------------
+ * Composed from the batched kernels above, driven by the plan's index arrays (the
+ * descendant maps of plan.py: per update source q of a target supernode, its panel
+ * pair eff/raw (ld, width w), the row run lo, the counts nrd = rows inside C_j and
+ * nro = rows beyond, and the int32 maps cpos (rows inside C_j, relative to c0) and
+ * rpos (searchsorted positions in R_j)).  Sources in reference order.
+ *
+ * rsc_schur_update (factor.py:383-398 _assemble_schur): UD[cpos, cpos] -=
+ *   eff[lo:lo+nrd] raw[lo:lo+nrd]^T and UO[rpos, cpos] -= eff[lo+nrd:] raw[lo:lo+nrd]^T,
+ *   summed in source order (ordered accumulation, bit-reproducible).  UD (nc x nc)
+ *   and UO (nr x nc) hold A's blocks on entry; either may be NULL.
+ * rsc_offdiag_products (factor.py:444-455 / 471-482): the source terms of Alg. 2;
+ *   trans = 0: W[rpos] -= E[hi:] (V[lo:hi]^T G[cpos]); trans = 1: W[cpos] -=
+ *   V[lo:hi] (E[hi:]^T G[rpos]).  W (wr x wc), G (x r), T: workspace of
+ *   sum_q w_q r doubles.  The caller adds A's term and the diagonal solve
+ *   (rsc_spmm_csr, rsc_trsm_batched / rsc_tree_trsm).
+ * rsc_interior_factor_batched (interior.py:105-156): L_B = chol(A_BB) in place
+ *   (+ Dinv, LAPACK info words) and Y_B = A(off_rows, C_B) L_B^{-T} in place.
+ * rsc_tree_trsm (diagblocks.py:192-273, Alg. 4): X (n x r) <- D^{-1} X (trans 0) or
+ *   D^{-T} X (trans 1) for a block tree of nnodes nodes: node i spans [lo, hi) of the
+ *   separator; split[i] < 0 marks a leaf (L, ldl, Dinv: its triangle), else the
+ *   coupling of [lo, split) into [split, hi) is dense B (rows hi-split x cols
+ *   split-lo) or, when k != NULL and V[i] != NULL, V U^T (V: rows x k[i], U: cols x
+ *   k[i]); tws: k_max x r doubles of workspace.
+ * rsc_apply_sweep (factor.py:187-218): one sweep of the apply program, phases of
+ *   rsc_gemv_multi problems run in order (flattened arrays, phase_count[p] problems
+ *   each); forward and backward sweeps are two programs (apply.py DeviceApply).
+ * rsc_nccl_*: NCCL resolved at run time (libnccl.so.2 or RSC_NCCL_LIB); -20 if
+ *   unavailable.  Communicator from a 128-byte unique id; FP64 sum all-reduce and
+ *   broadcast (the multi-GPU top-separator sums and apply rows, distributed.py). */
+int rsc_schur_update(double *UD, int ld_ud, int nc, double *UO, int ld_uo, int nr, int nsrc,
+                     const double *const *eff, const double *const *raw, const int *ld, const int *w, const int *lo,
+                     const int *nrd, const int *nro, const int *const *cpos, const int *const *rpos, void *stream);
+int rsc_offdiag_products(int trans, double *W, int ldw, int wr, int wc, const double *G, int ldg, int r, int nsrc,
+                         const double *const *eff, const double *const *raw, const int *ld, const int *w,
+                         const int *lo, const int *nrd, const int *nro, const int *const *cpos,
+                         const int *const *rpos, double *T, void *stream);
+int rsc_interior_factor_batched(int count, double *const *L, const int *n, const int *ldl, double *const *Dinv,
+                                double *const *Y, const int *m, const int *ldy, int *info_dev, void *stream);
+int rsc_tree_trsm(int trans, int nnodes, int root, const int *lo, const int *hi, const int *split, const int *left,
+                  const int *right, const double *const *L, const int *ldl, const double *const *Dinv,
+                  const double *const *B, const int *ldb, const double *const *V, const double *const *U,
+                  const int *ldv, const int *ldu, const int *k, double *X, int ldx, int r, double *tws,
+                  void *stream);
+int rsc_apply_sweep(int nphases, const int *phase_count, const double *const *M, const int *rows, const int *cols,
+                    const int *ldm, const double *const *x, const int *const *xidx, double *const *y,
+                    const int *const *yidx, const int *modes, const double *alphas, void *stream);
+int rsc_nccl_available(void);
+int rsc_nccl_unique_id(char *id128);
+int rsc_nccl_comm_init(int nranks, const char *id128, int rank, void **comm);
+int rsc_nccl_allreduce_sum_f64(void *comm, const double *send, double *recv, long long count, void *stream);
+int rsc_nccl_broadcast_f64(void *comm, const double *send, double *recv, long long count, int root, void *stream);
+int rsc_nccl_comm_destroy(void *comm);
+
 /* ---- Gaussian sketches (replaces the host draw at reference kernels.py:85-92,
  * np.random.Generator(np.random.PCG64(seed)).standard_normal((m, r)), seeded per
  * block by factor.py:324-326 _block_seed) ---------------------------------------

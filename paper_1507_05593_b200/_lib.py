@@ -79,6 +79,17 @@ EXPORTED = (
     "rsc_normal_pcg64",
     "rsc_log1p_fdlibm",
     "rsc_normal_debug_limits",
+    "rsc_schur_update",
+    "rsc_offdiag_products",
+    "rsc_interior_factor_batched",
+    "rsc_tree_trsm",
+    "rsc_apply_sweep",
+    "rsc_nccl_available",
+    "rsc_nccl_unique_id",
+    "rsc_nccl_comm_init",
+    "rsc_nccl_allreduce_sum_f64",
+    "rsc_nccl_broadcast_f64",
+    "rsc_nccl_comm_destroy",
     "rsc_launch_counter",
     "rsc_version",
     "rsc_device_arch",
@@ -143,6 +154,17 @@ _SIGS = {
     "rsc_normal_pcg64": (I, [I, P, P, P, P, ctypes.c_size_t, P]),
     "rsc_log1p_fdlibm": (D, [D]),
     "rsc_normal_debug_limits": (I, [I, I]),
+    "rsc_schur_update": (I, [P, I, I, P, I, I, I] + [P] * 10),
+    "rsc_offdiag_products": (I, [I, P, I, I, I, P, I, I, I] + [P] * 11),
+    "rsc_interior_factor_batched": (I, [I] + [P] * 9),
+    "rsc_tree_trsm": (I, [I, I, I] + [P] * 16 + [I, I, P, P]),
+    "rsc_apply_sweep": (I, [I] + [P] * 12),
+    "rsc_nccl_available": (I, []),
+    "rsc_nccl_unique_id": (I, [P]),
+    "rsc_nccl_comm_init": (I, [I, P, I, P]),
+    "rsc_nccl_allreduce_sum_f64": (I, [P, P, P, LL, P]),
+    "rsc_nccl_broadcast_f64": (I, [P, P, P, LL, I, P]),
+    "rsc_nccl_comm_destroy": (I, [P]),
     "rsc_launch_counter": (LL, [I]),
     "rsc_version": (ctypes.c_char_p, []),
     "rsc_device_arch": (I, []),
