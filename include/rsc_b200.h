@@ -75,6 +75,11 @@ int rsc_gemm_set_workspace(void *stream, void *ws_dev, long long bytes, int as_d
  * products), blocks.py:35-39 (LowRankBlock.matmat/rmatmat), kernels.py:107-112. */
 int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *problems,
                      int count, void *stream);
+/* The same launch with K balancing (engine.balance_k): accumulating problems (atomic
+ * or beta = 1) whose k-loop exceeds 1.5x the balanced per-CTA share of `ctas`
+ * concurrent CTAs are cut into K slabs of that share, in place and in order. */
+int rsc_gemm_grouped_balanced(int transA, int transB, const rsc_gemm_problem *problems, int count, int ctas,
+                              void *stream);
 
 /* Batched in-place lower Cholesky of `count` matrices (sizes may differ).
  * A[i] (n[i] x n[i], ld lda[i]) : lower triangle read, overwritten by L with the

@@ -30,6 +30,7 @@ assert GEMM_DTYPE.itemsize == 128
 # every symbol include/rsc_b200.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "rsc_gemm_grouped",
+    "rsc_gemm_grouped_balanced",
     "rsc_gemm_set_workspace",
     "rsc_potrf_batched",
     "rsc_trsm_batched",
@@ -104,6 +105,7 @@ LL = ctypes.c_longlong
 
 _SIGS = {
     "rsc_gemm_grouped": (I, [I, I, P, I, P]),
+    "rsc_gemm_grouped_balanced": (I, [I, I, P, I, I, P]),
     "rsc_gemm_set_workspace": (I, [P, P, LL, I]),
     "rsc_potrf_batched": (I, [I, P, P, P, P, P, P]),
     "rsc_trsm_batched": (I, [I, I, I, P, P, P, P, P, P, P, P]),

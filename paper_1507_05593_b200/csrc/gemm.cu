@@ -30,6 +30,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -719,6 +720,51 @@ int launch_reduce_tables(RedArgs &ra, char *tab, long long tab_used, cudaStream_
 }
 
 }  // namespace
+
+// K balancing of one grouped launch (engine.balance_k / split_k_var, restated here
+// so the host side of the sweep does not rebuild problem arrays in numpy): every
+// accumulating problem (atomic, or beta = 1) whose single-tile k-loop exceeds ~1.5x
+// the balanced per-CTA share is cut into K slabs of that share, in place and in
+// order (each slab accumulates: the ordered reduction keeps the slab order).
+extern "C" int rsc_gemm_grouped_balanced(int transA, int transB, const rsc_gemm_problem *problems, int count,
+                                         int ctas, void *stream) {
+    if (count < 0 || ctas <= 0) return -4;
+    if (count == 0) return 0;
+    double tot = 0.0;
+    for (int i = 0; i < count; ++i) {
+        const rsc_gemm_problem &p = problems[i];
+        const double tiles = std::ceil(p.M / 64.0) * std::ceil(p.N / 64.0) * p.batch;
+        tot += tiles * std::ceil(p.K / 16.0);
+    }
+    const long long target = std::max(8LL, (long long)std::ceil(tot / ctas));
+    static thread_local std::vector<rsc_gemm_problem> q;
+    q.clear();
+    bool any = false;
+    for (int i = 0; i < count; ++i) {
+        const rsc_gemm_problem &p = problems[i];
+        const double ks = std::ceil(p.K / 16.0);
+        const bool need = (p.atomic == 1 || p.beta == 1.0) && ks > 1.5 * (double)target;
+        if (!need) { q.push_back(p); continue; }
+        const long long lim = 16 * target, K = p.K;
+        const long long nsl = std::max(1LL, (K + lim - 1) / lim);
+        if (nsl == 1) { q.push_back(p); continue; }
+        any = true;
+        for (long long sl = 0; sl < nsl; ++sl) {
+            rsc_gemm_problem r = p;
+            const long long k0 = sl * lim;
+            r.K = (int)std::min(lim, K - k0);
+            r.A = transA ? p.A + k0 * p.lda : p.A + k0;
+            if (transB) r.B = p.B + k0;
+            else if (p.b_rows) r.b_rows = p.b_rows + k0;
+            else r.B = p.B + k0 * p.ldb;
+            r.atomic = 1;
+            r.beta = 1.0;
+            q.push_back(r);
+        }
+    }
+    if (!any) return rsc_gemm_grouped(transA, transB, problems, count, stream);
+    return rsc_gemm_grouped(transA, transB, q.data(), (int)q.size(), stream);
+}
 
 extern "C" int rsc_gemm_set_workspace(void *stream, void *ws_dev, long long bytes, int as_default) {
     if (bytes < 0) return -3;

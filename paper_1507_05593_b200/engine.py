@@ -263,6 +263,26 @@ def gemm_grouped(probs, transA=False, transB=False):
         prof.records.append((s, e, fl, TAG))
 
 
+def gemm_balanced(probs, transA=False, transB=False, ctas=None):
+    """gemm_grouped(balance_k(probs)) with the K balancing done in the library
+    (rsc_gemm_grouped_balanced: same splits, no numpy rebuild of the problem array)."""
+    probs = np.ascontiguousarray(probs, dtype=GEMM_DTYPE)
+    if probs.size == 0:
+        return
+    lib = ensure_gemm_workspace() if (probs["atomic"] != 0).any() or (probs["beta"] == 1.0).any() else require_cuda()
+    prof = PROFILE
+    if prof is not None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+    check(lib.rsc_gemm_grouped_balanced(int(transA), int(transB), addr(probs), int(probs.size),
+                                        int(ctas or GEMM_CONCURRENT_CTAS), stream_handle()),
+          "rsc_gemm_grouped_balanced")
+    if prof is not None:
+        e.record()
+        fl = float(np.sum(2.0 * probs["M"].astype(np.float64) * probs["N"] * probs["K"] * probs["batch"]))
+        prof.records.append((s, e, fl, TAG))
+
+
 def split_k(p, transA, transB, ks):
     """Cut every problem's K into slabs of at most `ks`, accumulated (in slab order,
     deterministically) into C: tall-K products (few output tiles, long K) then spread

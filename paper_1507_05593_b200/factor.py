@@ -227,7 +227,7 @@ class Grouped:
 
     def launch(self):
         if self.rows:
-            E.gemm_grouped(E.balance_k(np.array(self.rows, dtype=GEMM_DTYPE), self.tA, self.tB), self.tA, self.tB)
+            E.gemm_balanced(np.array(self.rows, dtype=GEMM_DTYPE), self.tA, self.tB)
             self.rows = []
 
 

@@ -464,7 +464,7 @@ class LevelPass(NumericPass):
         if probs:
             P = E.gcat(probs)
             if P.size:
-                E.gemm_grouped(E.balance_k(P, False, True), False, True)
+                E.gemm_balanced(P, False, True)
         self._reduce([t for pair in out for t in pair])
         return out
 
@@ -551,8 +551,8 @@ class LevelPass(NumericPass):
         keep = self._mine(s)
         p1, p2 = p1[keep], p2[keep]
         if p1.size:
-            E.gemm_grouped(E.balance_k(p1, True, False), True, False)
-            E.gemm_grouped(E.balance_k(p2, False, False), False, False)
+            E.gemm_balanced(p1, True, False)
+            E.gemm_balanced(p2, False, False)
 
     def approx_off_many(self, nodes, ranks):
         """Alg. 3 for every compressed off-diagonal of the level (factor.py:486-505)."""
@@ -635,7 +635,7 @@ class LevelPass(NumericPass):
             self._wflops(2.0 * P["M"] * P["N"], w=P["K"], wbase=np.concatenate(bases))
             P = P[np.concatenate(keeps)]
             if P.size:
-                E.gemm_grouped(E.balance_k(P, False, True), False, True)
+                E.gemm_balanced(P, False, True)
         self._reduce(Us)
         if LevelPass.fault_hook is not None and Us and LevelPass.fault_hook(self, items):
             Us[0][0, 0] = -1.0  # test hook: make the first leaf of this batch indefinite
@@ -745,8 +745,8 @@ class LevelPass(NumericPass):
             P2["batch"], P2["atomic"], P2["alpha"], P2["beta"] = 1, 1, -1.0, 1.0
             P1["atomic"] = 1  # T is zeroed: P1 accumulates, so its tall K may be split
             if P1.size:
-                E.gemm_grouped(E.balance_k(P1, True, False), True, False)
-                E.gemm_grouped(E.balance_k(P2, False, False), False, False)
+                E.gemm_balanced(P1, True, False)
+                E.gemm_balanced(P2, False, False)
         self._reduce(Ws)
         if transpose:
             sol2 = []

@@ -97,6 +97,14 @@ def test_gemm_ordered_accumulation_deterministic(cuda):
             assert np.array_equal(o[t], outs[0][t])
     for t in range(T):
         assert relerr(outs[0][t], ref[t]) < 1e-14
+    # the library-side K balancing (rsc_gemm_grouped_balanced) splits exactly like
+    # engine.balance_k: bit-identical results
+    P0 = np.concatenate(probs)
+    for t in range(T):
+        Cd[t].copy_(E.to_dev(C0[t]))
+    E.gemm_balanced(P0, ctas=8)
+    for t in range(T):
+        assert np.array_equal(Cd[t].cpu().numpy(), outs[0][t])
 
 
 def test_gemm_ordered_accumulation_row_mapped(cuda):
