@@ -29,7 +29,9 @@
 
 namespace {
 
-constexpr int CT = 256;  // threads per CTA (8 warps)
+constexpr int CT = 256;   // threads per CTA (8 warps): cluster QRCP, Q formation
+constexpr int MCT = 512;  // threads per CTA of the cooperative QRCP (16 warps: the owned-column updates and
+                          // block reductions of a column step spread over twice the warps)
 constexpr int MAXM = 96;
 constexpr double EPS = 2.220446049250313e-16;
 constexpr double TOL3Z = 1.0536712127723509e-08;
@@ -122,7 +124,7 @@ __device__ __forceinline__ void publish_candidate(const Ws &w, const double *vn1
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double best = -1.0;
     int bp = 0x7fffffff, bph = -1;
-    for (int phys = c0 + t; phys < c1; phys += CT) {
+    for (int phys = c0 + t; phys < c1; phys += MCT) {
         const int ps = posof[phys];
         if (ps < i) continue;
         const double vv = vn1[phys];
@@ -139,7 +141,7 @@ __device__ __forceinline__ void publish_candidate(const Ws &w, const double *vn1
     if (lane == 0) { red[warp] = best; redp[warp] = bp; redp[16 + warp] = bph; }
     __syncthreads();
     if (t == 0) {
-        for (int q = 1; q < CT / 32; ++q)
+        for (int q = 1; q < MCT / 32; ++q)
             if (red[q] > best || (red[q] == best && redp[q] < bp)) { best = red[q]; bp = redp[q]; bph = redp[16 + q]; }
         w.cand_v[par * CQ_MAX + lb] = best;
         w.cand_p[par * CQ_MAX + lb] = bp;
@@ -152,7 +154,7 @@ __device__ __forceinline__ void publish_candidate(const Ws &w, const double *vn1
         if (ph >= 0) {
             const double *src = cols + (long long)(ph - c0) * ldw;
             double *dst = w.cand_col + ((long long)par * w.cq2 + lb) * ldw;
-            for (int r = i + t; r < m; r += CT) dst[r] = src[r];
+            for (int r = i + t; r < m; r += MCT) dst[r] = src[r];
         }
     }
 }
@@ -162,7 +164,7 @@ __device__ __forceinline__ void publish_candidate(const Ws &w, const double *vn1
 template <int CB>
 __device__ __forceinline__ void block_sum_n(double (&x)[CB], double *red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = CT / 32;
+    constexpr int NW = MCT / 32;
 #pragma unroll
     for (int c = 0; c < CB; ++c) x[c] = warp_sum(x[c]);
     __syncthreads();
@@ -209,7 +211,7 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
 #pragma unroll
             for (int c = 0; c < CB; ++c) x[c] = 0.0;
 #pragma unroll 4
-            for (int r = i + 1 + t; r < m; r += CT) {
+            for (int r = i + 1 + t; r < m; r += MCT) {
                 const double vr = vsm ? vs[r] : __ldcg(vs + r);
 #pragma unroll
                 for (int c = 0; c < CB; ++c)
@@ -219,7 +221,7 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
 #pragma unroll
             for (int c = 0; c < CB; ++c) f[c] = on[c] ? tau * (x[c] + cji0[c]) : 0.0;
 #pragma unroll 4
-            for (int r = i + 1 + t; r < m; r += CT) {
+            for (int r = i + 1 + t; r < m; r += MCT) {
                 const double vr = vsm ? vs[r] : __ldcg(vs + r);
 #pragma unroll
                 for (int c = 0; c < CB; ++c)
@@ -257,7 +259,7 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
 #pragma unroll
             for (int c = 0; c < CB; ++c) x[c] = 0.0;
 #pragma unroll 4
-            for (int r = i + 1 + t; r < m; r += CT) {
+            for (int r = i + 1 + t; r < m; r += MCT) {
 #pragma unroll
                 for (int c = 0; c < CB; ++c)
                     if (redo[c]) x[c] = fma(cj[c][r], cj[c][r], x[c]);
@@ -277,9 +279,9 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs a) {
+__global__ void __launch_bounds__(MCT) mqrcp_kernel(const __grid_constant__ MArgs a) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ double red[32];
+    __shared__ double red[64]  /* block_sum_n: CB x MCT/32 */;
     __shared__ int redp[32];
     __shared__ int piv_s;
     // locate this CTA's matrix
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
     unsigned *bar = a.bar + g;
     const int m = d.m, k = d.k, ldw = d.ldw, cpc = d.cpc, nblk = d.nblk;
     const int lb = blockIdx.x - d.blk0;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = CT / 32;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = MCT / 32;
     const int c0 = lb * cpc, c1 = min(k, c0 + cpc);
     double *cols = SMEM ? sm : w.cols + (long long)c0 * ldw;
     const bool vsm = !SMEM && d.vsm;
@@ -303,11 +305,11 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
     double *vn2 = vn1 + cpc;
     unsigned epoch = 0;
 
-    for (long long e = t; e < (long long)m * (c1 - c0); e += CT) {
+    for (long long e = t; e < (long long)m * (c1 - c0); e += MCT) {
         const int r = (int)(e / (c1 - c0)), j = (int)(e % (c1 - c0));
         cols[(long long)j * ldw + r] = d.G[(long long)r * d.ldg + c0 + j];
     }
-    for (int j = t; j < k; j += CT) { pos2phys[j] = j; posof[j] = j; }
+    for (int j = t; j < k; j += MCT) { pos2phys[j] = j; posof[j] = j; }
     __syncthreads();
     for (int j = warp; j < c1 - c0; j += nw) {
         const double *cj = cols + (long long)j * ldw;
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
         const int par = i & 1;
         if (!SMEM && pend_c >= 0) {  // v still holds step pend_i's reflector
             double *ci = cols + (long long)(pend_c - c0) * ldw;
-            for (int r = pend_i + 1 + t; r < m; r += CT) ci[r] = v[r];
+            for (int r = pend_i + 1 + t; r < m; r += MCT) ci[r] = v[r];
             if (t == 0) ci[pend_i] = pend_beta;
             pend_c = -1;
             __syncthreads();
@@ -380,10 +382,10 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
                                 : SMEM ? w.cand_col + ((long long)par * w.cq2 + pc / cpc) * ldw
                                        : w.cols + (long long)pc * ldw;
 #pragma unroll 4
-            for (int r = i + t; r < m; r += CT) v[r] = own ? src[r] : __ldcg(src + r);
+            for (int r = i + t; r < m; r += MCT) v[r] = own ? src[r] : __ldcg(src + r);
             __syncthreads();
             double part = 0.0;
-            for (int r = i + 1 + t; r < m; r += CT) part += v[r] * v[r];
+            for (int r = i + 1 + t; r < m; r += MCT) part += v[r] * v[r];
             const double xnorm = sqrt(block_sum(part, red));
             const double alpha = v[i];
             double beta = alpha, scal = 0.0;
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
                 scal = 1.0 / (alpha - beta);
             }
             double *ci = (own && SMEM) ? cols + (long long)(pc - c0) * ldw : nullptr;
-            for (int r = i + 1 + t; r < m; r += CT) {
+            for (int r = i + 1 + t; r < m; r += MCT) {
                 const double x = (xnorm != 0.0) ? v[r] * scal : v[r];
                 v[r] = x;
                 if (ci) ci[r] = x;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
             if (pc >= c0 && pc < c1) {
                 double *ci = cols + (long long)(pc - c0) * ldw;
                 double part = 0.0;
-                for (int r = i + 1 + t; r < m; r += CT) part += ci[r] * ci[r];
+                for (int r = i + 1 + t; r < m; r += MCT) part += ci[r] * ci[r];
                 const double xnorm = sqrt(block_sum(part, red));
                 const double alpha = ci[i];
                 double tau0 = 0.0, beta = alpha, scal = 0.0;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
                     scal = 1.0 / (alpha - beta);
                 }
                 __syncthreads();
-                for (int r = i + 1 + t; r < m; r += CT) {
+                for (int r = i + 1 + t; r < m; r += MCT) {
                     const double x = (xnorm != 0.0) ? ci[r] * scal : ci[r];
                     ci[r] = x;
                     if (nblk > 1) w.vbuf[r] = x;
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
             group_barrier(bar, nblk, epoch);
             tau = __ldcg(w.tau + i);
             if (nblk > 1 && (SMEM || vsm)) {
-                for (int r = i + 1 + t; r < m; r += CT) v[r] = __ldcg(w.vbuf + r);
+                for (int r = i + 1 + t; r < m; r += MCT) v[r] = __ldcg(w.vbuf + r);
                 __syncthreads();
             }
         }
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
         if (!SMEM && nblk > 1) {
             // global-memory columns: the whole CTA works on its columns together
             // (rows spread over all threads, CB columns per pass, block reductions),
-            // so every step keeps ~CT x CB independent L2 loads in flight instead of
+            // so every step keeps ~MCT x CB independent L2 loads in flight instead of
             // one warp walking one column serially through L2
             coop_update(vn1, vn2, cols, vsm ? v : w.vbuf, vsm, posof, c0, c1, i, m, ldw, tau, red);
         } else {
@@ -490,15 +492,15 @@ __global__ void __launch_bounds__(CT) mqrcp_kernel(const __grid_constant__ MArgs
     }
     if (!SMEM && pend_c >= 0) {  // the last deferred reflector
         double *ci = cols + (long long)(pend_c - c0) * ldw;
-        for (int r = pend_i + 1 + t; r < m; r += CT) ci[r] = v[r];
+        for (int r = pend_i + 1 + t; r < m; r += MCT) ci[r] = v[r];
         if (t == 0) ci[pend_i] = pend_beta;
         __syncthreads();
     }
     // spill the owned columns (reflectors) for the Q kernel; publish the permutation
     if (SMEM)
-        for (long long e = t; e < (long long)ldw * (c1 - c0); e += CT) w.cols[(long long)c0 * ldw + e] = cols[e];
+        for (long long e = t; e < (long long)ldw * (c1 - c0); e += MCT) w.cols[(long long)c0 * ldw + e] = cols[e];
     if (lb == 0)
-        for (int j = t; j < k; j += CT) w.perm[j] = pos2phys[j];
+        for (int j = t; j < k; j += MCT) w.perm[j] = pos2phys[j];
 }
 
 
@@ -1294,7 +1296,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
                         per_sm = it->second;
                     } else {
                         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                            &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, CT, sm2);
+                            &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, MCT, sm2);
                         occ_b[{(int)smem, sm2}] = per_sm;
                     }
                 }
@@ -1324,7 +1326,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
             ma.bar = bar + start + (smem ? 0 : 0);
             void *args[] = {&ma};
             cudaError_t e = cudaLaunchCooperativeKernel(
-                smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, dim3(b0), dim3(CT), args, sm, s);
+                smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, dim3(b0), dim3(MCT), args, sm, s);
             rsc_count_launch();
             if (e != cudaSuccess) return (int)e;
             // Q formation (blocked compact-WY on DMMA GEMMs) for the same matrices
