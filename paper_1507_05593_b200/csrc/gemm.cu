@@ -533,6 +533,20 @@ int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
     }
     gemm_grouped_kernel<TA, TB, GATHER><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
     RSC_CHECK_LAUNCH();
+    static const bool log = getenv("RSC_GEMM_LOG") != nullptr;  // diagnostics: one line per launch
+    if (log) {
+        double fl = 0.0, pad = 0.0;
+        int maxk = 0;
+        for (int i = 0; i < args.count; ++i) {
+            const rsc_gemm_problem &p = args.p[i];
+            fl += 2.0 * p.M * p.N * (double)p.K * p.batch;
+            pad += 2.0 * ((p.M + BM - 1) / BM * BM) * ((p.N + BN - 1) / BN * BN) * (double)((p.K + BK - 1) / BK * BK) *
+                   p.batch;
+            maxk = std::max(maxk, p.K);
+        }
+        fprintf(stderr, "GEMMLOG %d %d %d tiles %lld probs %d flops %.0f padded %.0f maxk %d\n", (int)TA, (int)TB,
+                (int)GATHER, tiles, args.count, fl, pad, maxk);
+    }
     return 0;
 }
 
@@ -858,6 +872,28 @@ extern "C" int rsc_gemm_grouped(int transA, int transB, const rsc_gemm_problem *
                 q.strideC = p.strideC;
                 q.beta = 1.0;
             }
+        }
+        // longest k-loops first: the hardware dispatches CTAs in index order, so the
+        // tiles of long-K problems start in the first wave and the short ones fill in
+        // behind them (LPT order); the problems' results do not depend on the order
+        // (each writes its own partial or target; the ordered reduce keeps its own
+        // problem order)
+        static const bool no_lpt = getenv("RSC_GEMM_NO_LPT") != nullptr;
+        if (!no_lpt && args.count > 1) {
+            static thread_local std::vector<int> ord;
+            static thread_local std::vector<rsc_gemm_problem> tmp;
+            ord.resize(args.count);
+            for (int k = 0; k < args.count; ++k) ord[k] = k;
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return args.p[x].K > args.p[y].K; });
+            tmp.assign(args.p, args.p + args.count);
+            long long tb = 0;
+            for (int k = 0; k < args.count; ++k) {
+                const rsc_gemm_problem &q = tmp[ord[k]];
+                args.p[k] = q;
+                args.tile_begin[k] = tb;
+                tb += (long long)((q.M + BM - 1) / BM) * ((q.N + BN - 1) / BN) * q.batch;
+            }
+            args.tile_begin[args.count] = tb;
         }
         if (!reds.empty() && (rc = launch_reduce_tables(ra, ws.ptr + used, tab_used, s))) return rc;
         // the gathered-B loader is its own instantiation: its index prefetch costs the
