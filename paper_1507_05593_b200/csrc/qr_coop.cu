@@ -888,10 +888,10 @@ __global__ void build_vq_kernel(const __grid_constant__ VBuild a) {
 }
 
 struct TArgs {
-    int count, b;
-    const double *G[MAXM];    // Gram of the block (QB x QB, ld QB)
+    int count, nbk;           // matrices, blocks per matrix (CTA = matrix * nbk + block)
+    const double *G[MAXM];    // Gram of every block (nbk x QB x QB, ld QB)
     const double *tau[MAXM];
-    double *T[MAXM];          // QB x QB, ld QB
+    double *T[MAXM];          // nbk x QB x QB, ld QB
     int kmin[MAXM];
 };
 
@@ -906,12 +906,12 @@ struct TArgs {
 __global__ void __launch_bounds__(256) larft_kernel(const __grid_constant__ TArgs a) {
     __shared__ double M[QB][QB + 1];
     __shared__ double X[QB * QB / 4];  // G12 T22 of the pairs being joined
-    const int g = blockIdx.x;
-    const int j0 = a.b * QB;
+    const int g = blockIdx.x / a.nbk, bb = blockIdx.x % a.nbk;
+    const int j0 = bb * QB;
     const int nb = min(QB, a.kmin[g] - j0);
     if (nb <= 0) return;
-    double *T = a.T[g];
-    const double *G = a.G[g];
+    double *T = a.T[g] + (long long)bb * QB * QB;
+    const double *G = a.G[g] + (long long)bb * QB * QB;
     const double *tau = a.tau[g] + j0;
     const int t = threadIdx.x;
     for (int e = t; e < QB * QB; e += blockDim.x) {
@@ -1004,7 +1004,15 @@ long long rsc_qrcp_coop_doubles(int m, int k) {
     static_assert(QB == QB_WY, "candidate region offset assumes the WY block size");
     (void)kmin;
     // ... then the double-buffered pivot candidates and candidate columns
-    return coop_cand_base(m, k) + 4LL * CQ_MAX + 2LL * (k < CQ_MAX ? k : CQ_MAX) * ldw;
+    // ... and the Gram and T triangles of every 64-reflector block (Q formation)
+    const long long nbk = (kmin + QB - 1) / QB;
+    return coop_cand_base(m, k) + 4LL * CQ_MAX + 2LL * (k < CQ_MAX ? k : CQ_MAX) * ldw + 2LL * nbk * QB * QB;
+}
+
+// per-block Gram / T region of a matrix's workspace (rsc_qrcp_coop_doubles)
+static inline double *gt_base(double *W, int m, int k) {
+    const long long ldw = m | 1;
+    return W + coop_cand_base(m, k) + 4LL * CQ_MAX + 2LL * (k < CQ_MAX ? k : CQ_MAX) * ldw;
 }
 
 static inline double *wy_base(double *W, int m, int k) {
@@ -1051,38 +1059,62 @@ static int form_q_blocked(int cnt, const MatDesc *ds, cudaStream_t s) {
     build_vq_kernel<<<grid, 256, 0, s>>>(vb);
     RSC_CHECK_LAUNCH();
     const int nblocks = (maxk + QB - 1) / QB;
+    // Gram V_b^T V_b of every block of every matrix in ONE grouped launch (V is final
+    // before the Q formation starts), then every block's T in ONE dlarft launch; only
+    // the Q updates (W = V_b^T Q_b, W = T_b W, Q_b -= V_b W) stay a sequence over the
+    // blocks, last to first.  The long K (= rows) of the two V^T products is cut into
+    // KS-row slabs summed by the ordered accumulation, so each output tile gets
+    // rows / KS CTAs and a short k-loop.
+    constexpr int KS = 128;
     std::vector<rsc_gemm_problem> pg, pw, pt, pq;
+    ta.count = cnt;
+    ta.nbk = nblocks;
+    for (int c = 0; c < cnt; ++c) {
+        const MatDesc &d = ds[c];
+        const int km = vb.kmin[c];
+        double *V = vb.V[c];
+        double *GT = gt_base(d.W, d.m, d.k);
+        const int nbk = (km + QB - 1) / QB;
+        double *Gall = GT, *Tall = GT + (long long)nbk * QB * QB;
+        ta.G[c] = Gall; ta.T[c] = Tall; ta.kmin[c] = km;
+        ta.tau[c] = d.W + (long long)d.ldw * d.k + 2LL * d.k;
+        cudaMemsetAsync(Gall, 0, sizeof(double) * (size_t)nbk * QB * QB, s);
+        for (int b = 0; b < nbk; ++b) {
+            const int j0 = b * QB, nb = km - j0 < QB ? km - j0 : QB, rows = d.m - j0;
+            const double *Vb = V + (long long)j0 * km + j0;
+            for (int k0 = 0; k0 < rows; k0 += KS) {
+                const int kk = rows - k0 < KS ? rows - k0 : KS;
+                const double *Vk = Vb + (long long)k0 * km;
+                rsc_gemm_problem a = gp(Vk, km, Vk, km, Gall + (long long)b * QB * QB, QB, nb, nb, kk, 1.0, 1.0);
+                a.atomic = 1;
+                pg.push_back(a);
+            }
+        }
+    }
+    if (!pg.empty()) {
+        int rc = rsc_gemm_grouped(1, 0, pg.data(), (int)pg.size(), s);
+        if (rc) return rc;
+        larft_kernel<<<cnt * nblocks, 256, 0, s>>>(ta);
+        RSC_CHECK_LAUNCH();
+    }
     for (int b = nblocks - 1; b >= 0; --b) {
-        pg.clear(); pw.clear(); pt.clear(); pq.clear();
-        ta.count = cnt;
-        ta.b = b;
+        pw.clear(); pt.clear(); pq.clear();
         const int j0 = b * QB;
         for (int c = 0; c < cnt; ++c) {
             const MatDesc &d = ds[c];
             const int km = vb.kmin[c];
+            if (j0 >= km) continue;
             double *V = vb.V[c];
             double *Wb = V + (long long)d.m * km;
-            double *Gm = Wb + (long long)QB * km;
-            double *Tm = Gm + QB * QB;
-            const double *tau = d.W + (long long)d.ldw * d.k + 2LL * d.k;
-            ta.G[c] = Gm; ta.tau[c] = tau; ta.T[c] = Tm; ta.kmin[c] = km;
-            if (j0 >= km) continue;
+            const double *Tm = ta.T[c] + (long long)b * QB * QB;
             const int nb = km - j0 < QB ? km - j0 : QB;
             const int rows = d.m - j0, cols = km - j0;
             const double *Vb = V + (long long)j0 * km + j0;
             double *Qb = d.Q + (long long)j0 * d.ldq + j0;
-            // Gram = V_b^T V_b and W = V_b^T Q_b have a long K (= rows): split K into
-            // slabs accumulated atomically into zeroed outputs so each matrix gets
-            // rows/KS CTAs per output tile instead of one
-            cudaMemsetAsync(Gm, 0, sizeof(double) * QB * QB, s);
             cudaMemsetAsync(Wb, 0, sizeof(double) * (size_t)QB * km, s);
-            constexpr int KS = 512;
             for (int k0 = 0; k0 < rows; k0 += KS) {
                 const int kk = rows - k0 < KS ? rows - k0 : KS;
                 const double *Vk = Vb + (long long)k0 * km;
-                rsc_gemm_problem a = gp(Vk, km, Vk, km, Gm, QB, nb, nb, kk, 1.0, 1.0);  // Gram (TA)
-                a.atomic = 1;
-                pg.push_back(a);
                 rsc_gemm_problem w = gp(Vk, km, Qb + (long long)k0 * d.ldq, d.ldq, Wb, km, nb, cols, kk, 1.0, 1.0);
                 w.atomic = 1;                                                              // W = V^T Q (TA)
                 pw.push_back(w);
@@ -1090,11 +1122,8 @@ static int form_q_blocked(int cnt, const MatDesc *ds, cudaStream_t s) {
             pt.push_back(gp(Tm, QB, Wb, km, Wb, km, nb, cols, nb, 1.0, 0.0));           // W = T W (in place)
             pq.push_back(gp(Vb, km, Wb, km, Qb, d.ldq, rows, cols, nb, -1.0, 1.0));    // Q -= V W
         }
-        if (pg.empty()) continue;
-        int rc = rsc_gemm_grouped(1, 0, pg.data(), (int)pg.size(), s);
-        if (rc) return rc;
-        larft_kernel<<<cnt, 256, 0, s>>>(ta);
-        RSC_CHECK_LAUNCH();
+        if (pw.empty()) continue;
+        int rc;
         if ((rc = rsc_gemm_grouped(1, 0, pw.data(), (int)pw.size(), s))) return rc;
         if ((rc = rsc_gemm_grouped(0, 0, pt.data(), (int)pt.size(), s))) return rc;
         if ((rc = rsc_gemm_grouped(0, 0, pq.data(), (int)pq.size(), s))) return rc;

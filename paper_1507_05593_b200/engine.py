@@ -17,13 +17,27 @@ F64 = torch.float64
 I32 = torch.int32
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
-    if not torch.cuda.is_available():
-        raise RuntimeError("rsc_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("rsc_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        _CUDA_OK = True
     return _lib.load()
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle():
+    """cudaStream_t of torch's current stream (the capture stream inside a graph
+    capture).  The raw accessor skips building a torch.cuda.Stream object per call
+    (tens of thousands of calls per one-shot numeric pass)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -318,7 +332,7 @@ def split_k_var(p, transA, transB, ks):
     return q
 
 
-GEMM_CONCURRENT_CTAS = 148 * 5  # resident 64x64 GEMM CTAs on a B200 (5 per SM)
+GEMM_CONCURRENT_CTAS = int(os.environ.get("RSC_GEMM_CTAS", 148 * 5))  # balance_k target CTAs (5 per SM)
 
 
 def balance_k(p, transA, transB, ctas=GEMM_CONCURRENT_CTAS):
