@@ -322,7 +322,12 @@ def run_sparse(args, rank, world, torch, dist):
                    "kernel_time_top": {k: v for k, v in top}},
         "roofline": {"bound": "tensor", "achieved": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12,
                      "peak": peak, "unit": "TFLOP/s",
-                     "frac": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12 / peak, "traffic": None,
+                     "frac": prof["flops"] / max(prof["seconds"], 1e-12) / 1e12 / peak,
+                     # dram__bytes_read.sum + dram__bytes_write.sum of every grouped-GEMM
+                     # launch of one config[4] numeric pass (ncu, profiles/r02/
+                     # ncu_gemm_dram_cfg4.txt): 241.4 GB over 7905 launches
+                     "traffic": 241.4e9 / 7905 if cfg == 4 else None,
+                     "traffic_unit": "bytes per launch (mean over one numeric pass, ncu; not this run)",
                      "kernel": "gemm_grouped_kernel (all grouped GEMM launches of one factor+PCG)",
                      "kernel_seconds": prof["seconds"], "kernel_share_of_step": prof["seconds"] / t,
                      "all_kernels_seconds": busy_s,

@@ -535,17 +535,20 @@ int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
     RSC_CHECK_LAUNCH();
     static const bool log = getenv("RSC_GEMM_LOG") != nullptr;  // diagnostics: one line per launch
     if (log) {
-        double fl = 0.0, pad = 0.0;
+        double fl = 0.0, pad = 0.0, pad32m = 0.0, pad32n = 0.0;
         int maxk = 0;
         for (int i = 0; i < args.count; ++i) {
             const rsc_gemm_problem &p = args.p[i];
+            const double pk = (double)((p.K + BK - 1) / BK * BK) * p.batch;
+            const double pm = (p.M + BM - 1) / BM * BM, pn = (p.N + BN - 1) / BN * BN;
             fl += 2.0 * p.M * p.N * (double)p.K * p.batch;
-            pad += 2.0 * ((p.M + BM - 1) / BM * BM) * ((p.N + BN - 1) / BN * BN) * (double)((p.K + BK - 1) / BK * BK) *
-                   p.batch;
+            pad += 2.0 * pm * pn * pk;
+            pad32m += 2.0 * ((p.M + 31) / 32 * 32) * pn * pk;  // with 32-row tiles
+            pad32n += 2.0 * pm * ((p.N + 31) / 32 * 32) * pk;  // with 32-column tiles
             maxk = std::max(maxk, p.K);
         }
-        fprintf(stderr, "GEMMLOG %d %d %d tiles %lld probs %d flops %.0f padded %.0f maxk %d\n", (int)TA, (int)TB,
-                (int)GATHER, tiles, args.count, fl, pad, maxk);
+        fprintf(stderr, "GEMMLOG %d %d %d tiles %lld probs %d flops %.0f padded %.0f maxk %d pad32m %.0f pad32n %.0f\n",
+                (int)TA, (int)TB, (int)GATHER, tiles, args.count, fl, pad, maxk, pad32m, pad32n);
     }
     return 0;
 }

@@ -202,7 +202,7 @@ def test_tree_trsm_matches_device_tree(cuda, trans):
         assert relerr(Xc.cpu().numpy(), Xr.cpu().numpy()) < 1e-13
 
 
-def test_apply_sweep_reproduces_device_apply(cuda):
+def test_apply_sweep_reproduces_device_apply(cuda, monkeypatch):
     """factor.py:175-218 through rsc_apply_sweep: the apply program's phases (forward
     then backward) replayed from flat C arrays give the package's apply."""
     import torch
@@ -212,7 +212,7 @@ def test_apply_sweep_reproduces_device_apply(cuda):
     from paper_1507_05593_b200.apply import DeviceApply
 
     F, _ = _factor_with_trees()
-    DeviceApply.TASK_BYTES = 0
+    monkeypatch.setattr(DeviceApply, "TASK_BYTES", 0)  # phases only: the program is a flat sweep
     ap = DeviceApply(F)
     r = E.to_dev(np.random.default_rng(25).standard_normal(F.n))
     z_ref = E.empty(F.n)
