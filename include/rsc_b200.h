@@ -198,6 +198,10 @@ int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long long total_bl
  * accumulating ops use FP64 atomics.  Replaces the per-level launches of the
  * small units: one launch per sweep. */
 int rsc_apply_tasks(const void *ops, const int *task_ptr_dev, int ntasks, void *stream);
+/* The same op lists run by thread-block clusters of C <= 8 CTAs (one cluster per
+ * task: the Alg. 4 chain of one diagonal block tree); each op's blocks are dealt to
+ * the cluster's CTAs and a cluster barrier separates consecutive ops. */
+int rsc_apply_cluster_tasks(const void *ops, const int *task_ptr_dev, int ntasks, int C, void *stream);
 
 
 

@@ -49,6 +49,7 @@ EXPORTED = (
     "rsc_gemv_describe",
     "rsc_gemv_multi_dev",
     "rsc_apply_tasks",
+    "rsc_apply_cluster_tasks",
     "rsc_identity_batched",
     "rsc_transpose_batched",
     "rsc_gather_rows",
@@ -124,6 +125,7 @@ _SIGS = {
     "rsc_gemv_describe": (I, [I, P, P, P, P, P, P, P, P, P, P, P, P]),
     "rsc_gemv_multi_dev": (I, [P, P, LL, P]),
     "rsc_apply_tasks": (I, [P, P, I, P]),
+    "rsc_apply_cluster_tasks": (I, [P, P, I, I, P]),
 
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_identity_batched": (I, [I, P, P, P, P]),

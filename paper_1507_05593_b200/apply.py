@@ -52,6 +52,17 @@ class _Phase:
             self.items.append(item)
 
 
+class _ClusterTasks:
+    """One launch of cluster tasks (rsc_apply_cluster_tasks): the Alg. 4 op list of
+    every diagonal block tree of a level, one thread-block cluster per tree."""
+
+    items = ()
+    lr = ()
+
+    def __init__(self, ops):
+        self.ops = ops  # [_Phase]: one ordered op list per tree
+
+
 def _cap(lr):
     """Column capacity of a low-rank block: its U / V are views of the sketch-padded
     buffers (numeric._finalize_ranks), so a refactorization's rank fits this."""
@@ -221,6 +232,9 @@ class DeviceApply:
         self.launches = []
         self._lr_index = []  # (launch, item, U ptr): the items whose cols is a rank
         for ph in self.phases:
+            if isinstance(ph, _ClusterTasks):
+                self.launches.append((0, None, None))
+                continue
             self._lr_index.extend((len(self.launches), i, key) for i, key in ph.lr)
             c = list(zip(*ph.items))
             arrs = [ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3]), ptr_array(c[4]),
@@ -230,6 +244,34 @@ class DeviceApply:
         self._fn = lib.rsc_gemv_multi
         self._build_dev()
         self._build_tasks()
+        self._build_cluster_tasks()
+
+    def _build_cluster_tasks(self):
+        """Device descriptors of every cluster-task launch (rsc_gemv_describe over all
+        ops of the launch's trees plus one sentinel, per-tree op offsets)."""
+        lib = _lib.load()
+        db = lib.rsc_gemv_desc_bytes()
+        self.ctask_dev = {}
+        self._ctask_lr = []  # (phase index, tree index, item index, U ptr)
+        for li, ph in enumerate(self.phases):
+            if not isinstance(ph, _ClusterTasks):
+                continue
+            items, ptr = [], [0]
+            for ti, op in enumerate(ph.ops):
+                self._ctask_lr.extend((li, ti, i, key) for i, key in op.lr)
+                items.extend(op.items)
+                ptr.append(len(items))
+            items = items + [(items[0][0], 0, 0, 1, items[0][4], 0, items[0][6], 0, 0, 0.0)]  # sentinel
+            c = list(zip(*items))
+            arrs = [ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3]), ptr_array(c[4]),
+                    ptr_array(c[5]), ptr_array(c[6]), ptr_array(c[7]), int_array(c[8]),
+                    np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))]
+            n = len(items)
+            desc = np.empty(n * db, dtype=np.uint8)
+            blocks = np.empty(n, dtype=np.int64)
+            _lib.check(lib.rsc_gemv_describe(n, *[a.ctypes.data for a in arrs], desc.ctypes.data,
+                                             blocks.ctypes.data), "rsc_gemv_describe")
+            self.ctask_dev[li] = (E.to_dev(desc), E.to_dev(np.asarray(ptr, dtype=np.int32)), len(ph.ops))
 
     def _build_tasks(self):
         """Device descriptors of the subtree tasks of both sweeps (rsc_apply_tasks)."""
@@ -290,9 +332,9 @@ class DeviceApply:
                 for b in u.diag.blocks.values():
                     if isinstance(b, DevLR):
                         ks[b.U.data_ptr()] = b.k
-        if set(ks) != {key for _, _, key in self._lr_index} or len(F.dunits) != self.nunits:
-            return False
-        if {key for _, _, key in self._task_lr} - set(ks):
+        have = ({key for _, _, key in self._lr_index} | {key for _, _, key in self._task_lr}
+                | {key for _, _, _, key in self._ctask_lr})
+        if set(ks) != have or len(F.dunits) != self.nunits:
             return False
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]
@@ -304,6 +346,12 @@ class DeviceApply:
                     it[2] = ks[key]
                     ph.items[i] = tuple(it)
         self._build_tasks()
+        for li, ti, ii, key in self._ctask_lr:
+            op = self.phases[li].ops[ti]
+            it = list(op.items[ii])
+            it[2] = ks[key]
+            op.items[ii] = tuple(it)
+        self._build_cluster_tasks()
         self.graph = None
         self.calls = min(self.calls, self.GRAPH_AFTER)
         return True
@@ -322,7 +370,13 @@ class DeviceApply:
         for li, (n, _, args) in enumerate(self.launches):
             if li == self.n_local_fwd and self.dist:
                 self._reduce_top()
-            if li in dev:
+            if li in self.ctask_dev:
+                d, ptr, nt = self.ctask_dev[li]
+                _lib.check(lib.rsc_apply_cluster_tasks(d.data_ptr(), ptr.data_ptr(), nt, self.CLUSTER, s),
+                           "rsc_apply_cluster_tasks")
+            elif n == 0:
+                continue
+            elif li in dev:
                 d, b2p, tot = dev[li]
                 _lib.check(fdev(d.data_ptr(), b2p.data_ptr(), tot, s), "rsc_gemv_multi_dev")
             else:
@@ -418,16 +472,20 @@ class DeviceApply:
             first = _Phase()
             for u in dense:
                 self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, False)
-            first = self._tree_waves(trees, rhs, out, False, first)
+            small, big = self._split_trees(trees)
+            first = self._tree_waves(big, rhs, out, False, first)
             self._emit(first)
+            self._tree_cluster_tasks(small, rhs, out, False)
             self._couplings(cpl, plan, rhs, out, False)
         else:
             self._couplings(cpl, plan, rhs, out, True)
             first = _Phase()
             for u in dense:
                 self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, True)
-            first = self._tree_waves(trees, rhs, out, True, first)
+            small, big = self._split_trees(trees)
+            first = self._tree_waves(big, rhs, out, True, first)
             self._emit(first)
+            self._tree_cluster_tasks(small, rhs, out, True)
 
     def _couplings(self, cpl, plan, rhs, out, backward):
         a, b = _Phase(), _Phase()
@@ -457,6 +515,67 @@ class DeviceApply:
             a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out + c0, 0, rhs, rows, 0 | excl, -1.0)
         else:  # w -= L_O^T y[R]
             a.add(u.off.data_ptr(), u.rows.size, u.ncols, E.ld(u.off), out, rows, rhs + c0, 0, 1 | excl, -1.0)
+
+    # Alg. 4 of the diagonal trees as cluster tasks (one cluster per tree, its ops in
+    # order) instead of lock-step waves of dependent launches.  Off by default: on
+    # config[4] the apply measured 8.57 ms with waves, 8.9-9.2 ms with cluster tasks
+    # for the trees under 0.25-2 MB per op and 18.2 ms for all trees
+    # (profiles/r02/apply_tree_cluster_cfg4.txt): one 8-CTA cluster streams a tree's
+    # ops no faster than a dependent launch over the whole GPU.
+    TREE_CLUSTER = os.environ.get("RSC_APPLY_TREE_CLUSTER", "0") == "1"  # measured slower on config[4] (below)
+    CLUSTER = 8
+    # trees whose largest op moves more than this run as lock-step waves over the
+    # whole GPU (one cluster's bandwidth is too low for them)
+    TREE_CLUSTER_OP_BYTES = int(float(os.environ.get("RSC_APPLY_TREE_CLUSTER_MB", "0.5")) * (1 << 20))
+
+    def _split_trees(self, trees):
+        """(cluster-task trees, wave trees) by the bytes of each tree's largest op."""
+        if not self.TREE_CLUSTER:
+            return [], trees
+        small, big = [], []
+        for u in trees:
+            mx = 0
+            for b in u.diag.blocks.values():
+                if isinstance(b, DevLR):
+                    mx = max(mx, 8 * max(b.V.shape[0], b.U.shape[0]) * _cap(b))
+                elif isinstance(b, DenseTri):
+                    mx = max(mx, 4 * b.n * b.n)  # the explicit inverse's triangle
+                else:
+                    mx = max(mx, 8 * b.numel())
+            (small if mx <= self.TREE_CLUSTER_OP_BYTES else big).append(u)
+        return small, big
+
+    def _tree_cluster_tasks(self, trees, rhs, out, backward):
+        from .numeric import tree_ops
+
+        ybase = self.y.data_ptr()
+        off = lambda v: v.data_ptr() - ybase  # tree_ops hands out views of self.y
+        lists = []
+        for u in trees:
+            ph = _Phase()
+            for op in tree_ops(u.diag, None, self.y[u.c0:u.c1], backward):
+                if op[0] == "leaf":
+                    if op[1].n:
+                        self._solve(ph, op[1], rhs + off(op[2]), out + off(op[2]), backward)
+                    continue
+                _, b, Xs, Yd, tr = op
+                xp, yp = out + off(Xs), rhs + off(Yd)
+                if isinstance(b, DevLR):
+                    t = self._t(_cap(b))
+                    P1, P2 = (b.V, b.U) if tr else (b.U, b.V)
+                    key = b.U.data_ptr()
+                    # t = P1^T x: column sums over row slabs dealt to several CTAs (atomic)
+                    ph.add(P1.data_ptr(), P1.shape[0], b.k, E.ld(P1), xp, 0, t, 0, 1, 1.0, lr=key)
+                    # y -= P2 t: rows partitioned over the CTAs (exclusive)
+                    ph.add(P2.data_ptr(), P2.shape[0], b.k, E.ld(P2), t, 0, yp, 0, 0 | 16, -1.0, lr=key)
+                elif tr:  # Y -= B^T X: column sums (atomic)
+                    ph.add(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), xp, 0, yp, 0, 1, -1.0)
+                else:  # Y -= B X: rows (exclusive)
+                    ph.add(b.data_ptr(), b.shape[0], b.shape[1], E.ld(b), xp, 0, yp, 0, 0 | 16, -1.0)
+            if ph.items:
+                lists.append(ph)
+        if lists:
+            self.phases.append(_ClusterTasks(lists))
 
     def _tree_waves(self, trees, rhs, out, backward, first):
         """Alg. 4 of every tree in `trees`, in lock-step waves; wave w's leaf solves,

@@ -10,6 +10,7 @@
 //  gemv_batched : y[yidx[r]] += alpha * M[r,:] . x[xidx]     (trans = 0, warp per row)
 //                 y[c]       += alpha * sum_r M[r,c] x[xidx[r]]  (trans = 1, thread per column)
 //                 FP64 atomics on the output (units of one level share target rows).
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -284,6 +285,34 @@ __global__ void __launch_bounds__(T) apply_tasks_kernel(const GemvProb *__restri
     }
 }
 
+// Cluster tasks: one thread-block cluster of C CTAs per task (the Alg. 4 op list of
+// one diagonal block tree, diagblocks.py:192-273).  CTA q of the cluster runs blocks
+// q, q + C, ... of each op, and a cluster barrier (release / acquire at cluster
+// scope) separates consecutive ops -- a tree's dependent chain of leaf solves and
+// couplings costs one cluster barrier per op instead of one dependent kernel launch
+// per wave.  Ops whose blocks share outputs across CTAs (column sums) keep their
+// atomic epilogue; row-partitioned ops are exclusive per block.
+__global__ void __launch_bounds__(T) apply_cluster_tasks_kernel(const GemvProb *__restrict__ ops,
+                                                                 const int *__restrict__ task_ptr, int C) {
+    __shared__ double xr[SLAB];
+    __shared__ double part[T];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int task = blockIdx.x / C, q = (int)cl.block_rank();
+    const int o0 = __ldg(task_ptr + task), o1 = __ldg(task_ptr + task + 1);
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    for (int o = o0; o < o1; ++o) {
+        const GemvProb d = ops[o];
+        const long long nb = ops[o + 1].blk_begin - d.blk_begin;  // ops end with a sentinel
+        for (long long lb = q; lb < nb; lb += C) {
+            gemv_block(d, lb, xr, part);
+            __syncthreads();  // xr / part reuse by the next block
+        }
+        cl.sync();  // the next op reads this op's results
+    }
+}
+
 inline int pow2ceil(int v) {
     int p = 1;
     while (p < v) p <<= 1;
@@ -439,6 +468,28 @@ extern "C" int rsc_apply_tasks(const void *ops, const int *task_ptr_dev, int nta
     cfg.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, apply_tasks_kernel, static_cast<const GemvProb *>(ops),
                                              task_ptr_dev);
+    rsc_count_launch();
+    return e == cudaSuccess ? 0 : (int)e;
+}
+
+extern "C" int rsc_apply_cluster_tasks(const void *ops, const int *task_ptr_dev, int ntasks, int C, void *stream) {
+    if (ntasks < 0 || C < 1 || C > 8) return -3;
+    if (ntasks == 0) return 0;
+    if (!ops || !task_ptr_dev) return -1;
+    static const bool no_pdl = getenv("RSC_APPLY_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+    cfg.gridDim = dim3((unsigned)ntasks * C);
+    cfg.blockDim = dim3(T);
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, apply_cluster_tasks_kernel, static_cast<const GemvProb *>(ops),
+                                             task_ptr_dev, C);
     rsc_count_launch();
     return e == cudaSuccess ? 0 : (int)e;
 }

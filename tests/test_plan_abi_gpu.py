@@ -213,6 +213,7 @@ def test_apply_sweep_reproduces_device_apply(cuda, monkeypatch):
 
     F, _ = _factor_with_trees()
     monkeypatch.setattr(DeviceApply, "TASK_BYTES", 0)  # phases only: the program is a flat sweep
+    monkeypatch.setattr(DeviceApply, "TREE_CLUSTER", False)
     ap = DeviceApply(F)
     r = E.to_dev(np.random.default_rng(25).standard_normal(F.n))
     z_ref = E.empty(F.n)
