@@ -307,6 +307,38 @@ int rsc_csr_windows(long long nq, long long n, const long long *indptr, const lo
                     const long long *rp_off, const long long *nz_off, int *rowptr, int *colidx,
                     int *val);
 
+/* ---- The apply as one dataflow launch (factor.py:175-218) -------------------------
+ * rsc_flow_deps (host): the op graph of the apply's GEMV ops given in a valid
+ * sequential order -- op o reads x elements (contiguous from xaddr[o], or
+ * xaddr[o] + 8*idx[k] for an index list at device address xidx[o], xlen[o] of them)
+ * and writes y elements likewise (yassign[o] != 0: assignment, else accumulation,
+ * which commutes with other accumulations).  Vector addresses lie in the nbuf
+ * buffers [buf_base, buf_base + 8*buf_len); index lists are read from idx_host, the
+ * host copy of the device index buffer at idx_dev (idx_len ints).  Writes need[o]
+ * (predecessor count) and the successor CSR (succ_ptr nops+1, succ); returns the
+ * edge count (> succ_cap: nothing written to succ, call again with that capacity),
+ * <0 on bad input.
+ * rsc_flow_describe: descriptors (rsc_gemv_desc_bytes each) of the ops in queue
+ * order, at least one item per op, items numbered globally; item_op (total ints,
+ * may be null) = item -> op.  Returns the item count.
+ * rsc_apply_flow: zeroes `state` (1 + 2*nops ints) and runs every item in one
+ * persistent launch: an item waits until its op's predecessors have all completed. */
+long long rsc_flow_deps(int nops, const long long *xaddr, const long long *xidx, const int *xlen,
+                        const long long *yaddr, const long long *yidx, const int *ylen, const int *yassign,
+                        int nbuf, const long long *buf_base, const long long *buf_len, const int *idx_host,
+                        long long idx_dev, long long idx_len, int *need, int *succ_ptr, int *succ,
+                        long long succ_cap);
+long long rsc_flow_describe(int count, const double *const *M, const int *rows, const int *cols, const int *ldm,
+                            const double *const *x, const int *const *xidx, double *const *y,
+                            const int *const *yidx, const int *modes, const double *alphas, void *desc,
+                            int *item_op);
+int rsc_apply_flow(const void *ops, const int *item_op, const int *need, const int *succ_ptr, const int *succ,
+                   int *state, int nops, int total, void *stream);
+/* Diagnostics: the same launch recording, per item, 4 uint64 into `trace` (device,
+ * 4*total): %globaltimer when taken, after its dependency wait, at completion; SM id. */
+int rsc_apply_flow_trace(const void *ops, const int *item_op, const int *need, const int *succ_ptr,
+                         const int *succ, int *state, int nops, int total, void *trace, void *stream);
+
 /* ---- Plan compiler (plan.py NumericPlan; host threads) --------------------------
  * rsc_plan_pairs: every (target supernode j, update source s) pair with a row of s
  * inside C_j (is_target[j] != 0), grouped by target, sources by src_order within a

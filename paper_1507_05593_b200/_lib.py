@@ -50,6 +50,10 @@ EXPORTED = (
     "rsc_gemv_multi_dev",
     "rsc_apply_tasks",
     "rsc_apply_cluster_tasks",
+    "rsc_flow_describe",
+    "rsc_apply_flow",
+    "rsc_apply_flow_trace",
+    "rsc_flow_deps",
     "rsc_identity_batched",
     "rsc_transpose_batched",
     "rsc_gather_rows",
@@ -126,6 +130,10 @@ _SIGS = {
     "rsc_gemv_multi_dev": (I, [P, P, LL, P]),
     "rsc_apply_tasks": (I, [P, P, I, P]),
     "rsc_apply_cluster_tasks": (I, [P, P, I, I, P]),
+    "rsc_flow_describe": (LL, [I, P, P, P, P, P, P, P, P, P, P, P, P]),
+    "rsc_apply_flow": (I, [P, P, P, P, P, P, I, I, P]),
+    "rsc_apply_flow_trace": (I, [P, P, P, P, P, P, I, I, P, P]),
+    "rsc_flow_deps": (LL, [I, P, P, P, P, P, P, P, I, P, P, P, LL, LL, P, P, P, LL]),
 
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_identity_batched": (I, [I, P, P, P, P]),

@@ -106,7 +106,9 @@ class DeviceApply:
         uidx = {un.u: i for i, un in enumerate(units)}
         self.dist = getattr(F, "dist", None)
         shared = set(self.dist["top_units"]) if self.dist else set()
-        task_of = self._subtree_tasks(units, plan) if not self.dist else np.full(len(units), -1, dtype=np.int64)
+        self.flow = self.FLOW and not self.dist
+        task_of = self._subtree_tasks(units, plan) if not (self.dist or self.flow) else \
+            np.full(len(units), -1, dtype=np.int64)
 
         def levels(members):
             lv = {}
@@ -149,8 +151,70 @@ class DeviceApply:
             # rows (in the permuted order) this rank's result is exact on: its own + the top
             self.exact_cols = np.concatenate([own, cols]).astype(np.int64)
         self._pack()
+        self._idx = plan.idx
+        if self.flow:
+            self._build_flow()
         self.graph = None
         self.calls = 0
+
+    # -- the dataflow program ------------------------------------------------------
+    # The whole apply as one persistent launch (rsc_apply_flow): the level phases
+    # above give a valid sequential order of the GEMV ops; rsc_flow_deps turns it into
+    # the op graph (hazards on the vectors), and the kernel runs every op as soon as
+    # the ops feeding it are done.  Off by default (RSC_APPLY_FLOW=1 turns it on): on
+    # config[4] it measured 10.2 ms against 8.4 ms for the level phases + subtree
+    # tasks (profiles/r02/apply_flow_cfg4.txt).  Its trace shows why: the critical
+    # path is 898 dependent ops long (the top separators' unit chain, three GEMVs per
+    # low-rank unit), 1.7 us of signal latency plus ~6 us per op -- the same chain the
+    # phases walk, with a per-item cost the launch-per-phase path does not pay.
+    FLOW = os.environ.get("RSC_APPLY_FLOW", "0") == "1"
+
+    def _build_flow(self):
+        lib = _lib.load()
+        items = [it for ph in self.phases for it in ph.items]
+        nops = len(items)
+        self.flow_nops = nops
+        if nops == 0:
+            self.flow_dev = None
+            return
+        c = list(zip(*items))
+        M, rows, cols, ld = ptr_array(c[0]), int_array(c[1]), int_array(c[2]), int_array(c[3])
+        x, xi, y, yi = ptr_array(c[4]), ptr_array(c[5]), ptr_array(c[6]), ptr_array(c[7])
+        modes = int_array(c[8])
+        alphas = np.ascontiguousarray(np.asarray(c[9], dtype=np.float64))
+        trans = (modes & 1).astype(bool)
+        xlen = np.where(trans, rows, cols).astype(np.int32)
+        ylen = np.where(trans, cols, rows).astype(np.int32)
+        asg = ((modes & 4) != 0).astype(np.int32)
+        bases = np.array([self.y.data_ptr(), self.y2.data_ptr(), self.tall.data_ptr()], dtype=np.int64)
+        lens = np.array([self.n, self.n, self.tall.numel()], dtype=np.int64)
+        idx = self._idx
+        need = np.empty(nops, dtype=np.int32)
+        sptr = np.empty(nops + 1, dtype=np.int32)
+        cap = 8 * nops
+        while True:
+            succ = np.empty(max(cap, 1), dtype=np.int32)
+            ne = lib.rsc_flow_deps(nops, x.ctypes.data, xi.ctypes.data, xlen.ctypes.data, y.ctypes.data,
+                                   yi.ctypes.data, ylen.ctypes.data, asg.ctypes.data, 3, bases.ctypes.data,
+                                   lens.ctypes.data, idx.host.ctypes.data, idx.dev.data_ptr(), idx.host.size,
+                                   need.ctypes.data, sptr.ctypes.data, succ.ctypes.data, cap)
+            if ne < 0:
+                raise RuntimeError(f"rsc_flow_deps failed ({ne})")
+            if ne <= cap:
+                break
+            cap = ne
+        args = [M.ctypes.data, rows.ctypes.data, cols.ctypes.data, ld.ctypes.data, x.ctypes.data, xi.ctypes.data,
+                y.ctypes.data, yi.ctypes.data, modes.ctypes.data, alphas.ctypes.data]
+        db = lib.rsc_gemv_desc_bytes()
+        desc = np.empty(nops * db, dtype=np.uint8)
+        total = lib.rsc_flow_describe(nops, *args, desc.ctypes.data, None)
+        item_op = np.empty(total, dtype=np.int32)
+        total = lib.rsc_flow_describe(nops, *args, desc.ctypes.data, item_op.ctypes.data)
+        self.flow_edges = int(ne)
+        self.flow_items = int(total)
+        self.flow_dev = (E.to_dev(desc), E.to_dev(item_op), E.to_dev(need), E.to_dev(sptr),
+                         E.to_dev(succ[:max(int(ne), 1)]), torch.zeros(1 + 2 * nops, dtype=torch.int32,
+                                                                       device="cuda"))
 
     # -- subtree tasks -------------------------------------------------------------
     TASK_BYTES = int(float(os.environ.get("RSC_APPLY_TASK_MB", "1")) * (1 << 20))  # subtree tasks up to 1 MB (measured 3-5% faster applies on config[4])
@@ -338,6 +402,13 @@ class DeviceApply:
             return False
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]
+        for ph in self.phases:  # the flow program is rebuilt from the phase items
+            for i, key in ph.lr:
+                it = list(ph.items[i])
+                it[2] = ks[key]
+                ph.items[i] = tuple(it)
+        if self.flow:
+            self._build_flow()
         self._build_dev()  # the device descriptors carry the ranks too
         for bw, lst in self.tasks.items():  # task ops: rebuild with the new ranks
             for _, ph in lst:
@@ -359,6 +430,13 @@ class DeviceApply:
     def _run_program(self):
         s = E.stream_handle()
         lib = _lib.load()
+        if self.flow:
+            if self.flow_dev is not None:
+                d, io, nd, sp, sc, st = self.flow_dev
+                _lib.check(lib.rsc_apply_flow(d.data_ptr(), io.data_ptr(), nd.data_ptr(), sp.data_ptr(),
+                                              sc.data_ptr(), st.data_ptr(), self.flow_nops, self.flow_items, s),
+                           "rsc_apply_flow")
+            return
         dev, fdev = self.dev, lib.rsc_gemv_multi_dev
 
         def tasks(bw):
@@ -530,7 +608,7 @@ class DeviceApply:
 
     def _split_trees(self, trees):
         """(cluster-task trees, wave trees) by the bytes of each tree's largest op."""
-        if not self.TREE_CLUSTER:
+        if not self.TREE_CLUSTER or self.flow:
             return [], trees
         small, big = [], []
         for u in trees:

@@ -125,6 +125,7 @@ struct GemvProb {
     long long blk_begin;        // first block of this problem (within its launch / phase)
     int rows, cols, ld;
     int mode, lpr;              // lanes per row (transpose 0) / column tile width (transpose 1)
+    int nblk, grp;              // dataflow program: blocks of the op, blocks per item
 };
 
 struct GemvArgs {
@@ -135,7 +136,17 @@ struct GemvArgs {
 
 __device__ __forceinline__ double ldnc(const double *p) { return __ldg(p); }
 
+// x reads: through L1 (read-only path) for phases separated by kernel boundaries;
+// L2 only (ld.global.cg) inside the dataflow kernel, where x was written by other
+// CTAs of the same launch
+template <bool CG>
+__device__ __forceinline__ double ldx(const double *p) {
+    if constexpr (CG) return __ldcg(p);
+    else return *p;
+}
+
 // one CTA-block of work of problem d (block index lb within the problem)
+template <bool CG = false>
 __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, double *xr, double *part) {
     const int mode = d.mode;
     const bool trans = mode & 1, lower = mode & 2, assign = mode & 4, upper = mode & 8;
@@ -153,7 +164,51 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
         const int nseg = T / lpr;
         const int r = (int)lb * nseg + seg;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (r < rows) {
+        if (r < rows && (mode & 32)) {
+            // rows 16-byte aligned: double2 loads of column pairs (2p, 2p+1), four pairs in
+            // flight per lane; a lone first / last column is done by one lane
+            const double *Mr = M + (long long)r * ld;
+            const double2 *M2 = reinterpret_cast<const double2 *>(Mr);
+            const int cend = lower ? min(cols, r + 1) : cols;
+            int cb = upper ? r : 0;
+            if ((cb & 1) && cb < cend) {
+                if (sub == 0) s0 += ldnc(Mr + cb) * ldx<CG>(x + (xi ? __ldg(xi + cb) : cb));
+                ++cb;
+            }
+            const int pend = cend >> 1;
+            if ((cend & 1) && cend - 1 >= cb && sub == lpr - 1)
+                s1 += ldnc(Mr + cend - 1) * ldx<CG>(x + (xi ? __ldg(xi + cend - 1) : cend - 1));
+            int p = (cb >> 1) + sub;
+            if (xi) {
+                for (; p + 3 * lpr < pend; p += 4 * lpr) {
+                    const double2 m0 = __ldg(M2 + p), m1 = __ldg(M2 + p + lpr), m2 = __ldg(M2 + p + 2 * lpr),
+                                  m3 = __ldg(M2 + p + 3 * lpr);
+                    const int c0 = 2 * p, c1 = 2 * (p + lpr), c2 = 2 * (p + 2 * lpr), c3 = 2 * (p + 3 * lpr);
+                    s0 += m0.x * ldx<CG>(x + __ldg(xi + c0)) + m0.y * ldx<CG>(x + __ldg(xi + c0 + 1));
+                    s1 += m1.x * ldx<CG>(x + __ldg(xi + c1)) + m1.y * ldx<CG>(x + __ldg(xi + c1 + 1));
+                    s2 += m2.x * ldx<CG>(x + __ldg(xi + c2)) + m2.y * ldx<CG>(x + __ldg(xi + c2 + 1));
+                    s3 += m3.x * ldx<CG>(x + __ldg(xi + c3)) + m3.y * ldx<CG>(x + __ldg(xi + c3 + 1));
+                }
+                for (; p < pend; p += lpr) {
+                    const double2 m = __ldg(M2 + p);
+                    s0 += m.x * ldx<CG>(x + __ldg(xi + 2 * p)) + m.y * ldx<CG>(x + __ldg(xi + 2 * p + 1));
+                }
+            } else {
+                for (; p + 3 * lpr < pend; p += 4 * lpr) {
+                    const double2 m0 = __ldg(M2 + p), m1 = __ldg(M2 + p + lpr), m2 = __ldg(M2 + p + 2 * lpr),
+                                  m3 = __ldg(M2 + p + 3 * lpr);
+                    const int c0 = 2 * p, c1 = 2 * (p + lpr), c2 = 2 * (p + 2 * lpr), c3 = 2 * (p + 3 * lpr);
+                    s0 += m0.x * ldx<CG>(x + c0) + m0.y * ldx<CG>(x + c0 + 1);
+                    s1 += m1.x * ldx<CG>(x + c1) + m1.y * ldx<CG>(x + c1 + 1);
+                    s2 += m2.x * ldx<CG>(x + c2) + m2.y * ldx<CG>(x + c2 + 1);
+                    s3 += m3.x * ldx<CG>(x + c3) + m3.y * ldx<CG>(x + c3 + 1);
+                }
+                for (; p < pend; p += lpr) {
+                    const double2 m = __ldg(M2 + p);
+                    s0 += m.x * ldx<CG>(x + 2 * p) + m.y * ldx<CG>(x + 2 * p + 1);
+                }
+            }
+        } else if (r < rows) {
             const double *Mr = M + (long long)r * ld;
             const int cend = lower ? min(cols, r + 1) : cols;
             int c = (upper ? r : 0) + sub;
@@ -162,22 +217,22 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
                 for (; c + 3 * lpr < cend; c += step) {
                     const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + lpr), m2 = ldnc(Mr + c + 2 * lpr),
                                  m3 = ldnc(Mr + c + 3 * lpr);
-                    s0 += m0 * x[__ldg(xi + c)];
-                    s1 += m1 * x[__ldg(xi + c + lpr)];
-                    s2 += m2 * x[__ldg(xi + c + 2 * lpr)];
-                    s3 += m3 * x[__ldg(xi + c + 3 * lpr)];
+                    s0 += m0 * ldx<CG>(x + __ldg(xi + c));
+                    s1 += m1 * ldx<CG>(x + __ldg(xi + c + lpr));
+                    s2 += m2 * ldx<CG>(x + __ldg(xi + c + 2 * lpr));
+                    s3 += m3 * ldx<CG>(x + __ldg(xi + c + 3 * lpr));
                 }
-                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * x[__ldg(xi + c)];
+                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * ldx<CG>(x + __ldg(xi + c));
             } else {
                 for (; c + 3 * lpr < cend; c += step) {
                     const double m0 = ldnc(Mr + c), m1 = ldnc(Mr + c + lpr), m2 = ldnc(Mr + c + 2 * lpr),
                                  m3 = ldnc(Mr + c + 3 * lpr);
-                    s0 += m0 * x[c];
-                    s1 += m1 * x[c + lpr];
-                    s2 += m2 * x[c + 2 * lpr];
-                    s3 += m3 * x[c + 3 * lpr];
+                    s0 += m0 * ldx<CG>(x + c);
+                    s1 += m1 * ldx<CG>(x + c + lpr);
+                    s2 += m2 * ldx<CG>(x + c + 2 * lpr);
+                    s3 += m3 * ldx<CG>(x + c + 3 * lpr);
                 }
-                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * x[c];
+                for (; c < cend; c += lpr) s0 += ldnc(Mr + c) * ldx<CG>(x + c);
             }
         }
         double s = (s0 + s1) + (s2 + s3);
@@ -193,8 +248,58 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
         const int ntile = (cols + CTILE - 1) / CTILE;
         const int slab = (int)(lb / ntile), tile = (int)(lb % ntile);
         const int r0 = slab * SLAB, r1 = min(rows, r0 + SLAB);
-        for (int r = r0 + t; r < r1; r += T) xr[r - r0] = x[xi ? __ldg(xi + r) : r];
+        for (int r = r0 + t; r < r1; r += T) xr[r - r0] = ldx<CG>(x + (xi ? __ldg(xi + r) : r));
         __syncthreads();
+        if ((mode & 32) && !lower) {
+            // column pairs: a thread owns columns (c, c+1), double2 loads down its rows
+            const int cwp = cw >> 1;              // pair-threads per row group (16 .. 128)
+            const int nsub = T / cwp;
+            const int sub = t / cwp, c = tile * CTILE + 2 * (t % cwp);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+            if (c + 1 < cols) {
+                int r = r0 + sub;
+                const double *Mc = M + (long long)r * ld + c;
+                const long long st = (long long)nsub * ld;
+                for (; r + 3 * nsub < r1; r += 4 * nsub, Mc += 4 * st) {
+                    const double2 m0 = __ldg(reinterpret_cast<const double2 *>(Mc)),
+                                  m1 = __ldg(reinterpret_cast<const double2 *>(Mc + st)),
+                                  m2 = __ldg(reinterpret_cast<const double2 *>(Mc + 2 * st)),
+                                  m3 = __ldg(reinterpret_cast<const double2 *>(Mc + 3 * st));
+                    const double x0 = xr[r - r0], x1 = xr[r + nsub - r0], x2 = xr[r + 2 * nsub - r0],
+                                 x3 = xr[r + 3 * nsub - r0];
+                    a0 += m0.x * x0; b0 += m0.y * x0;
+                    a1 += m1.x * x1; b1 += m1.y * x1;
+                    a2 += m2.x * x2; b2 += m2.y * x2;
+                    a3 += m3.x * x3; b3 += m3.y * x3;
+                }
+                for (; r < r1; r += nsub, Mc += st) {
+                    const double2 m = __ldg(reinterpret_cast<const double2 *>(Mc));
+                    a0 += m.x * xr[r - r0];
+                    b0 += m.y * xr[r - r0];
+                }
+            } else if (c < cols) {
+                for (int r = r0 + sub; r < r1; r += nsub) a0 += ldnc(M + (long long)r * ld + c) * xr[r - r0];
+            }
+            part[2 * t] = (a0 + a1) + (a2 + a3);
+            part[2 * t + 1] = (b0 + b1) + (b2 + b3);
+            __syncthreads();
+            if (sub == 0 && c < cols) {
+                double sa = part[2 * t], sb = part[2 * t + 1];
+                for (int q = 1; q < nsub; ++q) {
+                    sa += part[2 * (t + q * cwp)];
+                    sb += part[2 * (t + q * cwp) + 1];
+                }
+                double *da = y + (yi ? __ldg(yi + c) : c);
+                if (mode & 16) *da += alpha * sa;
+                else atomicAdd(da, alpha * sa);
+                if (c + 1 < cols) {
+                    double *db = y + (yi ? __ldg(yi + c + 1) : c + 1);
+                    if (mode & 16) *db += alpha * sb;
+                    else atomicAdd(db, alpha * sb);
+                }
+            }
+            return;
+        }
         const int nsub = T / cw;                  // row subgroups
         const int sub = t / cw, c = tile * CTILE + (t % cw);
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -234,7 +339,7 @@ __device__ __forceinline__ int find_prob(const GemvProb *p, int lo, int hi, long
 
 __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a) {
     __shared__ double xr[SLAB];
-    __shared__ double part[T];
+    __shared__ double part[2 * T];
     const long long blk = blockIdx.x;
     const int p = find_prob(a.p, 0, a.count - 1, blk);
     // programmatic dependent launch: the apply's phases are chains of these launches;
@@ -253,7 +358,7 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
 // depend on the previous phase, so it is fetched before the dependency wait.
 __global__ void __launch_bounds__(T) gemv_dev_kernel(const GemvProb *__restrict__ P, const int *__restrict__ b2p) {
     __shared__ double xr[SLAB];
-    __shared__ double part[T];
+    __shared__ double part[2 * T];
     const long long blk = blockIdx.x;
     const GemvProb d = P[__ldg(b2p + blk)];
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -273,7 +378,7 @@ __global__ void __launch_bounds__(T) gemv_dev_kernel(const GemvProb *__restrict_
 __global__ void __launch_bounds__(T) apply_tasks_kernel(const GemvProb *__restrict__ ops,
                                                          const int *__restrict__ task_ptr) {
     __shared__ double xr[SLAB];
-    __shared__ double part[T];
+    __shared__ double part[2 * T];
     const int o0 = __ldg(task_ptr + blockIdx.x), o1 = __ldg(task_ptr + blockIdx.x + 1);
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -295,7 +400,7 @@ __global__ void __launch_bounds__(T) apply_tasks_kernel(const GemvProb *__restri
 __global__ void __launch_bounds__(T) apply_cluster_tasks_kernel(const GemvProb *__restrict__ ops,
                                                                  const int *__restrict__ task_ptr, int C) {
     __shared__ double xr[SLAB];
-    __shared__ double part[T];
+    __shared__ double part[2 * T];
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int task = blockIdx.x / C, q = (int)cl.block_rank();
@@ -313,6 +418,141 @@ __global__ void __launch_bounds__(T) apply_cluster_tasks_kernel(const GemvProb *
     }
 }
 
+// The whole apply (both sweeps) as ONE persistent dataflow launch.  Items = the
+// blocks of every op, in a topological order of the op graph (rsc_flow_deps); CTAs
+// take items from a global counter in that order, wait until the item's op has
+// received all its predecessors' completion signals, run the block, and the block
+// that completes an op signals the op's successors.  Deadlock-free without any
+// co-residency assumption: an item waits only on ops earlier in the order, whose
+// items were all taken by CTAs that are already running.  The level phases' ~1000
+// dependent launches (5-7 us of ramp, tail and launch latency each on config[4])
+// become flag waits on the ops that actually feed an op, and independent subtrees'
+// chains overlap instead of meeting at every level barrier.
+//
+// state: [0] item counter, [1, 1+nops) finished blocks per op, [1+nops, 1+2 nops)
+// completion signals received per op -- zeroed before every launch.
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ int atom_add_acqrel(int *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void red_add_release(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+
+// trace (diagnostics, rsc_apply_flow_trace): per item the %globaltimer at take, after
+// the dependency wait and at completion, and the SM
+#ifndef FLOW_PREFETCH
+#define FLOW_PREFETCH 1
+#endif
+// L2 prefetch of the matrix region of blocks [lb0, lb1) of op d (128-byte lines)
+__device__ __forceinline__ void prefetch_item(const GemvProb &d, int lb0, int lb1) {
+    if (d.rows <= 0 || d.cols <= 0) return;
+    const int t = threadIdx.x;
+    int r0, r1, c0, c1;
+    if (!(d.mode & 1)) {
+        const int nseg = T / d.lpr;
+        r0 = lb0 * nseg;
+        r1 = min(d.rows, lb1 * nseg);
+        c0 = 0;
+        c1 = d.cols;
+    } else {  // blocks = (slab, column tile), tile fastest: cover the slabs' full width
+        const int ntile = (d.cols + CTILE - 1) / CTILE;
+        r0 = (lb0 / ntile) * SLAB;
+        r1 = min(d.rows, ((lb1 - 1) / ntile + 1) * SLAB);
+        c0 = 0;
+        c1 = d.cols;
+    }
+    const long long first = (long long)(reinterpret_cast<size_t>(d.M + c0) >> 7);
+    const int lines = (int)(((reinterpret_cast<size_t>(d.M + c1 - 1)) >> 7) - first + 1);
+    const int n = (r1 - r0) * lines;
+    for (int i = t; i < n; i += T) {
+        const int r = r0 + i / lines, l = i % lines;
+        const char *a = reinterpret_cast<const char *>(d.M + (long long)r * d.ld + c0);
+        a = reinterpret_cast<const char *>((reinterpret_cast<size_t>(a) & ~size_t(127)) + 128 * (size_t)l);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
+template <bool TRACE>
+__global__ void __launch_bounds__(T) apply_flow_kernel(const GemvProb *__restrict__ ops,
+                                                        const int *__restrict__ item_op,
+                                                        const int *__restrict__ need,
+                                                        const int *__restrict__ succ_ptr,
+                                                        const int *__restrict__ succ, int *state, int nops,
+                                                        int total, unsigned long long *trace) {
+    __shared__ double xr[SLAB];
+    __shared__ double part[2 * T];
+    __shared__ int s_item[2], s_last;
+    int *head = state, *done = state + 1, *ready = state + 1 + nops;
+    const int t = threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (t == 0) s_item[0] = atomicAdd(head, 1);
+    __syncthreads();
+    int item = s_item[0], buf = 0;
+    while (item < total) {
+        unsigned long long t_take = 0, t_go = 0;
+        if (TRACE && t == 0) t_take = gtimer();
+        // take the next item now: the counter's round trip overlaps this item's work
+        if (t == 0) s_item[buf ^ 1] = atomicAdd(head, 1);
+        const int o = __ldg(item_op + item);
+        const GemvProb d = ops[o];
+        const int it = item - (int)d.blk_begin;
+        const int lb0 = it * d.grp, lb1 = min(lb0 + d.grp, d.nblk);
+        // the matrix tile does not depend on the predecessors: start pulling it into
+        // L2 now, so that after the wait only the vector loads see memory latency
+        if (FLOW_PREFETCH) prefetch_item(d, lb0, lb1);
+        if (t == 0) {
+            const int nd = __ldg(need + o);
+            if (nd > 0)
+                while (ld_acquire(ready + o) < nd) __nanosleep(32);
+            if (TRACE) t_go = gtimer();
+        }
+        __syncthreads();
+        for (int lb = lb0; lb < lb1; ++lb) gemv_block<true>(d, lb, xr, part);
+        __syncthreads();
+        if (t == 0) {
+            // release this CTA's writes (ordered before by the barrier) and count the item;
+            // the op's last item acquires every other item's writes before signalling
+            const int nitems = (d.nblk + d.grp - 1) / d.grp;
+            s_last = (nitems == 1) || (atom_add_acqrel(done + o, 1) == nitems - 1);
+            if (TRACE) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+                trace[4 * (long long)item] = t_take;
+                trace[4 * (long long)item + 1] = t_go;
+                trace[4 * (long long)item + 2] = gtimer();
+                trace[4 * (long long)item + 3] = smid;
+            }
+        }
+        __syncthreads();
+        if (s_last) {
+            const int e0 = __ldg(succ_ptr + o), e1 = __ldg(succ_ptr + o + 1);
+            if (e1 > e0) {
+                if (t == 0) __threadfence();
+                __syncthreads();
+                for (int e = e0 + t; e < e1; e += T) red_add_release(ready + __ldg(succ + e), 1);
+            }
+        }
+        buf ^= 1;
+        item = s_item[buf];
+    }
+}
+
 inline int pow2ceil(int v) {
     int p = 1;
     while (p < v) p <<= 1;
@@ -323,6 +563,10 @@ inline int pow2ceil(int v) {
 inline long long describe(GemvProb &d, const double *M, int rows, int cols, int ld, const double *x, const int *xi,
                           double *y, const int *yi, int mode, double alpha) {
     d.M = M; d.x = x; d.y = y; d.xidx = xi; d.yidx = yi;
+    // bit 5: every row starts 16-byte aligned (double2 loads)
+    static const bool scalar_only = getenv("RSC_GEMV_SCALAR") != nullptr;  // A/B switch
+    const bool vec = (reinterpret_cast<size_t>(M) % 16 == 0) && (ld % 2 == 0) && !scalar_only;
+    mode = (mode & ~32) | (vec ? 32 : 0);
     d.rows = rows; d.cols = cols; d.ld = ld; d.mode = mode; d.alpha = alpha;
     if (mode & 1) {
         d.lpr = cols >= CTILE ? CTILE : (pow2ceil(cols) < 32 ? 32 : pow2ceil(cols));
@@ -431,6 +675,97 @@ extern "C" int rsc_gemv_describe(int count, const double *const *M, const int *r
         total += blocks[i];
     }
     return 0;
+}
+
+inline long long flow_item_bytes() {
+    static const long long b = getenv("RSC_FLOW_ITEM_KB") ? atoll(getenv("RSC_FLOW_ITEM_KB")) * 1024 : 32 * 1024;
+    return b;
+}
+
+// Descriptors of the dataflow program: like rsc_gemv_describe, but every op gets at
+// least one item (an op whose rank dropped to 0 still completes and signals), the
+// items are numbered globally in op order (blk_begin), the plain-accumulate bit is
+// dropped (every accumulation is an L2 atomic: other CTAs may target the same rows),
+// and item_op (if not null) receives the item -> op map.  Returns the item count.
+extern "C" long long rsc_flow_describe(int count, const double *const *M, const int *rows, const int *cols,
+                                       const int *ldm, const double *const *x, const int *const *xidx,
+                                       double *const *y, const int *const *yidx, const int *modes,
+                                       const double *alphas, void *desc, int *item_op) {
+    if (count < 0) return -1;
+    if (count > 0 && (!M || !rows || !cols || !ldm || !x || !y || !modes || !alphas || !desc)) return -2;
+    GemvProb *d = static_cast<GemvProb *>(desc);
+    long long total = 0;
+    for (int i = 0; i < count; ++i) {
+        d[i] = GemvProb{};
+        long long nb = 0;
+        const int mode = modes[i] & ~16;
+        if (rows[i] > 0 && cols[i] > 0) {
+            const long long nblk = describe(d[i], M[i], rows[i], cols[i], ldm[i], x[i], xidx ? xidx[i] : nullptr,
+                                            y[i], yidx ? yidx[i] : nullptr, mode, alphas[i]);
+            // blocks per item: about FLOW_ITEM_BYTES of matrix per item (the per-item
+            // queue / wait / signal round trips are amortized over it)
+            const long long bb = (mode & 1) ? (long long)SLAB * (cols[i] < CTILE ? cols[i] : CTILE) * 8
+                                            : (long long)(T / d[i].lpr) * cols[i] * 8;
+            long long g = flow_item_bytes() / (bb > 0 ? bb : 1);
+            g = g < 1 ? 1 : (g > nblk ? nblk : g);
+            d[i].nblk = (int)nblk;
+            d[i].grp = (int)g;
+            nb = (nblk + g - 1) / g;
+        } else {  // an empty op (rank 0): one no-op item so that it still signals
+            d[i].M = M[i]; d[i].x = x[i]; d[i].y = y[i];
+            d[i].rows = 0; d[i].cols = 0; d[i].ld = 1; d[i].mode = 0; d[i].lpr = 32;  // no rows: no writes
+            d[i].nblk = 1; d[i].grp = 1;
+            d[i].alpha = alphas[i];
+            nb = 1;
+        }
+        d[i].blk_begin = total;
+        if (item_op)
+            for (long long b = 0; b < nb; ++b) item_op[total + b] = i;
+        total += nb;
+    }
+    return total;
+}
+
+int flow_launch(const void *ops, const int *item_op, const int *need, const int *succ_ptr, const int *succ,
+                int *state, int nops, int total, unsigned long long *trace, cudaStream_t s);
+
+extern "C" int rsc_apply_flow_trace(const void *ops, const int *item_op, const int *need, const int *succ_ptr,
+                                    const int *succ, int *state, int nops, int total, void *trace, void *stream) {
+    if (!trace) return -2;
+    return flow_launch(ops, item_op, need, succ_ptr, succ, state, nops, total,
+                       static_cast<unsigned long long *>(trace), (cudaStream_t)stream);
+}
+
+extern "C" int rsc_apply_flow(const void *ops, const int *item_op, const int *need, const int *succ_ptr,
+                              const int *succ, int *state, int nops, int total, void *stream) {
+    return flow_launch(ops, item_op, need, succ_ptr, succ, state, nops, total, nullptr, (cudaStream_t)stream);
+}
+
+int flow_launch(const void *ops, const int *item_op, const int *need, const int *succ_ptr, const int *succ,
+                int *state, int nops, int total, unsigned long long *trace, cudaStream_t s) {
+    if (nops < 0 || total < 0) return -1;
+    if (total == 0) return 0;
+    if (!ops || !item_op || !need || !succ_ptr || !succ || !state) return -2;
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_flow_kernel<false>, T, 0);
+        grid = nsm * (occ > 0 ? occ : 1);
+    }
+    cudaError_t e = cudaMemsetAsync(state, 0, sizeof(int) * (1 + 2 * (size_t)nops), s);
+    if (e != cudaSuccess) return (int)e;
+    const int g = grid < total ? grid : total;
+    if (trace)
+        apply_flow_kernel<true><<<g, T, 0, s>>>(static_cast<const GemvProb *>(ops), item_op, need, succ_ptr, succ,
+                                                 state, nops, total, trace);
+    else
+        apply_flow_kernel<false><<<g, T, 0, s>>>(static_cast<const GemvProb *>(ops), item_op, need, succ_ptr, succ,
+                                                  state, nops, total, nullptr);
+    rsc_count_launch();
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : (int)e;
 }
 
 extern "C" int rsc_gemv_multi_dev(const void *desc, const int *blk2prob, long long total_blocks, void *stream) {

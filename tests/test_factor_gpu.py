@@ -287,3 +287,32 @@ def test_stored_zeros_are_dropped(cuda):
     assert F0.ranks == F1.ranks and F0.stored_scalars() == F1.stored_scalars()
     r = np.random.default_rng(2).standard_normal(A0.n)
     assert np.array_equal(F0.apply(r), F1.apply(r)) or relerr(F0.apply(r), F1.apply(r)) < 1e-13
+
+
+@pytest.mark.gpu
+def test_apply_flow_matches_phases(cuda):
+    """The dataflow apply (one persistent launch over the op graph) against the level
+    phases on a problem with compressed blocks and diagonal trees."""
+    from paper_1507_05593_b200 import engine as E
+    from paper_1507_05593_b200.apply import DeviceApply
+    from paper_1507_05593_b200.factor import SolverConfig, factorize
+    from paper_1507_05593_b200.problems import laplacian_3d
+
+    A, coords = laplacian_3d(20)
+    F = factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64), coords=coords)
+    assert F.stats.compressed_offdiag > 0 and F.stats.compressed_diag > 0
+    r = E.to_dev(np.random.default_rng(3).standard_normal(A.n))
+    zs = {}
+    old = DeviceApply.FLOW
+    try:
+        for flow in (False, True):
+            DeviceApply.FLOW = flow
+            ap = DeviceApply(F)
+            assert ap.flow == flow
+            z = E.empty(A.n)
+            for _ in range(5):  # eager, then graph replays
+                ap(r, z)
+            zs[flow] = z.cpu().numpy()
+    finally:
+        DeviceApply.FLOW = old
+    assert relerr(zs[True], zs[False]) <= 1e-12
