@@ -217,6 +217,13 @@ int rsc_spmv_csr(int n, const int *rowptr_dev, const int *colidx_dev,
 int rsc_identity_batched(int count, double *const *dst, const int *n, const int *ldd, void *stream);
 int rsc_transpose_batched(int count, const double *const *src, double *const *dst, const int *n,
                           const int *lds, const int *ldd, void *stream);
+/* Batched rectangular copy (trans 0: dst = src) / transpose (trans 1: dst = src^T, src
+ * rows x cols): stages V, U and the dense couplings of the diagonal block trees before
+ * the tree solves that flatten each tree's inverse for the apply (apply.py
+ * refresh_inverses; the block substitution of diagblocks.py:192-273 folded into the
+ * factors once per factorization). */
+int rsc_copy2d_batched(int count, const double *const *src, double *const *dst, const int *rows,
+                       const int *cols, const int *lds, const int *ldd, int trans, void *stream);
 int rsc_gather_rows(int nrows, int ncols, const int *idx_dev, const double *src_dev,
                     int lds, double *dst_dev, int ldd, void *stream);
 int rsc_scatter_add_rows(int nrows, int ncols, const int *idx_dev, double alpha,

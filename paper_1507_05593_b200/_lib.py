@@ -56,6 +56,7 @@ EXPORTED = (
     "rsc_flow_deps",
     "rsc_identity_batched",
     "rsc_transpose_batched",
+    "rsc_copy2d_batched",
     "rsc_gather_rows",
     "rsc_scatter_add_rows",
     "rsc_dot",
@@ -138,6 +139,7 @@ _SIGS = {
     "rsc_gather_rows": (I, [I, I, P, P, I, P, I, P]),
     "rsc_identity_batched": (I, [I, P, P, P, P]),
     "rsc_transpose_batched": (I, [I, P, P, P, P, P, P]),
+    "rsc_copy2d_batched": (I, [I, P, P, P, P, P, P, I, P]),
     "rsc_scatter_add_rows": (I, [I, I, P, D, P, I, P, I, P]),
     "rsc_dot": (I, [I, P, P, P, P, P]),
     "rsc_pcg_update_xr": (I, [I, P, P, P, P, P, P, P]),

@@ -21,6 +21,15 @@ solved block is written to `y2` (couplings read solved values from `y2`); the
 backward sweep starts from `y2` and writes `y`.  All low-rank intermediates live in
 one buffer zeroed once per apply.  Descriptors are static after factorization and
 built once; after a few eager applies the whole sweep is replayed from a CUDA graph.
+
+Flattened tree inverses (TREE_INV, default): the block substitution of a diagonal
+tree (Alg. 4, diagblocks.py:192-273) is a chain of 3 L - 2 dependent phases for L
+leaves.  The inverse of a block triangle [[D1, 0], [V U^T, D2]] is
+[[D1^{-1}, 0], [-(D2^{-1} V)(D1^{-T} U)^T, D2^{-1}]]: the same tree with the same
+ranks.  So once per factorization every coupling is carried through its sibling
+subtrees' solves (V' = D2^{-1} V, U' = D1^{-T} U; dense couplings D2^{-1} B D1^{-1}),
+all in lock-step batched Alg. 4 waves, and every application of a tree is two
+phases: all leaf inverses and all U'^T r at once, then all V' t.
 """
 
 import os
@@ -400,6 +409,8 @@ class DeviceApply:
                 | {key for _, _, _, key in self._ctask_lr})
         if set(ks) != have or len(F.dunits) != self.nunits:
             return False
+        self._tree_inverse_buffers(F.dunits, old=self.tinv)  # the solves read the new ranks
+        self._refresh_graph = None
         for li, ii, key in self._lr_index:
             self.launches[li][1][2][ii] = ks[key]
         for ph in self.phases:  # the flow program is rebuilt from the phase items
@@ -503,12 +514,116 @@ class DeviceApply:
                     t.Linv = self.mem.empty(t.n, t.n)
                     t.LinvT = self.mem.empty(t.n, t.n)
                     t.inv_mem = self.mem  # a later program may reuse these views
+        self._tree_inverse_buffers(units)
         self.refresh_inverses()
 
-    def refresh_inverses(self):
-        tris = self.tris
-        if not tris:
+    # Flattened inverses of the diagonal block trees (module docstring).
+    # RSC_APPLY_TREE_INV=0 keeps the lock-step Alg. 4 waves.
+    TREE_INV = os.environ.get("RSC_APPLY_TREE_INV", "1") == "1"
+
+    def _tree_inverse_buffers(self, units, old=None):
+        """tree.inv[s] of every internal block s: (V', U') at the coupling's column
+        capacity, or (Y, W) for a dense coupling B (Y = D2^{-1} B, then
+        W = (Y D1^{-1})^T).  `old`: the tree units of the program being re-keyed,
+        whose buffers the new factor's trees adopt (same memory, same structure)."""
+        self.tinv = []
+        if not self.TREE_INV:
             return
+        trees = [u for u in units if isinstance(u.diag, DeviceTree)]
+        if old is not None:
+            for u, uo in zip(trees, old):
+                u.diag.inv, u.diag.inv_mem = uo.diag.inv, uo.diag.inv_mem
+        for u in trees:
+            tree = u.diag
+            if getattr(tree, "inv", None) is None:
+                mem = getattr(self, "mem", None)
+                if mem is None:
+                    mem = self.mem = E.Arena()
+                tree.inv, tree.inv_mem = {}, mem
+                for s, b in tree.blocks.items():
+                    nd = tree.shape.nodes[s]
+                    if nd.is_leaf:
+                        continue
+                    n1, n2 = nd.split - nd.lo, nd.hi - nd.split
+                    if isinstance(b, DevLR):
+                        cap = _cap(b)
+                        tree.inv[s] = (mem.empty(n2, cap), mem.empty(n1, cap))
+                    else:
+                        tree.inv[s] = (mem.empty(n2, n1), mem.empty(n1, n2))
+            self.tinv.append(u)
+        self._tinv_key = None
+
+    def _refresh_tree_inverses(self):
+        from .numeric import diag_solve_many
+
+        if not self.tinv:
+            return
+        lib = E.ensure_gemm_workspace()
+        cp, tp, it1, it2 = [], [], [], []
+        for u in self.tinv:
+            tree = u.diag
+            for s, (A0, A1) in tree.inv.items():
+                nd, b = tree.shape.nodes[s], tree.blocks[s]
+                if isinstance(b, DevLR):
+                    k = b.k
+                    if k == 0:
+                        continue
+                    Vi, Ui = A0[:, :k], A1[:, :k]
+                    cp.append((b.V, Vi))
+                    cp.append((b.U, Ui))
+                    it1.append((u, Vi, False, nd.right.s))
+                    it1.append((u, Ui, True, nd.left.s))
+                else:
+                    cp.append((b, A0))
+                    it1.append((u, A0, False, nd.right.s))
+                    tp.append((A0, A1))
+                    it2.append((u, A1, True, nd.left.s))
+
+        def copies(pairs, trans):
+            if not pairs:
+                return
+            arrs = [ptr_array([a.data_ptr() for a, _ in pairs]), ptr_array([d.data_ptr() for _, d in pairs]),
+                    int_array([a.shape[0] for a, _ in pairs]), int_array([a.shape[1] for a, _ in pairs]),
+                    int_array([E.ld(a) for a, _ in pairs]), int_array([E.ld(d) for _, d in pairs])]
+            _lib.check(lib.rsc_copy2d_batched(len(pairs), *[x.ctypes.data for x in arrs], trans,
+                                              E.stream_handle()), "rsc_copy2d_batched")
+
+        copies(cp, 0)
+        diag_solve_many(it1, E.empty)
+        copies(tp, 1)
+        diag_solve_many(it2, E.empty)
+
+    def refresh_inverses(self):
+        """Re-derive every explicit inverse from the factor's current values.  A
+        refactorization loop calls this once per factorization with unchanged
+        structure, so from the second call it is replayed from a CUDA graph (the
+        tree solves are ~400 small launches: host-bound when issued eagerly)."""
+        if not self.tris:
+            return
+        self._refresh_calls = getattr(self, "_refresh_calls", 0) + 1
+        g = getattr(self, "_refresh_graph", None)
+        if g is None and self._refresh_calls > 1 and self.REFRESH_GRAPH:
+            try:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    E.ensure_gemm_workspace()
+                    with torch.cuda.graph(g, stream=s):
+                        self._refresh_body()
+                torch.cuda.current_stream().wait_stream(s)
+            except Exception:
+                g = False
+            self._refresh_graph = g
+        if g:
+            g.replay()
+        else:
+            self._refresh_body()
+
+    REFRESH_GRAPH = os.environ.get("RSC_APPLY_REFRESH_GRAPH", "1") == "1"
+
+    def _refresh_body(self):
+        tris = self.tris
         lib = _lib.load()
         if self._sq is None:
             ns = [t.n for t in tris]
@@ -524,6 +639,7 @@ class DeviceApply:
                        [t.n for t in tris])
         _lib.check(lib.rsc_transpose_batched(len(tris), li.ctypes.data, lt.ctypes.data, n_.ctypes.data,
                                              ldi.ctypes.data, ldt.ctypes.data, s), "rsc_transpose_batched")
+        self._refresh_tree_inverses()
 
     def _rows_ptr(self, plan, un):
         key = ("int", un.u) if un.kind == "interior" else un.j
@@ -551,7 +667,7 @@ class DeviceApply:
             for u in dense:
                 self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, False)
             small, big = self._split_trees(trees)
-            first = self._tree_waves(big, rhs, out, False, first)
+            first = self._tree_phases(big, rhs, out, False, first)
             self._emit(first)
             self._tree_cluster_tasks(small, rhs, out, False)
             self._couplings(cpl, plan, rhs, out, False)
@@ -561,7 +677,7 @@ class DeviceApply:
             for u in dense:
                 self._solve(first, u.diag, rhs + 8 * u.c0, out + 8 * u.c0, True)
             small, big = self._split_trees(trees)
-            first = self._tree_waves(big, rhs, out, True, first)
+            first = self._tree_phases(big, rhs, out, True, first)
             self._emit(first)
             self._tree_cluster_tasks(small, rhs, out, True)
 
@@ -654,6 +770,43 @@ class DeviceApply:
                 lists.append(ph)
         if lists:
             self.phases.append(_ClusterTasks(lists))
+
+    def _tree_phases(self, trees, rhs, out, backward, first):
+        if self.TREE_INV and trees:
+            return self._tree_flat(trees, rhs, out, backward, first)
+        return self._tree_waves(trees, rhs, out, backward, first)
+
+    def _tree_flat(self, trees, rhs, out, backward, first):
+        """out = D^{-1} rhs (or D^{-T} rhs) of every tree through its flattened inverse:
+        `first` gets every leaf inverse and the first factor of every coupling (all
+        read rhs), a second phase accumulates the couplings' second factors into out."""
+        second = _Phase()
+        for u in trees:
+            tree, base = u.diag, 8 * u.c0
+            for s in tree.shape.order:
+                nd, b = tree.shape.nodes[s], tree.blocks[s]
+                if nd.is_leaf:
+                    if b.n:
+                        self._solve(first, b, rhs + base + 8 * nd.lo, out + base + 8 * nd.lo, backward)
+                    continue
+                A0, A1 = tree.inv[s]
+                x1, x2 = base + 8 * nd.lo, base + 8 * nd.split
+                n1, n2 = nd.split - nd.lo, nd.hi - nd.split
+                if isinstance(b, DevLR):
+                    t, key = self._t(_cap(b)), b.U.data_ptr()
+                    if not backward:  # out[X2] -= V' (U'^T rhs[X1])
+                        first.add(A1.data_ptr(), n1, b.k, E.ld(A1), rhs + x1, 0, t, 0, 1, 1.0, lr=key)
+                        second.add(A0.data_ptr(), n2, b.k, E.ld(A0), t, 0, out + x2, 0, 0, -1.0, lr=key)
+                    else:  # out[X1] -= U' (V'^T rhs[X2])
+                        first.add(A0.data_ptr(), n2, b.k, E.ld(A0), rhs + x2, 0, t, 0, 1, 1.0, lr=key)
+                        second.add(A1.data_ptr(), n1, b.k, E.ld(A1), t, 0, out + x1, 0, 0, -1.0, lr=key)
+                elif not backward:  # out[X2] -= W^T rhs[X1], W = (D2^{-1} B D1^{-1})^T
+                    second.add(A1.data_ptr(), n1, n2, E.ld(A1), rhs + x1, 0, out + x2, 0, 1, -1.0)
+                else:  # out[X1] -= W rhs[X2]
+                    second.add(A1.data_ptr(), n1, n2, E.ld(A1), rhs + x2, 0, out + x1, 0, 0, -1.0)
+        self._emit(first)
+        self._emit(second)
+        return _Phase()
 
     def _tree_waves(self, trees, rhs, out, backward, first):
         """Alg. 4 of every tree in `trees`, in lock-step waves; wave w's leaf solves,

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(T) trsv_kernel(const __grid_constant__ TrsvArg
 //   the CTA are covered by several row subgroups whose partial sums meet in shared
 //   memory before one atomic per column.
 constexpr int GMAXP = 224;
+constexpr int RPB = 4;       // rows per segment, transpose 0, full aligned rows
 constexpr int SLAB = 64;     // rows per CTA, transpose 1
 constexpr int CTILE = 256;   // columns per CTA, transpose 1
 
@@ -163,6 +164,57 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
         const int seg = t / lpr, sub = t % lpr;   // T / lpr segments per CTA
         const int nseg = T / lpr;
         const int r = (int)lb * nseg + seg;
+        if ((mode & 32) && !lower && !upper) {
+            // full rows, 16-byte aligned: a segment owns RPB consecutive rows and walks
+            // them together (one x pair feeds RPB double2 loads), so a CTA moves RPB times
+            // the bytes of the one-row path per launch slot and keeps 2 RPB loads per
+            // lane in flight
+            const int rb = ((int)lb * nseg + seg) * RPB;
+            double acc[RPB];
+#pragma unroll
+            for (int q = 0; q < RPB; ++q) acc[q] = 0.0;
+            if (rb < rows) {
+                const int nr = min(RPB, rows - rb);
+                const double2 *M2[RPB];
+#pragma unroll
+                for (int q = 0; q < RPB; ++q)
+                    M2[q] = reinterpret_cast<const double2 *>(M + (long long)(rb + (q < nr ? q : 0)) * ld);
+                const int pend = cols >> 1;
+#pragma unroll 2
+                for (int p = sub; p < pend; p += lpr) {
+                    const int c = 2 * p;
+                    const double x0 = ldx<CG>(x + (xi ? __ldg(xi + c) : c));
+                    const double x1 = ldx<CG>(x + (xi ? __ldg(xi + c + 1) : c + 1));
+#pragma unroll
+                    for (int q = 0; q < RPB; ++q) {
+                        const double2 mv = __ldg(M2[q] + p);
+                        acc[q] = fma(mv.y, x1, fma(mv.x, x0, acc[q]));
+                    }
+                }
+                if ((cols & 1) && sub == lpr - 1) {
+                    const int c = cols - 1;
+                    const double xv = ldx<CG>(x + (xi ? __ldg(xi + c) : c));
+#pragma unroll
+                    for (int q = 0; q < RPB; ++q)
+                        acc[q] = fma(ldnc(reinterpret_cast<const double *>(M2[q]) + c), xv, acc[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RPB; ++q)
+                for (int o = lpr >> 1; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            if (rb < rows && sub == 0) {
+                const int nr = min(RPB, rows - rb);
+#pragma unroll
+                for (int q = 0; q < RPB; ++q) {
+                    if (q >= nr) break;
+                    double *dst = y + (yi ? __ldg(yi + rb + q) : rb + q);
+                    if (assign) *dst = alpha * acc[q];
+                    else if (mode & 16) *dst += alpha * acc[q];
+                    else atomicAdd(dst, alpha * acc[q]);
+                }
+            }
+            return;
+        }
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         if (r < rows && (mode & 32)) {
             // rows 16-byte aligned: double2 loads of column pairs (2p, 2p+1), four pairs in
@@ -464,7 +516,7 @@ __device__ __forceinline__ void prefetch_item(const GemvProb &d, int lb0, int lb
     const int t = threadIdx.x;
     int r0, r1, c0, c1;
     if (!(d.mode & 1)) {
-        const int nseg = T / d.lpr;
+        const int nseg = (T / d.lpr) * (((d.mode & 32) && !(d.mode & (2 | 8))) ? RPB : 1);  // rows per block
         r0 = lb0 * nseg;
         r1 = min(d.rows, lb1 * nseg);
         c0 = 0;
@@ -574,6 +626,7 @@ inline long long describe(GemvProb &d, const double *M, int rows, int cols, int 
     }
     d.lpr = cols <= 64 ? 8 : (cols <= 256 ? 16 : 32);  // (lpr 32 from 65 columns measured slower)
     const int nseg = T / d.lpr;
+    if (vec && !(mode & (2 | 8))) return (rows + nseg * RPB - 1) / (nseg * RPB);  // RPB rows per segment
     return (rows + nseg - 1) / nseg;
 }
 
@@ -906,6 +959,77 @@ int sq_launch(int mode, int count, const double *const *src, double *const *dst,
     return 0;
 }
 }  // namespace
+
+// Batched rectangular copy (trans 0: dst = src) or transpose (trans 1: dst = src^T,
+// src rows x cols) for the diagonal trees' flattened inverses (apply.py: copies of
+// V / U and of the dense couplings before the tree solves).  Row tiles of every
+// matrix are dealt over gridDim.y.
+namespace {
+constexpr int RMAX = 768;
+struct RectArgs {
+    int count, trans;
+    const double *src[RMAX];
+    double *dst[RMAX];
+    int rows[RMAX], cols[RMAX], lds[RMAX], ldd[RMAX];
+};
+
+__global__ void __launch_bounds__(256) rect_copy_kernel(const __grid_constant__ RectArgs a) {
+    __shared__ double tile[32][33];
+    const int b = blockIdx.x;
+    const int rows = a.rows[b], cols = a.cols[b], lds = a.lds[b], ldd = a.ldd[b];
+    const double *S = a.src[b];
+    double *D = a.dst[b];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int i0 = 32 * blockIdx.y; i0 < rows; i0 += 32 * gridDim.y)
+        for (int j0 = 0; j0 < cols; j0 += 32) {
+            if (!a.trans) {
+                for (int q = ty; q < 32; q += 8) {
+                    const int i = i0 + q, j = j0 + tx;
+                    if (i < rows && j < cols) D[(long long)i * ldd + j] = S[(long long)i * lds + j];
+                }
+                continue;
+            }
+            for (int q = ty; q < 32; q += 8) {
+                const int i = i0 + q, j = j0 + tx;
+                tile[q][tx] = (i < rows && j < cols) ? S[(long long)i * lds + j] : 0.0;
+            }
+            __syncthreads();
+            for (int q = ty; q < 32; q += 8) {
+                const int i = j0 + q, j = i0 + tx;  // D[i][j] = S[j][i]
+                if (i < cols && j < rows) D[(long long)i * ldd + j] = tile[tx][q];
+            }
+            __syncthreads();
+        }
+}
+}  // namespace
+
+extern "C" int rsc_copy2d_batched(int count, const double *const *src, double *const *dst, const int *rows,
+                                  const int *cols, const int *lds, const int *ldd, int trans, void *stream) {
+    if (count < 0) return -1;
+    if (count == 0) return 0;
+    if (!src || !dst || !rows || !cols || !lds || !ldd) return -2;
+    static thread_local RectArgs a;
+    for (int c0 = 0; c0 < count; c0 += RMAX) {
+        const int cnt = count - c0 < RMAX ? count - c0 : RMAX;
+        a.count = cnt;
+        a.trans = trans ? 1 : 0;
+        int maxr = 1;
+        for (int i = 0; i < cnt; ++i) {
+            a.src[i] = src[c0 + i];
+            a.dst[i] = dst[c0 + i];
+            a.rows[i] = rows[c0 + i];
+            a.cols[i] = cols[c0 + i];
+            a.lds[i] = lds[c0 + i];
+            a.ldd[i] = ldd[c0 + i];
+            maxr = a.rows[i] > maxr ? a.rows[i] : maxr;
+        }
+        int gy = (maxr + 255) / 256;  // ~8 row tiles per CTA of the tallest matrix
+        gy = gy < 1 ? 1 : (gy > 64 ? 64 : gy);
+        rect_copy_kernel<<<dim3(cnt, gy), 256, 0, (cudaStream_t)stream>>>(a);
+        RSC_CHECK_LAUNCH();
+    }
+    return 0;
+}
 
 extern "C" int rsc_identity_batched(int count, double *const *dst, const int *n, const int *ldd, void *stream) {
     if (count < 0) return -1;

@@ -14,6 +14,7 @@ G0 = [E.to_dev(rng.standard_normal((m, k)) @ np.diag(np.logspace(0, -8, k))) for
 Gs = [g.clone() for g in G0]
 Qs = [E.empty(m, k) for _ in range(cnt)]
 rank = E.zeros(cnt, dtype=E.I32)
+E.ensure_gemm_workspace()
 
 
 def run():

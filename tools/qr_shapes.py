@@ -62,6 +62,8 @@ for m, k, ms in sorted(log, key=lambda x: -x[2])[:15]:
     big = len(m) - reg - sm
     print(f"  {ms:7.2f} ms  n={len(m):4d} (reg {reg}, smem {sm}, coop {big})  max m {m.max()} max k {k.max()}  "
           f"median m {int(np.median(m))} k {int(np.median(k))}")
+    o = np.argsort(-(m.astype(np.int64) * k * k))[:6]
+    print("      largest (m,k):", " ".join(f"({int(m[x])},{int(k[x])})" for x in o))
 
 if conds:
     c = np.array([x[2] for x in conds])
