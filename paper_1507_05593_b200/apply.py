@@ -604,14 +604,8 @@ class DeviceApply:
         g = getattr(self, "_refresh_graph", None)
         if g is None and self._refresh_calls > 1 and self.REFRESH_GRAPH:
             try:
-                s = torch.cuda.Stream()
-                s.wait_stream(torch.cuda.current_stream())
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.stream(s):
-                    E.ensure_gemm_workspace()
-                    with torch.cuda.graph(g, stream=s):
-                        self._refresh_body()
-                torch.cuda.current_stream().wait_stream(s)
+                E.ensure_gemm_workspace()
+                g = E.capture_graph(self._refresh_body)
             except Exception:
                 g = False
             self._refresh_graph = g
@@ -866,14 +860,7 @@ class DeviceApply:
         self.calls += 1
         if self.graph is None and self.calls > self.GRAPH_AFTER and not self.dist:
             try:
-                s = torch.cuda.Stream()
-                s.wait_stream(torch.cuda.current_stream())
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.stream(s):
-                    with torch.cuda.graph(g, stream=s):
-                        self._body()
-                torch.cuda.current_stream().wait_stream(s)
-                self.graph = g
+                self.graph = E.capture_graph(self._body)
             except Exception:
                 self.graph = False
         if self.graph:

@@ -112,7 +112,14 @@ __global__ void __launch_bounds__(T) trsv_kernel(const __grid_constant__ TrsvArg
 //   the CTA are covered by several row subgroups whose partial sums meet in shared
 //   memory before one atomic per column.
 constexpr int GMAXP = 224;
-constexpr int RPB = 4;       // rows per segment, transpose 0, full aligned rows
+#ifndef GEMV_RPB
+#define GEMV_RPB 4
+#endif
+#ifndef GEMV_MINB
+#define GEMV_MINB 5  // CTAs per SM of the phase kernels (51 registers: a few spilled words; measured 6% faster
+                     // applies than 4 CTAs at 62 registers -- the phases are bound by loads in flight)
+#endif
+constexpr int RPB = GEMV_RPB;  // rows per segment, transpose 0, full aligned rows
 constexpr int SLAB = 64;     // rows per CTA, transpose 1
 constexpr int CTILE = 256;   // columns per CTA, transpose 1
 
@@ -389,7 +396,7 @@ __device__ __forceinline__ int find_prob(const GemvProb *p, int lo, int hi, long
     return lo;
 }
 
-__global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArgs a) {
+__global__ void __launch_bounds__(T, GEMV_MINB) gemv_kernel(const __grid_constant__ GemvArgs a) {
     __shared__ double xr[SLAB];
     __shared__ double part[2 * T];
     const long long blk = blockIdx.x;
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(T) gemv_kernel(const __grid_constant__ GemvArg
 // back-to-back launches (config[4]'s interior-coupling phases have 4546 problems: 21
 // launches of ~19 us, each paying its own ramp and tail).  The descriptor does not
 // depend on the previous phase, so it is fetched before the dependency wait.
-__global__ void __launch_bounds__(T) gemv_dev_kernel(const GemvProb *__restrict__ P, const int *__restrict__ b2p) {
+__global__ void __launch_bounds__(T, GEMV_MINB) gemv_dev_kernel(const GemvProb *__restrict__ P, const int *__restrict__ b2p) {
     __shared__ double xr[SLAB];
     __shared__ double part[2 * T];
     const long long blk = blockIdx.x;

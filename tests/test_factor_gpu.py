@@ -316,3 +316,41 @@ def test_apply_flow_matches_phases(cuda):
     finally:
         DeviceApply.FLOW = old
     assert relerr(zs[True], zs[False]) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_apply_tree_inverse_matches_waves(cuda):
+    """The flattened inverses of the diagonal block trees (two phases per tree) against
+    the lock-step Alg. 4 waves (diagblocks.py:192-273), forward and backward sweeps,
+    eager and from the CUDA graphs; the refresh graph re-derives the same inverses."""
+    from paper_1507_05593_b200 import engine as E
+    from paper_1507_05593_b200.apply import DeviceApply
+    from paper_1507_05593_b200.factor import DeviceTree, SolverConfig, factorize
+    from paper_1507_05593_b200.problems import laplacian_3d
+
+    A, coords = laplacian_3d(20)
+    F = factorize(A, SolverConfig(tau_o=32, oversample=10, tau_d=64), coords=coords)
+    assert F.stats.compressed_diag > 0
+    assert any(isinstance(u.diag, DeviceTree) for u in F.dunits)
+    r = E.to_dev(np.random.default_rng(5).standard_normal(A.n))
+    zs, phases = {}, {}
+    old = DeviceApply.TREE_INV
+    try:
+        for inv in (False, True):
+            DeviceApply.TREE_INV = inv
+            ap = DeviceApply(F)
+            z = E.empty(A.n)
+            for _ in range(5):  # eager, then graph replays
+                ap(r, z)
+            zs[inv] = z.cpu().numpy()
+            phases[inv] = len(ap.launches)
+            if inv:
+                for _ in range(3):  # eager refresh, capture, replay
+                    ap.refresh_inverses()
+                assert ap._refresh_graph not in (None, False)
+                ap(r, z)
+                assert np.array_equal(z.cpu().numpy(), zs[inv]) or relerr(z.cpu().numpy(), zs[inv]) < 1e-13
+    finally:
+        DeviceApply.TREE_INV = old
+    assert phases[True] < phases[False]
+    assert relerr(zs[True], zs[False]) <= 1e-12

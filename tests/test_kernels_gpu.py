@@ -486,3 +486,32 @@ def test_potrf_fused_batch_mixed_sizes_lda_and_failures(cuda):
             inv = np.linalg.inv(Lref[j0:j0 + nb, j0:j0 + nb])
             assert relerr(blk[:, :nb], inv) < 1e-12, (i, n, j0)
             assert np.all(blk[:, nb:] == 0.0) and np.all(np.triu(blk[:, :nb], 1) == 0.0)
+
+
+def test_copy2d_batched_copy_and_transpose(cuda):
+    """rsc_copy2d_batched: strided rectangular copies and transposes, mixed shapes in
+    one launch (row tiles dealt over gridDim.y), more matrices than one parameter block."""
+    import torch
+
+    from paper_1507_05593_b200 import _lib
+    from paper_1507_05593_b200._lib import int_array, ptr_array
+
+    lib = _lib.load()
+    rng = np.random.default_rng(21)
+    shapes = [(1, 1), (31, 33), (64, 64), (700, 45), (45, 700), (3000, 17), (2, 513)] + [(5, 7)] * 800
+    for trans in (0, 1):
+        src = [torch.from_numpy(rng.standard_normal((r, c + 2))).cuda() for r, c in shapes]
+        dst = [torch.full((c if trans else r, (r if trans else c) + 3), -7.0, dtype=torch.float64, device="cuda")
+               for r, c in shapes]
+        arrs = [ptr_array([s.data_ptr() for s in src]), ptr_array([d.data_ptr() for d in dst]),
+                int_array([r for r, _ in shapes]), int_array([c for _, c in shapes]),
+                int_array([c + 2 for _, c in shapes]), int_array([d.shape[1] for d in dst])]
+        rc = lib.rsc_copy2d_batched(len(shapes), *[a.ctypes.data for a in arrs], trans,
+                                    torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        for (r, c), s, d in zip(shapes[:8], src, dst):
+            want = s[:, :c].T if trans else s[:, :c]
+            got = d[:, :want.shape[1]]
+            assert torch.equal(got, want)
+            assert bool((d[:, want.shape[1]:] == -7.0).all())  # nothing written past the block
