@@ -207,6 +207,11 @@ def run_sparse(args, rank, world, torch, dist):
         lib.rsc_launch_counter(1)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tf = []
+        # RSC_BENCH_PROFILE_RANGE=1: cudaProfilerStart/Stop around the timed steps, so an
+        # `ncu --profile-from-start off` launch list holds exactly the timed region
+        prof_range = os.environ.get("RSC_BENCH_PROFILE_RANGE") == "1"
+        if prof_range:
+            torch.cuda.profiler.start()
         ev0.record()
         for _ in range(args.steps):
             F = None
@@ -214,6 +219,8 @@ def run_sparse(args, rank, world, torch, dist):
             tf.append(F.stats.phase_times["numeric"])
         ev1.record()
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.profiler.stop()
         launches = int(lib.rsc_launch_counter(1))
         if dist is not None:
             dist.barrier()
