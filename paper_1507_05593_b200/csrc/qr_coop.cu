@@ -278,15 +278,18 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
     }
 }
 
+// Global-memory columns: capped at 64 registers so two groups (two large sketches of one
+// batch, e.g. config[4]'s two 6048x987 top-separator sketches) are co-resident, two CTAs
+// per SM, instead of running one after the other (52.6 vs 58.3 ms for that pair; the
+// few spilled values sit outside the column loops).  Bit-identical results.
 #ifndef MQ_GLOBAL_MINB
-#define MQ_GLOBAL_MINB 1
+#define MQ_GLOBAL_MINB 2
 #endif
 template <bool SMEM>
 __global__ void __launch_bounds__(MCT, SMEM ? 1 : MQ_GLOBAL_MINB) mqrcp_kernel(const __grid_constant__ MArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64]  /* block_sum_n: CB x MCT/32 */;
     __shared__ int redp[32];
-    __shared__ double pdot[16], pnrm[16];  // row partials of the split column updates
     __shared__ int piv_s;
     // locate this CTA's matrix
     int g = 0;
@@ -455,60 +458,6 @@ __global__ void __launch_bounds__(MCT, SMEM ? 1 : MQ_GLOBAL_MINB) mqrcp_kernel(c
         } else {
         const double *vsrc = (nblk == 1) ? cols + (long long)(pc - c0) * ldw  // the reflector lives in this CTA
                                          : v;
-        // A CTA that owns at most half as many columns as it has warps splits every
-        // column's rows over G warps (G a power of two): the step's critical path is
-        // this update, and with one warp per column only c1 - c0 of the 16 warps work.
-        // The G row partials of a dot product meet in shared memory behind a named
-        // barrier of the G warps and are added in warp order (fixed for a matrix).
-        int G = 1;
-        if (SMEM)
-            while (2 * G * (c1 - c0) <= nw) G *= 2;
-        if (SMEM && G > 1) {
-            const int j = warp / G, gsub = warp % G;
-            const int phys = c0 + j;
-            if (j < c1 - c0 && posof[phys] > i) {  // uniform over the G warps of column j
-                double *cj = cols + (long long)j * ldw;
-                const int step = 32 * G;
-                const double cji_old = cj[i], v1 = vn1[phys], v2 = vn2[phys];
-                double f = 0.0;
-                if (tau != 0.0) {
-                    double sp = 0.0;
-                    for (int r = i + 1 + lane + 32 * gsub; r < m; r += step) sp += vsrc[r] * cj[r];
-                    sp = warp_sum(sp);
-                    if (lane == 0) pdot[j * G + gsub] = sp;
-                }
-                // every warp of the group has read cj[i], vn1, vn2; the partials are visible
-                asm volatile("bar.sync %0, %1;\n" ::"r"(1 + j), "r"(step) : "memory");
-                if (tau != 0.0) {
-                    double tot = 0.0;
-                    for (int q2 = 0; q2 < G; ++q2) tot += pdot[j * G + q2];
-                    f = tau * (tot + cji_old);
-                    for (int r = i + 1 + lane + 32 * gsub; r < m; r += step) cj[r] -= f * vsrc[r];
-                }
-                const double cji = cji_old - f;
-                if (v1 != 0.0) {
-                    double temp = fabs(cji) / v1;
-                    temp = 1.0 - temp * temp;
-                    temp = temp < 0.0 ? 0.0 : temp;
-                    const double ratio = v1 / v2;
-                    const double temp2 = temp * ratio * ratio;
-                    if (temp2 <= TOL3Z) {  // same decision in all G warps
-                        double sq = 0.0;
-                        for (int r = i + 1 + lane + 32 * gsub; r < m; r += step) sq += cj[r] * cj[r];  // own rows
-                        sq = warp_sum(sq);
-                        if (lane == 0) pnrm[j * G + gsub] = sq;
-                        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + j), "r"(step) : "memory");
-                        double tot = 0.0;
-                        for (int q2 = 0; q2 < G; ++q2) tot += pnrm[j * G + q2];
-                        const double nv = (i + 1 < m) ? sqrt(tot) : 0.0;
-                        if (gsub == 0 && lane == 0) { vn1[phys] = nv; vn2[phys] = nv; }
-                    } else if (gsub == 0 && lane == 0) {
-                        vn1[phys] = v1 * sqrt(temp);
-                    }
-                }
-                if (gsub == 0 && lane == 0 && tau != 0.0) cj[i] = cji;
-            }
-        } else
         for (int j = warp; j < c1 - c0; j += nw) {
             const int phys = c0 + j;
             if (posof[phys] <= i) continue;
