@@ -396,6 +396,50 @@ __device__ __forceinline__ int find_prob(const GemvProb *p, int lo, int hi, long
     return lo;
 }
 
+// L2 prefetch of the matrix bytes that block lb of problem d reads (128-byte lines).
+// The factor's matrices are static during an apply, so the phase kernels issue this
+// BEFORE the programmatic-dependency wait: the DRAM fetch of a phase's matrices
+// overlaps the tail of the previous phase (the phases are chains of dependent
+// launches, most of them under one wave), and every line of a block is requested at
+// once instead of eight loads per lane at a time.  A hint only: results are unchanged.
+#ifndef GEMV_PREFETCH
+#define GEMV_PREFETCH 1
+#endif
+#ifndef GEMV_TASK_PREFETCH
+#define GEMV_TASK_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_block(const GemvProb &d, long long lb) {
+    const int mode = d.mode;
+    const bool trans = mode & 1, lower = mode & 2, upper = mode & 8;
+    int r0, r1, c0, c1;
+    if (!trans) {
+        const int per = (T / d.lpr) * (((mode & 32) && !lower && !upper) ? RPB : 1);  // rows per block
+        r0 = (int)lb * per;
+        r1 = min(d.rows, r0 + per);
+        c0 = 0;
+        c1 = d.cols;
+    } else {
+        const int ntile = (d.cols + CTILE - 1) / CTILE;
+        r0 = (int)(lb / ntile) * SLAB;
+        r1 = min(d.rows, r0 + SLAB);
+        c0 = (int)(lb % ntile) * CTILE;
+        c1 = min(d.cols, c0 + CTILE);
+    }
+    if (r1 <= r0 || c1 <= c0) return;
+    const int lines = ((c1 - c0) * 8 + 127) / 128 + 1;  // per row, upper bound
+    const int n = (r1 - r0) * lines;
+    for (int i = threadIdx.x; i < n; i += T) {
+        const int r = r0 + i / lines, l = i % lines;
+        const int a = upper ? max(c0, r) : c0, b = lower ? min(c1, r + 1) : c1;  // columns row r reads
+        if (b <= a) continue;
+        const double *row = d.M + (long long)r * d.ld;
+        const size_t lo = reinterpret_cast<size_t>(row + a) & ~size_t(127);
+        const size_t hi = reinterpret_cast<size_t>(row + b - 1);
+        const size_t q = lo + 128 * (size_t)l;
+        if (q <= hi) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+    }
+}
+
 __global__ void __launch_bounds__(T, GEMV_MINB) gemv_kernel(const __grid_constant__ GemvArgs a) {
     __shared__ double xr[SLAB];
     __shared__ double part[2 * T];
@@ -405,6 +449,7 @@ __global__ void __launch_bounds__(T, GEMV_MINB) gemv_kernel(const __grid_constan
     // let the next phase's CTAs be scheduled now, and wait here until the previous
     // phase (whose outputs are this phase's inputs) has completed and flushed
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (GEMV_PREFETCH) prefetch_block(a.p[p], blk - a.p[p].blk_begin);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(a.p[p], blk - a.p[p].blk_begin, xr, part);
 }
@@ -421,6 +466,7 @@ __global__ void __launch_bounds__(T, GEMV_MINB) gemv_dev_kernel(const GemvProb *
     const long long blk = blockIdx.x;
     const GemvProb d = P[__ldg(b2p + blk)];
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (GEMV_PREFETCH) prefetch_block(d, blk - d.blk_begin);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(d, blk - d.blk_begin, xr, part);
 }
@@ -440,10 +486,26 @@ __global__ void __launch_bounds__(T) apply_tasks_kernel(const GemvProb *__restri
     __shared__ double part[2 * T];
     const int o0 = __ldg(task_ptr + blockIdx.x), o1 = __ldg(task_ptr + blockIdx.x + 1);
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#if GEMV_TASK_PREFETCH
+    // the task's first op before the dependency wait, then always one op ahead
+    // (the ops of a task run one after the other, each a short dependent chain)
+    if (o0 < o1) {
+        const GemvProb d = ops[o0];
+        const long long nb = ops[o0 + 1].blk_begin - d.blk_begin;
+        for (long long lb = 0; lb < nb; ++lb) prefetch_block(d, lb);
+    }
+#endif
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     for (int o = o0; o < o1; ++o) {
         const GemvProb d = ops[o];
         const long long nb = ops[o + 1].blk_begin - d.blk_begin;  // ops end with a sentinel
+#if GEMV_TASK_PREFETCH
+        if (o + 1 < o1) {
+            const GemvProb e = ops[o + 1];
+            const long long ne = ops[o + 2].blk_begin - e.blk_begin;
+            for (long long lb = 0; lb < ne; ++lb) prefetch_block(e, lb);
+        }
+#endif
         for (long long lb = 0; lb < nb; ++lb) gemv_block(d, lb, xr, part);
         __syncthreads();  // the next op reads this op's results
     }

@@ -278,15 +278,14 @@ __device__ __forceinline__ void coop_update(double *vn1, double *vn2, double *co
     }
 }
 
-// Global-memory columns: capped at 64 registers so two groups (two large sketches of one
-// batch, e.g. config[4]'s two 6048x987 top-separator sketches) are co-resident, two CTAs
-// per SM, instead of running one after the other (52.6 vs 58.3 ms for that pair; the
-// few spilled values sit outside the column loops).  Bit-identical results.
-#ifndef MQ_GLOBAL_MINB
-#define MQ_GLOBAL_MINB 2
-#endif
-template <bool SMEM>
-__global__ void __launch_bounds__(MCT, SMEM ? 1 : MQ_GLOBAL_MINB) mqrcp_kernel(const __grid_constant__ MArgs a) {
+// Global-memory columns come in two builds: 128 registers / one CTA per SM (fastest
+// for a single sketch: 29.3 ms for 6048x987) and 64 registers / two CTAs per SM, so
+// that two groups (the two 6048x987 top-separator sketches of config[4]) are
+// co-resident instead of running one after the other (52.6 vs 58.3 ms for the pair,
+// 80.5 vs 95.3 ms for three 9000x700; a single sketch would take 41.7 ms).  The host
+// picks by the number of global-memory sketches left in the batch.  Bit-identical.
+template <bool SMEM, int MINB>
+__global__ void __launch_bounds__(MCT, MINB) mqrcp_kernel(const __grid_constant__ MArgs a) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[64]  /* block_sum_n: CB x MCT/32 */;
     __shared__ int redp[32];
@@ -1149,8 +1148,9 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
     nsm = std::min(nsm, CQ_MAX);  // a group never has more CTAs than pivot-candidate slots
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(mqrcp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
-        cudaFuncSetAttribute(mqrcp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
+        cudaFuncSetAttribute(mqrcp_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
+        cudaFuncSetAttribute(mqrcp_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
+        cudaFuncSetAttribute(mqrcp_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET + 8192);
         cudaFuncSetAttribute(mq_form_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BUDGET);
         attr = true;
     }
@@ -1320,6 +1320,11 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
             size_t sm = 0;
             int blocks = 0, cnt = 0;
             size_t start = pos;
+            // global-memory columns: the two-CTAs-per-SM build when at least two sketches are left
+            const bool pair = !smem && sel.size() - pos >= 2;
+            void *kfn = smem ? (void *)mqrcp_kernel<true, 1>
+                             : pair ? (void *)mqrcp_kernel<false, 2> : (void *)mqrcp_kernel<false, 1>;
+            const int kid = smem ? 1 : pair ? 2 : 0;
             while (pos < sel.size() && cnt < MAXM) {
                 const size_t sm2 = std::max(sm, sel[pos].sm);
                 static std::map<std::pair<int, size_t>, int> occ_b;
@@ -1327,13 +1332,12 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
                 int per_sm = 0;
                 {
                     std::lock_guard<std::mutex> lk(occ_bmu);
-                    auto it = occ_b.find({(int)smem, sm2});
+                    auto it = occ_b.find({kid, sm2});
                     if (it != occ_b.end()) {
                         per_sm = it->second;
                     } else {
-                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                            &per_sm, smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, MCT, sm2);
-                        occ_b[{(int)smem, sm2}] = per_sm;
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, MCT, sm2);
+                        occ_b[{kid, sm2}] = per_sm;
                     }
                 }
                 if (per_sm < 1) return 77;
@@ -1361,8 +1365,7 @@ int rsc_qrcp_multi(int n, const int *ids, double *const *G, const int *m, const 
             // distinct barrier counter per matrix of this launch
             ma.bar = bar + start + (smem ? 0 : 0);
             void *args[] = {&ma};
-            cudaError_t e = cudaLaunchCooperativeKernel(
-                smem ? (void *)mqrcp_kernel<true> : (void *)mqrcp_kernel<false>, dim3(b0), dim3(MCT), args, sm, s);
+            cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(b0), dim3(MCT), args, sm, s);
             rsc_count_launch();
             if (e != cudaSuccess) return (int)e;
             // Q formation (blocked compact-WY on DMMA GEMMs) for the same matrices

@@ -53,6 +53,31 @@ def zeros(*shape, dtype=F64):
     return torch.zeros(*shape, dtype=dtype, device=dev())
 
 
+class gc_paused:
+    """Pause Python's cyclic collector for the duration of a host-bound call: a
+    one-shot factorization builds ~10^6 short-lived descriptor objects (arrays, views,
+    tuples, none of them in reference cycles), and every generation-0/1/2 scan of the
+    collector walks the long-lived plan objects again.  Re-enabled on exit when it was
+    enabled on entry; RSC_GC=1 leaves the collector alone."""
+
+    _keep = os.environ.get("RSC_GC") == "1"
+
+    def __enter__(self):
+        import gc
+
+        self.was = gc.isenabled() and not self._keep
+        if self.was:
+            gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        if self.was:
+            import gc
+
+            gc.enable()
+        return False
+
+
 _CHUNK_POOL = []  # device chunks of dead arenas, reused before any new cudaMalloc
 
 

@@ -634,6 +634,11 @@ def factorize(A, config=None, coords=None, prepared=None):
     sweep on the device, restart with alpha_d *= alpha_d_growth on an indefinite
     pivot once a diagonal tree is in play, TooManyRestarts after max_restarts.
     """
+    with E.gc_paused():
+        return _factorize(A, config, coords, prepared)
+
+
+def _factorize(A, config, coords, prepared):
     A = _normalize(as_spd(A))
     reuse = prepared is not None
     if prepared is None:
