@@ -228,11 +228,6 @@ __global__ void __launch_bounds__(NT, RSC_GEMM_MINB) gemm_grouped_kernel(const _
     const int nk = (P.K + BK - 1) / BK;
     Loader<TA, TB, GATHER> ld;
     ld.init(P, A, B, m0, n0);
-    // launched with programmatic stream serialization (RSC_GEMM_PDL, default on): the
-    // problem lookup, the loader setup and the first gathered-row indices (plan data,
-    // never written by the sweep) run while the previous kernel drains; operands and C
-    // are touched only after it has completed and flushed.  A no-op otherwise.
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (nk > 0) {
         // STAGES-deep cp.async pipeline, one CTA barrier per k-tile
 #pragma unroll
@@ -337,7 +332,6 @@ constexpr int MW = (MAXP + 31) / 32;  // problem-mask words per row
 
 // Inverse maps of every mapped problem of the chunk (tables pre-set to -1).
 __global__ void __launch_bounds__(RT) reduce_tables_kernel(const __grid_constant__ RedArgs a) {
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the GEMM that follows does not read the tables
     const RedProb &P = a.p[blockIdx.x];
     const RedGroup &G = a.g[P.g];
     const int q = blockIdx.x - G.p0;
@@ -376,8 +370,6 @@ __global__ void __launch_bounds__(RT) reduce_tables_kernel(const __grid_constant
 constexpr int LIST_MAX = 4096;  // entries per CTA (TR x np bounded by the host)
 
 __global__ void __launch_bounds__(RT) ordered_reduce_kernel(const __grid_constant__ RedArgs a) {
-    // a grouped GEMM launched next (programmatic serialization) may set up its tiles now
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     __shared__ unsigned long long s_buf[LIST_MAX];  // fast path: packed row pointers; else s_q | s_i
     __shared__ int s_cnt[TR_MAX];
     int *s_q = reinterpret_cast<int *>(s_buf);
@@ -539,25 +531,8 @@ int launch_chunk(GemmArgs &args, long long tiles, cudaStream_t s) {
         cudaFuncSetAttribute(gemm_grouped_kernel<TA, TB, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
         attr = true;
     }
-    static const bool pdl = !(getenv("RSC_GEMM_PDL") && getenv("RSC_GEMM_PDL")[0] == '0');
-    if (pdl) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.gridDim = dim3((unsigned)tiles);
-        cfg.blockDim = dim3(NT);
-        cfg.dynamicSmemBytes = SMEM_BYTES;
-        cfg.stream = s;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_grouped_kernel<TA, TB, GATHER>, args);
-        rsc_count_launch();
-        if (e != cudaSuccess) return (int)e;
-    } else {
-        gemm_grouped_kernel<TA, TB, GATHER><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
-        RSC_CHECK_LAUNCH();
-    }
+    gemm_grouped_kernel<TA, TB, GATHER><<<(unsigned)tiles, NT, SMEM_BYTES, s>>>(args);
+    RSC_CHECK_LAUNCH();
     static const bool log = getenv("RSC_GEMM_LOG") != nullptr;  // diagnostics: one line per launch
     if (log) {
         double fl = 0.0, pad = 0.0, pad32m = 0.0, pad32n = 0.0;
