@@ -408,16 +408,6 @@ __device__ __forceinline__ int find_prob(const GemvProb *p, int lo, int hi, long
 #ifndef GEMV_TASK_PREFETCH
 #define GEMV_TASK_PREFETCH 0  // one op ahead inside the subtree tasks: measured 3% slower (3.71 vs 3.60 ms)
 #endif
-#ifndef GEMV_PREFETCH_AHEAD
-#define GEMV_PREFETCH_AHEAD 0
-#endif
-// one wave of resident CTAs: a CTA also requests the block of the CTA that will take
-// a slot one wave later, so that block's lines are in L2 when its loads are issued
-__device__ __forceinline__ long long prefetch_ahead() {
-    unsigned nsm;
-    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-    return (long long)nsm * GEMV_MINB;
-}
 __device__ __forceinline__ void prefetch_block(const GemvProb &d, long long lb) {
     const int mode = d.mode;
     const bool trans = mode & 1, lower = mode & 2, upper = mode & 8;
@@ -459,14 +449,7 @@ __global__ void __launch_bounds__(T, GEMV_MINB) gemv_kernel(const __grid_constan
     // let the next phase's CTAs be scheduled now, and wait here until the previous
     // phase (whose outputs are this phase's inputs) has completed and flushed
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    if (GEMV_PREFETCH) {
-        const long long ahead = prefetch_ahead();
-        if (!GEMV_PREFETCH_AHEAD || blk < ahead) prefetch_block(a.p[p], blk - a.p[p].blk_begin);
-        if (GEMV_PREFETCH_AHEAD && blk + ahead < a.total) {
-            const int q = find_prob(a.p, p, a.count - 1, blk + ahead);
-            prefetch_block(a.p[q], blk + ahead - a.p[q].blk_begin);
-        }
-    }
+    if (GEMV_PREFETCH) prefetch_block(a.p[p], blk - a.p[p].blk_begin);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(a.p[p], blk - a.p[p].blk_begin, xr, part);
 }
@@ -483,14 +466,7 @@ __global__ void __launch_bounds__(T, GEMV_MINB) gemv_dev_kernel(const GemvProb *
     const long long blk = blockIdx.x;
     const GemvProb d = P[__ldg(b2p + blk)];
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    if (GEMV_PREFETCH) {
-        const long long ahead = prefetch_ahead();
-        if (!GEMV_PREFETCH_AHEAD || blk < ahead) prefetch_block(d, blk - d.blk_begin);
-        if (GEMV_PREFETCH_AHEAD && blk + ahead < (long long)gridDim.x) {
-            const GemvProb e = P[__ldg(b2p + blk + ahead)];
-            prefetch_block(e, blk + ahead - e.blk_begin);
-        }
-    }
+    if (GEMV_PREFETCH) prefetch_block(d, blk - d.blk_begin);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     gemv_block(d, blk - d.blk_begin, xr, part);
 }
