@@ -223,21 +223,13 @@ __device__ __forceinline__ void gemv_block(const GemvProb &d, long long lb, doub
             return;
         }
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        if (r < rows && (mode & (32 | 64))) {
+        if (r < rows && (mode & 32)) {
             // rows 16-byte aligned: double2 loads of column pairs (2p, 2p+1), four pairs in
-            // flight per lane; a lone first / last column is done by one lane.  Odd leading
-            // dimension (bit 6): every other row starts 8 bytes off; such a row is walked
-            // from the aligned address one element before it, with the columns, x and the
-            // x index shifted by one (element 0 of the shifted row is never touched: the
-            // shifted first column is odd and goes through the lone-column step).
+            // flight per lane; a lone first / last column is done by one lane
             const double *Mr = M + (long long)r * ld;
-            const int sh = (mode & 64) ? (int)((reinterpret_cast<size_t>(Mr) >> 3) & 1) : 0;
-            Mr -= sh;
-            x -= sh;
-            if (xi) xi -= sh;
             const double2 *M2 = reinterpret_cast<const double2 *>(Mr);
-            const int cend = (lower ? min(cols, r + 1) : cols) + sh;
-            int cb = (upper ? r : 0) + sh;
+            const int cend = lower ? min(cols, r + 1) : cols;
+            int cb = upper ? r : 0;
             if ((cb & 1) && cb < cend) {
                 if (sub == 0) s0 += ldnc(Mr + cb) * ldx<CG>(x + (xi ? __ldg(xi + cb) : cb));
                 ++cb;
@@ -695,10 +687,7 @@ inline long long describe(GemvProb &d, const double *M, int rows, int cols, int 
     // bit 5: every row starts 16-byte aligned (double2 loads)
     static const bool scalar_only = getenv("RSC_GEMV_SCALAR") != nullptr;  // A/B switch
     const bool vec = (reinterpret_cast<size_t>(M) % 16 == 0) && (ld % 2 == 0) && !scalar_only;
-    // bit 6: odd leading dimension (or an 8-byte-aligned base): rows are paired per row (see gemv_block)
-    static const bool no_shift = getenv("RSC_GEMV_NOSHIFT") != nullptr;  // A/B switch
-    const bool shifted = !vec && !scalar_only && !no_shift && !(mode & 1);
-    mode = (mode & ~(32 | 64)) | (vec ? 32 : 0) | (shifted ? 64 : 0);
+    mode = (mode & ~32) | (vec ? 32 : 0);
     d.rows = rows; d.cols = cols; d.ld = ld; d.mode = mode; d.alpha = alpha;
     if (mode & 1) {
         d.lpr = cols >= CTILE ? CTILE : (pow2ceil(cols) < 32 ? 32 : pow2ceil(cols));
